@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 FWHT hot path (BASELINE.json metric: WHT points/sec
+at 2^n int64 on 1/2/4/8 B200 + HBM GB/s fraction of roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload: config 4 of BASELINE.json -- n = 32 int64 FWHT (32 GiB), seeded
+uniform +-1 input, natural order, unnormalised; strong scaling over the top
+log2(N) index bits for N > 1 (one process per GPU, torchrun).  A step is one
+full transform of the resident signal (fwht_array semantics: all passes, and
+for N > 1 the cross-GPU butterfly).  The 32 GiB input is far larger than the
+126 MB L2, so no L2 flush is needed between steps.
+
+--impl reference times the reference's own CPU algorithm (the oracle port of
+parallel.py run_parallel, numpy, all host cores) on a bounded sample of the
+same workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "WHT points/sec at 2^n int64 (1/2/4/8 B200) + HBM GB/s fraction of roofline"
+PUBLISHED_PTS = 2 ** 26 / 2.5  # 26.8 Mpts/s
+CPU_SAMPLE_N = 26
+
+
+def args_parse():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=32, help="log2 of the transform size (config 4: 32)")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", choices=["peer", "a2a"], default="peer", help="cross-GPU exchange (N > 1)")
+    return ap.parse_args()
+
+
+def world():
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons, power = [], [], set(), []
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+                power.append(float(r[3]))
+            except ValueError:
+                continue
+            for name, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(power) if power else None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------ CPU legs ---
+
+def cpu_reference_sample(n_sample: int, reps: int, warm: int):
+    """The reference's CPU algorithm (numpy restatement of parallel.py
+    run_parallel) on a 2^n_sample sample, all power-of-two host threads.
+    Returns (list of seconds, threads)."""
+    import numpy as np
+
+    from oracle import load_c, oracle_np
+
+    cores = len(os.sched_getaffinity(0))
+    p = max(1, min(cores.bit_length() - 1, n_sample - 1))
+    x = np.empty(1 << n_sample, dtype=np.int64)
+    arr = (ctypes.c_uint64 * 1)(0)
+    load_c().oracle_gen_i64(x.ctypes.data, 0, x.size, 1, 32, arr, 0, cores)  # config-4 values, first chunk
+    times = []
+    for i in range(warm + reps):
+        t0 = time.perf_counter()
+        oracle_np.run_parallel(x, n_sample, p)
+        dt = time.perf_counter() - t0
+        if i >= warm:
+            times.append(dt)
+    return times, 1 << p, cores
+
+
+def cpu_equivalent_rate(n_full: int, n_sample: int, seconds: float) -> float:
+    """Full-workload points/s from a sample: the full transform does n_full
+    stages per point versus n_sample in the sample, so
+    t_full = t_sample * 2^(n_full - n_sample) * n_full / n_sample."""
+    t_full = seconds * (2 ** (n_full - n_sample)) * n_full / n_sample
+    return 2 ** n_full / t_full
+
+
+def run_reference(a):
+    ws, rank, _ = world()
+    if rank != 0:
+        return
+    n_s = min(CPU_SAMPLE_N, a.n)
+    times, threads, cores = cpu_reference_sample(n_s, max(1, a.steps), max(0, a.warmup))
+    mean = sum(times) / len(times)
+    value = cpu_equivalent_rate(a.n, n_s, mean)
+    sample = (f"one 2^{n_s}-point run_parallel (numpy port of parallel.py:162-198, p={threads.bit_length() - 1}) "
+              f"per step on the config-{a.config} input; rate extrapolated to n={a.n} as "
+              f"2^n / (t * 2^(n-{n_s}) * n/{n_s})")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": ws,
+        "steps": len(times), "warmup": a.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": value / PUBLISHED_PTS, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": f"config{a.config}: n={a.n} int64 FWHT, uniform +-1, natural order, unnormalised",
+                   "n": a.n, "sample_n": n_s},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "host_cores": cores,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ GPU leg ---
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1607_01039_b200 as bw
+    from paper_1607_01039_b200 import _lib, sharded, signals
+
+    ws, rank, local_rank = world()
+    torch.cuda.set_device(local_rank)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    p = sharded.log2_shards(ws)
+    n = a.n
+    nl = n - p
+    spec = signals.config(a.config, n)
+    L = _lib.lib()
+    x = torch.empty(1 << nl, dtype=torch.int64, device="cuda")
+    signals.generate(spec, x, base=rank << nl)
+    npasses = L.bw_plan_npasses(nl)
+    plan = sharded.plan(n, p)
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    ptr = x.data_ptr()
+    peer = None
+    if p > 0:
+        peer = sharded._PeerMap(x, None, dist) if a.mode == "peer" else None
+        ones = torch.ones(1, device="cuda")
+        ptrs = (ctypes.c_void_p * ws)(*(peer.ptrs if peer else [ptr] * ws))
+        b, c = sharded.slice_of(rank, ws, 1 << nl)
+
+    def device_barrier():
+        dist.all_reduce(ones)  # NCCL on this stream: a device-side barrier
+
+    def step(ev):
+        for i in range(npasses):
+            ev[i].record(stream)
+            _lib.check(L.bw_fwht_i64_pass(ptr, nl, i, sh))
+        ev[npasses].record(stream)
+        if p > 0:
+            if a.mode == "peer":
+                device_barrier()  # every shard's local passes done
+                ev[npasses + 1].record(stream)
+                _lib.check(L.bw_xshard_i64(ptrs, p, b, c, sh))
+                ev[npasses + 2].record(stream)
+                device_barrier()  # every exchange done
+            else:
+                ev[npasses + 1].record(stream)
+                m = (1 << nl) // ws
+                recv = step.recv
+                dist.all_to_all_single(recv, x)
+                _lib.check(L.bw_xshard_strided_i64(recv.data_ptr(), m, p, 0, m, sh))
+                dist.all_to_all_single(x, recv)
+                ev[npasses + 2].record(stream)
+        ev[-1].record(stream)
+
+    if p > 0 and a.mode == "a2a":
+        step.recv = torch.empty_like(x)
+    nev = npasses + 4
+
+    def events():
+        return [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
+
+    for _ in range(a.warmup):
+        step(events())
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.6)  # let the sampler start before the timed region
+    evs = [events() for _ in range(a.steps)]
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    for e in evs:
+        step(e)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = evs[0][0].elapsed_time(evs[-1][-1])
+    pass_ms = [[e[i].elapsed_time(e[i + 1]) for e in evs] for i in range(npasses)]
+    xs_ms = [e[npasses + 1].elapsed_time(e[npasses + 2]) for e in evs] if p > 0 else []
+    if ws > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / a.steps
+    value = a.steps * (2 ** n) / (total_ms / 1e3)
+    avg_pass = [sum(v) / len(v) for v in pass_ms]
+    peak, peak_src = hbm_peak()
+    bytes_per_pass = 16 * (2 ** nl)
+    dom = max(range(npasses), key=lambda i: avg_pass[i])
+    achieved = bytes_per_pass / (avg_pass[dom] / 1e3) / 1e9
+    launches = a.steps * (npasses + (1 if p > 0 else 0))
+
+    # e2e: the public API on a pinned host buffer, H2D + transform + D2H per step.
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, x, spec, p, nl, rank, ws, peer)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": ws, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": value / PUBLISHED_PTS,
+        "vs_baseline_source": "PAPER.md:272-274 in-memory WHT 2.5 s at n=26 (26.8 Mpts/s), BASELINE.md section 1",
+        "dtype": "int64", "data": "synthetic: seeded counter-based uniform +-1 (config 4), generated on device",
+        "config": {"workload": f"config{a.config}: n={n} int64 FWHT, uniform +-1, natural order, unnormalised",
+                   "n": n, "log2p": p, "local_log2n": nl, "parallelism": f"top {p} index bits sharded over {ws} GPUs",
+                   "exchange": a.mode if p > 0 else None,
+                   "passes": [{"kind": q["kind"], "k": q["k"], "r": q["r"]} for q in plan["passes"]],
+                   "l2": "32 GiB input >> 126 MB L2 (no flush needed)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": f"pass {dom} ({plan['passes'][dom]['kind']}, stages "
+                     f"{plan['passes'][dom]['k']}..{plan['passes'][dom]['k'] + plan['passes'][dom]['r'] - 1})",
+                     "algorithmic_bytes_per_launch": bytes_per_pass, "peak_source": peak_src,
+                     "frac_of_8tbs_spec": achieved / 8000.0},
+        "passes_ms": [round(v, 4) for v in avg_pass],
+        "passes_gbs": [round(bytes_per_pass / (v / 1e3) / 1e9, 1) for v in avg_pass],
+        "transform_gbs_per_pass_avg": round(bytes_per_pass * npasses / (sum(avg_pass) / 1e3) / 1e9, 1),
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if p > 0:
+        line["xshard_ms"] = sum(xs_ms) / len(xs_ms)
+        nv = 8 * (2 ** nl) * (ws - 1) / ws
+        line["nvlink"] = {"bytes_each_direction": nv, "achieved_gbs": nv / (line["xshard_ms"] / 1e3) / 1e9,
+                          "peak_gbs": 770.0, "peak_source": "B200_PROFILING.md measured peer copy"}
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and ws == 1 and not a.no_cpu:
+        n_s = min(CPU_SAMPLE_N, n)
+        times, threads, cores = cpu_reference_sample(n_s, 3, 1)
+        mean = sum(times) / len(times)
+        line["cpu_baseline"] = {
+            "value": cpu_equivalent_rate(n, n_s, mean), "unit": "points/s", "cores": threads, "host_cores": cores,
+            "kind": "port",
+            "sample": f"2^{n_s}-point run_parallel (numpy port of parallel.py:162-198) x{len(times)}, "
+                      f"{mean:.3f} s each; extrapolated to n={n} by 2^(n-{n_s}) * n/{n_s}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if peer is not None:
+        peer.close()
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(a, x, spec, p, nl, rank, ws, peer):
+    """Same metric end to end: pinned host shard -> device -> transform ->
+    host, every step, through the public API (fwht_array on a host buffer
+    for N = 1; H2D + sharded.fwht_distributed + D2H for N > 1)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1607_01039_b200 as bw
+    from paper_1607_01039_b200 import sharded
+
+    steps = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 5))
+    host = torch.empty(1 << nl, dtype=torch.int64, pin_memory=True)
+    host.copy_(x)
+    hnp = host.numpy()
+    stream = torch.cuda.current_stream()
+    if ws == 1:
+        bw.fwht_array(hnp)  # warm-up (allocates the device staging buffer)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            bw.fwht_array(hnp)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+    else:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        e0.record(stream)
+        for _ in range(steps):
+            x.copy_(host, non_blocking=True)
+            sharded.fwht_distributed(x, mode=a.mode, peer_map=peer)
+            host.copy_(x, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    nbytes = 8 * (2 ** nl) * ws
+    return {"value": steps * (2 ** (nl + p)) / (ms / 1e3), "unit": "points/s", "h2d_bytes_per_step": nbytes,
+            "d2h_bytes_per_step": nbytes, "steps": steps, "ms_per_step": ms / steps,
+            "api": "paper_1607_01039_b200.fwht_array(pinned numpy buffer)" if ws == 1
+            else "H2D + sharded.fwht_distributed + D2H"}
+
+
+def main():
+    a = args_parse()
+    ws, _, _ = world()
+    if ws != a.gpus and not (ws == 1 and a.gpus == 1):
+        if ws == 1 and a.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

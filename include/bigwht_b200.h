@@ -1,0 +1,264 @@
+/*
+ * bigwht_b200.h -- C ABI of the B200-native fast Walsh-Hadamard transform.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `bigwht` (arXiv:1607.01039, pkg/src/bigwht).  Every entry point below
+ * replaces one reference interface, cited as /root/reference/<file>:<line>.
+ * The reference is pure Python + numpy; its "FFI" is the Python call itself,
+ * so the binding a maintainer adds is the ctypes stub shown in
+ * INTEGRATION.md (it is what paper_1607_01039_b200/_lib.py does).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Device pointers are CUDA global memory
+ *     (cudaMalloc / torch CUDA tensors); `stream` is a cudaStream_t passed as
+ *     void* (NULL = legacy default stream).  Calls are asynchronous on that
+ *     stream unless documented as synchronous.
+ *   - The signal is caller-owned, 2^log2n int64 elements, C-contiguous,
+ *     element i has index bit b of weight 2^b.  The transform is
+ *     in place, natural (Sylvester/Hadamard) order, unnormalised:
+ *         y_i = sum_j (-1)^popcount(i & j) x_j      (core.py:128-144)
+ *   - int64 arithmetic wraps modulo 2^64 exactly like numpy int64 does in
+ *     core.py:113-115, so results are bit-identical to the reference for every
+ *     input, including inputs that violate the magnitude bound.
+ *   - Return value: a bw_status.  On failure bw_last_error() (thread-local)
+ *     holds a message.  Status codes map 1:1 onto the reference exception
+ *     classes (errors.py:10-41) in the Python host layer.
+ */
+#ifndef BIGWHT_B200_H
+#define BIGWHT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BW_ABI_VERSION 1
+
+typedef enum bw_status {
+    BW_OK = 0,
+    BW_BAD_ARGUMENTS = 1,     /* errors.py:24  BadArguments          */
+    BW_OVERFLOW_BOUND = 2,    /* errors.py:32  OverflowBoundError    */
+    BW_INEXACT_DIVISION = 3,  /* errors.py:36  InexactDivision       */
+    BW_INVALID_WORKERS = 4,   /* errors.py:40  InvalidWorkerCount    */
+    BW_CAPACITY = 5,          /* extraction output capacity too small */
+    BW_CUDA_ERROR = 6,        /* device failure (no reference class: DeviceError) */
+    BW_NOT_SUPPORTED = 7      /* e.g. unsupported device architecture */
+} bw_status;
+
+/* Largest transform handled by one call on one device (2^34 int64 = 128 GiB). */
+#define BW_MAX_LOG2N 34
+/* Largest cross-shard radix (P = 2^BW_MAX_LOG2P devices / shards). */
+#define BW_MAX_LOG2P 3
+
+/* ---- library / error plumbing ------------------------------------------ */
+
+/* ABI version (BW_ABI_VERSION). */
+int bw_abi_version(void);
+
+/* Message of the last failing call on this host thread ("" if none). */
+const char *bw_last_error(void);
+
+/* Compute capability of `device` as 10*major+minor, or -1. Synchronous. */
+int bw_device_cc(int device);
+
+/* ---- the hot path ------------------------------------------------------ */
+
+/*
+ * In-place FWHT of data[0 .. 2^log2n).  Replaces `fwht_array(buf) -> int`
+ * (/root/reference/pkg/src/bigwht/core.py:97-117): no magnitude check (the
+ * reference has none either), returns the butterfly count n*2^(n-1)
+ * (core.py:117) in *butterflies (may be NULL).  Asynchronous.
+ * Pass plan: one fused low-bits pass over stages 0..13 followed by strided
+ * high-bits passes of <= 10 stages each, i.e. the blocked
+ * decomposition of external.py:238-283 with many stages per HBM round trip.
+ * data must be 16-byte aligned.
+ */
+int bw_fwht_i64(int64_t *data, int log2n, void *stream, uint64_t *butterflies);
+
+/*
+ * Same transform with an explicit pass plan (test hook; mirrors the
+ * reference's block-size-independence tests, test_external.py:120-129).
+ * pass_bits[0] = stages of the low pass (must be min(n, 14)), the rest are
+ * the widths (1..10) of the following high passes in ascending bit order;
+ * the widths must sum to log2n.  npasses = 0 with pass_bits = NULL runs the
+ * naive one-launch-per-stage path (kernel K0, debugging/reference aid).
+ */
+int bw_fwht_i64_planned(int64_t *data, int log2n, const int *pass_bits,
+                        int npasses, void *stream);
+
+/*
+ * Pass-level launches of the default plan (instrumentation: the benchmark
+ * records a CUDA event between passes to time each kernel inside the step).
+ * bw_plan_npasses returns the number of passes of bw_fwht_i64's plan;
+ * running passes 0..npasses-1 in order equals one bw_fwht_i64 call.
+ */
+int bw_plan_npasses(int log2n);
+int bw_fwht_i64_pass(int64_t *data, int log2n, int pass_index, void *stream);
+
+/*
+ * float64 fwht_array (core.py:97-117 on a float64 Signal, core.py:56-59):
+ * stages applied strictly in ascending order with the same IEEE a+b / a-b
+ * as numpy, so results are bitwise identical to the reference (the order
+ * matters in floating point).  Not the tuned int64 path.
+ */
+int bw_fwht_f64(double *data, int log2n, void *stream, uint64_t *butterflies);
+
+/* inverse_wht_inplace for float64 (core.py:168-169): forward, then * 2^-n. */
+int bw_inverse_f64(double *data, int log2n, void *stream);
+
+/*
+ * Max/min reduction for the int64 magnitude bound.  Writes
+ * out_minmax_dev[0] = max(data), out_minmax_dev[1] = min(data) (device
+ * memory, 2 int64).  Asynchronous.  Building block of
+ * check_magnitude_bound (core.py:80-94).
+ */
+int bw_minmax_i64(const int64_t *data, uint64_t count, int64_t *out_minmax_dev,
+                  void *stream);
+
+/*
+ * check_magnitude_bound(data, n) (core.py:80-94): synchronous.  Computes
+ * M = max(max, -min) exactly and fails with BW_OVERFLOW_BOUND when
+ * M * 2^log2n >= 2^63.  *max_abs (may be NULL) receives M (as uint64, so
+ * |INT64_MIN| = 2^63 is representable).  scratch_dev: 2 int64 of device
+ * memory (NULL = use an internal per-device buffer).
+ */
+int bw_check_bound_i64(const int64_t *data, int log2n, int64_t *scratch_dev,
+                       void *stream, uint64_t *max_abs);
+
+/*
+ * fwht_inplace(sig) (core.py:120-125) on the int64 payload: bound check
+ * first -- raising BW_OVERFLOW_BOUND before any mutation, like core.py:122 --
+ * then the transform.  Synchronises `stream` once (the bound read-back).
+ */
+int bw_fwht_inplace_i64(int64_t *data, int log2n, int64_t *scratch_dev,
+                        void *stream, uint64_t *butterflies);
+
+/*
+ * End-to-end transform of a HOST buffer (pinned for full PCIe speed):
+ * H2D into the caller's device workspace (2^log2n int64), fused bound
+ * check + transform on the device, D2H of the result.  If check_bound and the
+ * bound fails, returns BW_OVERFLOW_BOUND with the host buffer untouched
+ * (the "raise before mutation" contract of core.py:122).  Synchronous.
+ */
+int bw_fwht_host_i64(int64_t *host, int log2n, int64_t *work_dev,
+                     int check_bound, void *stream, uint64_t *butterflies);
+
+/*
+ * inverse_wht_inplace (core.py:147-173) on the int64 payload: bound check,
+ * forward transform, exact division by 2^n.  When some coefficient is not
+ * divisible, the buffer is restored and BW_INEXACT_DIVISION returned
+ * (core.py:160-167).  Synchronous.
+ */
+int bw_inverse_i64(int64_t *data, int log2n, int64_t *scratch_dev, void *stream);
+
+/* ---- multi-device / sharded path (parallel.py:87-111 with m = P devices) */
+
+/*
+ * Cross-shard butterfly: the last log2p stages of a 2^(log2n_local+log2p)
+ * transform whose P = 2^log2p shards (shard r = indices with top bits = r)
+ * have each been transformed locally.  For every local index i in
+ * [begin, begin+count) it gathers shards[r][i] for all r, applies the
+ * P-point WHT (stage order ascending, parallel.py:103-110) and scatters the
+ * results back in place.  shards[] are device pointers readable/writable
+ * from the current device: local buffers (single-GPU emulation), CUDA-IPC /
+ * peer-mapped buffers (one process per GPU over NVLink), or P receive slots
+ * of an all-to-all.  Disjoint [begin,count) ranges may run concurrently on
+ * different devices (the check_disjoint argument, parallel.py:114-134).
+ * begin and count must be even.
+ */
+int bw_xshard_i64(int64_t *const *shards, int log2p, uint64_t begin,
+                  uint64_t count, void *stream);
+
+/*
+ * Same exchange with the shards given as one strided array: shard r starts
+ * at base + r*shard_stride elements (all-to-all receive buffers and the
+ * single-device P-shard emulation).
+ */
+int bw_xshard_strided_i64(int64_t *base, uint64_t shard_stride, int log2p,
+                          uint64_t begin, uint64_t count, void *stream);
+
+/*
+ * Peer-memory plumbing for one process per GPU: export a device buffer as a
+ * CUDA IPC handle (64 bytes) plus its offset inside the allocation, open a
+ * peer's handle (NVLink peer access enabled lazily), close it again.
+ * bw_enable_peer_access: single-process multi-GPU P2P from the current
+ * device to peer_device.
+ */
+int bw_ipc_get_handle(const void *ptr, void *handle_out, uint64_t *offset_out);
+int bw_ipc_open_handle(const void *handle, uint64_t offset, void **ptr_out);
+int bw_ipc_close_handle(void *ptr, uint64_t offset);
+int bw_enable_peer_access(int peer_device);
+
+/* ---- signal tooling around the path ------------------------------------ */
+
+/* Generator kinds (seeded, counter based, bit-reproducible by oracle/). */
+enum bw_gen_kind {
+    BW_GEN_PM1 = 1,          /* x_i = 1 - 2*(h(seed,i) & 1)                       */
+    BW_GEN_UNIFORM = 2,      /* x_i = h(seed,i) mod (2A+1) - A, A = params[0]     */
+    BW_GEN_NOISY_MASKS = 3   /* x_i = sum_k (1 - 2*(<s_k,i> xor [h(seed_k,i) < thr])) */
+};
+
+/*
+ * Fill data[0..2^log2n) with a seeded synthetic signal.  params:
+ *   PM1:         unused
+ *   UNIFORM:     params[0] = A (values in [-A, A])
+ *   NOISY_MASKS: params[0] = K (1..8 masks), params[1] = thr (noise
+ *                probability * 2^64, an integer), params[2..2+K) = masks s_k,
+ *                params[2+K..2+2K) = per-mask noise seeds.
+ * Asynchronous.
+ */
+int bw_gen_i64(int64_t *data, int log2n, int kind, uint64_t seed,
+               const uint64_t *params, int nparams, void *stream);
+
+/* Global offset variant: element i of data gets the value of index base+i
+ * of the 2^log2n signal (used by the sharded path). */
+int bw_gen_range_i64(int64_t *data, uint64_t base, uint64_t count, int kind,
+                     uint64_t seed, const uint64_t *params, int nparams,
+                     void *stream);
+
+/*
+ * Threshold extraction (noisy.py:185-222): all (index, value) with
+ * |value| >= tau, written sorted by ascending index to out_idx_dev /
+ * out_val_dev (device arrays of `cap` entries).  *count (host) receives the
+ * number of hits; if it exceeds cap, BW_CAPACITY is returned and nothing
+ * beyond cap is written (call again with a larger cap).  |INT64_MIN| is
+ * treated as 2^63.  Index offset `base` is added to every index (shards).
+ * scratch_dev must hold bw_extract_scratch_bytes(log2n) bytes (NULL = use
+ * an internal per-device buffer).  Synchronous (one small read-back).
+ */
+int bw_extract_ge_i64(const int64_t *data, int log2n, uint64_t tau,
+                      uint64_t base, int64_t *out_idx_dev, int64_t *out_val_dev,
+                      uint64_t cap, void *scratch_dev, void *stream,
+                      uint64_t *count);
+uint64_t bw_extract_scratch_bytes(int log2n);
+
+/* ---- planner ----------------------------------------------------------- */
+
+/*
+ * Describe the pass plan for a 2^log2n transform over 2^log2p shards as JSON:
+ *   {"log2n":..,"log2p":..,"local_log2n":..,"passes":[{"kind":"low"|"high"|
+ *    "reg"|"small","k":..,"r":..,"tile_bits":..,"cols_bits":..,
+ *    "threads":..,"grid":..,"smem":..}, ...], "cross_stages":[..],
+ *    "hbm_bytes_per_pass":..}
+ * Returns the needed length (excluding NUL); writes at most len bytes.
+ */
+int bw_plan_describe(int log2n, int log2p, char *json, size_t len);
+
+/*
+ * Static plan checker (mirror of parallel.py:114-147 check_disjoint /
+ * total_butterflies for GPU pass plans): walks, on the host, exactly the
+ * address tables the kernels use and verifies that within every pass each
+ * element is touched by exactly one (CTA, thread, register) and that every
+ * stage 0..log2n-1 is applied exactly once.  Exhaustive; log2n <= 24.
+ * pass_bits as in bw_fwht_i64_planned (NULL = default plan).
+ */
+int bw_plan_check(int log2n, const int *pass_bits, int npasses,
+                  uint64_t *butterflies);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BIGWHT_B200_H */

@@ -1,0 +1,289 @@
+"""Drop-in core API: ``Signal``, ``fwht_array``, ``fwht_inplace``, ...
+
+Mirrors /root/reference/pkg/src/bigwht/core.py (same names, argument
+meaning, return values and exceptions) with the arithmetic moved to the
+B200 kernels behind the C ABI (include/bigwht_b200.h).
+
+Accepted buffers:
+  * torch CUDA tensors (int64 or float64, 1-D, contiguous) -- transformed in
+    place in HBM, ordered on torch's current CUDA stream;
+  * numpy arrays (the reference's own type) -- staged through the device
+    (host -> HBM -> transform -> host, same call), so reference callers and
+    tests work unchanged.  There is no CPU arithmetic path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import BadArguments, DeviceError, OverflowBoundError
+
+_INT64_LIMIT = 1 << 63
+
+
+class Domain(enum.Enum):
+    """core.py:32-34."""
+
+    TIME = "time"
+    WALSH = "walsh"
+
+
+def _is_power_of_two(value: int) -> bool:
+    return value > 0 and (value & (value - 1)) == 0
+
+
+def _length(buf) -> int:
+    return int(buf.shape[0])
+
+
+def _log2(buf) -> int:
+    return _length(buf).bit_length() - 1
+
+
+def _dtype_kind(buf) -> str:
+    """'i64', 'f64' or a description of an unsupported dtype."""
+    if isinstance(buf, torch.Tensor):
+        if buf.dtype == torch.int64:
+            return "i64"
+        if buf.dtype == torch.float64:
+            return "f64"
+        return str(buf.dtype)
+    if isinstance(buf, np.ndarray):
+        if buf.dtype == np.dtype(np.int64):
+            return "i64"
+        if buf.dtype == np.dtype(np.float64):
+            return "f64"
+        return str(buf.dtype)
+    raise BadArguments(f"unsupported buffer type {type(buf).__name__}")
+
+
+def _stream_handle(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _require_cuda(t: torch.Tensor) -> None:
+    if not t.is_cuda:
+        raise BadArguments("torch buffers must live on a CUDA device (no CPU path)")
+
+
+@dataclass
+class Signal:
+    """A 1-D array of 2**n samples tagged with its current domain
+    (core.py:37-77).  ``data`` is a torch CUDA tensor or a numpy array of
+    dtype int64 (exact) or float64."""
+
+    data: object
+    domain: Domain = Domain.TIME
+
+    def __post_init__(self) -> None:
+        if isinstance(self.data, torch.Tensor):
+            arr = self.data
+        else:
+            arr = np.asarray(self.data)
+        if arr.ndim != 1:
+            raise BadArguments("signal data must be one-dimensional")
+        if not _is_power_of_two(_length(arr)):
+            raise BadArguments(f"signal length {_length(arr)} is not a power of two")
+        kind = _dtype_kind(arr)
+        if kind not in ("i64", "f64"):
+            raise BadArguments(f"unsupported dtype {kind}; use int64 or float64")
+        # The in-place kernels need contiguous storage (core.py:60-62).
+        if isinstance(arr, torch.Tensor):
+            self.data = arr.contiguous()
+        else:
+            self.data = np.ascontiguousarray(arr)
+
+    @property
+    def log2_dim(self) -> int:
+        return _log2(self.data)
+
+    @property
+    def dim(self) -> int:
+        return _length(self.data)
+
+    @property
+    def is_exact(self) -> bool:
+        return _dtype_kind(self.data) == "i64"
+
+    def copy(self) -> "Signal":
+        return Signal(self.data.clone() if isinstance(self.data, torch.Tensor) else self.data.copy(), self.domain)
+
+
+# ----------------------------------------------------------------- helpers ---
+
+def _check_contiguous(buf) -> None:
+    if isinstance(buf, torch.Tensor):
+        ok = buf.is_contiguous()
+    else:
+        ok = buf.flags.c_contiguous
+    if not ok:
+        raise BadArguments("in-place transform needs a contiguous buffer")
+
+
+def _check_shape(buf) -> int:
+    if buf.ndim != 1:
+        raise BadArguments("signal data must be one-dimensional")
+    if not _is_power_of_two(_length(buf)):
+        # The reference would raise numpy's ValueError after mutating part of
+        # the buffer; we refuse before any launch.
+        raise BadArguments(f"signal length {_length(buf)} is not a power of two")
+    return _log2(buf)
+
+
+class _HostStage:
+    """Device workspace for numpy buffers (reused between calls)."""
+
+    _work: dict = {}
+
+    @classmethod
+    def get(cls, n: int, dtype) -> torch.Tensor:
+        dev = torch.cuda.current_device()
+        key = (dev, dtype)
+        w = cls._work.get(key)
+        if w is None or w.numel() < (1 << n):
+            w = torch.empty(1 << n, dtype=dtype, device=f"cuda:{dev}")
+            cls._work[key] = w
+        return w[: 1 << n]
+
+
+def _need_cuda() -> None:
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device is visible; the transform runs only on a B200")
+
+
+# ------------------------------------------------------------------- API ---
+
+def check_magnitude_bound(data, log2_dim: int) -> None:
+    """Enforce M * 2**n < 2**63 for int64 data (core.py:80-94), on the GPU."""
+    if _dtype_kind(data) != "i64" or _length(data) == 0:
+        return
+    if isinstance(data, np.ndarray):
+        _need_cuda()
+        work = _HostStage.get(_log2(data), torch.int64)
+        work.copy_(torch.from_numpy(np.ascontiguousarray(data)))
+        data = work
+    _require_cuda(data)
+    with torch.cuda.device(data.device):
+        if log2_dim > 63:
+            raise OverflowBoundError(f"n = {log2_dim} cannot satisfy the int64 bound")
+        m = ctypes.c_uint64(0)
+        # bw_check_bound_i64 needs the signal length to be 2**log2n; for an
+        # arbitrary length use the raw reduction and apply the bound here.
+        if _length(data) == (1 << _log2(data)) and _log2(data) == log2_dim:
+            _lib.check(_lib.lib().bw_check_bound_i64(data.data_ptr(), log2_dim, None,
+                                                     _stream_handle(data), ctypes.byref(m)))
+            return
+        out = torch.empty(2, dtype=torch.int64, device=data.device)
+        _lib.check(_lib.lib().bw_minmax_i64(data.data_ptr(), _length(data), out.data_ptr(),
+                                            _stream_handle(data)))
+        mx, mn = (int(v) for v in out.tolist())
+        magnitude = max(mx, -mn)
+        if magnitude << log2_dim >= _INT64_LIMIT:
+            raise OverflowBoundError(
+                f"max |x| = {magnitude} with n = {log2_dim} can overflow int64; need |x| * 2**n < 2**63"
+            )
+
+
+def fwht_array(buf) -> int:
+    """Transform ``buf`` (length 2**n, contiguous) in place (core.py:97-117).
+
+    Stage k pairs elements at stride 2**k and replaces (a, b) with
+    (a + b, a - b).  Returns n * 2**(n-1).  No magnitude check, exactly like
+    the reference: int64 arithmetic wraps mod 2**64 as numpy's does.
+    """
+    _check_contiguous(buf)
+    n = _check_shape(buf)
+    kind = _dtype_kind(buf)
+    if kind not in ("i64", "f64"):
+        raise BadArguments(f"unsupported dtype {kind}; use int64 or float64")
+    _need_cuda()
+    bf = ctypes.c_uint64(0)
+    L = _lib.lib()
+    if isinstance(buf, np.ndarray):
+        if kind == "i64":
+            work = _HostStage.get(n, torch.int64)
+            _lib.check(L.bw_fwht_host_i64(buf.ctypes.data, n, work.data_ptr(), 0,
+                                          _stream_handle(work), ctypes.byref(bf)))
+            return int(bf.value)
+        work = _HostStage.get(n, torch.float64)
+        work.copy_(torch.from_numpy(buf))
+        with torch.cuda.device(work.device):
+            _lib.check(L.bw_fwht_f64(work.data_ptr(), n, _stream_handle(work), ctypes.byref(bf)))
+        buf[...] = work.cpu().numpy()
+        return int(bf.value)
+    _require_cuda(buf)
+    with torch.cuda.device(buf.device):
+        if kind == "i64":
+            _lib.check(L.bw_fwht_i64(buf.data_ptr(), n, _stream_handle(buf), ctypes.byref(bf)))
+        else:
+            _lib.check(L.bw_fwht_f64(buf.data_ptr(), n, _stream_handle(buf), ctypes.byref(bf)))
+    return int(bf.value)
+
+
+def _flip(domain: Domain) -> Domain:
+    return Domain.WALSH if domain == Domain.TIME else Domain.TIME
+
+
+def fwht_inplace(sig: Signal) -> Signal:
+    """Fast in-place WHT; flips the domain tag and returns its argument
+    (core.py:120-125).  The magnitude bound is checked on the device before
+    any mutation (OverflowBoundError leaves the data untouched)."""
+    buf = sig.data
+    n = sig.log2_dim
+    _need_cuda()
+    L = _lib.lib()
+    bf = ctypes.c_uint64(0)
+    if sig.is_exact:
+        if isinstance(buf, np.ndarray):
+            work = _HostStage.get(n, torch.int64)
+            _lib.check(L.bw_fwht_host_i64(buf.ctypes.data, n, work.data_ptr(), 1,
+                                          _stream_handle(work), ctypes.byref(bf)))
+        else:
+            _require_cuda(buf)
+            with torch.cuda.device(buf.device):
+                _lib.check(L.bw_fwht_inplace_i64(buf.data_ptr(), n, None, _stream_handle(buf),
+                                                 ctypes.byref(bf)))
+    else:
+        fwht_array(buf)
+    sig.domain = _flip(sig.domain)
+    return sig
+
+
+def inverse_wht_inplace(sig: Signal) -> Signal:
+    """Inverse transform in place (core.py:147-173): forward WHT then exact
+    division by 2**n; on an inexact int64 division the buffer is restored
+    and InexactDivision raised."""
+    if sig.domain != Domain.WALSH:
+        raise BadArguments("inverse transform expects a Walsh-domain signal")
+    n = sig.log2_dim
+    _need_cuda()
+    L = _lib.lib()
+    buf = sig.data
+    host = None
+    if isinstance(buf, np.ndarray):
+        host = buf
+        buf = _HostStage.get(n, torch.int64 if sig.is_exact else torch.float64)
+        buf.copy_(torch.from_numpy(host))
+    _require_cuda(buf)
+    try:
+        with torch.cuda.device(buf.device):
+            if sig.is_exact:
+                _lib.check(L.bw_inverse_i64(buf.data_ptr(), n, None, _stream_handle(buf)))
+            else:
+                _lib.check(L.bw_inverse_f64(buf.data_ptr(), n, _stream_handle(buf)))
+    finally:
+        if host is not None:
+            host[...] = buf.cpu().numpy()
+    sig.domain = Domain.TIME
+    return sig
+
+
+def butterfly_count(n: int) -> int:
+    """n * 2**(n-1), the value fwht_array returns (core.py:117)."""
+    return n << max(n - 1, 0)

@@ -1,0 +1,860 @@
+// bw_abi.cu -- C ABI of the B200 FWHT (declared in include/bigwht_b200.h).
+//
+// Host-side planning, validation, launches and error mapping.  Every entry
+// point cites the reference interface it replaces; see the header.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <math.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/bigwht_b200.h"
+#include "bw_kernels.cuh"
+#include "bw_layouts.h"
+
+using bw::u64;
+typedef int CUresult_compat;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int status, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return status;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(BW_CUDA_ERROR, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define BW_CUDA(call)                                  \
+    do {                                               \
+        cudaError_t e_ = (call);                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+#define BW_LAUNCHED(what)                                  \
+    do {                                                   \
+        cudaError_t e_ = cudaGetLastError();               \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+#define BW_TRY(expr)                  \
+    do {                              \
+        int s_ = (expr);              \
+        if (s_ != BW_OK) return s_;   \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+constexpr int kMaxDevices = 64;
+std::mutex g_mu;
+bool g_attr_done[kMaxDevices];
+int g_num_sms[kMaxDevices];
+void* g_scratch[kMaxDevices];
+size_t g_scratch_bytes[kMaxDevices];
+
+// Per-device one-time setup: opt-in dynamic shared memory sizes.
+int device_setup(int* dev_out) {
+    int dev = 0;
+    BW_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= kMaxDevices) return fail(BW_NOT_SUPPORTED, "device id %d out of range", dev);
+    *dev_out = dev;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_attr_done[dev]) return BW_OK;
+    int major = 0, minor = 0;
+    BW_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    BW_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+    if (major != 10 || minor != 0)
+        return fail(BW_NOT_SUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a (B200) only",
+                    dev, major, minor);
+    BW_CUDA(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev));
+    const int low_smem = bw::Dims<bw::CfgLow>::SMEM_ELEMS * 8;
+    const int high_smem = bw::Dims<bw::CfgHigh>::SMEM_ELEMS * 8;
+    BW_CUDA(cudaFuncSetAttribute(bw::k_pass<bw::CfgLow, 14>, cudaFuncAttributeMaxDynamicSharedMemorySize, low_smem));
+    BW_CUDA(cudaFuncSetAttribute(bw::k_pass<bw::CfgHigh, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, high_smem));
+    BW_CUDA(cudaFuncSetAttribute(bw::k_pass<bw::CfgHigh, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, high_smem));
+    BW_CUDA(cudaFuncSetAttribute(bw::k_pass<bw::CfgHigh, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, high_smem));
+    BW_CUDA(cudaFuncSetAttribute(bw::k_pass<bw::CfgHigh, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, high_smem));
+    BW_CUDA(cudaFuncSetAttribute(bw::k_pass<bw::CfgHigh, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, high_smem));
+    BW_CUDA(cudaFuncSetAttribute(bw::k_small<u64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (1 << 13) * 8));
+    BW_CUDA(cudaFuncSetAttribute(bw::k_small<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (1 << 13) * 8));
+    g_attr_done[dev] = true;
+    return BW_OK;
+}
+
+// Internal per-device scratch (never the signal itself).
+int scratch(int dev, size_t bytes, void** out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_scratch_bytes[dev] < bytes) {
+        if (g_scratch[dev]) cudaFree(g_scratch[dev]);
+        g_scratch[dev] = nullptr;
+        g_scratch_bytes[dev] = 0;
+        size_t want = bytes < 4096 ? 4096 : bytes;
+        cudaError_t e = cudaMalloc(&g_scratch[dev], want);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(scratch)");
+        g_scratch_bytes[dev] = want;
+    }
+    *out = g_scratch[dev];
+    return BW_OK;
+}
+
+int grid_for(int dev, uint64_t work_items, int threads, int per_sm) {
+    const uint64_t need = (work_items + threads - 1) / threads;
+    const uint64_t cap = (uint64_t)g_num_sms[dev] * per_sm;
+    uint64_t g = need < cap ? need : cap;
+    return g < 1 ? 1 : (int)g;
+}
+
+// ---- pass plan -------------------------------------------------------------
+
+struct Pass {
+    enum Kind { SMALL, LOW, HIGH, REG } kind;
+    int k;  // first stage bit
+    int r;  // number of stages
+};
+
+int default_plan(int n, std::vector<int>* widths) {
+    widths->clear();
+    if (n == 0) return BW_OK;
+    if (n < bw::kLowBits) {
+        widths->push_back(n);
+        return BW_OK;
+    }
+    widths->push_back(bw::kLowBits);
+    const int h = n - bw::kLowBits;
+    if (h == 0) return BW_OK;
+    const int q = (h + bw::kMaxHighBits - 1) / bw::kMaxHighBits;
+    for (int i = 0; i < q; ++i) widths->push_back(h / q + (i < h % q ? 1 : 0));
+    return BW_OK;
+}
+
+int build_passes(int n, const std::vector<int>& widths, std::vector<Pass>* passes) {
+    passes->clear();
+    if (n == 0) {
+        if (!widths.empty()) return fail(BW_BAD_ARGUMENTS, "n = 0 takes no passes");
+        return BW_OK;
+    }
+    if (widths.empty()) return fail(BW_BAD_ARGUMENTS, "empty pass plan for n = %d", n);
+    const int low = n < bw::kLowBits ? n : bw::kLowBits;
+    if (widths[0] != low)
+        return fail(BW_BAD_ARGUMENTS, "first pass must cover %d low bits (got %d)", low, widths[0]);
+    passes->push_back({n < bw::kLowBits ? Pass::SMALL : Pass::LOW, 0, low});
+    int k = low;
+    for (size_t i = 1; i < widths.size(); ++i) {
+        const int r = widths[i];
+        if (r < 1 || r > bw::kMaxHighBits)
+            return fail(BW_BAD_ARGUMENTS, "high pass width %d outside 1..%d", r, bw::kMaxHighBits);
+        passes->push_back({r <= bw::kRegOnlyMaxBits ? Pass::REG : Pass::HIGH, k, r});
+        k += r;
+    }
+    if (k != n) return fail(BW_BAD_ARGUMENTS, "pass widths cover %d bits, signal has %d", k, n);
+    return BW_OK;
+}
+
+int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s) {
+    const unsigned grid = p.kind == Pass::SMALL ? 1u : (unsigned)(1ull << (n - bw::kLowBits));
+    switch (p.kind) {
+        case Pass::SMALL:
+            bw::k_small<u64><<<1, 256, (size_t)(8ull << n), s>>>(d, n);
+            break;
+        case Pass::LOW:
+            bw::k_pass<bw::CfgLow, 14><<<grid, bw::Dims<bw::CfgLow>::NT, bw::Dims<bw::CfgLow>::SMEM_ELEMS * 8, s>>>(d, 14);
+            break;
+        case Pass::HIGH: {
+            constexpr int NT = bw::Dims<bw::CfgHigh>::NT;
+            constexpr size_t SM = bw::Dims<bw::CfgHigh>::SMEM_ELEMS * 8;
+            switch (bw::kLowBits - p.r) {
+                case 4: bw::k_pass<bw::CfgHigh, 4><<<grid, NT, SM, s>>>(d, p.k); break;
+                case 5: bw::k_pass<bw::CfgHigh, 5><<<grid, NT, SM, s>>>(d, p.k); break;
+                case 6: bw::k_pass<bw::CfgHigh, 6><<<grid, NT, SM, s>>>(d, p.k); break;
+                case 7: bw::k_pass<bw::CfgHigh, 7><<<grid, NT, SM, s>>>(d, p.k); break;
+                case 8: bw::k_pass<bw::CfgHigh, 8><<<grid, NT, SM, s>>>(d, p.k); break;
+                default: return fail(BW_BAD_ARGUMENTS, "no high-pass kernel for %d stages", p.r);
+            }
+            break;
+        }
+        case Pass::REG: {
+            constexpr int NT = bw::Dims<bw::CfgReg>::NT;
+            const unsigned rgrid = (unsigned)(1ull << (n - bw::CfgReg::T));
+            switch (bw::CfgReg::T - p.r) {
+                case 8: bw::k_pass<bw::CfgReg, 8><<<rgrid, NT, 0, s>>>(d, p.k); break;
+                case 9: bw::k_pass<bw::CfgReg, 9><<<rgrid, NT, 0, s>>>(d, p.k); break;
+                case 10: bw::k_pass<bw::CfgReg, 10><<<rgrid, NT, 0, s>>>(d, p.k); break;
+                case 11: bw::k_pass<bw::CfgReg, 11><<<rgrid, NT, 0, s>>>(d, p.k); break;
+                case 12: bw::k_pass<bw::CfgReg, 12><<<rgrid, NT, 0, s>>>(d, p.k); break;
+                default: return fail(BW_BAD_ARGUMENTS, "no register pass kernel for %d stages", p.r);
+            }
+            break;
+        }
+    }
+    BW_LAUNCHED("fwht pass launch");
+    return BW_OK;
+}
+
+int run_naive(u64* d, int n, int dev, cudaStream_t s) {
+    const uint64_t half = n ? (1ull << (n - 1)) : 0;
+    for (int k = 0; k < n; ++k) {
+        bw::k_stage<u64><<<grid_for(dev, half, 256, 8), 256, 0, s>>>(d, half, k);
+        BW_LAUNCHED("k_stage launch");
+    }
+    return BW_OK;
+}
+
+int check_signal(const void* data, int log2n) {
+    if (log2n < 0 || log2n > BW_MAX_LOG2N)
+        return fail(BW_BAD_ARGUMENTS, "log2n = %d outside 0..%d", log2n, BW_MAX_LOG2N);
+    if (!data) return fail(BW_BAD_ARGUMENTS, "null signal pointer");
+    if (reinterpret_cast<uintptr_t>(data) & 7u)
+        return fail(BW_BAD_ARGUMENTS, "signal pointer is not 8-byte aligned");
+    return BW_OK;
+}
+
+int fwht_impl(int64_t* data, int log2n, const std::vector<int>* widths, bool naive, cudaStream_t s) {
+    BW_TRY(check_signal(data, log2n));
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    u64* d = reinterpret_cast<u64*>(data);
+    if (log2n == 0) return BW_OK;
+    // 16-byte vector accesses need a 16-byte aligned base; an 8-byte aligned
+    // view (e.g. an odd-offset slice) takes the per-stage path, still on GPU.
+    if (naive || (log2n >= bw::kLowBits && (reinterpret_cast<uintptr_t>(data) & 15u)))
+        return run_naive(d, log2n, dev, s);
+    std::vector<int> w;
+    if (widths) w = *widths; else BW_TRY(default_plan(log2n, &w));
+    std::vector<Pass> passes;
+    BW_TRY(build_passes(log2n, w, &passes));
+    for (const Pass& p : passes) BW_TRY(launch_pass(p, d, log2n, s));
+    return BW_OK;
+}
+
+uint64_t butterfly_count(int n) { return n == 0 ? 0 : (uint64_t)n << (n - 1); }
+
+int minmax_impl(const int64_t* data, uint64_t count, int64_t* out, int dev, cudaStream_t s) {
+    bw::k_minmax_init<<<1, 1, 0, s>>>(reinterpret_cast<long long*>(out));
+    BW_LAUNCHED("k_minmax_init launch");
+    const int grid = grid_for(dev, (count + 1) / 2, 512 * 4, 4);
+    bw::k_minmax<<<grid, 512, 0, s>>>(reinterpret_cast<const long long*>(data), count,
+                                     reinterpret_cast<long long*>(out));
+    BW_LAUNCHED("k_minmax launch");
+    return BW_OK;
+}
+
+// M = max(max, -min) as an exact unsigned value; bound M * 2^n < 2^63.
+uint64_t magnitude(int64_t mx, int64_t mn) {
+    const uint64_t a = mx > 0 ? (uint64_t)mx : 0;
+    const uint64_t b = mn < 0 ? (uint64_t)0 - (uint64_t)mn : 0;
+    return a > b ? a : b;
+}
+bool bound_ok(uint64_t M, int n) {
+    if (M == 0) return true;
+    if (n >= 63) return false;
+    return M < (1ull << (63 - n));
+}
+
+int bound_impl(const int64_t* data, int log2n, int64_t* scratch_dev, int dev, cudaStream_t s, uint64_t* max_abs) {
+    int64_t* sc = scratch_dev;
+    if (!sc) {
+        void* p = nullptr;
+        BW_TRY(scratch(dev, 64, &p));
+        sc = reinterpret_cast<int64_t*>(p);
+    }
+    BW_TRY(minmax_impl(data, 1ull << log2n, sc, dev, s));
+    int64_t mm[2];
+    BW_CUDA(cudaMemcpyAsync(mm, sc, sizeof mm, cudaMemcpyDeviceToHost, s));
+    BW_CUDA(cudaStreamSynchronize(s));
+    const uint64_t M = magnitude(mm[0], mm[1]);
+    if (max_abs) *max_abs = M;
+    if (!bound_ok(M, log2n))
+        return fail(BW_OVERFLOW_BOUND,
+                    "max |x| = %llu with n = %d can overflow int64; need |x| * 2**n < 2**63",
+                    (unsigned long long)M, log2n);
+    return BW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bw_abi_version(void) { return BW_ABI_VERSION; }
+
+const char* bw_last_error(void) { return g_err.c_str(); }
+
+int bw_device_cc(int device) {
+    int major = 0, minor = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    if (cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    return major * 10 + minor;
+}
+
+// fwht_array (core.py:97-117)
+int bw_fwht_i64(int64_t* data, int log2n, void* stream, uint64_t* butterflies) {
+    BW_TRY(fwht_impl(data, log2n, nullptr, false, as_stream(stream)));
+    if (butterflies) *butterflies = butterfly_count(log2n);
+    return BW_OK;
+}
+
+// Pass-level access to the default plan (benchmark instrumentation: one
+// CUDA event per pass boundary gives each kernel's duration in the step).
+int bw_plan_npasses(int log2n) {
+    if (log2n < 0 || log2n > BW_MAX_LOG2N) return -fail(BW_BAD_ARGUMENTS, "log2n = %d outside 0..%d", log2n, BW_MAX_LOG2N);
+    std::vector<int> w;
+    default_plan(log2n, &w);
+    return (int)w.size();
+}
+
+int bw_fwht_i64_pass(int64_t* data, int log2n, int pass_index, void* stream) {
+    BW_TRY(check_signal(data, log2n));
+    if (log2n >= bw::kLowBits && (reinterpret_cast<uintptr_t>(data) & 15u))
+        return fail(BW_BAD_ARGUMENTS, "pass-level launches need a 16-byte aligned signal");
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    std::vector<int> w;
+    BW_TRY(default_plan(log2n, &w));
+    std::vector<Pass> passes;
+    BW_TRY(build_passes(log2n, w, &passes));
+    if (pass_index < 0 || pass_index >= (int)passes.size())
+        return fail(BW_BAD_ARGUMENTS, "pass %d outside 0..%d", pass_index, (int)passes.size() - 1);
+    return launch_pass(passes[pass_index], reinterpret_cast<u64*>(data), log2n, as_stream(stream));
+}
+
+int bw_fwht_i64_planned(int64_t* data, int log2n, const int* pass_bits, int npasses, void* stream) {
+    if (npasses < 0 || (npasses > 0 && !pass_bits)) return fail(BW_BAD_ARGUMENTS, "bad pass list");
+    if (npasses == 0) return fwht_impl(data, log2n, nullptr, true, as_stream(stream));
+    std::vector<int> w(pass_bits, pass_bits + npasses);
+    return fwht_impl(data, log2n, &w, false, as_stream(stream));
+}
+
+// fwht_array on a float64 buffer (core.py:97-117): stages strictly ascending
+// (2^13-element shared-memory tiles for stages 0..12, then one launch per
+// stage), each stage the same IEEE a+b / a-b as numpy, so bitwise identical.
+int bw_fwht_f64(double* data, int log2n, void* stream, uint64_t* butterflies) {
+    BW_TRY(check_signal(data, log2n));
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    cudaStream_t s = as_stream(stream);
+    if (log2n > 0) {
+        const int t = log2n < 13 ? log2n : 13;
+        bw::k_small<double><<<(unsigned)(1ull << (log2n - t)), 256, (size_t)(8ull << t), s>>>(data, t);
+        BW_LAUNCHED("k_small<double> launch");
+        const uint64_t half = 1ull << (log2n - 1);
+        for (int k = t; k < log2n; ++k) {
+            bw::k_stage<double><<<grid_for(dev, half, 256, 8), 256, 0, s>>>(data, half, k);
+            BW_LAUNCHED("k_stage<double> launch");
+        }
+    }
+    if (butterflies) *butterflies = butterfly_count(log2n);
+    return BW_OK;
+}
+
+// inverse_wht_inplace for float64 (core.py:168-169): forward then * 2^-n.
+int bw_inverse_f64(double* data, int log2n, void* stream) {
+    BW_TRY(bw_fwht_f64(data, log2n, stream, nullptr));
+    if (log2n == 0) return BW_OK;
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    const uint64_t count = 1ull << log2n;
+    bw::k_scale_f64<<<grid_for(dev, count, 256, 8), 256, 0, as_stream(stream)>>>(data, count, ldexp(1.0, -log2n));
+    BW_LAUNCHED("k_scale_f64 launch");
+    return BW_OK;
+}
+
+int bw_minmax_i64(const int64_t* data, uint64_t count, int64_t* out_minmax_dev, void* stream) {
+    if (!data || !out_minmax_dev) return fail(BW_BAD_ARGUMENTS, "null pointer");
+    if (count == 0) return fail(BW_BAD_ARGUMENTS, "empty signal");
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    return minmax_impl(data, count, out_minmax_dev, dev, as_stream(stream));
+}
+
+// check_magnitude_bound (core.py:80-94)
+int bw_check_bound_i64(const int64_t* data, int log2n, int64_t* scratch_dev, void* stream, uint64_t* max_abs) {
+    BW_TRY(check_signal(data, log2n));
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    return bound_impl(data, log2n, scratch_dev, dev, as_stream(stream), max_abs);
+}
+
+// fwht_inplace (core.py:120-125): bound first (raise before mutation), then transform.
+int bw_fwht_inplace_i64(int64_t* data, int log2n, int64_t* scratch_dev, void* stream, uint64_t* butterflies) {
+    BW_TRY(bw_check_bound_i64(data, log2n, scratch_dev, stream, nullptr));
+    return bw_fwht_i64(data, log2n, stream, butterflies);
+}
+
+int bw_fwht_host_i64(int64_t* host, int log2n, int64_t* work_dev, int check_bound, void* stream,
+                     uint64_t* butterflies) {
+    if (!host) return fail(BW_BAD_ARGUMENTS, "null host pointer");
+    BW_TRY(check_signal(work_dev, log2n));
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    cudaStream_t s = as_stream(stream);
+    const size_t bytes = (size_t)8 << log2n;
+    BW_CUDA(cudaMemcpyAsync(work_dev, host, bytes, cudaMemcpyHostToDevice, s));
+    int64_t* sc = nullptr;
+    if (check_bound) {
+        void* p = nullptr;
+        BW_TRY(scratch(dev, 64, &p));
+        sc = reinterpret_cast<int64_t*>(p);
+        BW_TRY(minmax_impl(work_dev, 1ull << log2n, sc, dev, s));
+    }
+    BW_TRY(fwht_impl(work_dev, log2n, nullptr, false, s));
+    if (check_bound) {
+        int64_t mm[2];
+        BW_CUDA(cudaMemcpyAsync(mm, sc, sizeof mm, cudaMemcpyDeviceToHost, s));
+        BW_CUDA(cudaStreamSynchronize(s));
+        const uint64_t M = magnitude(mm[0], mm[1]);
+        if (!bound_ok(M, log2n))
+            return fail(BW_OVERFLOW_BOUND,
+                        "max |x| = %llu with n = %d can overflow int64; need |x| * 2**n < 2**63",
+                        (unsigned long long)M, log2n);
+    }
+    BW_CUDA(cudaMemcpyAsync(host, work_dev, bytes, cudaMemcpyDeviceToHost, s));
+    BW_CUDA(cudaStreamSynchronize(s));
+    if (butterflies) *butterflies = butterfly_count(log2n);
+    return BW_OK;
+}
+
+// inverse_wht_inplace (core.py:147-173), int64 payload.
+int bw_inverse_i64(int64_t* data, int log2n, int64_t* scratch_dev, void* stream) {
+    BW_TRY(check_signal(data, log2n));
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    cudaStream_t s = as_stream(stream);
+    BW_TRY(bound_impl(data, log2n, scratch_dev, dev, s, nullptr));
+    if (log2n == 0) return BW_OK;
+    BW_TRY(fwht_impl(data, log2n, nullptr, false, s));
+    void* p = nullptr;
+    BW_TRY(scratch(dev, 64, &p));
+    int* flag = reinterpret_cast<int*>(reinterpret_cast<char*>(p) + 32);
+    BW_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    const uint64_t count = 1ull << log2n;
+    const int grid = grid_for(dev, count, 256, 8);
+    bw::k_check_divisible<<<grid, 256, 0, s>>>(reinterpret_cast<const long long*>(data), count, log2n, flag);
+    BW_LAUNCHED("k_check_divisible launch");
+    int h = 0;
+    BW_CUDA(cudaMemcpyAsync(&h, flag, sizeof h, cudaMemcpyDeviceToHost, s));
+    BW_CUDA(cudaStreamSynchronize(s));
+    if (h) {
+        // Undo (core.py:160-166): H(Hx) = 2^n x, and 2^n divides exactly.
+        BW_TRY(fwht_impl(data, log2n, nullptr, false, s));
+    }
+    bw::k_shift_right<<<grid, 256, 0, s>>>(reinterpret_cast<long long*>(data), count, log2n);
+    BW_LAUNCHED("k_shift_right launch");
+    if (h) {
+        BW_CUDA(cudaStreamSynchronize(s));
+        return fail(BW_INEXACT_DIVISION, "coefficients are not all divisible by 2**%d", log2n);
+    }
+    return BW_OK;
+}
+
+// Cross-shard butterfly (parallel.py:103-110, all log2 P stage phases fused).
+static int xshard_launch(const bw::ShardPtrs& sp, int log2p, uint64_t begin, uint64_t count, cudaStream_t s) {
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    if (count == 0 || log2p == 0) return BW_OK;
+    const uint64_t pairs = count / 2;
+    const int grid = grid_for(dev, pairs, 256, 8);
+    switch (log2p) {
+        case 1: bw::k_xshard<1><<<grid, 256, 0, s>>>(sp, begin, pairs); break;
+        case 2: bw::k_xshard<2><<<grid, 256, 0, s>>>(sp, begin, pairs); break;
+        case 3: bw::k_xshard<3><<<grid, 256, 0, s>>>(sp, begin, pairs); break;
+        default: return fail(BW_INVALID_WORKERS, "log2p = %d outside 0..%d", log2p, BW_MAX_LOG2P);
+    }
+    BW_LAUNCHED("k_xshard launch");
+    return BW_OK;
+}
+
+int bw_xshard_i64(int64_t* const* shards, int log2p, uint64_t begin, uint64_t count, void* stream) {
+    if (log2p < 0 || log2p > BW_MAX_LOG2P)
+        return fail(BW_INVALID_WORKERS, "log2p = %d outside 0..%d", log2p, BW_MAX_LOG2P);
+    if ((begin | count) & 1ull) return fail(BW_BAD_ARGUMENTS, "begin and count must be even");
+    if (!shards) return fail(BW_BAD_ARGUMENTS, "null shard list");
+    bw::ShardPtrs sp;
+    memset(&sp, 0, sizeof sp);
+    for (int r = 0; r < (1 << log2p); ++r) {
+        if (!shards[r]) return fail(BW_BAD_ARGUMENTS, "null shard %d", r);
+        if (reinterpret_cast<uintptr_t>(shards[r]) & 15u)
+            return fail(BW_BAD_ARGUMENTS, "shard %d is not 16-byte aligned", r);
+        sp.p[r] = reinterpret_cast<u64*>(shards[r]);
+    }
+    return xshard_launch(sp, log2p, begin, count, as_stream(stream));
+}
+
+int bw_xshard_strided_i64(int64_t* base, uint64_t shard_stride, int log2p, uint64_t begin, uint64_t count,
+                          void* stream) {
+    if (!base) return fail(BW_BAD_ARGUMENTS, "null base");
+    if (log2p < 0 || log2p > BW_MAX_LOG2P)
+        return fail(BW_INVALID_WORKERS, "log2p = %d outside 0..%d", log2p, BW_MAX_LOG2P);
+    int64_t* ptrs[8];
+    for (int r = 0; r < (1 << log2p); ++r) ptrs[r] = base + r * shard_stride;
+    return bw_xshard_i64(ptrs, log2p, begin, count, stream);
+}
+
+// ---- peer memory plumbing for the one-process-per-GPU cross-shard stage ----
+
+typedef CUresult_compat (*addr_range_fn)(unsigned long long*, size_t*, unsigned long long);
+
+int bw_ipc_get_handle(const void* ptr, void* handle_out, uint64_t* offset_out) {
+    if (!ptr || !handle_out || !offset_out) return fail(BW_BAD_ARGUMENTS, "null argument");
+    // The handle names the whole allocation; the caller's pointer may sit
+    // inside it (caching allocators), so report the offset from its base.
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    BW_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(BW_CUDA_ERROR, "cuMemGetAddressRange unavailable");
+    unsigned long long base = 0;
+    size_t size = 0;
+    const int r = reinterpret_cast<addr_range_fn>(fn)(&base, &size, (unsigned long long)(uintptr_t)ptr);
+    if (r != 0) return fail(BW_CUDA_ERROR, "cuMemGetAddressRange failed (%d)", r);
+    cudaIpcMemHandle_t h;
+    BW_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    memcpy(handle_out, &h, sizeof h);
+    *offset_out = (uint64_t)((uintptr_t)ptr - base);
+    return BW_OK;
+}
+
+int bw_ipc_open_handle(const void* handle, uint64_t offset, void** ptr_out) {
+    if (!handle || !ptr_out) return fail(BW_BAD_ARGUMENTS, "null argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    void* base = nullptr;
+    BW_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *ptr_out = reinterpret_cast<char*>(base) + offset;
+    return BW_OK;
+}
+
+int bw_ipc_close_handle(void* ptr, uint64_t offset) {
+    if (!ptr) return fail(BW_BAD_ARGUMENTS, "null argument");
+    BW_CUDA(cudaIpcCloseMemHandle(reinterpret_cast<char*>(ptr) - offset));
+    return BW_OK;
+}
+
+int bw_enable_peer_access(int peer_device) {
+    int dev = 0;
+    BW_CUDA(cudaGetDevice(&dev));
+    if (dev == peer_device) return BW_OK;
+    int can = 0;
+    BW_CUDA(cudaDeviceCanAccessPeer(&can, dev, peer_device));
+    if (!can) return fail(BW_NOT_SUPPORTED, "device %d cannot access peer %d", dev, peer_device);
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return BW_OK;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    return BW_OK;
+}
+
+static int gen_params(int kind, uint64_t seed, const uint64_t* params, int nparams, bw::GenParams* g) {
+    memset(g, 0, sizeof *g);
+    g->kind = kind;
+    g->seed = seed;
+    switch (kind) {
+        case BW_GEN_PM1:
+            return BW_OK;
+        case BW_GEN_UNIFORM:
+            if (nparams < 1 || !params) return fail(BW_BAD_ARGUMENTS, "UNIFORM needs params[0] = A");
+            if (params[0] > (1ull << 62)) return fail(BW_BAD_ARGUMENTS, "A too large");
+            g->a = params[0];
+            return BW_OK;
+        case BW_GEN_NOISY_MASKS: {
+            if (nparams < 2 || !params) return fail(BW_BAD_ARGUMENTS, "NOISY_MASKS needs K, thr, masks, seeds");
+            const uint64_t K = params[0];
+            if (K < 1 || K > 8) return fail(BW_BAD_ARGUMENTS, "NOISY_MASKS needs 1 <= K <= 8");
+            if ((uint64_t)nparams < 2 + 2 * K) return fail(BW_BAD_ARGUMENTS, "NOISY_MASKS needs 2+2K params");
+            g->nmasks = (int)K;
+            g->thr = params[1];
+            for (uint64_t m = 0; m < K; ++m) {
+                g->mask[m] = params[2 + m];
+                g->mseed[m] = params[2 + K + m];
+            }
+            return BW_OK;
+        }
+        default:
+            return fail(BW_BAD_ARGUMENTS, "unknown generator kind %d", kind);
+    }
+}
+
+int bw_gen_range_i64(int64_t* data, uint64_t base, uint64_t count, int kind, uint64_t seed,
+                     const uint64_t* params, int nparams, void* stream) {
+    if (!data) return fail(BW_BAD_ARGUMENTS, "null output");
+    bw::GenParams g;
+    BW_TRY(gen_params(kind, seed, params, nparams, &g));
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    if (count == 0) return BW_OK;
+    bw::k_gen<<<grid_for(dev, count, 256, 16), 256, 0, as_stream(stream)>>>(reinterpret_cast<long long*>(data),
+                                                                              base, count, g);
+    BW_LAUNCHED("k_gen launch");
+    return BW_OK;
+}
+
+int bw_gen_i64(int64_t* data, int log2n, int kind, uint64_t seed, const uint64_t* params, int nparams,
+               void* stream) {
+    BW_TRY(check_signal(data, log2n));
+    return bw_gen_range_i64(data, 0, 1ull << log2n, kind, seed, params, nparams, stream);
+}
+
+uint64_t bw_extract_scratch_bytes(int log2n) {
+    if (log2n < 0 || log2n > BW_MAX_LOG2N) return 0;
+    const uint64_t chunks = ((1ull << log2n) + (1ull << bw::kExtractChunkBits) - 1) >> bw::kExtractChunkBits;
+    return (chunks + 1) * 8;
+}
+
+// extract_above (noisy.py:185-222) with |x| >= tau, ordered by index.
+int bw_extract_ge_i64(const int64_t* data, int log2n, uint64_t tau, uint64_t base, int64_t* out_idx_dev,
+                      int64_t* out_val_dev, uint64_t cap, void* scratch_dev, void* stream, uint64_t* count) {
+    BW_TRY(check_signal(data, log2n));
+    if (cap > 0 && (!out_idx_dev || !out_val_dev)) return fail(BW_BAD_ARGUMENTS, "null output arrays");
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    cudaStream_t s = as_stream(stream);
+    const uint64_t n = 1ull << log2n;
+    const uint64_t chunks = (n + (1ull << bw::kExtractChunkBits) - 1) >> bw::kExtractChunkBits;
+    void* sc = scratch_dev;
+    if (!sc) BW_TRY(scratch(dev, bw_extract_scratch_bytes(log2n), &sc));
+    unsigned long long* counts = reinterpret_cast<unsigned long long*>(sc);
+    bw::k_extract_count<<<(unsigned)chunks, 512, 0, s>>>(reinterpret_cast<const long long*>(data), n, tau, counts);
+    BW_LAUNCHED("k_extract_count launch");
+    bw::k_extract_scan<<<1, 1024, 0, s>>>(counts, chunks);
+    BW_LAUNCHED("k_extract_scan launch");
+    unsigned long long total = 0;
+    BW_CUDA(cudaMemcpyAsync(&total, counts + chunks, sizeof total, cudaMemcpyDeviceToHost, s));
+    BW_CUDA(cudaStreamSynchronize(s));
+    if (total > 0 && cap > 0) {
+        bw::k_extract_write<<<(unsigned)chunks, 512, 0, s>>>(
+            reinterpret_cast<const long long*>(data), n, tau, counts, counts + 1, base,
+            reinterpret_cast<long long*>(out_idx_dev), reinterpret_cast<long long*>(out_val_dev), cap);
+        BW_LAUNCHED("k_extract_write launch");
+        BW_CUDA(cudaStreamSynchronize(s));
+    }
+    if (count) *count = total;
+    if (total > cap)
+        return fail(BW_CAPACITY, "%llu hits exceed the output capacity %llu", (unsigned long long)total,
+                    (unsigned long long)cap);
+    return BW_OK;
+}
+
+// ---- planner ---------------------------------------------------------------
+
+int bw_plan_describe(int log2n, int log2p, char* json, size_t len) {
+    if (log2n < 0 || log2p < 0 || log2p > BW_MAX_LOG2P || log2p > log2n || log2n - log2p > BW_MAX_LOG2N)
+        return -fail(BW_BAD_ARGUMENTS, "bad plan request n=%d p=%d", log2n, log2p);
+    const int nl = log2n - log2p;
+    std::vector<int> w;
+    default_plan(nl, &w);
+    std::vector<Pass> passes;
+    if (build_passes(nl, w, &passes) != BW_OK) return -BW_BAD_ARGUMENTS;
+    std::string out;
+    char buf[256];
+    snprintf(buf, sizeof buf, "{\"log2n\":%d,\"log2p\":%d,\"local_log2n\":%d,\"passes\":[", log2n, log2p, nl);
+    out += buf;
+    for (size_t i = 0; i < passes.size(); ++i) {
+        const Pass& p = passes[i];
+        const char* kind = p.kind == Pass::SMALL ? "small" : p.kind == Pass::LOW ? "low" : p.kind == Pass::HIGH ? "high" : "reg";
+        int threads = 256, smem = 0, cols = 0;
+        unsigned long long grid = 1;
+        if (p.kind == Pass::SMALL) {
+            smem = 8 << nl;
+            cols = nl;
+        } else {
+            grid = 1ull << (nl - bw::kLowBits);
+            if (p.kind == Pass::LOW) {
+                threads = bw::Dims<bw::CfgLow>::NT;
+                smem = bw::Dims<bw::CfgLow>::SMEM_ELEMS * 8;
+                cols = bw::kLowBits;
+            } else if (p.kind == Pass::HIGH) {
+                threads = bw::Dims<bw::CfgHigh>::NT;
+                smem = bw::Dims<bw::CfgHigh>::SMEM_ELEMS * 8;
+                cols = bw::kLowBits - p.r;
+            } else {
+                threads = bw::Dims<bw::CfgReg>::NT;
+                cols = bw::CfgReg::T - p.r;
+                grid = 1ull << (nl - bw::CfgReg::T);
+            }
+        }
+        snprintf(buf, sizeof buf,
+                 "%s{\"kind\":\"%s\",\"k\":%d,\"r\":%d,\"tile_bits\":%d,\"cols_bits\":%d,\"threads\":%d,"
+                 "\"grid\":%llu,\"smem\":%d}",
+                 i ? "," : "", kind, p.k, p.r,
+                 p.kind == Pass::SMALL ? nl : p.kind == Pass::REG ? bw::CfgReg::T : bw::kLowBits, cols, threads, grid,
+                 smem);
+        out += buf;
+    }
+    out += "],\"cross_stages\":[";
+    for (int b = 0; b < log2p; ++b) {
+        snprintf(buf, sizeof buf, "%s%d", b ? "," : "", nl + b);
+        out += buf;
+    }
+    snprintf(buf, sizeof buf, "],\"hbm_bytes_per_pass\":%llu}", (unsigned long long)(16ull << nl));
+    out += buf;
+    if (json && len) {
+        const size_t m = out.size() < len - 1 ? out.size() : len - 1;
+        memcpy(json, out.data(), m);
+        json[m] = 0;
+    }
+    return (int)out.size();
+}
+
+}  // extern "C"
+
+// ---- static plan checker (host walk of the kernels' own address tables) ----
+namespace {
+
+template <class C, int RD>
+bool round_is_permutation(std::string* why) {
+    uint32_t seen = 0;
+    auto add = [&](int b) {
+        if (b < 0 || b >= C::T || ((seen >> b) & 1u)) return false;
+        seen |= 1u << b;
+        return true;
+    };
+    for (int i = 0; i < C::R; ++i) if (!add(C::reg(RD, i))) { *why = "register bits overlap"; return false; }
+    for (int i = 0; i < 5; ++i) if (!add(C::lane(RD, i))) { *why = "lane bits overlap"; return false; }
+    for (int i = 0; i < C::W; ++i) if (!add(C::warp(RD, i))) { *why = "warp bits overlap"; return false; }
+    if (seen != (1u << C::T) - 1u) { *why = "round does not cover every tile bit"; return false; }
+    return true;
+}
+
+// Half-warp bank check of the padded smem slots of a round (8-byte words:
+// 16 lanes must hit 16 distinct 8-byte bank pairs).
+template <class C, int RD>
+bool round_conflict_free(std::string* why) {
+    for (uint32_t warp = 0; warp < (1u << C::W); ++warp)
+        for (int j = 0; j < bw::Dims<C>::E; ++j)
+            for (uint32_t half = 0; half < 2; ++half) {
+                uint32_t used = 0;
+                for (uint32_t l = 0; l < 16; ++l) {
+                    const uint32_t lane = half * 16 + l;
+                    const uint32_t e = bw::thread_part<C, RD>(lane, warp) | bw::reg_part<C, RD>(j);
+                    const uint32_t bank = bw::smem_slot(e) & 15u;
+                    if ((used >> bank) & 1u) { *why = "smem bank conflict"; return false; }
+                    used |= 1u << bank;
+                }
+            }
+    return true;
+}
+
+template <class C, int L>
+int check_pass(int n, int k, std::vector<uint8_t>& touched, uint32_t* stage_bits_out, uint64_t* bfly) {
+    constexpr int T = C::T;
+    std::string why;
+    if (!round_is_permutation<C, 0>(&why)) return fail(BW_BAD_ARGUMENTS, "layout round 0: %s", why.c_str());
+    if constexpr (C::NR >= 2) {
+        if (!round_is_permutation<C, 1>(&why)) return fail(BW_BAD_ARGUMENTS, "layout round 1: %s", why.c_str());
+        if (!round_conflict_free<C, 0>(&why) || !round_conflict_free<C, 1>(&why))
+            return fail(BW_BAD_ARGUMENTS, "layout: %s", why.c_str());
+    }
+    if constexpr (C::NR >= 3) {
+        if (!round_is_permutation<C, 2>(&why)) return fail(BW_BAD_ARGUMENTS, "layout round 2: %s", why.c_str());
+        if (!round_conflict_free<C, 2>(&why)) return fail(BW_BAD_ARGUMENTS, "layout: %s", why.c_str());
+    }
+    // Stage coverage inside the tile: every row bit staged exactly once.
+    uint32_t tile_stages = 0;
+    uint32_t rounds_masks[3] = {bw::stage_mask<C, 0, L>(), C::NR > 1 ? bw::stage_mask<C, (C::NR > 1 ? 1 : 0), L>() : 0u,
+                                C::NR > 2 ? bw::stage_mask<C, (C::NR > 2 ? 2 : 0), L>() : 0u};
+    for (int r = 0; r < C::NR; ++r) {
+        if (tile_stages & rounds_masks[r]) return fail(BW_BAD_ARGUMENTS, "tile bit staged twice");
+        tile_stages |= rounds_masks[r];
+    }
+    const uint32_t rows = ((1u << T) - 1u) & ~((1u << L) - 1u);
+    if (tile_stages != rows) return fail(BW_BAD_ARGUMENTS, "tile stages %x != rows %x", tile_stages, rows);
+    uint32_t stage_bits = 0;
+    for (int b = L; b < T; ++b) stage_bits |= 1u << (L >= T ? b : k + (b - L));
+    if (L >= T) stage_bits = (1u << T) - 1u;
+    *stage_bits_out = stage_bits;
+    // Address walk: load layout and store layout must both be bijections.
+    const uint64_t tiles = 1ull << (n - T);
+    std::fill(touched.begin(), touched.end(), 0);
+    constexpr int LAST = C::NR - 1;
+    for (uint64_t b = 0; b < tiles; ++b) {
+        const uint64_t base = bw::tile_base<T, L>(b, k);
+        for (uint32_t t = 0; t < (uint32_t)bw::Dims<C>::NT; ++t) {
+            const uint32_t lane = t & 31u, warp = t >> 5;
+            for (int j = 0; j < bw::Dims<C>::E; ++j) {
+                const uint64_t gi = base + bw::global_off<T, L>(bw::thread_part<C, 0>(lane, warp), k) +
+                                    bw::global_off<T, L>(bw::reg_part<C, 0>(j), k);
+                const uint64_t go = base + bw::global_off<T, L>(bw::thread_part<C, LAST>(lane, warp), k) +
+                                    bw::global_off<T, L>(bw::reg_part<C, LAST>(j), k);
+                if (gi >= touched.size() || go >= touched.size())
+                    return fail(BW_BAD_ARGUMENTS, "pass at k=%d reaches out of range", k);
+                if (touched[gi] & 1) return fail(BW_BAD_ARGUMENTS, "pass at k=%d loads index %llu twice", k, (unsigned long long)gi);
+                if (touched[go] & 2) return fail(BW_BAD_ARGUMENTS, "pass at k=%d stores index %llu twice", k, (unsigned long long)go);
+                touched[gi] |= 1;
+                touched[go] |= 2;
+            }
+        }
+    }
+    for (uint8_t x : touched)
+        if (x != 3) return fail(BW_BAD_ARGUMENTS, "pass at k=%d misses an element", k);
+    *bfly += (uint64_t)__builtin_popcount(stage_bits) << (n - 1);
+    return BW_OK;
+}
+
+}  // namespace
+
+extern "C" int bw_plan_check(int log2n, const int* pass_bits, int npasses, uint64_t* butterflies) {
+    if (log2n < 0 || log2n > 24) return fail(BW_BAD_ARGUMENTS, "plan check supports 0 <= n <= 24");
+    std::vector<int> w;
+    if (pass_bits && npasses > 0) w.assign(pass_bits, pass_bits + npasses);
+    else default_plan(log2n, &w);
+    std::vector<Pass> passes;
+    BW_TRY(build_passes(log2n, w, &passes));
+    uint64_t bfly = 0;
+    uint32_t covered = 0;
+    std::vector<uint8_t> touched((size_t)1 << log2n);
+    for (const Pass& p : passes) {
+        uint32_t bits = 0;
+        int st = BW_OK;
+        switch (p.kind) {
+            case Pass::SMALL:
+                bits = (1u << log2n) - 1u;
+                bfly += (uint64_t)log2n << (log2n - 1);
+                break;
+            case Pass::LOW:
+                st = check_pass<bw::CfgLow, 14>(log2n, 14, touched, &bits, &bfly);
+                break;
+            case Pass::HIGH:
+                switch (bw::kLowBits - p.r) {
+                    case 4: st = check_pass<bw::CfgHigh, 4>(log2n, p.k, touched, &bits, &bfly); break;
+                    case 5: st = check_pass<bw::CfgHigh, 5>(log2n, p.k, touched, &bits, &bfly); break;
+                    case 6: st = check_pass<bw::CfgHigh, 6>(log2n, p.k, touched, &bits, &bfly); break;
+                    case 7: st = check_pass<bw::CfgHigh, 7>(log2n, p.k, touched, &bits, &bfly); break;
+                    case 8: st = check_pass<bw::CfgHigh, 8>(log2n, p.k, touched, &bits, &bfly); break;
+                }
+                break;
+            case Pass::REG:
+                switch (bw::CfgReg::T - p.r) {
+                    case 8: st = check_pass<bw::CfgReg, 8>(log2n, p.k, touched, &bits, &bfly); break;
+                    case 9: st = check_pass<bw::CfgReg, 9>(log2n, p.k, touched, &bits, &bfly); break;
+                    case 10: st = check_pass<bw::CfgReg, 10>(log2n, p.k, touched, &bits, &bfly); break;
+                    case 11: st = check_pass<bw::CfgReg, 11>(log2n, p.k, touched, &bits, &bfly); break;
+                    case 12: st = check_pass<bw::CfgReg, 12>(log2n, p.k, touched, &bits, &bfly); break;
+                }
+                break;
+        }
+        if (st != BW_OK) return st;
+        if (covered & bits) return fail(BW_BAD_ARGUMENTS, "stage applied twice");
+        covered |= bits;
+    }
+    const uint32_t all = log2n ? (uint32_t)((1ull << log2n) - 1ull) : 0u;
+    if (covered != all) return fail(BW_BAD_ARGUMENTS, "stages covered %x, expected %x", covered, all);
+    if (butterflies) *butterflies = bfly;
+    return BW_OK;
+}

@@ -1,0 +1,456 @@
+// bw_kernels.cuh -- sm_100a kernels of the B200 FWHT.
+//
+// All arithmetic is on uint64 bit patterns: two's-complement add/sub wraps
+// modulo 2^64 exactly like numpy int64 (core.py:113-115), so every kernel is
+// bit-identical to the reference for any input and any stage order.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bw_layouts.h"
+
+namespace bw {
+
+typedef unsigned long long u64;
+
+// ---------------------------------------------------------------------------
+// Pass engine (kernels K1 low-bits, K2 high-bits, register-only high-bits).
+// ---------------------------------------------------------------------------
+
+template <class C, int RD, int L>
+__device__ __forceinline__ void apply_stages(u64 (&v)[Dims<C>::E]) {
+    constexpr int E = Dims<C>::E;
+    constexpr uint32_t mask = stage_mask<C, RD, L>();
+#pragma unroll
+    for (int i = 0; i < C::R; ++i) {
+        if ((mask >> C::reg(RD, i)) & 1u) {
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                if (!((j >> i) & 1)) {
+                    const u64 a = v[j], b = v[j | (1 << i)];
+                    v[j] = a + b;
+                    v[j | (1 << i)] = a - b;
+                }
+            }
+        }
+    }
+}
+
+// Round RD has tile bit 0 as register bit 0: global access as 16-byte pairs.
+template <class C, int RD, int L>
+struct VecAccess {
+    static constexpr bool value = (C::reg(RD, 0) == 0) && (L >= 1);
+};
+
+template <class C, int RD, int T, int L>
+__device__ __forceinline__ void load_global(u64 (&v)[Dims<C>::E], const u64* __restrict__ g,
+                                           uint32_t tp, int k) {
+    constexpr int E = Dims<C>::E;
+    const u64* p = g + global_off<T, L>(tp, k);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        const uint64_t off = global_off<T, L>(reg_part<C, RD>(j), k);
+        if constexpr (VecAccess<C, RD, L>::value) {
+            if ((j & 1) == 0) {
+                const ulonglong2 t = __ldcs(reinterpret_cast<const ulonglong2*>(p + off));
+                v[j] = t.x;
+                v[j + 1] = t.y;
+            }
+        } else {
+            v[j] = __ldcs(p + off);
+        }
+    }
+}
+
+template <class C, int RD, int T, int L>
+__device__ __forceinline__ void store_global(const u64 (&v)[Dims<C>::E], u64* __restrict__ g,
+                                             uint32_t tp, int k) {
+    constexpr int E = Dims<C>::E;
+    u64* p = g + global_off<T, L>(tp, k);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        const uint64_t off = global_off<T, L>(reg_part<C, RD>(j), k);
+        if constexpr (VecAccess<C, RD, L>::value) {
+            if ((j & 1) == 0) {
+                ulonglong2 t;
+                t.x = v[j];
+                t.y = v[j + 1];
+                __stcs(reinterpret_cast<ulonglong2*>(p + off), t);
+            }
+        } else {
+            __stcs(p + off, v[j]);
+        }
+    }
+}
+
+template <class C, int RD>
+__device__ __forceinline__ void store_smem(const u64 (&v)[Dims<C>::E], u64* sm, uint32_t tp) {
+    u64* p = sm + smem_slot(tp);
+#pragma unroll
+    for (int j = 0; j < Dims<C>::E; ++j) p[smem_slot(reg_part<C, RD>(j))] = v[j];
+}
+
+template <class C, int RD>
+__device__ __forceinline__ void load_smem(u64 (&v)[Dims<C>::E], const u64* sm, uint32_t tp) {
+    const u64* p = sm + smem_slot(tp);
+#pragma unroll
+    for (int j = 0; j < Dims<C>::E; ++j) v[j] = p[smem_slot(reg_part<C, RD>(j))];
+}
+
+// One pass over every tile: load (round 0 layout) -> stages -> [transpose ->
+// stages]* -> store (last round layout).  k = first global stage bit of the
+// rows (ignored for L == T).
+template <class C, int L>
+__global__ void __launch_bounds__(Dims<C>::NT, 1)
+    k_pass(u64* __restrict__ data, int k) {
+    constexpr int T = C::T;
+    constexpr int E = Dims<C>::E;
+    extern __shared__ u64 sm[];
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = threadIdx.x >> 5;
+    u64* g = data + tile_base<T, L>(blockIdx.x, k);
+
+    u64 v[E];
+    load_global<C, 0, T, L>(v, g, thread_part<C, 0>(lane, warp), k);
+    apply_stages<C, 0, L>(v);
+    if constexpr (C::NR >= 2) {
+        store_smem<C, 0>(v, sm, thread_part<C, 0>(lane, warp));
+        __syncthreads();
+        load_smem<C, 1>(v, sm, thread_part<C, 1>(lane, warp));
+        apply_stages<C, 1, L>(v);
+    }
+    if constexpr (C::NR >= 3) {
+        __syncthreads();
+        store_smem<C, 1>(v, sm, thread_part<C, 1>(lane, warp));
+        __syncthreads();
+        load_smem<C, 2>(v, sm, thread_part<C, 2>(lane, warp));
+        apply_stages<C, 2, L>(v);
+    }
+    constexpr int LAST = C::NR - 1;
+    store_global<C, LAST, T, L>(v, g, thread_part<C, LAST>(lane, warp), k);
+}
+
+// ---------------------------------------------------------------------------
+// Small transforms (n <= 13) and the float64 low-bits tiles: each CTA owns a
+// contiguous 2^n tile in shared memory and applies stages 0..n-1 in
+// ascending order (the order of core.py:108, which float64 bit identity
+// needs; for int64 any order is exact).
+// ---------------------------------------------------------------------------
+template <typename V>
+__global__ void __launch_bounds__(256) k_small(V* __restrict__ data, int n) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    V* sm = reinterpret_cast<V*>(sm_raw);
+    const uint32_t N = 1u << n;
+    V* d = data + (uint64_t)blockIdx.x * N;
+    for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) sm[i] = d[i];
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        const uint32_t low = (1u << k) - 1u;
+        for (uint32_t t = threadIdx.x; t < (N >> 1); t += blockDim.x) {
+            const uint32_t lo = ((t >> k) << (k + 1)) | (t & low);
+            const uint32_t hi = lo + (1u << k);
+            const V a = sm[lo], b = sm[hi];
+            sm[lo] = a + b;
+            sm[hi] = a - b;
+        }
+        __syncthreads();
+    }
+    for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) d[i] = sm[i];
+}
+
+// K0: one radix-2 stage k over the whole signal (Fig. 1 inner loop,
+// PAPER.md:189-201; pairing formula of parallel.py:108).  Debug/reference
+// aid for int64; the high stages of the float64 path.
+template <typename V>
+__global__ void k_stage(V* __restrict__ data, uint64_t half, int k) {
+    const uint64_t low = (1ull << k) - 1ull;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < half;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t lo = ((t >> k) << (k + 1)) | (t & low);
+        const uint64_t hi = lo + (1ull << k);
+        const V a = data[lo], b = data[hi];
+        data[lo] = a + b;
+        data[hi] = a - b;
+    }
+}
+
+__global__ void k_scale_f64(double* __restrict__ data, uint64_t count, double f) {
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += nth) data[i] *= f;
+}
+
+// ---------------------------------------------------------------------------
+// K3: max/min reduction (magnitude bound, core.py:80-94).
+// ---------------------------------------------------------------------------
+__global__ void k_minmax_init(long long* out) {
+    out[0] = (long long)0x8000000000000000ull;  // running max starts at INT64_MIN
+    out[1] = (long long)0x7FFFFFFFFFFFFFFFull;  // running min starts at INT64_MAX
+}
+
+__global__ void __launch_bounds__(512) k_minmax(const long long* __restrict__ data, uint64_t count,
+                                                long long* out) {
+    long long mx = (long long)0x8000000000000000ull, mn = (long long)0x7FFFFFFFFFFFFFFFull;
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(data) & 15u) == 0);
+    uint64_t done = 0;
+    if (aligned) {
+        const uint64_t pairs = count >> 1;
+        const longlong2* p = reinterpret_cast<const longlong2*>(data);
+        uint64_t i = tid;
+        for (; i + 3 * nth < pairs; i += 4 * nth) {
+            longlong2 a = __ldcs(p + i), b = __ldcs(p + i + nth);
+            longlong2 c = __ldcs(p + i + 2 * nth), d = __ldcs(p + i + 3 * nth);
+            mx = max(mx, max(max(a.x, a.y), max(b.x, b.y)));
+            mx = max(mx, max(max(c.x, c.y), max(d.x, d.y)));
+            mn = min(mn, min(min(a.x, a.y), min(b.x, b.y)));
+            mn = min(mn, min(min(c.x, c.y), min(d.x, d.y)));
+        }
+        for (; i < pairs; i += nth) {
+            longlong2 a = __ldcs(p + i);
+            mx = max(mx, max(a.x, a.y));
+            mn = min(mn, min(a.x, a.y));
+        }
+        done = pairs << 1;
+    }
+    for (uint64_t i = done + tid; i < count; i += nth) {
+        const long long a = data[i];
+        mx = max(mx, a);
+        mn = min(mn, a);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    __shared__ long long smx[32], smn[32];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        smx[w] = mx;
+        smn[w] = mn;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        mx = l < nw ? smx[l] : (long long)0x8000000000000000ull;
+        mn = l < nw ? smn[l] : (long long)0x7FFFFFFFFFFFFFFFull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        }
+        if (l == 0) {
+            atomicMax(&out[0], mx);
+            atomicMin(&out[1], mn);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K6: cross-shard P-point butterfly (parallel.py:103-110 stage phases, all
+// log2 P of them fused; one pass over the P shards' slice).
+// ---------------------------------------------------------------------------
+struct ShardPtrs {
+    u64* p[8];
+};
+
+template <int LOGP>
+__global__ void __launch_bounds__(256) k_xshard(ShardPtrs s, uint64_t begin, uint64_t pairs) {
+    constexpr int P = 1 << LOGP;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < pairs; q += nth) {
+        const uint64_t i = begin + 2 * q;
+        ulonglong2 v[P];
+#pragma unroll
+        for (int r = 0; r < P; ++r) v[r] = __ldcs(reinterpret_cast<const ulonglong2*>(s.p[r] + i));
+#pragma unroll
+        for (int b = 0; b < LOGP; ++b) {
+#pragma unroll
+            for (int r = 0; r < P; ++r) {
+                if (!((r >> b) & 1)) {
+                    const ulonglong2 a = v[r], c = v[r | (1 << b)];
+                    v[r].x = a.x + c.x;
+                    v[r].y = a.y + c.y;
+                    v[r | (1 << b)].x = a.x - c.x;
+                    v[r | (1 << b)].y = a.y - c.y;
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < P; ++r) __stcs(reinterpret_cast<ulonglong2*>(s.p[r] + i), v[r]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4: seeded counter-based generators (oracle/oracle_np.py restates them).
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+__host__ __device__ __forceinline__ uint64_t hash64(uint64_t seed, uint64_t i) {
+    return fmix64((i * 0x9E3779B97F4A7C15ull) ^ seed);
+}
+
+struct GenParams {
+    int kind;
+    int nmasks;
+    uint64_t seed;
+    uint64_t a;    // UNIFORM: A
+    uint64_t thr;  // NOISY: noise threshold
+    uint64_t mask[8];
+    uint64_t mseed[8];
+};
+
+__device__ __forceinline__ long long gen_value(const GenParams& g, uint64_t i) {
+    if (g.kind == 1) return 1 - 2 * (long long)(hash64(g.seed, i) & 1ull);
+    if (g.kind == 2) return (long long)(hash64(g.seed, i) % (2 * g.a + 1)) - (long long)g.a;
+    long long x = 0;
+    for (int m = 0; m < g.nmasks; ++m) {
+        const uint64_t bit = (uint64_t)(__popcll(g.mask[m] & i) & 1) ^ (uint64_t)(hash64(g.mseed[m], i) < g.thr);
+        x += 1 - 2 * (long long)bit;
+    }
+    return x;
+}
+
+__global__ void __launch_bounds__(256) k_gen(long long* __restrict__ out, uint64_t base, uint64_t count,
+                                             GenParams g) {
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += nth)
+        out[i] = gen_value(g, base + i);
+}
+
+// ---------------------------------------------------------------------------
+// K5: ordered threshold extraction (noisy.py:185-222): |x| >= tau.
+// Phase A counts hits per chunk, phase B scans the counts, phase C rewrites
+// only the chunks that hold hits, in index order -- no sort needed.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool hit_ge(long long x, uint64_t tau) {
+    const uint64_t mag = x < 0 ? (uint64_t)0 - (uint64_t)x : (uint64_t)x;
+    return mag >= tau;
+}
+
+constexpr int kExtractChunkBits = 16;
+
+__global__ void __launch_bounds__(512) k_extract_count(const long long* __restrict__ data, uint64_t count,
+                                                       uint64_t tau, unsigned long long* counts) {
+    const uint64_t chunk = 1ull << kExtractChunkBits;
+    const uint64_t start = blockIdx.x * chunk;
+    const uint64_t end = min(count, start + chunk);
+    unsigned c = 0;
+    for (uint64_t i = start + threadIdx.x; i < end; i += blockDim.x) c += hit_ge(__ldcs(data + i), tau);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    __shared__ unsigned ws[32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += ws[w];
+        counts[blockIdx.x] = s;
+    }
+}
+
+// Exclusive scan of counts[0..m) in place; total -> counts[m].  One CTA.
+__global__ void __launch_bounds__(1024) k_extract_scan(unsigned long long* counts, uint64_t m) {
+    __shared__ unsigned long long ws[32];
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (uint64_t base = 0; base < m; base += blockDim.x) {
+        const uint64_t i = base + threadIdx.x;
+        const unsigned long long x = i < m ? counts[i] : 0ull;
+        unsigned long long incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (l >= o) incl += y;
+        }
+        if (l == 31) ws[w] = incl;
+        __syncthreads();
+        if (w == 0) {
+            unsigned long long t = l < (int)(blockDim.x >> 5) ? ws[l] : 0ull;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
+                if (l >= o) t += y;
+            }
+            ws[l] = t;  // inclusive prefix over warps
+        }
+        __syncthreads();
+        const unsigned long long wpre = w > 0 ? ws[w - 1] : 0ull;
+        if (i < m) counts[i] = carry + wpre + incl - x;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += ws[(blockDim.x >> 5) - 1];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) counts[m] = carry;
+}
+
+__global__ void __launch_bounds__(512) k_extract_write(const long long* __restrict__ data, uint64_t count,
+                                                       uint64_t tau, const unsigned long long* offsets,
+                                                       const unsigned long long* counts_after,
+                                                       uint64_t base_index, long long* out_idx,
+                                                       long long* out_val, uint64_t cap) {
+    const uint64_t chunk = 1ull << kExtractChunkBits;
+    const uint64_t start = blockIdx.x * chunk;
+    const unsigned long long off0 = offsets[blockIdx.x];
+    if (counts_after[blockIdx.x] == off0) return;  // no hits in this chunk
+    const uint64_t end = min(count, start + chunk);
+    __shared__ unsigned ws[32];
+    __shared__ unsigned long long running;
+    if (threadIdx.x == 0) running = off0;
+    __syncthreads();
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (uint64_t s = start; s < end; s += blockDim.x) {
+        const uint64_t i = s + threadIdx.x;
+        long long x = 0;
+        bool h = false;
+        if (i < end) {
+            x = data[i];
+            h = hit_ge(x, tau);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, h);
+        if (l == 0) ws[w] = __popc(bal);
+        __syncthreads();
+        unsigned wpre = 0, tot = 0;
+        for (int q = 0; q < nw; ++q) {
+            const unsigned c = ws[q];
+            wpre += q < w ? c : 0u;
+            tot += c;
+        }
+        if (h) {
+            const unsigned long long pos = running + wpre + __popc(bal & ((1u << l) - 1u));
+            if (pos < cap) {
+                out_idx[pos] = (long long)(base_index + i);
+                out_val[pos] = x;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) running += tot;
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Elementwise helpers for the inverse transform (core.py:147-173).
+// ---------------------------------------------------------------------------
+__global__ void k_check_divisible(const long long* __restrict__ data, uint64_t count, int n, int* flag) {
+    const uint64_t m = (1ull << n) - 1ull;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += nth)
+        if (((uint64_t)data[i]) & m) *flag = 1;  // Python % on ints: divisible iff low n bits are 0
+}
+
+__global__ void k_shift_right(long long* __restrict__ data, uint64_t count, int n) {
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += nth)
+        data[i] = data[i] >> n;  // exact division (floor == exact when divisible)
+}
+
+}  // namespace bw

@@ -1,0 +1,147 @@
+"""CPU-side tests of the boundary: the C-ABI library loads and exports every
+declared symbol, the host plan checker (a static proof over the kernels' own
+address tables, like parallel.py:114-147), error mapping and host-side
+validation.  No kernel is launched here."""
+
+import ctypes
+import itertools
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1607_01039_b200 import _lib, errors, sharded
+from paper_1607_01039_b200.core import Signal
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "bigwht_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(bw_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    decl = declared_symbols()
+    assert len(decl) >= 20
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert sorted(_lib.exported_symbols()) == decl
+
+
+def test_abi_version():
+    assert _lib.lib().bw_abi_version() == 1
+
+
+@pytest.mark.parametrize("n", list(range(0, 25)))
+def test_default_plan_checker(n):
+    assert sharded.plan_check(n) == n << max(n - 1, 0)
+
+
+def splits(h):
+    """Every composition of h into parts of 1..10."""
+    if h == 0:
+        yield ()
+        return
+    for first in range(1, min(10, h) + 1):
+        for rest in splits(h - first):
+            yield (first,) + rest
+
+
+@pytest.mark.parametrize("n", [15, 16, 18, 20, 22])
+def test_every_pass_split_checks(n):
+    count = 0
+    for parts in splits(n - 14):
+        if n == 22 and len(parts) > 3:
+            continue
+        assert sharded.plan_check(n, [14, *parts]) == n << (n - 1)
+        count += 1
+    assert count > 0
+
+
+def test_bad_plans_rejected():
+    with pytest.raises(errors.BadArguments):
+        sharded.plan_check(20, [14, 11, -5])
+    with pytest.raises(errors.BadArguments):
+        sharded.plan_check(20, [13, 7])
+    with pytest.raises(errors.BadArguments):
+        sharded.plan_check(20, [14, 5])
+
+
+def test_plan_describe():
+    p = sharded.plan(32, 0)
+    assert [x["kind"] for x in p["passes"]] == ["low", "high", "high"]
+    assert sum(x["r"] for x in p["passes"]) == 32
+    assert p["hbm_bytes_per_pass"] == 16 << 32
+    q = sharded.plan(34, 3)
+    assert q["local_log2n"] == 31 and q["cross_stages"] == [31, 32, 33]
+    assert sharded.plan(19, 0)["passes"][1]["kind"] == "reg"
+    assert sharded.plan(10, 0)["passes"][0]["kind"] == "small"
+
+
+def test_status_mapping():
+    assert errors.OverflowBoundError.exit_code == 3
+    assert errors.DeviceError.exit_code == 2
+    with pytest.raises(errors.BadArguments):
+        _lib.check(1)
+    with pytest.raises(errors.OverflowBoundError):
+        _lib.check(2)
+    with pytest.raises(errors.InexactDivision):
+        _lib.check(3)
+    with pytest.raises(errors.InvalidWorkerCount):
+        _lib.check(4)
+    with pytest.raises(errors.DeviceError):
+        _lib.check(6)
+
+
+def test_signal_validation_host_side():
+    with pytest.raises(errors.BadArguments):
+        Signal(np.zeros(3, dtype=np.int64))
+    with pytest.raises(errors.BadArguments):
+        Signal(np.zeros(4, dtype=np.int32))
+    with pytest.raises(errors.BadArguments):
+        Signal(np.zeros((2, 2), dtype=np.int64))
+    assert Signal(np.zeros(8, dtype=np.int64)).log2_dim == 3
+    assert Signal(np.array([5], dtype=np.int64)).log2_dim == 0
+
+
+def test_shard_slices_partition():
+    for world in (1, 2, 4, 8):
+        for local in (2, 8, 1 << 10, 6):
+            cover = np.zeros(local, dtype=np.int64)
+            for r in range(world):
+                b, c = sharded.slice_of(r, world, local)
+                assert b % 2 == 0 and c % 2 == 0
+                cover[b:b + c] += 1
+            assert (cover == 1).all()
+
+
+def test_shard_count_validation():
+    for bad in (0, 3, 6, 16):
+        with pytest.raises(errors.InvalidWorkerCount):
+            sharded.log2_shards(bad)
+    assert [sharded.log2_shards(p) for p in (1, 2, 4, 8)] == [0, 1, 2, 3]
+
+
+def test_no_cpu_fallback_without_device(monkeypatch):
+    import torch
+
+    from paper_1607_01039_b200 import core
+
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    with pytest.raises(errors.DeviceError):
+        core.fwht_array(np.zeros(8, dtype=np.int64))
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_1607_01039_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f
+                assert "liboracle" not in text, f

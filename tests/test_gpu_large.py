@@ -1,0 +1,100 @@
+"""Full-size GPU parity at the BASELINE.json configs (n = 30, 32, 34).
+
+Above n = 26 a full CPU transform per test is too slow, so exactness is
+checked by size-independent properties:
+  * the fold identity WHT(fold(x, L)) = WHT(x)[row_space(L)]
+    (/root/reference/pkg/src/bigwht/subspace.py:1-11, pinned by
+    test_acceptance.py:237-249): a seeded 2^20-output spot check computed
+    directly on the CPU (oracle/bw_oracle.c fold of the regenerated input +
+    the oracle FWHT), with the planted masks inside row_space(L);
+  * the extraction hits (configs 3 and 5) equal the planted masks, and every
+    hit value equals the CPU value of that coefficient;
+  * involution at n = 30 (H H x = 2^n x exactly).
+"""
+
+import ctypes
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1607_01039_b200 as bw
+from paper_1607_01039_b200 import signals
+from oracle import oracle_np
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+D_OUT = 20
+
+
+def fold_map(n, masks, seed):
+    """d_out x n full-rank binary map whose row space contains the masks."""
+    rng = np.random.default_rng(seed)
+    while True:
+        rows = rng.integers(0, 2, size=(D_OUT, n), dtype=np.uint8)
+        for r, m in enumerate(masks):
+            rows[r] = [(m >> c) & 1 for c in range(n)]
+        if oracle_np.gf2_rank(rows) == D_OUT:
+            return rows
+
+
+def cpu_spot_check(coracle, spec, rows):
+    """WHT(fold(x, L)) computed on the CPU from the regenerated input."""
+    cols = oracle_np.column_masks(rows).astype(np.uint64)
+    out = np.empty(1 << D_OUT, dtype=np.int64)
+    arr = (ctypes.c_uint64 * max(1, len(spec.params)))(*[int(p) for p in spec.params])
+    threads = max(1, len(os.sched_getaffinity(0)))
+    assert coracle.oracle_fold_i64(None, spec.n, cols.ctypes.data, D_OUT, spec.kind, spec.seed, arr,
+                                   len(spec.params), threads, out.ctypes.data) == 0
+    coracle.oracle_fwht_i64(out.ctypes.data, D_OUT)
+    return out
+
+
+def run_config(coracle, idx, n=None):
+    spec = signals.config(idx, n)
+    free, _ = torch.cuda.mem_get_info()
+    if free < (8 << spec.n) + (1 << 30):
+        pytest.skip(f"needs {(8 << spec.n) >> 30} GiB of free device memory")
+    t = signals.make(spec)
+    assert bw.fwht_array(t) == spec.n << (spec.n - 1)
+    rows = fold_map(spec.n, spec.masks, seed=spec.seed)
+    rs = torch.from_numpy(oracle_np.row_space(rows)).cuda()
+    got = t[rs].cpu().numpy()
+    hits = None
+    if spec.threshold is not None:
+        hits = bw.extract_gt(t, spec.threshold)
+    del t
+    torch.cuda.empty_cache()
+    want = cpu_spot_check(coracle, spec, rows)
+    assert np.array_equal(got, want)
+    return spec, hits, rows, want
+
+
+def test_config3_n30_secret_recovered(coracle):
+    spec, (i, v), rows, want = run_config(coracle, 3)
+    assert i.tolist() == spec.masks  # exactly the planted secret
+    # the hit value equals the CPU coefficient (mask = row 0 -> folded index 1)
+    assert v.tolist() == [int(want[1])]
+    assert v.item() > (1 << 26)
+
+
+def test_config4_n32_spot_check(coracle):
+    run_config(coracle, 4)
+
+
+def test_config5_n34_masks_recovered(coracle):
+    spec, (i, v), rows, want = run_config(coracle, 5)
+    assert i.tolist() == sorted(spec.masks)
+    by_mask = {m: int(want[1 << r]) for r, m in enumerate(spec.masks)}
+    assert v.tolist() == [by_mask[m] for m in i.tolist()]
+
+
+def test_involution_n30():
+    spec = signals.config(4, n=30)
+    t = signals.make(spec)
+    x = t.clone()
+    bw.fwht_array(t)
+    bw.fwht_array(t)
+    x.mul_(1 << 30)
+    assert torch.equal(t, x)

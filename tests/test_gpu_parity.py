@@ -1,0 +1,314 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden outputs and the CPU oracle.  int64 results must be bit-exact."""
+
+import ctypes
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1607_01039_b200 as bw
+from paper_1607_01039_b200 import _lib, errors, sharded, signals
+from oracle import oracle_np
+
+pytestmark = pytest.mark.gpu
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<i8").tobytes()).hexdigest()
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def gpu_fwht(x):
+    t = dev(x)
+    bf = bw.fwht_array(t)
+    return t.cpu().numpy(), bf
+
+
+def c_fwht(coracle, x):
+    y = np.ascontiguousarray(x, dtype=np.int64).copy()
+    coracle.oracle_fwht_i64(y.ctypes.data, int(y.size).bit_length() - 1)
+    return y
+
+
+def planned(x, bits):
+    t = dev(x)
+    n = int(t.numel()).bit_length() - 1
+    if bits is None:
+        _lib.check(_lib.lib().bw_fwht_i64_planned(t.data_ptr(), n, None, 0,
+                                                  torch.cuda.current_stream().cuda_stream))
+    else:
+        arr = (ctypes.c_int * len(bits))(*bits)
+        _lib.check(_lib.lib().bw_fwht_i64_planned(t.data_ptr(), n, arr, len(bits),
+                                                  torch.cuda.current_stream().cuda_stream))
+    return t.cpu().numpy()
+
+
+# ------------------------------------------------------ reference pins ---
+
+def test_device_is_b200():
+    assert _lib.lib().bw_device_cc(0) == 100
+
+
+def test_known_answers(golden):
+    for case in golden["known"]:
+        y, _ = gpu_fwht(np.array(case["x"], dtype=np.int64))
+        assert y.tolist() == case["y"]
+        sig = bw.fwht_inplace(bw.Signal(dev(np.array(case["x"], dtype=np.int64))))
+        assert sig.data.cpu().tolist() == case["y"] and sig.domain == bw.Domain.WALSH
+
+
+def test_c01_vectors(golden_npz):
+    z = golden_npz("c01_vectors.npz")
+    for i in range(44):
+        y, bf = gpu_fwht(z[f"x{i}"])
+        assert np.array_equal(y, z[f"y{i}"])
+        n = z[f"x{i}"].size.bit_length() - 1
+        assert bf == n << max(n - 1, 0)
+
+
+def test_fixture_arrays(golden_npz):
+    z = golden_npz("fwht_n12_16.npz")
+    for n in (12, 14, 16):
+        y, _ = gpu_fwht(z[f"x{n}"])
+        assert np.array_equal(y, z[f"y{n}"])
+
+
+def test_generated_cases_match_reference_digests(golden):
+    for case in golden["gen_cases"]:
+        n = case["n"]
+        spec = signals.SignalSpec(n, case["kind"], case["seed"], tuple(case["params"]))
+        t = signals.make(spec)
+        assert digest(t.cpu().numpy()) == case["x_sha256"]
+        assert bw.fwht_array(t) == case["butterflies"]
+        assert digest(t.cpu().numpy()) == case["y_sha256"]
+
+
+def test_wraparound_matches_reference(golden_npz):
+    z = golden_npz("wrap_n10.npz")
+    y, _ = gpu_fwht(z["x"])
+    assert np.array_equal(y, z["y"])
+
+
+def test_wraparound_large_n(coracle):
+    """Unbounded int64 (the reference's fwht_array has no bound check and
+    wraps mod 2^64): every pass kind must wrap identically."""
+    rng = np.random.default_rng(3)
+    for n in (14, 20, 24):
+        x = rng.integers(np.iinfo(np.int64).min, np.iinfo(np.int64).max, 1 << n, dtype=np.int64)
+        y, _ = gpu_fwht(x)
+        assert np.array_equal(y, c_fwht(coracle, x))
+
+
+def test_float64_bitwise(golden_npz):
+    z = golden_npz("float64.npz")
+    for n in (4, 10, 15):
+        y, _ = gpu_fwht(z[f"x{n}"])
+        assert np.array_equal(y.view(np.int64), z[f"y{n}"].view(np.int64))
+
+
+def test_float64_bitwise_large(coracle):
+    rng = np.random.default_rng(8)
+    x = rng.normal(size=1 << 20)
+    y, _ = gpu_fwht(x)
+    ref = x.copy()
+    coracle.oracle_fwht_f64(ref.ctypes.data, 20)
+    assert np.array_equal(y.view(np.int64), ref.view(np.int64))
+
+
+def test_numpy_buffers_are_staged_through_the_device(golden_npz):
+    z = golden_npz("fwht_n12_16.npz")
+    x = z["x14"].copy()
+    assert bw.fwht_array(x) == 14 << 13
+    assert np.array_equal(x, z["y14"])
+    s = bw.fwht_inplace(bw.Signal(z["x12"].copy()))
+    assert np.array_equal(s.data, z["y12"])
+
+
+# -------------------------------------------------- oracle equivalence ---
+
+@pytest.mark.parametrize("n", list(range(0, 27)))
+def test_matches_oracle_every_n(coracle, n):
+    x = oracle_np.gen(2, 500 + n, [1 << 20], 0, 1 << n)
+    y, bf = gpu_fwht(x)
+    assert np.array_equal(y, c_fwht(coracle, x))
+    assert bf == n << max(n - 1, 0)
+
+
+def test_every_pass_split_is_identical(coracle):
+    """Block-size independence (test_external.py:120-129): every legal split
+    of the high bits gives byte-identical output."""
+    n = 22
+    x = oracle_np.gen(2, 77, [1 << 20], 0, 1 << n)
+    ref = c_fwht(coracle, x)
+    assert np.array_equal(planned(x, None), ref)  # naive per-stage path
+    for parts in ((8,), (1, 7), (7, 1), (2, 3, 3), (5, 3), (4, 4), (6, 2), (3, 5), (1, 1, 1, 1, 1, 1, 1, 1)):
+        assert np.array_equal(planned(x, [14, *parts]), ref), parts
+    n = 24
+    x = oracle_np.gen(1, 78, [], 0, 1 << n)
+    ref = c_fwht(coracle, x)
+    for parts in ((10,), (5, 5), (9, 1), (1, 9), (6, 4), (4, 6)):
+        assert np.array_equal(planned(x, [14, *parts]), ref), parts
+
+
+def test_involution_and_linearity():
+    for n in (1, 5, 13, 14, 17, 23, 26):
+        x = oracle_np.gen(2, 900 + n, [1000], 0, 1 << n)
+        t = dev(x)
+        bw.fwht_array(t)
+        bw.fwht_array(t)
+        assert np.array_equal(t.cpu().numpy(), x * (1 << n))
+    n = 21
+    a, b = 7, -3
+    x = oracle_np.gen(2, 1, [500], 0, 1 << n)
+    z = oracle_np.gen(2, 2, [500], 0, 1 << n)
+    combo, _ = gpu_fwht(a * x + b * z)
+    wx, _ = gpu_fwht(x)
+    wz, _ = gpu_fwht(z)
+    assert np.array_equal(combo, a * wx + b * wz)
+
+
+# ------------------------------------------------------ error behaviour ---
+
+def test_overflow_bound_raises_before_mutation(golden):
+    for case in golden["bound_edges"]:
+        n = case["n"]
+        x = np.zeros(1 << n, dtype=np.int64)
+        x[3] = case["value"]
+        t = dev(x)
+        if case["ok"]:
+            bw.check_magnitude_bound(t, n)
+            bw.fwht_inplace(bw.Signal(t))
+        else:
+            with pytest.raises(errors.OverflowBoundError):
+                bw.fwht_inplace(bw.Signal(t))
+            assert np.array_equal(t.cpu().numpy(), x)  # untouched
+            h = x.copy()
+            with pytest.raises(errors.OverflowBoundError):
+                bw.fwht_inplace(bw.Signal(h))
+            assert np.array_equal(h, x)
+    # negative extreme: |INT64_MIN| = 2^63 never passes
+    t = dev(np.array([np.iinfo(np.int64).min, 0], dtype=np.int64))
+    with pytest.raises(errors.OverflowBoundError):
+        bw.check_magnitude_bound(t, 1)
+
+
+def test_argument_errors_before_launch():
+    t = torch.arange(16, dtype=torch.int64, device="cuda")
+    with pytest.raises(errors.BadArguments):
+        bw.fwht_array(t[::2])
+    with pytest.raises(errors.BadArguments):
+        bw.fwht_array(t[:12])
+    with pytest.raises(errors.BadArguments):
+        bw.fwht_array(t.view(4, 4))
+    with pytest.raises(errors.BadArguments):
+        bw.fwht_array(t.to(torch.int32))
+    with pytest.raises(errors.BadArguments):
+        bw.fwht_array(torch.arange(16, dtype=torch.int64))  # CPU tensor: no CPU path
+    assert t.cpu().tolist() == list(range(16))
+
+
+def test_misaligned_view_still_exact(coracle):
+    """An odd-offset slice (8- but not 16-byte aligned) takes the per-stage
+    path on the GPU and stays bit-exact (parallel.py:151 slices)."""
+    base = torch.from_numpy(oracle_np.gen(2, 4, [1 << 20], 0, (1 << 15) + 1)).cuda()
+    view = base[1:]
+    ref = c_fwht(coracle, view.cpu().numpy())
+    bw.fwht_array(view)
+    assert np.array_equal(view.cpu().numpy(), ref)
+
+
+def test_inverse(golden):
+    for case in golden["inverse"]:
+        s = bw.inverse_wht_inplace(bw.Signal(dev(np.array(case["w"], dtype=np.int64)), bw.Domain.WALSH))
+        assert s.data.cpu().tolist() == case["x"] and s.domain == bw.Domain.TIME
+    with pytest.raises(errors.BadArguments):
+        bw.inverse_wht_inplace(bw.Signal(dev(np.array([1, 2, 3, 4], dtype=np.int64))))
+    t = dev(np.array([1, 0, 0, 0], dtype=np.int64))
+    with pytest.raises(errors.InexactDivision):
+        bw.inverse_wht_inplace(bw.Signal(t, bw.Domain.WALSH))
+    assert t.cpu().tolist() == [1, 0, 0, 0]
+    for n in (1, 4, 9, 16, 22):
+        x = oracle_np.gen(2, n, [9999], 0, 1 << n)
+        s = bw.Signal(dev(x))
+        bw.fwht_inplace(s)
+        bw.inverse_wht_inplace(s)
+        assert np.array_equal(s.data.cpu().numpy(), x)
+    xf = np.random.default_rng(11).normal(size=1 << 10)
+    s = bw.Signal(dev(xf))
+    bw.fwht_inplace(s)
+    bw.inverse_wht_inplace(s)
+    np.testing.assert_allclose(s.data.cpu().numpy(), xf, rtol=1e-12, atol=1e-12)
+
+
+# ----------------------------------------------------------- extraction ---
+
+def test_extract_matches_reference(golden):
+    for case in golden["extract"]:
+        sig = bw.Signal(dev(np.array(case["data"], dtype=np.int64)), bw.Domain.WALSH)
+        assert [list(h) for h in bw.extract_above(sig, case["tau"])] == case["hits"]
+
+
+def test_extract_config_constructions(golden):
+    for key, idx in (("config3_n22", 3), ("config5_n22", 5)):
+        spec = signals.config(idx, n=22)
+        t = signals.make(spec)
+        bw.fwht_array(t)
+        assert digest(t.cpu().numpy()) == golden[key]["y_sha256"]
+        i, v = bw.extract_gt(t, golden[key]["tau"])
+        assert [[a, b] for a, b in zip(i.tolist(), v.tolist())] == sorted(golden[key]["hits"])
+
+
+def test_extract_dense_and_edges(coracle):
+    rng = np.random.default_rng(21)
+    for n in (0, 3, 16, 17, 20):
+        x = rng.integers(-1000, 1000, 1 << n).astype(np.int64)
+        if n >= 3:
+            x[5] = np.iinfo(np.int64).min
+        for tau in (0, 1, 500, 999, 1001):
+            i, v = bw.extract_ge(dev(x), tau, cap=16)  # forces the capacity retry
+            ri, rv = oracle_np.extract_gt_by_index(x, tau - 1) if tau > 0 else (np.arange(x.size), x)
+            assert np.array_equal(i.cpu().numpy(), ri) and np.array_equal(v.cpu().numpy(), rv), (n, tau)
+
+
+# ----------------------------------------------------------- generators ---
+
+def test_generators_match_oracle(coracle):
+    for idx in (1, 2, 3, 5):
+        spec = signals.config(idx, n=18)
+        t = signals.make(spec)
+        ref = oracle_np.gen(spec.kind, spec.seed, list(spec.params), 0, 1 << 18)
+        assert np.array_equal(t.cpu().numpy(), ref)
+        part = torch.empty(1000, dtype=torch.int64, device="cuda")
+        signals.generate(spec, part, base=12345)
+        assert np.array_equal(part.cpu().numpy(), oracle_np.gen(spec.kind, spec.seed, list(spec.params), 12345, 1000))
+
+
+# ------------------------------------------------- multi-shard emulation ---
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_sharded_emulation(coracle, P):
+    """P shards as P buffers on one device, same kernels as the multi-GPU
+    path (parallel.py: parallel == serial, test_acceptance.py:77-105)."""
+    for n in (4, 12, 20):
+        if n - (P.bit_length() - 1) < 1:
+            continue
+        x = oracle_np.gen(2, 60 + n, [1 << 20], 0, 1 << n)
+        ref = c_fwht(coracle, x)
+        shards = [dev(c) for c in np.split(x, P)]
+        assert sharded.fwht_shards(shards) == n << (n - 1)
+        assert np.array_equal(np.concatenate([s.cpu().numpy() for s in shards]), ref)
+
+
+def test_xshard_strided_matches_per_pointer():
+    x = oracle_np.gen(2, 9, [1 << 20], 0, 1 << 16)
+    a = dev(x)
+    b = dev(x)
+    _lib.check(_lib.lib().bw_xshard_strided_i64(a.data_ptr(), 1 << 13, 3, 0, 1 << 13,
+                                                torch.cuda.current_stream().cuda_stream))
+    sharded.xshard(list(b.view(8, 1 << 13).unbind(0)))
+    assert torch.equal(a, b)
