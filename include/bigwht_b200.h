@@ -257,6 +257,14 @@ int bw_plan_describe(int log2n, int log2p, char *json, size_t len);
 int bw_plan_check(int log2n, const int *pass_bits, int npasses,
                   uint64_t *butterflies);
 
+/*
+ * TEST HOOK ONLY -- never used by any product entry point.  Executes the
+ * default (or given) pass plan's exact address, stage-mask and shared-memory
+ * tables on HOST memory, so the kernels' layout logic is testable without a
+ * GPU.  log2n <= 24.
+ */
+int bw_debug_emulate_i64(int64_t *host, int log2n, const int *pass_bits, int npasses);
+
 #ifdef __cplusplus
 }
 #endif

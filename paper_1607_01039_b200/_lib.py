@@ -64,6 +64,7 @@ _SIGNATURES = {
     "bw_extract_ge_i64": ([P, I32, U64, U64, P, P, U64, P, P, PU64], I32),
     "bw_extract_scratch_bytes": ([I32], U64),
     "bw_plan_describe": ([I32, I32, ctypes.c_char_p, ctypes.c_size_t], I32),
+    "bw_debug_emulate_i64": ([P, I32, ctypes.POINTER(I32), I32], I32),
     "bw_plan_check": ([I32, ctypes.POINTER(I32), I32, PU64], I32),
 }
 

@@ -773,11 +773,11 @@ int check_pass(int n, int k, std::vector<uint8_t>& touched, uint32_t* stage_bits
         if (tile_stages & rounds_masks[r]) return fail(BW_BAD_ARGUMENTS, "tile bit staged twice");
         tile_stages |= rounds_masks[r];
     }
-    const uint32_t rows = ((1u << T) - 1u) & ~((1u << L) - 1u);
+    const uint32_t rows = L >= T ? (1u << T) - 1u : ((1u << T) - 1u) & ~((1u << L) - 1u);
     if (tile_stages != rows) return fail(BW_BAD_ARGUMENTS, "tile stages %x != rows %x", tile_stages, rows);
-    uint32_t stage_bits = 0;
-    for (int b = L; b < T; ++b) stage_bits |= 1u << (L >= T ? b : k + (b - L));
-    if (L >= T) stage_bits = (1u << T) - 1u;
+    uint32_t stage_bits = 0;  // the global bits the kernel's stage masks really cover
+    for (int b = 0; b < T; ++b)
+        if ((tile_stages >> b) & 1u) stage_bits |= 1u << (b < L ? b : k + (b - L));
     *stage_bits_out = stage_bits;
     // Address walk: load layout and store layout must both be bijections.
     const uint64_t tiles = 1ull << (n - T);
@@ -805,6 +805,65 @@ int check_pass(int n, int k, std::vector<uint8_t>& touched, uint32_t* stage_bits
         if (x != 3) return fail(BW_BAD_ARGUMENTS, "pass at k=%d misses an element", k);
     *bfly += (uint64_t)__builtin_popcount(stage_bits) << (n - 1);
     return BW_OK;
+}
+
+// Host emulation of k_pass<C, L>: the same address tables, rounds, stage
+// masks and shared-memory slots, executed thread by thread on host memory.
+template <class C, int L>
+void emulate_pass(u64* data, int n, int k) {
+    constexpr int T = C::T, E = bw::Dims<C>::E, NT = bw::Dims<C>::NT;
+    std::vector<u64> v((size_t)NT * E), sm((size_t)bw::Dims<C>::TILE * 2);
+    const uint64_t tiles = 1ull << (n - T);
+    auto stages = [&](uint32_t mask, int rd) {
+        for (int t = 0; t < NT; ++t)
+            for (int i = 0; i < C::R; ++i)
+                if ((mask >> C::reg(rd, i)) & 1u)
+                    for (int j = 0; j < E; ++j)
+                        if (!((j >> i) & 1)) {
+                            u64& a = v[(size_t)t * E + j];
+                            u64& b = v[(size_t)t * E + (j | (1 << i))];
+                            const u64 x = a, y = b;
+                            a = x + y;
+                            b = x - y;
+                        }
+    };
+    for (uint64_t b = 0; b < tiles; ++b) {
+        const uint64_t base = bw::tile_base<T, L>(b, k);
+        for (int t = 0; t < NT; ++t)
+            for (int j = 0; j < E; ++j)
+                v[(size_t)t * E + j] = data[base + bw::global_off<T, L>(bw::thread_part<C, 0>(t & 31, t >> 5), k) +
+                                            bw::global_off<T, L>(bw::reg_part<C, 0>(j), k)];
+        stages(bw::stage_mask<C, 0, L>(), 0);
+        if constexpr (C::NR >= 2) {
+            constexpr int R1 = C::NR >= 2 ? 1 : 0;
+            for (int t = 0; t < NT; ++t)
+                for (int j = 0; j < E; ++j)
+                    sm[bw::smem_slot(bw::thread_part<C, 0>(t & 31, t >> 5)) + bw::smem_slot(bw::reg_part<C, 0>(j))] =
+                        v[(size_t)t * E + j];
+            for (int t = 0; t < NT; ++t)
+                for (int j = 0; j < E; ++j)
+                    v[(size_t)t * E + j] =
+                        sm[bw::smem_slot(bw::thread_part<C, R1>(t & 31, t >> 5)) + bw::smem_slot(bw::reg_part<C, R1>(j))];
+            stages(bw::stage_mask<C, R1, L>(), R1);
+        }
+        if constexpr (C::NR >= 3) {
+            constexpr int R1 = C::NR >= 3 ? 1 : 0, R2 = C::NR >= 3 ? 2 : 0;
+            for (int t = 0; t < NT; ++t)
+                for (int j = 0; j < E; ++j)
+                    sm[bw::smem_slot(bw::thread_part<C, R1>(t & 31, t >> 5)) + bw::smem_slot(bw::reg_part<C, R1>(j))] =
+                        v[(size_t)t * E + j];
+            for (int t = 0; t < NT; ++t)
+                for (int j = 0; j < E; ++j)
+                    v[(size_t)t * E + j] =
+                        sm[bw::smem_slot(bw::thread_part<C, R2>(t & 31, t >> 5)) + bw::smem_slot(bw::reg_part<C, R2>(j))];
+            stages(bw::stage_mask<C, R2, L>(), R2);
+        }
+        constexpr int LAST = C::NR - 1;
+        for (int t = 0; t < NT; ++t)
+            for (int j = 0; j < E; ++j)
+                data[base + bw::global_off<T, L>(bw::thread_part<C, LAST>(t & 31, t >> 5), k) +
+                     bw::global_off<T, L>(bw::reg_part<C, LAST>(j), k)] = v[(size_t)t * E + j];
+    }
 }
 
 }  // namespace
@@ -856,5 +915,53 @@ extern "C" int bw_plan_check(int log2n, const int* pass_bits, int npasses, uint6
     const uint32_t all = log2n ? (uint32_t)((1ull << log2n) - 1ull) : 0u;
     if (covered != all) return fail(BW_BAD_ARGUMENTS, "stages covered %x, expected %x", covered, all);
     if (butterflies) *butterflies = bfly;
+    return BW_OK;
+}
+
+// TEST HOOK ONLY (never called by the product path): run the pass plan's
+// exact address/stage/shared-memory tables on HOST memory, to check the
+// kernels' layout logic without a GPU.  n <= 24.
+extern "C" int bw_debug_emulate_i64(int64_t* host, int log2n, const int* pass_bits, int npasses) {
+    if (!host || log2n < 0 || log2n > 24) return fail(BW_BAD_ARGUMENTS, "emulation supports 0 <= n <= 24");
+    std::vector<int> w;
+    if (pass_bits && npasses > 0) w.assign(pass_bits, pass_bits + npasses);
+    else default_plan(log2n, &w);
+    std::vector<Pass> passes;
+    BW_TRY(build_passes(log2n, w, &passes));
+    u64* d = reinterpret_cast<u64*>(host);
+    for (const Pass& p : passes) {
+        switch (p.kind) {
+            case Pass::SMALL: {
+                const uint64_t N = 1ull << log2n;
+                for (int k = 0; k < log2n; ++k)
+                    for (uint64_t t = 0; t < N / 2; ++t) {
+                        const uint64_t lo = ((t >> k) << (k + 1)) | (t & ((1ull << k) - 1)), hi = lo + (1ull << k);
+                        const u64 a = d[lo], b = d[hi];
+                        d[lo] = a + b;
+                        d[hi] = a - b;
+                    }
+                break;
+            }
+            case Pass::LOW: emulate_pass<bw::CfgLow, 14>(d, log2n, 14); break;
+            case Pass::HIGH:
+                switch (bw::kLowBits - p.r) {
+                    case 4: emulate_pass<bw::CfgHigh, 4>(d, log2n, p.k); break;
+                    case 5: emulate_pass<bw::CfgHigh, 5>(d, log2n, p.k); break;
+                    case 6: emulate_pass<bw::CfgHigh, 6>(d, log2n, p.k); break;
+                    case 7: emulate_pass<bw::CfgHigh, 7>(d, log2n, p.k); break;
+                    case 8: emulate_pass<bw::CfgHigh, 8>(d, log2n, p.k); break;
+                }
+                break;
+            case Pass::REG:
+                switch (bw::CfgReg::T - p.r) {
+                    case 8: emulate_pass<bw::CfgReg, 8>(d, log2n, p.k); break;
+                    case 9: emulate_pass<bw::CfgReg, 9>(d, log2n, p.k); break;
+                    case 10: emulate_pass<bw::CfgReg, 10>(d, log2n, p.k); break;
+                    case 11: emulate_pass<bw::CfgReg, 11>(d, log2n, p.k); break;
+                    case 12: emulate_pass<bw::CfgReg, 12>(d, log2n, p.k); break;
+                }
+                break;
+        }
+    }
     return BW_OK;
 }

@@ -114,7 +114,7 @@ BW_HD inline uint32_t thread_part(uint32_t lane, uint32_t warp) {
 // Stage mask of round RD for a tile whose low L bits are columns.
 template <class C, int RD, int L>
 BW_HD constexpr uint32_t stage_mask() {
-    return C::stage(RD) & ~((1u << L) - 1u);
+    return L >= C::T ? C::stage(RD) : (C::stage(RD) & ~((1u << L) - 1u));
 }
 
 // Global element offset (relative to the tile base) of tile index e.

@@ -145,3 +145,37 @@ def test_product_package_does_not_import_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "liboracle" not in text, f
+
+
+def emulate(x, bits=None):
+    y = np.ascontiguousarray(x, dtype=np.int64).copy()
+    n = int(y.size).bit_length() - 1
+    if bits:
+        arr = (ctypes.c_int * len(bits))(*bits)
+        _lib.check(_lib.lib().bw_debug_emulate_i64(y.ctypes.data, n, arr, len(bits)))
+    else:
+        _lib.check(_lib.lib().bw_debug_emulate_i64(y.ctypes.data, n, None, 0))
+    return y
+
+
+@pytest.mark.parametrize("n", [0, 1, 5, 13, 14, 15, 17, 19, 20, 23])
+def test_kernel_tables_emulated_on_host_match_oracle(coracle, n):
+    """The pass kernels' address/stage/smem tables, executed on the host
+    (bw_debug_emulate_i64), equal the oracle bit for bit."""
+    from oracle import oracle_np
+
+    x = oracle_np.gen(2, 300 + n, [1 << 20], 0, 1 << n)
+    ref = x.copy()
+    coracle.oracle_fwht_i64(ref.ctypes.data, n)
+    assert np.array_equal(emulate(x), ref)
+
+
+def test_kernel_tables_every_split_emulated(coracle):
+    from oracle import oracle_np
+
+    n = 21
+    x = oracle_np.gen(1, 5, [], 0, 1 << n)
+    ref = x.copy()
+    coracle.oracle_fwht_i64(ref.ctypes.data, n)
+    for parts in splits(n - 14):
+        assert np.array_equal(emulate(x, [14, *parts]), ref), parts
