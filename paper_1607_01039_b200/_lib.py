@@ -13,7 +13,8 @@ import os
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libbigwht_b200.so")
+# BW_LIB_PATH selects an alternative build of the same library (experiments).
+LIB_PATH = os.environ.get("BW_LIB_PATH") or os.path.join(_HERE, "lib", "libbigwht_b200.so")
 
 BW_OK = 0
 _STATUS = {

@@ -8,7 +8,10 @@
 #include <math.h>
 #include <string.h>
 
+#include <stdlib.h>
+
 #include <mutex>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -64,6 +67,8 @@ int g_num_sms[kMaxDevices];
 void* g_scratch[kMaxDevices];
 size_t g_scratch_bytes[kMaxDevices];
 
+int set_all_pass_attributes();
+
 // Per-device one-time setup: opt-in dynamic shared memory sizes.
 int device_setup(int* dev_out) {
     int dev = 0;
@@ -79,14 +84,7 @@ int device_setup(int* dev_out) {
         return fail(BW_NOT_SUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a (B200) only",
                     dev, major, minor);
     BW_CUDA(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev));
-    const int low_smem = bw::Dims<bw::CfgLow>::SMEM_ELEMS * 8;
-    const int high_smem = bw::Dims<bw::CfgHigh>::SMEM_ELEMS * 8;
-    BW_CUDA(cudaFuncSetAttribute(bw::k_pass<bw::CfgLow, 14>, cudaFuncAttributeMaxDynamicSharedMemorySize, low_smem));
-    BW_CUDA(cudaFuncSetAttribute(bw::k_pass<bw::CfgHigh, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, high_smem));
-    BW_CUDA(cudaFuncSetAttribute(bw::k_pass<bw::CfgHigh, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, high_smem));
-    BW_CUDA(cudaFuncSetAttribute(bw::k_pass<bw::CfgHigh, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, high_smem));
-    BW_CUDA(cudaFuncSetAttribute(bw::k_pass<bw::CfgHigh, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, high_smem));
-    BW_CUDA(cudaFuncSetAttribute(bw::k_pass<bw::CfgHigh, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, high_smem));
+    BW_TRY(set_all_pass_attributes());
     BW_CUDA(cudaFuncSetAttribute(bw::k_small<u64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (1 << 13) * 8));
     BW_CUDA(cudaFuncSetAttribute(bw::k_small<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (1 << 13) * 8));
     g_attr_done[dev] = true;
@@ -117,25 +115,107 @@ int grid_for(int dev, uint64_t work_items, int threads, int per_sm) {
 }
 
 // ---- pass plan -------------------------------------------------------------
+//
+// A plan is a list of pass widths: the low-bits pass (stages 0..w0-1 on
+// contiguous tiles; w0 = 13, 14 or 15 uses a cluster of 1, 2 or 4 CTAs, and
+// w0 = n <= 12 the single-CTA small kernel) followed by high-bits passes in
+// ascending bit order.  A high width r picks its kernel: r <= 5 the
+// register-only pass, r = 6..8 a single-CTA tile, r = 9 a cluster of 2 and
+// r = 10 a cluster of 4 (so every row segment stays >= 256 B).  Tests may
+// force the cluster size of a high pass with the entry r | (q + 1) << 4.
+
+enum PassKind { SMALL, LOW, HIGH, REG };
 
 struct Pass {
-    enum Kind { SMALL, LOW, HIGH, REG } kind;
+    PassKind kind;
     int k;  // first stage bit
     int r;  // number of stages
+    int q;  // log2 cluster size of LOW / HIGH passes
 };
 
+template <class T>
+struct tag {
+    using type = T;
+};
+template <int V>
+using ic = std::integral_constant<int, V>;
+
+// Calls f(tag<Cfg>, ic<L>) for the kernel instantiation L in [L, LMAX].
+template <class C, int L, int LMAX, class F>
+int with_L(int l, F& f) {
+    if (l == L) return f(tag<C>{}, ic<L>{});
+    if constexpr (L < LMAX) {
+        return with_L<C, L + 1, LMAX>(l, f);
+    } else {
+        return fail(BW_BAD_ARGUMENTS, "no pass kernel instantiated for %d column bits", l);
+    }
+}
+
+template <class F>
+int visit_pass(const Pass& p, F&& f) {
+    switch (p.kind) {
+        case LOW:
+            if (p.q == 0) return f(tag<bw::CfgLow13>{}, ic<13>{});
+            if (p.q == 1) return f(tag<bw::CfgLow14c>{}, ic<14>{});
+            return f(tag<bw::CfgLow15c>{}, ic<15>{});
+        case HIGH:
+            if (p.q == 0) return with_L<bw::CfgHigh13, 3, 7>(13 - p.r, f);
+            if (p.q == 1) return with_L<bw::CfgHigh14c, 4, 8>(14 - p.r, f);
+            return with_L<bw::CfgHigh15c, 5, 10>(15 - p.r, f);
+        case REG:
+            return with_L<bw::CfgReg, 8, 12>(bw::CfgReg::T - p.r, f);
+        default:
+            return fail(BW_BAD_ARGUMENTS, "small transforms have no tile kernel");
+    }
+}
+
+int high_default_q(int r) { return r <= 8 ? 0 : r == 9 ? 1 : 2; }
+
+// BW_PLAN="13,10,9" overrides the default plan for a matching n
+// (experiment knob; the checker and tests cover every legal plan).
+bool env_plan(int n, std::vector<int>* widths) {
+    const char* e = getenv("BW_PLAN");
+    if (!e || !*e) return false;
+    std::vector<int> w;
+    int sum = 0;
+    for (const char* c = e; *c;) {
+        char* end = nullptr;
+        const long v = strtol(c, &end, 10);
+        if (end == c) return false;
+        w.push_back((int)v);
+        sum += (int)v & 15;
+        c = (*end == ',') ? end + 1 : end;
+    }
+    if (w.empty() || sum - (w[0] & 15) + w[0] != n) return false;
+    *widths = w;
+    return true;
+}
+
+// Default plan: fewest HBM round trips, then the cheapest cluster shapes.
 int default_plan(int n, std::vector<int>* widths) {
     widths->clear();
+    if (env_plan(n, widths)) return BW_OK;
     if (n == 0) return BW_OK;
-    if (n < bw::kLowBits) {
+    if (n <= 15) {
         widths->push_back(n);
         return BW_OK;
     }
-    widths->push_back(bw::kLowBits);
-    const int h = n - bw::kLowBits;
-    if (h == 0) return BW_OK;
-    const int q = (h + bw::kMaxHighBits - 1) / bw::kMaxHighBits;
-    for (int i = 0; i < q; ++i) widths->push_back(h / q + (i < h % q ? 1 : 0));
+    int best_cost = 1 << 30;
+    for (int w0 = 13; w0 <= 15; ++w0) {
+        const int h = n - w0;
+        const int q = (h + bw::kMaxHighBits - 1) / bw::kMaxHighBits;
+        std::vector<int> w{w0};
+        int cost = (1 + q) * 100 + (w0 - 13);
+        for (int i = 0; i < q; ++i) {
+            const int r = h / q + (i < h % q ? 1 : 0);
+            w.push_back(r);
+            cost += r <= bw::kRegOnlyMaxBits ? 0 : high_default_q(r);
+        }
+        if (cost < best_cost) {
+            best_cost = cost;
+            *widths = w;
+        }
+    }
     return BW_OK;
 }
 
@@ -146,60 +226,92 @@ int build_passes(int n, const std::vector<int>& widths, std::vector<Pass>* passe
         return BW_OK;
     }
     if (widths.empty()) return fail(BW_BAD_ARGUMENTS, "empty pass plan for n = %d", n);
-    const int low = n < bw::kLowBits ? n : bw::kLowBits;
-    if (widths[0] != low)
-        return fail(BW_BAD_ARGUMENTS, "first pass must cover %d low bits (got %d)", low, widths[0]);
-    passes->push_back({n < bw::kLowBits ? Pass::SMALL : Pass::LOW, 0, low});
-    int k = low;
+    const int w0 = widths[0];
+    if (n <= 12) {
+        if (w0 != n || widths.size() != 1)
+            return fail(BW_BAD_ARGUMENTS, "a transform of n = %d <= 12 is one small pass", n);
+        passes->push_back({SMALL, 0, n, 0});
+        return BW_OK;
+    }
+    if (w0 < 13 || w0 > 15 || w0 > n)
+        return fail(BW_BAD_ARGUMENTS, "the low pass covers 13, 14 or 15 bits (got %d, n = %d)", w0, n);
+    passes->push_back({LOW, 0, w0, w0 - 13});
+    int k = w0;
     for (size_t i = 1; i < widths.size(); ++i) {
-        const int r = widths[i];
-        if (r < 1 || r > bw::kMaxHighBits)
-            return fail(BW_BAD_ARGUMENTS, "high pass width %d outside 1..%d", r, bw::kMaxHighBits);
-        passes->push_back({r <= bw::kRegOnlyMaxBits ? Pass::REG : Pass::HIGH, k, r});
+        const int r = widths[i] & 15;
+        const int forced = (widths[i] >> 4) - 1;
+        if (r < 1 || r > bw::kMaxHighBits || widths[i] < 0 || forced > bw::kMaxClusterLog2)
+            return fail(BW_BAD_ARGUMENTS, "bad high pass entry %d (width 1..%d, cluster q 0..%d)", widths[i],
+                        bw::kMaxHighBits, bw::kMaxClusterLog2);
+        if (r <= bw::kRegOnlyMaxBits && forced <= 0) {
+            passes->push_back({REG, k, r, 0});
+        } else {
+            const int q = forced >= 0 ? forced : high_default_q(r);
+            const int L = 13 + q - r;
+            const int lmin = q == 0 ? 3 : q == 1 ? 4 : 5;
+            if (L < lmin || L > (q == 0 ? 7 : q == 1 ? 8 : 10))
+                return fail(BW_BAD_ARGUMENTS, "no high-pass kernel for %d stages on a cluster of %d", r, 1 << q);
+            passes->push_back({HIGH, k, r, q});
+        }
         k += r;
     }
     if (k != n) return fail(BW_BAD_ARGUMENTS, "pass widths cover %d bits, signal has %d", k, n);
     return BW_OK;
 }
 
-int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s) {
-    const unsigned grid = p.kind == Pass::SMALL ? 1u : (unsigned)(1ull << (n - bw::kLowBits));
-    switch (p.kind) {
-        case Pass::SMALL:
-            bw::k_small<u64><<<1, 256, (size_t)(8ull << n), s>>>(d, n);
-            break;
-        case Pass::LOW:
-            bw::k_pass<bw::CfgLow, 14><<<grid, bw::Dims<bw::CfgLow>::NT, bw::Dims<bw::CfgLow>::SMEM_ELEMS * 8, s>>>(d, 14);
-            break;
-        case Pass::HIGH: {
-            constexpr int NT = bw::Dims<bw::CfgHigh>::NT;
-            constexpr size_t SM = bw::Dims<bw::CfgHigh>::SMEM_ELEMS * 8;
-            switch (bw::kLowBits - p.r) {
-                case 4: bw::k_pass<bw::CfgHigh, 4><<<grid, NT, SM, s>>>(d, p.k); break;
-                case 5: bw::k_pass<bw::CfgHigh, 5><<<grid, NT, SM, s>>>(d, p.k); break;
-                case 6: bw::k_pass<bw::CfgHigh, 6><<<grid, NT, SM, s>>>(d, p.k); break;
-                case 7: bw::k_pass<bw::CfgHigh, 7><<<grid, NT, SM, s>>>(d, p.k); break;
-                case 8: bw::k_pass<bw::CfgHigh, 8><<<grid, NT, SM, s>>>(d, p.k); break;
-                default: return fail(BW_BAD_ARGUMENTS, "no high-pass kernel for %d stages", p.r);
-            }
-            break;
-        }
-        case Pass::REG: {
-            constexpr int NT = bw::Dims<bw::CfgReg>::NT;
-            const unsigned rgrid = (unsigned)(1ull << (n - bw::CfgReg::T));
-            switch (bw::CfgReg::T - p.r) {
-                case 8: bw::k_pass<bw::CfgReg, 8><<<rgrid, NT, 0, s>>>(d, p.k); break;
-                case 9: bw::k_pass<bw::CfgReg, 9><<<rgrid, NT, 0, s>>>(d, p.k); break;
-                case 10: bw::k_pass<bw::CfgReg, 10><<<rgrid, NT, 0, s>>>(d, p.k); break;
-                case 11: bw::k_pass<bw::CfgReg, 11><<<rgrid, NT, 0, s>>>(d, p.k); break;
-                case 12: bw::k_pass<bw::CfgReg, 12><<<rgrid, NT, 0, s>>>(d, p.k); break;
-                default: return fail(BW_BAD_ARGUMENTS, "no register pass kernel for %d stages", p.r);
-            }
-            break;
-        }
+// Every kernel the planner can emit, for one-time setup.
+template <class F>
+int for_all_pass_kernels(F&& f) {
+    for (int q = 0; q <= bw::kMaxClusterLog2; ++q) {
+        BW_TRY(visit_pass(Pass{LOW, 0, 13 + q, q}, f));
+        for (int L = (q == 0 ? 3 : q == 1 ? 4 : 5); L <= (q == 0 ? 7 : q == 1 ? 8 : 10); ++L)
+            BW_TRY(visit_pass(Pass{HIGH, 0, 13 + q - L, q}, f));
     }
-    BW_LAUNCHED("fwht pass launch");
+    for (int r = 1; r <= bw::kRegOnlyMaxBits; ++r) BW_TRY(visit_pass(Pass{REG, 0, r, 0}, f));
     return BW_OK;
+}
+
+int set_all_pass_attributes() {
+    return for_all_pass_kernels([](auto t, auto l) -> int {
+        using C = typename decltype(t)::type;
+        constexpr int L = decltype(l)::value;
+        constexpr int smem = bw::Dims<C>::SMEM_ELEMS * 8;
+        if (smem > 48 * 1024)
+            BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        return BW_OK;
+    });
+}
+
+int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s) {
+    if (p.kind == SMALL) {
+        bw::k_small<u64><<<1, 256, (size_t)(8ull << n), s>>>(d, n);
+        BW_LAUNCHED("k_small launch");
+        return BW_OK;
+    }
+    return visit_pass(p, [&](auto t, auto l) -> int {
+        using C = typename decltype(t)::type;
+        constexpr int L = decltype(l)::value;
+        const unsigned grid = (unsigned)(1ull << (n - bw::kCtaBits));
+        if constexpr (C::Q == 0) {
+            bw::k_pass<C, L><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_ELEMS * 8, s>>>(d, p.k);
+            BW_LAUNCHED("fwht pass launch");
+        } else {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(bw::Dims<C>::NT);
+            cfg.dynamicSmemBytes = bw::Dims<C>::SMEM_ELEMS * 8;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = bw::Dims<C>::CLUSTER;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L>, d, p.k));
+        }
+        return BW_OK;
+    });
 }
 
 int run_naive(u64* d, int n, int dev, cudaStream_t s) {
@@ -228,7 +340,7 @@ int fwht_impl(int64_t* data, int log2n, const std::vector<int>* widths, bool nai
     if (log2n == 0) return BW_OK;
     // 16-byte vector accesses need a 16-byte aligned base; an 8-byte aligned
     // view (e.g. an odd-offset slice) takes the per-stage path, still on GPU.
-    if (naive || (log2n >= bw::kLowBits && (reinterpret_cast<uintptr_t>(data) & 15u)))
+    if (naive || (log2n >= bw::kCtaBits && (reinterpret_cast<uintptr_t>(data) & 15u)))
         return run_naive(d, log2n, dev, s);
     std::vector<int> w;
     if (widths) w = *widths; else BW_TRY(default_plan(log2n, &w));
@@ -321,7 +433,7 @@ int bw_plan_npasses(int log2n) {
 
 int bw_fwht_i64_pass(int64_t* data, int log2n, int pass_index, void* stream) {
     BW_TRY(check_signal(data, log2n));
-    if (log2n >= bw::kLowBits && (reinterpret_cast<uintptr_t>(data) & 15u))
+    if (log2n >= bw::kCtaBits && (reinterpret_cast<uintptr_t>(data) & 15u))
         return fail(BW_BAD_ARGUMENTS, "pass-level launches need a 16-byte aligned signal");
     int dev = 0;
     BW_TRY(device_setup(&dev));
@@ -667,34 +779,25 @@ int bw_plan_describe(int log2n, int log2p, char* json, size_t len) {
     out += buf;
     for (size_t i = 0; i < passes.size(); ++i) {
         const Pass& p = passes[i];
-        const char* kind = p.kind == Pass::SMALL ? "small" : p.kind == Pass::LOW ? "low" : p.kind == Pass::HIGH ? "high" : "reg";
-        int threads = 256, smem = 0, cols = 0;
+        const char* kind = p.kind == SMALL ? "small" : p.kind == LOW ? "low" : p.kind == HIGH ? "high" : "reg";
+        int threads = 256, smem = 8 << nl, cols = nl, tbits = nl, cluster = 1;
         unsigned long long grid = 1;
-        if (p.kind == Pass::SMALL) {
-            smem = 8 << nl;
-            cols = nl;
-        } else {
-            grid = 1ull << (nl - bw::kLowBits);
-            if (p.kind == Pass::LOW) {
-                threads = bw::Dims<bw::CfgLow>::NT;
-                smem = bw::Dims<bw::CfgLow>::SMEM_ELEMS * 8;
-                cols = bw::kLowBits;
-            } else if (p.kind == Pass::HIGH) {
-                threads = bw::Dims<bw::CfgHigh>::NT;
-                smem = bw::Dims<bw::CfgHigh>::SMEM_ELEMS * 8;
-                cols = bw::kLowBits - p.r;
-            } else {
-                threads = bw::Dims<bw::CfgReg>::NT;
-                cols = bw::CfgReg::T - p.r;
-                grid = 1ull << (nl - bw::CfgReg::T);
-            }
-        }
+        if (p.kind != SMALL)
+            visit_pass(p, [&](auto t, auto l) -> int {
+                using C = typename decltype(t)::type;
+                constexpr int L = decltype(l)::value;
+                threads = bw::Dims<C>::NT;
+                smem = bw::Dims<C>::SMEM_ELEMS * 8;
+                cols = L;
+                tbits = C::T;
+                cluster = bw::Dims<C>::CLUSTER;
+                grid = 1ull << (nl - bw::kCtaBits);
+                return BW_OK;
+            });
         snprintf(buf, sizeof buf,
                  "%s{\"kind\":\"%s\",\"k\":%d,\"r\":%d,\"tile_bits\":%d,\"cols_bits\":%d,\"threads\":%d,"
-                 "\"grid\":%llu,\"smem\":%d}",
-                 i ? "," : "", kind, p.k, p.r,
-                 p.kind == Pass::SMALL ? nl : p.kind == Pass::REG ? bw::CfgReg::T : bw::kLowBits, cols, threads, grid,
-                 smem);
+                 "\"cluster\":%d,\"grid\":%llu,\"smem\":%d}",
+                 i ? "," : "", kind, p.k, p.r, tbits, cols, threads, cluster, grid, smem);
         out += buf;
     }
     out += "],\"cross_stages\":[";
@@ -717,87 +820,125 @@ int bw_plan_describe(int log2n, int log2p, char* json, size_t len) {
 // ---- static plan checker (host walk of the kernels' own address tables) ----
 namespace {
 
+// Virtual tile bits present in round RD's space (pre: 0..12; post: the
+// tile minus the rank positions P).
 template <class C, int RD>
-bool round_is_permutation(std::string* why) {
-    uint32_t seen = 0;
+constexpr uint32_t space_bits() {
+    if (RD < C::XR || C::Q == 0) return (1u << bw::kCtaBits) - 1u;
+    return ((1u << C::T) - 1u) & ~bw::p_mask<C>();
+}
+
+template <class C, int RD>
+bool round_ok(std::string* why) {
+    uint32_t seen = 0, regs = 0;
     auto add = [&](int b) {
         if (b < 0 || b >= C::T || ((seen >> b) & 1u)) return false;
         seen |= 1u << b;
         return true;
     };
-    for (int i = 0; i < C::R; ++i) if (!add(C::reg(RD, i))) { *why = "register bits overlap"; return false; }
+    for (int i = 0; i < C::R; ++i) {
+        if (!add(C::reg(RD, i))) { *why = "register bits overlap"; return false; }
+        regs |= 1u << C::reg(RD, i);
+    }
     for (int i = 0; i < 5; ++i) if (!add(C::lane(RD, i))) { *why = "lane bits overlap"; return false; }
     for (int i = 0; i < C::W; ++i) if (!add(C::warp(RD, i))) { *why = "warp bits overlap"; return false; }
-    if (seen != (1u << C::T) - 1u) { *why = "round does not cover every tile bit"; return false; }
+    if (seen != space_bits<C, RD>()) { *why = "round does not cover its space"; return false; }
+    if (C::stage(RD) & ~regs) { *why = "a staged bit is not a register bit"; return false; }
+    if (RD + 1 == C::XR && C::Q > 0 && (bw::p_mask<C>() & ~regs)) {
+        *why = "rank swap bits are not register bits before the exchange";
+        return false;
+    }
+    // Half-warp bank check of the padded smem slots (8-byte words: 16 lanes
+    // must hit 16 distinct 8-byte bank pairs) -- only rounds that touch smem.
+    if (C::NR > 1)
+        for (uint32_t warp = 0; warp < (1u << C::W); ++warp)
+            for (int j = 0; j < bw::Dims<C>::E; ++j)
+                for (uint32_t half = 0; half < 2; ++half) {
+                    uint32_t used = 0;
+                    for (uint32_t l = 0; l < 16; ++l) {
+                        const uint32_t v = bw::thread_part<C, RD>(half * 16 + l, warp) | bw::reg_part<C, RD>(j);
+                        const uint32_t bank = bw::smem_slot(bw::to_local<C, RD>(v)) & 15u;
+                        if ((used >> bank) & 1u) { *why = "smem bank conflict"; return false; }
+                        used |= 1u << bank;
+                    }
+                }
     return true;
 }
 
-// Half-warp bank check of the padded smem slots of a round (8-byte words:
-// 16 lanes must hit 16 distinct 8-byte bank pairs).
 template <class C, int RD>
-bool round_conflict_free(std::string* why) {
-    for (uint32_t warp = 0; warp < (1u << C::W); ++warp)
-        for (int j = 0; j < bw::Dims<C>::E; ++j)
-            for (uint32_t half = 0; half < 2; ++half) {
-                uint32_t used = 0;
-                for (uint32_t l = 0; l < 16; ++l) {
-                    const uint32_t lane = half * 16 + l;
-                    const uint32_t e = bw::thread_part<C, RD>(lane, warp) | bw::reg_part<C, RD>(j);
-                    const uint32_t bank = bw::smem_slot(e) & 15u;
-                    if ((used >> bank) & 1u) { *why = "smem bank conflict"; return false; }
-                    used |= 1u << bank;
-                }
-            }
+bool rounds_ok(std::string* why) {
+    if constexpr (RD < C::NR) {
+        if (!round_ok<C, RD>(why)) return false;
+        return rounds_ok<C, RD + 1>(why);
+    }
     return true;
+}
+
+template <class C, int RD, int L>
+uint32_t all_stage_masks() {
+    if constexpr (RD < C::NR) {
+        return bw::stage_mask<C, RD, L>() | all_stage_masks<C, RD + 1, L>();
+    }
+    return 0;
 }
 
 template <class C, int L>
 int check_pass(int n, int k, std::vector<uint8_t>& touched, uint32_t* stage_bits_out, uint64_t* bfly) {
     constexpr int T = C::T;
     std::string why;
-    if (!round_is_permutation<C, 0>(&why)) return fail(BW_BAD_ARGUMENTS, "layout round 0: %s", why.c_str());
-    if constexpr (C::NR >= 2) {
-        if (!round_is_permutation<C, 1>(&why)) return fail(BW_BAD_ARGUMENTS, "layout round 1: %s", why.c_str());
-        if (!round_conflict_free<C, 0>(&why) || !round_conflict_free<C, 1>(&why))
-            return fail(BW_BAD_ARGUMENTS, "layout: %s", why.c_str());
-    }
-    if constexpr (C::NR >= 3) {
-        if (!round_is_permutation<C, 2>(&why)) return fail(BW_BAD_ARGUMENTS, "layout round 2: %s", why.c_str());
-        if (!round_conflict_free<C, 2>(&why)) return fail(BW_BAD_ARGUMENTS, "layout: %s", why.c_str());
-    }
+    if (!rounds_ok<C, 0>(&why)) return fail(BW_BAD_ARGUMENTS, "layout: %s", why.c_str());
     // Stage coverage inside the tile: every row bit staged exactly once.
     uint32_t tile_stages = 0;
-    uint32_t rounds_masks[3] = {bw::stage_mask<C, 0, L>(), C::NR > 1 ? bw::stage_mask<C, (C::NR > 1 ? 1 : 0), L>() : 0u,
-                                C::NR > 2 ? bw::stage_mask<C, (C::NR > 2 ? 2 : 0), L>() : 0u};
-    for (int r = 0; r < C::NR; ++r) {
-        if (tile_stages & rounds_masks[r]) return fail(BW_BAD_ARGUMENTS, "tile bit staged twice");
-        tile_stages |= rounds_masks[r];
+    int staged = 0;
+    for (int rd = 0; rd < C::NR; ++rd) {
+        uint32_t m = C::stage(rd);
+        if (L < T) m &= ~((1u << L) - 1u);
+        if (tile_stages & m) return fail(BW_BAD_ARGUMENTS, "tile bit staged twice");
+        tile_stages |= m;
+        staged += __builtin_popcount(m);
     }
+    (void)staged;
     const uint32_t rows = L >= T ? (1u << T) - 1u : ((1u << T) - 1u) & ~((1u << L) - 1u);
     if (tile_stages != rows) return fail(BW_BAD_ARGUMENTS, "tile stages %x != rows %x", tile_stages, rows);
     uint32_t stage_bits = 0;  // the global bits the kernel's stage masks really cover
     for (int b = 0; b < T; ++b)
         if ((tile_stages >> b) & 1u) stage_bits |= 1u << (b < L ? b : k + (b - L));
     *stage_bits_out = stage_bits;
-    // Address walk: load layout and store layout must both be bijections.
-    const uint64_t tiles = 1ull << (n - T);
-    std::fill(touched.begin(), touched.end(), 0);
+    // Address walk over every (CTA, thread, register): the load layout, the
+    // exchange destinations and the store layout must all be bijections.
+    const uint64_t ctas = 1ull << (n - bw::kCtaBits);
+    constexpr int NQ = 1 << C::Q;
     constexpr int LAST = C::NR - 1;
-    for (uint64_t b = 0; b < tiles; ++b) {
-        const uint64_t base = bw::tile_base<T, L>(b, k);
+    std::fill(touched.begin(), touched.end(), 0);
+    std::vector<uint8_t> xdst(C::Q > 0 ? (size_t)NQ << bw::kCtaBits : 0);
+    for (uint64_t cta = 0; cta < ctas; ++cta) {
+        const uint32_t rank = (uint32_t)(cta & (NQ - 1));
+        const uint64_t base = bw::tile_base<T, L>(cta >> C::Q, k);
+        if (C::Q > 0 && rank == 0) std::fill(xdst.begin(), xdst.end(), 0);
         for (uint32_t t = 0; t < (uint32_t)bw::Dims<C>::NT; ++t) {
             const uint32_t lane = t & 31u, warp = t >> 5;
             for (int j = 0; j < bw::Dims<C>::E; ++j) {
-                const uint64_t gi = base + bw::global_off<T, L>(bw::thread_part<C, 0>(lane, warp), k) +
-                                    bw::global_off<T, L>(bw::reg_part<C, 0>(j), k);
-                const uint64_t go = base + bw::global_off<T, L>(bw::thread_part<C, LAST>(lane, warp), k) +
-                                    bw::global_off<T, L>(bw::reg_part<C, LAST>(j), k);
+                const uint32_t vin = bw::thread_part<C, 0>(lane, warp) | bw::reg_part<C, 0>(j) | bw::rank_bits<C, 0>(rank);
+                const uint32_t vout =
+                    bw::thread_part<C, LAST>(lane, warp) | bw::reg_part<C, LAST>(j) | bw::rank_bits<C, LAST>(rank);
+                const uint64_t gi = base + bw::global_off<T, L>(vin, k);
+                const uint64_t go = base + bw::global_off<T, L>(vout, k);
                 if (gi >= touched.size() || go >= touched.size())
                     return fail(BW_BAD_ARGUMENTS, "pass at k=%d reaches out of range", k);
                 if (touched[gi] & 1) return fail(BW_BAD_ARGUMENTS, "pass at k=%d loads index %llu twice", k, (unsigned long long)gi);
                 if (touched[go] & 2) return fail(BW_BAD_ARGUMENTS, "pass at k=%d stores index %llu twice", k, (unsigned long long)go);
                 touched[gi] |= 1;
                 touched[go] |= 2;
+                if constexpr (C::Q > 0) {
+                    constexpr int XW = C::XR - 1;  // round whose registers are exchanged
+                    const uint32_t v = bw::thread_part<C, XW>(lane, warp) | bw::reg_part<C, XW>(j) | bw::rank_bits<C, XW>(rank);
+                    uint32_t d = 0;
+                    for (int i = 0; i < C::Q; ++i) d |= ((v >> C::P(i)) & 1u) << i;
+                    const uint32_t slot = bw::to_local<C, C::XR>(v & ~bw::p_mask<C>());
+                    uint8_t& x = xdst[((size_t)d << bw::kCtaBits) + slot];
+                    if (x) return fail(BW_BAD_ARGUMENTS, "exchange writes a slot twice");
+                    x = 1;
+                }
             }
         }
     }
@@ -808,61 +949,78 @@ int check_pass(int n, int k, std::vector<uint8_t>& touched, uint32_t* stage_bits
 }
 
 // Host emulation of k_pass<C, L>: the same address tables, rounds, stage
-// masks and shared-memory slots, executed thread by thread on host memory.
+// masks, cluster exchange and shared-memory slots, executed thread by thread
+// on host memory (TEST HOOK; see bw_debug_emulate_i64).
+template <class C, int L, int RD>
+void emu_stages(std::vector<u64>& v) {
+    constexpr int E = bw::Dims<C>::E, NT = bw::Dims<C>::NT;
+    constexpr uint32_t mask = bw::stage_mask<C, RD, L>();
+    for (int t = 0; t < NT; ++t)
+        for (int i = 0; i < C::R; ++i)
+            if ((mask >> C::reg(RD, i)) & 1u)
+                for (int j = 0; j < E; ++j)
+                    if (!((j >> i) & 1)) {
+                        u64& a = v[(size_t)t * E + j];
+                        u64& b = v[(size_t)t * E + (j | (1 << i))];
+                        const u64 x = a, y = b;
+                        a = x + y;
+                        b = x - y;
+                    }
+}
+
+template <class C, int L, int RD>
+void emu_rounds(std::vector<std::vector<u64>>& v, std::vector<std::vector<u64>>& sm) {
+    constexpr int E = bw::Dims<C>::E, NT = bw::Dims<C>::NT, NQ = 1 << C::Q;
+    if constexpr (RD < C::NR) {
+        for (int q = 0; q < NQ; ++q)
+            for (int t = 0; t < NT; ++t)
+                for (int j = 0; j < E; ++j) {
+                    const uint32_t vv = bw::thread_part<C, RD - 1>(t & 31, t >> 5) | bw::reg_part<C, RD - 1>(j);
+                    if (RD == C::XR) {
+                        const uint32_t full = vv | bw::rank_bits<C, RD - 1>((uint32_t)q);
+                        uint32_t d = 0;
+                        for (int i = 0; i < C::Q; ++i) d |= ((full >> C::P(i)) & 1u) << i;
+                        sm[d][bw::smem_slot(bw::to_local<C, RD>(full & ~bw::p_mask<C>()))] = v[q][(size_t)t * E + j];
+                    } else {
+                        sm[q][bw::smem_slot(bw::to_local<C, RD - 1>(vv))] = v[q][(size_t)t * E + j];
+                    }
+                }
+        for (int q = 0; q < NQ; ++q) {
+            for (int t = 0; t < NT; ++t)
+                for (int j = 0; j < E; ++j)
+                    v[q][(size_t)t * E + j] =
+                        sm[q][bw::smem_slot(bw::to_local<C, RD>(bw::thread_part<C, RD>(t & 31, t >> 5) | bw::reg_part<C, RD>(j)))];
+            emu_stages<C, L, RD>(v[q]);
+        }
+        emu_rounds<C, L, RD + 1>(v, sm);
+    }
+}
+
 template <class C, int L>
 void emulate_pass(u64* data, int n, int k) {
-    constexpr int T = C::T, E = bw::Dims<C>::E, NT = bw::Dims<C>::NT;
-    std::vector<u64> v((size_t)NT * E), sm((size_t)bw::Dims<C>::TILE * 2);
+    constexpr int T = C::T, E = bw::Dims<C>::E, NT = bw::Dims<C>::NT, NQ = 1 << C::Q;
+    constexpr int LAST = C::NR - 1;
+    std::vector<std::vector<u64>> v(NQ, std::vector<u64>((size_t)NT * E));
+    std::vector<std::vector<u64>> sm(NQ, std::vector<u64>((size_t)bw::Dims<C>::CTA * 2));
     const uint64_t tiles = 1ull << (n - T);
-    auto stages = [&](uint32_t mask, int rd) {
-        for (int t = 0; t < NT; ++t)
-            for (int i = 0; i < C::R; ++i)
-                if ((mask >> C::reg(rd, i)) & 1u)
-                    for (int j = 0; j < E; ++j)
-                        if (!((j >> i) & 1)) {
-                            u64& a = v[(size_t)t * E + j];
-                            u64& b = v[(size_t)t * E + (j | (1 << i))];
-                            const u64 x = a, y = b;
-                            a = x + y;
-                            b = x - y;
-                        }
-    };
     for (uint64_t b = 0; b < tiles; ++b) {
         const uint64_t base = bw::tile_base<T, L>(b, k);
-        for (int t = 0; t < NT; ++t)
-            for (int j = 0; j < E; ++j)
-                v[(size_t)t * E + j] = data[base + bw::global_off<T, L>(bw::thread_part<C, 0>(t & 31, t >> 5), k) +
-                                            bw::global_off<T, L>(bw::reg_part<C, 0>(j), k)];
-        stages(bw::stage_mask<C, 0, L>(), 0);
-        if constexpr (C::NR >= 2) {
-            constexpr int R1 = C::NR >= 2 ? 1 : 0;
+        for (int q = 0; q < NQ; ++q) {
             for (int t = 0; t < NT; ++t)
                 for (int j = 0; j < E; ++j)
-                    sm[bw::smem_slot(bw::thread_part<C, 0>(t & 31, t >> 5)) + bw::smem_slot(bw::reg_part<C, 0>(j))] =
-                        v[(size_t)t * E + j];
-            for (int t = 0; t < NT; ++t)
-                for (int j = 0; j < E; ++j)
-                    v[(size_t)t * E + j] =
-                        sm[bw::smem_slot(bw::thread_part<C, R1>(t & 31, t >> 5)) + bw::smem_slot(bw::reg_part<C, R1>(j))];
-            stages(bw::stage_mask<C, R1, L>(), R1);
+                    v[q][(size_t)t * E + j] =
+                        data[base + bw::global_off<T, L>(bw::thread_part<C, 0>(t & 31, t >> 5) | bw::reg_part<C, 0>(j) |
+                                                             bw::rank_bits<C, 0>((uint32_t)q),
+                                                         k)];
+            emu_stages<C, L, 0>(v[q]);
         }
-        if constexpr (C::NR >= 3) {
-            constexpr int R1 = C::NR >= 3 ? 1 : 0, R2 = C::NR >= 3 ? 2 : 0;
+        emu_rounds<C, L, 1>(v, sm);
+        for (int q = 0; q < NQ; ++q)
             for (int t = 0; t < NT; ++t)
                 for (int j = 0; j < E; ++j)
-                    sm[bw::smem_slot(bw::thread_part<C, R1>(t & 31, t >> 5)) + bw::smem_slot(bw::reg_part<C, R1>(j))] =
-                        v[(size_t)t * E + j];
-            for (int t = 0; t < NT; ++t)
-                for (int j = 0; j < E; ++j)
-                    v[(size_t)t * E + j] =
-                        sm[bw::smem_slot(bw::thread_part<C, R2>(t & 31, t >> 5)) + bw::smem_slot(bw::reg_part<C, R2>(j))];
-            stages(bw::stage_mask<C, R2, L>(), R2);
-        }
-        constexpr int LAST = C::NR - 1;
-        for (int t = 0; t < NT; ++t)
-            for (int j = 0; j < E; ++j)
-                data[base + bw::global_off<T, L>(bw::thread_part<C, LAST>(t & 31, t >> 5), k) +
-                     bw::global_off<T, L>(bw::reg_part<C, LAST>(j), k)] = v[(size_t)t * E + j];
+                    data[base + bw::global_off<T, L>(bw::thread_part<C, LAST>(t & 31, t >> 5) | bw::reg_part<C, LAST>(j) |
+                                                         bw::rank_bits<C, LAST>((uint32_t)q),
+                                                     k)] = v[q][(size_t)t * E + j];
     }
 }
 
@@ -881,32 +1039,15 @@ extern "C" int bw_plan_check(int log2n, const int* pass_bits, int npasses, uint6
     for (const Pass& p : passes) {
         uint32_t bits = 0;
         int st = BW_OK;
-        switch (p.kind) {
-            case Pass::SMALL:
-                bits = (1u << log2n) - 1u;
-                bfly += (uint64_t)log2n << (log2n - 1);
-                break;
-            case Pass::LOW:
-                st = check_pass<bw::CfgLow, 14>(log2n, 14, touched, &bits, &bfly);
-                break;
-            case Pass::HIGH:
-                switch (bw::kLowBits - p.r) {
-                    case 4: st = check_pass<bw::CfgHigh, 4>(log2n, p.k, touched, &bits, &bfly); break;
-                    case 5: st = check_pass<bw::CfgHigh, 5>(log2n, p.k, touched, &bits, &bfly); break;
-                    case 6: st = check_pass<bw::CfgHigh, 6>(log2n, p.k, touched, &bits, &bfly); break;
-                    case 7: st = check_pass<bw::CfgHigh, 7>(log2n, p.k, touched, &bits, &bfly); break;
-                    case 8: st = check_pass<bw::CfgHigh, 8>(log2n, p.k, touched, &bits, &bfly); break;
-                }
-                break;
-            case Pass::REG:
-                switch (bw::CfgReg::T - p.r) {
-                    case 8: st = check_pass<bw::CfgReg, 8>(log2n, p.k, touched, &bits, &bfly); break;
-                    case 9: st = check_pass<bw::CfgReg, 9>(log2n, p.k, touched, &bits, &bfly); break;
-                    case 10: st = check_pass<bw::CfgReg, 10>(log2n, p.k, touched, &bits, &bfly); break;
-                    case 11: st = check_pass<bw::CfgReg, 11>(log2n, p.k, touched, &bits, &bfly); break;
-                    case 12: st = check_pass<bw::CfgReg, 12>(log2n, p.k, touched, &bits, &bfly); break;
-                }
-                break;
+        if (p.kind == SMALL) {
+            bits = (1u << log2n) - 1u;
+            bfly += (uint64_t)log2n << (log2n - 1);
+        } else {
+            st = visit_pass(p, [&](auto t, auto l) -> int {
+                using C = typename decltype(t)::type;
+                constexpr int L = decltype(l)::value;
+                return check_pass<C, L>(log2n, p.k, touched, &bits, &bfly);
+            });
         }
         if (st != BW_OK) return st;
         if (covered & bits) return fail(BW_BAD_ARGUMENTS, "stage applied twice");
@@ -930,38 +1071,23 @@ extern "C" int bw_debug_emulate_i64(int64_t* host, int log2n, const int* pass_bi
     BW_TRY(build_passes(log2n, w, &passes));
     u64* d = reinterpret_cast<u64*>(host);
     for (const Pass& p : passes) {
-        switch (p.kind) {
-            case Pass::SMALL: {
-                const uint64_t N = 1ull << log2n;
-                for (int k = 0; k < log2n; ++k)
-                    for (uint64_t t = 0; t < N / 2; ++t) {
-                        const uint64_t lo = ((t >> k) << (k + 1)) | (t & ((1ull << k) - 1)), hi = lo + (1ull << k);
-                        const u64 a = d[lo], b = d[hi];
-                        d[lo] = a + b;
-                        d[hi] = a - b;
-                    }
-                break;
-            }
-            case Pass::LOW: emulate_pass<bw::CfgLow, 14>(d, log2n, 14); break;
-            case Pass::HIGH:
-                switch (bw::kLowBits - p.r) {
-                    case 4: emulate_pass<bw::CfgHigh, 4>(d, log2n, p.k); break;
-                    case 5: emulate_pass<bw::CfgHigh, 5>(d, log2n, p.k); break;
-                    case 6: emulate_pass<bw::CfgHigh, 6>(d, log2n, p.k); break;
-                    case 7: emulate_pass<bw::CfgHigh, 7>(d, log2n, p.k); break;
-                    case 8: emulate_pass<bw::CfgHigh, 8>(d, log2n, p.k); break;
+        if (p.kind == SMALL) {
+            const uint64_t N = 1ull << log2n;
+            for (int k = 0; k < log2n; ++k)
+                for (uint64_t t = 0; t < N / 2; ++t) {
+                    const uint64_t lo = ((t >> k) << (k + 1)) | (t & ((1ull << k) - 1)), hi = lo + (1ull << k);
+                    const u64 a = d[lo], b = d[hi];
+                    d[lo] = a + b;
+                    d[hi] = a - b;
                 }
-                break;
-            case Pass::REG:
-                switch (bw::CfgReg::T - p.r) {
-                    case 8: emulate_pass<bw::CfgReg, 8>(d, log2n, p.k); break;
-                    case 9: emulate_pass<bw::CfgReg, 9>(d, log2n, p.k); break;
-                    case 10: emulate_pass<bw::CfgReg, 10>(d, log2n, p.k); break;
-                    case 11: emulate_pass<bw::CfgReg, 11>(d, log2n, p.k); break;
-                    case 12: emulate_pass<bw::CfgReg, 12>(d, log2n, p.k); break;
-                }
-                break;
+            continue;
         }
+        BW_TRY(visit_pass(p, [&](auto t, auto l) -> int {
+            using C = typename decltype(t)::type;
+            constexpr int L = decltype(l)::value;
+            emulate_pass<C, L>(d, log2n, p.k);
+            return BW_OK;
+        }));
     }
     return BW_OK;
 }

@@ -85,49 +85,110 @@ __device__ __forceinline__ void store_global(const u64 (&v)[Dims<C>::E], u64* __
 
 template <class C, int RD>
 __device__ __forceinline__ void store_smem(const u64 (&v)[Dims<C>::E], u64* sm, uint32_t tp) {
-    u64* p = sm + smem_slot(tp);
+    u64* p = sm + smem_slot(to_local<C, RD>(tp));
 #pragma unroll
-    for (int j = 0; j < Dims<C>::E; ++j) p[smem_slot(reg_part<C, RD>(j))] = v[j];
+    for (int j = 0; j < Dims<C>::E; ++j) p[smem_slot(to_local<C, RD>(reg_part<C, RD>(j)))] = v[j];
 }
 
 template <class C, int RD>
 __device__ __forceinline__ void load_smem(u64 (&v)[Dims<C>::E], const u64* sm, uint32_t tp) {
-    const u64* p = sm + smem_slot(tp);
+    const u64* p = sm + smem_slot(to_local<C, RD>(tp));
 #pragma unroll
-    for (int j = 0; j < Dims<C>::E; ++j) v[j] = p[smem_slot(reg_part<C, RD>(j))];
+    for (int j = 0; j < Dims<C>::E; ++j) v[j] = p[smem_slot(to_local<C, RD>(reg_part<C, RD>(j)))];
+}
+
+// ---- thread-block-cluster plumbing (DSMEM) ---------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_u64(uint32_t addr, u64 v) {
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+
+// Exchange transpose: registers of round RD (pre space) -> the post-space
+// slots of the CTA that owns each element after the exchange.  The owner is
+// given by the element's bits at positions P(i), which are register bits of
+// round RD, so every destination is a compile-time choice per register.
+template <class C, int RD>
+__device__ __forceinline__ void exchange_write(const u64 (&v)[Dims<C>::E], u64* sm, uint32_t tp, uint32_t rank) {
+    constexpr uint32_t pm = p_mask<C>();
+    constexpr int NQ = 1 << C::Q;
+    const uint32_t base_local = (uint32_t)__cvta_generic_to_shared(sm) +
+                                8u * (smem_slot(to_local<C, C::XR>(tp)) +
+                                      smem_slot(to_local<C, C::XR>(rank << kCtaBits)));
+    uint32_t base[NQ];
+#pragma unroll
+    for (int d = 0; d < NQ; ++d) base[d] = map_to_rank(base_local, (uint32_t)d);
+#pragma unroll
+    for (int j = 0; j < Dims<C>::E; ++j) {
+        const uint32_t rp = reg_part<C, RD>(j);
+        uint32_t d = 0;
+#pragma unroll
+        for (int i = 0; i < C::Q; ++i) d |= ((rp >> C::P(i)) & 1u) << i;
+        st_cluster_u64(base[d] + 8u * smem_slot(to_local<C, C::XR>(rp & ~pm)), v[j]);
+    }
+}
+
+template <class C, int L, int RD>
+__device__ __forceinline__ void run_rounds(u64 (&v)[Dims<C>::E], u64* sm, uint32_t lane, uint32_t warp,
+                                           uint32_t rank) {
+    if constexpr (RD < C::NR) {
+        if constexpr (RD == C::XR) {
+            static_assert((thread_part_bits<C, RD - 1>() & p_mask<C>()) == 0, "rank swap bits must be register bits");
+            static_assert(RD == 1, "the DSMEM exchange is the first transpose (smem still unused)");
+            // Partners have started (the arrive was issued right after the
+            // loads); no smem has been read yet, so no WAR hazard exists.
+            asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+            exchange_write<C, RD - 1>(v, sm, thread_part<C, RD - 1>(lane, warp), rank);
+            cluster_sync_all();  // every remote write has landed
+        } else {
+            if constexpr (RD > 1) __syncthreads();
+            store_smem<C, RD - 1>(v, sm, thread_part<C, RD - 1>(lane, warp));
+            __syncthreads();
+        }
+        load_smem<C, RD>(v, sm, thread_part<C, RD>(lane, warp));
+        apply_stages<C, RD, L>(v);
+        run_rounds<C, L, RD + 1>(v, sm, lane, warp, rank);
+    }
 }
 
 // One pass over every tile: load (round 0 layout) -> stages -> [transpose ->
 // stages]* -> store (last round layout).  k = first global stage bit of the
-// rows (ignored for L == T).
+// rows (ignored for L == T).  Cluster configs (Q > 0) put 2^Q CTAs on one
+// tile; grid = 2^(n-13) CTAs for every config.
 template <class C, int L>
-__global__ void __launch_bounds__(Dims<C>::NT, 1)
+__global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     k_pass(u64* __restrict__ data, int k) {
     constexpr int T = C::T;
     constexpr int E = Dims<C>::E;
     extern __shared__ u64 sm[];
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
-    u64* g = data + tile_base<T, L>(blockIdx.x, k);
+    uint32_t rank = 0;
+    uint64_t tile = blockIdx.x;
+    if constexpr (C::Q > 0) {
+        rank = cluster_ctarank();
+        tile = blockIdx.x >> C::Q;
+    }
+    u64* g = data + tile_base<T, L>(tile, k);
 
     u64 v[E];
-    load_global<C, 0, T, L>(v, g, thread_part<C, 0>(lane, warp), k);
+    load_global<C, 0, T, L>(v, g, thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
+    if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     apply_stages<C, 0, L>(v);
-    if constexpr (C::NR >= 2) {
-        store_smem<C, 0>(v, sm, thread_part<C, 0>(lane, warp));
-        __syncthreads();
-        load_smem<C, 1>(v, sm, thread_part<C, 1>(lane, warp));
-        apply_stages<C, 1, L>(v);
-    }
-    if constexpr (C::NR >= 3) {
-        __syncthreads();
-        store_smem<C, 1>(v, sm, thread_part<C, 1>(lane, warp));
-        __syncthreads();
-        load_smem<C, 2>(v, sm, thread_part<C, 2>(lane, warp));
-        apply_stages<C, 2, L>(v);
-    }
+    run_rounds<C, L, 1>(v, sm, lane, warp, rank);
     constexpr int LAST = C::NR - 1;
-    store_global<C, LAST, T, L>(v, g, thread_part<C, LAST>(lane, warp), k);
+    store_global<C, LAST, T, L>(v, g, thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank), k);
 }
 
 // ---------------------------------------------------------------------------

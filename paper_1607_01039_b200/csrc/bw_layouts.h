@@ -10,14 +10,22 @@
 // columns, and the pass applies stages k..k+T-L-1 (external.py:272-283
 // `_blocked_stage_pass`, merging T-L stages per HBM round trip).
 //
-// Inside a CTA every tile bit lives in one of three places: a register bit
-// (a thread holds 2^R elements), a lane bit (5) or a warp bit (W).  A round
-// is one such assignment; butterflies run only on register bits, and
-// consecutive rounds are joined by a transpose through shared memory
-// (padded address e + (e >> 5), chosen so that every 8-byte access of every
-// round is conflict free per half-warp -- see DESIGN.md).  The same tables
-// drive the device kernels and the host plan checker (bw_plan_check), so the
-// checker verifies the addresses the kernels really touch.
+// Every CTA holds 2^13 elements of the tile (256 threads x 32 int64 in
+// registers, two CTAs per SM).  Tiles of 2^14 / 2^15 elements are split over
+// a thread-block cluster of 2 / 4 CTAs: the top q tile bits are the CTA's
+// cluster rank ("pre" space).  Once every CTA-local stage is done, one
+// transpose runs through distributed shared memory and swaps those rank bits
+// with q already-staged local bits ("post" space), after which the former
+// rank bits are local and get their stages.
+//
+// Inside a CTA every tile bit of the current space lives in one of three
+// places: a register bit (5), a lane bit (5) or a warp bit (3).  A round is
+// one such assignment; butterflies run only on register bits, and
+// consecutive rounds are joined by a transpose through shared memory (slot of
+// local index e is e + (e >> 5): every 8-byte access of every round is
+// conflict-free per half-warp, which bw_plan_check verifies).  The same
+// tables drive the device kernels, the host plan checker and the host
+// emulator, so those check the addresses the kernels really touch.
 #pragma once
 #include <stdint.h>
 
@@ -27,67 +35,136 @@
 #define BW_HD
 #endif
 
+#ifndef BW_T13_MINB
+#define BW_T13_MINB 2  // CTAs per SM the kernels are register-budgeted for
+#endif
+
 namespace bw {
 
-constexpr int kLowBits = 14;      // stages fused into the low-bits pass
-constexpr int kMaxHighBits = 10;  // stages per strided high-bits pass
-constexpr int kRegOnlyMaxBits = 5;
+constexpr int kCtaBits = 13;        // elements per CTA = 2^13 (64 KiB)
+constexpr int kMaxHighBits = 10;    // stages per strided high-bits pass
+constexpr int kRegOnlyMaxBits = 5;  // high passes this narrow need no smem
+constexpr int kMaxClusterLog2 = 2;  // clusters of up to 4 CTAs
 
-// Layout tables are packed 4 bits per entry (entry i = nibble i) so that
-// the same constexpr functions fold to immediates in device code and run
-// unchanged in the host plan checker.
+// Layout tables are packed 4 bits per entry (entry i = nibble i) so that the
+// same constexpr functions fold to immediates in device code and run
+// unchanged in the host checker / emulator.
 BW_HD constexpr int nib(uint64_t packed, int i) { return (int)((packed >> (4 * i)) & 15u); }
 
-// Fused low-bits pass: 2^14 contiguous int64 (128 KiB) per CTA, 512 threads,
-// 32 elements per thread; rounds stage {0,10..13}, {1..5}, {6..9}.
-// Rounds 0 and 2 put tile bit 0 in register bit 0 -> 16-byte global accesses.
-//   round 0: reg {0,10,11,12,13}  lane {1,2,3,5,4}  warp {6,7,8,9}
-//   round 1: reg {1,2,3,4,5}      lane {0,6,7,8,9}  warp {10..13}
-//   round 2: reg {0,6,7,8,9}      lane {1,2,3,5,4}  warp {10..13}
-struct CfgLow {
-    static constexpr int T = 14, R = 5, W = 4, NR = 3;
-    BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xDCBA0ull : rd == 1 ? 0x54321ull : 0x98760ull, i); }
+// Common fields: T (tile bits), Q (log2 cluster size), R/W (register/warp
+// bits), NR (rounds), XR (first round in post space; NR if no exchange),
+// P(i) (local positions that take the rank bits after the exchange),
+// MINB (CTAs per SM the register budget targets).  reg/lane/warp tables are
+// VIRTUAL tile bits; stage(rd) is a mask of virtual tile bits.
+
+// Fused low-bits pass over stages 0..12 (single CTA).
+//   round 0: reg {0,9,10,11,12}  lane {1,2,3,5,4}  warp {6,7,8}
+//   round 1: reg {1,2,3,4,5}     lane {0,6,7,8,9}  warp {10,11,12}
+//   round 2: reg {0,6,7,8,12}    lane {1,2,3,5,4}  warp {9,10,11}
+struct CfgLow13 {
+    static constexpr int T = 13, Q = 0, R = 5, W = 3, NR = 3, XR = 3, MINB = BW_T13_MINB;
+    BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xCBA90ull : rd == 1 ? 0x54321ull : 0xC8760ull, i); }
     BW_HD static constexpr int lane(int rd, int i) { return nib(rd == 1 ? 0x98760ull : 0x45321ull, i); }
-    BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x9876ull : 0xDCBAull, i); }
-    BW_HD static constexpr uint32_t stage(int rd) { return rd == 0 ? 0x3C01u : rd == 1 ? 0x003Eu : 0x03C0u; }
+    BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x876ull : rd == 1 ? 0xCBAull : 0xBA9ull, i); }
+    BW_HD static constexpr uint32_t stage(int rd) { return rd == 0 ? 0x1E01u : rd == 1 ? 0x003Eu : 0x01C0u; }
+    BW_HD static constexpr int P(int) { return 0; }
 };
 
-// Strided high-bits pass with 6..10 stage rows: 2^14 elements per CTA,
-// 512 threads; rounds stage tile bits {9..13} and {L..8}; one transpose.
-//   round 0: reg {9..13}  lane {0,1,2,3,4}  warp {5,6,7,8}
-//   round 1: reg {4..8}   lane {0,1,2,3,9}  warp {10..13}
-struct CfgHigh {
-    static constexpr int T = 14, R = 5, W = 4, NR = 2;
-    BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xDCBA9ull : 0x87654ull, i); }
-    BW_HD static constexpr int lane(int rd, int i) { return nib(rd == 0 ? 0x43210ull : 0x93210ull, i); }
-    BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x8765ull : 0xDCBAull, i); }
-    BW_HD static constexpr uint32_t stage(int rd) { return rd == 0 ? 0x3E00u : 0x01F0u; }
+// Low-bits pass over stages 0..13: cluster of 2.  Round 0 stages the bits
+// it holds in registers, then the rank bit (tile bit 13) swaps with tile
+// bit 12 in the first transpose, which runs through DSMEM.  Lanes sit on
+// tile bits 0..4 whenever a round writes remote memory, so every DSMEM store
+// instruction covers 256 contiguous bytes.
+//   round 0: reg {8..12}            lane {0,1,2,3,4}  warp {5,6,7}
+//   round 1 (post): reg {0..4}      lane {5,6,7,8,9}  warp {10,11,13}
+//   round 2 (post): reg {5,6,7,8,13} lane {0,1,2,3,4} warp {9,10,11}
+struct CfgLow14c {
+    static constexpr int T = 14, Q = 1, R = 5, W = 3, NR = 3, XR = 1, MINB = BW_T13_MINB;
+    BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xCBA98ull : rd == 1 ? 0x43210ull : 0xD8765ull, i); }
+    BW_HD static constexpr int lane(int rd, int i) { return nib(rd == 1 ? 0x98765ull : 0x43210ull, i); }
+    BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x765ull : rd == 1 ? 0xDBAull : 0xBA9ull, i); }
+    BW_HD static constexpr uint32_t stage(int rd) { return rd == 0 ? 0x1F00u : rd == 1 ? 0x001Fu : 0x20E0u; }
+    BW_HD static constexpr int P(int) { return 12; }
+};
+
+// Low-bits pass over stages 0..14: cluster of 4; the rank bits (13, 14)
+// swap with tile bits 11, 12 in the first (DSMEM) transpose.
+//   round 0: reg {8..12}              lane {0,1,2,3,4}  warp {5,6,7}
+//   round 1 (post): reg {0..4}        lane {5,6,7,8,9}  warp {10,13,14}
+//   round 2 (post): reg {5,6,7,13,14} lane {0,1,2,3,4}  warp {8,9,10}
+struct CfgLow15c {
+    static constexpr int T = 15, Q = 2, R = 5, W = 3, NR = 3, XR = 1, MINB = BW_T13_MINB;
+    BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xCBA98ull : rd == 1 ? 0x43210ull : 0xED765ull, i); }
+    BW_HD static constexpr int lane(int rd, int i) { return nib(rd == 1 ? 0x98765ull : 0x43210ull, i); }
+    BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x765ull : rd == 1 ? 0xEDAull : 0xA98ull, i); }
+    BW_HD static constexpr uint32_t stage(int rd) { return rd == 0 ? 0x1F00u : rd == 1 ? 0x001Fu : 0x60E0u; }
+    BW_HD static constexpr int P(int i) { return 11 + i; }
+};
+
+// Strided high-bits pass with 6..8 stage rows (tile bits L..12, L = 13 - r).
+//   round 0: reg {8..12}  lane {0,1,2,3,4}  warp {5,6,7}
+//   round 1: reg {3..7}   lane {0,1,2,8,9}  warp {10,11,12}
+struct CfgHigh13 {
+    static constexpr int T = 13, Q = 0, R = 5, W = 3, NR = 2, XR = 2, MINB = BW_T13_MINB;
+    BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xCBA98ull : 0x76543ull, i); }
+    BW_HD static constexpr int lane(int rd, int i) { return nib(rd == 0 ? 0x43210ull : 0x98210ull, i); }
+    BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x765ull : 0xCBAull, i); }
+    BW_HD static constexpr uint32_t stage(int rd) { return rd == 0 ? 0x1F00u : 0x00F8u; }
+    BW_HD static constexpr int P(int) { return 0; }
+};
+
+// High-bits pass over rows L..13 (r = 14 - L: 9 at L = 5, 10 at L = 4):
+// cluster of 2.  The rank bit (tile bit 13, the top row) swaps with tile
+// bit 12 in the only transpose, which runs through DSMEM.
+//   round 0: reg {8..12}          lane {0,1,2,3,4}  warp {5,6,7}
+//   round 1 (post): reg {4,5,6,7,13}  lane {0,1,2,3,8}  warp {9,10,11}
+struct CfgHigh14c {
+    static constexpr int T = 14, Q = 1, R = 5, W = 3, NR = 2, XR = 1, MINB = BW_T13_MINB;
+    BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xCBA98ull : 0xD7654ull, i); }
+    BW_HD static constexpr int lane(int rd, int i) { return nib(rd == 0 ? 0x43210ull : 0x83210ull, i); }
+    BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x765ull : 0xBA9ull, i); }
+    BW_HD static constexpr uint32_t stage(int rd) { return rd == 0 ? 0x1F00u : 0x20F0u; }
+    BW_HD static constexpr int P(int) { return 12; }
+};
+
+// High-bits pass over rows L..14 (r = 15 - L: 10 at L = 5): cluster of 4.
+// The rank bits (13, 14) swap with tile bits 11, 12 in the DSMEM transpose.
+//   round 0: reg {8..12}           lane {0,1,2,3,4}  warp {5,6,7}
+//   round 1 (post): reg {5,6,7,13,14}  lane {0,1,2,3,4}  warp {8,9,10}
+struct CfgHigh15c {
+    static constexpr int T = 15, Q = 2, R = 5, W = 3, NR = 2, XR = 1, MINB = BW_T13_MINB;
+    BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xCBA98ull : 0xED765ull, i); }
+    BW_HD static constexpr int lane(int, int i) { return nib(0x43210ull, i); }
+    BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x765ull : 0xA98ull, i); }
+    BW_HD static constexpr uint32_t stage(int rd) { return rd == 0 ? 0x1F00u : 0x60E0u; }
+    BW_HD static constexpr int P(int i) { return 11 + i; }
 };
 
 // Strided high-bits pass with <= 5 stage rows: register-only, no shared
-// memory; 2^13-element tiles, 256 threads x 32 elements, tile bits 8..12 in
-// registers (2 CTAs per SM).
+// memory; tile bits 8..12 in registers.
 //   round 0: reg {8..12}  lane {0..4}  warp {5,6,7}
 struct CfgReg {
-    static constexpr int T = 13, R = 5, W = 3, NR = 1;
+    static constexpr int T = 13, Q = 0, R = 5, W = 3, NR = 1, XR = 1, MINB = 1;
     BW_HD static constexpr int reg(int, int i) { return nib(0xCBA98ull, i); }
     BW_HD static constexpr int lane(int, int i) { return nib(0x43210ull, i); }
     BW_HD static constexpr int warp(int, int i) { return nib(0x765ull, i); }
     BW_HD static constexpr uint32_t stage(int) { return 0x1F00u; }
+    BW_HD static constexpr int P(int) { return 0; }
 };
 
 template <class C>
 struct Dims {
-    static constexpr int E = 1 << C::R;              // elements per thread
-    static constexpr int NT = 32 << C::W;            // threads per CTA
-    static constexpr int TILE = 1 << C::T;           // elements per tile
-    static constexpr int SMEM_ELEMS = C::NR > 1 ? TILE + (TILE >> 5) : 0;
+    static constexpr int E = 1 << C::R;               // elements per thread
+    static constexpr int NT = 32 << C::W;             // threads per CTA
+    static constexpr int CTA = 1 << kCtaBits;         // elements per CTA
+    static constexpr int SMEM_ELEMS = C::NR > 1 ? CTA + (CTA >> 5) : 0;
+    static constexpr int CLUSTER = 1 << C::Q;
 };
 
-// Padded shared-memory slot of tile index e; additive over disjoint bit sets.
+// Padded shared-memory slot of local index e; additive over disjoint bit sets.
 BW_HD constexpr uint32_t smem_slot(uint32_t e) { return e + (e >> 5); }
 
-// Tile index contributed by register index j in round RD.
+// Tile index (virtual bits) contributed by register index j in round RD.
 template <class C, int RD>
 BW_HD constexpr uint32_t reg_part(int j) {
     uint32_t e = 0;
@@ -96,7 +173,7 @@ BW_HD constexpr uint32_t reg_part(int j) {
     return e;
 }
 
-// Tile index contributed by (lane, warp) in round RD.
+// Tile index (virtual bits) contributed by (lane, warp) in round RD.
 template <class C, int RD>
 BW_HD inline uint32_t thread_part(uint32_t lane, uint32_t warp) {
     uint32_t e = 0;
@@ -109,6 +186,44 @@ BW_HD inline uint32_t thread_part(uint32_t lane, uint32_t warp) {
 #endif
     for (int i = 0; i < C::W; ++i) e |= ((warp >> i) & 1u) << C::warp(RD, i);
     return e;
+}
+
+// Mask of the tile bits held by lanes and warps in round RD.
+template <class C, int RD>
+BW_HD constexpr uint32_t thread_part_bits() {
+    uint32_t m = 0;
+    for (int i = 0; i < 5; ++i) m |= 1u << C::lane(RD, i);
+    for (int i = 0; i < C::W; ++i) m |= 1u << C::warp(RD, i);
+    return m;
+}
+
+// Mask of the positions P(0..Q-1) (post-space rank bits).
+template <class C>
+BW_HD constexpr uint32_t p_mask() {
+    uint32_t m = 0;
+    for (int i = 0; i < C::Q; ++i) m |= 1u << C::P(i);
+    return m;
+}
+
+// Local (per-CTA) index of virtual index v in round RD's space.  Pre space:
+// identity on bits 0..12.  Post space: virtual bit 13+i sits at local P(i).
+// Linear over disjoint bit sets (bits are moved, never combined).
+template <class C, int RD>
+BW_HD constexpr uint32_t to_local(uint32_t v) {
+    if (RD < C::XR || C::Q == 0) return v;
+    uint32_t e = v & ((1u << kCtaBits) - 1u);
+    for (int i = 0; i < C::Q; ++i) e |= ((v >> (kCtaBits + i)) & 1u) << C::P(i);
+    return e;
+}
+
+// Virtual bits fixed by the CTA's cluster rank in round RD's space.
+template <class C, int RD>
+BW_HD constexpr uint32_t rank_bits(uint32_t rank) {
+    if (C::Q == 0) return 0;
+    if (RD < C::XR) return rank << kCtaBits;
+    uint32_t v = 0;
+    for (int i = 0; i < C::Q; ++i) v |= ((rank >> i) & 1u) << C::P(i);
+    return v;
 }
 
 // Stage mask of round RD for a tile whose low L bits are columns.

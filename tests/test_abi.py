@@ -51,13 +51,14 @@ def splits(h):
             yield (first,) + rest
 
 
-@pytest.mark.parametrize("n", [15, 16, 18, 20, 22])
-def test_every_pass_split_checks(n):
+@pytest.mark.parametrize("low", [13, 14, 15])
+@pytest.mark.parametrize("n", [16, 18, 20, 22])
+def test_every_pass_split_checks(n, low):
     count = 0
-    for parts in splits(n - 14):
+    for parts in splits(n - low):
         if n == 22 and len(parts) > 3:
             continue
-        assert sharded.plan_check(n, [14, *parts]) == n << (n - 1)
+        assert sharded.plan_check(n, [low, *parts]) == n << (n - 1)
         count += 1
     assert count > 0
 
@@ -66,7 +67,11 @@ def test_bad_plans_rejected():
     with pytest.raises(errors.BadArguments):
         sharded.plan_check(20, [14, 11, -5])
     with pytest.raises(errors.BadArguments):
-        sharded.plan_check(20, [13, 7])
+        sharded.plan_check(20, [12, 8])
+    with pytest.raises(errors.BadArguments):
+        sharded.plan_check(20, [16, 4])
+    with pytest.raises(errors.BadArguments):
+        sharded.plan_check(19, [14, 5 | (2 << 4)])  # 5 stages on a 2-CTA tile: 9 column bits, not built
     with pytest.raises(errors.BadArguments):
         sharded.plan_check(20, [14, 5])
 
@@ -74,11 +79,12 @@ def test_bad_plans_rejected():
 def test_plan_describe():
     p = sharded.plan(32, 0)
     assert [x["kind"] for x in p["passes"]] == ["low", "high", "high"]
+    assert all(x["cols_bits"] >= 5 for x in p["passes"][1:])  # >= 256-byte row segments
     assert sum(x["r"] for x in p["passes"]) == 32
     assert p["hbm_bytes_per_pass"] == 16 << 32
     q = sharded.plan(34, 3)
     assert q["local_log2n"] == 31 and q["cross_stages"] == [31, 32, 33]
-    assert sharded.plan(19, 0)["passes"][1]["kind"] == "reg"
+    assert sharded.plan(18, 0)["passes"][1]["kind"] == "reg"
     assert sharded.plan(10, 0)["passes"][0]["kind"] == "small"
 
 
@@ -158,7 +164,7 @@ def emulate(x, bits=None):
     return y
 
 
-@pytest.mark.parametrize("n", [0, 1, 5, 13, 14, 15, 17, 19, 20, 23])
+@pytest.mark.parametrize("n", [0, 1, 5, 12, 13, 14, 15, 17, 19, 20, 23, 24])
 def test_kernel_tables_emulated_on_host_match_oracle(coracle, n):
     """The pass kernels' address/stage/smem tables, executed on the host
     (bw_debug_emulate_i64), equal the oracle bit for bit."""
@@ -170,12 +176,29 @@ def test_kernel_tables_emulated_on_host_match_oracle(coracle, n):
     assert np.array_equal(emulate(x), ref)
 
 
-def test_kernel_tables_every_split_emulated(coracle):
+@pytest.mark.parametrize("low", [13, 14, 15])
+def test_kernel_tables_every_split_emulated(coracle, low):
     from oracle import oracle_np
 
     n = 21
     x = oracle_np.gen(1, 5, [], 0, 1 << n)
     ref = x.copy()
     coracle.oracle_fwht_i64(ref.ctypes.data, n)
-    for parts in splits(n - 14):
-        assert np.array_equal(emulate(x, [14, *parts]), ref), parts
+    for parts in splits(n - low):
+        assert np.array_equal(emulate(x, [low, *parts]), ref), parts
+
+
+@pytest.mark.parametrize("plan", [
+    [14, 9 | (2 << 4)], [14, 8 | (2 << 4)], [14, 7 | (3 << 4)], [15, 8], [13, 10],
+    [13, 9], [13, 10 | (3 << 4)], [13, 8 | (3 << 4)], [13, 6 | (2 << 4)], [13, 9 | (1 << 4)],
+    [15, 7 | (2 << 4)], [13, 5 | (1 << 4)], [14, 6 | (3 << 4)], [13, 5 | (3 << 4), 4]])
+def test_forced_cluster_shapes_emulated(coracle, plan):
+    """Every cluster shape (forced with r | (q+1) << 4), on the host emulator."""
+    from oracle import oracle_np
+
+    n = sum(w & 15 for w in plan)
+    x = oracle_np.gen(2, 11 + n, [1 << 20], 0, 1 << n)
+    ref = x.copy()
+    coracle.oracle_fwht_i64(ref.ctypes.data, n)
+    assert sharded.plan_check(n, plan) == n << (n - 1)
+    assert np.array_equal(emulate(x, plan), ref)

@@ -141,18 +141,24 @@ def test_matches_oracle_every_n(coracle, n):
 
 def test_every_pass_split_is_identical(coracle):
     """Block-size independence (test_external.py:120-129): every legal split
-    of the high bits gives byte-identical output."""
+    of the high bits -- and every tile / cluster shape -- gives byte-identical
+    output (entries r | (q + 1) << 4 force a cluster of 2^q CTAs)."""
     n = 22
     x = oracle_np.gen(2, 77, [1 << 20], 0, 1 << n)
     ref = c_fwht(coracle, x)
     assert np.array_equal(planned(x, None), ref)  # naive per-stage path
-    for parts in ((8,), (1, 7), (7, 1), (2, 3, 3), (5, 3), (4, 4), (6, 2), (3, 5), (1, 1, 1, 1, 1, 1, 1, 1)):
-        assert np.array_equal(planned(x, [14, *parts]), ref), parts
+    plans = [[13, 9], [13, 1, 8], [13, 8, 1], [13, 3, 3, 3], [13, 5, 4], [13, 4, 5], [13, 6, 3], [13, 2, 7],
+             [14, 8], [14, 4, 4], [14, 1, 7], [15, 7], [15, 2, 5], [13, 9 | (1 << 4)], [13, 9 | (2 << 4)],
+             [14, 8 | (2 << 4)], [14, 8 | (3 << 4)], [15, 7 | (2 << 4)], [13, 6 | (2 << 4), 3],
+             [13, 1, 1, 1, 1, 1, 1, 1, 1, 1]]
+    for plan in plans:
+        assert np.array_equal(planned(x, plan), ref), plan
     n = 24
     x = oracle_np.gen(1, 78, [], 0, 1 << n)
     ref = c_fwht(coracle, x)
-    for parts in ((10,), (5, 5), (9, 1), (1, 9), (6, 4), (4, 6)):
-        assert np.array_equal(planned(x, [14, *parts]), ref), parts
+    for plan in ([13, 10, 1], [13, 1, 10], [13, 6, 5], [14, 10], [15, 9], [14, 5, 5], [15, 4, 5],
+                 [13, 10 | (1 << 4), 1], [14, 10 | (2 << 4)], [15, 9 | (3 << 4)]):
+        assert np.array_equal(planned(x, plan), ref), plan
 
 
 def test_involution_and_linearity():
