@@ -169,7 +169,18 @@ int visit_pass(const Pass& p, F&& f) {
     }
 }
 
-int high_default_q(int r) { return r <= 8 ? 0 : r == 9 ? 1 : 2; }
+// Cluster size of a high pass by default: 9 and 10 stages run on a cluster
+// of 2 (a 2^14 tile keeps 256-/128-byte row segments); the 4-CTA shapes
+// are kept for tests and experiments (measured slower).
+int high_default_q(int r) { return r <= 8 ? 0 : 1; }
+
+// Relative cost of a pass shape beyond its HBM round trip (measured on
+// B200, profiles/: a 2-CTA low pass runs at ~90% of the 1-CTA one, 10-stage
+// high passes at ~85%, 4-CTA low passes at ~70%).
+int pass_cost(bool low, int w) {
+    if (low) return w == 13 ? 0 : w == 14 ? 1 : 5;
+    return w == 10 ? 2 : 0;
+}
 
 // BW_PLAN="13,10,9" overrides the default plan for a matching n
 // (experiment knob; the checker and tests cover every legal plan).
@@ -205,11 +216,11 @@ int default_plan(int n, std::vector<int>* widths) {
         const int h = n - w0;
         const int q = (h + bw::kMaxHighBits - 1) / bw::kMaxHighBits;
         std::vector<int> w{w0};
-        int cost = (1 + q) * 100 + (w0 - 13);
+        int cost = (1 + q) * 100 + pass_cost(true, w0);
         for (int i = 0; i < q; ++i) {
             const int r = h / q + (i < h % q ? 1 : 0);
             w.push_back(r);
-            cost += r <= bw::kRegOnlyMaxBits ? 0 : high_default_q(r);
+            cost += pass_cost(false, r);
         }
         if (cost < best_cost) {
             best_cost = cost;
@@ -275,7 +286,7 @@ int set_all_pass_attributes() {
     return for_all_pass_kernels([](auto t, auto l) -> int {
         using C = typename decltype(t)::type;
         constexpr int L = decltype(l)::value;
-        constexpr int smem = bw::Dims<C>::SMEM_ELEMS * 8;
+        constexpr int smem = bw::Dims<C>::SMEM_BYTES;
         if (smem > 48 * 1024)
             BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         return BW_OK;
@@ -293,13 +304,13 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s) {
         constexpr int L = decltype(l)::value;
         const unsigned grid = (unsigned)(1ull << (n - bw::kCtaBits));
         if constexpr (C::Q == 0) {
-            bw::k_pass<C, L><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_ELEMS * 8, s>>>(d, p.k);
+            bw::k_pass<C, L><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k);
             BW_LAUNCHED("fwht pass launch");
         } else {
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(grid);
             cfg.blockDim = dim3(bw::Dims<C>::NT);
-            cfg.dynamicSmemBytes = bw::Dims<C>::SMEM_ELEMS * 8;
+            cfg.dynamicSmemBytes = bw::Dims<C>::SMEM_BYTES;
             cfg.stream = s;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -787,7 +798,7 @@ int bw_plan_describe(int log2n, int log2p, char* json, size_t len) {
                 using C = typename decltype(t)::type;
                 constexpr int L = decltype(l)::value;
                 threads = bw::Dims<C>::NT;
-                smem = bw::Dims<C>::SMEM_ELEMS * 8;
+                smem = bw::Dims<C>::SMEM_BYTES;
                 cols = L;
                 tbits = C::T;
                 cluster = bw::Dims<C>::CLUSTER;

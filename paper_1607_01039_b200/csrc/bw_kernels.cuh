@@ -114,28 +114,55 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void st_cluster_u64(uint32_t addr, u64 v) {
     asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
 }
+// Remote store that also signals `bytes` of transaction completion on the
+// destination CTA's mbarrier (no fence, no cluster-wide barrier needed).
+__device__ __forceinline__ void st_async_u64(uint32_t addr, u64 v, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr), "l"(v),
+                 "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t mbar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(mbar), "r"(parity)
+            : "memory");
+    }
+}
 
 // Exchange transpose: registers of round RD (pre space) -> the post-space
 // slots of the CTA that owns each element after the exchange.  The owner is
 // given by the element's bits at positions P(i), which are register bits of
 // round RD, so every destination is a compile-time choice per register.
+// Elements staying in this CTA use plain shared stores; the others go out as
+// st.async, which counts their bytes on the receiver's mbarrier.
 template <class C, int RD>
 __device__ __forceinline__ void exchange_write(const u64 (&v)[Dims<C>::E], u64* sm, uint32_t tp, uint32_t rank) {
     constexpr uint32_t pm = p_mask<C>();
     constexpr int NQ = 1 << C::Q;
-    const uint32_t base_local = (uint32_t)__cvta_generic_to_shared(sm) +
-                                8u * (smem_slot(to_local<C, C::XR>(tp)) +
-                                      smem_slot(to_local<C, C::XR>(rank << kCtaBits)));
-    uint32_t base[NQ];
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
+    const uint32_t off = 8u * (smem_slot(to_local<C, C::XR>(tp)) + smem_slot(to_local<C, C::XR>(rank << kCtaBits)));
+    const uint32_t mbar_local = sbase + 8u * Dims<C>::SMEM_ELEMS;
+    uint32_t base[NQ], mbar[NQ];
 #pragma unroll
-    for (int d = 0; d < NQ; ++d) base[d] = map_to_rank(base_local, (uint32_t)d);
+    for (int d = 0; d < NQ; ++d) {
+        base[d] = map_to_rank(sbase + off, (uint32_t)d);
+        mbar[d] = map_to_rank(mbar_local, (uint32_t)d);
+    }
 #pragma unroll
     for (int j = 0; j < Dims<C>::E; ++j) {
         const uint32_t rp = reg_part<C, RD>(j);
         uint32_t d = 0;
 #pragma unroll
         for (int i = 0; i < C::Q; ++i) d |= ((rp >> C::P(i)) & 1u) << i;
-        st_cluster_u64(base[d] + 8u * smem_slot(to_local<C, C::XR>(rp & ~pm)), v[j]);
+        const uint32_t slot_off = 8u * smem_slot(to_local<C, C::XR>(rp & ~pm));
+        if (d == rank) {
+            sm[(off + slot_off) / 8u] = v[j];
+        } else {
+            st_async_u64(base[d] + slot_off, v[j], mbar[d]);
+        }
     }
 }
 
@@ -150,7 +177,8 @@ __device__ __forceinline__ void run_rounds(u64 (&v)[Dims<C>::E], u64* sm, uint32
             // loads); no smem has been read yet, so no WAR hazard exists.
             asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
             exchange_write<C, RD - 1>(v, sm, thread_part<C, RD - 1>(lane, warp), rank);
-            cluster_sync_all();  // every remote write has landed
+            __syncthreads();  // this CTA's own stores
+            mbar_wait_parity((uint32_t)__cvta_generic_to_shared(sm + Dims<C>::SMEM_ELEMS), 0u);  // remote bytes
         } else {
             if constexpr (RD > 1) __syncthreads();
             store_smem<C, RD - 1>(v, sm, thread_part<C, RD - 1>(lane, warp));
@@ -182,6 +210,18 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     }
     u64* g = data + tile_base<T, L>(tile, k);
 
+    if constexpr (C::Q > 0) {
+        // mbarrier counting the bytes the partners will deliver to this CTA;
+        // made visible cluster-wide before the (relaxed) cluster arrive.
+        if (threadIdx.x == 0) {
+            const uint32_t mb = (uint32_t)__cvta_generic_to_shared(sm + Dims<C>::SMEM_ELEMS);
+            constexpr uint32_t bytes_in = 8u * (Dims<C>::CTA - Dims<C>::CTA / Dims<C>::CLUSTER);
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes_in) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
     u64 v[E];
     load_global<C, 0, T, L>(v, g, thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
     if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");

@@ -159,6 +159,9 @@ struct Dims {
     static constexpr int CTA = 1 << kCtaBits;         // elements per CTA
     static constexpr int SMEM_ELEMS = C::NR > 1 ? CTA + (CTA >> 5) : 0;
     static constexpr int CLUSTER = 1 << C::Q;
+    // dynamic shared memory: the transpose buffer, plus one mbarrier for the
+    // DSMEM exchange of cluster configs
+    static constexpr int SMEM_BYTES = SMEM_ELEMS * 8 + (C::Q > 0 ? 8 : 0);
 };
 
 // Padded shared-memory slot of local index e; additive over disjoint bit sets.
