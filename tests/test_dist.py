@@ -1,0 +1,121 @@
+"""Multi-process sharded transform (parallel.py:87-198 with m = P ranks).
+
+* CPU (gloo, world size 2 and 4): the all-to-all orchestration of
+  ``sharded.fwht_distributed(mode="a2a")`` with the CPU oracle plugged in as
+  the compute backend (test-only), checked against the oracle's full
+  transform.
+* GPU (one device, 2 processes, gloo for the host barriers): the CUDA-IPC
+  peer path -- each process maps the other's shard and runs kernel K6 on its
+  own slice in place.  No kernel waits on another, so two ranks on one GPU
+  are safe.
+"""
+
+import ctypes
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+class OracleBackend:
+    """Test-only compute backend: the CPU oracle on CPU tensors."""
+
+    def __init__(self):
+        from oracle import load_c
+
+        self.lib = load_c()
+
+    def local_fwht(self, t):
+        a = t.numpy()
+        self.lib.oracle_fwht_i64(a.ctypes.data, int(a.size).bit_length() - 1)
+
+    def xshard_slots(self, slots, p):
+        rows = slots.numpy()  # [P, m] view, modified in place
+        for b in range(p):  # ascending stage order (parallel.py:103-110)
+            step = 1 << b
+            for r in range(rows.shape[0]):
+                if not (r >> b) & 1:
+                    a = rows[r].copy()
+                    c = rows[r + step].copy()
+                    rows[r] = a + c
+                    rows[r + step] = a - c
+
+    def sync(self, t):
+        pass
+
+
+def _a2a_worker(rank, world, port, n, out_dir):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from oracle import oracle_np
+    from paper_1607_01039_b200 import sharded
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    p = world.bit_length() - 1
+    nl = n - p
+    x = oracle_np.gen(2, 99, [1 << 20], rank << nl, 1 << nl)
+    t = torch.from_numpy(x.copy())
+    bf = sharded.fwht_distributed(t, mode="a2a", backend=OracleBackend())
+    assert bf == n << (n - 1)
+    np.save(os.path.join(out_dir, f"shard{rank}.npy"), t.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_a2a_orchestration_gloo(tmp_path, coracle, world):
+    from oracle import oracle_np
+
+    n = 12
+    mp.spawn(_a2a_worker, args=(world, free_port(), n, str(tmp_path)), nprocs=world, join=True)
+    got = np.concatenate([np.load(tmp_path / f"shard{r}.npy") for r in range(world)])
+    ref = oracle_np.gen(2, 99, [1 << 20], 0, 1 << n)
+    coracle.oracle_fwht_i64(ref.ctypes.data, n)
+    assert np.array_equal(got, ref)
+
+
+def _peer_worker(rank, world, port, n, out_dir):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from oracle import oracle_np
+    from paper_1607_01039_b200 import sharded
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    p = world.bit_length() - 1
+    nl = n - p
+    x = oracle_np.gen(2, 7, [1 << 20], rank << nl, 1 << nl)
+    t = torch.from_numpy(x).cuda()
+    bf = sharded.fwht_distributed(t, mode="peer")
+    assert bf == n << (n - 1)
+    np.save(os.path.join(out_dir, f"shard{rank}.npy"), t.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_peer_ipc_two_processes_one_gpu(tmp_path, coracle):
+    from oracle import oracle_np
+
+    n, world = 20, 2
+    mp.spawn(_peer_worker, args=(world, free_port(), n, str(tmp_path)), nprocs=world, join=True)
+    got = np.concatenate([np.load(tmp_path / f"shard{r}.npy") for r in range(world)])
+    ref = oracle_np.gen(2, 7, [1 << 20], 0, 1 << n)
+    coracle.oracle_fwht_i64(ref.ctypes.data, n)
+    assert np.array_equal(got, ref)
