@@ -138,12 +138,12 @@ __device__ __forceinline__ void mbar_wait_parity(uint32_t mbar, uint32_t parity)
 // round RD, so every destination is a compile-time choice per register.
 // Elements staying in this CTA use plain shared stores; the others go out as
 // st.async, which counts their bytes on the receiver's mbarrier.
-template <class C, int RD>
-__device__ __forceinline__ void exchange_write(const u64 (&v)[Dims<C>::E], u64* sm, uint32_t tp, uint32_t rank) {
+template <class C, int RD, int RANK>
+__device__ __forceinline__ void exchange_write_rank(const u64 (&v)[Dims<C>::E], u64* sm, uint32_t tp) {
     constexpr uint32_t pm = p_mask<C>();
     constexpr int NQ = 1 << C::Q;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
-    const uint32_t off = 8u * (smem_slot(to_local<C, C::XR>(tp)) + smem_slot(to_local<C, C::XR>(rank << kCtaBits)));
+    const uint32_t off = 8u * (smem_slot(to_local<C, C::XR>(tp)) + smem_slot(to_local<C, C::XR>(RANK << kCtaBits)));
     const uint32_t mbar_local = sbase + 8u * Dims<C>::SMEM_ELEMS;
     uint32_t base[NQ], mbar[NQ];
 #pragma unroll
@@ -151,17 +151,42 @@ __device__ __forceinline__ void exchange_write(const u64 (&v)[Dims<C>::E], u64* 
         base[d] = map_to_rank(sbase + off, (uint32_t)d);
         mbar[d] = map_to_rank(mbar_local, (uint32_t)d);
     }
+    u64* local = sm + off / 8u;
+    // Remote stores first (their latency overlaps the local ones), then the
+    // registers that stay in this CTA.  d is a compile-time value per j.
 #pragma unroll
-    for (int j = 0; j < Dims<C>::E; ++j) {
-        const uint32_t rp = reg_part<C, RD>(j);
-        uint32_t d = 0;
+    for (int pass = 0; pass < 2; ++pass) {
 #pragma unroll
-        for (int i = 0; i < C::Q; ++i) d |= ((rp >> C::P(i)) & 1u) << i;
-        const uint32_t slot_off = 8u * smem_slot(to_local<C, C::XR>(rp & ~pm));
-        if (d == rank) {
-            sm[(off + slot_off) / 8u] = v[j];
-        } else {
-            st_async_u64(base[d] + slot_off, v[j], mbar[d]);
+        for (int j = 0; j < Dims<C>::E; ++j) {
+            const uint32_t rp = reg_part<C, RD>(j);
+            uint32_t d = 0;
+#pragma unroll
+            for (int i = 0; i < C::Q; ++i) d |= ((rp >> C::P(i)) & 1u) << i;
+            const uint32_t slot = smem_slot(to_local<C, C::XR>(rp & ~pm));
+            if (pass == 1 && d != (uint32_t)RANK) st_async_u64(base[d] + 8u * slot, v[j], mbar[d]);
+            if (pass == 0 && d == (uint32_t)RANK) local[slot] = v[j];
+        }
+    }
+}
+
+// Exchange transpose: registers of round RD (pre space) -> the post-space
+// slots of the CTA that owns each element after the exchange.  The owner is
+// given by the element's bits at positions P(i), which are register bits of
+// round RD, so every destination is a compile-time choice per register; the
+// code is specialised per cluster rank so no store needs a runtime branch.
+// Elements staying in this CTA use plain shared stores; the others go out as
+// st.async, which counts their bytes on the receiver's mbarrier.
+template <class C, int RD>
+__device__ __forceinline__ void exchange_write(const u64 (&v)[Dims<C>::E], u64* sm, uint32_t tp, uint32_t rank) {
+    if constexpr (C::Q == 1) {
+        if (rank == 0) exchange_write_rank<C, RD, 0>(v, sm, tp);
+        else exchange_write_rank<C, RD, 1>(v, sm, tp);
+    } else if constexpr (C::Q == 2) {
+        switch (rank) {
+            case 0: exchange_write_rank<C, RD, 0>(v, sm, tp); break;
+            case 1: exchange_write_rank<C, RD, 1>(v, sm, tp); break;
+            case 2: exchange_write_rank<C, RD, 2>(v, sm, tp); break;
+            default: exchange_write_rank<C, RD, 3>(v, sm, tp); break;
         }
     }
 }
