@@ -153,6 +153,24 @@ int bw_fwht_host_i64(int64_t *host, int log2n, int64_t *work_dev,
  */
 int bw_inverse_i64(int64_t *data, int log2n, int64_t *scratch_dev, void *stream);
 
+/*
+ * wht_bruteforce (core.py:128-144): y_i = sum_j (-1)^popcount(i & j) x_j by
+ * the defining double sum, O(4^n), out of place (x unchanged).  The Python
+ * layer enforces the reference's oracle limit (14 by default); the ABI
+ * accepts n <= 20.  Asynchronous.
+ */
+int bw_wht_bruteforce_i64(const int64_t *x, int64_t *y, int log2n, void *stream);
+
+/*
+ * parseval_energy (core.py:176-185) building block: the exact sum of x^2
+ * over x[0..count) as nblocks partial 192-bit integers, written to
+ * partial_dev[3*b + {0,1,2}] = (low, middle, high) 64-bit words.  The sum of
+ * all partials is the exact energy (beyond int64, as the reference's Python
+ * int arithmetic).  Asynchronous.
+ */
+int bw_sumsq_partials_i64(const int64_t *x, uint64_t count, uint64_t *partial_dev,
+                          int nblocks, void *stream);
+
 /* ---- multi-device / sharded path (parallel.py:87-111 with m = P devices) */
 
 /*

@@ -18,6 +18,8 @@ from .core import (
     fwht_array,
     fwht_inplace,
     inverse_wht_inplace,
+    parseval_energy,
+    wht_bruteforce,
 )
 from .errors import (
     BadArguments,
@@ -25,6 +27,7 @@ from .errors import (
     DeviceError,
     InexactDivision,
     InvalidWorkerCount,
+    OracleTooLarge,
     OverflowBoundError,
     ValidationError,
 )
@@ -40,6 +43,8 @@ __all__ = [
     "fwht_array",
     "fwht_inplace",
     "inverse_wht_inplace",
+    "parseval_energy",
+    "wht_bruteforce",
     "extract_above",
     "extract_ge",
     "extract_gt",
@@ -49,6 +54,7 @@ __all__ = [
     "DeviceError",
     "InexactDivision",
     "InvalidWorkerCount",
+    "OracleTooLarge",
     "OverflowBoundError",
     "ValidationError",
     "__version__",

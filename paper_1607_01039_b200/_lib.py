@@ -54,6 +54,8 @@ _SIGNATURES = {
     "bw_fwht_host_i64": ([P, I32, P, I32, P, PU64], I32),
     "bw_inverse_i64": ([P, I32, P, P], I32),
     "bw_inverse_f64": ([P, I32, P], I32),
+    "bw_wht_bruteforce_i64": ([P, P, I32, P], I32),
+    "bw_sumsq_partials_i64": ([P, U64, P, I32, P], I32),
     "bw_xshard_i64": ([ctypes.POINTER(P), I32, U64, U64, P], I32),
     "bw_xshard_strided_i64": ([P, U64, I32, U64, U64, P], I32),
     "bw_ipc_get_handle": ([P, P, PU64], I32),

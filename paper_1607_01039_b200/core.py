@@ -22,7 +22,10 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import BadArguments, DeviceError, OverflowBoundError
+from .errors import BadArguments, DeviceError, OracleTooLarge, OverflowBoundError
+
+# Brute force costs O(4**n); core.py:24-27 uses the same default limit.
+ORACLE_LIMIT_DEFAULT = 14
 
 _INT64_LIMIT = 1 << 63
 
@@ -282,6 +285,48 @@ def inverse_wht_inplace(sig: Signal) -> Signal:
             host[...] = buf.cpu().numpy()
     sig.domain = Domain.TIME
     return sig
+
+
+def _device_copy(buf) -> torch.Tensor:
+    if isinstance(buf, torch.Tensor):
+        _require_cuda(buf)
+        return buf
+    _need_cuda()
+    return torch.from_numpy(np.ascontiguousarray(buf)).cuda()
+
+
+def wht_bruteforce(sig: Signal, limit: int = ORACLE_LIMIT_DEFAULT) -> Signal:
+    """Reference transform by the defining double sum (core.py:128-144);
+    input unchanged, result returned as a new Signal of the same kind
+    (torch CUDA or numpy) with the domain flipped.  O(4**n) on the GPU."""
+    n = sig.log2_dim
+    if n > limit:
+        raise OracleTooLarge(f"n = {n} exceeds the oracle limit {limit}")
+    if not sig.is_exact:
+        raise BadArguments("the device brute force is implemented for int64 signals")
+    check_magnitude_bound(sig.data, n)
+    x = _device_copy(sig.data)
+    y = torch.empty_like(x)
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.lib().bw_wht_bruteforce_i64(x.data_ptr(), y.data_ptr(), n, _stream_handle(x)))
+    out = y if isinstance(sig.data, torch.Tensor) else y.cpu().numpy()
+    return Signal(out, _flip(sig.domain))
+
+
+def parseval_energy(sig: Signal):
+    """Sum of squared components (core.py:176-185).  int64: exact (Python
+    int, beyond 2**63), from 192-bit partial sums computed on the GPU.
+    float64: float."""
+    x = _device_copy(sig.data)
+    if not sig.is_exact:
+        return float(torch.dot(x, x).item())
+    nblocks = 592
+    part = torch.empty(3 * nblocks, dtype=torch.int64, device=x.device)
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.lib().bw_sumsq_partials_i64(x.data_ptr(), x.numel(), part.data_ptr(), nblocks,
+                                                    _stream_handle(x)))
+    words = [w & ((1 << 64) - 1) for w in part.cpu().tolist()]
+    return sum(words[3 * b] + (words[3 * b + 1] << 64) + (words[3 * b + 2] << 128) for b in range(nblocks))
 
 
 def butterfly_count(n: int) -> int:

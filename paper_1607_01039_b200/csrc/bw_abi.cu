@@ -586,6 +586,32 @@ int bw_inverse_i64(int64_t* data, int log2n, int64_t* scratch_dev, void* stream)
     return BW_OK;
 }
 
+// wht_bruteforce (core.py:128-144): out of place, n <= limit (default 14).
+int bw_wht_bruteforce_i64(const int64_t* x, int64_t* y, int log2n, void* stream) {
+    BW_TRY(check_signal(x, log2n));
+    BW_TRY(check_signal(y, log2n));
+    if (log2n > 20) return fail(BW_BAD_ARGUMENTS, "brute force is O(4^n); n = %d is too large", log2n);
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    const uint32_t N = 1u << log2n;
+    bw::k_bruteforce<<<(N + 255) / 256, 256, 0, as_stream(stream)>>>(reinterpret_cast<const long long*>(x),
+                                                                       reinterpret_cast<long long*>(y), log2n);
+    BW_LAUNCHED("k_bruteforce launch");
+    return BW_OK;
+}
+
+// parseval_energy partial sums (core.py:176-185): writes nblocks x (lo, hi,
+// top) 64-bit words of the exact sum of squares; the caller adds them.
+int bw_sumsq_partials_i64(const int64_t* x, uint64_t count, uint64_t* partial_dev, int nblocks, void* stream) {
+    if (!x || !partial_dev || nblocks < 1 || count == 0) return fail(BW_BAD_ARGUMENTS, "bad arguments");
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    bw::k_sumsq<<<nblocks, 256, 0, as_stream(stream)>>>(reinterpret_cast<const long long*>(x), count,
+                                                        reinterpret_cast<unsigned long long*>(partial_dev));
+    BW_LAUNCHED("k_sumsq launch");
+    return BW_OK;
+}
+
 // Cross-shard butterfly (parallel.py:103-110, all log2 P stage phases fused).
 static int xshard_launch(const bw::ShardPtrs& sp, int log2p, uint64_t begin, uint64_t count, cudaStream_t s) {
     int dev = 0;

@@ -564,6 +564,63 @@ __global__ void __launch_bounds__(512) k_extract_write(const long long* __restri
 }
 
 // ---------------------------------------------------------------------------
+// wht_bruteforce (core.py:128-144): y_i = sum_j (-1)^popcount(i & j) x_j,
+// O(4^n), out of place; the "oracle of the oracle" for n <= 14.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_bruteforce(const long long* __restrict__ x, long long* __restrict__ y,
+                                                    int n) {
+    __shared__ long long xs[2048];
+    const uint32_t N = 1u << n;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    u64 acc = 0;
+    for (uint32_t j0 = 0; j0 < N; j0 += 2048) {
+        const uint32_t m = min(2048u, N - j0);
+        __syncthreads();
+        for (uint32_t t = threadIdx.x; t < m; t += blockDim.x) xs[t] = x[j0 + t];
+        __syncthreads();
+        if (i < N)
+            for (uint32_t t = 0; t < m; ++t) {
+                const u64 v = (u64)xs[t];
+                acc += (__popc(i & (j0 + t)) & 1) ? (u64)0 - v : v;
+            }
+    }
+    if (i < N) y[i] = (long long)acc;
+}
+
+// parseval_energy (core.py:176-185), exact for int64: every thread sums x^2
+// as a 192-bit integer (x^2 < 2^127), blocks write (lo, hi, top) partials.
+__global__ void __launch_bounds__(256) k_sumsq(const long long* __restrict__ x, uint64_t count,
+                                               unsigned long long* partial) {
+    unsigned __int128 acc = 0;
+    unsigned long long top = 0;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += nth) {
+        const long long v = x[i];
+        const unsigned long long a = v < 0 ? 0ull - (unsigned long long)v : (unsigned long long)v;
+        const unsigned __int128 sq = (unsigned __int128)a * a;
+        acc += sq;
+        top += acc < sq;
+    }
+    __shared__ unsigned long long s_lo[256], s_hi[256], s_top[256];
+    s_lo[threadIdx.x] = (unsigned long long)acc;
+    s_hi[threadIdx.x] = (unsigned long long)(acc >> 64);
+    s_top[threadIdx.x] = top;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned __int128 sum = 0;
+        unsigned long long t = 0;
+        for (int k = 0; k < (int)blockDim.x; ++k) {
+            const unsigned __int128 p = ((unsigned __int128)s_hi[k] << 64) | s_lo[k];
+            sum += p;
+            t += (sum < p) + s_top[k];
+        }
+        partial[3 * blockIdx.x + 0] = (unsigned long long)sum;
+        partial[3 * blockIdx.x + 1] = (unsigned long long)(sum >> 64);
+        partial[3 * blockIdx.x + 2] = t;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Elementwise helpers for the inverse transform (core.py:147-173).
 // ---------------------------------------------------------------------------
 __global__ void k_check_divisible(const long long* __restrict__ data, uint64_t count, int n, int* flag) {

@@ -318,3 +318,44 @@ def test_xshard_strided_matches_per_pointer():
                                                 torch.cuda.current_stream().cuda_stream))
     sharded.xshard(list(b.view(8, 1 << 13).unbind(0)))
     assert torch.equal(a, b)
+
+
+# ------------------------------------------------- oracle + energy (GPU) ---
+
+def test_bruteforce_matches_reference(golden_npz, golden):
+    z = golden_npz("c01_vectors.npz")
+    for i in range(44):
+        x = z[f"x{i}"]
+        sig = bw.Signal(dev(x))
+        out = bw.wht_bruteforce(sig)
+        assert np.array_equal(out.data.cpu().numpy(), z[f"y{i}"])
+        assert out.domain == bw.Domain.WALSH and np.array_equal(sig.data.cpu().numpy(), x)
+    # numpy input returns numpy (reference type), known answer (test_core.py:48-55)
+    assert bw.wht_bruteforce(bw.Signal(np.array([1, 2, 3, 4], dtype=np.int64))).data.tolist() == [10, -2, -4, 0]
+    with pytest.raises(errors.OracleTooLarge):
+        bw.wht_bruteforce(bw.Signal(dev(np.zeros(16, dtype=np.int64))), limit=3)
+    with pytest.raises(errors.OverflowBoundError):
+        bw.wht_bruteforce(bw.Signal(dev(np.array([1 << 61, 0, 0, 0], dtype=np.int64))))
+    x = oracle_np.gen(2, 5, [1 << 20], 0, 1 << 14)
+    assert np.array_equal(bw.wht_bruteforce(bw.Signal(dev(x))).data.cpu().numpy(), oracle_np.wht_bruteforce(x))
+
+
+def test_parseval_exact():
+    E = bw.parseval_energy
+    assert E(bw.Signal(dev(np.array([1, 1, 1, 1], dtype=np.int64)))) == 4
+    assert E(bw.Signal(dev(np.array([10, -2, -4, 0], dtype=np.int64)))) == 120
+    assert E(bw.Signal(dev(np.zeros(8, dtype=np.int64)))) == 0
+    assert E(bw.Signal(dev(np.array([1 << 40] * 4, dtype=np.int64)))) == 4 * (1 << 80)  # beyond int64
+    assert E(bw.Signal(dev(np.array([np.iinfo(np.int64).min, 3], dtype=np.int64)))) == (1 << 126) + 9
+    for n in (0, 3, 8, 14, 20):
+        x = oracle_np.gen(2, 70 + n, [1 << 20], 0, 1 << n)
+        sig = bw.Signal(dev(x))
+        before = E(sig)
+        assert before == sum(int(v) * int(v) for v in x.tolist())
+        bw.fwht_inplace(sig)
+        assert E(sig) == before * (1 << n)  # Parseval, exactly (test_core.py:195-202)
+    xf = np.random.default_rng(6).normal(size=1 << 10)
+    sig = bw.Signal(dev(xf))
+    before = E(sig)
+    bw.fwht_inplace(sig)
+    assert E(sig) == pytest.approx(before * (1 << 10), rel=1e-9)
