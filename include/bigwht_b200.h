@@ -252,6 +252,16 @@ int bw_extract_ge_i64(const int64_t *data, int log2n, uint64_t tau,
                       uint64_t *count);
 uint64_t bw_extract_scratch_bytes(int log2n);
 
+/*
+ * The transform followed by the extraction, with the threshold test fused
+ * into the last pass's epilogue (no extra read of the signal): equivalent to
+ * bw_fwht_i64 then bw_extract_ge_i64 -- the BASELINE configs 3 and 5
+ * workload.  Hits come back sorted by index.  Synchronous.
+ */
+int bw_fwht_extract_i64(int64_t *data, int log2n, uint64_t tau, uint64_t base,
+                        int64_t *out_idx, int64_t *out_val, uint64_t cap,
+                        void *stream, uint64_t *count);
+
 /* ---- planner ----------------------------------------------------------- */
 
 /*

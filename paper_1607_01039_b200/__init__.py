@@ -31,7 +31,7 @@ from .errors import (
     OverflowBoundError,
     ValidationError,
 )
-from .extract import extract_above, extract_ge, extract_gt
+from .extract import extract_above, extract_ge, extract_gt, fwht_extract_ge, fwht_extract_gt
 
 __version__ = "0.1.0"
 
@@ -48,6 +48,8 @@ __all__ = [
     "extract_above",
     "extract_ge",
     "extract_gt",
+    "fwht_extract_ge",
+    "fwht_extract_gt",
     "errors",
     "BadArguments",
     "BigWHTError",

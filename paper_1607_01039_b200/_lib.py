@@ -65,6 +65,7 @@ _SIGNATURES = {
     "bw_gen_i64": ([P, I32, I32, U64, PU64, I32, P], I32),
     "bw_gen_range_i64": ([P, U64, U64, I32, U64, PU64, I32, P], I32),
     "bw_extract_ge_i64": ([P, I32, U64, U64, P, P, U64, P, P, PU64], I32),
+    "bw_fwht_extract_i64": ([P, I32, U64, U64, P, P, U64, P, PU64], I32),
     "bw_extract_scratch_bytes": ([I32], U64),
     "bw_plan_describe": ([I32, I32, ctypes.c_char_p, ctypes.c_size_t], I32),
     "bw_debug_emulate_i64": ([P, I32, ctypes.POINTER(I32), I32], I32),

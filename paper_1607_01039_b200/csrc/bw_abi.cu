@@ -293,7 +293,9 @@ int set_all_pass_attributes() {
     });
 }
 
-int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s) {
+int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractArgs* exp = nullptr) {
+    bw::ExtractArgs ex = {};
+    if (exp) ex = *exp;
     if (p.kind == SMALL) {
         bw::k_small<u64><<<1, 256, (size_t)(8ull << n), s>>>(d, n);
         BW_LAUNCHED("k_small launch");
@@ -304,7 +306,7 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s) {
         constexpr int L = decltype(l)::value;
         const unsigned grid = (unsigned)(1ull << (n - bw::kCtaBits));
         if constexpr (C::Q == 0) {
-            bw::k_pass<C, L><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k);
+            bw::k_pass<C, L><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k, ex);
             BW_LAUNCHED("fwht pass launch");
         } else {
             cudaLaunchConfig_t cfg = {};
@@ -319,7 +321,7 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s) {
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L>, d, p.k));
+            BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L>, d, p.k, ex));
         }
         return BW_OK;
     });
@@ -758,6 +760,51 @@ int bw_gen_i64(int64_t* data, int log2n, int kind, uint64_t seed, const uint64_t
                void* stream) {
     BW_TRY(check_signal(data, log2n));
     return bw_gen_range_i64(data, 0, 1ull << log2n, kind, seed, params, nparams, stream);
+}
+
+// Transform + extraction fused into the last pass (configs 3/5 of
+// BASELINE.json: fwht, then all |W| >= tau sorted by index).
+int bw_fwht_extract_i64(int64_t* data, int log2n, uint64_t tau, uint64_t base, int64_t* out_idx,
+                        int64_t* out_val, uint64_t cap, void* stream, uint64_t* count) {
+    BW_TRY(check_signal(data, log2n));
+    if (cap > 0 && (!out_idx || !out_val)) return fail(BW_BAD_ARGUMENTS, "null output arrays");
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    cudaStream_t s = as_stream(stream);
+    std::vector<int> w;
+    BW_TRY(default_plan(log2n, &w));
+    std::vector<Pass> passes;
+    BW_TRY(build_passes(log2n, w, &passes));
+    const bool fusable = !passes.empty() && passes.back().kind != SMALL && !(reinterpret_cast<uintptr_t>(data) & 15u);
+    if (!fusable) {
+        BW_TRY(fwht_impl(data, log2n, nullptr, false, s));
+        return bw_extract_ge_i64(data, log2n, tau, base, out_idx, out_val, cap, nullptr, stream, count);
+    }
+    void* sc = nullptr;
+    BW_TRY(scratch(dev, 64, &sc));
+    unsigned long long* dcount = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(sc) + 48);
+    BW_CUDA(cudaMemsetAsync(dcount, 0, sizeof(unsigned long long), s));
+    bw::ExtractArgs ex = {tau, base, reinterpret_cast<long long*>(out_idx), reinterpret_cast<long long*>(out_val),
+                          dcount, cap};
+    u64* d = reinterpret_cast<u64*>(data);
+    for (size_t i = 0; i < passes.size(); ++i)
+        BW_TRY(launch_pass(passes[i], d, log2n, s, i + 1 == passes.size() ? &ex : nullptr));
+    unsigned long long total = 0;
+    BW_CUDA(cudaMemcpyAsync(&total, dcount, sizeof total, cudaMemcpyDeviceToHost, s));
+    BW_CUDA(cudaStreamSynchronize(s));
+    if (total <= cap && total <= 2048) {
+        if (total > 1) {
+            bw::k_sort_hits<<<1, 1024, 0, s>>>(reinterpret_cast<long long*>(out_idx), reinterpret_cast<long long*>(out_val),
+                                             dcount);
+            BW_LAUNCHED("k_sort_hits launch");
+            BW_CUDA(cudaStreamSynchronize(s));
+        }
+        if (count) *count = total;
+        return BW_OK;
+    }
+    // Too many hits to sort in one CTA (or more than cap): ordered two-phase
+    // extraction over the transformed signal.
+    return bw_extract_ge_i64(data, log2n, tau, base, out_idx, out_val, cap, nullptr, stream, count);
 }
 
 uint64_t bw_extract_scratch_bytes(int log2n) {

@@ -215,13 +215,61 @@ __device__ __forceinline__ void run_rounds(u64 (&v)[Dims<C>::E], u64* sm, uint32
     }
 }
 
+// Threshold extraction fused into the last pass (noisy.py:185-222 with
+// |x| >= tau): the final register values are tested before the store and
+// hits are appended (warp-aggregated) to an unordered list; bw_abi sorts
+// the few hits by index afterwards.  count == nullptr disables it.
+struct ExtractArgs {
+    unsigned long long tau;
+    unsigned long long base;  // index offset of element 0 (shards)
+    long long* idx;
+    long long* val;
+    unsigned long long* count;
+    unsigned long long cap;
+};
+
+__device__ __forceinline__ bool hit_ge_u(u64 x, unsigned long long tau) {
+    const u64 mag = (long long)x < 0 ? (u64)0 - x : x;
+    return mag >= tau;
+}
+
+template <class C, int RD, int T, int L>
+__device__ __forceinline__ void extract_hits(const u64 (&v)[Dims<C>::E], uint64_t gbase, uint32_t tp, int k,
+                                             const ExtractArgs& ex) {
+    constexpr int E = Dims<C>::E;
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < E; ++j) any |= hit_ge_u(v[j], ex.tau);
+    if (!__any_sync(0xffffffffu, any)) return;  // the common case: no hit in this warp
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t t0 = gbase + global_off<T, L>(tp, k);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        const bool h = hit_ge_u(v[j], ex.tau);
+        const unsigned b = __ballot_sync(0xffffffffu, h);
+        if (b) {
+            const int leader = __ffs(b) - 1;
+            unsigned long long first = 0;
+            if ((int)lane == leader) first = atomicAdd(ex.count, (unsigned long long)__popc(b));
+            first = __shfl_sync(0xffffffffu, first, leader);
+            if (h) {
+                const unsigned long long pos = first + __popc(b & ((1u << lane) - 1u));
+                if (pos < ex.cap) {
+                    ex.idx[pos] = (long long)(ex.base + t0 + global_off<T, L>(reg_part<C, RD>(j), k));
+                    ex.val[pos] = (long long)v[j];
+                }
+            }
+        }
+    }
+}
+
 // One pass over every tile: load (round 0 layout) -> stages -> [transpose ->
 // stages]* -> store (last round layout).  k = first global stage bit of the
 // rows (ignored for L == T).  Cluster configs (Q > 0) put 2^Q CTAs on one
 // tile; grid = 2^(n-13) CTAs for every config.
 template <class C, int L>
 __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
-    k_pass(u64* __restrict__ data, int k) {
+    k_pass(u64* __restrict__ data, int k, ExtractArgs ex) {
     constexpr int T = C::T;
     constexpr int E = Dims<C>::E;
     extern __shared__ u64 sm[];
@@ -253,7 +301,43 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     apply_stages<C, 0, L>(v);
     run_rounds<C, L, 1>(v, sm, lane, warp, rank);
     constexpr int LAST = C::NR - 1;
-    store_global<C, LAST, T, L>(v, g, thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank), k);
+    const uint32_t tp_last = thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank);
+    if (ex.count != nullptr) extract_hits<C, LAST, T, L>(v, tile_base<T, L>(tile, k), tp_last, k, ex);
+    store_global<C, LAST, T, L>(v, g, tp_last, k);
+}
+
+// Sort the (few) fused-extraction hits by index in place: one CTA, bitonic
+// in shared memory, count <= 2048.
+__global__ void __launch_bounds__(1024) k_sort_hits(long long* idx, long long* val, const unsigned long long* count) {
+    __shared__ long long sk[2048], sv[2048];
+    const unsigned m = (unsigned)*count;
+    for (unsigned i = threadIdx.x; i < 2048; i += blockDim.x) {
+        sk[i] = i < m ? idx[i] : 0x7FFFFFFFFFFFFFFFll;
+        sv[i] = i < m ? val[i] : 0;
+    }
+    __syncthreads();
+    for (unsigned size = 2; size <= 2048; size <<= 1) {
+        for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+            for (unsigned i = threadIdx.x; i < 2048; i += blockDim.x) {
+                const unsigned jx = i ^ stride;
+                if (jx > i) {
+                    const bool up = (i & size) == 0;
+                    if ((sk[i] > sk[jx]) == up) {
+                        const long long a = sk[i], b = sv[i];
+                        sk[i] = sk[jx];
+                        sv[i] = sv[jx];
+                        sk[jx] = a;
+                        sv[jx] = b;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (unsigned i = threadIdx.x; i < m; i += blockDim.x) {
+        idx[i] = sk[i];
+        val[i] = sv[i];
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -57,6 +57,39 @@ def extract_ge(data, tau: int, base: int = 0, cap: int = 1 << 16):
         return idx[:k], val[:k]
 
 
+def fwht_extract_ge(data: torch.Tensor, tau: int, base: int = 0, cap: int = 1 << 16):
+    """Transform ``data`` in place (fwht_array) and return every hit with
+    |W| >= tau as (index, value) CUDA tensors sorted by index; the threshold
+    test runs in the last pass's epilogue (configs 3/5 of BASELINE.json)."""
+    if tau < 0:
+        raise BadArguments(f"tau must be >= 0, got {tau}")
+    _need_cuda()
+    if not isinstance(data, torch.Tensor) or not data.is_cuda or data.dtype != torch.int64:
+        raise BadArguments("fwht_extract needs a CUDA int64 tensor")
+    if not data.is_contiguous():
+        raise BadArguments("in-place transform needs a contiguous buffer")
+    n = _log2(data)
+    if data.numel() != 1 << n:
+        raise BadArguments(f"signal length {data.numel()} is not a power of two")
+    L = _lib.lib()
+    idx = torch.empty(max(cap, 1), dtype=torch.int64, device=data.device)
+    val = torch.empty(max(cap, 1), dtype=torch.int64, device=data.device)
+    count = ctypes.c_uint64(0)
+    with torch.cuda.device(data.device):
+        st = L.bw_fwht_extract_i64(data.data_ptr(), n, int(tau), int(base), idx.data_ptr(), val.data_ptr(), cap,
+                                   _stream_handle(data), ctypes.byref(count))
+    if st == _lib.BW_CAPACITY:  # the transform is done; re-extract with room
+        return extract_ge(data, tau, base, cap=int(count.value))
+    _lib.check(st)
+    k = int(count.value)
+    return idx[:k], val[:k]
+
+
+def fwht_extract_gt(data: torch.Tensor, tau: int, base: int = 0):
+    """Config semantics: transform, then |W| > tau sorted by index."""
+    return fwht_extract_ge(data, int(tau) + 1, base)
+
+
 def extract_gt(data, tau: int, base: int = 0):
     """Config semantics: |W| > tau, (index, value) sorted by index."""
     return extract_ge(data, int(tau) + 1, base)

@@ -57,13 +57,16 @@ def run_config(coracle, idx, n=None):
     if free < (8 << spec.n) + (1 << 30):
         pytest.skip(f"needs {(8 << spec.n) >> 30} GiB of free device memory")
     t = signals.make(spec)
-    assert bw.fwht_array(t) == spec.n << (spec.n - 1)
+    hits = None
+    if spec.threshold is not None:  # the configs' workload: transform + fused extraction
+        hits = bw.fwht_extract_gt(t, spec.threshold)
+        i2, v2 = bw.extract_gt(t, spec.threshold)  # two-step path on the same output
+        assert torch.equal(hits[0], i2) and torch.equal(hits[1], v2)
+    else:
+        assert bw.fwht_array(t) == spec.n << (spec.n - 1)
     rows = fold_map(spec.n, spec.masks, seed=spec.seed)
     rs = torch.from_numpy(oracle_np.row_space(rows)).cuda()
     got = t[rs].cpu().numpy()
-    hits = None
-    if spec.threshold is not None:
-        hits = bw.extract_gt(t, spec.threshold)
     del t
     torch.cuda.empty_cache()
     want = cpu_spot_check(coracle, spec, rows)

@@ -359,3 +359,31 @@ def test_parseval_exact():
     before = E(sig)
     bw.fwht_inplace(sig)
     assert E(sig) == pytest.approx(before * (1 << 10), rel=1e-9)
+
+
+def test_fused_extraction_matches_two_step():
+    """Extraction fused into the last pass == transform then ordered
+    extraction, for sparse hits, many hits (> 2048: fallback) and tau = 0."""
+    for n, tau in ((14, 0), (16, 3000), (20, 1 << 14), (22, 1 << 17), (23, 1 << 30), (24, 25000)):
+        x = oracle_np.gen(2, 40 + n, [1 << 10], 0, 1 << n)
+        a, b = dev(x), dev(x)
+        i1, v1 = bw.fwht_extract_ge(a, tau, cap=1 << 18)
+        bw.fwht_array(b)
+        i2, v2 = bw.extract_ge(b, tau, cap=1 << 18)
+        assert torch.equal(a, b), n
+        assert torch.equal(i1, i2) and torch.equal(v1, v2), (n, tau, i1.numel())
+    # too many hits for the capacity: still complete and ordered
+    x = oracle_np.gen(2, 3, [1 << 10], 0, 1 << 18)
+    a, b = dev(x), dev(x)
+    i1, v1 = bw.fwht_extract_ge(a, 0, cap=16)
+    bw.fwht_array(b)
+    assert torch.equal(i1, torch.arange(1 << 18, device="cuda")) and torch.equal(v1, b)
+
+
+def test_fused_extraction_configs(golden):
+    for key, idx in (("config3_n22", 3), ("config5_n22", 5)):
+        spec = signals.config(idx, n=22)
+        t = signals.make(spec)
+        i, v = bw.fwht_extract_gt(t, golden[key]["tau"])
+        assert digest(t.cpu().numpy()) == golden[key]["y_sha256"]
+        assert [[a, b] for a, b in zip(i.tolist(), v.tolist())] == sorted(golden[key]["hits"])
