@@ -4,12 +4,14 @@ at 2^n int64 on 1/2/4/8 B200 + HBM GB/s fraction of roofline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload: config 4 of BASELINE.json -- n = 32 int64 FWHT (32 GiB), seeded
-uniform +-1 input, natural order, unnormalised; strong scaling over the top
-log2(N) index bits for N > 1 (one process per GPU, torchrun).  A step is one
-full transform of the resident signal (fwht_array semantics: all passes, and
-for N > 1 the cross-GPU butterfly).  The 32 GiB input is far larger than the
-126 MB L2, so no L2 flush is needed between steps.
+Workload (default): config 4 of BASELINE.json -- n = 32 int64 FWHT (32 GiB),
+seeded uniform +-1 input, natural order, unnormalised; strong scaling over
+the top log2(N) index bits for N > 1 (one process per GPU, torchrun).  A step
+is one full transform of the resident signal (fwht_array semantics: all
+passes, and for N > 1 the cross-GPU butterfly).  The 32 GiB input is far
+larger than the 126 MB L2, so no L2 flush is needed between steps.
+--config 1..5 selects the other BASELINE configs (3 and 5 add the fused
+|W| > tau extraction to every step; 1 and 2 flush L2 between steps).
 
 --impl reference times the reference's own CPU algorithm (the oracle port of
 parallel.py run_parallel, numpy, all host cores) on a bounded sample of the
@@ -42,13 +44,24 @@ def args_parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=32, help="log2 of the transform size (config 4: 32)")
-    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE.json config (default 4: n=32 +-1, the strong-scaling config)")
+    ap.add_argument("--n", type=int, default=None, help="log2 size (default: the config's n)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--mode", choices=["peer", "a2a"], default="peer", help="cross-GPU exchange (N > 1)")
     return ap.parse_args()
+
+
+CONFIG_N = {1: 20, 2: 24, 3: 30, 4: 32, 5: 34}
+CONFIG_TEXT = {
+    1: "uniform +-1",
+    2: "uniform integers in [-2^20, 2^20]",
+    3: "noisy-sparse +-1 (secret s, e ~ Bernoulli(0.45)) + extraction |W| > 2^26 sorted by index",
+    4: "uniform +-1",
+    5: "noisy-sparse, 8 planted masks, e ~ Bernoulli(0.48) + extraction |W| > 2^29 sorted by index",
+}
 
 
 def world():
@@ -167,8 +180,8 @@ def run_reference(a):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": ws,
         "steps": len(times), "warmup": a.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": value / PUBLISHED_PTS, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"config{a.config}: n={a.n} int64 FWHT, uniform +-1, natural order, unnormalised",
-                   "n": a.n, "sample_n": n_s},
+        "config": {"workload": f"config{a.config}: n={a.n} int64 FWHT, {CONFIG_TEXT[a.config]}, natural order, "
+                               "unnormalised", "n": a.n, "sample_n": n_s},
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "host_cores": cores,
                          "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -182,7 +195,6 @@ def run_ours(a):
     import torch
     import torch.distributed as dist
 
-    import paper_1607_01039_b200 as bw
     from paper_1607_01039_b200 import _lib, sharded, signals
 
     ws, rank, local_rank = world()
@@ -208,13 +220,36 @@ def run_ours(a):
         ptrs = (ctypes.c_void_p * ws)(*(peer.ptrs if peer else [ptr] * ws))
         b, c = sharded.slice_of(rank, ws, 1 << nl)
 
+    # Configs 3 and 5: the step is the transform with the |W| > tau test
+    # fused into the last local pass, then the hits sorted by index.
+    extract = spec.threshold is not None and p == 0
+    if extract:
+        cap = 4096
+        hit_idx = torch.empty(cap, dtype=torch.int64, device="cuda")
+        hit_val = torch.empty(cap, dtype=torch.int64, device="cuda")
+        hit_cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        tau = spec.threshold + 1
+
+    # Inputs smaller than 4x L2 would stay cache resident between steps:
+    # flush L2 between steps (outside each step's events) for those.
+    flush = (8 << nl) < (512 << 20)
+    if flush:
+        scrub = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
     def device_barrier():
         dist.all_reduce(ones)  # NCCL on this stream: a device-side barrier
 
     def step(ev):
+        if extract:
+            hit_cnt.zero_()
         for i in range(npasses):
             ev[i].record(stream)
-            _lib.check(L.bw_fwht_i64_pass(ptr, nl, i, sh))
+            if extract and i == npasses - 1:
+                _lib.check(L.bw_fwht_i64_pass_extract(ptr, nl, i, tau, 0, hit_idx.data_ptr(), hit_val.data_ptr(),
+                                                      cap, hit_cnt.data_ptr(), sh))
+                _lib.check(L.bw_sort_hits_i64(hit_idx.data_ptr(), hit_val.data_ptr(), hit_cnt.data_ptr(), sh))
+            else:
+                _lib.check(L.bw_fwht_i64_pass(ptr, nl, i, sh))
         ev[npasses].record(stream)
         if p > 0:
             if a.mode == "peer":
@@ -240,8 +275,14 @@ def run_ours(a):
     def events():
         return [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
 
-    for _ in range(a.warmup):
+    hits_first = None
+    for w in range(a.warmup):
+        if extract:  # each transform doubles the data: restore the input between steps
+            signals.generate(spec, x, base=rank << nl)
         step(events())
+        if extract and w == 0:
+            k = int(hit_cnt.item())
+            hits_first = list(zip(hit_idx[:k].tolist(), hit_val[:k].tolist()))
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
@@ -253,12 +294,18 @@ def run_ours(a):
     if ws > 1:
         dist.barrier()
     for e in evs:
+        if extract:  # restore the config input (outside the step's events)
+            signals.generate(spec, x, base=rank << nl)
+        if flush:
+            scrub.fill_(1)
         step(e)
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     clk = clocks.stop()
-    total_ms = evs[0][0].elapsed_time(evs[-1][-1])
+    step_ms = [e[0].elapsed_time(e[-1]) for e in evs]
+    per_step = flush or extract  # something untimed runs between steps
+    total_ms = sum(step_ms) if per_step else evs[0][0].elapsed_time(evs[-1][-1])
     pass_ms = [[e[i].elapsed_time(e[i + 1]) for e in evs] for i in range(npasses)]
     xs_ms = [e[npasses + 1].elapsed_time(e[npasses + 2]) for e in evs] if p > 0 else []
     if ws > 1:
@@ -272,9 +319,8 @@ def run_ours(a):
     bytes_per_pass = 16 * (2 ** nl)
     dom = max(range(npasses), key=lambda i: avg_pass[i])
     achieved = bytes_per_pass / (avg_pass[dom] / 1e3) / 1e9
-    launches = a.steps * (npasses + (1 if p > 0 else 0))
+    launches = a.steps * (npasses + (1 if extract else 0) + (1 if p > 0 else 0))
 
-    # e2e: the public API on a pinned host buffer, H2D + transform + D2H per step.
     e2e = None
     if not a.no_e2e:
         e2e = run_e2e(a, x, spec, p, nl, rank, ws, peer)
@@ -284,12 +330,20 @@ def run_ours(a):
         "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": value / PUBLISHED_PTS,
         "vs_baseline_source": "PAPER.md:272-274 in-memory WHT 2.5 s at n=26 (26.8 Mpts/s), BASELINE.md section 1",
-        "dtype": "int64", "data": "synthetic: seeded counter-based uniform +-1 (config 4), generated on device",
-        "config": {"workload": f"config{a.config}: n={n} int64 FWHT, uniform +-1, natural order, unnormalised",
+        "dtype": "int64",
+        "data": f"synthetic: seeded counter-based {CONFIG_TEXT[a.config].split(' + ')[0]} (config {a.config}), "
+                "generated on device",
+        "config": {"workload": f"config{a.config}: n={n} int64 FWHT, {CONFIG_TEXT[a.config]}, natural order, "
+                               "unnormalised",
                    "n": n, "log2p": p, "local_log2n": nl, "parallelism": f"top {p} index bits sharded over {ws} GPUs",
                    "exchange": a.mode if p > 0 else None,
-                   "passes": [{"kind": q["kind"], "k": q["k"], "r": q["r"]} for q in plan["passes"]],
-                   "l2": "32 GiB input >> 126 MB L2 (no flush needed)"},
+                   "passes": [{"kind": q["kind"], "k": q["k"], "r": q["r"], "cluster": q["cluster"]}
+                              for q in plan["passes"]],
+                   "l2": ("L2 flushed between steps (256 MiB write, outside the step events)" if flush
+                          else f"{(8 << nl) >> 30} GiB input >> 126 MB L2 (no flush needed)"),
+                   "timing": ("per-step CUDA events; the input is regenerated between steps (outside the events)"
+                              if extract else "per-step CUDA events" if flush
+                              else "CUDA events around the K back-to-back steps")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "kernel": f"pass {dom} ({plan['passes'][dom]['kind']}, stages "
                      f"{plan['passes'][dom]['k']}..{plan['passes'][dom]['k'] + plan['passes'][dom]['r'] - 1})",
@@ -301,6 +355,11 @@ def run_ours(a):
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if extract:
+        line["extraction"] = {"tau": spec.threshold, "rule": "|W| > tau, sorted by index, fused into the last pass",
+                              "hits": len(hits_first), "hit_indices": [h[0] for h in hits_first][:16],
+                              "planted": sorted(spec.masks),
+                              "recovered_planted": sorted(h[0] for h in hits_first) == sorted(spec.masks)}
     if p > 0:
         line["xshard_ms"] = sum(xs_ms) / len(xs_ms)
         nv = 8 * (2 ** nl) * (ws - 1) / ws
@@ -326,35 +385,61 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+def host_ram_bytes() -> int:
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):
+        return 0
+
+
 def run_e2e(a, x, spec, p, nl, rank, ws, peer):
     """Same metric end to end: pinned host shard -> device -> transform ->
     host, every step, through the public API (fwht_array on a host buffer
-    for N = 1; H2D + sharded.fwht_distributed + D2H for N > 1)."""
+    for N = 1, fwht_extract for configs 3/5; H2D + sharded.fwht_distributed
+    + D2H for N > 1)."""
     import torch
     import torch.distributed as dist
 
     import paper_1607_01039_b200 as bw
-    from paper_1607_01039_b200 import sharded
+    from paper_1607_01039_b200 import sharded, signals
 
+    nbytes_local = 8 << nl
+    if ws == 1 and nbytes_local * 2 > host_ram_bytes() // 2:
+        return {"value": None, "unit": "points/s", "skipped": f"a pinned {nbytes_local >> 30} GiB host buffer "
+                "does not fit comfortably in host RAM"}
     steps = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 5))
     host = torch.empty(1 << nl, dtype=torch.int64, pin_memory=True)
+    signals.generate(spec, x, base=rank << nl)
     host.copy_(x)
     hnp = host.numpy()
     stream = torch.cuda.current_stream()
-    if ws == 1:
+    extract = spec.threshold is not None and ws == 1
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    if ws == 1 and not extract:
         bw.fwht_array(hnp)  # warm-up (allocates the device staging buffer)
         torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(steps):
             bw.fwht_array(hnp)
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
+        api = "paper_1607_01039_b200.fwht_array(pinned numpy buffer)"
+    elif extract:
+        out = host.clone().pin_memory()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(steps):
+            x.copy_(host, non_blocking=True)
+            idx, val = bw.fwht_extract_gt(x, spec.threshold)
+            out.copy_(x, non_blocking=True)
+            idx.cpu(), val.cpu()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        api = "H2D + paper_1607_01039_b200.fwht_extract_gt + D2H of the transform and the hits"
     else:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
         dist.barrier()
         e0.record(stream)
         for _ in range(steps):
@@ -366,15 +451,16 @@ def run_e2e(a, x, spec, p, nl, rank, ws, peer):
         t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    nbytes = 8 * (2 ** nl) * ws
+        api = "H2D + sharded.fwht_distributed + D2H"
+    nbytes = nbytes_local * ws
     return {"value": steps * (2 ** (nl + p)) / (ms / 1e3), "unit": "points/s", "h2d_bytes_per_step": nbytes,
-            "d2h_bytes_per_step": nbytes, "steps": steps, "ms_per_step": ms / steps,
-            "api": "paper_1607_01039_b200.fwht_array(pinned numpy buffer)" if ws == 1
-            else "H2D + sharded.fwht_distributed + D2H"}
+            "d2h_bytes_per_step": nbytes, "steps": steps, "ms_per_step": ms / steps, "api": api}
 
 
 def main():
     a = args_parse()
+    if a.n is None:
+        a.n = CONFIG_N[a.config]
     ws, _, _ = world()
     if ws != a.gpus and not (ws == 1 and a.gpus == 1):
         if ws == 1 and a.gpus > 1:

@@ -98,6 +98,18 @@ int bw_plan_npasses(int log2n);
 int bw_fwht_i64_pass(int64_t *data, int log2n, int pass_index, void *stream);
 
 /*
+ * Pass-level form of bw_fwht_extract_i64 for instrumentation: pass
+ * pass_index of the default plan with the |x| >= tau test fused into its
+ * epilogue; hits are appended unordered (at most cap) and counted in
+ * *count_dev (device, caller zeroes it).  bw_sort_hits_i64 then orders up to
+ * 2048 hits by index.  Both asynchronous.
+ */
+int bw_fwht_i64_pass_extract(int64_t *data, int log2n, int pass_index, uint64_t tau,
+                             uint64_t base, int64_t *out_idx, int64_t *out_val,
+                             uint64_t cap, uint64_t *count_dev, void *stream);
+int bw_sort_hits_i64(int64_t *idx, int64_t *val, const uint64_t *count_dev, void *stream);
+
+/*
  * float64 fwht_array (core.py:97-117 on a float64 Signal, core.py:56-59):
  * stages applied strictly in ascending order with the same IEEE a+b / a-b
  * as numpy, so results are bitwise identical to the reference (the order

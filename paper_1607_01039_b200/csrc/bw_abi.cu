@@ -459,6 +459,40 @@ int bw_fwht_i64_pass(int64_t* data, int log2n, int pass_index, void* stream) {
     return launch_pass(passes[pass_index], reinterpret_cast<u64*>(data), log2n, as_stream(stream));
 }
 
+// Pass-level launch with the threshold test fused into its epilogue (the
+// benchmark's instrumented form of bw_fwht_extract_i64): hits are appended
+// unordered to out_idx/out_val, their number accumulated in *count_dev.
+int bw_fwht_i64_pass_extract(int64_t* data, int log2n, int pass_index, uint64_t tau, uint64_t base,
+                             int64_t* out_idx, int64_t* out_val, uint64_t cap, uint64_t* count_dev, void* stream) {
+    BW_TRY(check_signal(data, log2n));
+    if (!count_dev || (cap > 0 && (!out_idx || !out_val))) return fail(BW_BAD_ARGUMENTS, "null extraction output");
+    if (log2n >= bw::kCtaBits && (reinterpret_cast<uintptr_t>(data) & 15u))
+        return fail(BW_BAD_ARGUMENTS, "pass-level launches need a 16-byte aligned signal");
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    std::vector<int> w;
+    BW_TRY(default_plan(log2n, &w));
+    std::vector<Pass> passes;
+    BW_TRY(build_passes(log2n, w, &passes));
+    if (pass_index < 0 || pass_index >= (int)passes.size() || passes[pass_index].kind == SMALL)
+        return fail(BW_BAD_ARGUMENTS, "pass %d cannot carry a fused extraction", pass_index);
+    bw::ExtractArgs ex = {tau, base, reinterpret_cast<long long*>(out_idx), reinterpret_cast<long long*>(out_val),
+                          reinterpret_cast<unsigned long long*>(count_dev), cap};
+    return launch_pass(passes[pass_index], reinterpret_cast<u64*>(data), log2n, as_stream(stream), &ex);
+}
+
+// Sort up to 2048 fused-extraction hits by index in place (async).
+int bw_sort_hits_i64(int64_t* idx, int64_t* val, const uint64_t* count_dev, void* stream) {
+    if (!idx || !val || !count_dev) return fail(BW_BAD_ARGUMENTS, "null pointer");
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    bw::k_sort_hits<<<1, 1024, 0, as_stream(stream)>>>(reinterpret_cast<long long*>(idx),
+                                                       reinterpret_cast<long long*>(val),
+                                                       reinterpret_cast<const unsigned long long*>(count_dev));
+    BW_LAUNCHED("k_sort_hits launch");
+    return BW_OK;
+}
+
 int bw_fwht_i64_planned(int64_t* data, int log2n, const int* pass_bits, int npasses, void* stream) {
     if (npasses < 0 || (npasses > 0 && !pass_bits)) return fail(BW_BAD_ARGUMENTS, "bad pass list");
     if (npasses == 0) return fwht_impl(data, log2n, nullptr, true, as_stream(stream));

@@ -310,7 +310,8 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
 // in shared memory, count <= 2048.
 __global__ void __launch_bounds__(1024) k_sort_hits(long long* idx, long long* val, const unsigned long long* count) {
     __shared__ long long sk[2048], sv[2048];
-    const unsigned m = (unsigned)*count;
+    const unsigned long long c = *count;
+    const unsigned m = c < 2048ull ? (unsigned)c : 2048u;  // callers sort only when count <= 2048
     for (unsigned i = threadIdx.x; i < 2048; i += blockDim.x) {
         sk[i] = i < m ? idx[i] : 0x7FFFFFFFFFFFFFFFll;
         sv[i] = i < m ? val[i] : 0;
