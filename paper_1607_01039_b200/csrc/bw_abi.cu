@@ -175,10 +175,10 @@ int visit_pass(const Pass& p, F&& f) {
 int high_default_q(int r) { return r <= 8 ? 0 : 1; }
 
 // Relative cost of a pass shape beyond its HBM round trip (measured on
-// B200, profiles/: a 2-CTA low pass runs at ~90% of the 1-CTA one, 10-stage
-// high passes at ~85%, 4-CTA low passes at ~70%).
+// B200, profiles/: a 2-CTA low pass runs at 80-90% of the 1-CTA one and
+// varies by box, 10-stage high passes at ~90%, 4-CTA low passes at ~70%).
 int pass_cost(bool low, int w) {
-    if (low) return w == 13 ? 0 : w == 14 ? 1 : 5;
+    if (low) return w == 13 ? 0 : w == 14 ? 3 : 5;
     return w == 10 ? 2 : 0;
 }
 
