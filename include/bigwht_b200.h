@@ -158,6 +158,21 @@ int bw_fwht_host_i64(int64_t *host, int log2n, int64_t *work_dev,
                      int check_bound, void *stream, uint64_t *butterflies);
 
 /*
+ * Out-of-core transform of a HOST array larger than the device workspace --
+ * the paper's blocked external algorithm (external.py:65-283, PAPER.md
+ * Fig. 3) with host memory in the role of the disk and the GPU as the
+ * in-memory engine.  work_dev holds 2^log2_work int64 (>= 2^15).  Pass 0
+ * transforms contiguous chunks of 2^(log2_work-1) elements; every further
+ * pass transforms up to log2_work-14 high bits on chunks of 64 KiB-wide
+ * rows moved with 2-D copies, double-buffered on two streams (H2D of one
+ * chunk overlaps the other's compute and D2H).  *host_passes (may be NULL)
+ * receives the number of passes over host memory.  host should be pinned
+ * for full PCIe bandwidth.  Synchronous.
+ */
+int bw_fwht_host_ooc_i64(int64_t *host, int log2n, int64_t *work_dev, int log2_work,
+                         void *stream, int *host_passes);
+
+/*
  * inverse_wht_inplace (core.py:147-173) on the int64 payload: bound check,
  * forward transform, exact division by 2^n.  When some coefficient is not
  * divisible, the buffer is restored and BW_INEXACT_DIVISION returned

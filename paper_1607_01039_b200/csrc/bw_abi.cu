@@ -365,6 +365,25 @@ int fwht_impl(int64_t* data, int log2n, const std::vector<int>* widths, bool nai
 
 uint64_t butterfly_count(int n) { return n == 0 ? 0 : (uint64_t)n << (n - 1); }
 
+// Stages [lo, n) of a device buffer only (lo >= 13), through high passes:
+// the out-of-core mode's device chunk holds 2^(n-lo) rows of 2^lo columns.
+int fwht_high_bits(u64* d, int n, int lo, cudaStream_t s) {
+    const int h = n - lo;
+    if (h <= 0) return BW_OK;
+    if (lo < bw::kCtaBits) return fail(BW_BAD_ARGUMENTS, "high-bit transform needs lo >= %d", bw::kCtaBits);
+    const int q = (h + bw::kMaxHighBits - 1) / bw::kMaxHighBits;
+    int k = lo;
+    for (int i = 0; i < q; ++i) {
+        const int r = h / q + (i < h % q ? 1 : 0);
+        const Pass p = r <= bw::kRegOnlyMaxBits ? Pass{REG, k, r, 0} : Pass{HIGH, k, r, high_default_q(r)};
+        BW_TRY(launch_pass(p, d, n, s));
+        k += r;
+    }
+    return BW_OK;
+}
+
+
+
 int minmax_impl(const int64_t* data, uint64_t count, int64_t* out, int dev, cudaStream_t s) {
     bw::k_minmax_init<<<1, 1, 0, s>>>(reinterpret_cast<long long*>(out));
     BW_LAUNCHED("k_minmax_init launch");
@@ -586,6 +605,112 @@ int bw_fwht_host_i64(int64_t* host, int log2n, int64_t* work_dev, int check_boun
     BW_CUDA(cudaMemcpyAsync(host, work_dev, bytes, cudaMemcpyDeviceToHost, s));
     BW_CUDA(cudaStreamSynchronize(s));
     if (butterflies) *butterflies = butterfly_count(log2n);
+    return BW_OK;
+}
+
+// ---- out-of-core transform of a host array (external.py:65-283) ----------
+//
+// The paper's blocked external algorithm with the GPU as the in-memory
+// engine and host memory as the "disk": pass 0 transforms contiguous chunks
+// of 2^cb elements (_initial_pass, external.py:238-254, with 2^B = chunk);
+// each following pass takes g <= cb - 13 consecutive high bits [k, k+g) and
+// moves 2^g rows x 64 KiB columns per chunk with 2-D copies (the paper's
+// _blocked_stage_pass, external.py:272-283, but g stages per pass instead of
+// one).  Two streams alternate over the two halves of the workspace, so one
+// chunk's H2D overlaps the other's transform and D2H.
+namespace {
+cudaStream_t g_ooc_streams[kMaxDevices][2];
+int ooc_streams(int dev, cudaStream_t* out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (int i = 0; i < 2; ++i) {
+        if (!g_ooc_streams[dev][i]) {
+            cudaError_t e = cudaStreamCreateWithFlags(&g_ooc_streams[dev][i], cudaStreamNonBlocking);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+        }
+        out[i] = g_ooc_streams[dev][i];
+    }
+    return BW_OK;
+}
+}  // namespace
+
+int bw_fwht_host_ooc_i64(int64_t* host, int log2n, int64_t* work_dev, int log2_work, void* stream,
+                         int* host_passes) {
+    if (!host) return fail(BW_BAD_ARGUMENTS, "null host pointer");
+    BW_TRY(check_signal(work_dev, log2_work));
+    if (reinterpret_cast<uintptr_t>(work_dev) & 15u) return fail(BW_BAD_ARGUMENTS, "workspace must be 16-byte aligned");
+    if (log2n < 0 || log2n > 40) return fail(BW_BAD_ARGUMENTS, "log2n = %d outside 0..40", log2n);
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    cudaStream_t caller = as_stream(stream);
+    const int cb = log2_work - 1;  // two half-workspaces of 2^cb elements
+    if (log2n <= log2_work) {  // fits: one in-memory transform
+        const size_t bytes = (size_t)8 << log2n;
+        BW_CUDA(cudaMemcpyAsync(work_dev, host, bytes, cudaMemcpyHostToDevice, caller));
+        BW_TRY(fwht_impl(work_dev, log2n, nullptr, false, caller));
+        BW_CUDA(cudaMemcpyAsync(host, work_dev, bytes, cudaMemcpyDeviceToHost, caller));
+        BW_CUDA(cudaStreamSynchronize(caller));
+        if (host_passes) *host_passes = 1;
+        return BW_OK;
+    }
+    if (cb < bw::kCtaBits + 1) return fail(BW_BAD_ARGUMENTS, "workspace too small: need 2^%d elements", bw::kCtaBits + 2);
+    cudaStream_t st[2];
+    BW_TRY(ooc_streams(dev, st));
+    cudaEvent_t start;
+    BW_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    BW_CUDA(cudaEventRecord(start, caller));  // order after the caller's prior work
+    for (int i = 0; i < 2; ++i) BW_CUDA(cudaStreamWaitEvent(st[i], start, 0));
+    cudaEventDestroy(start);
+    u64* buf[2] = {reinterpret_cast<u64*>(work_dev), reinterpret_cast<u64*>(work_dev) + (1ull << cb)};
+    int passes = 0;
+    // Pass 0: contiguous chunks, stages 0..cb-1.
+    {
+        const uint64_t chunks = 1ull << (log2n - cb);
+        const size_t bytes = (size_t)8 << cb;
+        for (uint64_t c = 0; c < chunks; ++c) {
+            const int b = (int)(c & 1);
+            int64_t* h = host + (c << cb);
+            BW_CUDA(cudaMemcpyAsync(buf[b], h, bytes, cudaMemcpyHostToDevice, st[b]));
+            BW_TRY(fwht_impl(reinterpret_cast<int64_t*>(buf[b]), cb, nullptr, false, st[b]));
+            BW_CUDA(cudaMemcpyAsync(h, buf[b], bytes, cudaMemcpyDeviceToHost, st[b]));
+        }
+        ++passes;
+    }
+    // Passes over the high bits: 2^g rows at stride 2^k x 2^13 columns.
+    const int cols = bw::kCtaBits;
+    const int gmax = cb - cols;
+    for (int k = cb; k < log2n;) {
+        {  // this pass reads what both streams wrote in the previous one: join them
+            cudaEvent_t ev[2];
+            for (int i = 0; i < 2; ++i) {
+                BW_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+                BW_CUDA(cudaEventRecord(ev[i], st[i]));
+            }
+            BW_CUDA(cudaStreamWaitEvent(st[1], ev[0], 0));
+            BW_CUDA(cudaStreamWaitEvent(st[0], ev[1], 0));
+            for (int i = 0; i < 2; ++i) cudaEventDestroy(ev[i]);
+        }
+        const int rem = log2n - k;
+        const int npass = (rem + gmax - 1) / gmax;
+        const int g = (rem + npass - 1) / npass;
+        const int w = cb - g;                                   // row width: as many columns as fit
+        const uint64_t lo_chunks = 1ull << (k - w);             // bits [w, k)
+        const uint64_t hi_chunks = 1ull << (log2n - k - g);     // bits [k+g, n)
+        const size_t width = (size_t)8 << w, pitch = (size_t)8 << k;
+        uint64_t c = 0;
+        for (uint64_t hc = 0; hc < hi_chunks; ++hc)
+            for (uint64_t lc = 0; lc < lo_chunks; ++lc, ++c) {
+                const int b = (int)(c & 1);
+                int64_t* h = host + ((lc << w) | (hc << (k + g)));
+                BW_CUDA(cudaMemcpy2DAsync(buf[b], width, h, pitch, width, (size_t)1 << g, cudaMemcpyHostToDevice, st[b]));
+                BW_TRY(fwht_high_bits(buf[b], cb, w, st[b]));
+                BW_CUDA(cudaMemcpy2DAsync(h, pitch, buf[b], width, width, (size_t)1 << g, cudaMemcpyDeviceToHost, st[b]));
+            }
+        k += g;
+        ++passes;
+    }
+    BW_CUDA(cudaStreamSynchronize(st[0]));
+    BW_CUDA(cudaStreamSynchronize(st[1]));
+    if (host_passes) *host_passes = passes;
     return BW_OK;
 }
 
