@@ -159,6 +159,14 @@ def main():
         {"value": 1 << 59, "n": 4, "ok": False},
         {"value": (1 << 59) - 1, "n": 4, "ok": True},
     ]
+    # 13. A dataset written by the reference (dataset.py:427-446), kept as
+    #     raw payload + sidecar for the format-compatibility pins.
+    from bigwht import dataset as ref_dataset
+    ds_path = os.path.join(HERE, "ref_dataset_n8.bin")
+    for pth in (ds_path, ds_path + ".meta.json"):
+        if os.path.exists(pth):
+            os.remove(pth)
+    ref_dataset.write_signal(ds_path, oracle_np.gen(2, 8, [1000], 0, 1 << 8), domain="time")
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(out, f, indent=1)
     print("wrote fixtures to", HERE)
