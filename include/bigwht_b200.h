@@ -289,6 +289,20 @@ int bw_fwht_extract_i64(int64_t *data, int log2n, uint64_t tau, uint64_t base,
                         int64_t *out_idx, int64_t *out_val, uint64_t cap,
                         void *stream, uint64_t *count);
 
+/*
+ * fold (subspace.py:150-161) on the device: out_dev[L.j] += x[j] for every
+ * j < 2^d_in (wrapping int64 sums), where L.j is the XOR of col_masks[c]
+ * (column c of the d_out x d_in binary map as a d_out-bit mask,
+ * subspace.py:61-65) over the set bits c of j.  out_dev holds 2^d_out int64
+ * and is zeroed first.  bw_fold_gen_i64 folds the seeded generator's signal
+ * (bw_gen_i64 kinds) without materialising it.  d_in <= 40, d_out <= 30.
+ * Synchronous.  WHT(fold(x, L)) = WHT(x)[row_space(L)] (subspace.py:1-11).
+ */
+int bw_fold_i64(const int64_t *x, int d_in, const uint64_t *col_masks, int d_out,
+                int64_t *out_dev, void *stream);
+int bw_fold_gen_i64(int d_in, int kind, uint64_t seed, const uint64_t *params, int nparams,
+                    const uint64_t *col_masks, int d_out, int64_t *out_dev, void *stream);
+
 /* ---- planner ----------------------------------------------------------- */
 
 /*

@@ -59,6 +59,8 @@ _SIGNATURES = {
     "bw_inverse_f64": ([P, I32, P], I32),
     "bw_wht_bruteforce_i64": ([P, P, I32, P], I32),
     "bw_sumsq_partials_i64": ([P, U64, P, I32, P], I32),
+    "bw_fold_i64": ([P, I32, PU64, I32, P, P], I32),
+    "bw_fold_gen_i64": ([I32, I32, U64, PU64, I32, PU64, I32, P, P], I32),
     "bw_xshard_i64": ([ctypes.POINTER(P), I32, U64, U64, P], I32),
     "bw_xshard_strided_i64": ([P, U64, I32, U64, U64, P], I32),
     "bw_ipc_get_handle": ([P, P, PU64], I32),

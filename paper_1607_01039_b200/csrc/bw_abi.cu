@@ -773,6 +773,59 @@ int bw_sumsq_partials_i64(const int64_t* x, uint64_t count, uint64_t* partial_de
     return BW_OK;
 }
 
+// fold (subspace.py:150-161) of a device signal, or of a generated one.
+static int fold_impl(const int64_t* x, int d_in, const uint64_t* col_masks, int d_out, int64_t* out_dev,
+                     const bw::GenParams& g, cudaStream_t s) {
+    if (!col_masks || !out_dev) return fail(BW_BAD_ARGUMENTS, "null pointer");
+    if (d_out < 1 || d_in < d_out || d_in > 8 * bw::kFoldGroups || d_out > 30)
+        return fail(BW_BAD_ARGUMENTS, "need 1 <= d_out <= d_in <= 40, d_out <= 30 (got %d, %d)", d_out, d_in);
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    const int groups = (d_in + 7) / 8;
+    std::vector<unsigned> tab((size_t)groups * 256, 0u);
+    for (int q = 0; q < groups; ++q)
+        for (int v = 0; v < 256; ++v) {
+            uint64_t t = 0;
+            for (int b = 0; b < 8; ++b)
+                if (((v >> b) & 1) && 8 * q + b < d_in) t ^= col_masks[8 * q + b];
+            if (t >> d_out) return fail(BW_BAD_ARGUMENTS, "column mask wider than d_out bits");
+            tab[(size_t)q * 256 + v] = (unsigned)t;
+        }
+    void* sc = nullptr;
+    BW_TRY(scratch(dev, 4096 + tab.size() * 4, &sc));
+    unsigned* dtab = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(sc) + 4096);
+    BW_CUDA(cudaMemcpyAsync(dtab, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, s));
+    BW_CUDA(cudaMemsetAsync(out_dev, 0, (size_t)8 << d_out, s));
+    const uint64_t count = 1ull << d_in;
+    const int grid = grid_for(dev, count, 256, 8);
+    unsigned long long* out = reinterpret_cast<unsigned long long*>(out_dev);
+    if (d_out <= 12)
+        bw::k_fold<true><<<grid, 256, (size_t)8 << d_out, s>>>(reinterpret_cast<const long long*>(x), count, dtab,
+                                                              groups, d_out, out, g);
+    else
+        bw::k_fold<false><<<grid, 256, 0, s>>>(reinterpret_cast<const long long*>(x), count, dtab, groups, d_out, out,
+                                               g);
+    BW_LAUNCHED("k_fold launch");
+    BW_CUDA(cudaStreamSynchronize(s));  // the table lives in shared scratch
+    return BW_OK;
+}
+
+int bw_fold_i64(const int64_t* x, int d_in, const uint64_t* col_masks, int d_out, int64_t* out_dev, void* stream) {
+    BW_TRY(check_signal(x, d_in));
+    bw::GenParams g;
+    memset(&g, 0, sizeof g);
+    return fold_impl(x, d_in, col_masks, d_out, out_dev, g, as_stream(stream));
+}
+
+static int gen_params(int kind, uint64_t seed, const uint64_t* params, int nparams, bw::GenParams* g);
+
+int bw_fold_gen_i64(int d_in, int kind, uint64_t seed, const uint64_t* params, int nparams,
+                    const uint64_t* col_masks, int d_out, int64_t* out_dev, void* stream) {
+    bw::GenParams g;
+    BW_TRY(gen_params(kind, seed, params, nparams, &g));
+    return fold_impl(nullptr, d_in, col_masks, d_out, out_dev, g, as_stream(stream));
+}
+
 // Cross-shard butterfly (parallel.py:103-110, all log2 P stage phases fused).
 static int xshard_launch(const bw::ShardPtrs& sp, int log2p, uint64_t begin, uint64_t count, cudaStream_t s) {
     int dev = 0;

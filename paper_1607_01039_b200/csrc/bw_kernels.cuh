@@ -706,6 +706,42 @@ __global__ void __launch_bounds__(256) k_sumsq(const long long* __restrict__ x, 
 }
 
 // ---------------------------------------------------------------------------
+// fold (subspace.py:150-161): out[L.j] += x[j] over j in [0, 2^d_in), where
+// L.j is the XOR of the column masks of L selected by the bits of j
+// (apply_map_array, subspace.py:116-121), looked up 8 index bits at a time.
+// Small outputs (d_out <= 12) are accumulated per CTA in shared memory.
+// x == nullptr folds the seeded generator's signal on the fly (no input).
+// ---------------------------------------------------------------------------
+constexpr int kFoldGroups = 5;  // d_in <= 40
+
+template <bool SMEM_BINS>
+__global__ void __launch_bounds__(256) k_fold(const long long* __restrict__ x, uint64_t count,
+                                              const unsigned* __restrict__ table, int groups, int d_out,
+                                              unsigned long long* out, GenParams g) {
+    __shared__ unsigned tab[kFoldGroups * 256];
+    extern __shared__ unsigned long long bins[];
+    for (int i = threadIdx.x; i < groups * 256; i += blockDim.x) tab[i] = table[i];
+    if (SMEM_BINS)
+        for (int i = threadIdx.x; i < (1 << d_out); i += blockDim.x) bins[i] = 0ull;
+    __syncthreads();
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < count; j += nth) {
+        unsigned t = 0;
+        for (int q = 0; q < groups; ++q) t ^= tab[q * 256 + ((j >> (8 * q)) & 255u)];
+        const unsigned long long v = x ? (unsigned long long)x[j] : (unsigned long long)gen_value(g, j);
+        if (SMEM_BINS)
+            atomicAdd(&bins[t], v);
+        else
+            atomicAdd(&out[t], v);
+    }
+    if (SMEM_BINS) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < (1 << d_out); i += blockDim.x)
+            if (bins[i]) atomicAdd(&out[i], bins[i]);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Elementwise helpers for the inverse transform (core.py:147-173).
 // ---------------------------------------------------------------------------
 __global__ void k_check_divisible(const long long* __restrict__ data, uint64_t count, int n, int* flag) {

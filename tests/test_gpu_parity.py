@@ -387,3 +387,28 @@ def test_fused_extraction_configs(golden):
         i, v = bw.fwht_extract_gt(t, golden[key]["tau"])
         assert digest(t.cpu().numpy()) == golden[key]["y_sha256"]
         assert [[a, b] for a, b in zip(i.tolist(), v.tolist())] == sorted(golden[key]["hits"])
+
+
+def test_fold_matches_reference(golden_npz, coracle):
+    from paper_1607_01039_b200 import subspace
+
+    z = golden_npz("fold_16_8.npz")
+    x = oracle_np.gen(1, 77, [], 0, 1 << 16)
+    f = subspace.fold(bw.Signal(dev(x)), z["rows"])
+    assert np.array_equal(f.data.cpu().numpy(), z["folded"])
+    fn = subspace.fold(bw.Signal(x.copy()), z["rows"])  # numpy in, numpy out
+    assert isinstance(fn.data, np.ndarray) and np.array_equal(fn.data, z["folded"])
+    with pytest.raises(subspace.DimMismatch):
+        subspace.fold(bw.Signal(dev(x[:1 << 15])), z["rows"])
+    # large outputs (global atomics) and generated inputs
+    for n, d_out, idx in ((22, 14, 2), (24, 20, 5), (20, 8, 3)):
+        spec = signals.config(idx, n)
+        rows = subspace.random_full_rank(n, d_out, n)
+        want = np.empty(1 << d_out, dtype=np.int64)
+        cols = oracle_np.column_masks(rows).astype(np.uint64)
+        arr = (ctypes.c_uint64 * len(spec.params))(*spec.params) if spec.params else None
+        assert coracle.oracle_fold_i64(None, n, cols.ctypes.data, d_out, spec.kind, spec.seed, arr,
+                                       len(spec.params), 4, want.ctypes.data) == 0
+        assert np.array_equal(subspace.fold_generated(spec, rows).cpu().numpy(), want)
+        t = signals.make(spec)
+        assert np.array_equal(subspace.fold(bw.Signal(t), rows).data.cpu().numpy(), want)

@@ -196,3 +196,15 @@ def test_oracle_against_live_reference():
     ) % (REF_SRC, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
+
+
+def test_subspace_host_helpers_match_reference(golden_npz):
+    """The product's host-side map helpers restate subspace.py exactly."""
+    from paper_1607_01039_b200 import subspace
+
+    z = golden_npz("fold_16_8.npz")
+    rows = subspace.random_full_rank(16, 8, 7)
+    assert np.array_equal(rows, z["rows"])
+    assert np.array_equal(subspace.row_space(rows), z["row_space"])
+    assert subspace.column_masks(rows) == [int(c) for c in oracle_np.column_masks(rows)]
+    assert subspace.gf2_rank(rows) == 8
