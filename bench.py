@@ -320,6 +320,16 @@ def run_ours(a):
     dom = max(range(npasses), key=lambda i: avg_pass[i])
     achieved = bytes_per_pass / (avg_pass[dom] / 1e3) / 1e9
     launches = a.steps * (npasses + (1 if extract else 0) + (1 if p > 0 else 0))
+    traffic = None  # dram read + write of the dominant pass, from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", f"r01_traffic_n{nl}.json")) as f:
+            tr = json.load(f)
+        plan_kinds = [q["kind"] for q in plan["passes"]]
+        if len(tr["passes"]) == npasses and plan_kinds[0] == "low":
+            t_dom = tr["passes"][dom]
+            traffic = t_dom["dram_read_bytes"] + t_dom["dram_write_bytes"]
+    except (OSError, KeyError, ValueError):
+        traffic = None
 
     e2e = None
     if not a.no_e2e:
@@ -345,7 +355,7 @@ def run_ours(a):
                               if extract else "per-step CUDA events" if flush
                               else "CUDA events around the K back-to-back steps")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": f"pass {dom} ({plan['passes'][dom]['kind']}, stages "
+                     "traffic": traffic, "kernel": f"pass {dom} ({plan['passes'][dom]['kind']}, stages "
                      f"{plan['passes'][dom]['k']}..{plan['passes'][dom]['k'] + plan['passes'][dom]['r'] - 1})",
                      "algorithmic_bytes_per_launch": bytes_per_pass, "peak_source": peak_src,
                      "frac_of_8tbs_spec": achieved / 8000.0},

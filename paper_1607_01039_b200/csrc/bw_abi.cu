@@ -287,8 +287,10 @@ int set_all_pass_attributes() {
         using C = typename decltype(t)::type;
         constexpr int L = decltype(l)::value;
         constexpr int smem = bw::Dims<C>::SMEM_BYTES;
-        if (smem > 48 * 1024)
-            BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        if (smem > 48 * 1024) {
+            BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        }
         return BW_OK;
     });
 }
@@ -306,7 +308,10 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractA
         constexpr int L = decltype(l)::value;
         const unsigned grid = (unsigned)(1ull << (n - bw::kCtaBits));
         if constexpr (C::Q == 0) {
-            bw::k_pass<C, L><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k, ex);
+            if (ex.count)
+                bw::k_pass<C, L, true><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k, ex);
+            else
+                bw::k_pass<C, L, false><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k, ex);
             BW_LAUNCHED("fwht pass launch");
         } else {
             cudaLaunchConfig_t cfg = {};
@@ -321,7 +326,10 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractA
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L>, d, p.k, ex));
+            if (ex.count)
+                BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L, true>, d, p.k, ex));
+            else
+                BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L, false>, d, p.k, ex));
         }
         return BW_OK;
     });

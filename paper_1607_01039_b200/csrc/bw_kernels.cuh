@@ -267,7 +267,7 @@ __device__ __forceinline__ void extract_hits(const u64 (&v)[Dims<C>::E], uint64_
 // stages]* -> store (last round layout).  k = first global stage bit of the
 // rows (ignored for L == T).  Cluster configs (Q > 0) put 2^Q CTAs on one
 // tile; grid = 2^(n-13) CTAs for every config.
-template <class C, int L>
+template <class C, int L, bool EX = false>
 __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     k_pass(u64* __restrict__ data, int k, ExtractArgs ex) {
     constexpr int T = C::T;
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     run_rounds<C, L, 1>(v, sm, lane, warp, rank);
     constexpr int LAST = C::NR - 1;
     const uint32_t tp_last = thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank);
-    if (ex.count != nullptr) extract_hits<C, LAST, T, L>(v, tile_base<T, L>(tile, k), tp_last, k, ex);
+    if constexpr (EX) extract_hits<C, LAST, T, L>(v, tile_base<T, L>(tile, k), tp_last, k, ex);
     store_global<C, LAST, T, L>(v, g, tp_last, k);
 }
 
