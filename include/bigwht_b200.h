@@ -110,6 +110,16 @@ int bw_fwht_i64_pass_extract(int64_t *data, int log2n, int pass_index, uint64_t 
 int bw_sort_hits_i64(int64_t *idx, int64_t *val, const uint64_t *count_dev, void *stream);
 
 /*
+ * int32 input (the north_star's "seeded int32 inputs"), int64 output, out of
+ * place: bit-identical to the reference's fwht_array(x.astype(int64)), with
+ * overflow-free int64 accumulation (|x| < 2^31 and n <= 32 keep every sum
+ * below 2^63).  The first pass reads the int32 source directly (4 B/point)
+ * and writes dst; the others run in place on dst.  Asynchronous.
+ */
+int bw_fwht_widen_i32(const int32_t *src, int64_t *dst, int log2n, void *stream,
+                      uint64_t *butterflies);
+
+/*
  * float64 fwht_array (core.py:97-117 on a float64 Signal, core.py:56-59):
  * stages applied strictly in ascending order with the same IEEE a+b / a-b
  * as numpy, so results are bitwise identical to the reference (the order

@@ -17,6 +17,7 @@ from .core import (
     check_magnitude_bound,
     fwht_array,
     fwht_inplace,
+    fwht_widen,
     inverse_wht_inplace,
     parseval_energy,
     wht_bruteforce,
@@ -42,6 +43,7 @@ __all__ = [
     "check_magnitude_bound",
     "fwht_array",
     "fwht_inplace",
+    "fwht_widen",
     "inverse_wht_inplace",
     "parseval_energy",
     "wht_bruteforce",

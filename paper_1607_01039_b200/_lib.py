@@ -49,6 +49,7 @@ _SIGNATURES = {
     "bw_fwht_i64_pass": ([P, I32, I32, P], I32),
     "bw_fwht_i64_pass_extract": ([P, I32, I32, U64, U64, P, P, U64, P, P], I32),
     "bw_sort_hits_i64": ([P, P, P, P], I32),
+    "bw_fwht_widen_i32": ([P, P, I32, P, PU64], I32),
     "bw_fwht_f64": ([P, I32, P, PU64], I32),
     "bw_minmax_i64": ([P, U64, P, P], I32),
     "bw_check_bound_i64": ([P, I32, P, P, PU64], I32),

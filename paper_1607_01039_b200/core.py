@@ -229,6 +229,26 @@ def fwht_array(buf) -> int:
     return int(bf.value)
 
 
+def fwht_widen(x) -> torch.Tensor:
+    """Out-of-place transform of an int32 signal into a new int64 CUDA
+    tensor: the reference's fwht_array(x.astype(np.int64)) (core.py:97-117;
+    a bare int32 buffer there would wrap in int32), computed with the first
+    pass reading the int32 source directly.  Accepts a CUDA int32 tensor or a
+    numpy int32 array."""
+    if isinstance(x, np.ndarray):
+        _need_cuda()
+        x = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    if not isinstance(x, torch.Tensor) or x.dtype != torch.int32:
+        raise BadArguments("fwht_widen expects int32 input")
+    _require_cuda(x)
+    _check_contiguous(x)
+    n = _check_shape(x)
+    out = torch.empty(1 << n, dtype=torch.int64, device=x.device)
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.lib().bw_fwht_widen_i32(x.data_ptr(), out.data_ptr(), n, _stream_handle(x), None))
+    return out
+
+
 def _flip(domain: Domain) -> Domain:
     return Domain.WALSH if domain == Domain.TIME else Domain.TIME
 

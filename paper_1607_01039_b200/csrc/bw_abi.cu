@@ -290,14 +290,19 @@ int set_all_pass_attributes() {
         if (smem > 48 * 1024) {
             BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            if constexpr (L >= C::T)
+                BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem));
         }
         return BW_OK;
     });
 }
 
-int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractArgs* exp = nullptr) {
+int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractArgs* exp = nullptr,
+                const int* src32 = nullptr) {
     bw::ExtractArgs ex = {};
     if (exp) ex = *exp;
+    if (src32 && p.kind != LOW) return fail(BW_BAD_ARGUMENTS, "only the low pass widens int32 input");
     if (p.kind == SMALL) {
         bw::k_small<u64><<<1, 256, (size_t)(8ull << n), s>>>(d, n);
         BW_LAUNCHED("k_small launch");
@@ -307,11 +312,19 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractA
         using C = typename decltype(t)::type;
         constexpr int L = decltype(l)::value;
         const unsigned grid = (unsigned)(1ull << (n - bw::kCtaBits));
+        constexpr bool kLow = L >= C::T;
         if constexpr (C::Q == 0) {
+            if constexpr (kLow) {
+                if (src32) {
+                    bw::k_pass<C, L, false, true><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k, ex, src32);
+                    BW_LAUNCHED("fwht widening pass launch");
+                    return BW_OK;
+                }
+            }
             if (ex.count)
-                bw::k_pass<C, L, true><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k, ex);
+                bw::k_pass<C, L, true><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k, ex, nullptr);
             else
-                bw::k_pass<C, L, false><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k, ex);
+                bw::k_pass<C, L, false><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k, ex, nullptr);
             BW_LAUNCHED("fwht pass launch");
         } else {
             cudaLaunchConfig_t cfg = {};
@@ -326,10 +339,17 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractA
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
+            const int* none = nullptr;
+            if constexpr (kLow) {
+                if (src32) {
+                    BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L, false, true>, d, p.k, ex, src32));
+                    return BW_OK;
+                }
+            }
             if (ex.count)
-                BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L, true>, d, p.k, ex));
+                BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L, true>, d, p.k, ex, none));
             else
-                BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L, false>, d, p.k, ex));
+                BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L, false>, d, p.k, ex, none));
         }
         return BW_OK;
     });
@@ -525,6 +545,34 @@ int bw_fwht_i64_planned(int64_t* data, int log2n, const int* pass_bits, int npas
     if (npasses == 0) return fwht_impl(data, log2n, nullptr, true, as_stream(stream));
     std::vector<int> w(pass_bits, pass_bits + npasses);
     return fwht_impl(data, log2n, &w, false, as_stream(stream));
+}
+
+// int32 input, int64 output (out of place): the first pass reads the int32
+// source (4 B/point) and writes int64, the rest run in place on dst -- the
+// reference's fwht_array on x.astype(int64), with overflow-free int64 sums.
+int bw_fwht_widen_i32(const int32_t* src, int64_t* dst, int log2n, void* stream, uint64_t* butterflies) {
+    BW_TRY(check_signal(dst, log2n));
+    if (!src || (reinterpret_cast<uintptr_t>(src) & 7u)) return fail(BW_BAD_ARGUMENTS, "int32 source must be 8-byte aligned");
+    if (reinterpret_cast<uintptr_t>(dst) & 15u) return fail(BW_BAD_ARGUMENTS, "int64 destination must be 16-byte aligned");
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    cudaStream_t s = as_stream(stream);
+    u64* d = reinterpret_cast<u64*>(dst);
+    std::vector<int> w;
+    BW_TRY(default_plan(log2n, &w));
+    std::vector<Pass> passes;
+    BW_TRY(build_passes(log2n, w, &passes));
+    if (passes.empty() || passes[0].kind != LOW) {  // tiny signals: widen, then transform
+        const uint64_t count = 1ull << log2n;
+        bw::k_widen_i32<<<grid_for(dev, count, 256, 4), 256, 0, s>>>(src, reinterpret_cast<long long*>(dst), count);
+        BW_LAUNCHED("k_widen_i32 launch");
+        BW_TRY(fwht_impl(dst, log2n, nullptr, false, s));
+    } else {
+        BW_TRY(launch_pass(passes[0], d, log2n, s, nullptr, src));
+        for (size_t i = 1; i < passes.size(); ++i) BW_TRY(launch_pass(passes[i], d, log2n, s));
+    }
+    if (butterflies) *butterflies = butterfly_count(log2n);
+    return BW_OK;
 }
 
 // fwht_array on a float64 buffer (core.py:97-117): stages strictly ascending

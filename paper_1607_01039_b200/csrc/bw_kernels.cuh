@@ -62,6 +62,28 @@ __device__ __forceinline__ void load_global(u64 (&v)[Dims<C>::E], const u64* __r
     }
 }
 
+// Widening load (int32 source, int64 registers) for the out-of-place first
+// pass of bw_fwht_widen_i32: same addressing, 4-byte elements.
+template <class C, int RD, int T, int L>
+__device__ __forceinline__ void load_global_i32(u64 (&v)[Dims<C>::E], const int* __restrict__ g, uint32_t tp,
+                                               int k) {
+    constexpr int E = Dims<C>::E;
+    const int* p = g + global_off<T, L>(tp, k);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        const uint64_t off = global_off<T, L>(reg_part<C, RD>(j), k);
+        if constexpr (VecAccess<C, RD, L>::value) {
+            if ((j & 1) == 0) {
+                const int2 t = __ldcs(reinterpret_cast<const int2*>(p + off));
+                v[j] = (u64)(long long)t.x;
+                v[j + 1] = (u64)(long long)t.y;
+            }
+        } else {
+            v[j] = (u64)(long long)__ldcs(p + off);
+        }
+    }
+}
+
 template <class C, int RD, int T, int L>
 __device__ __forceinline__ void store_global(const u64 (&v)[Dims<C>::E], u64* __restrict__ g,
                                              uint32_t tp, int k) {
@@ -267,9 +289,9 @@ __device__ __forceinline__ void extract_hits(const u64 (&v)[Dims<C>::E], uint64_
 // stages]* -> store (last round layout).  k = first global stage bit of the
 // rows (ignored for L == T).  Cluster configs (Q > 0) put 2^Q CTAs on one
 // tile; grid = 2^(n-13) CTAs for every config.
-template <class C, int L, bool EX = false>
+template <class C, int L, bool EX = false, bool SRC32 = false>
 __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
-    k_pass(u64* __restrict__ data, int k, ExtractArgs ex) {
+    k_pass(u64* __restrict__ data, int k, ExtractArgs ex, const int* __restrict__ src32) {
     constexpr int T = C::T;
     constexpr int E = Dims<C>::E;
     extern __shared__ u64 sm[];
@@ -296,7 +318,10 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
         __syncthreads();
     }
     u64 v[E];
-    load_global<C, 0, T, L>(v, g, thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
+    if constexpr (SRC32)
+        load_global_i32<C, 0, T, L>(v, src32 + tile_base<T, L>(tile, k), thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
+    else
+        load_global<C, 0, T, L>(v, g, thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
     if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     apply_stages<C, 0, L>(v);
     run_rounds<C, L, 1>(v, sm, lane, warp, rank);
@@ -342,6 +367,11 @@ __global__ void __launch_bounds__(1024) k_sort_hits(long long* idx, long long* v
 }
 
 // ---------------------------------------------------------------------------
+__global__ void k_widen_i32(const int* __restrict__ src, long long* __restrict__ dst, uint64_t count) {
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += nth) dst[i] = src[i];
+}
+
 // Small transforms (n <= 13) and the float64 low-bits tiles: each CTA owns a
 // contiguous 2^n tile in shared memory and applies stages 0..n-1 in
 // ascending order (the order of core.py:108, which float64 bit identity

@@ -412,3 +412,16 @@ def test_fold_matches_reference(golden_npz, coracle):
         assert np.array_equal(subspace.fold_generated(spec, rows).cpu().numpy(), want)
         t = signals.make(spec)
         assert np.array_equal(subspace.fold(bw.Signal(t), rows).data.cpu().numpy(), want)
+
+
+def test_int32_inputs_widened(coracle):
+    """int32 inputs: the reference widened to int64 (overflow-free sums)."""
+    rng = np.random.default_rng(32)
+    for n in (0, 1, 5, 12, 13, 14, 15, 19, 22):
+        x = rng.integers(np.iinfo(np.int32).min, np.iinfo(np.int32).max, 1 << n, dtype=np.int64).astype(np.int32)
+        ref = c_fwht(coracle, x.astype(np.int64))
+        out = bw.fwht_widen(torch.from_numpy(x).cuda())
+        assert out.dtype == torch.int64 and np.array_equal(out.cpu().numpy(), ref), n
+        assert np.array_equal(bw.fwht_widen(x).cpu().numpy(), ref)
+    with pytest.raises(errors.BadArguments):
+        bw.fwht_widen(torch.zeros(8, dtype=torch.int64, device="cuda"))
