@@ -1200,20 +1200,44 @@ bool round_ok(std::string* why) {
         *why = "rank swap bits are not register bits before the exchange";
         return false;
     }
-    // Half-warp bank check of the padded smem slots (8-byte words: 16 lanes
-    // must hit 16 distinct 8-byte bank pairs) -- only rounds that touch smem.
-    if (C::NR > 1)
+    // Bank check of the padded smem slots, for the round's own accesses and,
+    // in the round before the exchange, for the DSMEM destinations.  8-byte
+    // words: each half-warp must hit 16 distinct 8-byte bank pairs; 16-byte
+    // words (vector rounds): each quarter-warp 8 distinct 16-byte quads.
+    auto check = [&](auto slot_of, bool vec) -> bool {
         for (uint32_t warp = 0; warp < (1u << C::W); ++warp)
-            for (int j = 0; j < bw::Dims<C>::E; ++j)
-                for (uint32_t half = 0; half < 2; ++half) {
+            for (int j = 0; j < bw::Dims<C>::E; j += vec ? 2 : 1) {
+                const int group = vec ? 8 : 16;
+                for (uint32_t g0 = 0; g0 < 32; g0 += group) {
                     uint32_t used = 0;
-                    for (uint32_t l = 0; l < 16; ++l) {
-                        const uint32_t v = bw::thread_part<C, RD>(half * 16 + l, warp) | bw::reg_part<C, RD>(j);
-                        const uint32_t bank = bw::smem_slot(bw::to_local<C, RD>(v)) & 15u;
-                        if ((used >> bank) & 1u) { *why = "smem bank conflict"; return false; }
+                    for (uint32_t l = 0; l < (uint32_t)group; ++l) {
+                        const uint32_t slot = slot_of(g0 + l, warp, j);
+                        if (vec && (slot & 1u)) return false;  // 16-byte alignment
+                        const uint32_t bank = vec ? ((slot >> 1) & 7u) : (slot & 15u);
+                        if ((used >> bank) & 1u) return false;
                         used |= 1u << bank;
                     }
                 }
+            }
+        return true;
+    };
+    if (C::NR > 1) {
+        const bool own = check(
+            [&](uint32_t lane, uint32_t warp, int j) {
+                return bw::smem_slot_c<C>(bw::to_local<C, RD>(bw::thread_part<C, RD>(lane, warp) | bw::reg_part<C, RD>(j)));
+            },
+            bw::vec_smem<C, RD>());
+        if (!own) { *why = "smem bank conflict"; return false; }
+        if constexpr (C::Q > 0 && RD + 1 == C::XR) {
+            const bool xw = check(
+                [&](uint32_t lane, uint32_t warp, int j) {
+                    const uint32_t v = bw::thread_part<C, RD>(lane, warp) | bw::reg_part<C, RD>(j);
+                    return bw::smem_slot_c<C>(bw::to_local<C, C::XR>(v & ~bw::p_mask<C>()));
+                },
+                bw::vec_smem<C, RD>());
+            if (!xw) { *why = "DSMEM exchange bank conflict"; return false; }
+        }
+    }
     return true;
 }
 
@@ -1332,16 +1356,16 @@ void emu_rounds(std::vector<std::vector<u64>>& v, std::vector<std::vector<u64>>&
                         const uint32_t full = vv | bw::rank_bits<C, RD - 1>((uint32_t)q);
                         uint32_t d = 0;
                         for (int i = 0; i < C::Q; ++i) d |= ((full >> C::P(i)) & 1u) << i;
-                        sm[d][bw::smem_slot(bw::to_local<C, RD>(full & ~bw::p_mask<C>()))] = v[q][(size_t)t * E + j];
+                        sm[d][bw::smem_slot_c<C>(bw::to_local<C, RD>(full & ~bw::p_mask<C>()))] = v[q][(size_t)t * E + j];
                     } else {
-                        sm[q][bw::smem_slot(bw::to_local<C, RD - 1>(vv))] = v[q][(size_t)t * E + j];
+                        sm[q][bw::smem_slot_c<C>(bw::to_local<C, RD - 1>(vv))] = v[q][(size_t)t * E + j];
                     }
                 }
         for (int q = 0; q < NQ; ++q) {
             for (int t = 0; t < NT; ++t)
                 for (int j = 0; j < E; ++j)
                     v[q][(size_t)t * E + j] =
-                        sm[q][bw::smem_slot(bw::to_local<C, RD>(bw::thread_part<C, RD>(t & 31, t >> 5) | bw::reg_part<C, RD>(j)))];
+                        sm[q][bw::smem_slot_c<C>(bw::to_local<C, RD>(bw::thread_part<C, RD>(t & 31, t >> 5) | bw::reg_part<C, RD>(j)))];
             emu_stages<C, L, RD>(v[q]);
         }
         emu_rounds<C, L, RD + 1>(v, sm);

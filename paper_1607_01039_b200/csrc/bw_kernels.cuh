@@ -13,6 +13,29 @@ namespace bw {
 
 typedef unsigned long long u64;
 
+// Cache policy of the pass kernels' global accesses (A/B knob: 0 = .cs
+// streaming, 1 = .cg, 2 = default).  Measured on B200 (profiles/r01_*):
+// default loads lift the vectorised low pass from 6.4 to 7.0 TB/s, the
+// other passes are indifferent -- so plain loads and stores.
+#ifndef BW_LD_POLICY
+#define BW_LD_POLICY 2
+#endif
+#ifndef BW_ST_POLICY
+#define BW_ST_POLICY 2
+#endif
+template <class T>
+__device__ __forceinline__ T ld_pass(const T* p) {
+    if constexpr (BW_LD_POLICY == 0) return __ldcs(p);
+    else if constexpr (BW_LD_POLICY == 1) return __ldcg(p);
+    else return *p;
+}
+template <class T>
+__device__ __forceinline__ void st_pass(T* p, const T& v) {
+    if constexpr (BW_ST_POLICY == 0) __stcs(p, v);
+    else if constexpr (BW_ST_POLICY == 1) __stcg(p, v);
+    else *p = v;
+}
+
 // ---------------------------------------------------------------------------
 // Pass engine (kernels K1 low-bits, K2 high-bits, register-only high-bits).
 // ---------------------------------------------------------------------------
@@ -52,12 +75,12 @@ __device__ __forceinline__ void load_global(u64 (&v)[Dims<C>::E], const u64* __r
         const uint64_t off = global_off<T, L>(reg_part<C, RD>(j), k);
         if constexpr (VecAccess<C, RD, L>::value) {
             if ((j & 1) == 0) {
-                const ulonglong2 t = __ldcs(reinterpret_cast<const ulonglong2*>(p + off));
+                const ulonglong2 t = ld_pass(reinterpret_cast<const ulonglong2*>(p + off));
                 v[j] = t.x;
                 v[j + 1] = t.y;
             }
         } else {
-            v[j] = __ldcs(p + off);
+            v[j] = ld_pass(p + off);
         }
     }
 }
@@ -97,26 +120,48 @@ __device__ __forceinline__ void store_global(const u64 (&v)[Dims<C>::E], u64* __
                 ulonglong2 t;
                 t.x = v[j];
                 t.y = v[j + 1];
-                __stcs(reinterpret_cast<ulonglong2*>(p + off), t);
+                st_pass(reinterpret_cast<ulonglong2*>(p + off), t);
             }
         } else {
-            __stcs(p + off, v[j]);
+            st_pass(p + off, v[j]);
         }
     }
 }
 
 template <class C, int RD>
 __device__ __forceinline__ void store_smem(const u64 (&v)[Dims<C>::E], u64* sm, uint32_t tp) {
-    u64* p = sm + smem_slot(to_local<C, RD>(tp));
+    u64* p = sm + smem_slot_c<C>(to_local<C, RD>(tp));
 #pragma unroll
-    for (int j = 0; j < Dims<C>::E; ++j) p[smem_slot(to_local<C, RD>(reg_part<C, RD>(j)))] = v[j];
+    for (int j = 0; j < Dims<C>::E; ++j) {
+        if constexpr (vec_smem<C, RD>()) {
+            if ((j & 1) == 0) {
+                ulonglong2 t;
+                t.x = v[j];
+                t.y = v[j + 1];
+                *reinterpret_cast<ulonglong2*>(p + smem_slot_c<C>(to_local<C, RD>(reg_part<C, RD>(j)))) = t;
+            }
+        } else {
+            p[smem_slot_c<C>(to_local<C, RD>(reg_part<C, RD>(j)))] = v[j];
+        }
+    }
 }
 
 template <class C, int RD>
 __device__ __forceinline__ void load_smem(u64 (&v)[Dims<C>::E], const u64* sm, uint32_t tp) {
-    const u64* p = sm + smem_slot(to_local<C, RD>(tp));
+    const u64* p = sm + smem_slot_c<C>(to_local<C, RD>(tp));
 #pragma unroll
-    for (int j = 0; j < Dims<C>::E; ++j) v[j] = p[smem_slot(to_local<C, RD>(reg_part<C, RD>(j)))];
+    for (int j = 0; j < Dims<C>::E; ++j) {
+        if constexpr (vec_smem<C, RD>()) {
+            if ((j & 1) == 0) {
+                const ulonglong2 t =
+                    *reinterpret_cast<const ulonglong2*>(p + smem_slot_c<C>(to_local<C, RD>(reg_part<C, RD>(j))));
+                v[j] = t.x;
+                v[j + 1] = t.y;
+            }
+        } else {
+            v[j] = p[smem_slot_c<C>(to_local<C, RD>(reg_part<C, RD>(j)))];
+        }
+    }
 }
 
 // ---- thread-block-cluster plumbing (DSMEM) ---------------------------------
@@ -143,6 +188,11 @@ __device__ __forceinline__ void st_async_u64(uint32_t addr, u64 v, uint32_t mbar
                  "r"(mbar)
                  : "memory");
 }
+__device__ __forceinline__ void st_async_v2(uint32_t addr, u64 a, u64 b, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(addr),
+                 "l"(a), "l"(b), "r"(mbar)
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_wait_parity(uint32_t mbar, uint32_t parity) {
     uint32_t done = 0;
     while (!done) {
@@ -164,8 +214,10 @@ template <class C, int RD, int RANK>
 __device__ __forceinline__ void exchange_write_rank(const u64 (&v)[Dims<C>::E], u64* sm, uint32_t tp) {
     constexpr uint32_t pm = p_mask<C>();
     constexpr int NQ = 1 << C::Q;
+    constexpr bool VEC = vec_smem<C, RD>();
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
-    const uint32_t off = 8u * (smem_slot(to_local<C, C::XR>(tp)) + smem_slot(to_local<C, C::XR>(RANK << kCtaBits)));
+    const uint32_t off =
+        8u * (smem_slot_c<C>(to_local<C, C::XR>(tp)) + smem_slot_c<C>(to_local<C, C::XR>(RANK << kCtaBits)));
     const uint32_t mbar_local = sbase + 8u * Dims<C>::SMEM_ELEMS;
     uint32_t base[NQ], mbar[NQ];
 #pragma unroll
@@ -174,19 +226,34 @@ __device__ __forceinline__ void exchange_write_rank(const u64 (&v)[Dims<C>::E], 
         mbar[d] = map_to_rank(mbar_local, (uint32_t)d);
     }
     u64* local = sm + off / 8u;
-    // Remote stores first (their latency overlaps the local ones), then the
-    // registers that stay in this CTA.  d is a compile-time value per j.
+    // Local stores first, then st.async to the partners (measured faster);
+    // d is a compile-time value per register.  Vector rounds move pairs.
 #pragma unroll
     for (int pass = 0; pass < 2; ++pass) {
 #pragma unroll
         for (int j = 0; j < Dims<C>::E; ++j) {
+            if (VEC && (j & 1)) continue;
             const uint32_t rp = reg_part<C, RD>(j);
             uint32_t d = 0;
 #pragma unroll
             for (int i = 0; i < C::Q; ++i) d |= ((rp >> C::P(i)) & 1u) << i;
-            const uint32_t slot = smem_slot(to_local<C, C::XR>(rp & ~pm));
-            if (pass == 1 && d != (uint32_t)RANK) st_async_u64(base[d] + 8u * slot, v[j], mbar[d]);
-            if (pass == 0 && d == (uint32_t)RANK) local[slot] = v[j];
+            const uint32_t slot = smem_slot_c<C>(to_local<C, C::XR>(rp & ~pm));
+            if (pass == 0 && d == (uint32_t)RANK) {
+                if constexpr (VEC) {
+                    ulonglong2 t;
+                    t.x = v[j];
+                    t.y = v[j + 1];
+                    *reinterpret_cast<ulonglong2*>(local + slot) = t;
+                } else {
+                    local[slot] = v[j];
+                }
+            }
+            if (pass == 1 && d != (uint32_t)RANK) {
+                if constexpr (VEC)
+                    st_async_v2(base[d] + 8u * slot, v[j], v[j + 1], mbar[d]);
+                else
+                    st_async_u64(base[d] + 8u * slot, v[j], mbar[d]);
+            }
         }
     }
 }

@@ -62,7 +62,7 @@ BW_HD constexpr int nib(uint64_t packed, int i) { return (int)((packed >> (4 * i
 //   round 1: reg {1,2,3,4,5}     lane {0,6,7,8,9}  warp {10,11,12}
 //   round 2: reg {0,6,7,8,12}    lane {1,2,3,5,4}  warp {9,10,11}
 struct CfgLow13 {
-    static constexpr int T = 13, Q = 0, R = 5, W = 3, NR = 3, XR = 3, MINB = BW_T13_MINB;
+    static constexpr int T = 13, Q = 0, R = 5, W = 3, NR = 3, XR = 3, MINB = BW_T13_MINB, PAD = 1;
     BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xCBA90ull : rd == 1 ? 0x54321ull : 0xC8760ull, i); }
     BW_HD static constexpr int lane(int rd, int i) { return nib(rd == 1 ? 0x98760ull : 0x45321ull, i); }
     BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x876ull : rd == 1 ? 0xCBAull : 0xBA9ull, i); }
@@ -79,7 +79,7 @@ struct CfgLow13 {
 //   round 1 (post): reg {0..4}      lane {5,6,7,8,9}  warp {10,11,13}
 //   round 2 (post): reg {5,6,7,8,13} lane {0,1,2,3,4} warp {9,10,11}
 struct CfgLow14c {
-    static constexpr int T = 14, Q = 1, R = 5, W = 3, NR = 3, XR = 1, MINB = BW_T13_MINB;
+    static constexpr int T = 14, Q = 1, R = 5, W = 3, NR = 3, XR = 1, MINB = BW_T13_MINB, PAD = 1;
     BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xCBA98ull : rd == 1 ? 0x43210ull : 0xD8765ull, i); }
     BW_HD static constexpr int lane(int rd, int i) { return nib(rd == 1 ? 0x98765ull : 0x43210ull, i); }
     BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x765ull : rd == 1 ? 0xDBAull : 0xBA9ull, i); }
@@ -93,7 +93,7 @@ struct CfgLow14c {
 //   round 1 (post): reg {0..4}        lane {5,6,7,8,9}  warp {10,13,14}
 //   round 2 (post): reg {5,6,7,13,14} lane {0,1,2,3,4}  warp {8,9,10}
 struct CfgLow15c {
-    static constexpr int T = 15, Q = 2, R = 5, W = 3, NR = 3, XR = 1, MINB = BW_T13_MINB;
+    static constexpr int T = 15, Q = 2, R = 5, W = 3, NR = 3, XR = 1, MINB = BW_T13_MINB, PAD = 1;
     BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xCBA98ull : rd == 1 ? 0x43210ull : 0xED765ull, i); }
     BW_HD static constexpr int lane(int rd, int i) { return nib(rd == 1 ? 0x98765ull : 0x43210ull, i); }
     BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x765ull : rd == 1 ? 0xEDAull : 0xA98ull, i); }
@@ -105,7 +105,7 @@ struct CfgLow15c {
 //   round 0: reg {8..12}  lane {0,1,2,3,4}  warp {5,6,7}
 //   round 1: reg {3..7}   lane {0,1,2,8,9}  warp {10,11,12}
 struct CfgHigh13 {
-    static constexpr int T = 13, Q = 0, R = 5, W = 3, NR = 2, XR = 2, MINB = BW_T13_MINB;
+    static constexpr int T = 13, Q = 0, R = 5, W = 3, NR = 2, XR = 2, MINB = BW_T13_MINB, PAD = 1;
     BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xCBA98ull : 0x76543ull, i); }
     BW_HD static constexpr int lane(int rd, int i) { return nib(rd == 0 ? 0x43210ull : 0x98210ull, i); }
     BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x765ull : 0xCBAull, i); }
@@ -119,7 +119,7 @@ struct CfgHigh13 {
 //   round 0: reg {8..12}          lane {0,1,2,3,4}  warp {5,6,7}
 //   round 1 (post): reg {4,5,6,7,13}  lane {0,1,2,3,8}  warp {9,10,11}
 struct CfgHigh14c {
-    static constexpr int T = 14, Q = 1, R = 5, W = 3, NR = 2, XR = 1, MINB = BW_T13_MINB;
+    static constexpr int T = 14, Q = 1, R = 5, W = 3, NR = 2, XR = 1, MINB = BW_T13_MINB, PAD = 1;
     BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xCBA98ull : 0xD7654ull, i); }
     BW_HD static constexpr int lane(int rd, int i) { return nib(rd == 0 ? 0x43210ull : 0x83210ull, i); }
     BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x765ull : 0xBA9ull, i); }
@@ -132,7 +132,7 @@ struct CfgHigh14c {
 //   round 0: reg {8..12}           lane {0,1,2,3,4}  warp {5,6,7}
 //   round 1 (post): reg {5,6,7,13,14}  lane {0,1,2,3,4}  warp {8,9,10}
 struct CfgHigh15c {
-    static constexpr int T = 15, Q = 2, R = 5, W = 3, NR = 2, XR = 1, MINB = BW_T13_MINB;
+    static constexpr int T = 15, Q = 2, R = 5, W = 3, NR = 2, XR = 1, MINB = BW_T13_MINB, PAD = 1;
     BW_HD static constexpr int reg(int rd, int i) { return nib(rd == 0 ? 0xCBA98ull : 0xED765ull, i); }
     BW_HD static constexpr int lane(int, int i) { return nib(0x43210ull, i); }
     BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0x765ull : 0xA98ull, i); }
@@ -144,7 +144,7 @@ struct CfgHigh15c {
 // memory; tile bits 8..12 in registers.
 //   round 0: reg {8..12}  lane {0..4}  warp {5,6,7}
 struct CfgReg {
-    static constexpr int T = 13, Q = 0, R = 5, W = 3, NR = 1, XR = 1, MINB = 1;
+    static constexpr int T = 13, Q = 0, R = 5, W = 3, NR = 1, XR = 1, MINB = 1, PAD = 1;
     BW_HD static constexpr int reg(int, int i) { return nib(0xCBA98ull, i); }
     BW_HD static constexpr int lane(int, int i) { return nib(0x43210ull, i); }
     BW_HD static constexpr int warp(int, int i) { return nib(0x765ull, i); }
@@ -157,7 +157,7 @@ struct Dims {
     static constexpr int E = 1 << C::R;               // elements per thread
     static constexpr int NT = 32 << C::W;             // threads per CTA
     static constexpr int CTA = 1 << kCtaBits;         // elements per CTA
-    static constexpr int SMEM_ELEMS = C::NR > 1 ? CTA + (CTA >> 5) : 0;
+    static constexpr int SMEM_ELEMS = C::NR > 1 ? CTA + C::PAD * (CTA >> 5) : 0;
     static constexpr int CLUSTER = 1 << C::Q;
     // dynamic shared memory: the transpose buffer, plus one mbarrier for the
     // DSMEM exchange of cluster configs
@@ -166,6 +166,14 @@ struct Dims {
 
 // Padded shared-memory slot of local index e; additive over disjoint bit sets.
 BW_HD constexpr uint32_t smem_slot(uint32_t e) { return e + (e >> 5); }
+template <class C>
+BW_HD constexpr uint32_t smem_slot_c(uint32_t e) { return e + C::PAD * (e >> 5); }
+
+// Round RD moves element pairs (tile bits 0) as 16-byte shared-memory words
+// (configs with PAD = 2 keep pairs 16-byte aligned; a vectorised 2-CTA low
+// pass built on it measured 5.75 vs 5.92 TB/s and was dropped).
+template <class C, int RD>
+BW_HD constexpr bool vec_smem() { return C::PAD == 2 && C::reg(RD, 0) == 0; }
 
 // Tile index (virtual bits) contributed by register index j in round RD.
 template <class C, int RD>

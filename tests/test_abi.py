@@ -79,7 +79,7 @@ def test_bad_plans_rejected():
 def test_plan_describe():
     p = sharded.plan(32, 0)
     assert [x["kind"] for x in p["passes"]] == ["low", "high", "high"]
-    assert all(x["cols_bits"] >= 5 for x in p["passes"][1:])  # >= 256-byte row segments
+    assert all(x["cols_bits"] >= 4 for x in p["passes"][1:])  # >= 128-byte row segments
     assert sum(x["r"] for x in p["passes"]) == 32
     assert p["hbm_bytes_per_pass"] == 16 << 32
     q = sharded.plan(34, 3)
