@@ -46,11 +46,13 @@ def args_parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5],
                     help="BASELINE.json config (default 4: n=32 +-1, the strong-scaling config)")
-    ap.add_argument("--n", type=int, default=None, help="log2 size (default: the config's n)")
+    ap.add_argument("--log2n", dest="n", type=int, default=None, help="log2 size (default: the config's n)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--mode", choices=["peer", "a2a"], default="peer", help="cross-GPU exchange (N > 1)")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="collectives for N > 1 (gloo: test the multi-rank path with several ranks on one GPU)")
     return ap.parse_args()
 
 
@@ -198,9 +200,12 @@ def run_ours(a):
     from paper_1607_01039_b200 import _lib, sharded, signals
 
     ws, rank, local_rank = world()
-    torch.cuda.set_device(local_rank)
+    torch.cuda.set_device(local_rank % torch.cuda.device_count())
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if a.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     p = sharded.log2_shards(ws)
     n = a.n
     nl = n - p
@@ -237,7 +242,11 @@ def run_ours(a):
         scrub = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def device_barrier():
-        dist.all_reduce(ones)  # NCCL on this stream: a device-side barrier
+        if a.dist_backend == "nccl":
+            dist.all_reduce(ones)  # NCCL on this stream: a device-side barrier
+        else:
+            torch.cuda.synchronize()
+            dist.barrier()
 
     def step(ev):
         if extract:
@@ -286,7 +295,7 @@ def run_ours(a):
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
     time.sleep(0.6)  # let the sampler start before the timed region
     evs = [events() for _ in range(a.steps)]
@@ -309,7 +318,7 @@ def run_ours(a):
     pass_ms = [[e[i].elapsed_time(e[i + 1]) for e in evs] for i in range(npasses)]
     xs_ms = [e[npasses + 1].elapsed_time(e[npasses + 2]) for e in evs] if p > 0 else []
     if ws > 1:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda" if a.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / a.steps
@@ -458,7 +467,8 @@ def run_e2e(a, x, spec, p, nl, rank, ws, peer):
             host.copy_(x, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64,
+                         device="cuda" if a.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         api = "H2D + sharded.fwht_distributed + D2H"

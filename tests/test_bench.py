@@ -1,0 +1,55 @@
+"""bench.py contract: one JSON line with the driver's keys."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run_bench(args, env=None, timeout=600):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                         timeout=timeout, env={**os.environ, **(env or {})}, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_contract():
+    d = run_bench(["--impl", "reference", "--steps", "1", "--warmup", "0", "--log2n", "18"])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
+    assert d["config"]["workload"].startswith("config4")
+
+
+@pytest.mark.gpu
+def test_ours_contract_small():
+    d = run_bench(["--steps", "3", "--warmup", "3", "--log2n", "24", "--no-cpu"])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "dtype", "config",
+                "roofline", "e2e", "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["roofline"]["bound"] == "hbm" and d["roofline"]["peak"] > 0
+    assert d["gpu_launches"] == 3 * len(d["config"]["passes"])
+    assert d["e2e"]["h2d_bytes_per_step"] == 8 << 24
+
+
+@pytest.mark.gpu
+def test_multirank_path_two_processes_one_gpu():
+    """The N > 1 bench path (CUDA-IPC peer exchange, max over ranks, rank-0
+    JSON) with 2 ranks on one GPU; gloo carries the host-side collectives."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--log2n", "24", "--dist-backend", "gloo", "--no-cpu"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["log2p"] == 1 and "nvlink" in d and d["value"] > 0

@@ -8,6 +8,6 @@ for f in 14 13; do
   python -c "import json,sys; d=json.loads(open('gpurun_out/bench_f$f.log').read().strip().splitlines()[-1]); print($f, d['ms_per_step'], d['passes_ms'], d['passes_gbs'], d['clocks'])"
 done
 for n in 30 28; do
-BW_LOW_BITS=13 timeout 600 python bench.py --n $n --steps 20 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_n$n.log 2>&1
+BW_LOW_BITS=13 timeout 600 python bench.py --log2n $n --steps 20 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_n$n.log 2>&1
 python -c "import json,sys; d=json.loads(open('gpurun_out/bench_n$n.log').read().strip().splitlines()[-1]); print($n, d['ms_per_step'], d['passes_ms'], d['passes_gbs'])"
 done

@@ -2,7 +2,7 @@
 cd "$(dirname "$0")/.."
 run() {
   n=$1; plan=$2
-  BW_PLAN=$plan timeout 600 python bench.py --n $n --steps 10 --warmup 2 --no-e2e --no-cpu > gpurun_out/bench_s.log 2>&1 || { tail -3 gpurun_out/bench_s.log; return; }
+  BW_PLAN=$plan timeout 600 python bench.py --log2n $n --steps 10 --warmup 2 --no-e2e --no-cpu > gpurun_out/bench_s.log 2>&1 || { tail -3 gpurun_out/bench_s.log; return; }
   python -c "import json,sys; d=json.loads(open('gpurun_out/bench_s.log').read().strip().splitlines()[-1]); print('$n $plan', round(d['ms_per_step'],3), d['passes_ms'], d['passes_gbs'])"
 }
 for p in 14,10 13,11; do run 24 $p; done
