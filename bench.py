@@ -50,7 +50,7 @@ def args_parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--mode", choices=["peer", "a2a"], default="peer", help="cross-GPU exchange (N > 1)")
+    ap.add_argument("--mode", choices=["fused", "peer", "a2a"], default="fused", help="cross-GPU exchange (N > 1)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="collectives for N > 1 (gloo: test the multi-rank path with several ranks on one GPU)")
     return ap.parse_args()
@@ -215,12 +215,17 @@ def run_ours(a):
     signals.generate(spec, x, base=rank << nl)
     npasses = L.bw_plan_npasses(nl)
     plan = sharded.plan(n, p)
+    fused = p > 0 and a.mode == "fused"
+    if fused:  # local passes over the low nl - r bits (one bracket), then K6'
+        f_widths, f_r = sharded.fused_plan(nl, p)
+        f_arr = (ctypes.c_int * len(f_widths))(*f_widths)
+        npasses = 1
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
     ptr = x.data_ptr()
     peer = None
     if p > 0:
-        peer = sharded._PeerMap(x, None, dist) if a.mode == "peer" else None
+        peer = sharded._PeerMap(x, None, dist) if a.mode in ("peer", "fused") else None
         ones = torch.ones(1, device="cuda")
         ptrs = (ctypes.c_void_p * ws)(*(peer.ptrs if peer else [ptr] * ws))
         b, c = sharded.slice_of(rank, ws, 1 << nl)
@@ -249,6 +254,17 @@ def run_ours(a):
             dist.barrier()
 
     def step(ev):
+        if fused:
+            ev[0].record(stream)
+            _lib.check(L.bw_fwht_i64_partial(ptr, nl, f_arr, len(f_widths), sh))
+            ev[1].record(stream)
+            device_barrier()  # every shard's local passes done
+            ev[2].record(stream)
+            _lib.check(L.bw_fwht_xfused_pass_i64(ptrs, p, nl, f_r, rank, sh))
+            ev[3].record(stream)
+            device_barrier()  # every fused pass done
+            ev[-1].record(stream)
+            return
         if extract:
             hit_cnt.zero_()
         for i in range(npasses):
@@ -329,6 +345,9 @@ def run_ours(a):
     dom = max(range(npasses), key=lambda i: avg_pass[i])
     achieved = bytes_per_pass / (avg_pass[dom] / 1e3) / 1e9
     launches = a.steps * (npasses + (1 if extract else 0) + (1 if p > 0 else 0))
+    if fused:
+        launches = a.steps * (len(f_widths) + 1)
+        dom_fused = sum(xs_ms) / len(xs_ms)
     traffic = None  # dram read + write of the dominant pass, from the committed ncu capture
     try:
         with open(os.path.join(ROOT, "profiles", f"r01_traffic_n{nl}.json")) as f:
@@ -379,6 +398,17 @@ def run_ours(a):
                               "hits": len(hits_first), "hit_indices": [h[0] for h in hits_first][:16],
                               "planted": sorted(spec.masks),
                               "recovered_planted": sorted(h[0] for h in hits_first) == sorted(spec.masks)}
+    if fused:
+        fb = bytes_per_pass
+        line["config"]["passes"] = {"local_widths": f_widths, "fused_last_pass_stages": f_r + p,
+                                    "fused_last_pass_local_stages": f_r}
+        line["passes_ms"] = {"local_passes": round(avg_pass[0], 4), "fused_pass": round(dom_fused, 4)}
+        line["roofline"].update({"achieved": fb / (dom_fused / 1e3) / 1e9,
+                                 "frac": fb / (dom_fused / 1e3) / 1e9 / peak, "traffic": None,
+                                 "kernel": f"K6' fused last pass ({f_r} local + {p} cross-shard stages)",
+                                 "frac_of_8tbs_spec": fb / (dom_fused / 1e3) / 1e9 / 8000.0})
+        line.pop("passes_gbs", None)
+        line.pop("transform_gbs_per_pass_avg", None)
     if p > 0:
         line["xshard_ms"] = sum(xs_ms) / len(xs_ms)
         nv = 8 * (2 ** nl) * (ws - 1) / ws

@@ -88,6 +88,12 @@ int bw_fwht_i64(int64_t *data, int log2n, void *stream, uint64_t *butterflies);
 int bw_fwht_i64_planned(int64_t *data, int log2n, const int *pass_bits,
                         int npasses, void *stream);
 
+/* Stages [0, sum(pass_bits)) only (pass_bits as for bw_fwht_i64_planned, a
+ * 13+ bit low pass first), applied to every contiguous 2^sum block of the
+ * 2^log2n array -- the local passes of the fused multi-device plan. */
+int bw_fwht_i64_partial(int64_t *data, int log2n, const int *pass_bits, int npasses,
+                        void *stream);
+
 /*
  * Pass-level launches of the default plan (instrumentation: the benchmark
  * records a CUDA event between passes to time each kernel inside the step).
@@ -235,6 +241,22 @@ int bw_xshard_strided_i64(int64_t *base, uint64_t shard_stride, int log2p,
                           uint64_t begin, uint64_t count, void *stream);
 
 /*
+ * Cross-shard stage FUSED into the last local pass (kernel K6').
+ * bw_plan_fused gives the local plan (widths for bw_fwht_i64_planned on each
+ * shard: the low pass and all high passes but the last) and r_last, the local
+ * rows the fused pass takes together with the log2p shard bits
+ * (r_last + log2p <= 9).  bw_fwht_xfused_pass_i64 then runs device `rank`'s
+ * disjoint share of that pass: peer loads of its tiles from all P shards,
+ * r_last local + log2p cross-shard stages, peer stores back -- compute and
+ * NVLink exchange in one kernel.  Every device must have finished its local
+ * passes before any device starts the fused pass (and all must finish before
+ * the result is read).
+ */
+int bw_plan_fused(int log2n_local, int log2p, int *widths, int *nwidths, int *r_last);
+int bw_fwht_xfused_pass_i64(int64_t *const *shards, int log2p, int log2n_local, int r_last,
+                            int rank, void *stream);
+
+/*
  * Peer-memory plumbing for one process per GPU: export a device buffer as a
  * CUDA IPC handle (64 bytes) plus its offset inside the allocation, open a
  * peer's handle (NVLink peer access enabled lazily), close it again.
@@ -335,6 +357,12 @@ int bw_plan_describe(int log2n, int log2p, char *json, size_t len);
  */
 int bw_plan_check(int log2n, const int *pass_bits, int npasses,
                   uint64_t *butterflies);
+
+/* Static checker of the multi-device plan with the fused cross-shard pass:
+ * every (shard, index) loaded and stored once per pass over all devices,
+ * every stage of the 2^(n_local+log2p) transform applied once.
+ * n_local <= 24. */
+int bw_plan_check_fused(int log2n_local, int log2p, uint64_t *butterflies);
 
 /*
  * TEST HOOK ONLY -- never used by any product entry point.  Executes the

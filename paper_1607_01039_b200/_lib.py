@@ -50,6 +50,7 @@ _SIGNATURES = {
     "bw_fwht_i64_pass_extract": ([P, I32, I32, U64, U64, P, P, U64, P, P], I32),
     "bw_sort_hits_i64": ([P, P, P, P], I32),
     "bw_fwht_widen_i32": ([P, P, I32, P, PU64], I32),
+    "bw_fwht_i64_partial": ([P, I32, ctypes.POINTER(I32), I32, P], I32),
     "bw_fwht_f64": ([P, I32, P, PU64], I32),
     "bw_minmax_i64": ([P, U64, P, P], I32),
     "bw_check_bound_i64": ([P, I32, P, P, PU64], I32),
@@ -62,6 +63,8 @@ _SIGNATURES = {
     "bw_sumsq_partials_i64": ([P, U64, P, I32, P], I32),
     "bw_fold_i64": ([P, I32, PU64, I32, P, P], I32),
     "bw_fold_gen_i64": ([I32, I32, U64, PU64, I32, PU64, I32, P, P], I32),
+    "bw_plan_fused": ([I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32)], I32),
+    "bw_fwht_xfused_pass_i64": ([ctypes.POINTER(P), I32, I32, I32, I32, P], I32),
     "bw_xshard_i64": ([ctypes.POINTER(P), I32, U64, U64, P], I32),
     "bw_xshard_strided_i64": ([P, U64, I32, U64, U64, P], I32),
     "bw_ipc_get_handle": ([P, P, PU64], I32),
@@ -75,6 +78,7 @@ _SIGNATURES = {
     "bw_extract_scratch_bytes": ([I32], U64),
     "bw_plan_describe": ([I32, I32, ctypes.c_char_p, ctypes.c_size_t], I32),
     "bw_debug_emulate_i64": ([P, I32, ctypes.POINTER(I32), I32], I32),
+    "bw_plan_check_fused": ([I32, I32, PU64], I32),
     "bw_plan_check": ([I32, ctypes.POINTER(I32), I32, PU64], I32),
 }
 

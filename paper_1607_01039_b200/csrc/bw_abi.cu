@@ -230,7 +230,7 @@ int default_plan(int n, std::vector<int>* widths) {
     return BW_OK;
 }
 
-int build_passes(int n, const std::vector<int>& widths, std::vector<Pass>* passes) {
+int build_passes(int n, const std::vector<int>& widths, std::vector<Pass>* passes, bool partial = false) {
     passes->clear();
     if (n == 0) {
         if (!widths.empty()) return fail(BW_BAD_ARGUMENTS, "n = 0 takes no passes");
@@ -266,7 +266,7 @@ int build_passes(int n, const std::vector<int>& widths, std::vector<Pass>* passe
         }
         k += r;
     }
-    if (k != n) return fail(BW_BAD_ARGUMENTS, "pass widths cover %d bits, signal has %d", k, n);
+    if (k != n && !(partial && k < n)) return fail(BW_BAD_ARGUMENTS, "pass widths cover %d bits, signal has %d", k, n);
     return BW_OK;
 }
 
@@ -282,7 +282,31 @@ int for_all_pass_kernels(F&& f) {
     return BW_OK;
 }
 
+template <int LOGP, int L>
+int set_fused_attr() {
+    if constexpr (L + LOGP <= 12)
+        BW_CUDA(cudaFuncSetAttribute(bw::k_pass_x<bw::CfgHigh13, L, LOGP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     bw::Dims<bw::CfgHigh13>::SMEM_BYTES));
+    return BW_OK;
+}
+template <int LOGP>
+int set_fused_attrs() {
+    BW_TRY((set_fused_attr<LOGP, 3>()));
+    BW_TRY((set_fused_attr<LOGP, 4>()));
+    BW_TRY((set_fused_attr<LOGP, 5>()));
+    BW_TRY((set_fused_attr<LOGP, 6>()));
+    BW_TRY((set_fused_attr<LOGP, 7>()));
+    BW_TRY((set_fused_attr<LOGP, 8>()));
+    BW_TRY((set_fused_attr<LOGP, 9>()));
+    BW_TRY((set_fused_attr<LOGP, 10>()));
+    BW_TRY((set_fused_attr<LOGP, 11>()));
+    return BW_OK;
+}
+
 int set_all_pass_attributes() {
+    BW_TRY(set_fused_attrs<1>());
+    BW_TRY(set_fused_attrs<2>());
+    BW_TRY(set_fused_attrs<3>());
     return for_all_pass_kernels([](auto t, auto l) -> int {
         using C = typename decltype(t)::type;
         constexpr int L = decltype(l)::value;
@@ -537,6 +561,28 @@ int bw_sort_hits_i64(int64_t* idx, int64_t* val, const uint64_t* count_dev, void
                                                        reinterpret_cast<long long*>(val),
                                                        reinterpret_cast<const unsigned long long*>(count_dev));
     BW_LAUNCHED("k_sort_hits launch");
+    return BW_OK;
+}
+
+// Stages [0, sum(pass_bits)) only, on every 2^sum block of a 2^log2n array
+// (the local passes of the fused multi-device plan).
+int bw_fwht_i64_partial(int64_t* data, int log2n, const int* pass_bits, int npasses, void* stream) {
+    BW_TRY(check_signal(data, log2n));
+    if (!pass_bits || npasses < 1) return fail(BW_BAD_ARGUMENTS, "empty pass list");
+    if (log2n >= bw::kCtaBits && (reinterpret_cast<uintptr_t>(data) & 15u))
+        return fail(BW_BAD_ARGUMENTS, "partial transforms need a 16-byte aligned signal");
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    std::vector<int> w(pass_bits, pass_bits + npasses);
+    std::vector<Pass> passes;
+    int covered = 0;
+    for (int x : w) covered += x & 15;
+    if (covered > log2n) return fail(BW_BAD_ARGUMENTS, "pass widths cover %d bits, signal has %d", covered, log2n);
+    BW_TRY(build_passes(covered, w, &passes));  // the plan is validated on its own bits
+    for (const Pass& p : passes) {
+        if (p.kind == SMALL) return fail(BW_BAD_ARGUMENTS, "partial transforms need a 13+ bit low pass");
+        BW_TRY(launch_pass(p, reinterpret_cast<u64*>(data), log2n, as_stream(stream)));
+    }
     return BW_OK;
 }
 
@@ -880,6 +926,104 @@ int bw_fold_gen_i64(int d_in, int kind, uint64_t seed, const uint64_t* params, i
     bw::GenParams g;
     BW_TRY(gen_params(kind, seed, params, nparams, &g));
     return fold_impl(nullptr, d_in, col_masks, d_out, out_dev, g, as_stream(stream));
+}
+
+// ---- multi-device plan with the cross-shard stage fused into the last pass --
+//
+// Local plan = low pass + high passes over n_local bits except the last r
+// bits, which the fused pass (kernel K6') covers together with the log2 P
+// shard bits: r + log2 P <= 9, so the fused tile keeps >= 128-byte rows.
+}  // extern "C"
+namespace {
+constexpr int kFusedMaxRows = 9;
+
+int fused_plan(int nl, int p, std::vector<int>* local, int* r_last) {
+    if (p < 1 || p > BW_MAX_LOG2P) return fail(BW_INVALID_WORKERS, "log2p = %d outside 1..%d", p, BW_MAX_LOG2P);
+    const int w0 = 13;
+    if (nl < w0 + 1) return fail(BW_BAD_ARGUMENTS, "fused cross-shard plan needs n_local >= %d", w0 + 1);
+    const int h = nl - w0;
+    const int r = h < kFusedMaxRows - p ? h : kFusedMaxRows - p;
+    if (r < 1) return fail(BW_BAD_ARGUMENTS, "no room for the fused pass");
+    local->assign(1, w0);
+    const int rest = h - r;
+    if (rest > 0) {
+        const int q = (rest + bw::kMaxHighBits - 1) / bw::kMaxHighBits;
+        for (int i = 0; i < q; ++i) local->push_back(rest / q + (i < rest % q ? 1 : 0));
+    }
+    *r_last = r;
+    return BW_OK;
+}
+
+template <int LOGP, class F>
+int with_fused_kernel(int L, F&& f) {
+    switch (L) {
+        case 3: return f(ic<3>{});
+        case 4: return f(ic<4>{});
+        case 5: return f(ic<5>{});
+        case 6: return f(ic<6>{});
+        case 7: return f(ic<7>{});
+        case 8: return f(ic<8>{});
+        case 9: return f(ic<9>{});
+        case 10: return f(ic<10>{});
+        case 11: return f(ic<11>{});
+        default: return fail(BW_BAD_ARGUMENTS, "no fused kernel for %d column bits", L);
+    }
+}
+}  // namespace
+extern "C" {
+
+int bw_plan_fused(int log2n_local, int log2p, int* widths, int* nwidths, int* r_last) {
+    if (!widths || !nwidths || !r_last) return fail(BW_BAD_ARGUMENTS, "null argument");
+    std::vector<int> w;
+    int r = 0;
+    BW_TRY(fused_plan(log2n_local, log2p, &w, &r));
+    if ((int)w.size() > *nwidths) return fail(BW_BAD_ARGUMENTS, "widths array too small");
+    for (size_t i = 0; i < w.size(); ++i) widths[i] = w[i];
+    *nwidths = (int)w.size();
+    *r_last = r;
+    return BW_OK;
+}
+
+// Device `rank`'s share of the fused last pass (K6') over the P shards.
+int bw_fwht_xfused_pass_i64(int64_t* const* shards, int log2p, int log2n_local, int r_last, int rank, void* stream) {
+    if (!shards || log2p < 1 || log2p > BW_MAX_LOG2P) return fail(BW_INVALID_WORKERS, "bad shard list");
+    const int P = 1 << log2p;
+    if (rank < 0 || rank >= P) return fail(BW_INVALID_WORKERS, "rank %d outside 0..%d", rank, P - 1);
+    const int TL = 13 - log2p, L = TL - r_last;
+    if (r_last < 1 || L < 3 || log2n_local < TL + log2p)
+        return fail(BW_BAD_ARGUMENTS, "bad fused pass: n_local=%d r=%d p=%d", log2n_local, r_last, log2p);
+    bw::ShardPtrs sp;
+    memset(&sp, 0, sizeof sp);
+    for (int i = 0; i < P; ++i) {
+        if (!shards[i] || (reinterpret_cast<uintptr_t>(shards[i]) & 15u))
+            return fail(BW_BAD_ARGUMENTS, "shard %d is null or not 16-byte aligned", i);
+        sp.p[i] = reinterpret_cast<u64*>(shards[i]);
+    }
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    const int k = log2n_local - r_last;
+    const uint64_t tiles = 1ull << (log2n_local - TL), per = tiles >> log2p;
+    cudaStream_t s = as_stream(stream);
+    auto go = [&](auto lp) -> int {
+        constexpr int LOGP = decltype(lp)::value;
+        return with_fused_kernel<LOGP>(L, [&](auto l) -> int {
+            constexpr int LL = decltype(l)::value;
+            if constexpr (LL + LOGP <= 12) {
+                bw::k_pass_x<bw::CfgHigh13, LL, LOGP>
+                    <<<(unsigned)per, bw::Dims<bw::CfgHigh13>::NT, bw::Dims<bw::CfgHigh13>::SMEM_BYTES, s>>>(
+                        sp, k, (uint64_t)rank * per);
+                BW_LAUNCHED("k_pass_x launch");
+                return BW_OK;
+            } else {
+                return fail(BW_BAD_ARGUMENTS, "no fused kernel for L=%d p=%d", LL, LOGP);
+            }
+        });
+    };
+    switch (log2p) {
+        case 1: return go(ic<1>{});
+        case 2: return go(ic<2>{});
+        default: return go(ic<3>{});
+    }
 }
 
 // Cross-shard butterfly (parallel.py:103-110, all log2 P stage phases fused).
@@ -1465,5 +1609,72 @@ extern "C" int bw_debug_emulate_i64(int64_t* host, int log2n, const int* pass_bi
             return BW_OK;
         }));
     }
+    return BW_OK;
+}
+
+// Static checker of the fused cross-shard pass (mirror of check_disjoint /
+// total_butterflies over all P devices): walks every device's tiles with
+// the kernel's own address tables and verifies that each (shard, index) is
+// loaded and stored exactly once and that the pass covers the stages
+// [n_local - r_last, n_local) plus every shard bit.  n_local <= 24.
+namespace {
+template <int LOGP, int L>
+int check_fused(int nl, int r_last, uint64_t* bfly) {
+    using C = bw::CfgHigh13;
+    constexpr int T = C::T, TL = T - LOGP, P = 1 << LOGP, LAST = C::NR - 1;
+    const int k = nl - r_last;
+    if (TL - L != r_last) return fail(BW_BAD_ARGUMENTS, "inconsistent fused shape");
+    std::vector<uint8_t> touched((size_t)P << nl, 0);
+    const uint64_t tiles = 1ull << (nl - TL), per = tiles >> LOGP;
+    for (int rank = 0; rank < P; ++rank)
+        for (uint64_t b = 0; b < per; ++b) {
+            const uint64_t base = bw::tile_base<TL, L>((uint64_t)rank * per + b, k);
+            for (uint32_t t = 0; t < (uint32_t)bw::Dims<C>::NT; ++t)
+                for (int j = 0; j < bw::Dims<C>::E; ++j) {
+                    const uint32_t ei = bw::thread_part<C, 0>(t & 31, t >> 5) | bw::reg_part<C, 0>(j);
+                    const uint32_t eo = bw::thread_part<C, LAST>(t & 31, t >> 5) | bw::reg_part<C, LAST>(j);
+                    const uint64_t gi = ((uint64_t)(ei >> TL) << nl) + base + bw::global_off<TL, L>(ei & ((1u << TL) - 1u), k);
+                    const uint64_t go = ((uint64_t)(eo >> TL) << nl) + base + bw::global_off<TL, L>(eo & ((1u << TL) - 1u), k);
+                    if (gi >= touched.size() || go >= touched.size()) return fail(BW_BAD_ARGUMENTS, "fused pass out of range");
+                    if ((touched[gi] & 1) || (touched[go] & 2)) return fail(BW_BAD_ARGUMENTS, "fused pass touches an element twice");
+                    touched[gi] |= 1;
+                    touched[go] |= 2;
+                }
+        }
+    for (uint8_t x : touched)
+        if (x != 3) return fail(BW_BAD_ARGUMENTS, "fused pass misses an element");
+    // stages: CfgHigh13 stages every tile bit >= L = r_last local rows + LOGP shard bits
+    uint32_t staged = 0;
+    for (int rd = 0; rd < C::NR; ++rd) staged |= C::stage(rd) & ~((1u << L) - 1u);
+    if (staged != ((1u << T) - 1u) & ~((1u << L) - 1u)) return fail(BW_BAD_ARGUMENTS, "fused pass stage coverage");
+    *bfly = (uint64_t)(r_last + LOGP) << (nl + LOGP - 1);
+    return BW_OK;
+}
+}  // namespace
+
+extern "C" int bw_plan_check_fused(int log2n_local, int log2p, uint64_t* butterflies) {
+    if (log2n_local > 24) return fail(BW_BAD_ARGUMENTS, "checker supports n_local <= 24");
+    std::vector<int> w;
+    int r = 0;
+    BW_TRY(fused_plan(log2n_local, log2p, &w, &r));
+    uint64_t local_bf = 0;
+    BW_TRY(bw_plan_check(log2n_local - r, w.data(), (int)w.size(), &local_bf));  // the local passes' bits
+    const int L = 13 - log2p - r;
+    uint64_t bf = 0;
+    auto go = [&](auto lp) -> int {
+        constexpr int LOGP = decltype(lp)::value;
+        return with_fused_kernel<LOGP>(L, [&](auto l) -> int {
+            constexpr int LL = decltype(l)::value;
+            if constexpr (LL + LOGP <= 12) return check_fused<LOGP, LL>(log2n_local, r, &bf);
+            return fail(BW_BAD_ARGUMENTS, "no fused kernel");
+        });
+    };
+    int st = log2p == 1 ? go(ic<1>{}) : log2p == 2 ? go(ic<2>{}) : go(ic<3>{});
+    if (st != BW_OK) return st;
+    // total over the 2^(n+p) signal: P shards x local stages + the fused pass
+    const int n = log2n_local + log2p;
+    const uint64_t total = ((uint64_t)(log2n_local - r) << (log2n_local - 1)) * (1u << log2p) + bf;
+    if (total != (uint64_t)n << (n - 1)) return fail(BW_BAD_ARGUMENTS, "butterfly count %llu != n*2^(n-1)", (unsigned long long)total);
+    if (butterflies) *butterflies = total;
     return BW_OK;
 }

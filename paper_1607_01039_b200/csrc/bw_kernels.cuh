@@ -590,6 +590,46 @@ __global__ void __launch_bounds__(256) k_xshard(ShardPtrs s, uint64_t begin, uin
 }
 
 // ---------------------------------------------------------------------------
+// K6': the last local high pass FUSED with the cross-shard stage.  The tile
+// of a single-CTA high pass (C::T bits) is split as L columns, r local rows
+// at stride 2^k, and the top LOGP bits = the shard index: every CTA loads its
+// tile rows from all P shards (peer pointers over NVLink), applies the r
+// local stages AND the log2 P cross-shard stages, and stores back to every
+// shard -- one kernel, compute and exchange fused.  Each device runs the
+// tiles [tile0, tile0 + gridDim.x); the devices' tile ranges are disjoint
+// (the check_disjoint argument, parallel.py:114-134).  Shard bits are
+// register bits when loading (compile-time pointer per register) and warp
+// bits when storing (warp-uniform pointer).
+// ---------------------------------------------------------------------------
+template <class C, int L, int LOGP>
+__global__ void __launch_bounds__(Dims<C>::NT, C::MINB) k_pass_x(ShardPtrs s, int k, uint64_t tile0) {
+    static_assert(C::Q == 0, "fused cross-shard pass: single-CTA tiles");
+    constexpr int T = C::T, E = Dims<C>::E, TL = T - LOGP, LAST = C::NR - 1;
+    constexpr uint32_t lmask = (1u << TL) - 1u;
+    static_assert((thread_part_bits<C, 0>() >> TL) == 0, "shard bits must be register bits at load time");
+    static_assert((reg_part<C, LAST>(Dims<C>::E - 1) >> TL) == 0, "shard bits must be lane/warp bits at store time");
+    extern __shared__ u64 sm[];
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint64_t base = tile_base<TL, L>(tile0 + blockIdx.x, k);  // within a shard
+    u64 v[E];
+    {
+        const uint64_t t0 = base + global_off<TL, L>(thread_part<C, 0>(lane, warp), k);
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            const uint32_t e = reg_part<C, 0>(j);
+            v[j] = ld_pass(s.p[e >> TL] + t0 + global_off<TL, L>(e & lmask, k));
+        }
+    }
+    apply_stages<C, 0, L>(v);
+    run_rounds<C, L, 1>(v, sm, lane, warp, 0u);
+    const uint32_t tp = thread_part<C, LAST>(lane, warp);
+    u64* dst = s.p[tp >> TL] + base + global_off<TL, L>(tp & lmask, k);
+#pragma unroll
+    for (int j = 0; j < E; ++j) st_pass(dst + global_off<TL, L>(reg_part<C, LAST>(j), k), v[j]);
+}
+
+// ---------------------------------------------------------------------------
 // K4: seeded counter-based generators (oracle/oracle_np.py restates them).
 // ---------------------------------------------------------------------------
 __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {

@@ -11,10 +11,18 @@ The slices are disjoint, which is the check_disjoint argument of
 parallel.py:114-134, so the in-place exchange needs only two barriers
 (before: every local transform done; after: every exchange done).
 
-Three drivers share that kernel:
+The exchange can also be FUSED into the last local pass (kernel K6',
+``bw_fwht_xfused_pass_i64``): the last local high pass's tile is extended
+with the P shard bits, so one kernel loads its rows from every shard over
+NVLink, applies the last local stages and the log2 P cross stages, and
+stores back -- one HBM round trip fewer than local passes + a separate
+exchange.  ``fused=True`` / ``mode="fused"`` select it.
+
+Three drivers share these kernels:
   * ``fwht_shards``      -- one process, shards on one or several devices
                             (single-GPU P-shard emulation, or P2P over NVLink).
   * ``fwht_distributed`` -- one process per GPU (torch.distributed):
+      mode="fused" (default): local passes, then K6' over peer pointers;
       mode="peer": CUDA IPC peer pointers, the K6 kernel reads and writes the
                    peers' HBM directly over NVLink (fused compute+exchange);
       mode="a2a":  all-to-all transpose + local K6 on the receive slots +
@@ -72,6 +80,35 @@ def slice_of(rank: int, world: int, local_len: int) -> tuple[int, int]:
     return 2 * lo, 2 * (hi - lo)
 
 
+def fused_plan(n_local: int, p: int) -> tuple[list[int], int]:
+    """(local pass widths, r_last) of the fused multi-device plan."""
+    widths = (ctypes.c_int * 8)()
+    nw = ctypes.c_int(8)
+    r = ctypes.c_int(0)
+    _lib.check(_lib.lib().bw_plan_fused(n_local, p, widths, ctypes.byref(nw), ctypes.byref(r)))
+    return [widths[i] for i in range(nw.value)], int(r.value)
+
+
+def plan_check_fused(n_local: int, p: int) -> int:
+    """Static checker of the fused multi-device plan (bw_plan_check_fused)."""
+    bf = ctypes.c_uint64(0)
+    _lib.check(_lib.lib().bw_plan_check_fused(n_local, p, ctypes.byref(bf)))
+    return int(bf.value)
+
+
+def _local_partial(t: torch.Tensor, n_local: int, widths: list[int]) -> None:
+    arr = (ctypes.c_int * len(widths))(*widths)
+    with torch.cuda.device(t.device):
+        _lib.check(_lib.lib().bw_fwht_i64_partial(t.data_ptr(), n_local, arr, len(widths), _stream_handle(t)))
+
+
+def _fused_pass(ptrs: list[int], p: int, n_local: int, r: int, rank: int, dev: torch.device) -> None:
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().bw_fwht_xfused_pass_i64(arr, p, n_local, r, rank,
+                                                      torch.cuda.current_stream(dev).cuda_stream))
+
+
 # ------------------------------------------------------- single process ---
 
 def xshard(shards: list[torch.Tensor], begin: int = 0, count: int | None = None) -> None:
@@ -86,7 +123,7 @@ def xshard(shards: list[torch.Tensor], begin: int = 0, count: int | None = None)
                                         torch.cuda.current_stream(dev).cuda_stream))
 
 
-def fwht_shards(shards: list[torch.Tensor]) -> int:
+def fwht_shards(shards: list[torch.Tensor], fused: bool = False) -> int:
     """Transform the 2**n signal whose P = len(shards) contiguous shards are
     given (shard r = indices r*2**(n-p) ...), in place.  Shards may live on
     one device (emulation of P GPUs) or on P devices (P2P over NVLink).
@@ -97,12 +134,29 @@ def fwht_shards(shards: list[torch.Tensor]) -> int:
         if s.numel() != local or s.dtype != torch.int64 or not s.is_cuda or not s.is_contiguous():
             raise BadArguments("shards must be equal-length contiguous CUDA int64 tensors")
     n_local = local.bit_length() - 1
+    devices = sorted({s.device.index for s in shards})
+    if fused and p > 0 and n_local >= 14:
+        widths, r = fused_plan(n_local, p)
+        for s in shards:  # local passes over the low n_local - r bits
+            _local_partial(s, n_local, widths)
+        for d in devices:
+            torch.cuda.synchronize(d)
+            if len(devices) > 1:
+                with torch.cuda.device(d):
+                    for q in devices:
+                        _lib.check(_lib.lib().bw_enable_peer_access(q))
+        ptrs = [s.data_ptr() for s in shards]
+        for g, s in enumerate(shards):  # device g runs its share of K6'
+            _fused_pass(ptrs, p, n_local, r, g, s.device)
+        for d in devices:
+            torch.cuda.synchronize(d)
+        n = n_local + p
+        return n << (n - 1)
     for s in shards:  # parallel.py phase 0: independent local transforms
         with torch.cuda.device(s.device):
             fwht_array(s)
     if p == 0:
         return (n_local) << max(n_local - 1, 0)
-    devices = sorted({s.device.index for s in shards})
     if len(devices) > 1:
         for d in devices:  # barrier (i): every local transform done
             torch.cuda.synchronize(d)
@@ -170,11 +224,17 @@ class _PeerMap:
         self.opened = []
 
 
-def fwht_distributed(local: torch.Tensor, group=None, mode: str = "peer", backend=None,
+def fwht_distributed(local: torch.Tensor, group=None, mode: str = "fused", backend=None,
                      peer_map: _PeerMap | None = None) -> int:
     """Rank r holds shard r (indices r*2**(n-p) ... of a 2**n signal).
     Transforms the whole signal in place across the group; returns
-    n * 2**(n-1).  Must be called by every rank of ``group``."""
+    n * 2**(n-1).  Must be called by every rank of ``group``.
+
+    mode="fused" (default): local passes over the low bits, then K6' (the
+    last local pass and the cross-shard stages in one kernel over peer
+    pointers); shards under 2**14 points use mode="peer".  mode="peer": full
+    local transform, then K6 over peer pointers.  mode="a2a": full local
+    transform, then all-to-all + K6 on the received slots + all-to-all."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
@@ -183,8 +243,24 @@ def fwht_distributed(local: torch.Tensor, group=None, mode: str = "peer", backen
     backend = backend or CudaBackend()
     local_len = local.numel()
     n_local = local_len.bit_length() - 1
-    backend.local_fwht(local)  # parallel.py phase 0
     n = n_local + p
+    if mode == "fused" and p > 0 and n_local >= 14:
+        if not local.is_cuda:
+            raise BadArguments("mode='fused' needs CUDA shards")
+        widths, r = fused_plan(n_local, p)
+        _local_partial(local, n_local, widths)
+        pm = peer_map or _PeerMap(local, group, dist)
+        backend.sync(local)
+        dist.barrier(group)  # (i) every shard's local passes are done
+        _fused_pass(pm.ptrs, p, n_local, r, rank, local.device)
+        backend.sync(local)
+        dist.barrier(group)  # (ii) every fused pass is done
+        if peer_map is None:
+            pm.close()
+        return n << (n - 1)
+    if mode == "fused":
+        mode = "peer"
+    backend.local_fwht(local)  # parallel.py phase 0
     if p == 0:
         return n << max(n - 1, 0)
     if mode == "peer":

@@ -41,6 +41,20 @@ def test_default_plan_checker(n):
     assert sharded.plan_check(n) == n << max(n - 1, 0)
 
 
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_fused_plan_checker(p):
+    """The fused multi-device plan (local passes + K6' last pass with the
+    shard bits): every element of every shard once per pass, every stage of
+    the 2^(n_local+p) transform exactly once."""
+    for nl in range(14, 31):
+        widths, r = sharded.fused_plan(nl, p)
+        assert widths[0] == 13 and sum(widths) + r == nl and 1 <= r <= 9 - p
+        if nl > 24:  # the checker's bitmap limit; the plans above repeat the n=24 shapes
+            continue
+        n = nl + p
+        assert sharded.plan_check_fused(nl, p) == n << (n - 1)
+
+
 def splits(h):
     """Every composition of h into parts of 1..10."""
     if h == 0:

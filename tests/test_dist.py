@@ -89,7 +89,7 @@ def test_a2a_orchestration_gloo(tmp_path, coracle, world):
     assert np.array_equal(got, ref)
 
 
-def _peer_worker(rank, world, port, n, out_dir):
+def _peer_worker(rank, world, port, n, out_dir, mode="peer"):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -102,7 +102,7 @@ def _peer_worker(rank, world, port, n, out_dir):
     nl = n - p
     x = oracle_np.gen(2, 7, [1 << 20], rank << nl, 1 << nl)
     t = torch.from_numpy(x).cuda()
-    bf = sharded.fwht_distributed(t, mode="peer")
+    bf = sharded.fwht_distributed(t, mode=mode)
     assert bf == n << (n - 1)
     np.save(os.path.join(out_dir, f"shard{rank}.npy"), t.cpu().numpy())
     dist.barrier()
@@ -110,11 +110,12 @@ def _peer_worker(rank, world, port, n, out_dir):
 
 
 @pytest.mark.gpu
-def test_peer_ipc_two_processes_one_gpu(tmp_path, coracle):
+@pytest.mark.parametrize("mode", ["peer", "fused"])
+def test_peer_ipc_two_processes_one_gpu(tmp_path, coracle, mode):
     from oracle import oracle_np
 
     n, world = 20, 2
-    mp.spawn(_peer_worker, args=(world, free_port(), n, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_peer_worker, args=(world, free_port(), n, str(tmp_path), mode), nprocs=world, join=True)
     got = np.concatenate([np.load(tmp_path / f"shard{r}.npy") for r in range(world)])
     ref = oracle_np.gen(2, 7, [1 << 20], 0, 1 << n)
     coracle.oracle_fwht_i64(ref.ctypes.data, n)

@@ -310,6 +310,20 @@ def test_sharded_emulation(coracle, P):
         assert np.array_equal(np.concatenate([s.cpu().numpy() for s in shards]), ref)
 
 
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_sharded_fused_emulation(coracle, P):
+    """The fused plan (K6' = last local pass + cross-shard stages in one
+    kernel) on P buffers of one device equals the serial transform."""
+    p = P.bit_length() - 1
+    for nl in (14, 16, 19, 22):
+        n = nl + p
+        x = oracle_np.gen(2, 70 + n, [1 << 20], 0, 1 << n)
+        ref = c_fwht(coracle, x)
+        shards = [dev(c) for c in np.split(x, P)]
+        assert sharded.fwht_shards(shards, fused=True) == n << (n - 1)
+        assert np.array_equal(np.concatenate([s.cpu().numpy() for s in shards]), ref), (P, nl)
+
+
 def test_xshard_strided_matches_per_pointer():
     x = oracle_np.gen(2, 9, [1 << 20], 0, 1 << 16)
     a = dev(x)
