@@ -169,17 +169,83 @@ int visit_pass(const Pass& p, F&& f) {
     }
 }
 
-// Cluster size of a high pass by default: 9 and 10 stages run on a cluster
-// of 2 (a 2^14 tile keeps 256-/128-byte row segments); the 4-CTA shapes
-// are kept for tests and experiments (measured slower).
+// Cluster size of a high pass when a plan entry does not force one (the
+// out-of-core chunks and the fused multi-device plan): 9 and 10 stages run
+// on a cluster of 2 (a 2^14 tile keeps 256-/128-byte row segments).
 int high_default_q(int r) { return r <= 8 ? 0 : 1; }
 
-// Relative cost of a pass shape beyond its HBM round trip (measured on
-// B200, profiles/: a 2-CTA low pass runs at 80-90% of the 1-CTA one and
-// varies by box, 10-stage high passes at ~90%, 4-CTA low passes at ~70%).
-int pass_cost(bool low, int w) {
-    if (low) return w == 13 ? 0 : w == 14 ? 3 : 5;
-    return w == 10 ? 2 : 0;
+// ---- measured cost model of the default planner --------------------------
+// HBM TB/s of every pass shape the planner can emit, by the stage bit k the
+// pass starts at (tools/sweep_shapes.py on one B200, profiles/r01_shapes_*;
+// n = 32 and 34 agree to 1%: the rate depends on the row stride 2^k and the
+// row-segment length, not on n).  A pass moves 16 B/point whatever its
+// shape, so a plan's time is proportional to sum(1 / rate).
+// generated by tools/gen_shape_table.py from profiles/r01_shapes_n34.json (NVIDIA B200)
+// low passes 13 / 14 / 15 bits:
+constexpr int kLowEff[3] = {701, 593, 450};
+// rows: reg r=3,4,5; high r=6..10 x q=0,1.  columns: k = 13..31
+constexpr int kShapeEff[13][19] = {
+    {695, 695, 682, 696, 695, 691, 691, 685, 685, 687, 688, 688, 689, 689, 691, 690, 687, 687, 688},  // r=3 q=0
+    {698, 698, 698, 696, 668, 689, 686, 681, 683, 683, 684, 686, 686, 686, 685, 683, 682, 683, 683},  // r=4 q=0
+    {662, 662, 659, 652, 644, 640, 639, 637, 636, 636, 639, 638, 639, 638, 639, 628, 628, 628, 628},  // r=5 q=0
+    {684, 697, 694, 678, 670, 664, 642, 616, 610, 619, 624, 606, 594, 594, 595, 600, 600, 600, 600},  // r=6 q=0
+    {624, 622, 621, 616, 616, 614, 613, 611, 612, 613, 614, 614, 614, 613, 610, 604, 604, 604, 604},  // r=6 q=1
+    {681, 684, 676, 647, 659, 640, 633, 628, 630, 636, 626, 612, 616, 614, 607, 607, 607, 607, 607},  // r=7 q=0
+    {626, 625, 623, 624, 625, 622, 625, 622, 616, 619, 622, 624, 623, 625, 622, 622, 622, 622, 622},  // r=7 q=1
+    {648, 642, 628, 645, 645, 634, 632, 636, 625, 619, 618, 596, 612, 617, 617, 617, 617, 617, 617},  // r=8 q=0
+    {666, 653, 646, 648, 645, 654, 654, 646, 640, 653, 655, 655, 653, 647, 647, 647, 647, 647, 647},  // r=8 q=1
+    {602, 600, 592, 593, 592, 584, 573, 545, 493, 489, 490, 489, 492, 492, 492, 492, 492, 492, 492},  // r=9 q=0
+    {657, 640, 644, 629, 647, 651, 638, 616, 638, 645, 645, 646, 645, 645, 645, 645, 645, 645, 645},  // r=9 q=1
+    {395, 390, 390, 375, 356, 349, 338, 324, 290, 290, 290, 290, 290, 290, 290, 290, 290, 290, 290},  // r=10 q=0
+    {582, 603, 610, 618, 614, 608, 597, 578, 520, 520, 521, 520, 520, 520, 520, 520, 520, 520, 520},  // r=10 q=1
+};
+
+int shape_eff(int r, int q, int k) {
+    const int kk = k < 13 ? 0 : k > 31 ? 18 : k - 13;
+    if (r <= bw::kRegOnlyMaxBits) return kShapeEff[(r < 3 ? 3 : r) - 3][kk];
+    return kShapeEff[3 + 2 * (r - 6) + q][kk];
+}
+
+// Cheapest split of stages [k0, k0 + h) into high passes (h / 10 rounded up
+// passes, or one more), each with its best cluster shape at its k.  Returns
+// the cost in units of 1e6 / (TB/s x 100); entries are r | (q + 1) << 4.
+long long best_high_split(int k0, int h, std::vector<int>* out) {
+    out->clear();
+    if (h <= 0) return 0;
+    const int m0 = (h + bw::kMaxHighBits - 1) / bw::kMaxHighBits;
+    long long best = -1;
+    std::vector<int> cur;
+    // depth-first over compositions of h into m parts of 1..10
+    struct Rec {
+        static void go(int k, int left, int parts, long long cost, std::vector<int>& cur, std::vector<int>* out,
+                       long long* best) {
+            if (parts == 0) {
+                if (left == 0 && (*best < 0 || cost < *best)) {
+                    *best = cost;
+                    *out = cur;
+                }
+                return;
+            }
+            for (int r = 1; r <= bw::kMaxHighBits && r <= left - (parts - 1); ++r) {
+                if (left - r > (parts - 1) * bw::kMaxHighBits) continue;
+                int entry = r, eff = shape_eff(r, 0, k);
+                if (r > bw::kRegOnlyMaxBits) {
+                    const int e1 = shape_eff(r, 1, k);
+                    if (e1 > eff) {
+                        eff = e1;
+                        entry = r | (2 << 4);
+                    } else {
+                        entry = r | (1 << 4);
+                    }
+                }
+                cur.push_back(entry);
+                go(k + r, left - r, parts - 1, cost + 1000000 / eff, cur, out, best);
+                cur.pop_back();
+            }
+        }
+    };
+    for (int m = m0; m <= m0 + 1 && m <= h; ++m) Rec::go(k0, h, m, 0, cur, out, &best);
+    return best;
 }
 
 // BW_PLAN="13,10,9" overrides the default plan for a matching n
@@ -202,7 +268,8 @@ bool env_plan(int n, std::vector<int>* widths) {
     return true;
 }
 
-// Default plan: fewest HBM round trips, then the cheapest cluster shapes.
+// Default plan: the cheapest plan under the measured cost model (low pass
+// of 13, 14 or 15 bits, then the best split of the rest).  Cached per n.
 int default_plan(int n, std::vector<int>* widths) {
     widths->clear();
     if (env_plan(n, widths)) return BW_OK;
@@ -211,22 +278,24 @@ int default_plan(int n, std::vector<int>* widths) {
         widths->push_back(n);
         return BW_OK;
     }
-    int best_cost = 1 << 30;
-    for (int w0 = 13; w0 <= 15; ++w0) {
-        const int h = n - w0;
-        const int q = (h + bw::kMaxHighBits - 1) / bw::kMaxHighBits;
-        std::vector<int> w{w0};
-        int cost = (1 + q) * 100 + pass_cost(true, w0);
-        for (int i = 0; i < q; ++i) {
-            const int r = h / q + (i < h % q ? 1 : 0);
-            w.push_back(r);
-            cost += pass_cost(false, r);
-        }
-        if (cost < best_cost) {
+    static std::mutex mu;
+    static std::vector<int> cache[BW_MAX_LOG2N + 1];
+    std::lock_guard<std::mutex> lock(mu);
+    if (n <= BW_MAX_LOG2N && !cache[n].empty()) {
+        *widths = cache[n];
+        return BW_OK;
+    }
+    long long best_cost = -1;
+    std::vector<int> hi;
+    for (int w0 = 13; w0 <= 15 && w0 <= n; ++w0) {
+        const long long cost = 1000000 / kLowEff[w0 - 13] + best_high_split(w0, n - w0, &hi);
+        if (best_cost < 0 || cost < best_cost) {
             best_cost = cost;
-            *widths = w;
+            widths->assign(1, w0);
+            widths->insert(widths->end(), hi.begin(), hi.end());
         }
     }
+    if (n <= BW_MAX_LOG2N) cache[n] = *widths;
     return BW_OK;
 }
 
@@ -423,11 +492,12 @@ int fwht_high_bits(u64* d, int n, int lo, cudaStream_t s) {
     const int h = n - lo;
     if (h <= 0) return BW_OK;
     if (lo < bw::kCtaBits) return fail(BW_BAD_ARGUMENTS, "high-bit transform needs lo >= %d", bw::kCtaBits);
-    const int q = (h + bw::kMaxHighBits - 1) / bw::kMaxHighBits;
+    std::vector<int> split;
+    best_high_split(lo, h, &split);
     int k = lo;
-    for (int i = 0; i < q; ++i) {
-        const int r = h / q + (i < h % q ? 1 : 0);
-        const Pass p = r <= bw::kRegOnlyMaxBits ? Pass{REG, k, r, 0} : Pass{HIGH, k, r, high_default_q(r)};
+    for (int e : split) {
+        const int r = e & 15, q = (e >> 4) - 1;
+        const Pass p = r <= bw::kRegOnlyMaxBits ? Pass{REG, k, r, 0} : Pass{HIGH, k, r, q};
         BW_TRY(launch_pass(p, d, n, s));
         k += r;
     }
