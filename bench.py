@@ -503,8 +503,24 @@ def run_e2e(a, x, spec, p, nl, rank, ws, peer):
         ms = float(t.item())
         api = "H2D + sharded.fwht_distributed + D2H"
     nbytes = nbytes_local * ws
-    return {"value": steps * (2 ** (nl + p)) / (ms / 1e3), "unit": "points/s", "h2d_bytes_per_step": nbytes,
-            "d2h_bytes_per_step": nbytes, "steps": steps, "ms_per_step": ms / steps, "api": api}
+    # The PCIe copies alone (one H2D + one D2H of the shard, CUDA events):
+    # the bound the end-to-end step cannot beat, since no output exists
+    # before every input has arrived.
+    e2 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    x.copy_(host, non_blocking=True)
+    e1.record(stream)
+    host.copy_(x, non_blocking=True)
+    e2.record(stream)
+    torch.cuda.synchronize()
+    h2d_s, d2h_s = e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3
+    value = steps * (2 ** (nl + p)) / (ms / 1e3)
+    bound = (2 ** (nl + p)) / (h2d_s + d2h_s)
+    return {"value": value, "unit": "points/s", "h2d_bytes_per_step": nbytes,
+            "d2h_bytes_per_step": nbytes, "steps": steps, "ms_per_step": ms / steps, "api": api,
+            "pcie": {"h2d_gbs": nbytes_local / h2d_s / 1e9, "d2h_gbs": nbytes_local / d2h_s / 1e9,
+                     "copy_only_points_per_s": bound, "frac_of_copy_bound": value / bound}}
 
 
 def main():

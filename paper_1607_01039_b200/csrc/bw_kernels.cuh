@@ -322,19 +322,33 @@ __device__ __forceinline__ bool hit_ge_u(u64 x, unsigned long long tau) {
     return mag >= tau;
 }
 
-template <class C, int RD, int T, int L>
-__device__ __forceinline__ void extract_hits(const u64 (&v)[Dims<C>::E], uint64_t gbase, uint32_t tp, int k,
-                                             const ExtractArgs& ex) {
-    constexpr int E = Dims<C>::E;
+// Any |v[j]| >= tau, in one add + one unsigned compare per element:
+// |x| < tau  <=>  x + (tau - 1) in [0, 2 tau - 2] (mod 2^64), 1 <= tau <= 2^63.
+template <int E>
+__device__ __forceinline__ bool any_hit(const u64 (&v)[E], unsigned long long tau) {
+    if (tau == 0) return true;
+    if (tau > (1ull << 63)) return false;
+    const u64 b = tau - 1, c = 2 * (tau - 1);
     bool any = false;
 #pragma unroll
-    for (int j = 0; j < E; ++j) any |= hit_ge_u(v[j], ex.tau);
-    if (!__any_sync(0xffffffffu, any)) return;  // the common case: no hit in this warp
+    for (int j = 0; j < E; ++j) any |= (v[j] + b) > c;
+    return any;
+}
+
+// Slow path (a warp holds a hit): re-read the warp's just-stored values
+// (the thread's own stores, program-ordered) so the registers of the tile
+// are dead before the store; warp-aggregated append.  Out of line so the
+// common path keeps the pass kernel's register budget.
+template <class C, int RD, int T, int L>
+__device__ __noinline__ void extract_slow(const u64* g, uint64_t gbase, uint32_t tp, int k, ExtractArgs ex) {
+    constexpr int E = Dims<C>::E;
     const uint32_t lane = threadIdx.x & 31u;
-    const uint64_t t0 = gbase + global_off<T, L>(tp, k);
-#pragma unroll
+    const uint64_t t0 = global_off<T, L>(tp, k);
+#pragma unroll 1
     for (int j = 0; j < E; ++j) {
-        const bool h = hit_ge_u(v[j], ex.tau);
+        const uint64_t off = t0 + global_off<T, L>(reg_part<C, RD>(j), k);
+        const u64 x = g[off];
+        const bool h = hit_ge_u(x, ex.tau);
         const unsigned b = __ballot_sync(0xffffffffu, h);
         if (b) {
             const int leader = __ffs(b) - 1;
@@ -344,12 +358,19 @@ __device__ __forceinline__ void extract_hits(const u64 (&v)[Dims<C>::E], uint64_
             if (h) {
                 const unsigned long long pos = first + __popc(b & ((1u << lane) - 1u));
                 if (pos < ex.cap) {
-                    ex.idx[pos] = (long long)(ex.base + t0 + global_off<T, L>(reg_part<C, RD>(j), k));
-                    ex.val[pos] = (long long)v[j];
+                    ex.idx[pos] = (long long)(ex.base + gbase + off);
+                    ex.val[pos] = (long long)x;
                 }
             }
         }
     }
+}
+
+template <class C, int RD, int T, int L>
+__device__ __forceinline__ void extract_hits(const u64 (&v)[Dims<C>::E], const u64* g, uint64_t gbase, uint32_t tp,
+                                             int k, const ExtractArgs& ex) {
+    if (!__any_sync(0xffffffffu, any_hit<Dims<C>::E>(v, ex.tau))) return;  // the common case: no hit in this warp
+    extract_slow<C, RD, T, L>(g, gbase, tp, k, ex);
 }
 
 // One pass over every tile: load (round 0 layout) -> stages -> [transpose ->
@@ -394,8 +415,8 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     run_rounds<C, L, 1>(v, sm, lane, warp, rank);
     constexpr int LAST = C::NR - 1;
     const uint32_t tp_last = thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank);
-    if constexpr (EX) extract_hits<C, LAST, T, L>(v, tile_base<T, L>(tile, k), tp_last, k, ex);
     store_global<C, LAST, T, L>(v, g, tp_last, k);
+    if constexpr (EX) extract_hits<C, LAST, T, L>(v, g, tile_base<T, L>(tile, k), tp_last, k, ex);
 }
 
 // Sort the (few) fused-extraction hits by index in place: one CTA, bitonic
