@@ -364,6 +364,14 @@ int bw_plan_check(int log2n, const int *pass_bits, int npasses,
  * n_local <= 24. */
 int bw_plan_check_fused(int log2n_local, int log2p, uint64_t *butterflies);
 
+/* Static checker of the float64 plan (ascending stage order per element on
+ * top of the bw_plan_check walk).  n <= 24. */
+int bw_plan_check_f64(int log2n, uint64_t *butterflies);
+
+/* TEST HOOK ONLY: the float64 plan's address tables run on host memory with
+ * IEEE double add/sub.  n <= 24. */
+int bw_debug_emulate_f64(double *host, int log2n);
+
 /*
  * TEST HOOK ONLY -- never used by any product entry point.  Executes the
  * default (or given) pass plan's exact address, stage-mask and shared-memory

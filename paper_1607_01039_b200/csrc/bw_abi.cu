@@ -351,6 +351,55 @@ int for_all_pass_kernels(F&& f) {
     return BW_OK;
 }
 
+// ---- float64 passes (ascending stage order, CfgLow13F / CfgHigh13F / CfgReg)
+template <class F>
+int visit_pass_f64(const Pass& p, F&& f) {
+    switch (p.kind) {
+        case LOW:
+            return f(tag<bw::CfgLow13F>{}, ic<13>{});
+        case HIGH:
+            if (p.r == 8) return f(tag<bw::CfgHigh13F<5>>{}, ic<5>{});
+            if (p.r == 7) return f(tag<bw::CfgHigh13F<6>>{}, ic<6>{});
+            if (p.r == 6) return f(tag<bw::CfgHigh13F<7>>{}, ic<7>{});
+            break;
+        case REG:
+            return with_L<bw::CfgReg, 8, 12>(bw::CfgReg::T - p.r, f);
+        default:
+            break;
+    }
+    return fail(BW_BAD_ARGUMENTS, "no float64 pass kernel for %d stages", p.r);
+}
+
+// float64 plan: one small pass (n <= 12), or the 13-bit low pass and then
+// high passes of <= 8 stages in ascending bit order.
+constexpr int kF64MaxHigh = 8;
+int f64_passes(int n, std::vector<Pass>* passes) {
+    passes->clear();
+    if (n <= 0) return BW_OK;
+    if (n <= 12) {
+        passes->push_back({SMALL, 0, n, 0});
+        return BW_OK;
+    }
+    passes->push_back({LOW, 0, 13, 0});
+    const int h = n - 13;
+    const int m = (h + kF64MaxHigh - 1) / kF64MaxHigh;
+    int k = 13;
+    for (int i = 0; i < m; ++i) {
+        const int r = h / m + (i < h % m ? 1 : 0);
+        passes->push_back({r <= bw::kRegOnlyMaxBits ? REG : HIGH, k, r, 0});
+        k += r;
+    }
+    return BW_OK;
+}
+
+template <class F>
+int for_all_f64_pass_kernels(F&& f) {
+    BW_TRY(visit_pass_f64(Pass{LOW, 0, 13, 0}, f));
+    for (int r = 1; r <= kF64MaxHigh; ++r)
+        BW_TRY(visit_pass_f64(Pass{r <= bw::kRegOnlyMaxBits ? REG : HIGH, 0, r, 0}, f));
+    return BW_OK;
+}
+
 template <int LOGP, int L>
 int set_fused_attr() {
     if constexpr (L + LOGP <= 12)
@@ -376,6 +425,15 @@ int set_all_pass_attributes() {
     BW_TRY(set_fused_attrs<1>());
     BW_TRY(set_fused_attrs<2>());
     BW_TRY(set_fused_attrs<3>());
+    BW_TRY(for_all_f64_pass_kernels([](auto t, auto l) -> int {
+        using C = typename decltype(t)::type;
+        constexpr int L = decltype(l)::value;
+        constexpr int smem = bw::Dims<C>::SMEM_BYTES;
+        if (smem > 48 * 1024)
+            BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, false, false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        return BW_OK;
+    }));
     return for_all_pass_kernels([](auto t, auto l) -> int {
         using C = typename decltype(t)::type;
         constexpr int L = decltype(l)::value;
@@ -699,15 +757,23 @@ int bw_fwht_f64(double* data, int log2n, void* stream, uint64_t* butterflies) {
     int dev = 0;
     BW_TRY(device_setup(&dev));
     cudaStream_t s = as_stream(stream);
-    if (log2n > 0) {
-        const int t = log2n < 13 ? log2n : 13;
-        bw::k_small<double><<<(unsigned)(1ull << (log2n - t)), 256, (size_t)(8ull << t), s>>>(data, t);
-        BW_LAUNCHED("k_small<double> launch");
-        const uint64_t half = 1ull << (log2n - 1);
-        for (int k = t; k < log2n; ++k) {
-            bw::k_stage<double><<<grid_for(dev, half, 256, 8), 256, 0, s>>>(data, half, k);
-            BW_LAUNCHED("k_stage<double> launch");
+    std::vector<Pass> passes;
+    BW_TRY(f64_passes(log2n, &passes));
+    for (const Pass& p : passes) {
+        if (p.kind == SMALL) {
+            bw::k_small<double><<<1, 256, (size_t)(8ull << log2n), s>>>(data, log2n);
+            BW_LAUNCHED("k_small<double> launch");
+            continue;
         }
+        BW_TRY(visit_pass_f64(p, [&](auto t, auto l) -> int {
+            using C = typename decltype(t)::type;
+            constexpr int L = decltype(l)::value;
+            const unsigned grid = (unsigned)(1ull << (log2n - bw::kCtaBits));
+            bw::k_pass<C, L, false, false, true><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(
+                reinterpret_cast<u64*>(data), p.k, bw::ExtractArgs{}, nullptr);
+            BW_LAUNCHED("float64 pass launch");
+            return BW_OK;
+        }));
     }
     if (butterflies) *butterflies = butterfly_count(log2n);
     return BW_OK;
@@ -1541,7 +1607,23 @@ int check_pass(int n, int k, std::vector<uint8_t>& touched, uint32_t* stage_bits
 // Host emulation of k_pass<C, L>: the same address tables, rounds, stage
 // masks, cluster exchange and shared-memory slots, executed thread by thread
 // on host memory (TEST HOOK; see bw_debug_emulate_i64).
-template <class C, int L, int RD>
+template <bool FP>
+void emu_butterfly(u64& a, u64& b) {
+    if constexpr (FP) {
+        double x, y;
+        memcpy(&x, &a, 8);
+        memcpy(&y, &b, 8);
+        const double s = x + y, d = x - y;
+        memcpy(&a, &s, 8);
+        memcpy(&b, &d, 8);
+    } else {
+        const u64 x = a, y = b;
+        a = x + y;
+        b = x - y;
+    }
+}
+
+template <class C, int L, int RD, bool FP = false>
 void emu_stages(std::vector<u64>& v) {
     constexpr int E = bw::Dims<C>::E, NT = bw::Dims<C>::NT;
     constexpr uint32_t mask = bw::stage_mask<C, RD, L>();
@@ -1549,16 +1631,11 @@ void emu_stages(std::vector<u64>& v) {
         for (int i = 0; i < C::R; ++i)
             if ((mask >> C::reg(RD, i)) & 1u)
                 for (int j = 0; j < E; ++j)
-                    if (!((j >> i) & 1)) {
-                        u64& a = v[(size_t)t * E + j];
-                        u64& b = v[(size_t)t * E + (j | (1 << i))];
-                        const u64 x = a, y = b;
-                        a = x + y;
-                        b = x - y;
-                    }
+                    if (!((j >> i) & 1))
+                        emu_butterfly<FP>(v[(size_t)t * E + j], v[(size_t)t * E + (j | (1 << i))]);
 }
 
-template <class C, int L, int RD>
+template <class C, int L, int RD, bool FP = false>
 void emu_rounds(std::vector<std::vector<u64>>& v, std::vector<std::vector<u64>>& sm) {
     constexpr int E = bw::Dims<C>::E, NT = bw::Dims<C>::NT, NQ = 1 << C::Q;
     if constexpr (RD < C::NR) {
@@ -1580,13 +1657,13 @@ void emu_rounds(std::vector<std::vector<u64>>& v, std::vector<std::vector<u64>>&
                 for (int j = 0; j < E; ++j)
                     v[q][(size_t)t * E + j] =
                         sm[q][bw::smem_slot_c<C>(bw::to_local<C, RD>(bw::thread_part<C, RD>(t & 31, t >> 5) | bw::reg_part<C, RD>(j)))];
-            emu_stages<C, L, RD>(v[q]);
+            emu_stages<C, L, RD, FP>(v[q]);
         }
-        emu_rounds<C, L, RD + 1>(v, sm);
+        emu_rounds<C, L, RD + 1, FP>(v, sm);
     }
 }
 
-template <class C, int L>
+template <class C, int L, bool FP = false>
 void emulate_pass(u64* data, int n, int k) {
     constexpr int T = C::T, E = bw::Dims<C>::E, NT = bw::Dims<C>::NT, NQ = 1 << C::Q;
     constexpr int LAST = C::NR - 1;
@@ -1602,9 +1679,9 @@ void emulate_pass(u64* data, int n, int k) {
                         data[base + bw::global_off<T, L>(bw::thread_part<C, 0>(t & 31, t >> 5) | bw::reg_part<C, 0>(j) |
                                                              bw::rank_bits<C, 0>((uint32_t)q),
                                                          k)];
-            emu_stages<C, L, 0>(v[q]);
+            emu_stages<C, L, 0, FP>(v[q]);
         }
-        emu_rounds<C, L, 1>(v, sm);
+        emu_rounds<C, L, 1, FP>(v, sm);
         for (int q = 0; q < NQ; ++q)
             for (int t = 0; t < NT; ++t)
                 for (int j = 0; j < E; ++j)
@@ -1676,6 +1753,85 @@ extern "C" int bw_debug_emulate_i64(int64_t* host, int log2n, const int* pass_bi
             using C = typename decltype(t)::type;
             constexpr int L = decltype(l)::value;
             emulate_pass<C, L>(d, log2n, p.k);
+            return BW_OK;
+        }));
+    }
+    return BW_OK;
+}
+
+// float64: the order in which a pass applies its stage bits (round by
+// round, register index by register index).
+namespace {
+template <class C, int L, int RD>
+void stage_order(int k, std::vector<int>* out) {
+    if constexpr (RD < C::NR) {
+        constexpr uint32_t m = bw::stage_mask<C, RD, L>();
+        for (int i = 0; i < C::R; ++i) {
+            const int b = C::reg(RD, i);
+            if ((m >> b) & 1u) out->push_back(b < L ? b : k + (b - L));
+        }
+        stage_order<C, L, RD + 1>(k, out);
+    }
+}
+}  // namespace
+
+// Static checker of the float64 plan: the check_pass walk of every pass
+// (bijective loads/stores, every stage once) plus strictly ascending stage
+// order per element across the whole plan (bitwise numpy equality).
+extern "C" int bw_plan_check_f64(int log2n, uint64_t* butterflies) {
+    if (log2n < 0 || log2n > 24) return fail(BW_BAD_ARGUMENTS, "plan check supports 0 <= n <= 24");
+    std::vector<Pass> passes;
+    BW_TRY(f64_passes(log2n, &passes));
+    uint64_t bfly = 0;
+    uint32_t covered = 0;
+    std::vector<int> order;
+    std::vector<uint8_t> touched((size_t)1 << log2n);
+    for (const Pass& p : passes) {
+        uint32_t bits = 0;
+        if (p.kind == SMALL) {
+            bits = (1u << log2n) - 1u;
+            bfly += (uint64_t)log2n << (log2n - 1);
+            for (int k = 0; k < log2n; ++k) order.push_back(k);
+        } else {
+            BW_TRY(visit_pass_f64(p, [&](auto t, auto l) -> int {
+                using C = typename decltype(t)::type;
+                constexpr int L = decltype(l)::value;
+                stage_order<C, L, 0>(p.k, &order);
+                return check_pass<C, L>(log2n, p.k, touched, &bits, &bfly);
+            }));
+        }
+        if (covered & bits) return fail(BW_BAD_ARGUMENTS, "stage applied twice");
+        covered |= bits;
+    }
+    const uint32_t all = log2n ? (uint32_t)((1ull << log2n) - 1ull) : 0u;
+    if (covered != all) return fail(BW_BAD_ARGUMENTS, "stages covered %x, expected %x", covered, all);
+    for (size_t i = 0; i < order.size(); ++i)
+        if (order[i] != (int)i) return fail(BW_BAD_ARGUMENTS, "float64 stage %d applied at position %zu", order[i], i);
+    if (butterflies) *butterflies = bfly;
+    return BW_OK;
+}
+
+// TEST HOOK ONLY: the float64 plan's exact tables executed on HOST memory
+// with IEEE double add/sub (n <= 24).
+extern "C" int bw_debug_emulate_f64(double* host, int log2n) {
+    if (!host || log2n < 0 || log2n > 24) return fail(BW_BAD_ARGUMENTS, "emulation supports 0 <= n <= 24");
+    std::vector<Pass> passes;
+    BW_TRY(f64_passes(log2n, &passes));
+    u64* d = reinterpret_cast<u64*>(host);
+    for (const Pass& p : passes) {
+        if (p.kind == SMALL) {
+            const uint64_t N = 1ull << log2n;
+            for (int k = 0; k < log2n; ++k)
+                for (uint64_t t = 0; t < N / 2; ++t) {
+                    const uint64_t lo = ((t >> k) << (k + 1)) | (t & ((1ull << k) - 1)), hi = lo + (1ull << k);
+                    emu_butterfly<true>(d[lo], d[hi]);
+                }
+            continue;
+        }
+        BW_TRY(visit_pass_f64(p, [&](auto t, auto l) -> int {
+            using C = typename decltype(t)::type;
+            constexpr int L = decltype(l)::value;
+            emulate_pass<C, L, true>(d, log2n, p.k);
             return BW_OK;
         }));
     }

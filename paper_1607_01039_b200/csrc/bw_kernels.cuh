@@ -40,7 +40,24 @@ __device__ __forceinline__ void st_pass(T* p, const T& v) {
 // Pass engine (kernels K1 low-bits, K2 high-bits, register-only high-bits).
 // ---------------------------------------------------------------------------
 
-template <class C, int RD, int L>
+// One butterfly on bit patterns: int64 (wrapping) or float64 (IEEE add /
+// sub, single rounding each, exactly numpy's a + b and a - b).
+template <bool FP>
+__device__ __forceinline__ void butterfly(u64& x, u64& y) {
+    if constexpr (FP) {
+        const double a = __longlong_as_double((long long)x), b = __longlong_as_double((long long)y);
+        x = (u64)__double_as_longlong(__dadd_rn(a, b));
+        y = (u64)__double_as_longlong(__dsub_rn(a, b));
+    } else {
+        const u64 a = x, b = y;
+        x = a + b;
+        y = a - b;
+    }
+}
+
+// Stages of round RD, register index i = 0..R-1 in order (for float64
+// configs that order is ascending in the stage bit).
+template <class C, int RD, int L, bool FP = false>
 __device__ __forceinline__ void apply_stages(u64 (&v)[Dims<C>::E]) {
     constexpr int E = Dims<C>::E;
     constexpr uint32_t mask = stage_mask<C, RD, L>();
@@ -49,11 +66,7 @@ __device__ __forceinline__ void apply_stages(u64 (&v)[Dims<C>::E]) {
         if ((mask >> C::reg(RD, i)) & 1u) {
 #pragma unroll
             for (int j = 0; j < E; ++j) {
-                if (!((j >> i) & 1)) {
-                    const u64 a = v[j], b = v[j | (1 << i)];
-                    v[j] = a + b;
-                    v[j | (1 << i)] = a - b;
-                }
+                if (!((j >> i) & 1)) butterfly<FP>(v[j], v[j | (1 << i)]);
             }
         }
     }
@@ -280,7 +293,7 @@ __device__ __forceinline__ void exchange_write(const u64 (&v)[Dims<C>::E], u64* 
     }
 }
 
-template <class C, int L, int RD>
+template <class C, int L, int RD, bool FP = false>
 __device__ __forceinline__ void run_rounds(u64 (&v)[Dims<C>::E], u64* sm, uint32_t lane, uint32_t warp,
                                            uint32_t rank) {
     if constexpr (RD < C::NR) {
@@ -299,8 +312,8 @@ __device__ __forceinline__ void run_rounds(u64 (&v)[Dims<C>::E], u64* sm, uint32
             __syncthreads();
         }
         load_smem<C, RD>(v, sm, thread_part<C, RD>(lane, warp));
-        apply_stages<C, RD, L>(v);
-        run_rounds<C, L, RD + 1>(v, sm, lane, warp, rank);
+        apply_stages<C, RD, L, FP>(v);
+        run_rounds<C, L, RD + 1, FP>(v, sm, lane, warp, rank);
     }
 }
 
@@ -377,7 +390,7 @@ __device__ __forceinline__ void extract_hits(const u64 (&v)[Dims<C>::E], const u
 // stages]* -> store (last round layout).  k = first global stage bit of the
 // rows (ignored for L == T).  Cluster configs (Q > 0) put 2^Q CTAs on one
 // tile; grid = 2^(n-13) CTAs for every config.
-template <class C, int L, bool EX = false, bool SRC32 = false>
+template <class C, int L, bool EX = false, bool SRC32 = false, bool FP = false>
 __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     k_pass(u64* __restrict__ data, int k, ExtractArgs ex, const int* __restrict__ src32) {
     constexpr int T = C::T;
@@ -411,8 +424,8 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     else
         load_global<C, 0, T, L>(v, g, thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
     if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-    apply_stages<C, 0, L>(v);
-    run_rounds<C, L, 1>(v, sm, lane, warp, rank);
+    apply_stages<C, 0, L, FP>(v);
+    run_rounds<C, L, 1, FP>(v, sm, lane, warp, rank);
     constexpr int LAST = C::NR - 1;
     const uint32_t tp_last = thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank);
     store_global<C, LAST, T, L>(v, g, tp_last, k);

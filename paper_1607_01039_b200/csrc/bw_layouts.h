@@ -152,6 +152,61 @@ struct CfgReg {
     BW_HD static constexpr int P(int) { return 0; }
 };
 
+// ---- float64 layouts ---------------------------------------------------
+// numpy's float64 result depends on the order of the stages (rounding), so
+// the float64 passes apply every element's stages in ascending bit order:
+// rounds take increasing stage bits and each round's register indices list
+// them in increasing order (bw_plan_check_f64 verifies this).
+//
+// Fused low-bits pass over stages 0..12, four rounds (round 0 only loads):
+//   round 0: reg {8..12}          lane {0..4}  warp {5,6,7}
+//   round 1: reg {0..4}           lane {5..9}  warp {10,11,12}  stages 0..4
+//   round 2: reg {5..9}           lane {0..4}  warp {10,11,12}  stages 5..9
+//   round 3: reg {10,11,12,5,6}   lane {0..4}  warp {7,8,9}     stages 10..12
+struct CfgLow13F {
+    static constexpr int T = 13, Q = 0, R = 5, W = 3, NR = 4, XR = 4, MINB = BW_T13_MINB, PAD = 1;
+    BW_HD static constexpr int reg(int rd, int i) {
+        return nib(rd == 0 ? 0xCBA98ull : rd == 1 ? 0x43210ull : rd == 2 ? 0x98765ull : 0x65CBAull, i);
+    }
+    BW_HD static constexpr int lane(int rd, int i) { return nib(rd == 1 ? 0x98765ull : 0x43210ull, i); }
+    BW_HD static constexpr int warp(int rd, int i) {
+        return nib(rd == 0 ? 0x765ull : rd == 3 ? 0x987ull : 0xCBAull, i);
+    }
+    BW_HD static constexpr uint32_t stage(int rd) {
+        return rd == 0 ? 0u : rd == 1 ? 0x001Fu : rd == 2 ? 0x03E0u : 0x1C00u;
+    }
+    BW_HD static constexpr int P(int) { return 0; }
+};
+
+// Strided high-bits pass with LL column bits (r = 13 - LL = 6..8 rows,
+// tile bits LL..12), ascending: round 0 stages the five lowest rows, round 1
+// the rest; lanes stay on columns 0..4 (256-byte accesses).
+//   LL=5: round 0 reg {5..9}  warp {10,11,12}; round 1 reg {10,11,12,5,6} warp {7,8,9}
+//   LL=6: round 0 reg {6..10} warp {5,11,12};  round 1 reg {11,12,5,6,7}  warp {8,9,10}
+//   LL=7: round 0 reg {7..11} warp {5,6,12};   round 1 reg {12,5,6,7,8}   warp {9,10,11}
+template <int LL>
+struct CfgHigh13F {
+    static_assert(LL >= 5 && LL <= 7, "float64 high pass covers 6..8 rows");
+    static constexpr int T = 13, Q = 0, R = 5, W = 3, NR = 2, XR = 2, MINB = BW_T13_MINB, PAD = 1;
+    BW_HD static constexpr int reg(int rd, int i) {
+        return nib(LL == 5 ? (rd == 0 ? 0x98765ull : 0x65CBAull)
+                   : LL == 6 ? (rd == 0 ? 0xA9876ull : 0x765CBull)
+                             : (rd == 0 ? 0xBA987ull : 0x8765Cull),
+                   i);
+    }
+    BW_HD static constexpr int lane(int, int i) { return nib(0x43210ull, i); }
+    BW_HD static constexpr int warp(int rd, int i) {
+        return nib(LL == 5 ? (rd == 0 ? 0xCBAull : 0x987ull)
+                   : LL == 6 ? (rd == 0 ? 0xCB5ull : 0xA98ull)
+                             : (rd == 0 ? 0xC65ull : 0xBA9ull),
+                   i);
+    }
+    BW_HD static constexpr uint32_t stage(int rd) {
+        return rd == 0 ? (0x1Fu << LL) : (0x1FFFu << (LL + 5)) & 0x1FFFu;
+    }
+    BW_HD static constexpr int P(int) { return 0; }
+};
+
 template <class C>
 struct Dims {
     static constexpr int E = 1 << C::R;               // elements per thread

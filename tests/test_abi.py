@@ -190,6 +190,28 @@ def test_kernel_tables_emulated_on_host_match_oracle(coracle, n):
     assert np.array_equal(emulate(x), ref)
 
 
+@pytest.mark.parametrize("n", list(range(0, 25)))
+def test_float64_plan_checker(n):
+    """float64 plan: every stage once, every element's stages in ascending
+    bit order (what bitwise numpy equality needs)."""
+    bf = ctypes.c_uint64(0)
+    _lib.check(_lib.lib().bw_plan_check_f64(n, ctypes.byref(bf)))
+    assert bf.value == (n << (n - 1) if n else 0)
+
+
+@pytest.mark.parametrize("n", [3, 12, 13, 14, 16, 19, 21, 22])
+def test_float64_kernel_tables_emulated_on_host_bitwise(coracle, n):
+    """The float64 pass kernels' tables with IEEE add/sub on the host equal
+    numpy's float64 fwht_array bit for bit (oracle/bw_oracle.c restates it)."""
+    rng = np.random.default_rng(40 + n)
+    x = rng.normal(scale=1e3, size=1 << n)
+    ref = x.copy()
+    coracle.oracle_fwht_f64(ref.ctypes.data, n)
+    y = x.copy()
+    _lib.check(_lib.lib().bw_debug_emulate_f64(y.ctypes.data, n))
+    assert np.array_equal(y.view(np.int64), ref.view(np.int64))
+
+
 @pytest.mark.parametrize("low", [13, 14, 15])
 def test_kernel_tables_every_split_emulated(coracle, low):
     from oracle import oracle_np

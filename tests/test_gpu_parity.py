@@ -111,12 +111,14 @@ def test_float64_bitwise(golden_npz):
         assert np.array_equal(y.view(np.int64), z[f"y{n}"].view(np.int64))
 
 
-def test_float64_bitwise_large(coracle):
-    rng = np.random.default_rng(8)
-    x = rng.normal(size=1 << 20)
+@pytest.mark.parametrize("n", [13, 16, 20, 21, 24, 26])
+def test_float64_bitwise_large(coracle, n):
+    """float64 pass kernels (ascending stage order) vs numpy's order, bitwise."""
+    rng = np.random.default_rng(8 + n)
+    x = rng.normal(size=1 << n)
     y, _ = gpu_fwht(x)
     ref = x.copy()
-    coracle.oracle_fwht_f64(ref.ctypes.data, 20)
+    coracle.oracle_fwht_f64(ref.ctypes.data, n)
     assert np.array_equal(y.view(np.int64), ref.view(np.int64))
 
 
