@@ -405,6 +405,10 @@ int set_fused_attr() {
     if constexpr (L + LOGP <= 12)
         BW_CUDA(cudaFuncSetAttribute(bw::k_pass_x<bw::CfgHigh13, L, LOGP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      bw::Dims<bw::CfgHigh13>::SMEM_BYTES));
+    if constexpr (L >= 4 && L <= 8 && L + LOGP <= 13)
+        BW_CUDA(cudaFuncSetAttribute(bw::k_pass_x<bw::CfgHigh14c, L, LOGP>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     bw::Dims<bw::CfgHigh14c>::SMEM_BYTES));
     return BW_OK;
 }
 template <int LOGP>
@@ -1071,24 +1075,49 @@ int bw_fold_gen_i64(int d_in, int kind, uint64_t seed, const uint64_t* params, i
 // shard bits: r + log2 P <= 9, so the fused tile keeps >= 128-byte rows.
 }  // extern "C"
 namespace {
-constexpr int kFusedMaxRows = 9;
 
+// Tile of the fused pass: a 2-CTA cluster tile (2^14, 256-byte rows at the
+// default r_last + log2 P = 9) when its column count fits the 2-CTA kernels
+// (L = 4..8), else a single-CTA tile.
+void fused_shape(int p, int r_last, int* q, int* L) {
+    const int l1 = 14 - p - r_last;
+    if (l1 >= 4 && l1 <= 8) {
+        *q = 1;
+        *L = l1;
+    } else {
+        *q = 0;
+        *L = 13 - p - r_last;
+    }
+}
+
+// Fused multi-device plan: a 13-bit low pass, local high passes, then the
+// fused pass with r_last local rows + log2 P shard rows (<= 10 rows).
+// r_last minimises the measured cost model (the fused pass is costed as a
+// local high pass of r_last + log2 P rows at k = n_local - r_last).
 int fused_plan(int nl, int p, std::vector<int>* local, int* r_last) {
     if (p < 1 || p > BW_MAX_LOG2P) return fail(BW_INVALID_WORKERS, "log2p = %d outside 1..%d", p, BW_MAX_LOG2P);
     const int w0 = 13;
     if (nl < w0 + 1) return fail(BW_BAD_ARGUMENTS, "fused cross-shard plan needs n_local >= %d", w0 + 1);
     const int h = nl - w0;
-    const int r = h < kFusedMaxRows - p ? h : kFusedMaxRows - p;
-    if (r < 1) return fail(BW_BAD_ARGUMENTS, "no room for the fused pass");
-    local->assign(1, w0);
-    const int rest = h - r;
-    if (rest > 0) {
-        const int q = (rest + bw::kMaxHighBits - 1) / bw::kMaxHighBits;
-        for (int i = 0; i < q; ++i) local->push_back(rest / q + (i < rest % q ? 1 : 0));
+    long long best = -1;
+    std::vector<int> hi;
+    for (int r = 1; r <= h && r + p <= bw::kMaxHighBits; ++r) {
+        int q = 0, L = 0;
+        fused_shape(p, r, &q, &L);
+        const int rows = r + p;
+        const int eff = rows <= bw::kRegOnlyMaxBits ? shape_eff(rows, 0, nl - r) : shape_eff(rows, q, nl - r);
+        const long long cost = best_high_split(w0, h - r, &hi) + 1000000 / eff;
+        if (best < 0 || cost < best) {
+            best = cost;
+            local->assign(1, w0);
+            local->insert(local->end(), hi.begin(), hi.end());
+            *r_last = r;
+        }
     }
-    *r_last = r;
+    if (best < 0) return fail(BW_BAD_ARGUMENTS, "no room for the fused pass");
     return BW_OK;
 }
+
 
 template <int LOGP, class F>
 int with_fused_kernel(int L, F&& f) {
@@ -1125,7 +1154,9 @@ int bw_fwht_xfused_pass_i64(int64_t* const* shards, int log2p, int log2n_local, 
     if (!shards || log2p < 1 || log2p > BW_MAX_LOG2P) return fail(BW_INVALID_WORKERS, "bad shard list");
     const int P = 1 << log2p;
     if (rank < 0 || rank >= P) return fail(BW_INVALID_WORKERS, "rank %d outside 0..%d", rank, P - 1);
-    const int TL = 13 - log2p, L = TL - r_last;
+    int q = 0, L = 0;
+    fused_shape(log2p, r_last, &q, &L);
+    const int TL = 13 + q - log2p;
     if (r_last < 1 || L < 3 || log2n_local < TL + log2p)
         return fail(BW_BAD_ARGUMENTS, "bad fused pass: n_local=%d r=%d p=%d", log2n_local, r_last, log2p);
     bw::ShardPtrs sp;
@@ -1144,6 +1175,26 @@ int bw_fwht_xfused_pass_i64(int64_t* const* shards, int log2p, int log2n_local, 
         constexpr int LOGP = decltype(lp)::value;
         return with_fused_kernel<LOGP>(L, [&](auto l) -> int {
             constexpr int LL = decltype(l)::value;
+            if (q == 1) {
+                if constexpr (LL >= 4 && LL <= 8 && LL + LOGP <= 13) {
+                    using C = bw::CfgHigh14c;
+                    cudaLaunchConfig_t cfg = {};
+                    cfg.gridDim = dim3((unsigned)(per << 1));
+                    cfg.blockDim = dim3(bw::Dims<C>::NT);
+                    cfg.dynamicSmemBytes = bw::Dims<C>::SMEM_BYTES;
+                    cfg.stream = s;
+                    cudaLaunchAttribute attr[1];
+                    attr[0].id = cudaLaunchAttributeClusterDimension;
+                    attr[0].val.clusterDim.x = 2;
+                    attr[0].val.clusterDim.y = 1;
+                    attr[0].val.clusterDim.z = 1;
+                    cfg.attrs = attr;
+                    cfg.numAttrs = 1;
+                    BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass_x<C, LL, LOGP>, sp, k, (uint64_t)rank * per));
+                    return BW_OK;
+                }
+                return fail(BW_BAD_ARGUMENTS, "no cluster fused kernel for L=%d p=%d", LL, LOGP);
+            }
             if constexpr (LL + LOGP <= 12) {
                 bw::k_pass_x<bw::CfgHigh13, LL, LOGP>
                     <<<(unsigned)per, bw::Dims<bw::CfgHigh13>::NT, bw::Dims<bw::CfgHigh13>::SMEM_BYTES, s>>>(
@@ -1844,35 +1895,47 @@ extern "C" int bw_debug_emulate_f64(double* host, int log2n) {
 // loaded and stored exactly once and that the pass covers the stages
 // [n_local - r_last, n_local) plus every shard bit.  n_local <= 24.
 namespace {
-template <int LOGP, int L>
+template <class C, int LOGP, int L>
 int check_fused(int nl, int r_last, uint64_t* bfly) {
-    using C = bw::CfgHigh13;
-    constexpr int T = C::T, TL = T - LOGP, P = 1 << LOGP, LAST = C::NR - 1;
+    constexpr int T = C::T, TL = T - LOGP, P = 1 << LOGP, LAST = C::NR - 1, NQ = 1 << C::Q;
     const int k = nl - r_last;
     if (TL - L != r_last) return fail(BW_BAD_ARGUMENTS, "inconsistent fused shape");
+    std::string why;
+    if (!rounds_ok<C, 0>(&why)) return fail(BW_BAD_ARGUMENTS, "layout: %s", why.c_str());
     std::vector<uint8_t> touched((size_t)P << nl, 0);
     const uint64_t tiles = 1ull << (nl - TL), per = tiles >> LOGP;
-    for (int rank = 0; rank < P; ++rank)
+    for (int dev = 0; dev < P; ++dev)
         for (uint64_t b = 0; b < per; ++b) {
-            const uint64_t base = bw::tile_base<TL, L>((uint64_t)rank * per + b, k);
-            for (uint32_t t = 0; t < (uint32_t)bw::Dims<C>::NT; ++t)
-                for (int j = 0; j < bw::Dims<C>::E; ++j) {
-                    const uint32_t ei = bw::thread_part<C, 0>(t & 31, t >> 5) | bw::reg_part<C, 0>(j);
-                    const uint32_t eo = bw::thread_part<C, LAST>(t & 31, t >> 5) | bw::reg_part<C, LAST>(j);
-                    const uint64_t gi = ((uint64_t)(ei >> TL) << nl) + base + bw::global_off<TL, L>(ei & ((1u << TL) - 1u), k);
-                    const uint64_t go = ((uint64_t)(eo >> TL) << nl) + base + bw::global_off<TL, L>(eo & ((1u << TL) - 1u), k);
-                    if (gi >= touched.size() || go >= touched.size()) return fail(BW_BAD_ARGUMENTS, "fused pass out of range");
-                    if ((touched[gi] & 1) || (touched[go] & 2)) return fail(BW_BAD_ARGUMENTS, "fused pass touches an element twice");
-                    touched[gi] |= 1;
-                    touched[go] |= 2;
-                }
+            const uint64_t base = bw::tile_base<TL, L>((uint64_t)dev * per + b, k);
+            for (int q = 0; q < NQ; ++q)
+                for (uint32_t t = 0; t < (uint32_t)bw::Dims<C>::NT; ++t)
+                    for (int j = 0; j < bw::Dims<C>::E; ++j) {
+                        const uint32_t ei = bw::thread_part<C, 0>(t & 31, t >> 5) | bw::reg_part<C, 0>(j) |
+                                            bw::rank_bits<C, 0>((uint32_t)q);
+                        const uint32_t eo = bw::thread_part<C, LAST>(t & 31, t >> 5) | bw::reg_part<C, LAST>(j) |
+                                            bw::rank_bits<C, LAST>((uint32_t)q);
+                        const uint64_t gi =
+                            ((uint64_t)(ei >> TL) << nl) + base + bw::global_off<TL, L>(ei & ((1u << TL) - 1u), k);
+                        const uint64_t go =
+                            ((uint64_t)(eo >> TL) << nl) + base + bw::global_off<TL, L>(eo & ((1u << TL) - 1u), k);
+                        if (gi >= touched.size() || go >= touched.size())
+                            return fail(BW_BAD_ARGUMENTS, "fused pass out of range");
+                        if ((touched[gi] & 1) || (touched[go] & 2))
+                            return fail(BW_BAD_ARGUMENTS, "fused pass touches an element twice");
+                        touched[gi] |= 1;
+                        touched[go] |= 2;
+                    }
         }
     for (uint8_t x : touched)
         if (x != 3) return fail(BW_BAD_ARGUMENTS, "fused pass misses an element");
-    // stages: CfgHigh13 stages every tile bit >= L = r_last local rows + LOGP shard bits
+    // stages: every tile bit >= L = r_last local rows + LOGP shard bits, once
     uint32_t staged = 0;
-    for (int rd = 0; rd < C::NR; ++rd) staged |= C::stage(rd) & ~((1u << L) - 1u);
-    if (staged != ((1u << T) - 1u) & ~((1u << L) - 1u)) return fail(BW_BAD_ARGUMENTS, "fused pass stage coverage");
+    for (int rd = 0; rd < C::NR; ++rd) {
+        const uint32_t m = C::stage(rd) & ~((1u << L) - 1u);
+        if (staged & m) return fail(BW_BAD_ARGUMENTS, "fused pass stages a bit twice");
+        staged |= m;
+    }
+    if (staged != (((1u << T) - 1u) & ~((1u << L) - 1u))) return fail(BW_BAD_ARGUMENTS, "fused pass stage coverage");
     *bfly = (uint64_t)(r_last + LOGP) << (nl + LOGP - 1);
     return BW_OK;
 }
@@ -1885,13 +1948,19 @@ extern "C" int bw_plan_check_fused(int log2n_local, int log2p, uint64_t* butterf
     BW_TRY(fused_plan(log2n_local, log2p, &w, &r));
     uint64_t local_bf = 0;
     BW_TRY(bw_plan_check(log2n_local - r, w.data(), (int)w.size(), &local_bf));  // the local passes' bits
-    const int L = 13 - log2p - r;
+    int q = 0, L = 0;
+    fused_shape(log2p, r, &q, &L);
     uint64_t bf = 0;
     auto go = [&](auto lp) -> int {
         constexpr int LOGP = decltype(lp)::value;
         return with_fused_kernel<LOGP>(L, [&](auto l) -> int {
             constexpr int LL = decltype(l)::value;
-            if constexpr (LL + LOGP <= 12) return check_fused<LOGP, LL>(log2n_local, r, &bf);
+            if (q == 1) {
+                if constexpr (LL >= 4 && LL <= 8 && LL + LOGP <= 13)
+                    return check_fused<bw::CfgHigh14c, LOGP, LL>(log2n_local, r, &bf);
+                return fail(BW_BAD_ARGUMENTS, "no cluster fused kernel");
+            }
+            if constexpr (LL + LOGP <= 12) return check_fused<bw::CfgHigh13, LOGP, LL>(log2n_local, r, &bf);
             return fail(BW_BAD_ARGUMENTS, "no fused kernel");
         });
     };

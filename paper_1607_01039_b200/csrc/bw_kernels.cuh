@@ -625,42 +625,57 @@ __global__ void __launch_bounds__(256) k_xshard(ShardPtrs s, uint64_t begin, uin
 
 // ---------------------------------------------------------------------------
 // K6': the last local high pass FUSED with the cross-shard stage.  The tile
-// of a single-CTA high pass (C::T bits) is split as L columns, r local rows
-// at stride 2^k, and the top LOGP bits = the shard index: every CTA loads its
-// tile rows from all P shards (peer pointers over NVLink), applies the r
-// local stages AND the log2 P cross-shard stages, and stores back to every
-// shard -- one kernel, compute and exchange fused.  Each device runs the
-// tiles [tile0, tile0 + gridDim.x); the devices' tile ranges are disjoint
-// (the check_disjoint argument, parallel.py:114-134).  Shard bits are
-// register bits when loading (compile-time pointer per register) and warp
-// bits when storing (warp-uniform pointer).
+// of a high pass (C::T bits, one CTA or a 2-CTA cluster) is split as L
+// columns, r local rows at stride 2^k, and the top LOGP bits = the shard
+// index: every CTA loads its tile rows from all P shards (peer pointers over
+// NVLink), applies the r local stages AND the log2 P cross-shard stages, and
+// stores back to every shard -- one kernel, compute and exchange fused.
+// Each device runs the tiles [tile0, tile0 + gridDim.x / 2^Q); the devices'
+// tile ranges are disjoint (the check_disjoint argument,
+// parallel.py:114-134).  In the round-0 and last-round layouts the shard
+// bits are register, warp or cluster-rank bits, so every shard-pointer
+// lookup is warp-uniform.
 // ---------------------------------------------------------------------------
 template <class C, int L, int LOGP>
 __global__ void __launch_bounds__(Dims<C>::NT, C::MINB) k_pass_x(ShardPtrs s, int k, uint64_t tile0) {
-    static_assert(C::Q == 0, "fused cross-shard pass: single-CTA tiles");
     constexpr int T = C::T, E = Dims<C>::E, TL = T - LOGP, LAST = C::NR - 1;
     constexpr uint32_t lmask = (1u << TL) - 1u;
-    static_assert((thread_part_bits<C, 0>() >> TL) == 0, "shard bits must be register bits at load time");
-    static_assert((reg_part<C, LAST>(Dims<C>::E - 1) >> TL) == 0, "shard bits must be lane/warp bits at store time");
     extern __shared__ u64 sm[];
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
-    const uint64_t base = tile_base<TL, L>(tile0 + blockIdx.x, k);  // within a shard
+    uint32_t rank = 0;
+    if constexpr (C::Q > 0) {
+        rank = cluster_ctarank();
+        if (threadIdx.x == 0) {
+            const uint32_t mb = (uint32_t)__cvta_generic_to_shared(sm + Dims<C>::SMEM_ELEMS);
+            constexpr uint32_t bytes_in = 8u * (Dims<C>::CTA - Dims<C>::CTA / Dims<C>::CLUSTER);
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes_in) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    const uint64_t base = tile_base<TL, L>(tile0 + (blockIdx.x >> C::Q), k);  // within a shard
     u64 v[E];
     {
-        const uint64_t t0 = base + global_off<TL, L>(thread_part<C, 0>(lane, warp), k);
+        const uint32_t tp = thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank);
+        const uint64_t t0 = base + global_off<TL, L>(tp & lmask, k);
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             const uint32_t e = reg_part<C, 0>(j);
-            v[j] = ld_pass(s.p[e >> TL] + t0 + global_off<TL, L>(e & lmask, k));
+            v[j] = ld_pass(s.p[(tp | e) >> TL] + t0 + global_off<TL, L>(e & lmask, k));
         }
     }
+    if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     apply_stages<C, 0, L>(v);
-    run_rounds<C, L, 1>(v, sm, lane, warp, 0u);
-    const uint32_t tp = thread_part<C, LAST>(lane, warp);
-    u64* dst = s.p[tp >> TL] + base + global_off<TL, L>(tp & lmask, k);
+    run_rounds<C, L, 1>(v, sm, lane, warp, rank);
+    const uint32_t tp = thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank);
+    const uint64_t t1 = base + global_off<TL, L>(tp & lmask, k);
 #pragma unroll
-    for (int j = 0; j < E; ++j) st_pass(dst + global_off<TL, L>(reg_part<C, LAST>(j), k), v[j]);
+    for (int j = 0; j < E; ++j) {
+        const uint32_t e = reg_part<C, LAST>(j);
+        st_pass(s.p[(tp | e) >> TL] + t1 + global_off<TL, L>(e & lmask, k), v[j]);
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -317,7 +317,7 @@ def test_sharded_fused_emulation(coracle, P):
     """The fused plan (K6' = last local pass + cross-shard stages in one
     kernel) on P buffers of one device equals the serial transform."""
     p = P.bit_length() - 1
-    for nl in (14, 16, 19, 22):
+    for nl in (14, 16, 19, 20, 22, 24):
         n = nl + p
         x = oracle_np.gen(2, 70 + n, [1 << 20], 0, 1 << n)
         ref = c_fwht(coracle, x)
