@@ -1,0 +1,53 @@
+"""Summarise an ncu --set full report into profiles/: one row per kernel of
+the headline metrics, the full details page, and the per-pass DRAM traffic
+JSON that bench.py reports as roofline.traffic.
+
+    python tools/ncu_summary.py gpurun_out/prof_n32_final.ncu-rep r01_final_n32 [n]
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+rep, tag = sys.argv[1], sys.argv[2]
+n = int(sys.argv[3]) if len(sys.argv) > 3 else 32
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+head, units, data = rows[0], rows[1], rows[2:]
+want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__cluster_dim_x", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "lts__t_sector_hit_rate.pct", "dram__cycles_active.avg.pct_of_peak_sustained_elapsed"]
+idx = {h: i for i, h in enumerate(head)}
+cols = [w for w in want if w in idx]
+with open(f"profiles/{tag}_summary.csv", "w", newline="") as f:
+    w = csv.writer(f)
+    w.writerow(["Kernel Name"] + cols)
+    w.writerow([""] + [units[idx[c]] for c in cols])
+    for r in data:
+        w.writerow([r[idx["Kernel Name"]]] + [r[idx[c]] for c in cols])
+det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True, check=True).stdout
+with open(f"profiles/{tag}_details.csv", "w") as f:
+    f.write(det)
+
+
+def to_bytes(v, unit):
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[unit]
+    return float(v.replace(",", "")) * scale
+
+
+passes = []
+for i, r in enumerate(data):
+    passes.append({"pass": i, "kernel": r[idx["Kernel Name"]].split("(")[0].replace("void ", ""),
+                   "duration_ms": float(r[idx["gpu__time_duration.sum"]].replace(",", "")) *
+                   {"ms": 1, "us": 1e-3, "usecond": 1e-3, "msecond": 1, "ns": 1e-6, "nsecond": 1e-6}.get(
+                       units[idx["gpu__time_duration.sum"]], 1),
+                   "dram_read_bytes": to_bytes(r[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_read.sum"]]),
+                   "dram_write_bytes": to_bytes(r[idx["dram__bytes_write.sum"]], units[idx["dram__bytes_write.sum"]])})
+with open(f"profiles/r01_traffic_n{n}.json", "w") as f:
+    json.dump({"source": f"ncu --set full --clock-control none, tools/gpu_prof_final.sh ({rep})", "n": n,
+               "algorithmic_bytes_per_pass": 16 * 2 ** n, "passes": passes}, f, indent=1)
+for p in passes:
+    print(p)
