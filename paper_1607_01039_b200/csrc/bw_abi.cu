@@ -433,9 +433,12 @@ int set_all_pass_attributes() {
         using C = typename decltype(t)::type;
         constexpr int L = decltype(l)::value;
         constexpr int smem = bw::Dims<C>::SMEM_BYTES;
-        if (smem > 48 * 1024)
+        if (smem > 48 * 1024) {
             BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, false, false, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, false, false, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        }
         return BW_OK;
     }));
     return for_all_pass_kernels([](auto t, auto l) -> int {
@@ -528,16 +531,44 @@ int check_signal(const void* data, int log2n) {
     return BW_OK;
 }
 
+// The ascending-order layouts (8-byte accesses only): the float64 transform
+// (FP) and int64 views that are 8- but not 16-byte aligned.
+template <bool FP>
+int run_scalar_plan(u64* d, int log2n, cudaStream_t s) {
+    std::vector<Pass> passes;
+    BW_TRY(f64_passes(log2n, &passes));
+    for (const Pass& p : passes) {
+        if (p.kind == SMALL) {
+            if constexpr (FP)
+                bw::k_small<double><<<1, 256, (size_t)(8ull << log2n), s>>>(reinterpret_cast<double*>(d), log2n);
+            else
+                bw::k_small<u64><<<1, 256, (size_t)(8ull << log2n), s>>>(d, log2n);
+            BW_LAUNCHED("k_small launch");
+            continue;
+        }
+        BW_TRY(visit_pass_f64(p, [&](auto t, auto l) -> int {
+            using C = typename decltype(t)::type;
+            constexpr int L = decltype(l)::value;
+            const unsigned grid = (unsigned)(1ull << (log2n - bw::kCtaBits));
+            bw::k_pass<C, L, false, false, FP><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(
+                d, p.k, bw::ExtractArgs{}, nullptr);
+            BW_LAUNCHED("scalar-layout pass launch");
+            return BW_OK;
+        }));
+    }
+    return BW_OK;
+}
+
 int fwht_impl(int64_t* data, int log2n, const std::vector<int>* widths, bool naive, cudaStream_t s) {
     BW_TRY(check_signal(data, log2n));
     int dev = 0;
     BW_TRY(device_setup(&dev));
     u64* d = reinterpret_cast<u64*>(data);
     if (log2n == 0) return BW_OK;
+    if (naive) return run_naive(d, log2n, dev, s);
     // 16-byte vector accesses need a 16-byte aligned base; an 8-byte aligned
-    // view (e.g. an odd-offset slice) takes the per-stage path, still on GPU.
-    if (naive || (log2n >= bw::kCtaBits && (reinterpret_cast<uintptr_t>(data) & 15u)))
-        return run_naive(d, log2n, dev, s);
+    // view (e.g. an odd-offset slice) takes the 8-byte-access layouts.
+    if (log2n >= bw::kCtaBits && (reinterpret_cast<uintptr_t>(data) & 15u)) return run_scalar_plan<false>(d, log2n, s);
     std::vector<int> w;
     if (widths) w = *widths; else BW_TRY(default_plan(log2n, &w));
     std::vector<Pass> passes;
@@ -760,25 +791,7 @@ int bw_fwht_f64(double* data, int log2n, void* stream, uint64_t* butterflies) {
     BW_TRY(check_signal(data, log2n));
     int dev = 0;
     BW_TRY(device_setup(&dev));
-    cudaStream_t s = as_stream(stream);
-    std::vector<Pass> passes;
-    BW_TRY(f64_passes(log2n, &passes));
-    for (const Pass& p : passes) {
-        if (p.kind == SMALL) {
-            bw::k_small<double><<<1, 256, (size_t)(8ull << log2n), s>>>(data, log2n);
-            BW_LAUNCHED("k_small<double> launch");
-            continue;
-        }
-        BW_TRY(visit_pass_f64(p, [&](auto t, auto l) -> int {
-            using C = typename decltype(t)::type;
-            constexpr int L = decltype(l)::value;
-            const unsigned grid = (unsigned)(1ull << (log2n - bw::kCtaBits));
-            bw::k_pass<C, L, false, false, true><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(
-                reinterpret_cast<u64*>(data), p.k, bw::ExtractArgs{}, nullptr);
-            BW_LAUNCHED("float64 pass launch");
-            return BW_OK;
-        }));
-    }
+    BW_TRY(run_scalar_plan<true>(reinterpret_cast<u64*>(data), log2n, as_stream(stream)));
     if (butterflies) *butterflies = butterfly_count(log2n);
     return BW_OK;
 }

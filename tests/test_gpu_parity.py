@@ -220,14 +220,16 @@ def test_argument_errors_before_launch():
     assert t.cpu().tolist() == list(range(16))
 
 
-def test_misaligned_view_still_exact(coracle):
-    """An odd-offset slice (8- but not 16-byte aligned) takes the per-stage
-    path on the GPU and stays bit-exact (parallel.py:151 slices)."""
-    base = torch.from_numpy(oracle_np.gen(2, 4, [1 << 20], 0, (1 << 15) + 1)).cuda()
+@pytest.mark.parametrize("n", [12, 13, 15, 19, 22, 26])
+def test_misaligned_view_still_exact(coracle, n):
+    """An odd-offset slice (8- but not 16-byte aligned) takes the 8-byte
+    access layouts on the GPU and stays bit-exact (parallel.py:151 slices)."""
+    base = torch.from_numpy(oracle_np.gen(2, 4 + n, [1 << 20], 0, (1 << n) + 1)).cuda()
     view = base[1:]
     ref = c_fwht(coracle, view.cpu().numpy())
-    bw.fwht_array(view)
+    assert bw.fwht_array(view) == n << (n - 1)
     assert np.array_equal(view.cpu().numpy(), ref)
+    assert base[0].item() == oracle_np.gen(2, 4 + n, [1 << 20], 0, 1)[0]  # the element before is untouched
 
 
 def test_inverse(golden):
