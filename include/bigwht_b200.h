@@ -309,6 +309,12 @@ int bw_extract_ge_i64(const int64_t *data, int log2n, uint64_t tau,
                       uint64_t base, int64_t *out_idx_dev, int64_t *out_val_dev,
                       uint64_t cap, void *scratch_dev, void *stream,
                       uint64_t *count);
+/* float64 Walsh-domain variant: |x| >= tau in double (NaN never hits), hits
+ * in index order with their float64 values; same scratch and capacity rules. */
+int bw_extract_ge_f64(const double *data, int log2n, double tau, uint64_t base,
+                      int64_t *out_idx_dev, double *out_val_dev, uint64_t cap,
+                      void *scratch_dev, void *stream, uint64_t *count);
+
 uint64_t bw_extract_scratch_bytes(int log2n);
 
 /*

@@ -140,7 +140,8 @@ def extract_above(data: np.ndarray, tau) -> list:
     """noisy.py:185-198 + 217-222: (index, value) with |value| >= tau,
     sorted by (-|value|, index)."""
     picked = np.nonzero(np.abs(data) >= tau)[0]
-    hits = [(int(i), int(data[i])) for i in picked.tolist()]
+    exact = data.dtype.kind == "i"  # noisy.py:219-222: int values for int arrays, float otherwise
+    hits = [(int(i), int(data[i]) if exact else float(data[i])) for i in picked.tolist()]
     hits.sort(key=lambda item: (-abs(item[1]), item[0]))
     return hits
 

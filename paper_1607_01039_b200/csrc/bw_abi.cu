@@ -1426,8 +1426,12 @@ uint64_t bw_extract_scratch_bytes(int log2n) {
 }
 
 // extract_above (noisy.py:185-222) with |x| >= tau, ordered by index.
-int bw_extract_ge_i64(const int64_t* data, int log2n, uint64_t tau, uint64_t base, int64_t* out_idx_dev,
-                      int64_t* out_val_dev, uint64_t cap, void* scratch_dev, void* stream, uint64_t* count) {
+}  // extern "C"
+namespace {
+// count -> scan -> ordered write (kernel K5) for any hit predicate.
+template <class H>
+int extract_impl(const void* data, int log2n, H hit, uint64_t base, int64_t* out_idx_dev, void* out_val_dev,
+                 uint64_t cap, void* scratch_dev, void* stream, uint64_t* count) {
     BW_TRY(check_signal(data, log2n));
     if (cap > 0 && (!out_idx_dev || !out_val_dev)) return fail(BW_BAD_ARGUMENTS, "null output arrays");
     int dev = 0;
@@ -1438,7 +1442,8 @@ int bw_extract_ge_i64(const int64_t* data, int log2n, uint64_t tau, uint64_t bas
     void* sc = scratch_dev;
     if (!sc) BW_TRY(scratch(dev, bw_extract_scratch_bytes(log2n), &sc));
     unsigned long long* counts = reinterpret_cast<unsigned long long*>(sc);
-    bw::k_extract_count<<<(unsigned)chunks, 512, 0, s>>>(reinterpret_cast<const long long*>(data), n, tau, counts);
+    const long long* d = reinterpret_cast<const long long*>(data);
+    bw::k_extract_count<H><<<(unsigned)chunks, 512, 0, s>>>(d, n, hit, counts);
     BW_LAUNCHED("k_extract_count launch");
     bw::k_extract_scan<<<1, 1024, 0, s>>>(counts, chunks);
     BW_LAUNCHED("k_extract_scan launch");
@@ -1446,9 +1451,9 @@ int bw_extract_ge_i64(const int64_t* data, int log2n, uint64_t tau, uint64_t bas
     BW_CUDA(cudaMemcpyAsync(&total, counts + chunks, sizeof total, cudaMemcpyDeviceToHost, s));
     BW_CUDA(cudaStreamSynchronize(s));
     if (total > 0 && cap > 0) {
-        bw::k_extract_write<<<(unsigned)chunks, 512, 0, s>>>(
-            reinterpret_cast<const long long*>(data), n, tau, counts, counts + 1, base,
-            reinterpret_cast<long long*>(out_idx_dev), reinterpret_cast<long long*>(out_val_dev), cap);
+        bw::k_extract_write<H><<<(unsigned)chunks, 512, 0, s>>>(d, n, hit, counts, counts + 1, base,
+                                                               reinterpret_cast<long long*>(out_idx_dev),
+                                                               reinterpret_cast<long long*>(out_val_dev), cap);
         BW_LAUNCHED("k_extract_write launch");
         BW_CUDA(cudaStreamSynchronize(s));
     }
@@ -1457,6 +1462,21 @@ int bw_extract_ge_i64(const int64_t* data, int log2n, uint64_t tau, uint64_t bas
         return fail(BW_CAPACITY, "%llu hits exceed the output capacity %llu", (unsigned long long)total,
                     (unsigned long long)cap);
     return BW_OK;
+}
+}  // namespace
+extern "C" {
+
+int bw_extract_ge_i64(const int64_t* data, int log2n, uint64_t tau, uint64_t base, int64_t* out_idx_dev,
+                      int64_t* out_val_dev, uint64_t cap, void* scratch_dev, void* stream, uint64_t* count) {
+    return extract_impl(data, log2n, bw::HitI64{tau}, base, out_idx_dev, out_val_dev, cap, scratch_dev, stream, count);
+}
+
+// float64 Walsh-domain signals (noisy.py:217-222 with a float chunk):
+// |x| >= tau in double, hits in index order with their float64 values.
+int bw_extract_ge_f64(const double* data, int log2n, double tau, uint64_t base, int64_t* out_idx_dev,
+                      double* out_val_dev, uint64_t cap, void* scratch_dev, void* stream, uint64_t* count) {
+    if (!(tau >= 0.0)) return fail(BW_BAD_ARGUMENTS, "tau must be >= 0");
+    return extract_impl(data, log2n, bw::HitF64{tau}, base, out_idx_dev, out_val_dev, cap, scratch_dev, stream, count);
 }
 
 // ---- planner ---------------------------------------------------------------

@@ -733,13 +733,26 @@ __device__ __forceinline__ bool hit_ge(long long x, uint64_t tau) {
 
 constexpr int kExtractChunkBits = 16;
 
+// Hit predicates of the extraction kernels (noisy.py:218 np.abs(x) >= tau).
+struct HitI64 {
+    uint64_t tau;
+    __device__ __forceinline__ bool operator()(long long x) const { return hit_ge(x, tau); }
+};
+struct HitF64 {  // NaN never hits, like numpy's comparison
+    double tau;
+    __device__ __forceinline__ bool operator()(long long bits) const {
+        return fabs(__longlong_as_double(bits)) >= tau;
+    }
+};
+
+template <class H>
 __global__ void __launch_bounds__(512) k_extract_count(const long long* __restrict__ data, uint64_t count,
-                                                       uint64_t tau, unsigned long long* counts) {
+                                                       H hit, unsigned long long* counts) {
     const uint64_t chunk = 1ull << kExtractChunkBits;
     const uint64_t start = blockIdx.x * chunk;
     const uint64_t end = min(count, start + chunk);
     unsigned c = 0;
-    for (uint64_t i = start + threadIdx.x; i < end; i += blockDim.x) c += hit_ge(__ldcs(data + i), tau);
+    for (uint64_t i = start + threadIdx.x; i < end; i += blockDim.x) c += hit(__ldcs(data + i));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     __shared__ unsigned ws[32];
@@ -789,8 +802,9 @@ __global__ void __launch_bounds__(1024) k_extract_scan(unsigned long long* count
     if (threadIdx.x == 0) counts[m] = carry;
 }
 
+template <class H>
 __global__ void __launch_bounds__(512) k_extract_write(const long long* __restrict__ data, uint64_t count,
-                                                       uint64_t tau, const unsigned long long* offsets,
+                                                       H hit, const unsigned long long* offsets,
                                                        const unsigned long long* counts_after,
                                                        uint64_t base_index, long long* out_idx,
                                                        long long* out_val, uint64_t cap) {
@@ -810,7 +824,7 @@ __global__ void __launch_bounds__(512) k_extract_write(const long long* __restri
         bool h = false;
         if (i < end) {
             x = data[i];
-            h = hit_ge(x, tau);
+            h = hit(x);
         }
         const unsigned bal = __ballot_sync(0xffffffffu, h);
         if (l == 0) ws[w] = __popc(bal);

@@ -31,24 +31,31 @@ def _as_device(data) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(data)).cuda()
 
 
-def extract_ge(data, tau: int, base: int = 0, cap: int = 1 << 16):
-    """All hits with |x| >= tau as (index, value) int64 CUDA tensors, sorted
-    by index.  ``base`` is added to every index (shards of a larger signal)."""
+def extract_ge(data, tau, base: int = 0, cap: int = 1 << 16):
+    """All hits with |x| >= tau as (index, value) CUDA tensors sorted by
+    index (values int64, or float64 for float64 signals, noisy.py:217-222).
+    ``base`` is added to every index (shards of a larger signal)."""
     if tau < 0:
         raise BadArguments(f"tau must be >= 0, got {tau}")
     _need_cuda()
     d = _as_device(data)
-    if d.dtype != torch.int64:
-        raise BadArguments("GPU extraction is implemented for int64 signals")
+    if d.dtype not in (torch.int64, torch.float64):
+        raise BadArguments("GPU extraction is implemented for int64 and float64 signals")
+    if not d.is_contiguous():
+        raise BadArguments("extraction needs a contiguous buffer")
     n = _log2(d)
     L = _lib.lib()
     while True:
         idx = torch.empty(max(cap, 1), dtype=torch.int64, device=d.device)
-        val = torch.empty(max(cap, 1), dtype=torch.int64, device=d.device)
+        val = torch.empty(max(cap, 1), dtype=d.dtype, device=d.device)
         count = ctypes.c_uint64(0)
         with torch.cuda.device(d.device):
-            st = L.bw_extract_ge_i64(d.data_ptr(), n, int(tau), int(base), idx.data_ptr(), val.data_ptr(),
-                                     cap, None, _stream_handle(d), ctypes.byref(count))
+            if d.dtype == torch.float64:
+                st = L.bw_extract_ge_f64(d.data_ptr(), n, float(tau), int(base), idx.data_ptr(), val.data_ptr(),
+                                         cap, None, _stream_handle(d), ctypes.byref(count))
+            else:
+                st = L.bw_extract_ge_i64(d.data_ptr(), n, int(tau), int(base), idx.data_ptr(), val.data_ptr(),
+                                         cap, None, _stream_handle(d), ctypes.byref(count))
         if st == _lib.BW_CAPACITY:
             cap = int(count.value)
             continue
@@ -95,16 +102,18 @@ def extract_gt(data, tau: int, base: int = 0):
     return extract_ge(data, int(tau) + 1, base)
 
 
-def extract_above(sig: Signal, tau) -> list[tuple[int, int]]:
+def extract_above(sig: Signal, tau) -> list[tuple[int, int | float]]:
     """noisy.py:185-198: (index, coefficient) with |coefficient| >= tau,
-    largest magnitude first, ties by ascending index."""
+    largest magnitude first, ties by ascending index (int values for int64
+    signals, float values for float64 ones, noisy.py:219-222)."""
     if sig.domain != Domain.WALSH:
         raise BadArguments("extraction expects a Walsh-domain signal")
     if tau < 0:
         raise BadArguments(f"tau must be >= 0, got {tau}")
-    if not sig.is_exact:
-        raise BadArguments("GPU extraction is implemented for int64 signals")
-    t = int(-(-tau // 1)) if not isinstance(tau, int) else tau  # ceil for float tau
+    if sig.is_exact:
+        t = int(-(-tau // 1)) if not isinstance(tau, int) else tau  # ceil for float tau
+    else:
+        t = float(tau)
     idx, val = extract_ge(sig.data, t)
     hits = list(zip(idx.tolist(), val.tolist()))
     hits.sort(key=lambda item: (-abs(item[1]), item[0]))

@@ -111,6 +111,15 @@ def main():
     hits = extract_above(Signal(data, Domain.WALSH), 700)
     ext.append({"data": data.tolist(), "tau": 700, "hits": [list(h) for h in hits]})
     out["extract"] = ext
+    # 7b. float64 Walsh-domain extraction (noisy.py:217-222: float values).
+    rng = np.random.default_rng(13)
+    data = rng.normal(scale=100.0, size=1 << 10)
+    data[1], data[2], data[3] = -np.inf, -0.0, np.nan
+    ext_f = []
+    for tau in (0.0, 150.5, 250.0):
+        hits = extract_above(Signal(data.copy(), Domain.WALSH), tau)
+        ext_f.append({"tau": tau, "hits": [[int(i), float(v)] for i, v in hits]})
+    out["extract_f64"] = {"data": [float(v) for v in data], "cases": ext_f}
     # 8. Noisy-secret construction of config 3 at n = 22 (threshold scaled
     #    by 2^-8 from 2^26): the reference recovers exactly the secret.
     from paper_1607_01039_b200.signals import config  # parameter derivation only (pure Python)

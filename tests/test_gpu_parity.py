@@ -285,6 +285,34 @@ def test_extract_dense_and_edges(coracle):
             assert np.array_equal(i.cpu().numpy(), ri) and np.array_equal(v.cpu().numpy(), rv), (n, tau)
 
 
+def test_extract_float64_matches_golden(golden):
+    g = golden["extract_f64"]
+    x = np.array(g["data"], dtype=np.float64)
+    sig = bw.Signal(dev(x), bw.Domain.WALSH)
+    for case in g["cases"]:
+        assert [[i, v] for i, v in bw.extract_above(sig, case["tau"])] == case["hits"]
+
+
+def test_extract_float64_matches_reference_semantics():
+    """float64 Walsh-domain extraction (noisy.py:185-222 on a float array):
+    |x| >= tau in double, NaN never hits, -0.0 / inf handled like numpy,
+    float values, sorted by (-|x|, index)."""
+    rng = np.random.default_rng(22)
+    for n in (4, 16, 19):
+        x = rng.normal(scale=100.0, size=1 << n)
+        x[1] = np.nan
+        x[2] = -np.inf
+        x[3] = -0.0
+        sig = bw.Signal(dev(x), bw.Domain.WALSH)
+        for tau in (0.0, 50.0, 150.5, 1e300):
+            got = bw.extract_above(sig, tau)
+            assert got == oracle_np.extract_above(x, tau), (n, tau)
+        i, v = bw.extract_ge(dev(x), 120.0, cap=4)  # capacity retry, index order, float values
+        sel = np.nonzero(np.abs(x) >= 120.0)[0]
+        assert np.array_equal(i.cpu().numpy(), sel) and v.dtype == torch.float64
+        assert np.array_equal(v.cpu().numpy().view(np.int64), x[sel].view(np.int64))
+
+
 # ----------------------------------------------------------- generators ---
 
 def test_generators_match_oracle(coracle):

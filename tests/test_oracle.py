@@ -108,6 +108,15 @@ def test_extract_matches_reference(golden):
         assert [list(h) for h in got] == case["hits"]
 
 
+def test_extract_float64_matches_reference(golden):
+    g = golden["extract_f64"]
+    data = np.array(g["data"], dtype=np.float64)
+    for case in g["cases"]:
+        got = oracle_np.extract_above(data, case["tau"])
+        assert [[i, v] for i, v in got] == case["hits"]
+        assert all(isinstance(v, float) for _, v in got)
+
+
 def test_config_constructions(golden):
     from paper_1607_01039_b200.signals import config
 
