@@ -4,7 +4,8 @@ the reference package ``bigwht`` (arXiv:1607.01039).
 Same names and semantics as /root/reference/pkg/src/bigwht/core.py
 (``Signal``, ``Domain``, ``fwht_array``, ``fwht_inplace``,
 ``check_magnitude_bound``, ``inverse_wht_inplace``), noisy.py
-(``extract_above``) and parallel.py (multi-GPU sharding in ``sharded``),
+(``extract_above``) and parallel.py (``plan_parallel`` / ``run_parallel``,
+and multi-GPU sharding in ``sharded``),
 computed by hand-written sm_100a kernels behind the C ABI in
 include/bigwht_b200.h.  No CPU arithmetic path exists.
 """
@@ -33,6 +34,7 @@ from .errors import (
     ValidationError,
 )
 from .extract import extract_above, extract_ge, extract_gt, fwht_extract_ge, fwht_extract_gt
+from .parallel import ParallelPlan, check_disjoint, plan_parallel, run_parallel, total_butterflies
 
 __version__ = "0.1.0"
 
@@ -52,6 +54,11 @@ __all__ = [
     "extract_gt",
     "fwht_extract_ge",
     "fwht_extract_gt",
+    "ParallelPlan",
+    "plan_parallel",
+    "run_parallel",
+    "check_disjoint",
+    "total_butterflies",
     "errors",
     "BadArguments",
     "BigWHTError",

@@ -356,6 +356,37 @@ def test_sharded_fused_emulation(coracle, P):
         assert np.array_equal(np.concatenate([s.cpu().numpy() for s in shards]), ref), (P, nl)
 
 
+@pytest.mark.parametrize("n,p", [(2, 1), (4, 3), (12, 2), (16, 1), (16, 3), (17, 4), (20, 2), (24, 3)])
+def test_run_parallel_drop_in(coracle, n, p):
+    """parallel.run_parallel (parallel.py:162-198) on the GPU equals the
+    serial transform (test_parallel.py:104-129), calls on_phase_complete
+    for every phase in order and flips the domain."""
+    x = oracle_np.gen(2, 90 + n, [1 << 20], 0, 1 << n)
+    ref = c_fwht(coracle, x)
+    sig = bw.Signal(dev(x))
+    seen = []
+    out = bw.run_parallel(sig, bw.plan_parallel(n, p), on_phase_complete=seen.append)
+    assert out is sig and sig.domain == bw.Domain.WALSH
+    assert seen == list(range(p + 1))
+    assert np.array_equal(sig.data.cpu().numpy(), ref)
+
+
+def test_run_parallel_float64_and_host_buffers(coracle):
+    rng = np.random.default_rng(31)
+    x = rng.normal(size=1 << 18)
+    ref = x.copy()
+    coracle.oracle_fwht_f64(ref.ctypes.data, 18)
+    sig = bw.Signal(x.copy())  # numpy buffer: staged through the device, written back
+    bw.run_parallel(sig, bw.plan_parallel(18, 2))
+    assert np.array_equal(sig.data.view(np.int64), ref.view(np.int64))
+    with pytest.raises(errors.BadArguments):
+        bw.run_parallel(bw.Signal(dev(np.zeros(16, dtype=np.int64))), bw.plan_parallel(5, 1))
+    big = np.zeros(1 << 10, dtype=np.int64)
+    big[0] = 1 << 60
+    with pytest.raises(errors.OverflowBoundError):
+        bw.run_parallel(bw.Signal(dev(big)), bw.plan_parallel(10, 1))
+
+
 def test_xshard_strided_matches_per_pointer():
     x = oracle_np.gen(2, 9, [1 << 20], 0, 1 << 16)
     a = dev(x)

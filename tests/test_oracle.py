@@ -217,3 +217,31 @@ def test_subspace_host_helpers_match_reference(golden_npz):
     assert np.array_equal(subspace.row_space(rows), z["row_space"])
     assert subspace.column_masks(rows) == [int(c) for c in oracle_np.column_masks(rows)]
     assert subspace.gf2_rank(rows) == 8
+
+
+def test_product_plan_parallel_matches_reference(golden):
+    """The product's host-side plan objects (paper_1607_01039_b200.parallel)
+    restate parallel.py:87-147 exactly."""
+    from paper_1607_01039_b200 import errors, parallel
+
+    for case in golden["plans"]:
+        plan = parallel.plan_parallel(case["n"], case["p"])
+        ref = case["phases"]
+        assert len(plan.phases) == len(ref)
+        assert ref[0]["stage"] is None and [list(c) for c in plan.phases[0].chunks] == [list(c) for c in ref[0]["chunks"]]
+        for ph, rp in zip(plan.phases[1:], ref[1:]):
+            assert ph.stage == rp["stage"]
+            assert [[w.start, w.stride, w.count] for w in ph.workloads] == rp["workloads"]
+        parallel.check_disjoint(plan)
+        n = case["n"]
+        assert parallel.total_butterflies(plan) == n << (n - 1)
+    for n, p in ((4, 0), (4, 4), (1, 1)):
+        with pytest.raises(errors.InvalidWorkerCount):
+            parallel.plan_parallel(n, p)
+    with pytest.raises(errors.InvalidWorkerCount):
+        parallel.log2_workers_for(3)
+    bad = parallel.plan_parallel(6, 2)
+    broken = parallel.ParallelPlan(bad.log2_dim, bad.log2_workers,
+                                   bad.phases[:1] + (parallel.Phase(stage=4, workloads=bad.phases[1].workloads[:1] * 2),))
+    with pytest.raises(errors.ValidationError):
+        parallel.check_disjoint(broken)
