@@ -70,20 +70,24 @@ int bw_device_cc(int device);
  * (/root/reference/pkg/src/bigwht/core.py:97-117): no magnitude check (the
  * reference has none either), returns the butterfly count n*2^(n-1)
  * (core.py:117) in *butterflies (may be NULL).  Asynchronous.
- * Pass plan: one fused low-bits pass over stages 0..13 followed by strided
- * high-bits passes of <= 10 stages each, i.e. the blocked
- * decomposition of external.py:238-283 with many stages per HBM round trip.
- * data must be 16-byte aligned.
+ * Pass plan: one fused low-bits pass over stages 0..12/13/14 followed by
+ * strided high-bits passes of <= 10 stages each, chosen by the measured
+ * cost model, i.e. the blocked decomposition of
+ * external.py:238-283 with many stages per HBM round trip.  data must be
+ * 8-byte aligned; an 8- but not 16-byte aligned view runs the 8-byte-access
+ * layouts (slower, same result).
  */
 int bw_fwht_i64(int64_t *data, int log2n, void *stream, uint64_t *butterflies);
 
 /*
  * Same transform with an explicit pass plan (test hook; mirrors the
  * reference's block-size-independence tests, test_external.py:120-129).
- * pass_bits[0] = stages of the low pass (must be min(n, 14)), the rest are
- * the widths (1..10) of the following high passes in ascending bit order;
- * the widths must sum to log2n.  npasses = 0 with pass_bits = NULL runs the
- * naive one-launch-per-stage path (kernel K0, debugging/reference aid).
+ * pass_bits[0] = stages of the low pass (13, 14 or 15 = a cluster of 1, 2
+ * or 4 CTAs; n itself when n <= 12), the rest are the widths (1..10) of the
+ * following high passes in ascending bit order, optionally r | (q+1) << 4
+ * to force a cluster of 2^q CTAs; the widths must sum to log2n.
+ * npasses = 0 with pass_bits = NULL runs the naive one-launch-per-stage
+ * path (kernel K0, debugging/reference aid).
  */
 int bw_fwht_i64_planned(int64_t *data, int log2n, const int *pass_bits,
                         int npasses, void *stream);
