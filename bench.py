@@ -215,6 +215,8 @@ def run_ours(a):
     signals.generate(spec, x, base=rank << nl)
     npasses = L.bw_plan_npasses(nl)
     plan = sharded.plan(n, p)
+    if p > 0 and a.mode == "fused" and nl < 14:
+        a.mode = "peer"  # the fused plan needs 2^14-point shards
     fused = p > 0 and a.mode == "fused"
     if fused:  # local passes over the low nl - r bits (one bracket), then K6'
         f_widths, f_r = sharded.fused_plan(nl, p)
