@@ -94,12 +94,14 @@ int bw_fwht_i64_planned(int64_t *data, int log2n, const int *pass_bits,
 
 /* Stages [0, sum(pass_bits)) only (pass_bits as for bw_fwht_i64_planned, a
  * 13+ bit low pass first), applied to every contiguous 2^sum block of the
- * 2^log2n array -- the local passes of the fused multi-device plan. */
+ * 2^log2n array: parallel.py:93-94's phase-0 chunk transforms, here the local
+ * passes of the fused multi-device plan. */
 int bw_fwht_i64_partial(int64_t *data, int log2n, const int *pass_bits, int npasses,
                         void *stream);
 
 /*
- * Pass-level launches of the default plan (instrumentation: the benchmark
+ * Pass-level launches of the default plan (the passes of
+ * external.py:238-283, one HBM round trip each; instrumentation: the benchmark
  * records a CUDA event between passes to time each kernel inside the step).
  * bw_plan_npasses returns the number of passes of bw_fwht_i64's plan;
  * running passes 0..npasses-1 in order equals one bw_fwht_i64 call.
@@ -121,7 +123,8 @@ int bw_sort_hits_i64(int64_t *idx, int64_t *val, const uint64_t *count_dev, void
 
 /*
  * int32 input (the north_star's "seeded int32 inputs"), int64 output, out of
- * place: bit-identical to the reference's fwht_array(x.astype(int64)), with
+ * place: bit-identical to the reference's fwht_array(x.astype(int64))
+ * (core.py:97-117; Signal rejects int32, core.py:56-59), with
  * overflow-free int64 accumulation (|x| < 2^31 and n <= 32 keep every sum
  * below 2^63).  The first pass reads the int32 source directly (4 B/point)
  * and writes dst; the others run in place on dst.  Asynchronous.
@@ -237,19 +240,22 @@ int bw_xshard_i64(int64_t *const *shards, int log2p, uint64_t begin,
                   uint64_t count, void *stream);
 
 /*
- * Same exchange with the shards given as one strided array: shard r starts
- * at base + r*shard_stride elements (all-to-all receive buffers and the
- * single-device P-shard emulation).
+ * Same exchange (parallel.py:103-110 stage phases) with the shards given as
+ * one strided array: shard r starts at base + r*shard_stride elements
+ * (all-to-all receive buffers and the single-device P-shard emulation).
  */
 int bw_xshard_strided_i64(int64_t *base, uint64_t shard_stride, int log2p,
                           uint64_t begin, uint64_t count, void *stream);
 
 /*
- * Cross-shard stage FUSED into the last local pass (kernel K6').
- * bw_plan_fused gives the local plan (widths for bw_fwht_i64_planned on each
+ * Cross-shard stage FUSED into the last local pass (kernel K6'): the
+ * run_parallel schedule of parallel.py:87-111 / 162-198 (phase 0 = each
+ * shard's local transform, phases k = n-p..n-1 = the cross-shard stages)
+ * with the stage phases merged into the last local HBM round trip.
+ * bw_plan_fused gives the local plan (widths for bw_fwht_i64_partial on each
  * shard: the low pass and all high passes but the last) and r_last, the local
  * rows the fused pass takes together with the log2p shard bits
- * (r_last + log2p <= 9).  bw_fwht_xfused_pass_i64 then runs device `rank`'s
+ * (r_last + log2p <= 10).  bw_fwht_xfused_pass_i64 then runs device `rank`'s
  * disjoint share of that pass: peer loads of its tiles from all P shards,
  * r_last local + log2p cross-shard stages, peer stores back -- compute and
  * NVLink exchange in one kernel.  Every device must have finished its local
@@ -313,8 +319,9 @@ int bw_extract_ge_i64(const int64_t *data, int log2n, uint64_t tau,
                       uint64_t base, int64_t *out_idx_dev, int64_t *out_val_dev,
                       uint64_t cap, void *scratch_dev, void *stream,
                       uint64_t *count);
-/* float64 Walsh-domain variant: |x| >= tau in double (NaN never hits), hits
- * in index order with their float64 values; same scratch and capacity rules. */
+/* float64 Walsh-domain variant (noisy.py:217-222 on a float chunk): |x| >= tau
+ * in double (NaN never hits), hits in index order with their float64 values;
+ * same scratch and capacity rules. */
 int bw_extract_ge_f64(const double *data, int log2n, double tau, uint64_t base,
                       int64_t *out_idx_dev, double *out_val_dev, uint64_t cap,
                       void *scratch_dev, void *stream, uint64_t *count);
@@ -322,8 +329,9 @@ int bw_extract_ge_f64(const double *data, int log2n, double tau, uint64_t base,
 uint64_t bw_extract_scratch_bytes(int log2n);
 
 /*
- * The transform followed by the extraction, with the threshold test fused
- * into the last pass's epilogue (no extra read of the signal): equivalent to
+ * The transform followed by the extraction (core.py:97-117 then
+ * noisy.py:185-222), with the threshold test fused into the last pass's
+ * epilogue (no extra read of the signal): equivalent to
  * bw_fwht_i64 then bw_extract_ge_i64 -- the BASELINE configs 3 and 5
  * workload.  Hits come back sorted by index.  Synchronous.
  */
@@ -368,14 +376,16 @@ int bw_plan_describe(int log2n, int log2p, char *json, size_t len);
 int bw_plan_check(int log2n, const int *pass_bits, int npasses,
                   uint64_t *butterflies);
 
-/* Static checker of the multi-device plan with the fused cross-shard pass:
+/* Static checker of the multi-device plan with the fused cross-shard pass
+ * (parallel.py:114-147 check_disjoint / total_butterflies over all devices):
  * every (shard, index) loaded and stored once per pass over all devices,
  * every stage of the 2^(n_local+log2p) transform applied once.
  * n_local <= 24. */
 int bw_plan_check_fused(int log2n_local, int log2p, uint64_t *butterflies);
 
-/* Static checker of the float64 plan (ascending stage order per element on
- * top of the bw_plan_check walk).  n <= 24. */
+/* Static checker of the float64 plan: ascending stage order per element
+ * (numpy's order, core.py:108-115; the float64 bit-identity of
+ * test_parallel.py:123-129) on top of the bw_plan_check walk.  n <= 24. */
 int bw_plan_check_f64(int log2n, uint64_t *butterflies);
 
 /* TEST HOOK ONLY: the float64 plan's address tables run on host memory with
