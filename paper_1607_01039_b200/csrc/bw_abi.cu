@@ -64,6 +64,8 @@ constexpr int kMaxDevices = 64;
 std::mutex g_mu;
 bool g_attr_done[kMaxDevices];
 int g_num_sms[kMaxDevices];
+// BW_TWO_PASS=0 disables the single-launch path for two-pass plans (A/B knob).
+const bool g_two_pass = !(getenv("BW_TWO_PASS") && getenv("BW_TWO_PASS")[0] == '0');
 void* g_scratch[kMaxDevices];
 size_t g_scratch_bytes[kMaxDevices];
 
@@ -425,7 +427,25 @@ int set_fused_attrs() {
     return BW_OK;
 }
 
+template <class C2, int L2>
+int set_two_pass_attr() {
+    constexpr int smem = bw::Dims<bw::CfgLow13>::SMEM_BYTES > bw::Dims<C2>::SMEM_BYTES ? bw::Dims<bw::CfgLow13>::SMEM_BYTES
+                                                                                     : bw::Dims<C2>::SMEM_BYTES;
+    BW_CUDA(cudaFuncSetAttribute(bw::k_two_pass<bw::CfgLow13, 13, C2, L2, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    return BW_OK;
+}
+
 int set_all_pass_attributes() {
+    for (int r = 1; r <= 8; ++r) {
+        const Pass p{r <= bw::kRegOnlyMaxBits ? REG : HIGH, 13, r, 0};
+        BW_TRY(visit_pass(p, [](auto t, auto l) -> int {
+            using C = typename decltype(t)::type;
+            constexpr int L = decltype(l)::value;
+            if constexpr (C::Q == 0 && L < C::T) return set_two_pass_attr<C, L>();
+            return BW_OK;
+        }));
+    }
     BW_TRY(set_fused_attrs<1>());
     BW_TRY(set_fused_attrs<2>());
     BW_TRY(set_fused_attrs<3>());
@@ -531,6 +551,34 @@ int check_signal(const void* data, int log2n) {
     return BW_OK;
 }
 
+// Two-pass plans of single-CTA kernels whose grid fits on the GPU at once
+// (n = 16..20 by default): one cooperative launch of k_two_pass.  Returns
+// BW_OK with *done = false when the shape or the residency does not allow it.
+int launch_two_pass(const std::vector<Pass>& passes, u64* d, int n, int dev, cudaStream_t s, bool* done) {
+    *done = false;
+    if (passes.size() != 2 || passes[0].kind != LOW || passes[0].q != 0 || passes[1].q != 0) return BW_OK;
+    if (passes[1].kind != HIGH && passes[1].kind != REG) return BW_OK;
+    const unsigned grid = 1u << (n - bw::kCtaBits);
+    return visit_pass(passes[1], [&](auto t, auto l) -> int {
+        using C2 = typename decltype(t)::type;
+        constexpr int L2 = decltype(l)::value;
+        if constexpr (C2::Q == 0 && L2 < C2::T) {
+            auto kern = bw::k_two_pass<bw::CfgLow13, 13, C2, L2, false>;
+            constexpr int smem = bw::Dims<bw::CfgLow13>::SMEM_BYTES > bw::Dims<C2>::SMEM_BYTES
+                                     ? bw::Dims<bw::CfgLow13>::SMEM_BYTES
+                                     : bw::Dims<C2>::SMEM_BYTES;
+            int per_sm = 0;
+            BW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+            if ((long long)per_sm * g_num_sms[dev] < (long long)grid) return BW_OK;
+            int k2 = passes[1].k;
+            void* args[] = {&d, &k2};
+            BW_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(256), args, smem, s));
+            *done = true;
+        }
+        return BW_OK;
+    });
+}
+
 // The ascending-order layouts (8-byte accesses only): the float64 transform
 // (FP) and int64 views that are 8- but not 16-byte aligned.
 template <bool FP>
@@ -573,6 +621,11 @@ int fwht_impl(int64_t* data, int log2n, const std::vector<int>* widths, bool nai
     if (widths) w = *widths; else BW_TRY(default_plan(log2n, &w));
     std::vector<Pass> passes;
     BW_TRY(build_passes(log2n, w, &passes));
+    if (!widths && g_two_pass) {
+        bool done = false;
+        BW_TRY(launch_two_pass(passes, d, log2n, dev, s, &done));
+        if (done) return BW_OK;
+    }
     for (const Pass& p : passes) BW_TRY(launch_pass(p, d, log2n, s));
     return BW_OK;
 }

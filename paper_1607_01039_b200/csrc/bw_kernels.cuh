@@ -4,6 +4,7 @@
 // modulo 2^64 exactly like numpy int64 (core.py:113-115), so every kernel is
 // bit-identical to the reference for any input and any stage order.
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -430,6 +431,36 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     const uint32_t tp_last = thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank);
     store_global<C, LAST, T, L>(v, g, tp_last, k);
     if constexpr (EX) extract_hits<C, LAST, T, L>(v, g, tile_base<T, L>(tile, k), tp_last, k, ex);
+}
+
+// ---------------------------------------------------------------------------
+// Small transforms (n <= 21): both passes of a two-pass plan in ONE
+// cooperative launch -- every CTA transforms its low-bits tile, the grid
+// synchronises (gpu-scope fences; each element was written by exactly one
+// CTA), then every CTA runs its high-bits tile.  Saves a launch and the
+// inter-kernel drain on the latency-bound sizes.  Single-CTA configs only.
+// ---------------------------------------------------------------------------
+template <class C, int L, bool FP>
+__device__ __forceinline__ void single_tile(u64* __restrict__ data, int k, uint64_t tile, u64* sm) {
+    static_assert(C::Q == 0, "single-CTA tiles only");
+    constexpr int T = C::T, E = Dims<C>::E, LAST = C::NR - 1;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = threadIdx.x >> 5;
+    u64* g = data + tile_base<T, L>(tile, k);
+    u64 v[E];
+    load_global<C, 0, T, L>(v, g, thread_part<C, 0>(lane, warp), k);
+    apply_stages<C, 0, L, FP>(v);
+    run_rounds<C, L, 1, FP>(v, sm, lane, warp, 0u);
+    store_global<C, LAST, T, L>(v, g, thread_part<C, LAST>(lane, warp), k);
+}
+
+template <class C1, int L1, class C2, int L2, bool FP = false>
+__global__ void __launch_bounds__(256, 1) k_two_pass(u64* __restrict__ data, int k2) {
+    extern __shared__ u64 sm[];
+    single_tile<C1, L1, FP>(data, 0, blockIdx.x, sm);
+    __syncthreads();  // shared memory is reused by the second tile
+    cooperative_groups::this_grid().sync();
+    single_tile<C2, L2, FP>(data, k2, blockIdx.x, sm);
 }
 
 // Sort the (few) fused-extraction hits by index in place: one CTA, bitonic
