@@ -108,6 +108,28 @@ def write_signal(path: str, data: np.ndarray, domain: str = "time") -> None:
     _write_sidecar(path, {"format_version": FORMAT_VERSION, "log2_dim": n, "element_kind": kind, "domain": domain})
 
 
+def adopt(path: str, element_kind: str, domain: str) -> int:
+    """Write a sidecar for a bare payload of 8 * 2**n bytes, inferring n
+    from the file size (dataset.py:408-435 semantics).  Returns n."""
+    if element_kind not in _DTYPES:
+        raise BadArguments(f"bad element_kind {element_kind!r}")
+    if domain not in _DOMAINS:
+        raise BadArguments(f"bad domain {domain!r}")
+    if os.path.exists(sidecar_path(path)):
+        raise PathExists(f"{sidecar_path(path)} already exists")
+    try:
+        size = os.path.getsize(path)
+    except OSError as exc:
+        raise SizeMismatch(f"payload {path} is missing: {exc}") from exc
+    count = size // ELEMENT_BYTES
+    if size % ELEMENT_BYTES or count < 1 or count & (count - 1):
+        raise SizeMismatch(f"{path} is {size} bytes, not 8 * 2**n; cannot infer a dimension")
+    n = count.bit_length() - 1
+    _write_sidecar(path, {"format_version": FORMAT_VERSION, "log2_dim": n, "element_kind": element_kind,
+                          "domain": domain})
+    return n
+
+
 def read_signal(path: str) -> tuple[np.ndarray, str, str]:
     """(array, element_kind, domain) -- the whole payload in memory."""
     meta = read_meta(path)
@@ -115,5 +137,5 @@ def read_signal(path: str) -> tuple[np.ndarray, str, str]:
     return arr, meta["element_kind"], meta["domain"]
 
 
-__all__ = ["BadMetadata", "SizeMismatch", "PathExists", "BigWHTError", "open_memmap", "read_meta", "read_signal",
-           "set_domain", "sidecar_path", "write_signal"]
+__all__ = ["BadMetadata", "SizeMismatch", "PathExists", "BigWHTError", "adopt", "open_memmap", "read_meta",
+           "read_signal", "set_domain", "sidecar_path", "write_signal"]

@@ -95,6 +95,34 @@ def _check_map(rows, d_in: int):
     return rows
 
 
+def save_map(rows, path: str) -> None:
+    """The reference's map file (subspace.py:288-293): d_out lines of d_in
+    '0'/'1' characters, character c = the coefficient of input bit c."""
+    rows = np.asarray(rows, dtype=np.uint8)
+    with open(path, "w", encoding="utf-8") as f:
+        for row in rows:
+            f.write("".join("1" if v else "0" for v in row.tolist()) + "\n")
+
+
+def load_map(path: str) -> np.ndarray:
+    """subspace.py:296-310: the rows of a map file (BadMetadata on any
+    malformed row)."""
+    from .dataset import BadMetadata
+
+    try:
+        with open(path, "r", encoding="utf-8") as f:
+            lines = [line.strip() for line in f if line.strip()]
+    except OSError as exc:
+        raise BadMetadata(f"cannot read map file {path}: {exc}") from exc
+    if not lines:
+        raise BadMetadata(f"map file {path} is empty")
+    width = len(lines[0])
+    for line in lines:
+        if len(line) != width or set(line) - {"0", "1"}:
+            raise BadMetadata(f"map file {path}: bad row {line!r}")
+    return np.array([[1 if ch == "1" else 0 for ch in line] for line in lines], dtype=np.uint8)
+
+
 def fold(sig: Signal, rows) -> Signal:
     """x'[L.j] += x[j] (subspace.py:150-161) on the GPU; returns a new
     time-domain Signal of 2**d_out samples (numpy in -> numpy out)."""
