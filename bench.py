@@ -35,7 +35,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "WHT points/sec at 2^n int64 (1/2/4/8 B200) + HBM GB/s fraction of roofline"
 PUBLISHED_PTS = 2 ** 26 / 2.5  # 26.8 Mpts/s
-CPU_SAMPLE_N = 26
+CPU_SAMPLE_N = 28  # 2^28-point samples: ~2 s each on 16 host cores
 
 
 def args_parse():
@@ -437,7 +437,7 @@ def run_ours(a):
         line["e2e"] = e2e
     if rank == 0 and ws == 1 and not a.no_cpu:
         n_s = min(CPU_SAMPLE_N, n)
-        times, threads, cores = cpu_reference_sample(n_s, 3, 1)
+        times, threads, cores = cpu_reference_sample(n_s, 4, 1)
         mean = sum(times) / len(times)
         line["cpu_baseline"] = {
             "value": cpu_equivalent_rate(n, n_s, mean), "unit": "points/s", "cores": threads, "host_cores": cores,
