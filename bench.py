@@ -50,7 +50,9 @@ def args_parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--mode", choices=["fused", "peer", "a2a"], default="fused", help="cross-GPU exchange (N > 1)")
+    ap.add_argument("--mode", choices=["auto", "fused", "peer", "a2a"], default="auto",
+                    help="cross-GPU exchange (N > 1); auto times fused and a2a (peer with gloo) on two "
+                         "steps each and keeps the faster")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="collectives for N > 1 (gloo: test the multi-rank path with several ranks on one GPU)")
     return ap.parse_args()
@@ -222,19 +224,36 @@ def run_ours(a):
              and all(q["cluster"] == 1 for q in plan["passes"]) and os.environ.get("BW_TWO_PASS", "1") != "0")
     if whole:
         npasses = 1
-    if p > 0 and a.mode == "fused" and nl < 14:
-        a.mode = "peer"  # the fused plan needs 2^14-point shards
-    fused = p > 0 and a.mode == "fused"
-    if fused:  # local passes over the low nl - r bits (one bracket), then K6'
-        f_widths, f_r = sharded.fused_plan(nl, p)
-        f_arr = (ctypes.c_int * len(f_widths))(*f_widths)
-        npasses = 1
+    # Cross-GPU exchange candidates (N > 1): the fused pass over peer
+    # pointers (K6'), the separate peer exchange (K6), or NCCL all-to-all +
+    # K6 on the receive rows.  "auto" times the first two that apply.
+    if p == 0:
+        candidates = ["none"]
+    elif a.mode == "auto":
+        candidates = ["fused" if nl >= 14 else "peer", "a2a" if a.dist_backend == "nccl" else "peer"]
+        candidates = list(dict.fromkeys(candidates))
+    else:
+        candidates = ["peer" if (a.mode == "fused" and nl < 14) else a.mode]  # fused needs 2^14-point shards
+    base_npasses = npasses
+    st = {}
+
+    def configure(mode):
+        st["mode"] = mode
+        st["fused"] = mode == "fused"
+        st["npasses"] = 1 if st["fused"] else base_npasses
+        if st["fused"]:  # local passes over the low nl - r bits (one bracket), then K6'
+            st["f_widths"], st["f_r"] = sharded.fused_plan(nl, p)
+            st["f_arr"] = (ctypes.c_int * len(st["f_widths"]))(*st["f_widths"])
+        if mode == "a2a" and "recv" not in st:
+            st["recv"] = torch.empty_like(x)
+        st["nev"] = 2 if whole else st["npasses"] + 4
+
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
     ptr = x.data_ptr()
     peer = None
     if p > 0:
-        peer = sharded._PeerMap(x, None, dist) if a.mode in ("peer", "fused") else None
+        peer = sharded._PeerMap(x, None, dist) if any(m in ("peer", "fused") for m in candidates) else None
         ones = torch.ones(1, device="cuda")
         ptrs = (ctypes.c_void_p * ws)(*(peer.ptrs if peer else [ptr] * ws))
         b, c = sharded.slice_of(rank, ws, 1 << nl)
@@ -263,18 +282,19 @@ def run_ours(a):
             dist.barrier()
 
     def step(ev):
+        npasses = st["npasses"]
         if whole:
             ev[0].record(stream)
             _lib.check(L.bw_fwht_i64(ptr, nl, sh, None))
             ev[1].record(stream)  # == ev[-1]
             return
-        if fused:
+        if st["fused"]:
             ev[0].record(stream)
-            _lib.check(L.bw_fwht_i64_partial(ptr, nl, f_arr, len(f_widths), sh))
+            _lib.check(L.bw_fwht_i64_partial(ptr, nl, st["f_arr"], len(st["f_widths"]), sh))
             ev[1].record(stream)
             device_barrier()  # every shard's local passes done
             ev[2].record(stream)
-            _lib.check(L.bw_fwht_xfused_pass_i64(ptrs, p, nl, f_r, rank, sh))
+            _lib.check(L.bw_fwht_xfused_pass_i64(ptrs, p, nl, st["f_r"], rank, sh))
             ev[3].record(stream)
             device_barrier()  # every fused pass done
             ev[-1].record(stream)
@@ -291,7 +311,7 @@ def run_ours(a):
                 _lib.check(L.bw_fwht_i64_pass(ptr, nl, i, sh))
         ev[npasses].record(stream)
         if p > 0:
-            if a.mode == "peer":
+            if st["mode"] == "peer":
                 device_barrier()  # every shard's local passes done
                 ev[npasses + 1].record(stream)
                 _lib.check(L.bw_xshard_i64(ptrs, p, b, c, sh))
@@ -300,19 +320,40 @@ def run_ours(a):
             else:
                 ev[npasses + 1].record(stream)
                 m = (1 << nl) // ws
-                recv = step.recv
+                recv = st["recv"]
                 dist.all_to_all_single(recv, x)
                 _lib.check(L.bw_xshard_strided_i64(recv.data_ptr(), m, p, 0, m, sh))
                 dist.all_to_all_single(x, recv)
                 ev[npasses + 2].record(stream)
         ev[-1].record(stream)
 
-    if p > 0 and a.mode == "a2a":
-        step.recv = torch.empty_like(x)
-    nev = 2 if whole else npasses + 4
-
     def events():
-        return [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
+        return [torch.cuda.Event(enable_timing=True) for _ in range(st["nev"])]
+
+    trial_ms = {}
+    if len(candidates) > 1:  # two timed steps per candidate after one warm-up step, max over ranks
+        for m in candidates:
+            configure(m)
+            step(events())
+            tr = [events() for _ in range(2)]
+            for e in tr:
+                step(e)
+            torch.cuda.synchronize()
+            t = torch.tensor([sum(e[0].elapsed_time(e[-1]) for e in tr) / len(tr)], dtype=torch.float64,
+                             device="cuda" if a.dist_backend == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            trial_ms[m] = float(t.item())
+        configure(min(trial_ms, key=trial_ms.get))
+        if st["mode"] != "a2a" and "recv" in st:
+            del st["recv"]
+            torch.cuda.empty_cache()
+    else:
+        configure(candidates[0])
+    npasses = st["npasses"]
+    fused = st["fused"]
+    a.exchange = st["mode"]  # the e2e leg uses the same exchange
+    if fused:
+        f_widths, f_r = st["f_widths"], st["f_r"]
 
     hits_first = None
     for w in range(a.warmup):
@@ -388,7 +429,8 @@ def run_ours(a):
         "config": {"workload": f"config{a.config}: n={n} int64 FWHT, {CONFIG_TEXT[a.config]}, natural order, "
                                "unnormalised",
                    "n": n, "log2p": p, "local_log2n": nl, "parallelism": f"top {p} index bits sharded over {ws} GPUs",
-                   "exchange": a.mode if p > 0 else None,
+                   "exchange": st["mode"] if p > 0 else None,
+                   "exchange_trial_ms": trial_ms or None,
                    "passes": [{"kind": q["kind"], "k": q["k"], "r": q["r"], "cluster": q["cluster"]}
                               for q in plan["passes"]],
                    "l2": ("L2 flushed between steps (256 MiB write, outside the step events)" if flush
@@ -512,7 +554,7 @@ def run_e2e(a, x, spec, p, nl, rank, ws, peer):
         e0.record(stream)
         for _ in range(steps):
             x.copy_(host, non_blocking=True)
-            sharded.fwht_distributed(x, mode=a.mode, peer_map=peer)
+            sharded.fwht_distributed(x, mode=a.exchange, peer_map=peer)
             host.copy_(x, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
