@@ -157,7 +157,7 @@ int bw_minmax_i64(const int64_t *data, uint64_t count, int64_t *out_minmax_dev,
  * M = max(max, -min) exactly and fails with BW_OVERFLOW_BOUND when
  * M * 2^log2n >= 2^63.  *max_abs (may be NULL) receives M (as uint64, so
  * |INT64_MIN| = 2^63 is representable).  scratch_dev: 2 int64 of device
- * memory (NULL = use an internal per-device buffer).
+ * memory (NULL = use an internal buffer private to the calling host thread).
  */
 int bw_check_bound_i64(const int64_t *data, int log2n, int64_t *scratch_dev,
                        void *stream, uint64_t *max_abs);
@@ -313,7 +313,8 @@ int bw_gen_range_i64(int64_t *data, uint64_t base, uint64_t count, int kind,
  * beyond cap is written (call again with a larger cap).  |INT64_MIN| is
  * treated as 2^63.  Index offset `base` is added to every index (shards).
  * scratch_dev must hold bw_extract_scratch_bytes(log2n) bytes (NULL = use
- * an internal per-device buffer).  Synchronous (one small read-back).
+ * an internal buffer private to the calling host thread).  Synchronous
+ * (one small read-back).
  */
 int bw_extract_ge_i64(const int64_t *data, int log2n, uint64_t tau,
                       uint64_t base, int64_t *out_idx_dev, int64_t *out_val_dev,

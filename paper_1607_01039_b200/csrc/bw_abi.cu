@@ -66,8 +66,15 @@ bool g_attr_done[kMaxDevices];
 int g_num_sms[kMaxDevices];
 // BW_TWO_PASS=0 disables the single-launch path for two-pass plans (A/B knob).
 const bool g_two_pass = !(getenv("BW_TWO_PASS") && getenv("BW_TWO_PASS")[0] == '0');
-void* g_scratch[kMaxDevices];
-size_t g_scratch_bytes[kMaxDevices];
+// Small device scratch (reduction results, extraction counts, fold tables)
+// for calls that get none from the caller.  Per host thread: every call that
+// uses it synchronises its stream before returning, so a thread never has two
+// uses in flight, and calls from different threads never share a buffer.
+struct ThreadScratch {
+    void* p[kMaxDevices] = {};
+    size_t bytes[kMaxDevices] = {};
+};
+thread_local ThreadScratch t_scratch;
 
 int set_all_pass_attributes();
 
@@ -95,17 +102,17 @@ int device_setup(int* dev_out) {
 
 // Internal per-device scratch (never the signal itself).
 int scratch(int dev, size_t bytes, void** out) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (g_scratch_bytes[dev] < bytes) {
-        if (g_scratch[dev]) cudaFree(g_scratch[dev]);
-        g_scratch[dev] = nullptr;
-        g_scratch_bytes[dev] = 0;
+    ThreadScratch& t = t_scratch;
+    if (t.bytes[dev] < bytes) {
+        if (t.p[dev]) cudaFree(t.p[dev]);  // the previous use on this thread has completed
+        t.p[dev] = nullptr;
+        t.bytes[dev] = 0;
         size_t want = bytes < 4096 ? 4096 : bytes;
-        cudaError_t e = cudaMalloc(&g_scratch[dev], want);
+        cudaError_t e = cudaMalloc(&t.p[dev], want);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(scratch)");
-        g_scratch_bytes[dev] = want;
+        t.bytes[dev] = want;
     }
-    *out = g_scratch[dev];
+    *out = t.p[dev];
     return BW_OK;
 }
 

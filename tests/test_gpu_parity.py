@@ -502,3 +502,33 @@ def test_int32_inputs_widened(coracle):
         assert np.array_equal(bw.fwht_widen(x).cpu().numpy(), ref)
     with pytest.raises(errors.BadArguments):
         bw.fwht_widen(torch.zeros(8, dtype=torch.int64, device="cuda"))
+
+
+def test_concurrent_host_threads_do_not_share_scratch():
+    """Calls that use the library's internal scratch (bound check, extraction)
+    from several host threads on their own streams stay correct."""
+    import threading
+
+    results = {}
+
+    def worker(tid):
+        torch.cuda.set_device(0)
+        stream = torch.cuda.Stream()
+        rng = np.random.default_rng(100 + tid)
+        x = rng.integers(-1000, 1000, 1 << 18).astype(np.int64)
+        x[tid * 7 + 1] = 5000 + tid
+        ok = True
+        with torch.cuda.stream(stream):
+            t = dev(x)
+            for _ in range(20):
+                bw.check_magnitude_bound(t, 18)
+                i, v = bw.extract_ge(t, 4000)
+                ok &= i.tolist() == [tid * 7 + 1] and v.tolist() == [5000 + tid]
+        results[tid] = ok
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert results == {k: True for k in range(4)}
