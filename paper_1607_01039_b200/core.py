@@ -15,6 +15,7 @@ Accepted buffers:
 from __future__ import annotations
 
 import ctypes
+import threading
 import enum
 from dataclasses import dataclass
 
@@ -140,18 +141,23 @@ def _check_shape(buf) -> int:
 
 
 class _HostStage:
-    """Device workspace for numpy buffers (reused between calls)."""
+    """Device workspace for numpy buffers, reused between calls.  One per
+    host thread (the calls using it are synchronous, so a thread never has
+    two uses in flight and threads never share one)."""
 
-    _work: dict = {}
+    _local = threading.local()
 
     @classmethod
     def get(cls, n: int, dtype) -> torch.Tensor:
+        work = getattr(cls._local, "work", None)
+        if work is None:
+            work = cls._local.work = {}
         dev = torch.cuda.current_device()
         key = (dev, dtype)
-        w = cls._work.get(key)
+        w = work.get(key)
         if w is None or w.numel() < (1 << n):
             w = torch.empty(1 << n, dtype=dtype, device=f"cuda:{dev}")
-            cls._work[key] = w
+            work[key] = w
         return w[: 1 << n]
 
 
