@@ -370,6 +370,8 @@ int visit_pass_f64(const Pass& p, F&& f) {
             if (p.r == 8) return f(tag<bw::CfgHigh13F<5>>{}, ic<5>{});
             if (p.r == 7) return f(tag<bw::CfgHigh13F<6>>{}, ic<6>{});
             if (p.r == 6) return f(tag<bw::CfgHigh13F<7>>{}, ic<7>{});
+            if (p.r == 9) return f(tag<bw::CfgHigh14cF<5>>{}, ic<5>{});
+            if (p.r == 10) return f(tag<bw::CfgHigh14cF<4>>{}, ic<4>{});
             break;
         case REG:
             return with_L<bw::CfgReg, 8, 12>(bw::CfgReg::T - p.r, f);
@@ -380,8 +382,9 @@ int visit_pass_f64(const Pass& p, F&& f) {
 }
 
 // float64 plan: one small pass (n <= 12), or the 13-bit low pass and then
-// high passes of <= 8 stages in ascending bit order.
-constexpr int kF64MaxHigh = 8;
+// high passes of <= 10 stages in ascending bit order (9 and 10 stages on
+// 2-CTA cluster tiles).
+constexpr int kF64MaxHigh = 10;
 int f64_passes(int n, std::vector<Pass>* passes) {
     passes->clear();
     if (n <= 0) return BW_OK;
@@ -605,9 +608,26 @@ int run_scalar_plan(u64* d, int log2n, cudaStream_t s) {
             using C = typename decltype(t)::type;
             constexpr int L = decltype(l)::value;
             const unsigned grid = (unsigned)(1ull << (log2n - bw::kCtaBits));
-            bw::k_pass<C, L, false, false, FP><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(
-                d, p.k, bw::ExtractArgs{}, nullptr);
-            BW_LAUNCHED("scalar-layout pass launch");
+            if constexpr (C::Q == 0) {
+                bw::k_pass<C, L, false, false, FP><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(
+                    d, p.k, bw::ExtractArgs{}, nullptr);
+                BW_LAUNCHED("scalar-layout pass launch");
+            } else {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(grid);
+                cfg.blockDim = dim3(bw::Dims<C>::NT);
+                cfg.dynamicSmemBytes = bw::Dims<C>::SMEM_BYTES;
+                cfg.stream = s;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = bw::Dims<C>::CLUSTER;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                const int* none = nullptr;
+                BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L, false, false, FP>, d, p.k, bw::ExtractArgs{}, none));
+            }
             return BW_OK;
         }));
     }

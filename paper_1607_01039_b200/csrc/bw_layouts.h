@@ -207,6 +207,31 @@ struct CfgHigh13F {
     BW_HD static constexpr int P(int) { return 0; }
 };
 
+// Strided high-bits pass over rows LL..13 (r = 14 - LL = 9 / 10) on a
+// cluster of 2, ascending: round 0 stages the five lowest rows, the DSMEM
+// transpose brings the rank row (tile bit 13) into the CTA at local
+// position P = LL + 4 (already staged), round 1 stages the rest in order.
+//   LL=5: round 0 reg {5..9}  lane {0..4}        warp {10,11,12}  P = 9
+//         round 1 reg {10,11,12,13,5}  lane {0..4}  warp {6,7,8}
+//   LL=4: round 0 reg {4..8}  lane {0,1,2,3,12}  warp {9,10,11}   P = 8
+//         round 1 reg {9..13}  lane {0..4}          warp {5,6,7}
+template <int LL>
+struct CfgHigh14cF {
+    static_assert(LL == 4 || LL == 5, "float64 cluster pass covers 9 or 10 rows");
+    static constexpr int T = 14, Q = 1, R = 5, W = 3, NR = 2, XR = 1, MINB = BW_T13_MINB, PAD = 1;
+    BW_HD static constexpr int reg(int rd, int i) {
+        return nib(LL == 5 ? (rd == 0 ? 0x98765ull : 0x5DCBAull) : (rd == 0 ? 0x87654ull : 0xDCBA9ull), i);
+    }
+    BW_HD static constexpr int lane(int rd, int i) { return nib(LL == 4 && rd == 0 ? 0xC3210ull : 0x43210ull, i); }
+    BW_HD static constexpr int warp(int rd, int i) {
+        return nib(LL == 5 ? (rd == 0 ? 0xCBAull : 0x876ull) : (rd == 0 ? 0xBA9ull : 0x765ull), i);
+    }
+    BW_HD static constexpr uint32_t stage(int rd) {
+        return rd == 0 ? (0x1Fu << LL) : (0x3FFFu << (LL + 5)) & 0x3FFFu;
+    }
+    BW_HD static constexpr int P(int) { return LL + 4; }
+};
+
 template <class C>
 struct Dims {
     static constexpr int E = 1 << C::R;               // elements per thread
