@@ -191,22 +191,22 @@ int high_default_q(int r) { return r <= 8 ? 0 : 1; }
 // shape, so a plan's time is proportional to sum(1 / rate).
 // generated by tools/gen_shape_table.py from profiles/r01_shapes_n34.json (NVIDIA B200)
 // low passes 13 / 14 / 15 bits:
-constexpr int kLowEff[3] = {701, 593, 450};
+constexpr int kLowEff[3] = {702, 593, 450};
 // rows: reg r=3,4,5; high r=6..10 x q=0,1.  columns: k = 13..31
 constexpr int kShapeEff[13][19] = {
-    {695, 695, 682, 696, 695, 691, 691, 685, 685, 687, 688, 688, 689, 689, 691, 690, 687, 687, 688},  // r=3 q=0
-    {698, 698, 698, 696, 668, 689, 686, 681, 683, 683, 684, 686, 686, 686, 685, 683, 682, 683, 683},  // r=4 q=0
-    {662, 662, 659, 652, 644, 640, 639, 637, 636, 636, 639, 638, 639, 638, 639, 628, 628, 628, 628},  // r=5 q=0
-    {684, 697, 694, 678, 670, 664, 642, 616, 610, 619, 624, 606, 594, 594, 595, 600, 600, 600, 600},  // r=6 q=0
-    {624, 622, 621, 616, 616, 614, 613, 611, 612, 613, 614, 614, 614, 613, 610, 604, 604, 604, 604},  // r=6 q=1
-    {681, 684, 676, 647, 659, 640, 633, 628, 630, 636, 626, 612, 616, 614, 607, 607, 607, 607, 607},  // r=7 q=0
-    {626, 625, 623, 624, 625, 622, 625, 622, 616, 619, 622, 624, 623, 625, 622, 622, 622, 622, 622},  // r=7 q=1
-    {648, 642, 628, 645, 645, 634, 632, 636, 625, 619, 618, 596, 612, 617, 617, 617, 617, 617, 617},  // r=8 q=0
-    {666, 653, 646, 648, 645, 654, 654, 646, 640, 653, 655, 655, 653, 647, 647, 647, 647, 647, 647},  // r=8 q=1
-    {602, 600, 592, 593, 592, 584, 573, 545, 493, 489, 490, 489, 492, 492, 492, 492, 492, 492, 492},  // r=9 q=0
-    {657, 640, 644, 629, 647, 651, 638, 616, 638, 645, 645, 646, 645, 645, 645, 645, 645, 645, 645},  // r=9 q=1
-    {395, 390, 390, 375, 356, 349, 338, 324, 290, 290, 290, 290, 290, 290, 290, 290, 290, 290, 290},  // r=10 q=0
-    {582, 603, 610, 618, 614, 608, 597, 578, 520, 520, 521, 520, 520, 520, 520, 520, 520, 520, 520},  // r=10 q=1
+    {696, 695, 697, 696, 695, 677, 691, 685, 686, 687, 688, 688, 689, 689, 691, 690, 687, 687, 688},  // r=3 q=0
+    {698, 698, 698, 696, 692, 690, 687, 681, 683, 683, 684, 686, 686, 686, 686, 684, 682, 684, 684},  // r=4 q=0
+    {698, 698, 697, 693, 687, 685, 682, 679, 679, 680, 682, 684, 683, 682, 681, 672, 670, 670, 670},  // r=5 q=0
+    {684, 697, 695, 678, 670, 664, 642, 619, 617, 632, 634, 625, 614, 602, 596, 603, 603, 603, 603},  // r=6 q=0
+    {628, 626, 626, 621, 621, 619, 617, 616, 616, 618, 619, 618, 617, 618, 615, 608, 608, 608, 608},  // r=6 q=1
+    {680, 684, 676, 646, 659, 639, 633, 650, 638, 644, 647, 629, 623, 605, 619, 619, 619, 619, 619},  // r=7 q=0
+    {625, 624, 622, 624, 624, 621, 625, 622, 614, 616, 618, 623, 623, 622, 624, 624, 624, 624, 624},  // r=7 q=1
+    {647, 642, 640, 645, 645, 634, 650, 643, 629, 639, 640, 602, 601, 589, 589, 589, 589, 589, 589},  // r=8 q=0
+    {666, 653, 646, 647, 644, 654, 653, 646, 639, 652, 654, 654, 654, 645, 645, 645, 645, 645, 645},  // r=8 q=1
+    {612, 610, 602, 602, 600, 588, 571, 564, 510, 511, 502, 500, 506, 506, 506, 506, 506, 506, 506},  // r=9 q=0
+    {657, 639, 642, 641, 646, 649, 636, 613, 637, 643, 644, 646, 644, 644, 644, 644, 644, 644, 644},  // r=9 q=1
+    {401, 397, 395, 383, 367, 360, 347, 331, 299, 299, 299, 299, 299, 299, 299, 299, 299, 299, 299},  // r=10 q=0
+    {594, 612, 619, 626, 621, 615, 604, 583, 530, 530, 531, 531, 531, 531, 531, 531, 531, 531, 531},  // r=10 q=1
 };
 
 int shape_eff(int r, int q, int k) {

@@ -15,11 +15,15 @@ namespace bw {
 typedef unsigned long long u64;
 
 // Cache policy of the pass kernels' global accesses (A/B knob: 0 = .cs
-// streaming, 1 = .cg, 2 = default).  Measured on B200 (profiles/r01_*):
-// default loads lift the vectorised low pass from 6.4 to 7.0 TB/s, the
-// other passes are indifferent -- so plain loads and stores.
+// streaming, 1 = .cg, 2 = default, 3 = default + L2::256B fetch size).
+// Measured on B200 (profiles/r01_*): default loads lift the vectorised low
+// pass from 6.4 to 7.0 TB/s; the 256-byte L2 fetch makes every DRAM access
+// cover two neighbouring 128-byte row segments (the next tile's, already in
+// L2 when that tile loads): 10-stage passes +1.5-2.2%, 5-stage register
+// passes +5% (profiles/r01_shapes_l2_256B.json).  So: loads with L2::256B,
+// plain stores.
 #ifndef BW_LD_POLICY
-#define BW_LD_POLICY 2
+#define BW_LD_POLICY 3
 #endif
 #ifndef BW_ST_POLICY
 #define BW_ST_POLICY 2
@@ -28,7 +32,17 @@ template <class T>
 __device__ __forceinline__ T ld_pass(const T* p) {
     if constexpr (BW_LD_POLICY == 0) return __ldcs(p);
     else if constexpr (BW_LD_POLICY == 1) return __ldcg(p);
-    else return *p;
+    else if constexpr (BW_LD_POLICY == 3) {  // L2 fetch granularity 256 B (experiment)
+        if constexpr (sizeof(T) == 16) {
+            T v;
+            asm volatile("ld.global.L2::256B.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+            return v;
+        } else {
+            T v;
+            asm volatile("ld.global.L2::256B.u64 %0, [%1];" : "=l"(v) : "l"(p));
+            return v;
+        }
+    } else return *p;
 }
 template <class T>
 __device__ __forceinline__ void st_pass(T* p, const T& v) {
