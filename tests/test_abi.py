@@ -238,3 +238,39 @@ def test_forced_cluster_shapes_emulated(coracle, plan):
     coracle.oracle_fwht_i64(ref.ctypes.data, n)
     assert sharded.plan_check(n, plan) == n << (n - 1)
     assert np.array_equal(emulate(x, plan), ref)
+
+
+def _compile_c_consumer(tmp_path):
+    import shutil
+    import subprocess
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    out = str(tmp_path / "abi_smoke")
+    cmd = [cc, "-O2", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "tests", "c", "abi_smoke.c"), "-L", os.path.dirname(_lib.LIB_PATH), "-lbigwht_b200",
+           "-L", os.path.join(ROOT, "oracle"), "-loracle", "-L", "/usr/local/cuda/lib64", "-lcudart", "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return out
+
+
+def test_c_consumer_compiles_against_the_header(tmp_path):
+    """The header is plain C (no C++ or torch types) and the library links
+    into a C program without Python."""
+    _compile_c_consumer(tmp_path)
+
+
+@pytest.mark.gpu
+def test_c_consumer_runs(tmp_path):
+    import subprocess
+
+    exe = _compile_c_consumer(tmp_path)
+    env = dict(os.environ)
+    env["LD_LIBRARY_PATH"] = ":".join([os.path.dirname(_lib.LIB_PATH), os.path.join(ROOT, "oracle"),
+                                       "/usr/local/cuda/lib64", env.get("LD_LIBRARY_PATH", "")])
+    for n in ("13", "22", "24"):
+        r = subprocess.run([exe, n], capture_output=True, text=True, env=env, timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert "c abi ok" in r.stdout
