@@ -964,25 +964,71 @@ __global__ void __launch_bounds__(256) k_fold(const long long* __restrict__ x, u
                                               const unsigned* __restrict__ table, int groups, int d_out,
                                               unsigned long long* out, GenParams g) {
     __shared__ unsigned tab[kFoldGroups * 256];
-    extern __shared__ unsigned long long bins[];
+    // Shared bins as separate low / high 32-bit words: a 64-bit shared
+    // atomicAdd compiles to a CAS loop, 32-bit ones are native.  The low
+    // word's returned old value gives the exact carry into the high word,
+    // so hi * 2^32 + lo is the exact sum mod 2^64.
+    extern __shared__ unsigned bins32[];
+    unsigned* lo = bins32;
+    unsigned* hi = bins32 + (SMEM_BINS ? (1 << d_out) : 0);
     for (int i = threadIdx.x; i < groups * 256; i += blockDim.x) tab[i] = table[i];
     if (SMEM_BINS)
-        for (int i = threadIdx.x; i < (1 << d_out); i += blockDim.x) bins[i] = 0ull;
+        for (int i = threadIdx.x; i < (2 << d_out); i += blockDim.x) bins32[i] = 0u;
     __syncthreads();
     const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < count; j += nth) {
-        unsigned t = 0;
-        for (int q = 0; q < groups; ++q) t ^= tab[q * 256 + ((j >> (8 * q)) & 255u)];
-        const unsigned long long v = x ? (unsigned long long)x[j] : (unsigned long long)gen_value(g, j);
-        if (SMEM_BINS)
-            atomicAdd(&bins[t], v);
-        else
+    auto add = [&](unsigned t, unsigned long long v) {
+        if (SMEM_BINS) {
+            const unsigned vl = (unsigned)v, vh = (unsigned)(v >> 32);
+            const unsigned old = atomicAdd(&lo[t], vl);
+            const unsigned carry = (old + vl) < old ? 1u : 0u;
+            if (vh + carry) atomicAdd(&hi[t], vh + carry);
+        } else {
             atomicAdd(&out[t], v);
+        }
+    };
+    if (count >= 4) {
+        // Quads of consecutive indices: L.j is linear, so L.(4m + i) =
+        // L.(4m) ^ L.i -- one set of table lookups per four points, and two
+        // 16-byte loads.
+        const unsigned l1 = tab[1], l2 = tab[2], l3 = tab[3];
+        const bool vec = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
+        const uint64_t quads = count >> 2;
+        for (uint64_t m = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; m < quads; m += nth) {
+            const uint64_t j = m << 2;
+            unsigned t = 0;
+            for (int q = 0; q < groups; ++q) t ^= tab[q * 256 + ((j >> (8 * q)) & 255u)];
+            unsigned long long v0, v1, v2, v3;
+            if (x && vec) {
+                const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(x + j);
+                const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(x + j + 2);
+                v0 = a.x, v1 = a.y, v2 = b.x, v3 = b.y;
+            } else if (x) {  // 8-byte aligned view
+                v0 = (unsigned long long)x[j], v1 = (unsigned long long)x[j + 1];
+                v2 = (unsigned long long)x[j + 2], v3 = (unsigned long long)x[j + 3];
+            } else {
+                v0 = (unsigned long long)gen_value(g, j);
+                v1 = (unsigned long long)gen_value(g, j + 1);
+                v2 = (unsigned long long)gen_value(g, j + 2);
+                v3 = (unsigned long long)gen_value(g, j + 3);
+            }
+            add(t, v0);
+            add(t ^ l1, v1);
+            add(t ^ l2, v2);
+            add(t ^ l3, v3);
+        }
+    } else {
+        for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < count; j += nth) {
+            unsigned t = 0;
+            for (int q = 0; q < groups; ++q) t ^= tab[q * 256 + ((j >> (8 * q)) & 255u)];
+            add(t, x ? (unsigned long long)x[j] : (unsigned long long)gen_value(g, j));
+        }
     }
     if (SMEM_BINS) {
         __syncthreads();
-        for (int i = threadIdx.x; i < (1 << d_out); i += blockDim.x)
-            if (bins[i]) atomicAdd(&out[i], bins[i]);
+        for (int i = threadIdx.x; i < (1 << d_out); i += blockDim.x) {
+            const unsigned long long b = ((unsigned long long)hi[i] << 32) | lo[i];
+            if (b) atomicAdd(&out[i], b);
+        }
     }
 }
 
