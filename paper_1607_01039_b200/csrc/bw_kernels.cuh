@@ -959,8 +959,8 @@ __global__ void __launch_bounds__(256) k_sumsq(const long long* __restrict__ x, 
 // ---------------------------------------------------------------------------
 constexpr int kFoldGroups = 5;  // d_in <= 40
 
-template <bool SMEM_BINS>
-__global__ void __launch_bounds__(256) k_fold(const long long* __restrict__ x, uint64_t count,
+template <bool SMEM_BINS, int NT = 256>
+__global__ void __launch_bounds__(NT) k_fold(const long long* __restrict__ x, uint64_t count,
                                               const unsigned* __restrict__ table, int groups, int d_out,
                                               unsigned long long* out, GenParams g) {
     __shared__ unsigned tab[kFoldGroups * 256];

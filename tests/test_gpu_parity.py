@@ -478,7 +478,7 @@ def test_fold_matches_reference(golden_npz, coracle):
     with pytest.raises(subspace.DimMismatch):
         subspace.fold(bw.Signal(dev(x[:1 << 15])), z["rows"])
     # large outputs (global atomics) and generated inputs
-    for n, d_out, idx in ((22, 14, 2), (24, 20, 5), (20, 8, 3)):
+    for n, d_out, idx in ((22, 14, 2), (23, 13, 2), (24, 12, 2), (24, 20, 5), (20, 8, 3)):
         spec = signals.config(idx, n)
         rows = subspace.random_full_rank(n, d_out, n)
         want = np.empty(1 << d_out, dtype=np.int64)
