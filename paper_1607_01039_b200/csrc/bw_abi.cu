@@ -487,6 +487,26 @@ int set_all_pass_attributes() {
     });
 }
 
+// Launch `kern` on `grid` CTAs of config C's shape (threads, dynamic shared
+// memory) -- as thread-block clusters of C's size when C::Q > 0.
+template <class C, class... KArgs, class... Args>
+int launch_cfg(void (*kern)(KArgs...), unsigned grid, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(bw::Dims<C>::NT);
+    cfg.dynamicSmemBytes = bw::Dims<C>::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = bw::Dims<C>::CLUSTER;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = C::Q > 0 ? 1 : 0;
+    BW_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+    return BW_OK;
+}
+
 int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractArgs* exp = nullptr,
                 const int* src32 = nullptr) {
     bw::ExtractArgs ex = {};
@@ -502,45 +522,12 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractA
         constexpr int L = decltype(l)::value;
         const unsigned grid = (unsigned)(1ull << (n - bw::kCtaBits));
         constexpr bool kLow = L >= C::T;
-        if constexpr (C::Q == 0) {
-            if constexpr (kLow) {
-                if (src32) {
-                    bw::k_pass<C, L, false, true><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k, ex, src32);
-                    BW_LAUNCHED("fwht widening pass launch");
-                    return BW_OK;
-                }
-            }
-            if (ex.count)
-                bw::k_pass<C, L, true><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k, ex, nullptr);
-            else
-                bw::k_pass<C, L, false><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(d, p.k, ex, nullptr);
-            BW_LAUNCHED("fwht pass launch");
-        } else {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(grid);
-            cfg.blockDim = dim3(bw::Dims<C>::NT);
-            cfg.dynamicSmemBytes = bw::Dims<C>::SMEM_BYTES;
-            cfg.stream = s;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = bw::Dims<C>::CLUSTER;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            const int* none = nullptr;
-            if constexpr (kLow) {
-                if (src32) {
-                    BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L, false, true>, d, p.k, ex, src32));
-                    return BW_OK;
-                }
-            }
-            if (ex.count)
-                BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L, true>, d, p.k, ex, none));
-            else
-                BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L, false>, d, p.k, ex, none));
+        const int* none = nullptr;
+        if constexpr (kLow) {
+            if (src32) return launch_cfg<C>(bw::k_pass<C, L, false, true>, grid, s, d, p.k, ex, src32);
         }
-        return BW_OK;
+        if (ex.count) return launch_cfg<C>(bw::k_pass<C, L, true>, grid, s, d, p.k, ex, none);
+        return launch_cfg<C>(bw::k_pass<C, L, false>, grid, s, d, p.k, ex, none);
     });
 }
 
@@ -609,27 +596,8 @@ int run_scalar_plan(u64* d, int log2n, cudaStream_t s) {
             using C = typename decltype(t)::type;
             constexpr int L = decltype(l)::value;
             const unsigned grid = (unsigned)(1ull << (log2n - bw::kCtaBits));
-            if constexpr (C::Q == 0) {
-                bw::k_pass<C, L, false, false, FP><<<grid, bw::Dims<C>::NT, bw::Dims<C>::SMEM_BYTES, s>>>(
-                    d, p.k, bw::ExtractArgs{}, nullptr);
-                BW_LAUNCHED("scalar-layout pass launch");
-            } else {
-                cudaLaunchConfig_t cfg = {};
-                cfg.gridDim = dim3(grid);
-                cfg.blockDim = dim3(bw::Dims<C>::NT);
-                cfg.dynamicSmemBytes = bw::Dims<C>::SMEM_BYTES;
-                cfg.stream = s;
-                cudaLaunchAttribute attr[1];
-                attr[0].id = cudaLaunchAttributeClusterDimension;
-                attr[0].val.clusterDim.x = bw::Dims<C>::CLUSTER;
-                attr[0].val.clusterDim.y = 1;
-                attr[0].val.clusterDim.z = 1;
-                cfg.attrs = attr;
-                cfg.numAttrs = 1;
-                const int* none = nullptr;
-                BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass<C, L, false, false, FP>, d, p.k, bw::ExtractArgs{}, none));
-            }
-            return BW_OK;
+            const int* none = nullptr;
+            return launch_cfg<C>(bw::k_pass<C, L, false, false, FP>, grid, s, d, p.k, bw::ExtractArgs{}, none);
         }));
     }
     return BW_OK;
@@ -1270,31 +1238,14 @@ int bw_fwht_xfused_pass_i64(int64_t* const* shards, int log2p, int log2n_local, 
         return with_fused_kernel<LOGP>(L, [&](auto l) -> int {
             constexpr int LL = decltype(l)::value;
             if (q == 1) {
-                if constexpr (LL >= 4 && LL <= 8 && LL + LOGP <= 13) {
-                    using C = bw::CfgHigh14c;
-                    cudaLaunchConfig_t cfg = {};
-                    cfg.gridDim = dim3((unsigned)(per << 1));
-                    cfg.blockDim = dim3(bw::Dims<C>::NT);
-                    cfg.dynamicSmemBytes = bw::Dims<C>::SMEM_BYTES;
-                    cfg.stream = s;
-                    cudaLaunchAttribute attr[1];
-                    attr[0].id = cudaLaunchAttributeClusterDimension;
-                    attr[0].val.clusterDim.x = 2;
-                    attr[0].val.clusterDim.y = 1;
-                    attr[0].val.clusterDim.z = 1;
-                    cfg.attrs = attr;
-                    cfg.numAttrs = 1;
-                    BW_CUDA(cudaLaunchKernelEx(&cfg, bw::k_pass_x<C, LL, LOGP>, sp, k, (uint64_t)rank * per));
-                    return BW_OK;
-                }
+                if constexpr (LL >= 4 && LL <= 8 && LL + LOGP <= 13)
+                    return launch_cfg<bw::CfgHigh14c>(bw::k_pass_x<bw::CfgHigh14c, LL, LOGP>, (unsigned)(per << 1), s,
+                                                      sp, k, (uint64_t)rank * per);
                 return fail(BW_BAD_ARGUMENTS, "no cluster fused kernel for L=%d p=%d", LL, LOGP);
             }
             if constexpr (LL + LOGP <= 12) {
-                bw::k_pass_x<bw::CfgHigh13, LL, LOGP>
-                    <<<(unsigned)per, bw::Dims<bw::CfgHigh13>::NT, bw::Dims<bw::CfgHigh13>::SMEM_BYTES, s>>>(
-                        sp, k, (uint64_t)rank * per);
-                BW_LAUNCHED("k_pass_x launch");
-                return BW_OK;
+                return launch_cfg<bw::CfgHigh13>(bw::k_pass_x<bw::CfgHigh13, LL, LOGP>, (unsigned)per, s, sp, k,
+                                                 (uint64_t)rank * per);
             } else {
                 return fail(BW_BAD_ARGUMENTS, "no fused kernel for L=%d p=%d", LL, LOGP);
             }
