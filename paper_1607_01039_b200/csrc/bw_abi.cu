@@ -66,6 +66,8 @@ bool g_attr_done[kMaxDevices];
 int g_num_sms[kMaxDevices];
 // BW_TWO_PASS=0 disables the single-launch path for two-pass plans (A/B knob).
 const bool g_two_pass = !(getenv("BW_TWO_PASS") && getenv("BW_TWO_PASS")[0] == '0');
+// BW_HOST_PIPELINE=0 disables the copy/compute overlap of host-buffer transforms (A/B knob).
+const bool g_host_pipeline = !(getenv("BW_HOST_PIPELINE") && getenv("BW_HOST_PIPELINE")[0] == '0');
 // Small device scratch (reduction results, extraction counts, fold tables)
 // for calls that get none from the caller.  Per host thread: every call that
 // uses it synchronises its stream before returning, so a thread never has two
@@ -879,6 +881,75 @@ int bw_fwht_inplace_i64(int64_t* data, int log2n, int64_t* scratch_dev, void* st
     return bw_fwht_i64(data, log2n, stream, butterflies);
 }
 
+}  // extern "C"
+namespace {
+// Host buffer -> device -> host with the copies overlapping the passes:
+// the H2D of each chunk is followed at once by the passes that stay inside
+// a chunk (every pass but the last), and the last pass runs in column
+// slices, each slice's rows going back with a 2-D D2H copy while the next
+// slice computes.  Copies run on a per-device copy stream, ordered against
+// the caller's stream with events.  *done = false when the plan does not
+// have that shape (the caller then runs the plain sequence).
+cudaStream_t g_copy_stream[kMaxDevices];
+
+int host_pipelined(int64_t* host, int log2n, u64* d, int dev, cudaStream_t s, bool* done) {
+    *done = false;
+    if (log2n < 24) return BW_OK;
+    std::vector<int> w;
+    BW_TRY(default_plan(log2n, &w));
+    std::vector<Pass> passes;
+    BW_TRY(build_passes(log2n, w, &passes));
+    if (passes.size() < 2) return BW_OK;
+    const Pass last = passes.back();
+    if ((last.kind != HIGH && last.kind != REG) || last.k + last.r != log2n) return BW_OK;
+    const int B = last.k;                                  // the other passes cover stages [0, B)
+    const int cb = B > log2n - 7 ? B : log2n - 7;          // H2D chunks of 2^cb points (<= 128 chunks)
+    const int wb = B - 4;                                  // last pass in 16 column slices of 2^wb columns
+    int colbits = 0;
+    BW_TRY(visit_pass(last, [&](auto t, auto l) -> int {
+        colbits = decltype(l)::value;
+        return BW_OK;
+    }));
+    if (wb < colbits || wb + last.r < bw::kCtaBits + last.q) return BW_OK;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!g_copy_stream[dev]) BW_CUDA(cudaStreamCreateWithFlags(&g_copy_stream[dev], cudaStreamNonBlocking));
+    }
+    cudaStream_t cs = g_copy_stream[dev];
+    const int nchunks = 1 << (log2n - cb), nslices = 1 << (B - wb);
+    std::vector<cudaEvent_t> ev(nchunks + nslices + 2);
+    for (auto& e : ev) BW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const int st = [&]() -> int {
+        BW_CUDA(cudaEventRecord(ev[0], s));  // the copy stream follows earlier work on the caller's stream
+        BW_CUDA(cudaStreamWaitEvent(cs, ev[0], 0));
+        for (int c = 0; c < nchunks; ++c) {
+            const size_t off = (size_t)c << cb;
+            BW_CUDA(cudaMemcpyAsync(d + off, host + off, (size_t)8 << cb, cudaMemcpyHostToDevice, cs));
+            BW_CUDA(cudaEventRecord(ev[1 + c], cs));
+            BW_CUDA(cudaStreamWaitEvent(s, ev[1 + c], 0));
+            for (size_t i = 0; i + 1 < passes.size(); ++i) BW_TRY(launch_pass(passes[i], d + off, cb, s));
+        }
+        for (int j = 0; j < nslices; ++j) {
+            const size_t off = (size_t)j << wb;
+            BW_TRY(launch_pass(last, d + off, wb + last.r, s));
+            BW_CUDA(cudaEventRecord(ev[1 + nchunks + j], s));
+            BW_CUDA(cudaStreamWaitEvent(cs, ev[1 + nchunks + j], 0));
+            BW_CUDA(cudaMemcpy2DAsync(host + off, (size_t)8 << B, d + off, (size_t)8 << B, (size_t)8 << wb,
+                                      (size_t)1 << last.r, cudaMemcpyDeviceToHost, cs));
+        }
+        BW_CUDA(cudaEventRecord(ev.back(), cs));
+        BW_CUDA(cudaStreamWaitEvent(s, ev.back(), 0));
+        return BW_OK;
+    }();
+    BW_CUDA(cudaStreamSynchronize(s));
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (st != BW_OK) return st;
+    *done = true;
+    return BW_OK;
+}
+}  // namespace
+extern "C" {
+
 int bw_fwht_host_i64(int64_t* host, int log2n, int64_t* work_dev, int check_bound, void* stream,
                      uint64_t* butterflies) {
     if (!host) return fail(BW_BAD_ARGUMENTS, "null host pointer");
@@ -886,6 +957,14 @@ int bw_fwht_host_i64(int64_t* host, int log2n, int64_t* work_dev, int check_boun
     int dev = 0;
     BW_TRY(device_setup(&dev));
     cudaStream_t s = as_stream(stream);
+    if (!check_bound && !(reinterpret_cast<uintptr_t>(work_dev) & 15u) && g_host_pipeline) {
+        bool done = false;
+        BW_TRY(host_pipelined(host, log2n, reinterpret_cast<u64*>(work_dev), dev, s, &done));
+        if (done) {
+            if (butterflies) *butterflies = butterfly_count(log2n);
+            return BW_OK;
+        }
+    }
     const size_t bytes = (size_t)8 << log2n;
     BW_CUDA(cudaMemcpyAsync(work_dev, host, bytes, cudaMemcpyHostToDevice, s));
     int64_t* sc = nullptr;

@@ -532,3 +532,19 @@ def test_concurrent_host_threads_do_not_share_scratch():
     for th in threads:
         th.join()
     assert results == {k: True for k in range(4)}
+
+
+@pytest.mark.parametrize("n", [24, 26])
+def test_host_buffer_transform_overlapped_copies(coracle, n):
+    """fwht_array on a host numpy buffer (pageable and pinned): the copy /
+    compute pipeline (chunked H2D + per-chunk passes, column-sliced last pass
+    + 2-D D2H) equals the oracle."""
+    x = oracle_np.gen(2, 500 + n, [1 << 20], 0, 1 << n)
+    ref = c_fwht(coracle, x)
+    a = x.copy()
+    assert bw.fwht_array(a) == n << (n - 1)
+    assert np.array_equal(a, ref)
+    pinned = torch.from_numpy(x.copy()).pin_memory()
+    b = pinned.numpy()
+    assert bw.fwht_array(b) == n << (n - 1)
+    assert np.array_equal(b, ref)
