@@ -195,6 +195,14 @@ def run_reference(a):
 
 # ------------------------------------------------------------ GPU leg ---
 
+def pass_stages(q) -> str:
+    """Stage bits of a plan pass: 'k..k+r-1', or both runs of a split-row pass."""
+    k, r, sa = q["k"], q["r"], q.get("split_a", 0)
+    if not sa:
+        return f"{k}..{k + r - 1}"
+    return f"{k}..{k + sa - 1} + {q['k2']}..{q['k2'] + r - sa - 1}"
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -431,7 +439,8 @@ def run_ours(a):
                    "n": n, "log2p": p, "local_log2n": nl, "parallelism": f"top {p} index bits sharded over {ws} GPUs",
                    "exchange": st["mode"] if p > 0 else None,
                    "exchange_trial_ms": trial_ms or None,
-                   "passes": [{"kind": q["kind"], "k": q["k"], "r": q["r"], "cluster": q["cluster"]}
+                   "passes": [dict({"kind": q["kind"], "k": q["k"], "r": q["r"], "cluster": q["cluster"]},
+                                   **({"rows": pass_stages(q)} if q.get("split_a") else {}))
                               for q in plan["passes"]],
                    "l2": ("L2 flushed between steps (256 MiB write, outside the step events)" if flush
                           else f"{(8 << nl) >> 30} GiB input >> 126 MB L2 (no flush needed)"),
@@ -440,7 +449,7 @@ def run_ours(a):
                               else "CUDA events around the K back-to-back steps")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": f"pass {dom} ({plan['passes'][dom]['kind']}, stages "
-                     f"{plan['passes'][dom]['k']}..{plan['passes'][dom]['k'] + plan['passes'][dom]['r'] - 1})",
+                     f"{pass_stages(plan['passes'][dom])})",
                      "algorithmic_bytes_per_launch": bytes_per_pass, "peak_source": peak_src,
                      "frac_of_8tbs_spec": achieved / 8000.0},
         "passes_ms": [round(v, 4) for v in avg_pass],

@@ -66,6 +66,8 @@ bool g_attr_done[kMaxDevices];
 int g_num_sms[kMaxDevices];
 // BW_TWO_PASS=0 disables the single-launch path for two-pass plans (A/B knob).
 const bool g_two_pass = !(getenv("BW_TWO_PASS") && getenv("BW_TWO_PASS")[0] == '0');
+// BW_SPLIT_PLANS=0 keeps the default planner to one-run high passes (A/B knob).
+const bool g_split_plans = !(getenv("BW_SPLIT_PLANS") && getenv("BW_SPLIT_PLANS")[0] == '0');
 // BW_HOST_PIPELINE=0 disables the copy/compute overlap of host-buffer transforms (A/B knob).
 const bool g_host_pipeline = !(getenv("BW_HOST_PIPELINE") && getenv("BW_HOST_PIPELINE")[0] == '0');
 // Small device scratch (reduction results, extraction counts, fold tables)
@@ -135,14 +137,31 @@ int grid_for(int dev, uint64_t work_items, int threads, int per_sm) {
 // register-only pass, r = 6..8 a single-CTA tile, r = 9 a cluster of 2 and
 // r = 10 a cluster of 4 (so every row segment stays >= 256 B).  Tests may
 // force the cluster size of a high pass with the entry r | (q + 1) << 4.
+//
+// A high entry r | (q + 1) << 4 | a << 8 | k2 << 12 with a > 0 is a SPLIT
+// pass (bw_layouts.h): its first a rows start at the lowest stage bit no
+// earlier pass covered, the other r - a rows are bits [k2, k2 + r - a).
+// A plain entry always starts at the lowest uncovered bit, so passes may
+// come in any order (int64 stages commute); the plan must cover every bit
+// exactly once.
 
 enum PassKind { SMALL, LOW, HIGH, REG };
 
 struct Pass {
     PassKind kind;
-    int k;  // first stage bit
-    int r;  // number of stages
-    int q;  // log2 cluster size of LOW / HIGH passes
+    int k;       // first stage bit
+    int r;       // number of stages
+    int q;       // log2 cluster size of LOW / HIGH passes
+    int a = 0;   // split passes: rows [k, k+a) u [k2, k2+r-a); 0 = one run [k, k+r)
+    int k2 = 0;
+    // the kernels' int k argument (bw::split_pack for split passes)
+    int karg() const { return a ? bw::split_pack(k, a, k2) : k; }
+    // mask of the global stage bits of a LOW / HIGH / REG pass
+    uint64_t stage_mask() const {
+        if (kind == LOW) return (1ull << r) - 1ull;
+        if (!a) return ((1ull << r) - 1ull) << k;
+        return (((1ull << a) - 1ull) << k) | (((1ull << (r - a)) - 1ull) << k2);
+    }
 };
 
 template <class T>
@@ -171,6 +190,11 @@ int visit_pass(const Pass& p, F&& f) {
             if (p.q == 1) return f(tag<bw::CfgLow14c>{}, ic<14>{});
             return f(tag<bw::CfgLow15c>{}, ic<15>{});
         case HIGH:
+            if (p.a > 0) {  // split rows: 6..8 rows on one CTA, 9..10 on a cluster of 2
+                if (p.q == 0) return with_L<bw::CfgHigh13S, 5, 7>(13 - p.r, f);
+                if (p.q == 1) return with_L<bw::CfgHigh14cS, 4, 5>(14 - p.r, f);
+                return fail(BW_BAD_ARGUMENTS, "split rows need a cluster of 1 or 2");
+            }
             if (p.q == 0) return with_L<bw::CfgHigh13, 3, 7>(13 - p.r, f);
             if (p.q == 1) return with_L<bw::CfgHigh14c, 4, 8>(14 - p.r, f);
             return with_L<bw::CfgHigh15c, 5, 10>(15 - p.r, f);
@@ -280,8 +304,47 @@ bool env_plan(int n, std::vector<int>* widths) {
     return true;
 }
 
+// Split-row passes on a cluster of 2 (9 or 10 rows: a low rows right above
+// the low pass plus the top rows of the signal), TB/s x 100 by a = 1..9.
+// Measured by tools/sweep_split.py at n = 32, 33, 34 (profiles/
+// r01_split_n*.json): the rate depends on a (how many rows share a DRAM
+// page neighbourhood), not on n or on where the top run starts.
+constexpr int kSplitEff[10] = {0, 552, 566, 572, 580, 583, 583, 583, 583, 583};
+
+// Three-pass plans with a split pass: low w0, the split pass (rows
+// [w0, w0+a) u [n-(rs-a), n)), and one contiguous pass over the bits in
+// between.  The contiguous pass is listed last, so a fused extraction runs
+// on it.  Returns the cost (units as best_high_split) or -1.
+long long best_split_plan(int n, int w0, std::vector<int>* out) {
+    long long best = -1;
+    for (int rs = 9; rs <= 10; ++rs) {
+        const int rm = n - w0 - rs;
+        if (rm < 1 || rm > bw::kMaxHighBits) continue;
+        for (int a = 1; a < rs; ++a) {
+            const int k2 = n - (rs - a), km = w0 + a;
+            int em = shape_eff(rm, 0, km), entry = rm;
+            if (rm > bw::kRegOnlyMaxBits) {
+                const int e1 = shape_eff(rm, 1, km);
+                if (e1 > em) {
+                    em = e1;
+                    entry = rm | (2 << 4);
+                } else {
+                    entry = rm | (1 << 4);
+                }
+            }
+            const long long cost = 1000000 / kSplitEff[a] + 1000000 / em;
+            if (best < 0 || cost < best) {
+                best = cost;
+                out->assign({rs | (2 << 4) | (a << 8) | (k2 << 12), entry});
+            }
+        }
+    }
+    return best;
+}
+
 // Default plan: the cheapest plan under the measured cost model (low pass
-// of 13, 14 or 15 bits, then the best split of the rest).  Cached per n.
+// of 13, 14 or 15 bits, then the best split of the rest into one-run high
+// passes, or a split-row pass plus one contiguous pass).  Cached per n.
 int default_plan(int n, std::vector<int>* widths) {
     widths->clear();
     if (env_plan(n, widths)) return BW_OK;
@@ -306,6 +369,14 @@ int default_plan(int n, std::vector<int>* widths) {
             widths->assign(1, w0);
             widths->insert(widths->end(), hi.begin(), hi.end());
         }
+        if (g_split_plans) {
+            const long long sc = best_split_plan(n, w0, &hi);
+            if (sc >= 0 && 1000000 / kLowEff[w0 - 13] + sc < best_cost) {
+                best_cost = 1000000 / kLowEff[w0 - 13] + sc;
+                widths->assign(1, w0);
+                widths->insert(widths->end(), hi.begin(), hi.end());
+            }
+        }
     }
     if (n <= BW_MAX_LOG2N) cache[n] = *widths;
     return BW_OK;
@@ -328,26 +399,44 @@ int build_passes(int n, const std::vector<int>& widths, std::vector<Pass>* passe
     if (w0 < 13 || w0 > 15 || w0 > n)
         return fail(BW_BAD_ARGUMENTS, "the low pass covers 13, 14 or 15 bits (got %d, n = %d)", w0, n);
     passes->push_back({LOW, 0, w0, w0 - 13});
-    int k = w0;
+    uint64_t covered = (1ull << w0) - 1ull;
     for (size_t i = 1; i < widths.size(); ++i) {
-        const int r = widths[i] & 15;
-        const int forced = (widths[i] >> 4) - 1;
-        if (r < 1 || r > bw::kMaxHighBits || widths[i] < 0 || forced > bw::kMaxClusterLog2)
-            return fail(BW_BAD_ARGUMENTS, "bad high pass entry %d (width 1..%d, cluster q 0..%d)", widths[i],
+        const int e = widths[i];
+        const int r = e & 15;
+        const int forced = ((e >> 4) & 15) - 1;
+        const int a = (e >> 8) & 15, k2 = (e >> 12) & 63;
+        if (e < 0 || (e >> 18) || r < 1 || r > bw::kMaxHighBits || forced > bw::kMaxClusterLog2 || a >= r)
+            return fail(BW_BAD_ARGUMENTS, "bad high pass entry %d (width 1..%d, cluster q 0..%d, split 0..r-1)", e,
                         bw::kMaxHighBits, bw::kMaxClusterLog2);
-        if (r <= bw::kRegOnlyMaxBits && forced <= 0) {
-            passes->push_back({REG, k, r, 0});
+        const int k = __builtin_ctzll(~covered);  // lowest uncovered bit
+        Pass p;
+        if (r <= bw::kRegOnlyMaxBits && forced <= 0 && a == 0) {
+            p = {REG, k, r, 0};
         } else {
             const int q = forced >= 0 ? forced : high_default_q(r);
             const int L = 13 + q - r;
             const int lmin = q == 0 ? 3 : q == 1 ? 4 : 5;
             if (L < lmin || L > (q == 0 ? 7 : q == 1 ? 8 : 10))
                 return fail(BW_BAD_ARGUMENTS, "no high-pass kernel for %d stages on a cluster of %d", r, 1 << q);
-            passes->push_back({HIGH, k, r, q});
+            p = {HIGH, k, r, q};
+            if (a > 0) {
+                if (k2 < k + a || (q == 0 ? (r < 6 || r > 8) : (q != 1 || r < 9)))
+                    return fail(BW_BAD_ARGUMENTS, "bad split pass: rows [%d,%d) + [%d,%d) on a cluster of %d", k,
+                                k + a, k2, k2 + r - a, 1 << q);
+                p.a = a;
+                p.k2 = k2;
+            }
         }
-        k += r;
+        const uint64_t m = p.stage_mask();
+        if (k + (a ? a : r) > 63 || (a && k2 + r - a > 63) || (m & covered))
+            return fail(BW_BAD_ARGUMENTS, "high pass entry %d overlaps earlier passes", e);
+        covered |= m;
+        passes->push_back(p);
     }
-    if (k != n && !(partial && k < n)) return fail(BW_BAD_ARGUMENTS, "pass widths cover %d bits, signal has %d", k, n);
+    const uint64_t all = n >= 64 ? ~0ull : (1ull << n) - 1ull;
+    if (covered & ~all) return fail(BW_BAD_ARGUMENTS, "pass widths reach beyond the signal's %d bits", n);
+    if (covered != all && !(partial && covered == ((1ull << __builtin_ctzll(~covered)) - 1ull)))
+        return fail(BW_BAD_ARGUMENTS, "pass widths cover %d of the signal's %d bits", __builtin_popcountll(covered), n);
     return BW_OK;
 }
 
@@ -360,6 +449,11 @@ int for_all_pass_kernels(F&& f) {
             BW_TRY(visit_pass(Pass{HIGH, 0, 13 + q - L, q}, f));
     }
     for (int r = 1; r <= bw::kRegOnlyMaxBits; ++r) BW_TRY(visit_pass(Pass{REG, 0, r, 0}, f));
+    for (int r = 6; r <= 10; ++r) {  // split-row variants
+        Pass p{HIGH, 0, r, r <= 8 ? 0 : 1};
+        p.a = 1;
+        BW_TRY(visit_pass(p, f));
+    }
     return BW_OK;
 }
 
@@ -455,7 +549,7 @@ int set_all_pass_attributes() {
         BW_TRY(visit_pass(p, [](auto t, auto l) -> int {
             using C = typename decltype(t)::type;
             constexpr int L = decltype(l)::value;
-            if constexpr (C::Q == 0 && L < C::T) return set_two_pass_attr<C, L>();
+            if constexpr (C::Q == 0 && L < C::T && !bw::SplitOf<C>::value) return set_two_pass_attr<C, L>();
             return BW_OK;
         }));
     }
@@ -478,7 +572,10 @@ int set_all_pass_attributes() {
         using C = typename decltype(t)::type;
         constexpr int L = decltype(l)::value;
         constexpr int smem = bw::Dims<C>::SMEM_BYTES;
-        if (smem > 48 * 1024) {
+        if constexpr (bw::SplitOf<C>::value) {
+            BW_CUDA(cudaFuncSetAttribute(bw::k_pass_split<C, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            BW_CUDA(cudaFuncSetAttribute(bw::k_pass_split<C, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        } else if (smem > 48 * 1024) {
             BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             if constexpr (L >= C::T)
@@ -509,6 +606,20 @@ int launch_cfg(void (*kern)(KArgs...), unsigned grid, cudaStream_t s, Args... ar
     return BW_OK;
 }
 
+// Element offsets of every register index in the load and the store round
+// of a split-row pass (k_pass_split reads them from its parameters).
+template <class C, int L>
+bw::SplitTab split_table(int karg) {
+    static_assert(bw::Dims<C>::E == 32, "32 registers per thread");
+    constexpr int LAST = C::NR - 1;
+    bw::SplitTab t;
+    for (int j = 0; j < 32; ++j) {
+        t.ld[j] = bw::global_off<C::T, L, true>(bw::reg_part<C, 0>(j), karg);
+        t.st[j] = bw::global_off<C::T, L, true>(bw::reg_part<C, LAST>(j), karg);
+    }
+    return t;
+}
+
 int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractArgs* exp = nullptr,
                 const int* src32 = nullptr) {
     bw::ExtractArgs ex = {};
@@ -525,11 +636,17 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractA
         const unsigned grid = (unsigned)(1ull << (n - bw::kCtaBits));
         constexpr bool kLow = L >= C::T;
         const int* none = nullptr;
+        if constexpr (bw::SplitOf<C>::value) {
+            const bw::SplitTab tab = split_table<C, L>(p.karg());
+            if (ex.count) return launch_cfg<C>(bw::k_pass_split<C, L, true>, grid, s, d, p.karg(), ex, tab);
+            return launch_cfg<C>(bw::k_pass_split<C, L, false>, grid, s, d, p.karg(), ex, tab);
+        } else {
         if constexpr (kLow) {
             if (src32) return launch_cfg<C>(bw::k_pass<C, L, false, true>, grid, s, d, p.k, ex, src32);
         }
         if (ex.count) return launch_cfg<C>(bw::k_pass<C, L, true>, grid, s, d, p.k, ex, none);
         return launch_cfg<C>(bw::k_pass<C, L, false>, grid, s, d, p.k, ex, none);
+        }
     });
 }
 
@@ -556,13 +673,13 @@ int check_signal(const void* data, int log2n) {
 // BW_OK with *done = false when the shape or the residency does not allow it.
 int launch_two_pass(const std::vector<Pass>& passes, u64* d, int n, int dev, cudaStream_t s, bool* done) {
     *done = false;
-    if (passes.size() != 2 || passes[0].kind != LOW || passes[0].q != 0 || passes[1].q != 0) return BW_OK;
+    if (passes.size() != 2 || passes[0].kind != LOW || passes[0].q != 0 || passes[1].q != 0 || passes[1].a) return BW_OK;
     if (passes[1].kind != HIGH && passes[1].kind != REG) return BW_OK;
     const unsigned grid = 1u << (n - bw::kCtaBits);
     return visit_pass(passes[1], [&](auto t, auto l) -> int {
         using C2 = typename decltype(t)::type;
         constexpr int L2 = decltype(l)::value;
-        if constexpr (C2::Q == 0 && L2 < C2::T) {
+        if constexpr (C2::Q == 0 && L2 < C2::T && !bw::SplitOf<C2>::value) {
             auto kern = bw::k_two_pass<bw::CfgLow13, 13, C2, L2, false>;
             constexpr int smem = bw::Dims<bw::CfgLow13>::SMEM_BYTES > bw::Dims<C2>::SMEM_BYTES
                                      ? bw::Dims<bw::CfgLow13>::SMEM_BYTES
@@ -901,7 +1018,9 @@ int host_pipelined(int64_t* host, int log2n, u64* d, int dev, cudaStream_t s, bo
     BW_TRY(build_passes(log2n, w, &passes));
     if (passes.size() < 2) return BW_OK;
     const Pass last = passes.back();
-    if ((last.kind != HIGH && last.kind != REG) || last.k + last.r != log2n) return BW_OK;
+    if ((last.kind != HIGH && last.kind != REG) || last.a || last.k + last.r != log2n) return BW_OK;
+    for (const Pass& p : passes)
+        if (p.a) return BW_OK;  // split rows leave a chunk
     const int B = last.k;                                  // the other passes cover stages [0, B)
     const int cb = B > log2n - 7 ? B : log2n - 7;          // H2D chunks of 2^cb points (<= 128 chunks)
     const int wb = B - 4;                                  // last pass in 16 column slices of 2^wb columns
@@ -1622,9 +1741,9 @@ int bw_plan_describe(int log2n, int log2p, char* json, size_t len) {
                 return BW_OK;
             });
         snprintf(buf, sizeof buf,
-                 "%s{\"kind\":\"%s\",\"k\":%d,\"r\":%d,\"tile_bits\":%d,\"cols_bits\":%d,\"threads\":%d,"
-                 "\"cluster\":%d,\"grid\":%llu,\"smem\":%d}",
-                 i ? "," : "", kind, p.k, p.r, tbits, cols, threads, cluster, grid, smem);
+                 "%s{\"kind\":\"%s\",\"k\":%d,\"r\":%d,\"split_a\":%d,\"k2\":%d,\"tile_bits\":%d,"
+                 "\"cols_bits\":%d,\"threads\":%d,\"cluster\":%d,\"grid\":%llu,\"smem\":%d}",
+                 i ? "," : "", kind, p.k, p.r, p.a, p.a ? p.k2 : 0, tbits, cols, threads, cluster, grid, smem);
         out += buf;
     }
     out += "],\"cross_stages\":[";
@@ -1753,7 +1872,8 @@ int check_pass(int n, int k, std::vector<uint8_t>& touched, uint32_t* stage_bits
     if (tile_stages != rows) return fail(BW_BAD_ARGUMENTS, "tile stages %x != rows %x", tile_stages, rows);
     uint32_t stage_bits = 0;  // the global bits the kernel's stage masks really cover
     for (int b = 0; b < T; ++b)
-        if ((tile_stages >> b) & 1u) stage_bits |= 1u << (b < L ? b : k + (b - L));
+        if ((tile_stages >> b) & 1u)
+            stage_bits |= 1u << (b < L ? b : __builtin_ctzll(bw::global_off<T, L, bw::SplitOf<C>::value>(1u << b, k)));
     *stage_bits_out = stage_bits;
     // Address walk over every (CTA, thread, register): the load layout, the
     // exchange destinations and the store layout must all be bijections.
@@ -1764,7 +1884,7 @@ int check_pass(int n, int k, std::vector<uint8_t>& touched, uint32_t* stage_bits
     std::vector<uint8_t> xdst(C::Q > 0 ? (size_t)NQ << bw::kCtaBits : 0);
     for (uint64_t cta = 0; cta < ctas; ++cta) {
         const uint32_t rank = (uint32_t)(cta & (NQ - 1));
-        const uint64_t base = bw::tile_base<T, L>(cta >> C::Q, k);
+        const uint64_t base = bw::tile_base<T, L, bw::SplitOf<C>::value>(cta >> C::Q, k);
         if (C::Q > 0 && rank == 0) std::fill(xdst.begin(), xdst.end(), 0);
         for (uint32_t t = 0; t < (uint32_t)bw::Dims<C>::NT; ++t) {
             const uint32_t lane = t & 31u, warp = t >> 5;
@@ -1772,8 +1892,8 @@ int check_pass(int n, int k, std::vector<uint8_t>& touched, uint32_t* stage_bits
                 const uint32_t vin = bw::thread_part<C, 0>(lane, warp) | bw::reg_part<C, 0>(j) | bw::rank_bits<C, 0>(rank);
                 const uint32_t vout =
                     bw::thread_part<C, LAST>(lane, warp) | bw::reg_part<C, LAST>(j) | bw::rank_bits<C, LAST>(rank);
-                const uint64_t gi = base + bw::global_off<T, L>(vin, k);
-                const uint64_t go = base + bw::global_off<T, L>(vout, k);
+                const uint64_t gi = base + bw::global_off<T, L, bw::SplitOf<C>::value>(vin, k);
+                const uint64_t go = base + bw::global_off<T, L, bw::SplitOf<C>::value>(vout, k);
                 if (gi >= touched.size() || go >= touched.size())
                     return fail(BW_BAD_ARGUMENTS, "pass at k=%d reaches out of range", k);
                 if (touched[gi] & 1) return fail(BW_BAD_ARGUMENTS, "pass at k=%d loads index %llu twice", k, (unsigned long long)gi);
@@ -1866,12 +1986,12 @@ void emulate_pass(u64* data, int n, int k) {
     std::vector<std::vector<u64>> sm(NQ, std::vector<u64>((size_t)bw::Dims<C>::CTA * 2));
     const uint64_t tiles = 1ull << (n - T);
     for (uint64_t b = 0; b < tiles; ++b) {
-        const uint64_t base = bw::tile_base<T, L>(b, k);
+        const uint64_t base = bw::tile_base<T, L, bw::SplitOf<C>::value>(b, k);
         for (int q = 0; q < NQ; ++q) {
             for (int t = 0; t < NT; ++t)
                 for (int j = 0; j < E; ++j)
                     v[q][(size_t)t * E + j] =
-                        data[base + bw::global_off<T, L>(bw::thread_part<C, 0>(t & 31, t >> 5) | bw::reg_part<C, 0>(j) |
+                        data[base + bw::global_off<T, L, bw::SplitOf<C>::value>(bw::thread_part<C, 0>(t & 31, t >> 5) | bw::reg_part<C, 0>(j) |
                                                              bw::rank_bits<C, 0>((uint32_t)q),
                                                          k)];
             emu_stages<C, L, 0, FP>(v[q]);
@@ -1880,7 +2000,7 @@ void emulate_pass(u64* data, int n, int k) {
         for (int q = 0; q < NQ; ++q)
             for (int t = 0; t < NT; ++t)
                 for (int j = 0; j < E; ++j)
-                    data[base + bw::global_off<T, L>(bw::thread_part<C, LAST>(t & 31, t >> 5) | bw::reg_part<C, LAST>(j) |
+                    data[base + bw::global_off<T, L, bw::SplitOf<C>::value>(bw::thread_part<C, LAST>(t & 31, t >> 5) | bw::reg_part<C, LAST>(j) |
                                                          bw::rank_bits<C, LAST>((uint32_t)q),
                                                      k)] = v[q][(size_t)t * E + j];
     }
@@ -1908,7 +2028,7 @@ extern "C" int bw_plan_check(int log2n, const int* pass_bits, int npasses, uint6
             st = visit_pass(p, [&](auto t, auto l) -> int {
                 using C = typename decltype(t)::type;
                 constexpr int L = decltype(l)::value;
-                return check_pass<C, L>(log2n, p.k, touched, &bits, &bfly);
+                return check_pass<C, L>(log2n, p.karg(), touched, &bits, &bfly);
             });
         }
         if (st != BW_OK) return st;
@@ -1947,7 +2067,7 @@ extern "C" int bw_debug_emulate_i64(int64_t* host, int log2n, const int* pass_bi
         BW_TRY(visit_pass(p, [&](auto t, auto l) -> int {
             using C = typename decltype(t)::type;
             constexpr int L = decltype(l)::value;
-            emulate_pass<C, L>(d, log2n, p.k);
+            emulate_pass<C, L>(d, log2n, p.karg());
             return BW_OK;
         }));
     }

@@ -97,10 +97,10 @@ template <class C, int RD, int T, int L>
 __device__ __forceinline__ void load_global(u64 (&v)[Dims<C>::E], const u64* __restrict__ g,
                                            uint32_t tp, int k) {
     constexpr int E = Dims<C>::E;
-    const u64* p = g + global_off<T, L>(tp, k);
+    const u64* p = g + global_off<T, L, SplitOf<C>::value>(tp, k);
 #pragma unroll
     for (int j = 0; j < E; ++j) {
-        const uint64_t off = global_off<T, L>(reg_part<C, RD>(j), k);
+        const uint64_t off = global_off<T, L, SplitOf<C>::value>(reg_part<C, RD>(j), k);
         if constexpr (VecAccess<C, RD, L>::value) {
             if ((j & 1) == 0) {
                 const ulonglong2 t = ld_pass(reinterpret_cast<const ulonglong2*>(p + off));
@@ -119,10 +119,10 @@ template <class C, int RD, int T, int L>
 __device__ __forceinline__ void load_global_i32(u64 (&v)[Dims<C>::E], const int* __restrict__ g, uint32_t tp,
                                                int k) {
     constexpr int E = Dims<C>::E;
-    const int* p = g + global_off<T, L>(tp, k);
+    const int* p = g + global_off<T, L, SplitOf<C>::value>(tp, k);
 #pragma unroll
     for (int j = 0; j < E; ++j) {
-        const uint64_t off = global_off<T, L>(reg_part<C, RD>(j), k);
+        const uint64_t off = global_off<T, L, SplitOf<C>::value>(reg_part<C, RD>(j), k);
         if constexpr (VecAccess<C, RD, L>::value) {
             if ((j & 1) == 0) {
                 const int2 t = __ldcs(reinterpret_cast<const int2*>(p + off));
@@ -139,10 +139,10 @@ template <class C, int RD, int T, int L>
 __device__ __forceinline__ void store_global(const u64 (&v)[Dims<C>::E], u64* __restrict__ g,
                                              uint32_t tp, int k) {
     constexpr int E = Dims<C>::E;
-    u64* p = g + global_off<T, L>(tp, k);
+    u64* p = g + global_off<T, L, SplitOf<C>::value>(tp, k);
 #pragma unroll
     for (int j = 0; j < E; ++j) {
-        const uint64_t off = global_off<T, L>(reg_part<C, RD>(j), k);
+        const uint64_t off = global_off<T, L, SplitOf<C>::value>(reg_part<C, RD>(j), k);
         if constexpr (VecAccess<C, RD, L>::value) {
             if ((j & 1) == 0) {
                 ulonglong2 t;
@@ -154,6 +154,34 @@ __device__ __forceinline__ void store_global(const u64 (&v)[Dims<C>::E], u64* __
             st_pass(p + off, v[j]);
         }
     }
+}
+
+// Split-row passes: the element offset of every register index of the load
+// round and of the store round, computed once on the host (bw_abi
+// split_table) and read straight from the kernel's parameter space -- one
+// 64-bit add per element, where evaluating the two-run row map per element
+// measured 40% more instructions and 5.2 instead of ~6.2 TB/s.
+struct SplitTab {
+    unsigned long long ld[32];
+    unsigned long long st[32];
+};
+
+template <class C, int T, int L>
+__device__ __forceinline__ void load_global_tab(u64 (&v)[Dims<C>::E], const u64* __restrict__ g, uint32_t tp,
+                                                int k, const SplitTab& tab) {
+    static_assert(Dims<C>::E == 32 && !VecAccess<C, 0, L>::value, "split passes use 8-byte accesses");
+    const u64* p = g + global_off<T, L, true>(tp, k);
+#pragma unroll
+    for (int j = 0; j < Dims<C>::E; ++j) v[j] = ld_pass(p + tab.ld[j]);
+}
+
+template <class C, int T, int L>
+__device__ __forceinline__ void store_global_tab(const u64 (&v)[Dims<C>::E], u64* __restrict__ g, uint32_t tp,
+                                                 int k, const SplitTab& tab) {
+    static_assert(Dims<C>::E == 32 && !VecAccess<C, C::NR - 1, L>::value, "split passes use 8-byte accesses");
+    u64* p = g + global_off<T, L, true>(tp, k);
+#pragma unroll
+    for (int j = 0; j < Dims<C>::E; ++j) st_pass(p + tab.st[j], v[j]);
 }
 
 template <class C, int RD>
@@ -371,10 +399,10 @@ template <class C, int RD, int T, int L>
 __device__ __noinline__ void extract_slow(const u64* g, uint64_t gbase, uint32_t tp, int k, ExtractArgs ex) {
     constexpr int E = Dims<C>::E;
     const uint32_t lane = threadIdx.x & 31u;
-    const uint64_t t0 = global_off<T, L>(tp, k);
+    const uint64_t t0 = global_off<T, L, SplitOf<C>::value>(tp, k);
 #pragma unroll 1
     for (int j = 0; j < E; ++j) {
-        const uint64_t off = t0 + global_off<T, L>(reg_part<C, RD>(j), k);
+        const uint64_t off = t0 + global_off<T, L, SplitOf<C>::value>(reg_part<C, RD>(j), k);
         const u64 x = g[off];
         const bool h = hit_ge_u(x, ex.tau);
         const unsigned b = __ballot_sync(0xffffffffu, h);
@@ -408,6 +436,7 @@ __device__ __forceinline__ void extract_hits(const u64 (&v)[Dims<C>::E], const u
 template <class C, int L, bool EX = false, bool SRC32 = false, bool FP = false>
 __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     k_pass(u64* __restrict__ data, int k, ExtractArgs ex, const int* __restrict__ src32) {
+    static_assert(!SplitOf<C>::value, "split-row configs launch k_pass_split");
     constexpr int T = C::T;
     constexpr int E = Dims<C>::E;
     extern __shared__ u64 sm[];
@@ -447,6 +476,51 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     if constexpr (EX) extract_hits<C, LAST, T, L>(v, g, tile_base<T, L>(tile, k), tp_last, k, ex);
 }
 
+// Split-row pass (k = bw::split_pack(k, a, k2)): k_pass with the global
+// loads and stores driven by the per-register offsets in the kernel's
+// parameter space.  (A separate body, not a flag on k_pass: routing k_pass
+// through a shared device function perturbed its register allocation and
+// cost the 9-stage pass 1%, tools/gpu_ab.sh.)
+template <class C, int L, bool EX = false>
+__global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
+    k_pass_split(u64* __restrict__ data, int k, ExtractArgs ex, const __grid_constant__ SplitTab tab) {
+    static_assert(SplitOf<C>::value && L < C::T, "k_pass_split takes split-row high-pass configs");
+    constexpr int T = C::T;
+    constexpr int E = Dims<C>::E;
+    extern __shared__ u64 sm[];
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = threadIdx.x >> 5;
+    uint32_t rank = 0;
+    uint64_t tile = blockIdx.x;
+    if constexpr (C::Q > 0) {
+        rank = cluster_ctarank();
+        tile = blockIdx.x >> C::Q;
+    }
+    u64* g = data + tile_base<T, L, true>(tile, k);
+
+    if constexpr (C::Q > 0) {
+        // mbarrier counting the bytes the partners will deliver to this CTA;
+        // made visible cluster-wide before the (relaxed) cluster arrive.
+        if (threadIdx.x == 0) {
+            const uint32_t mb = (uint32_t)__cvta_generic_to_shared(sm + Dims<C>::SMEM_ELEMS);
+            constexpr uint32_t bytes_in = 8u * (Dims<C>::CTA - Dims<C>::CTA / Dims<C>::CLUSTER);
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes_in) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    u64 v[E];
+    load_global_tab<C, T, L>(v, g, thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k, tab);
+    if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    apply_stages<C, 0, L>(v);
+    run_rounds<C, L, 1>(v, sm, lane, warp, rank);
+    constexpr int LAST = C::NR - 1;
+    const uint32_t tp_last = thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank);
+    store_global_tab<C, T, L>(v, g, tp_last, k, tab);
+    if constexpr (EX) extract_hits<C, LAST, T, L>(v, g, tile_base<T, L, true>(tile, k), tp_last, k, ex);
+}
+
 // ---------------------------------------------------------------------------
 // Small transforms (n <= 21): both passes of a two-pass plan in ONE
 // cooperative launch -- every CTA transforms its low-bits tile, the grid
@@ -460,7 +534,7 @@ __device__ __forceinline__ void single_tile(u64* __restrict__ data, int k, uint6
     constexpr int T = C::T, E = Dims<C>::E, LAST = C::NR - 1;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
-    u64* g = data + tile_base<T, L>(tile, k);
+    u64* g = data + tile_base<T, L, SplitOf<C>::value>(tile, k);
     u64 v[E];
     load_global<C, 0, T, L>(v, g, thread_part<C, 0>(lane, warp), k);
     apply_stages<C, 0, L, FP>(v);

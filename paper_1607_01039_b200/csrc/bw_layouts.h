@@ -140,6 +140,15 @@ struct CfgHigh15c {
     BW_HD static constexpr int P(int i) { return 11 + i; }
 };
 
+// Split-row variants of the 1- and 2-CTA high passes: the same rounds, but
+// the tile's rows are two runs of global bits (see split_rows below).
+struct CfgHigh13S : CfgHigh13 {
+    static constexpr bool SPLIT = true;
+};
+struct CfgHigh14cS : CfgHigh14c {
+    static constexpr bool SPLIT = true;
+};
+
 // Strided high-bits pass with <= 5 stage rows: register-only, no shared
 // memory; tile bits 8..12 in registers.
 //   round 0: reg {8..12}  lane {0..4}  warp {5,6,7}
@@ -323,19 +332,64 @@ BW_HD constexpr uint32_t stage_mask() {
     return L >= C::T ? C::stage(RD) : (C::stage(RD) & ~((1u << L) - 1u));
 }
 
+// ---- split rows ----------------------------------------------------------
+// A high pass normally stages one run of global bits [k, k+r).  A SPLIT pass
+// stages two runs: tile row i (0 <= i < r) is global bit k + i for i < a and
+// k2 + (i - a) for i >= a (k + a <= k2).  Its kernels receive the three
+// numbers packed in their int k argument.  Split rows let a plan give a
+// pass the low rows {k..k+a-1} of a large-stride pass: the tile then spans
+// 2^(r-a) DRAM pages instead of 2^r (n = 34: rows {14..17} u {28..33} run at
+// 6.27 TB/s, rows {24..33} at 5.77 -- tools/mb_split.cu).  Stages on
+// distinct bits commute in Z/2^64, so any such plan is bit-identical for
+// int64 (float64 keeps its ascending one-run plans).
+BW_HD constexpr int split_pack(int k, int a, int k2) { return k | (a << 8) | (k2 << 16); }
+BW_HD constexpr int split_k(int packed) { return packed & 255; }
+BW_HD constexpr int split_a(int packed) { return (packed >> 8) & 255; }
+BW_HD constexpr int split_k2(int packed) { return packed >> 16; }
+
+// C::SPLIT if the config declares it, else false.
+template <class C, class = void>
+struct SplitOf {
+    static constexpr bool value = false;
+};
+template <class C>
+struct SplitOf<C, decltype(void(C::SPLIT))> {
+    static constexpr bool value = C::SPLIT;
+};
+
 // Global element offset (relative to the tile base) of tile index e.
-template <int T, int L>
+// Linear over disjoint bit sets (every tile bit maps to one global bit).
+template <int T, int L, bool S = false>
 BW_HD inline uint64_t global_off(uint32_t e, int k) {
     if (L >= T) return e;
-    return (uint64_t)(e & ((1u << L) - 1u)) + ((uint64_t)(e >> L) << k);
+    const uint64_t col = e & ((1u << L) - 1u);
+    const uint32_t row = e >> L;
+    if constexpr (!S) {
+        return col + ((uint64_t)row << k);
+    } else {
+        const int a = split_a(k);
+        return col + ((uint64_t)(row & ((1u << a) - 1u)) << split_k(k)) + ((uint64_t)(row >> a) << split_k2(k));
+    }
 }
 
-// Global index of element 0 of tile `b` for a pass over bits [k, k+T-L).
-template <int T, int L>
+// Global index of element 0 of tile `b` for a pass over bits [k, k+T-L)
+// (split: the free global bits [L, k), [k+a, k2), [k2+r-a, ...) take the
+// tile id's bits in ascending order, so neighbouring tiles are neighbouring
+// column groups, as for one run).
+template <int T, int L, bool S = false>
 BW_HD inline uint64_t tile_base(uint64_t b, int k) {
     if (L >= T) return b << T;
-    const int mid = k - L;  // global bits L..k-1 come from the low tile-id bits
-    return ((b & ((1ull << mid) - 1ull)) << L) | ((b >> mid) << (k + T - L));
+    if constexpr (!S) {
+        const int mid = k - L;  // global bits L..k-1 come from the low tile-id bits
+        return ((b & ((1ull << mid) - 1ull)) << L) | ((b >> mid) << (k + T - L));
+    } else {
+        const int k1 = split_k(k), a = split_a(k), k2 = split_k2(k);
+        const int m1 = k1 - L, m2 = k2 - (k1 + a);
+        const uint64_t lo = b & ((1ull << m1) - 1ull);
+        const uint64_t mid = (b >> m1) & ((1ull << m2) - 1ull);
+        const uint64_t hi = b >> (m1 + m2);
+        return (lo << L) | (mid << (k1 + a)) | (hi << (k2 + (T - L) - a));
+    }
 }
 
 }  // namespace bw

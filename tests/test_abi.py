@@ -90,6 +90,42 @@ def test_bad_plans_rejected():
         sharded.plan_check(20, [14, 5])
 
 
+def split(r, q, a, k2):
+    """Plan entry of a split-row high pass: rows [k, k+a) u [k2, k2+r-a),
+    k = the lowest bit no earlier pass covers (bw_layouts.h split rows)."""
+    return r | ((q + 1) << 4) | (a << 8) | (k2 << 12)
+
+
+SPLIT_PLANS = [
+    (24, [13, split(6, 0, 3, 21), 5]),           # rows {13,14,15} u {21,22,23}, then 16..20 in registers
+    (24, [13, split(9, 1, 4, 19), 2]),           # 2-CTA: {13..16} u {19..23}, then 17, 18
+    (24, [13, split(10, 1, 1, 15), 1]),          # 2-CTA, 10 rows: {13} u {15..23}
+    (24, [13, 2, split(7, 0, 3, 20), 2]),        # split pass in the middle
+    (23, [13, split(8, 0, 2, 17), 2]),           # 1-CTA, 8 rows
+    (24, [14, split(9, 1, 2, 17), 1]),         # n=34-like: 14 + split + contiguous rest
+    (22, [13, split(9, 1, 8, 21)]),              # degenerate split (runs adjacent): one run in effect
+]
+
+
+@pytest.mark.parametrize("n,plan", SPLIT_PLANS)
+def test_split_plan_checks(n, plan):
+    """Split-row passes: every element once per pass, every stage once."""
+    assert sharded.plan_check(n, plan) == n << (n - 1)
+
+
+def test_split_plans_rejected():
+    for n, plan in [
+        (24, [13, split(6, 0, 3, 15), 5]),    # second run overlaps the first
+        (24, [13, split(6, 0, 3, 22), 5]),    # reaches bit 24
+        (24, [13, split(5, 0, 2, 20), 6]),    # no split register-only pass
+        (24, [13, split(9, 0, 2, 20), 2]),    # 9 rows need a cluster of 2
+        (24, [13, split(6, 0, 3, 21), 4]),    # leaves bit 20 uncovered
+        (24, [13, split(6, 0, 3, 18), 5]),    # second run overlaps the contiguous pass
+    ]:
+        with pytest.raises(errors.BadArguments):
+            sharded.plan_check(n, plan)
+
+
 def test_plan_describe():
     p = sharded.plan(32, 0)
     assert [x["kind"] for x in p["passes"]] == ["low", "high", "high"]
@@ -188,6 +224,16 @@ def test_kernel_tables_emulated_on_host_match_oracle(coracle, n):
     ref = x.copy()
     coracle.oracle_fwht_i64(ref.ctypes.data, n)
     assert np.array_equal(emulate(x), ref)
+
+
+@pytest.mark.parametrize("n,plan", SPLIT_PLANS)
+def test_split_plans_emulated_on_host_match_oracle(coracle, n, plan):
+    from oracle import oracle_np
+
+    x = oracle_np.gen(2, 700 + n, [1 << 20], 0, 1 << n)
+    ref = x.copy()
+    coracle.oracle_fwht_i64(ref.ctypes.data, n)
+    assert np.array_equal(emulate(x, plan), ref)
 
 
 @pytest.mark.parametrize("n", list(range(0, 25)))

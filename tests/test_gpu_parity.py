@@ -163,6 +163,57 @@ def test_every_pass_split_is_identical(coracle):
         assert np.array_equal(planned(x, plan), ref), plan
 
 
+def split_entry(r, q, a, k2):
+    return r | ((q + 1) << 4) | (a << 8) | (k2 << 12)
+
+
+def test_split_row_plans_identical(coracle):
+    """Split-row passes (rows [k, k+a) u [k2, k2+r-a), bw_layouts.h) on the
+    device: 1- and 2-CTA tiles, the split pass first, in the middle or last,
+    every split point a of a 10-row pass -- byte-identical to the oracle."""
+    sp = split_entry
+    cases = [
+        (24, [[13, sp(6, 0, 3, 21), 5], [13, sp(9, 1, 4, 19), 2], [13, sp(10, 1, 1, 15), 1],
+              [13, 2, sp(7, 0, 3, 20), 2], [14, sp(9, 1, 2, 17), 1], [13, sp(9, 1, 8, 21), 2]]),
+        (27, [[14, sp(10, 1, a, 17 + a), 3] for a in range(1, 10)] +
+             [[13, sp(9, 1, a, 18 + a), 5] for a in (1, 4, 8)] + [[13, sp(8, 0, 3, 22), 6]]),
+    ]
+    for n, plans in cases:
+        x = oracle_np.gen(1, 90 + n, [], 0, 1 << n)
+        ref = c_fwht(coracle, x)
+        for plan in plans:
+            assert np.array_equal(planned(x, plan), ref), plan
+
+
+def test_split_row_pass_extraction(monkeypatch):
+    """The fused extraction on a split-row pass (the hits' global indices come
+    from the split address map).  Passes commute for int64, so the split pass
+    runs last: pass 0, pass 2, then pass 1 with the |W| >= tau epilogue."""
+    n = 24
+    x = oracle_np.gen(2, 41, [1 << 10], 0, 1 << n)
+    b = dev(x)
+    bw.fwht_array(b)
+    tau = 1 << 23  # ~4 sigma: about a thousand hits
+    i2, v2 = bw.extract_ge(b, tau, cap=1 << 18)
+    monkeypatch.setenv("BW_PLAN", ",".join(str(v) for v in [13, split_entry(6, 0, 3, 21), 5]))
+    L = _lib.lib()
+    a = dev(x)
+    sh = torch.cuda.current_stream().cuda_stream
+    cap = 1 << 18
+    idx = torch.empty(cap, dtype=torch.int64, device="cuda")
+    val = torch.empty(cap, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _lib.check(L.bw_fwht_i64_pass(a.data_ptr(), n, 0, sh))
+    _lib.check(L.bw_fwht_i64_pass(a.data_ptr(), n, 2, sh))
+    _lib.check(L.bw_fwht_i64_pass_extract(a.data_ptr(), n, 1, tau, 0, idx.data_ptr(), val.data_ptr(), cap,
+                                          cnt.data_ptr(), sh))
+    assert torch.equal(a, b)
+    k = int(cnt.item())
+    assert k == i2.numel() and 10 < k < cap
+    order = torch.argsort(idx[:k])
+    assert torch.equal(idx[:k][order], i2) and torch.equal(val[:k][order], v2)
+
+
 def test_involution_and_linearity():
     for n in (1, 5, 13, 14, 17, 23, 26):
         x = oracle_np.gen(2, 900 + n, [1000], 0, 1 << n)
