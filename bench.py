@@ -50,7 +50,7 @@ def args_parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--mode", choices=["auto", "fused", "peer", "a2a"], default="auto",
+    ap.add_argument("--mode", choices=["auto", "fused", "peer", "a2a", "narrow"], default="auto",
                     help="cross-GPU exchange (N > 1); auto times fused and a2a (peer with gloo) on two "
                          "steps each and keeps the faster")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
@@ -239,6 +239,8 @@ def run_ours(a):
         candidates = ["none"]
     elif a.mode == "auto":
         candidates = ["fused" if nl >= 14 else "peer", "a2a" if a.dist_backend == "nccl" else "peer"]
+        if nl >= 14 and sharded.narrow_ok(1 << nl, p):  # int8 exchange first (falls back when too wide)
+            candidates.append("narrow")
         candidates = list(dict.fromkeys(candidates))
     else:
         candidates = ["peer" if (a.mode == "fused" and nl < 14) else a.mode]  # fused needs 2^14-point shards
@@ -248,8 +250,12 @@ def run_ours(a):
     def configure(mode):
         st["mode"] = mode
         st["fused"] = mode == "fused"
-        st["npasses"] = 1 if st["fused"] else base_npasses
-        if st["fused"]:  # local passes over the low nl - r bits (one bracket), then K6'
+        st["narrow"] = mode == "narrow"
+        st["npasses"] = 1 if (st["fused"] or st["narrow"]) else base_npasses
+        if st["narrow"] and "nw" not in st:
+            st["nw"] = sharded.NarrowWire(x, None, dist)
+            st["narrow_fallbacks"] = 0
+        if st["fused"] or st["narrow"]:  # local passes over the low nl - r bits (one bracket), then K6'
             st["f_widths"], st["f_r"] = sharded.fused_plan(nl, p)
             st["f_arr"] = (ctypes.c_int * len(st["f_widths"]))(*st["f_widths"])
         if mode == "a2a" and "recv" not in st:
@@ -261,7 +267,7 @@ def run_ours(a):
     ptr = x.data_ptr()
     peer = None
     if p > 0:
-        peer = sharded._PeerMap(x, None, dist) if any(m in ("peer", "fused") for m in candidates) else None
+        peer = sharded._PeerMap(x, None, dist) if any(m in ("peer", "fused", "narrow") for m in candidates) else None
         ones = torch.ones(1, device="cuda")
         ptrs = (ctypes.c_void_p * ws)(*(peer.ptrs if peer else [ptr] * ws))
         b, c = sharded.slice_of(rank, ws, 1 << nl)
@@ -291,6 +297,23 @@ def run_ours(a):
 
     def step(ev):
         npasses = st["npasses"]
+        if st["narrow"]:
+            # ev[0] start, ev[1] packed + flags agreed, ev[2] = ev[1], ev[3]
+            # exchanged (barrier passed), ev[4] local transforms done
+            def mark(i):
+                ev[(0, 1, 3, 4)[i]].record(stream)
+                if i == 1:
+                    ev[2].record(stream)
+            if not sharded.narrow_step(x, st["nw"], None, dist, p, device_barrier=device_barrier, mark=mark):
+                st["narrow_fallbacks"] += 1  # data too wide for the wire: the int64 fused path
+                _lib.check(L.bw_fwht_i64_partial(ptr, nl, st["f_arr"], len(st["f_widths"]), sh))
+                device_barrier()
+                _lib.check(L.bw_fwht_xfused_pass_i64(ptrs, p, nl, st["f_r"], rank, sh))
+                device_barrier()
+                for i in (1, 2, 3, 4):
+                    ev[i].record(stream)
+            ev[-1].record(stream)
+            return
         if whole:
             ev[0].record(stream)
             _lib.check(L.bw_fwht_i64(ptr, nl, sh, None))
@@ -338,13 +361,18 @@ def run_ours(a):
     def events():
         return [torch.cuda.Event(enable_timing=True) for _ in range(st["nev"])]
 
+    def restore():  # the config input again (outside every step's events)
+        signals.generate(spec, x, base=rank << nl)
+
     trial_ms = {}
     if len(candidates) > 1:  # two timed steps per candidate after one warm-up step, max over ranks
-        for m in candidates:
+        for m in candidates:  # every step on the config input: the narrow wire depends on its magnitude
             configure(m)
+            restore()
             step(events())
             tr = [events() for _ in range(2)]
             for e in tr:
+                restore()
                 step(e)
             torch.cuda.synchronize()
             t = torch.tensor([sum(e[0].elapsed_time(e[-1]) for e in tr) / len(tr)], dtype=torch.float64,
@@ -360,13 +388,18 @@ def run_ours(a):
     npasses = st["npasses"]
     fused = st["fused"]
     a.exchange = st["mode"]  # the e2e leg uses the same exchange
+    a.narrow_wire = st.get("nw")
     if fused:
         f_widths, f_r = st["f_widths"], st["f_r"]
 
+    # Each transform changes the data; the fused extraction (configs 3/5) and
+    # the narrow wire (int8 only while |x| <= 127 >> log2 P) need the config
+    # input at every step, so it is regenerated between steps.
+    restore_each = extract or st["narrow"]
     hits_first = None
     for w in range(a.warmup):
-        if extract:  # each transform doubles the data: restore the input between steps
-            signals.generate(spec, x, base=rank << nl)
+        if restore_each:
+            restore()
         step(events())
         if extract and w == 0:
             k = int(hit_cnt.item())
@@ -382,8 +415,8 @@ def run_ours(a):
     if ws > 1:
         dist.barrier()
     for e in evs:
-        if extract:  # restore the config input (outside the step's events)
-            signals.generate(spec, x, base=rank << nl)
+        if restore_each:  # outside the step's events
+            restore()
         if flush:
             scrub.fill_(1)
         step(e)
@@ -392,7 +425,7 @@ def run_ours(a):
         dist.barrier()
     clk = clocks.stop()
     step_ms = [e[0].elapsed_time(e[-1]) for e in evs]
-    per_step = flush or extract  # something untimed runs between steps
+    per_step = flush or restore_each  # something untimed runs between steps
     total_ms = sum(step_ms) if per_step else evs[0][0].elapsed_time(evs[-1][-1])
     pass_ms = [[e[i].elapsed_time(e[i + 1]) for e in evs] for i in range(npasses)]
     xs_ms = [e[npasses + 1].elapsed_time(e[npasses + 2]) for e in evs] if p > 0 else []
@@ -411,6 +444,10 @@ def run_ours(a):
     if fused:
         launches = a.steps * (len(f_widths) + 1)
         dom_fused = sum(xs_ms) / len(xs_ms)
+    narrow = st["narrow"]
+    if narrow:  # pack, exchange, then the local plan with a widening first pass
+        local_ms = sum(e[3].elapsed_time(e[4]) for e in evs) / len(evs)
+        launches = a.steps * (2 + L.bw_plan_npasses(nl))
     traffic = None  # dram read + write of the dominant pass, from the committed ncu capture
     try:
         with open(os.path.join(ROOT, "profiles", f"r01_traffic_n{nl}.json")) as f:
@@ -445,7 +482,7 @@ def run_ours(a):
                    "l2": ("L2 flushed between steps (256 MiB write, outside the step events)" if flush
                           else f"{(8 << nl) >> 30} GiB input >> 126 MB L2 (no flush needed)"),
                    "timing": ("per-step CUDA events; the input is regenerated between steps (outside the events)"
-                              if extract else "per-step CUDA events" if flush
+                              if restore_each else "per-step CUDA events" if flush
                               else "CUDA events around the K back-to-back steps")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": f"pass {dom} ({plan['passes'][dom]['kind']}, stages "
@@ -479,9 +516,26 @@ def run_ours(a):
                                  "frac_of_8tbs_spec": fb / (dom_fused / 1e3) / 1e9 / 8000.0})
         line.pop("passes_gbs", None)
         line.pop("transform_gbs_per_pass_avg", None)
+    if narrow:
+        plan_local = sharded.plan(nl, 0)
+        nloc = len(plan_local["passes"])
+        # local transform bytes: the first pass reads 1 B and writes 8 B per point, the others 16 B
+        lb = (2 ** nl) * (9 + 16 * (nloc - 1))
+        line["config"]["passes"] = {"exchange": "int8 narrow wire, cross-shard stages first",
+                                    "local_plan": [dict({"kind": q["kind"], "k": q["k"], "r": q["r"],
+                                                         "cluster": q["cluster"]}) for q in plan_local["passes"]],
+                                    "fallbacks_to_int64": st["narrow_fallbacks"]}
+        line["passes_ms"] = {"pack_and_agree": round(avg_pass[0], 4), "exchange": round(sum(xs_ms) / len(xs_ms), 4),
+                             "local_transform": round(local_ms, 4)}
+        line["roofline"].update({"achieved": lb / (local_ms / 1e3) / 1e9, "frac": lb / (local_ms / 1e3) / 1e9 / peak,
+                                 "traffic": None, "algorithmic_bytes_per_launch": lb,
+                                 "kernel": f"local transform ({nloc} passes, the first widening int8)",
+                                 "frac_of_8tbs_spec": lb / (local_ms / 1e3) / 1e9 / 8000.0})
+        line.pop("passes_gbs", None)
+        line.pop("transform_gbs_per_pass_avg", None)
     if p > 0:
         line["xshard_ms"] = sum(xs_ms) / len(xs_ms)
-        nv = 8 * (2 ** nl) * (ws - 1) / ws
+        nv = (1 if narrow else 8) * (2 ** nl) * (ws - 1) / ws
         line["nvlink"] = {"bytes_each_direction": nv, "achieved_gbs": nv / (line["xshard_ms"] / 1e3) / 1e9,
                           "peak_gbs": 770.0, "peak_source": "B200_PROFILING.md measured peer copy"}
     if e2e:
@@ -563,7 +617,7 @@ def run_e2e(a, x, spec, p, nl, rank, ws, peer):
         e0.record(stream)
         for _ in range(steps):
             x.copy_(host, non_blocking=True)
-            sharded.fwht_distributed(x, mode=a.exchange, peer_map=peer)
+            sharded.fwht_distributed(x, mode=a.exchange, peer_map=peer, narrow_wire=a.narrow_wire)
             host.copy_(x, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()

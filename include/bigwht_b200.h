@@ -133,6 +133,14 @@ int bw_fwht_widen_i32(const int32_t *src, int64_t *dst, int log2n, void *stream,
                       uint64_t *butterflies);
 
 /*
+ * Same for any narrow signed source: src_bytes = 4 (int32), 2 (int16) or 1
+ * (int8), src aligned to 2*src_bytes.  The narrow-wire multi-device
+ * transform uses it to widen its packed, already cross-transformed shard.
+ */
+int bw_fwht_widen(const void *src, int src_bytes, int64_t *dst, int log2n, void *stream,
+                  uint64_t *butterflies);
+
+/*
  * float64 fwht_array (core.py:97-117 on a float64 Signal, core.py:56-59):
  * stages applied strictly in ascending order with the same IEEE a+b / a-b
  * as numpy, so results are bitwise identical to the reference (the order
@@ -246,6 +254,26 @@ int bw_xshard_i64(int64_t *const *shards, int log2p, uint64_t begin,
  */
 int bw_xshard_strided_i64(int64_t *base, uint64_t shard_stride, int log2p,
                           uint64_t begin, uint64_t count, void *stream);
+
+/*
+ * Narrow-wire cross-shard stage (parallel.py:103-110 stage phases run
+ * FIRST; int64 stages on distinct bits commute, so the result is still
+ * bit-identical).  If every |x| <= floor(WMAX / 2^log2p) (WMAX = 127 for a
+ * 1-byte wire, 32767 for 2 bytes), no value of the P-point butterfly leaves
+ * the wire type, so the exchange can move wire_bytes per point over NVLink
+ * instead of 8:
+ *   bw_pack_narrow_i64: shard -> packed copy; *flag_dev |= 1 if some |x| is
+ *     too large (then use the int64 path; the shard is untouched).
+ *     count % 8 == 0, 16-byte aligned buffers.  Asynchronous.
+ *   bw_xshard_narrow: the P-point butterfly over elements [begin,
+ *     begin+count) of the P packed shards (peer pointers), in place;
+ *     begin, count multiples of 16 / wire_bytes.  Asynchronous.
+ * then bw_fwht_widen(packed, wire_bytes, shard, n_local) on every device.
+ */
+int bw_pack_narrow_i64(const int64_t *src, uint64_t count, int wire_bytes, int log2p,
+                       void *out, uint32_t *flag_dev, void *stream);
+int bw_xshard_narrow(void *const *packed, int wire_bytes, int log2p, uint64_t begin,
+                     uint64_t count, void *stream);
 
 /*
  * Cross-shard stage FUSED into the last local pass (kernel K6'): the

@@ -578,9 +578,14 @@ int set_all_pass_attributes() {
         } else if (smem > 48 * 1024) {
             BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            if constexpr (L >= C::T)
-                BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            if constexpr (L >= C::T) {  // widening low passes (int32 / int16 / int8 sources)
+                BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              smem));
+                BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem));
+                BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem));
+            }
         }
         return BW_OK;
     });
@@ -620,11 +625,15 @@ bw::SplitTab split_table(int karg) {
     return t;
 }
 
+// src != nullptr: the (low) pass reads a narrow source of src_bytes-byte
+// integers and writes the int64 result to d (widening first pass).
 int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractArgs* exp = nullptr,
-                const int* src32 = nullptr) {
+                const void* src = nullptr, int src_bytes = 0) {
     bw::ExtractArgs ex = {};
     if (exp) ex = *exp;
-    if (src32 && p.kind != LOW) return fail(BW_BAD_ARGUMENTS, "only the low pass widens int32 input");
+    if (src && p.kind != LOW) return fail(BW_BAD_ARGUMENTS, "only the low pass widens a narrow input");
+    if (src && src_bytes != 1 && src_bytes != 2 && src_bytes != 4)
+        return fail(BW_BAD_ARGUMENTS, "narrow sources are 1, 2 or 4 bytes per point (got %d)", src_bytes);
     if (p.kind == SMALL) {
         bw::k_small<u64><<<1, 256, (size_t)(8ull << n), s>>>(d, n);
         BW_LAUNCHED("k_small launch");
@@ -635,14 +644,16 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractA
         constexpr int L = decltype(l)::value;
         const unsigned grid = (unsigned)(1ull << (n - bw::kCtaBits));
         constexpr bool kLow = L >= C::T;
-        const int* none = nullptr;
+        const void* none = nullptr;
         if constexpr (bw::SplitOf<C>::value) {
             const bw::SplitTab tab = split_table<C, L>(p.karg());
             if (ex.count) return launch_cfg<C>(bw::k_pass_split<C, L, true>, grid, s, d, p.karg(), ex, tab);
             return launch_cfg<C>(bw::k_pass_split<C, L, false>, grid, s, d, p.karg(), ex, tab);
         } else {
         if constexpr (kLow) {
-            if (src32) return launch_cfg<C>(bw::k_pass<C, L, false, true>, grid, s, d, p.k, ex, src32);
+            if (src && src_bytes == 4) return launch_cfg<C>(bw::k_pass<C, L, false, 4>, grid, s, d, p.k, ex, src);
+            if (src && src_bytes == 2) return launch_cfg<C>(bw::k_pass<C, L, false, 2>, grid, s, d, p.k, ex, src);
+            if (src) return launch_cfg<C>(bw::k_pass<C, L, false, 1>, grid, s, d, p.k, ex, src);
         }
         if (ex.count) return launch_cfg<C>(bw::k_pass<C, L, true>, grid, s, d, p.k, ex, none);
         return launch_cfg<C>(bw::k_pass<C, L, false>, grid, s, d, p.k, ex, none);
@@ -715,7 +726,7 @@ int run_scalar_plan(u64* d, int log2n, cudaStream_t s) {
             using C = typename decltype(t)::type;
             constexpr int L = decltype(l)::value;
             const unsigned grid = (unsigned)(1ull << (log2n - bw::kCtaBits));
-            const int* none = nullptr;
+            const void* none = nullptr;
             return launch_cfg<C>(bw::k_pass<C, L, false, false, FP>, grid, s, d, p.k, bw::ExtractArgs{}, none);
         }));
     }
@@ -924,12 +935,16 @@ int bw_fwht_i64_planned(int64_t* data, int log2n, const int* pass_bits, int npas
     return fwht_impl(data, log2n, &w, false, as_stream(stream));
 }
 
-// int32 input, int64 output (out of place): the first pass reads the int32
-// source (4 B/point) and writes int64, the rest run in place on dst -- the
-// reference's fwht_array on x.astype(int64), with overflow-free int64 sums.
-int bw_fwht_widen_i32(const int32_t* src, int64_t* dst, int log2n, void* stream, uint64_t* butterflies) {
+// Narrow integer input, int64 output (out of place): the first pass reads
+// the src_bytes-byte source (4 / 2 / 1 B per point) and writes int64, the
+// rest run in place on dst -- the reference's fwht_array on
+// x.astype(int64), with overflow-free int64 sums.
+int bw_fwht_widen(const void* src, int src_bytes, int64_t* dst, int log2n, void* stream, uint64_t* butterflies) {
     BW_TRY(check_signal(dst, log2n));
-    if (!src || (reinterpret_cast<uintptr_t>(src) & 7u)) return fail(BW_BAD_ARGUMENTS, "int32 source must be 8-byte aligned");
+    if (src_bytes != 1 && src_bytes != 2 && src_bytes != 4)
+        return fail(BW_BAD_ARGUMENTS, "narrow sources are 1, 2 or 4 bytes per point (got %d)", src_bytes);
+    if (!src || (reinterpret_cast<uintptr_t>(src) & (2u * src_bytes - 1u)))
+        return fail(BW_BAD_ARGUMENTS, "narrow source must be %d-byte aligned", 2 * src_bytes);
     if (reinterpret_cast<uintptr_t>(dst) & 15u) return fail(BW_BAD_ARGUMENTS, "int64 destination must be 16-byte aligned");
     int dev = 0;
     BW_TRY(device_setup(&dev));
@@ -941,15 +956,23 @@ int bw_fwht_widen_i32(const int32_t* src, int64_t* dst, int log2n, void* stream,
     BW_TRY(build_passes(log2n, w, &passes));
     if (passes.empty() || passes[0].kind != LOW) {  // tiny signals: widen, then transform
         const uint64_t count = 1ull << log2n;
-        bw::k_widen_i32<<<grid_for(dev, count, 256, 4), 256, 0, s>>>(src, reinterpret_cast<long long*>(dst), count);
-        BW_LAUNCHED("k_widen_i32 launch");
+        const int grid = grid_for(dev, count, 256, 4);
+        long long* dl = reinterpret_cast<long long*>(dst);
+        if (src_bytes == 4) bw::k_widen<int><<<grid, 256, 0, s>>>(reinterpret_cast<const int*>(src), dl, count);
+        else if (src_bytes == 2) bw::k_widen<short><<<grid, 256, 0, s>>>(reinterpret_cast<const short*>(src), dl, count);
+        else bw::k_widen<signed char><<<grid, 256, 0, s>>>(reinterpret_cast<const signed char*>(src), dl, count);
+        BW_LAUNCHED("k_widen launch");
         BW_TRY(fwht_impl(dst, log2n, nullptr, false, s));
     } else {
-        BW_TRY(launch_pass(passes[0], d, log2n, s, nullptr, src));
+        BW_TRY(launch_pass(passes[0], d, log2n, s, nullptr, src, src_bytes));
         for (size_t i = 1; i < passes.size(); ++i) BW_TRY(launch_pass(passes[i], d, log2n, s));
     }
     if (butterflies) *butterflies = butterfly_count(log2n);
     return BW_OK;
+}
+
+int bw_fwht_widen_i32(const int32_t* src, int64_t* dst, int log2n, void* stream, uint64_t* butterflies) {
+    return bw_fwht_widen(src, 4, dst, log2n, stream, butterflies);
 }
 
 // fwht_array on a float64 buffer (core.py:97-117): stages strictly ascending
@@ -1497,6 +1520,70 @@ int bw_xshard_strided_i64(int64_t* base, uint64_t shard_stride, int log2p, uint6
     int64_t* ptrs[8];
     for (int r = 0; r < (1 << log2p); ++r) ptrs[r] = base + r * shard_stride;
     return bw_xshard_i64(ptrs, log2p, begin, count, stream);
+}
+
+// ---- narrow-wire cross-shard stage (cross stages first, W-byte exchange) ----
+
+// Pack a shard to wire_bytes-byte integers; *flag_dev |= 1 when some |x| >
+// floor(WMAX / 2^log2p), i.e. when the narrow exchange could leave the
+// wire type (the caller then runs the int64 path; the shard is unchanged).
+int bw_pack_narrow_i64(const int64_t* src, uint64_t count, int wire_bytes, int log2p, void* out, uint32_t* flag_dev,
+                       void* stream) {
+    if (!src || !out || !flag_dev) return fail(BW_BAD_ARGUMENTS, "null pointer");
+    if (wire_bytes != 1 && wire_bytes != 2) return fail(BW_BAD_ARGUMENTS, "wire is 1 or 2 bytes (got %d)", wire_bytes);
+    if (log2p < 0 || log2p > BW_MAX_LOG2P)
+        return fail(BW_INVALID_WORKERS, "log2p = %d outside 0..%d", log2p, BW_MAX_LOG2P);
+    if (count % 8) return fail(BW_BAD_ARGUMENTS, "count must be a multiple of 8");
+    if ((reinterpret_cast<uintptr_t>(src) & 15u) || (reinterpret_cast<uintptr_t>(out) & 15u))
+        return fail(BW_BAD_ARGUMENTS, "source and packed buffer must be 16-byte aligned");
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    cudaStream_t s = as_stream(stream);
+    if (count == 0) return BW_OK;
+    const int grid = grid_for(dev, count / 8, 256, 8);
+    const long long* x = reinterpret_cast<const long long*>(src);
+    unsigned* f = reinterpret_cast<unsigned*>(flag_dev);
+    if (wire_bytes == 1)
+        bw::k_pack_narrow<signed char><<<grid, 256, 0, s>>>(x, reinterpret_cast<signed char*>(out), count,
+                                                            127ll >> log2p, f);
+    else
+        bw::k_pack_narrow<short><<<grid, 256, 0, s>>>(x, reinterpret_cast<short*>(out), count, 32767ll >> log2p, f);
+    BW_LAUNCHED("k_pack_narrow launch");
+    return BW_OK;
+}
+
+// The P-point cross-shard butterfly over elements [begin, begin + count) of
+// the packed shards (peer pointers); begin and count multiples of 16 / wire.
+int bw_xshard_narrow(void* const* packed, int wire_bytes, int log2p, uint64_t begin, uint64_t count, void* stream) {
+    if (!packed) return fail(BW_BAD_ARGUMENTS, "null shard list");
+    if (wire_bytes != 1 && wire_bytes != 2) return fail(BW_BAD_ARGUMENTS, "wire is 1 or 2 bytes (got %d)", wire_bytes);
+    if (log2p < 0 || log2p > BW_MAX_LOG2P)
+        return fail(BW_INVALID_WORKERS, "log2p = %d outside 0..%d", log2p, BW_MAX_LOG2P);
+    const uint64_t per = 16 / (uint64_t)wire_bytes;
+    if ((begin | count) % per) return fail(BW_BAD_ARGUMENTS, "begin and count must be multiples of %llu", (unsigned long long)per);
+    bw::NarrowPtrs sp;
+    memset(&sp, 0, sizeof sp);
+    for (int r = 0; r < (1 << log2p); ++r) {
+        if (!packed[r] || (reinterpret_cast<uintptr_t>(packed[r]) & 15u))
+            return fail(BW_BAD_ARGUMENTS, "packed shard %d is null or not 16-byte aligned", r);
+        sp.p[r] = packed[r];
+    }
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    cudaStream_t s = as_stream(stream);
+    if (count == 0 || log2p == 0) return BW_OK;
+    const int grid = grid_for(dev, count / per, 256, 8);
+    auto go = [&](auto w) -> int {
+        using W = decltype(w);
+        switch (log2p) {
+            case 1: bw::k_xshard_narrow<W, 1><<<grid, 256, 0, s>>>(sp, begin, count); break;
+            case 2: bw::k_xshard_narrow<W, 2><<<grid, 256, 0, s>>>(sp, begin, count); break;
+            default: bw::k_xshard_narrow<W, 3><<<grid, 256, 0, s>>>(sp, begin, count); break;
+        }
+        BW_LAUNCHED("k_xshard_narrow launch");
+        return BW_OK;
+    };
+    return wire_bytes == 1 ? go((signed char)0) : go((short)0);
 }
 
 // ---- peer memory plumbing for the one-process-per-GPU cross-shard stage ----

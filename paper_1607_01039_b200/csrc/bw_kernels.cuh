@@ -113,21 +113,42 @@ __device__ __forceinline__ void load_global(u64 (&v)[Dims<C>::E], const u64* __r
     }
 }
 
-// Widening load (int32 source, int64 registers) for the out-of-place first
-// pass of bw_fwht_widen_i32: same addressing, 4-byte elements.
-template <class C, int RD, int T, int L>
-__device__ __forceinline__ void load_global_i32(u64 (&v)[Dims<C>::E], const int* __restrict__ g, uint32_t tp,
-                                               int k) {
+// Widening load (int32 / int16 / int8 source, int64 registers) for the
+// out-of-place first pass of bw_fwht_widen_i32 and of the narrow-wire
+// multi-device transform: same addressing, SB-byte elements.
+template <int SB>
+struct NarrowType;
+template <>
+struct NarrowType<4> {
+    typedef int one;
+    typedef int2 pair;
+};
+template <>
+struct NarrowType<2> {
+    typedef short one;
+    typedef short2 pair;
+};
+template <>
+struct NarrowType<1> {
+    typedef signed char one;
+    typedef char2 pair;
+};
+
+template <class C, int RD, int T, int L, int SB>
+__device__ __forceinline__ void load_global_narrow(u64 (&v)[Dims<C>::E], const void* __restrict__ src, uint32_t tp,
+                                                   int k) {
+    typedef typename NarrowType<SB>::one S1;
+    typedef typename NarrowType<SB>::pair S2;
     constexpr int E = Dims<C>::E;
-    const int* p = g + global_off<T, L, SplitOf<C>::value>(tp, k);
+    const S1* p = reinterpret_cast<const S1*>(src) + global_off<T, L, SplitOf<C>::value>(tp, k);
 #pragma unroll
     for (int j = 0; j < E; ++j) {
         const uint64_t off = global_off<T, L, SplitOf<C>::value>(reg_part<C, RD>(j), k);
         if constexpr (VecAccess<C, RD, L>::value) {
             if ((j & 1) == 0) {
-                const int2 t = __ldcs(reinterpret_cast<const int2*>(p + off));
-                v[j] = (u64)(long long)t.x;
-                v[j + 1] = (u64)(long long)t.y;
+                const S2 t = __ldcs(reinterpret_cast<const S2*>(p + off));
+                v[j] = (u64)(long long)(S1)t.x;
+                v[j + 1] = (u64)(long long)(S1)t.y;
             }
         } else {
             v[j] = (u64)(long long)__ldcs(p + off);
@@ -432,10 +453,11 @@ __device__ __forceinline__ void extract_hits(const u64 (&v)[Dims<C>::E], const u
 // One pass over every tile: load (round 0 layout) -> stages -> [transpose ->
 // stages]* -> store (last round layout).  k = first global stage bit of the
 // rows (ignored for L == T).  Cluster configs (Q > 0) put 2^Q CTAs on one
-// tile; grid = 2^(n-13) CTAs for every config.
-template <class C, int L, bool EX = false, bool SRC32 = false, bool FP = false>
+// tile; grid = 2^(n-13) CTAs for every config.  SB > 0: the loads read a
+// narrow SB-byte source `src` (widening first pass), the stores go to data.
+template <class C, int L, bool EX = false, int SB = 0, bool FP = false>
 __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
-    k_pass(u64* __restrict__ data, int k, ExtractArgs ex, const int* __restrict__ src32) {
+    k_pass(u64* __restrict__ data, int k, ExtractArgs ex, const void* __restrict__ src) {
     static_assert(!SplitOf<C>::value, "split-row configs launch k_pass_split");
     constexpr int T = C::T;
     constexpr int E = Dims<C>::E;
@@ -463,8 +485,9 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
         __syncthreads();
     }
     u64 v[E];
-    if constexpr (SRC32)
-        load_global_i32<C, 0, T, L>(v, src32 + tile_base<T, L>(tile, k), thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
+    if constexpr (SB > 0)
+        load_global_narrow<C, 0, T, L, SB>(v, reinterpret_cast<const typename NarrowType<SB>::one*>(src) + tile_base<T, L>(tile, k),
+                                           thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
     else
         load_global<C, 0, T, L>(v, g, thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
     if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
@@ -587,7 +610,8 @@ __global__ void __launch_bounds__(1024) k_sort_hits(long long* idx, long long* v
 }
 
 // ---------------------------------------------------------------------------
-__global__ void k_widen_i32(const int* __restrict__ src, long long* __restrict__ dst, uint64_t count) {
+template <typename S>
+__global__ void k_widen(const S* __restrict__ src, long long* __restrict__ dst, uint64_t count) {
     const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += nth) dst[i] = src[i];
 }
@@ -739,6 +763,98 @@ __global__ void __launch_bounds__(256) k_xshard(ShardPtrs s, uint64_t begin, uin
         }
 #pragma unroll
         for (int r = 0; r < P; ++r) __stcs(reinterpret_cast<ulonglong2*>(s.p[r] + i), v[r]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Narrow-wire cross-shard stage: the log2 P cross stages run FIRST, on the
+// untransformed input (stages on distinct bits commute in Z/2^64).  When
+// every |x| <= lim = floor(WMAX / P) (WMAX = 127 for int8, 32767 for int16),
+// every intermediate of the P-point butterfly satisfies |y| <= P * lim <=
+// WMAX, so the shards are packed to W-byte integers, the exchange moves W
+// bytes per point over NVLink instead of 8, and each device's local
+// transform widens its packed shard in the first pass (bw_fwht_widen).
+// ---------------------------------------------------------------------------
+template <typename W>
+struct WireWord;
+template <>
+struct WireWord<signed char> {  // 4 int8 lanes per 32-bit word
+    static __device__ __forceinline__ unsigned add(unsigned a, unsigned b) { return __vadd4(a, b); }
+    static __device__ __forceinline__ unsigned sub(unsigned a, unsigned b) { return __vsub4(a, b); }
+};
+template <>
+struct WireWord<short> {  // 2 int16 lanes per 32-bit word
+    static __device__ __forceinline__ unsigned add(unsigned a, unsigned b) { return __vadd2(a, b); }
+    static __device__ __forceinline__ unsigned sub(unsigned a, unsigned b) { return __vsub2(a, b); }
+};
+
+// int64 -> W, 8 points per thread (64-byte read, 8W-byte write); *flag |= 1
+// if some |x| > lim (the caller then takes the int64 path; x is unchanged).
+template <typename W>
+__global__ void __launch_bounds__(256) k_pack_narrow(const long long* __restrict__ x, W* __restrict__ out,
+                                                     uint64_t count, long long lim, unsigned* flag) {
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    bool bad = false;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < count / 8; q += nth) {
+        const longlong2* src = reinterpret_cast<const longlong2*>(x + 8 * q);
+        W w[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const longlong2 a = __ldcs(src + i);
+            bad |= (a.x > lim) | (a.x < -lim) | (a.y > lim) | (a.y < -lim);
+            w[2 * i] = (W)a.x;
+            w[2 * i + 1] = (W)a.y;
+        }
+        if constexpr (sizeof(W) == 1) {
+            uint2 o;
+            o.x = (unsigned)(unsigned char)w[0] | (unsigned)(unsigned char)w[1] << 8 |
+                  (unsigned)(unsigned char)w[2] << 16 | (unsigned)(unsigned char)w[3] << 24;
+            o.y = (unsigned)(unsigned char)w[4] | (unsigned)(unsigned char)w[5] << 8 |
+                  (unsigned)(unsigned char)w[6] << 16 | (unsigned)(unsigned char)w[7] << 24;
+            *reinterpret_cast<uint2*>(out + 8 * q) = o;
+        } else {
+            uint4 o;
+            o.x = (unsigned)(unsigned short)w[0] | (unsigned)(unsigned short)w[1] << 16;
+            o.y = (unsigned)(unsigned short)w[2] | (unsigned)(unsigned short)w[3] << 16;
+            o.z = (unsigned)(unsigned short)w[4] | (unsigned)(unsigned short)w[5] << 16;
+            o.w = (unsigned)(unsigned short)w[6] | (unsigned)(unsigned short)w[7] << 16;
+            *reinterpret_cast<uint4*>(out + 8 * q) = o;
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31u) == 0) atomicOr(flag, 1u);
+}
+
+struct NarrowPtrs {
+    void* p[8];
+};
+
+// The P-point butterfly over elements [begin, begin + count) of the P packed
+// shards (peer pointers), 16 bytes of every shard per thread, packed SIMD
+// add/sub on the W-bit lanes (exact: no lane leaves the W range).
+template <typename W, int LOGP>
+__global__ void __launch_bounds__(256) k_xshard_narrow(NarrowPtrs s, uint64_t begin, uint64_t count) {
+    constexpr int P = 1 << LOGP, PER = 16 / sizeof(W);
+    typedef WireWord<W> WW;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < count / PER; q += nth) {
+        const uint64_t e = begin + q * PER;
+        uint4 v[P];
+#pragma unroll
+        for (int r = 0; r < P; ++r) v[r] = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<W*>(s.p[r]) + e));
+#pragma unroll
+        for (int b = 0; b < LOGP; ++b) {
+#pragma unroll
+            for (int r = 0; r < P; ++r) {
+                if (!((r >> b) & 1)) {
+                    const uint4 a = v[r], c = v[r | (1 << b)];
+                    v[r] = make_uint4(WW::add(a.x, c.x), WW::add(a.y, c.y), WW::add(a.z, c.z), WW::add(a.w, c.w));
+                    v[r | (1 << b)] =
+                        make_uint4(WW::sub(a.x, c.x), WW::sub(a.y, c.y), WW::sub(a.z, c.z), WW::sub(a.w, c.w));
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < P; ++r) __stcs(reinterpret_cast<uint4*>(reinterpret_cast<W*>(s.p[r]) + e), v[r]);
     }
 }
 

@@ -18,6 +18,16 @@ NVLink, applies the last local stages and the log2 P cross stages, and
 stores back -- one HBM round trip fewer than local passes + a separate
 exchange.  ``fused=True`` / ``mode="fused"`` select it.
 
+NARROW WIRE (``mode="narrow"``): the log2 P cross-shard stages run FIRST,
+on the untransformed input (int64 stages on distinct bits commute, so the
+result is still bit-identical).  When every |x| <= floor(127 / P) (a +-1
+Boolean signal, the paper's use case), no intermediate of the P-point
+butterfly leaves int8, so each shard is packed to one byte per point, the
+exchange moves 1 byte per point over NVLink instead of 8, and every device
+then transforms its shard locally, the first pass widening the packed
+bytes (bw_fwht_widen).  Larger inputs fall back to the fused int64 path
+(the pack kernel flags them; the shards are untouched).
+
 Three drivers share these kernels:
   * ``fwht_shards``      -- one process, shards on one or several devices
                             (single-GPU P-shard emulation, or P2P over NVLink).
@@ -26,7 +36,8 @@ Three drivers share these kernels:
       mode="peer": CUDA IPC peer pointers, the K6 kernel reads and writes the
                    peers' HBM directly over NVLink (fused compute+exchange);
       mode="a2a":  all-to-all transpose + local K6 on the receive slots +
-                   all-to-all back (NCCL on GPUs; gloo on CPU for tests).
+                   all-to-all back (NCCL on GPUs; gloo on CPU for tests);
+      mode="narrow": the int8 exchange first, then the local transforms.
 """
 
 from __future__ import annotations
@@ -102,6 +113,34 @@ def _local_partial(t: torch.Tensor, n_local: int, widths: list[int]) -> None:
         _lib.check(_lib.lib().bw_fwht_i64_partial(t.data_ptr(), n_local, arr, len(widths), _stream_handle(t)))
 
 
+WIRE_BYTES = 1  # narrow wire: int8 (|x| <= 127 >> log2 P)
+
+
+def narrow_ok(local_len: int, p: int) -> bool:
+    """The narrow exchange needs 16-point-aligned slices of every shard."""
+    return p > 0 and local_len % (16 << p) == 0
+
+
+def _pack(t: torch.Tensor, packed: torch.Tensor, flag: torch.Tensor, p: int) -> None:
+    with torch.cuda.device(t.device):
+        _lib.check(_lib.lib().bw_pack_narrow_i64(t.data_ptr(), t.numel(), WIRE_BYTES, p, packed.data_ptr(),
+                                                 flag.data_ptr(), _stream_handle(t)))
+
+
+def _xshard_narrow(ptrs: list[int], p: int, begin: int, count: int, dev: torch.device) -> None:
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().bw_xshard_narrow(arr, WIRE_BYTES, p, begin, count,
+                                               torch.cuda.current_stream(dev).cuda_stream))
+
+
+def _widen(packed: torch.Tensor, t: torch.Tensor) -> None:
+    n_local = t.numel().bit_length() - 1
+    with torch.cuda.device(t.device):
+        _lib.check(_lib.lib().bw_fwht_widen(packed.data_ptr(), WIRE_BYTES, t.data_ptr(), n_local,
+                                            _stream_handle(t), None))
+
+
 def _fused_pass(ptrs: list[int], p: int, n_local: int, r: int, rank: int, dev: torch.device) -> None:
     arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
     with torch.cuda.device(dev):
@@ -123,10 +162,12 @@ def xshard(shards: list[torch.Tensor], begin: int = 0, count: int | None = None)
                                         torch.cuda.current_stream(dev).cuda_stream))
 
 
-def fwht_shards(shards: list[torch.Tensor], fused: bool = False) -> int:
+def fwht_shards(shards: list[torch.Tensor], fused: bool = False, narrow: bool = False) -> int:
     """Transform the 2**n signal whose P = len(shards) contiguous shards are
     given (shard r = indices r*2**(n-p) ...), in place.  Shards may live on
     one device (emulation of P GPUs) or on P devices (P2P over NVLink).
+    fused: K6' (last local pass + cross stages); narrow: the narrow-wire
+    exchange first (falls back to fused when an input is too large).
     Returns n * 2**(n-1)."""
     p = log2_shards(len(shards))
     local = shards[0].numel()
@@ -135,6 +176,30 @@ def fwht_shards(shards: list[torch.Tensor], fused: bool = False) -> int:
             raise BadArguments("shards must be equal-length contiguous CUDA int64 tensors")
     n_local = local.bit_length() - 1
     devices = sorted({s.device.index for s in shards})
+    if narrow and narrow_ok(local, p):
+        packed = [torch.empty(local, dtype=torch.int8, device=s.device) for s in shards]
+        flags = [torch.zeros(1, dtype=torch.int32, device=s.device) for s in shards]
+        for s, pk, f in zip(shards, packed, flags):
+            _pack(s, pk, f, p)
+        if any(int(f.item()) for f in flags):  # (synchronises every device: barrier (i))
+            return fwht_shards(shards, fused=True)
+        if len(devices) > 1:
+            for d in devices:
+                with torch.cuda.device(d):
+                    for q in devices:
+                        _lib.check(_lib.lib().bw_enable_peer_access(q))
+        ptrs = [pk.data_ptr() for pk in packed]
+        m = local >> p
+        for g, s in enumerate(shards):  # device g exchanges slice g of every packed shard
+            _xshard_narrow(ptrs, p, g * m, m, s.device)
+        for d in devices:  # barrier (ii)
+            torch.cuda.synchronize(d)
+        for s, pk in zip(shards, packed):
+            _widen(pk, s)
+        for d in devices:
+            torch.cuda.synchronize(d)
+        n = n_local + p
+        return n << (n - 1)
     if fused and p > 0 and n_local >= 14:
         widths, r = fused_plan(n_local, p)
         for s in shards:  # local passes over the low n_local - r bits
@@ -224,19 +289,74 @@ class _PeerMap:
         self.opened = []
 
 
+class NarrowWire:
+    """Reusable state of the narrow-wire exchange on one rank: the packed
+    shard, the overflow flag and the IPC map of every rank's packed shard."""
+
+    def __init__(self, local: torch.Tensor, group, dist):
+        self.packed = torch.empty(local.numel() * WIRE_BYTES, dtype=torch.int8, device=local.device)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=local.device)
+        self.peers = _PeerMap(self.packed, group, dist)
+
+    def close(self):
+        self.peers.close()
+
+
+def narrow_step(local: torch.Tensor, nw: NarrowWire, group, dist, p: int, device_barrier=None, mark=None) -> bool:
+    """The narrow-wire transform of this rank's shard (every rank calls it).
+    Returns False, with the shard untouched, when some input is too large for
+    the wire (the caller then runs the int64 path).  mark(i), if given, is
+    called at the phase boundaries (0: start, 1: packed and agreed, 2:
+    exchanged, 3: transformed) -- the benchmark records CUDA events there."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    mark = mark or (lambda i: None)
+    mark(0)
+    nw.flag.zero_()
+    _pack(local, nw.packed, nw.flag, p)
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(nw.flag, op=dist.ReduceOp.MAX, group=group)  # also barrier (i): every pack is done
+        bad = int(nw.flag.item())
+    else:
+        f = nw.flag.cpu()
+        dist.all_reduce(f, op=dist.ReduceOp.MAX, group=group)
+        bad = int(f.item())
+    if bad:
+        return False
+    mark(1)
+    m = local.numel() // world
+    _xshard_narrow(nw.peers.ptrs, p, rank * m, m, local.device)
+    if device_barrier is not None:
+        device_barrier()
+    else:
+        torch.cuda.synchronize(local.device)
+        dist.barrier(group)  # (ii) every slice exchanged before anyone widens
+    mark(2)
+    _widen(nw.packed, local)
+    mark(3)
+    return True
+
+
+last_exchange = None  # the exchange the last fwht_distributed call actually ran (diagnostics)
+
+
 def fwht_distributed(local: torch.Tensor, group=None, mode: str = "fused", backend=None,
-                     peer_map: _PeerMap | None = None) -> int:
+                     peer_map: _PeerMap | None = None, narrow_wire: NarrowWire | None = None) -> int:
     """Rank r holds shard r (indices r*2**(n-p) ... of a 2**n signal).
     Transforms the whole signal in place across the group; returns
     n * 2**(n-1).  Must be called by every rank of ``group``.
 
     mode="fused" (default): local passes over the low bits, then K6' (the
     last local pass and the cross-shard stages in one kernel over peer
-    pointers); shards under 2**14 points use mode="peer".  mode="peer": full
+    pointers); shards under 2**14 points use mode="peer".  mode="narrow":
+    the int8 exchange first, then the local transforms (module docstring);
+    falls back to "fused" for inputs above 127 >> log2 P.  mode="peer": full
     local transform, then K6 over peer pointers.  mode="a2a": full local
     transform, then all-to-all + K6 on the received slots + all-to-all."""
     import torch.distributed as dist
 
+    global last_exchange
+    last_exchange = None
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     p = log2_shards(world)
@@ -244,6 +364,17 @@ def fwht_distributed(local: torch.Tensor, group=None, mode: str = "fused", backe
     local_len = local.numel()
     n_local = local_len.bit_length() - 1
     n = n_local + p
+    if mode == "narrow":
+        if p > 0 and local.is_cuda and narrow_ok(local_len, p):
+            nw = narrow_wire or NarrowWire(local, group, dist)
+            done = narrow_step(local, nw, group, dist, p)
+            if narrow_wire is None:  # barrier (ii) passed: no peer touches our packed shard any more
+                torch.cuda.synchronize(local.device)
+                nw.close()
+            if done:
+                last_exchange = "narrow"
+                return n << (n - 1)
+        mode = "fused"
     if mode == "fused" and p > 0 and n_local >= 14:
         if not local.is_cuda:
             raise BadArguments("mode='fused' needs CUDA shards")
@@ -257,6 +388,7 @@ def fwht_distributed(local: torch.Tensor, group=None, mode: str = "fused", backe
         dist.barrier(group)  # (ii) every fused pass is done
         if peer_map is None:
             pm.close()
+        last_exchange = "fused"
         return n << (n - 1)
     if mode == "fused":
         mode = "peer"
@@ -277,6 +409,7 @@ def fwht_distributed(local: torch.Tensor, group=None, mode: str = "fused", backe
         dist.barrier(group)  # (ii) every exchange is done before anyone reads
         if peer_map is None:
             pm.close()
+        last_exchange = "peer"
         return n << (n - 1)
     if mode == "a2a":
         if local_len % world:
@@ -286,5 +419,6 @@ def fwht_distributed(local: torch.Tensor, group=None, mode: str = "fused", backe
         dist.all_to_all_single(recv, local, group=group)  # slot r = shard r's slice `rank`
         backend.xshard_slots(recv.view(world, m), p)
         dist.all_to_all_single(local, recv, group=group)
+        last_exchange = "a2a"
         return n << (n - 1)
     raise BadArguments(f"unknown mode {mode!r}")

@@ -126,6 +126,25 @@ def test_split_plans_rejected():
             sharded.plan_check(n, plan)
 
 
+def test_narrow_wire_arguments_validated_before_launch():
+    L = _lib.lib()
+    buf = np.zeros(64, dtype=np.int64)
+    flag = np.zeros(1, dtype=np.int32)
+    ptr = (buf.ctypes.data + 15) & ~15
+    for args in [(ptr, 64, 3, 1, ptr, flag.ctypes.data, None),   # wire of 3 bytes
+                 (ptr, 60, 1, 1, ptr, flag.ctypes.data, None),   # count not a multiple of 8
+                 (ptr + 8, 56, 1, 1, ptr, flag.ctypes.data, None),  # misaligned source
+                 (ptr, 56, 1, 4, ptr, flag.ctypes.data, None)]:  # 16 shards
+        with pytest.raises((errors.BadArguments, errors.InvalidWorkerCount)):
+            _lib.check(L.bw_pack_narrow_i64(*args))
+    arr = (ctypes.c_void_p * 2)(ptr, ptr)
+    with pytest.raises(errors.BadArguments):
+        _lib.check(L.bw_xshard_narrow(arr, 1, 1, 8, 16, None))  # begin not a multiple of 16
+    with pytest.raises(errors.BadArguments):
+        _lib.check(L.bw_fwht_widen(ptr, 3, ptr, 4, None, None))
+    assert sharded.narrow_ok(1 << 10, 3) and not sharded.narrow_ok(64, 3) and not sharded.narrow_ok(1 << 10, 0)
+
+
 def test_plan_describe():
     p = sharded.plan(32, 0)
     assert [x["kind"] for x in p["passes"]] == ["low", "high", "high"]

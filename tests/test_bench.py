@@ -53,3 +53,19 @@ def test_multirank_path_two_processes_one_gpu():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["log2p"] == 1 and "nvlink" in d and d["value"] > 0
+
+
+@pytest.mark.gpu
+def test_multirank_narrow_wire_two_processes_one_gpu():
+    """bench --mode narrow: the int8 cross-first exchange, timed by phase,
+    with no fallback on config 4's +-1 signal."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29518", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--log2n", "24", "--dist-backend", "gloo", "--no-cpu",
+           "--mode", "narrow"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["config"]["exchange"] == "narrow" and d["config"]["passes"]["fallbacks_to_int64"] == 0
+    assert set(d["passes_ms"]) == {"pack_and_agree", "exchange", "local_transform"}
+    assert d["nvlink"]["bytes_each_direction"] == (1 << 23) / 2

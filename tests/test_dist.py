@@ -89,7 +89,7 @@ def test_a2a_orchestration_gloo(tmp_path, coracle, world):
     assert np.array_equal(got, ref)
 
 
-def _peer_worker(rank, world, port, n, out_dir, mode="peer"):
+def _peer_worker(rank, world, port, n, out_dir, mode="peer", kind=2):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -100,10 +100,12 @@ def _peer_worker(rank, world, port, n, out_dir, mode="peer"):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     p = world.bit_length() - 1
     nl = n - p
-    x = oracle_np.gen(2, 7, [1 << 20], rank << nl, 1 << nl)
+    x = oracle_np.gen(kind, 7, [1 << 20] if kind == 2 else [], rank << nl, 1 << nl)
     t = torch.from_numpy(x).cuda()
     bf = sharded.fwht_distributed(t, mode=mode)
     assert bf == n << (n - 1)
+    with open(os.path.join(out_dir, f"mode{rank}.txt"), "w") as f:
+        f.write(str(sharded.last_exchange))
     np.save(os.path.join(out_dir, f"shard{rank}.npy"), t.cpu().numpy())
     dist.barrier()
     dist.destroy_process_group()
@@ -120,3 +122,20 @@ def test_peer_ipc_two_processes_one_gpu(tmp_path, coracle, mode):
     ref = oracle_np.gen(2, 7, [1 << 20], 0, 1 << n)
     coracle.oracle_fwht_i64(ref.ctypes.data, n)
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,expect", [(1, "narrow"), (2, "fused")])
+def test_narrow_wire_two_processes_one_gpu(tmp_path, coracle, kind, expect):
+    """mode="narrow" over CUDA IPC: a +-1 signal takes the int8 exchange;
+    a wide one (|x| up to 2^20) is flagged by the pack kernel and falls back
+    to the fused int64 path.  Both equal the oracle."""
+    from oracle import oracle_np
+
+    n, world = 20, 2
+    mp.spawn(_peer_worker, args=(world, free_port(), n, str(tmp_path), "narrow", kind), nprocs=world, join=True)
+    got = np.concatenate([np.load(tmp_path / f"shard{r}.npy") for r in range(world)])
+    ref = oracle_np.gen(kind, 7, [1 << 20] if kind == 2 else [], 0, 1 << n)
+    coracle.oracle_fwht_i64(ref.ctypes.data, n)
+    assert np.array_equal(got, ref)
+    assert [open(tmp_path / f"mode{r}.txt").read() for r in range(world)] == [expect] * world

@@ -407,6 +407,55 @@ def test_sharded_fused_emulation(coracle, P):
         assert np.array_equal(np.concatenate([s.cpu().numpy() for s in shards]), ref), (P, nl)
 
 
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_sharded_narrow_emulation(coracle, P):
+    """Narrow-wire exchange (int8 cross stages first, then widening local
+    transforms) on P buffers of one device: +-1 signals, values at the wire
+    limit +-(127 >> log2 P), and one value over it (falls back to fused)."""
+    p = P.bit_length() - 1
+    lim = 127 >> p
+    rng = np.random.default_rng(P)
+    for nl in (8, 13, 14, 18, 22):
+        n = nl + p
+        cases = [oracle_np.gen(1, 80 + n, [], 0, 1 << n),
+                 rng.choice(np.array([-lim, lim, 0, 1], dtype=np.int64), 1 << n)]
+        over = cases[1].copy()
+        over[(1 << n) - 3] = lim + 1
+        cases.append(over)
+        for x in cases:
+            ref = c_fwht(coracle, x)
+            shards = [dev(c) for c in np.split(x, P)]
+            assert sharded.fwht_shards(shards, narrow=True) == n << (n - 1)
+            assert np.array_equal(np.concatenate([s.cpu().numpy() for s in shards]), ref), (P, nl)
+
+
+def test_narrow_primitives():
+    """bw_pack_narrow_i64 flags exactly the values over 127 >> log2 P;
+    bw_fwht_widen on int8 / int16 / int32 sources equals the int64 transform."""
+    L = _lib.lib()
+    sh = torch.cuda.current_stream().cuda_stream
+    for p in (1, 2, 3):
+        lim = 127 >> p
+        for bad_val, flagged in ((lim, 0), (-lim, 0), (lim + 1, 1), (-lim - 1, 1)):
+            x = torch.zeros(1 << 12, dtype=torch.int64, device="cuda")
+            x[777] = bad_val
+            out = torch.empty(1 << 12, dtype=torch.int8, device="cuda")
+            flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+            _lib.check(L.bw_pack_narrow_i64(x.data_ptr(), x.numel(), 1, p, out.data_ptr(), flag.data_ptr(), sh))
+            assert int(flag.item()) == flagged, (p, bad_val)
+            if not flagged:
+                assert torch.equal(out.to(torch.int64), x)
+    for dt, hi in ((torch.int8, 127), (torch.int16, 32767), (torch.int32, 1 << 30)):
+        for n in (5, 13, 16, 21):
+            src = torch.randint(-hi, hi + 1, (1 << n,), dtype=torch.int64, device="cuda")
+            ref = src.clone()
+            bw.fwht_array(ref)
+            dst = torch.empty_like(ref)
+            s8 = src.to(dt)
+            _lib.check(L.bw_fwht_widen(s8.data_ptr(), s8.element_size(), dst.data_ptr(), n, sh, None))
+            assert torch.equal(dst, ref), (dt, n)
+
+
 @pytest.mark.parametrize("n,p", [(2, 1), (4, 3), (12, 2), (16, 1), (16, 3), (17, 4), (20, 2), (24, 3)])
 def test_run_parallel_drop_in(coracle, n, p):
     """parallel.run_parallel (parallel.py:162-198) on the GPU equals the

@@ -1,8 +1,9 @@
 """Single-GPU timing of the multi-GPU kernels: P shards as P buffers of one
 device (same kernels and addressing as P GPUs, but every "peer" access is
 local HBM, so this times the kernels' HBM efficiency, not NVLink).
-Compares mode peer (full local transform + K6) with mode fused (partial
-local plan + K6')."""
+Compares mode peer (full local transform + K6), mode fused (partial local
+plan + K6') and mode narrow (int8 pack, int8 cross-shard exchange, local
+transforms widening the packed shard)."""
 import os
 import sys
 
@@ -16,14 +17,15 @@ for P in (2, 4, 8):
     p = P.bit_length() - 1
     nl = n - p
     shards = [torch.zeros(1 << nl, dtype=torch.int64, device="cuda") for _ in range(P)]
-    for fused in (False, True):
-        sharded.fwht_shards(shards, fused=fused)
+    for mode in ("peer", "fused", "narrow"):
+        fused, narrow = mode == "fused", mode == "narrow"
+        sharded.fwht_shards(shards, fused=fused, narrow=narrow)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = 3
         e0.record()
         for _ in range(reps):
-            sharded.fwht_shards(shards, fused=fused)
+            sharded.fwht_shards(shards, fused=fused, narrow=narrow)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
@@ -31,7 +33,7 @@ for P in (2, 4, 8):
         if fused:
             w, r = sharded.fused_plan(nl, p)
             extra = f"local widths {w} + fused pass ({r} local + {p} shard stages)"
-        print(f"n={n} P={P} {'fused' if fused else 'peer '} {ms:8.3f} ms  {2**n / (ms / 1e3):.3e} points/s  {extra}",
+        print(f"n={n} P={P} {mode:6s} {ms:8.3f} ms  {2**n / (ms / 1e3):.3e} points/s  {extra}",
               flush=True)
     del shards
     torch.cuda.empty_cache()
