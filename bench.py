@@ -50,6 +50,9 @@ def args_parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--intermediates", choices=["narrow", "int64"], default="int64",
+                    help="narrow: the narrow-intermediate plan (int16/int32 between passes, checked, int64 "
+                         "fallback; measured no faster, DESIGN.md section 5); int64: the plain int64 plan")
     ap.add_argument("--mode", choices=["auto", "fused", "peer", "a2a", "narrow"], default="auto",
                     help="cross-GPU exchange (N > 1); auto times fused and a2a (peer with gloo) on two "
                          "steps each and keeps the faster")
@@ -232,6 +235,20 @@ def run_ours(a):
              and all(q["cluster"] == 1 for q in plan["passes"]) and os.environ.get("BW_TWO_PASS", "1") != "0")
     if whole:
         npasses = 1
+    # Narrow intermediates (one GPU, no fused extraction): the library's
+    # bw_fwht_i64_narrow plan, pass by pass -- int16 after the low pass
+    # (checked), int32 after the middle pass, int64 in place at the end.
+    nn = L.bw_narrow_npasses(nl) if p == 0 else 0
+    narrow_local = a.intermediates == "narrow" and nn > 0 and spec.threshold is None and not whole
+    if narrow_local:
+        nneed = int(L.bw_narrow_scratch_bytes(nl))
+        if nneed + (2 << 30) > torch.cuda.mem_get_info()[0]:
+            narrow_local = False
+    if narrow_local:
+        nwork = torch.empty(nneed, dtype=torch.uint8, device="cuda")
+        nflag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        npasses = nn
+        n_fallback = 0
     # Cross-GPU exchange candidates (N > 1): the fused pass over peer
     # pointers (K6'), the separate peer exchange (K6), or NCCL all-to-all +
     # K6 on the receive rows.  "auto" times the first two that apply.
@@ -260,7 +277,7 @@ def run_ours(a):
             st["f_arr"] = (ctypes.c_int * len(st["f_widths"]))(*st["f_widths"])
         if mode == "a2a" and "recv" not in st:
             st["recv"] = torch.empty_like(x)
-        st["nev"] = 2 if whole else st["npasses"] + 4
+        st["nev"] = 2 if whole else 2 * nn + 1 if narrow_local else st["npasses"] + 4
 
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
@@ -297,6 +314,28 @@ def run_ours(a):
 
     def step(ev):
         npasses = st["npasses"]
+        if narrow_local:
+            # ev[2i] .. ev[2i+1]: narrow pass i; ev[1] .. ev[2]: the flag readback
+            nonlocal n_fallback
+            ev[0].record(stream)
+            nflag.zero_()
+            _lib.check(L.bw_fwht_i64_narrow_pass(ptr, nl, nwork.data_ptr(), nneed, 0, nflag.data_ptr(), sh))
+            ev[1].record(stream)
+            bad = int(nflag.item())
+            ev[2].record(stream)
+            if bad:  # a value over int16 after the low pass: the int64 plan (the signal is untouched)
+                n_fallback += 1
+                _lib.check(L.bw_fwht_i64(ptr, nl, sh, None))
+                for i in range(3, 2 * nn + 1):
+                    ev[i].record(stream)
+                return
+            for i in range(1, nn):
+                _lib.check(L.bw_fwht_i64_narrow_pass(ptr, nl, nwork.data_ptr(), nneed, i, nflag.data_ptr(), sh))
+                ev[2 * i + 1].record(stream)
+                if i + 1 < nn:
+                    ev[2 * i + 2].record(stream)
+            ev[-1].record(stream)
+            return
         if st["narrow"]:
             # ev[0] start, ev[1] packed + flags agreed, ev[2] = ev[1], ev[3]
             # exchanged (barrier passed), ev[4] local transforms done
@@ -395,7 +434,7 @@ def run_ours(a):
     # Each transform changes the data; the fused extraction (configs 3/5) and
     # the narrow wire (int8 only while |x| <= 127 >> log2 P) need the config
     # input at every step, so it is regenerated between steps.
-    restore_each = extract or st["narrow"]
+    restore_each = extract or st["narrow"] or narrow_local
     hits_first = None
     for w in range(a.warmup):
         if restore_each:
@@ -427,7 +466,11 @@ def run_ours(a):
     step_ms = [e[0].elapsed_time(e[-1]) for e in evs]
     per_step = flush or restore_each  # something untimed runs between steps
     total_ms = sum(step_ms) if per_step else evs[0][0].elapsed_time(evs[-1][-1])
-    pass_ms = [[e[i].elapsed_time(e[i + 1]) for e in evs] for i in range(npasses)]
+    if narrow_local:  # pass i runs between ev[2i] and ev[2i+1]; ev[1] .. ev[2] is the flag readback
+        pass_ms = [[e[0 if i == 0 else 2 * i].elapsed_time(e[1 if i == 0 else 2 * i + 1]) for e in evs]
+                   for i in range(npasses)]
+    else:
+        pass_ms = [[e[i].elapsed_time(e[i + 1]) for e in evs] for i in range(npasses)]
     xs_ms = [e[npasses + 1].elapsed_time(e[npasses + 2]) for e in evs] if p > 0 else []
     if ws > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda" if a.dist_backend == "nccl" else "cpu")
@@ -438,8 +481,10 @@ def run_ours(a):
     avg_pass = [sum(v) / len(v) for v in pass_ms]
     peak, peak_src = hbm_peak()
     bytes_per_pass = 16 * (2 ** nl) * (2 if whole else 1)
+    # algorithmic bytes per point of each pass (read + write)
+    bpp = ([10, 6, 12] if npasses == 3 else [10, 10]) if narrow_local else [bytes_per_pass // (2 ** nl)] * npasses
     dom = max(range(npasses), key=lambda i: avg_pass[i])
-    achieved = bytes_per_pass / (avg_pass[dom] / 1e3) / 1e9
+    achieved = bpp[dom] * (2 ** nl) / (avg_pass[dom] / 1e3) / 1e9
     launches = a.steps * (npasses + (1 if extract else 0) + (1 if p > 0 else 0))  # whole: 1 launch per step
     if fused:
         launches = a.steps * (len(f_widths) + 1)
@@ -450,7 +495,8 @@ def run_ours(a):
         launches = a.steps * (2 + L.bw_plan_npasses(nl))
     traffic = None  # dram read + write of the dominant pass, from the committed ncu capture
     try:
-        with open(os.path.join(ROOT, "profiles", f"r01_traffic_n{nl}.json")) as f:
+        tname = f"r01_traffic_n{nl}_narrow.json" if narrow_local else f"r01_traffic_n{nl}.json"
+        with open(os.path.join(ROOT, "profiles", tname)) as f:
             tr = json.load(f)
         plan_kinds = [q["kind"] for q in plan["passes"]]
         if len(tr["passes"]) == npasses and plan_kinds[0] == "low":
@@ -487,14 +533,25 @@ def run_ours(a):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": f"pass {dom} ({plan['passes'][dom]['kind']}, stages "
                      f"{pass_stages(plan['passes'][dom])})",
-                     "algorithmic_bytes_per_launch": bytes_per_pass, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bpp[dom] * (2 ** nl), "peak_source": peak_src,
                      "frac_of_8tbs_spec": achieved / 8000.0},
         "passes_ms": [round(v, 4) for v in avg_pass],
-        "passes_gbs": [round(bytes_per_pass / (v / 1e3) / 1e9, 1) for v in avg_pass],
-        "transform_gbs_per_pass_avg": round(bytes_per_pass * npasses / (sum(avg_pass) / 1e3) / 1e9, 1),
+        "passes_gbs": [round(b * (2 ** nl) / (v / 1e3) / 1e9, 1) for b, v in zip(bpp, avg_pass)],
+        "transform_gbs_per_pass_avg": round(sum(bpp) * (2 ** nl) / (sum(avg_pass) / 1e3) / 1e9, 1),
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if narrow_local:
+        line["config"]["intermediates"] = ("int16 after the low pass (checked, int64 plan on overflow), "
+                                           + ("int32 after the middle pass, " if npasses == 3 else "")
+                                           + "int64 in place after the last; each stored tile-major for its reader")
+        line["config"]["narrow_fallbacks"] = n_fallback
+        line["config"]["algorithmic_bytes_per_point"] = bpp
+        line["roofline"]["kernel"] = (f"narrow pass {dom} (k_pass_map, "
+                                      f"{['int64->int16', 'int16->int32', 'int32->int64'][dom] if npasses == 3 else ['int64->int16', 'int16->int64'][dom]})")
+        line["flag_readback_ms"] = round(sum(e[1].elapsed_time(e[2]) for e in evs) / len(evs), 4)
+    else:
+        line["config"]["intermediates"] = "int64"
     if whole:
         line["roofline"]["kernel"] = "k_two_pass (both passes of the plan in one cooperative launch)"
         line["passes_ms"] = {"both_passes_one_launch": round(avg_pass[0], 4)}

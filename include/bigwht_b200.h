@@ -141,6 +141,30 @@ int bw_fwht_widen(const void *src, int src_bytes, int64_t *dst, int log2n, void 
                   uint64_t *butterflies);
 
 /*
+ * fwht_array with NARROW INTERMEDIATES (the +-1 Boolean-signal case of the
+ * paper): the low pass reads int64 and writes int16, a middle pass writes
+ * int32, the last pass writes int64 back in place -- 10 + 6 + 12 bytes per
+ * point of HBM traffic for a three-pass plan instead of 3 x 16.  Each
+ * intermediate is stored tile-major for the pass that reads it (contiguous
+ * tile loads).  Exact: the int16 store is checked (every value after the
+ * low pass within +-32767; over it, the signal is still untouched and the
+ * int64 plan runs instead, *used_narrow = 0), and |y| <= 32767 * 2^r <
+ * 2^31 for the <= 16 stages of the middle pass.  work: device buffer of
+ * bw_narrow_scratch_bytes(log2n) bytes (0 = no narrow plan for this n: the
+ * call then runs the int64 plan).  Synchronises the stream once (the flag).
+ * Reference: fwht_array (core.py:97-117); results bit-identical.
+ */
+int bw_fwht_i64_narrow(int64_t *data, int log2n, void *work, uint64_t work_bytes, void *stream,
+                       int *used_narrow, uint64_t *butterflies);
+uint64_t bw_narrow_scratch_bytes(int log2n);
+int bw_narrow_npasses(int log2n);
+/* One narrow pass, asynchronous; pass 0 ORs 1 into *flag_dev on an int16 overflow. */
+int bw_fwht_i64_narrow_pass(int64_t *data, int log2n, void *work, uint64_t work_bytes, int pass_index,
+                            uint32_t *flag_dev, void *stream);
+/* Test hook: static check of the narrow plan's layouts (16 <= n <= 24). */
+int bw_plan_check_narrow(int log2n);
+
+/*
  * float64 fwht_array (core.py:97-117 on a float64 Signal, core.py:56-59):
  * stages applied strictly in ascending order with the same IEEE a+b / a-b
  * as numpy, so results are bitwise identical to the reference (the order

@@ -51,6 +51,11 @@ _SIGNATURES = {
     "bw_sort_hits_i64": ([P, P, P, P], I32),
     "bw_fwht_widen_i32": ([P, P, I32, P, PU64], I32),
     "bw_fwht_widen": ([P, I32, P, I32, P, PU64], I32),
+    "bw_fwht_i64_narrow": ([P, I32, P, U64, P, ctypes.POINTER(I32), PU64], I32),
+    "bw_narrow_scratch_bytes": ([I32], U64),
+    "bw_narrow_npasses": ([I32], I32),
+    "bw_fwht_i64_narrow_pass": ([P, I32, P, U64, I32, P, P], I32),
+    "bw_plan_check_narrow": ([I32], I32),
     "bw_pack_narrow_i64": ([P, U64, I32, I32, P, P, P], I32),
     "bw_xshard_narrow": ([ctypes.POINTER(P), I32, I32, U64, U64, P], I32),
     "bw_extract_ge_f64": ([P, I32, ctypes.c_double, ctypes.c_uint64, P, P, ctypes.c_uint64, P, P, PU64], I32),

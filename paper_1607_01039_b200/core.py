@@ -15,6 +15,7 @@ Accepted buffers:
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 import enum
 from dataclasses import dataclass
@@ -199,13 +200,46 @@ def check_magnitude_bound(data, log2_dim: int) -> None:
             )
 
 
-def fwht_array(buf) -> int:
+last_narrow = False  # whether the last fwht_array call ran the narrow plan (diagnostics)
+NARROW_MIN_N = 22  # below this the transform is launch-bound and the flag readback costs more than it saves
+
+
+def _narrow_wanted(n: int, narrow) -> int:
+    """Work-buffer bytes of the narrow-intermediate plan if it should be
+    tried for this call, else 0.  narrow=None follows BW_NARROW=1 (off by
+    default: measured no faster than the int64 plan),
+    for n >= NARROW_MIN_N and when the work buffer fits in free device
+    memory with 2 GiB left."""
+    if narrow is False:
+        return 0
+    need = int(_lib.lib().bw_narrow_scratch_bytes(n))
+    if need == 0:
+        return 0
+    if narrow is None:
+        if os.environ.get("BW_NARROW", "0") != "1" or n < NARROW_MIN_N:
+            return 0
+        free, _ = torch.cuda.mem_get_info()
+        if need + (2 << 30) > free:
+            return 0
+    return need
+
+
+def fwht_array(buf, narrow=None) -> int:
     """Transform ``buf`` (length 2**n, contiguous) in place (core.py:97-117).
 
     Stage k pairs elements at stride 2**k and replaces (a, b) with
     (a + b, a - b).  Returns n * 2**(n-1).  No magnitude check, exactly like
     the reference: int64 arithmetic wraps mod 2**64 as numpy's does.
+
+    narrow=True runs the narrow-intermediate plan on a CUDA int64 tensor
+    (bw_fwht_i64_narrow: int16 / int32 intermediates for signals whose
+    values stay within +-32767 after the low pass, e.g. +-1 Boolean
+    signals; otherwise the int64 plan runs, results identical either way).
+    It measured no faster than the int64 plan, so the default (None) uses
+    it only when BW_NARROW=1.
     """
+    global last_narrow
+    last_narrow = False
     _check_contiguous(buf)
     n = _check_shape(buf)
     kind = _dtype_kind(buf)
@@ -228,7 +262,14 @@ def fwht_array(buf) -> int:
         return int(bf.value)
     _require_cuda(buf)
     with torch.cuda.device(buf.device):
-        if kind == "i64":
+        need = _narrow_wanted(n, narrow) if kind == "i64" else 0
+        if need:
+            work = torch.empty(need, dtype=torch.uint8, device=buf.device)
+            used = ctypes.c_int(0)
+            _lib.check(L.bw_fwht_i64_narrow(buf.data_ptr(), n, work.data_ptr(), need, _stream_handle(buf),
+                                            ctypes.byref(used), ctypes.byref(bf)))
+            last_narrow = bool(used.value)
+        elif kind == "i64":
             _lib.check(L.bw_fwht_i64(buf.data_ptr(), n, _stream_handle(buf), ctypes.byref(bf)))
         else:
             _lib.check(L.bw_fwht_f64(buf.data_ptr(), n, _stream_handle(buf), ctypes.byref(bf)))

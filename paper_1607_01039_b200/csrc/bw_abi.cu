@@ -1023,6 +1023,310 @@ int bw_fwht_inplace_i64(int64_t* data, int log2n, int64_t* scratch_dev, void* st
 
 }  // extern "C"
 namespace {
+// ---- narrow intermediates (bw_fwht_i64_narrow) ----------------------------
+//
+// A layout is a permutation of the index bits: pos[b] = the offset bit that
+// global index bit b lands on.  Natural order: pos[b] = b.  Tile-major for
+// pass q: q's tile bits keep their tile-local position, q's tile-id bits
+// follow above them (tiles stored one after another, in launch order).
+struct Layout {
+    int pos[64];
+};
+
+// Geometry of a pass: tile bits T, column bits L and the global bit of
+// every virtual tile bit (one-run passes).
+struct PassGeom {
+    int T = 0, L = 0;
+    int gb[16] = {};
+    uint64_t tile_mask = 0;  // global bits that are tile bits
+};
+
+int pass_geom(const Pass& p, PassGeom* g) {
+    if (p.a) return fail(BW_BAD_ARGUMENTS, "split-row passes have no narrow form");
+    return visit_pass(p, [&](auto t, auto l) -> int {
+        using C = typename decltype(t)::type;
+        g->T = C::T;
+        g->L = decltype(l)::value;
+        if (g->L > g->T) g->L = g->T;
+        g->tile_mask = 0;
+        for (int vb = 0; vb < g->T; ++vb) {
+            g->gb[vb] = vb < g->L ? vb : p.k + (vb - g->L);
+            g->tile_mask |= 1ull << g->gb[vb];
+        }
+        return BW_OK;
+    });
+}
+
+Layout natural_layout(int n) {
+    Layout o;
+    for (int b = 0; b < 64; ++b) o.pos[b] = b < n ? b : -1;
+    return o;
+}
+
+Layout tile_major_layout(const PassGeom& q, int n) {
+    Layout o;
+    for (int b = 0; b < 64; ++b) o.pos[b] = -1;
+    for (int vb = 0; vb < q.T; ++vb) o.pos[q.gb[vb]] = vb;
+    int t = 0;
+    for (int b = 0; b < n; ++b)
+        if (!((q.tile_mask >> b) & 1)) o.pos[b] = q.T + t++;
+    return o;
+}
+
+template <class C, int RD>
+void fill_layout_tab(const PassGeom& g, int n, const Layout& lay, bw::LayoutTab* t) {
+    memset(t, 0, sizeof *t);
+    for (int j = 0; j < 32; ++j)
+        for (int i = 0; i < C::R; ++i)
+            if ((j >> i) & 1) t->reg[j] += 1ull << lay.pos[g.gb[C::reg(RD, i)]];
+    for (int vb = 0; vb < g.T; ++vb) t->bit[vb] = 1ull << lay.pos[g.gb[vb]];
+    // tile id bit i <-> the i-th free global bit (ascending, as tile_base enumerates)
+    int tid = 0;
+    for (int b = 0; b < n; ++b) {
+        if ((g.tile_mask >> b) & 1) continue;
+        const int d = lay.pos[b];
+        const int r = t->nruns - 1;
+        if (r >= 0 && t->rsrc[r] + t->rlen[r] == tid && t->rdst[r] + t->rlen[r] == d) {
+            ++t->rlen[r];
+        } else {
+            t->rsrc[t->nruns] = tid;
+            t->rlen[t->nruns] = 1;
+            t->rdst[t->nruns] = d;
+            ++t->nruns;
+        }
+        ++tid;
+    }
+}
+
+enum NarrowRole { NARROW_FIRST, NARROW_MID, NARROW_LAST_FROM16, NARROW_LAST_FROM32 };
+
+int launch_mapped(const Pass& p, int n, NarrowRole role, const void* src, void* dst, const Layout& ld,
+                  const Layout& st, unsigned* flag, cudaStream_t s) {
+    PassGeom g;
+    BW_TRY(pass_geom(p, &g));
+    return visit_pass(p, [&](auto t, auto l) -> int {
+        using C = typename decltype(t)::type;
+        constexpr int L = decltype(l)::value;
+        if constexpr (C::Q > 1 || bw::SplitOf<C>::value) {
+            return fail(BW_BAD_ARGUMENTS, "no narrow form of this pass shape");
+        } else {
+            bw::MapArgs m;
+            fill_layout_tab<C, 0>(g, n, ld, &m.ld);
+            fill_layout_tab<C, C::NR - 1>(g, n, st, &m.st);
+            if (m.ld.nruns > 6 || m.st.nruns > 6) return fail(BW_BAD_ARGUMENTS, "layout needs too many runs");
+            m.lim = 32767;
+            const unsigned grid = (unsigned)(1ull << (n - bw::kCtaBits));
+            constexpr int smem = bw::Dims<C>::SMEM_BYTES;
+            constexpr bool kLow = L >= C::T;
+            auto go = [&](auto kern, const auto* sp, auto* dp) -> int {
+                if (smem > 48 * 1024) BW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                return launch_cfg<C>(kern, grid, s, sp, dp, flag, m);
+            };
+            if constexpr (kLow) {
+                if (role != NARROW_FIRST) return fail(BW_BAD_ARGUMENTS, "a low pass is only the first narrow pass");
+                return go(bw::k_pass_map<C, L, long long, short>, reinterpret_cast<const long long*>(src),
+                          reinterpret_cast<short*>(dst));
+            } else {
+                if (role == NARROW_MID)
+                    return go(bw::k_pass_map<C, L, short, int>, reinterpret_cast<const short*>(src),
+                              reinterpret_cast<int*>(dst));
+                if (role == NARROW_LAST_FROM16)
+                    return go(bw::k_pass_map<C, L, short, long long>, reinterpret_cast<const short*>(src),
+                              reinterpret_cast<long long*>(dst));
+                if (role == NARROW_LAST_FROM32)
+                    return go(bw::k_pass_map<C, L, int, long long>, reinterpret_cast<const int*>(src),
+                              reinterpret_cast<long long*>(dst));
+                return fail(BW_BAD_ARGUMENTS, "a high pass is never the first narrow pass");
+            }
+        }
+    });
+}
+
+// Plans with a narrow form: a low pass of 13 or 14 bits, then one or two
+// one-run high passes on tiles of one or two CTAs.
+bool narrow_plan(int n, std::vector<Pass>* passes) {
+    std::vector<int> w;
+    if (default_plan(n, &w) != BW_OK) return false;
+    if (build_passes(n, w, passes) != BW_OK) return false;
+    if (passes->size() < 2 || passes->size() > 3 || (*passes)[0].kind != LOW || (*passes)[0].q > 1) return false;
+    for (size_t i = 1; i < passes->size(); ++i)
+        if ((*passes)[i].a || (*passes)[i].q > 1 || (*passes)[i].r > 16) return false;
+    return true;
+}
+
+uint64_t narrow_scratch_bytes(int n, size_t npasses) {
+    return (2ull << n) + (npasses == 3 ? (4ull << n) : 0ull);
+}
+
+// Pass i of the narrow plan: 0 = int64 -> int16 (flags values over
+// +-32767), then int16 -> int32 -> int64 (three passes) or int16 -> int64.
+int narrow_pass(int64_t* data, int n, void* work, const std::vector<Pass>& passes, int i, unsigned* flag,
+                cudaStream_t s) {
+    std::vector<PassGeom> g(passes.size());
+    for (size_t q = 0; q < passes.size(); ++q) BW_TRY(pass_geom(passes[q], &g[q]));
+    short* a16 = reinterpret_cast<short*>(work);
+    int* b32 = reinterpret_cast<int*>(reinterpret_cast<char*>(work) + (2ull << n));
+    const Layout nat = natural_layout(n);
+    const Layout tm1 = tile_major_layout(g[1], n);
+    if (i == 0) return launch_mapped(passes[0], n, NARROW_FIRST, data, a16, nat, tm1, flag, s);
+    if (passes.size() == 2) return launch_mapped(passes[1], n, NARROW_LAST_FROM16, a16, data, tm1, nat, flag, s);
+    const Layout tm2 = tile_major_layout(g[2], n);
+    if (i == 1) return launch_mapped(passes[1], n, NARROW_MID, a16, b32, tm1, tm2, flag, s);
+    return launch_mapped(passes[2], n, NARROW_LAST_FROM32, b32, data, tm2, nat, flag, s);
+}
+
+int narrow_args(int64_t* data, int log2n, void* work, uint64_t work_bytes, std::vector<Pass>* passes) {
+    BW_TRY(check_signal(data, log2n));
+    if ((reinterpret_cast<uintptr_t>(data) & 15u) || !narrow_plan(log2n, passes))
+        return fail(BW_BAD_ARGUMENTS, "no narrow plan for this signal (n = %d)", log2n);
+    const uint64_t need = narrow_scratch_bytes(log2n, passes->size());
+    if (!work || work_bytes < need || (reinterpret_cast<uintptr_t>(work) & 15u))
+        return fail(BW_BAD_ARGUMENTS, "narrow work buffer needs %llu bytes, 16-byte aligned (bw_narrow_scratch_bytes)",
+                    (unsigned long long)need);
+    return BW_OK;
+}
+}  // namespace
+extern "C" {
+
+uint64_t bw_narrow_scratch_bytes(int log2n) {
+    if (log2n < 0 || log2n > BW_MAX_LOG2N) return 0;
+    std::vector<Pass> passes;
+    if (!narrow_plan(log2n, &passes)) return 0;
+    return narrow_scratch_bytes(log2n, passes.size());
+}
+
+int bw_narrow_npasses(int log2n) {
+    std::vector<Pass> passes;
+    if (log2n < 0 || log2n > BW_MAX_LOG2N || !narrow_plan(log2n, &passes)) return 0;
+    return (int)passes.size();
+}
+
+// One pass of the narrow plan, asynchronous (benchmark instrumentation and
+// callers that check the flag themselves): pass 0 ORs 1 into *flag_dev when
+// a value does not fit int16 -- the signal is then untouched and the caller
+// must run the int64 plan instead of the later passes.
+int bw_fwht_i64_narrow_pass(int64_t* data, int log2n, void* work, uint64_t work_bytes, int pass_index,
+                            uint32_t* flag_dev, void* stream) {
+    std::vector<Pass> passes;
+    BW_TRY(narrow_args(data, log2n, work, work_bytes, &passes));
+    if (pass_index < 0 || pass_index >= (int)passes.size() || (pass_index == 0 && !flag_dev))
+        return fail(BW_BAD_ARGUMENTS, "bad narrow pass %d (or null flag)", pass_index);
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    return narrow_pass(data, log2n, work, passes, pass_index, reinterpret_cast<unsigned*>(flag_dev), as_stream(stream));
+}
+
+// Static checker of the narrow plan (TEST HOOK, n <= 24): runs the mapped
+// kernels' exact address computation (layout tables, thread / rank parts,
+// tile runs) for every element of every pass and checks that pass 0 loads
+// and the last pass stores in natural order, that every store offset is a
+// bijection onto [0, 2^n), and that pass i+1 loads every element exactly
+// where pass i stored it.
+int bw_plan_check_narrow(int log2n) {
+    if (log2n < 16 || log2n > 24) return fail(BW_BAD_ARGUMENTS, "narrow plan check supports 16 <= n <= 24");
+    std::vector<Pass> passes;
+    if (!narrow_plan(log2n, &passes)) return fail(BW_BAD_ARGUMENTS, "no narrow plan for n = %d", log2n);
+    const uint64_t N = 1ull << log2n;
+    std::vector<PassGeom> g(passes.size());
+    for (size_t q = 0; q < passes.size(); ++q) BW_TRY(pass_geom(passes[q], &g[q]));
+    std::vector<Layout> lay;  // layout between pass q-1 and pass q (lay[0] = input)
+    lay.push_back(natural_layout(log2n));
+    for (size_t q = 1; q < passes.size(); ++q) lay.push_back(tile_major_layout(g[q], log2n));
+    lay.push_back(natural_layout(log2n));
+    std::vector<uint64_t> ld(N), st(N);
+    std::vector<uint8_t> seen(N);
+    auto base_of = [](const bw::LayoutTab& t, uint64_t tile, uint32_t vt) {
+        unsigned long long off = 0;
+        for (int r = 0; r < t.nruns; ++r) off += ((tile >> t.rsrc[r]) & ((1ull << t.rlen[r]) - 1ull)) << t.rdst[r];
+        for (int b = 0; b < 16; ++b)
+            if ((vt >> b) & 1u) off += t.bit[b];
+        return off;
+    };
+    std::vector<uint64_t> prev_st;
+    for (size_t q = 0; q < passes.size(); ++q) {
+        const int st_ok = visit_pass(passes[q], [&](auto t, auto l) -> int {
+            using C = typename decltype(t)::type;
+            constexpr int L = decltype(l)::value;
+            constexpr int T = C::T, NQ = 1 << C::Q, LAST = C::NR - 1;
+            if constexpr (C::Q > 1 || bw::SplitOf<C>::value) {
+                return fail(BW_BAD_ARGUMENTS, "no narrow form");
+            } else {
+                bw::LayoutTab tl, ts;
+                fill_layout_tab<C, 0>(g[q], log2n, lay[q], &tl);
+                fill_layout_tab<C, LAST>(g[q], log2n, lay[q + 1], &ts);
+                std::fill(seen.begin(), seen.end(), 0);
+                const uint64_t ctas = 1ull << (log2n - bw::kCtaBits);
+                for (uint64_t cta = 0; cta < ctas; ++cta) {
+                    const uint32_t rank = (uint32_t)(cta & (NQ - 1));
+                    const uint64_t tile = cta >> C::Q;
+                    const uint64_t gbase = bw::tile_base<T, L>(tile, passes[q].k);
+                    for (uint32_t th = 0; th < (uint32_t)bw::Dims<C>::NT; ++th) {
+                        const uint32_t lane = th & 31u, warp = th >> 5;
+                        const uint32_t v0 = bw::thread_part<C, 0>(lane, warp) | bw::rank_bits<C, 0>(rank);
+                        const uint32_t v1 = bw::thread_part<C, LAST>(lane, warp) | bw::rank_bits<C, LAST>(rank);
+                        const uint64_t b0 = base_of(tl, tile, v0), b1 = base_of(ts, tile, v1);
+                        for (int j = 0; j < bw::Dims<C>::E; ++j) {
+                            const uint64_t gi = gbase + bw::global_off<T, L>(v0 | bw::reg_part<C, 0>(j), passes[q].k);
+                            const uint64_t go = gbase + bw::global_off<T, L>(v1 | bw::reg_part<C, LAST>(j), passes[q].k);
+                            if (gi >= N || go >= N) return fail(BW_BAD_ARGUMENTS, "pass %d leaves the signal", (int)q);
+                            ld[gi] = b0 + tl.reg[j];
+                            st[go] = b1 + ts.reg[j];
+                            if (st[go] >= N || seen[st[go]]) return fail(BW_BAD_ARGUMENTS, "pass %d stores twice", (int)q);
+                            seen[st[go]] = 1;
+                        }
+                    }
+                }
+                return BW_OK;
+            }
+        });
+        if (st_ok != BW_OK) return st_ok;
+        for (uint64_t i = 0; i < N; ++i) {
+            if (q == 0 && ld[i] != i) return fail(BW_BAD_ARGUMENTS, "pass 0 does not load in natural order");
+            if (q > 0 && ld[i] != prev_st[i]) return fail(BW_BAD_ARGUMENTS, "pass %d loads index %llu elsewhere", (int)q,
+                                                          (unsigned long long)i);
+            if (q + 1 == passes.size() && st[i] != i) return fail(BW_BAD_ARGUMENTS, "last pass does not store in natural order");
+        }
+        prev_st = st;
+    }
+    return BW_OK;
+}
+
+// fwht_array with narrow intermediates: pass 1 reads int64 and writes int16
+// (checked: every value after the low pass within +-32767), a middle pass
+// writes int32 (exact: |y| <= 32767 * 2^r < 2^31 for r <= 16), the last
+// pass writes int64 back in place; each intermediate is stored tile-major
+// for the pass that reads it.  When a value does not fit, the signal is
+// still untouched (pass 1 only read it) and the int64 plan runs instead.
+// Synchronises the stream once (the overflow flag after pass 1).  Plans
+// without a narrow form (n < 16, split rows, 4-CTA tiles) run the int64 plan.
+int bw_fwht_i64_narrow(int64_t* data, int log2n, void* work, uint64_t work_bytes, void* stream,
+                       int* used_narrow, uint64_t* butterflies) {
+    BW_TRY(check_signal(data, log2n));
+    if (used_narrow) *used_narrow = 0;
+    if (butterflies) *butterflies = butterfly_count(log2n);
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    cudaStream_t s = as_stream(stream);
+    std::vector<Pass> passes;
+    if ((reinterpret_cast<uintptr_t>(data) & 15u) || !narrow_plan(log2n, &passes))
+        return fwht_impl(data, log2n, nullptr, false, s);
+    BW_TRY(narrow_args(data, log2n, work, work_bytes, &passes));
+    void* sc = nullptr;
+    BW_TRY(scratch(dev, 64, &sc));
+    unsigned* flag = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(sc) + 40);
+    BW_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned), s));
+    BW_TRY(narrow_pass(data, log2n, work, passes, 0, flag, s));
+    unsigned bad = 0;
+    BW_CUDA(cudaMemcpyAsync(&bad, flag, sizeof bad, cudaMemcpyDeviceToHost, s));
+    BW_CUDA(cudaStreamSynchronize(s));
+    if (bad) return fwht_impl(data, log2n, nullptr, false, s);  // data untouched: the int64 plan
+    for (size_t i = 1; i < passes.size(); ++i) BW_TRY(narrow_pass(data, log2n, work, passes, (int)i, flag, s));
+    if (used_narrow) *used_narrow = 1;
+    return BW_OK;
+}
+
+}  // extern "C"
+namespace {
 // Host buffer -> device -> host with the copies overlapping the passes:
 // the H2D of each chunk is followed at once by the passes that stay inside
 // a chunk (every pass but the last), and the last pass runs in column

@@ -545,6 +545,117 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
 }
 
 // ---------------------------------------------------------------------------
+// Mapped passes (the narrow-intermediate transform, bw_fwht_i64_narrow):
+// k_pass's rounds, but the source and the destination each have their own
+// element type and their own LAYOUT -- a permutation of the index bits (the
+// natural order, or "tile-major for pass Q": pass Q's tiles stored one
+// after another, tile-local index inside).  So a pass can write its output
+// narrow (int16 / int32) and already in the order its successor reads,
+// which then loads each tile as one contiguous block.  Offsets are linear
+// over disjoint bits: per-register offsets (host table), per tile bit of
+// the thread / cluster-rank part, and runs of tile-id bits per CTA.
+// ---------------------------------------------------------------------------
+struct LayoutTab {
+    unsigned long long reg[32];  // offset of register index j (its tile bits) in the round
+    unsigned long long bit[16];  // offset of virtual tile bit b
+    int nruns;                   // tile id -> offset: sum of ((t >> src) & (2^len - 1)) << dst
+    int rsrc[6], rlen[6], rdst[6];
+};
+struct MapArgs {
+    LayoutTab ld, st;
+    long long lim;  // stores narrower than 8 bytes: every |v| <= lim, else *flag |= 1
+};
+
+template <typename T>
+struct PairOf;
+template <>
+struct PairOf<short> {
+    typedef short2 type;
+};
+template <>
+struct PairOf<int> {
+    typedef int2 type;
+};
+template <>
+struct PairOf<long long> {
+    typedef longlong2 type;
+};
+
+__device__ __forceinline__ unsigned long long layout_base(const LayoutTab& t, uint64_t tile, uint32_t vt) {
+    unsigned long long off = 0;
+#pragma unroll 1
+    for (int r = 0; r < t.nruns; ++r) off += ((tile >> t.rsrc[r]) & ((1ull << t.rlen[r]) - 1ull)) << t.rdst[r];
+#pragma unroll
+    for (int b = 0; b < 16; ++b)
+        if ((vt >> b) & 1u) off += t.bit[b];
+    return off;
+}
+
+template <class C, int L, typename ST, typename DT>
+__global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
+    k_pass_map(const ST* __restrict__ src, DT* __restrict__ dst, unsigned* flag, const __grid_constant__ MapArgs m) {
+    constexpr int E = Dims<C>::E, LAST = C::NR - 1;
+    extern __shared__ u64 sm[];
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = threadIdx.x >> 5;
+    uint32_t rank = 0;
+    uint64_t tile = blockIdx.x;
+    if constexpr (C::Q > 0) {
+        rank = cluster_ctarank();
+        tile = blockIdx.x >> C::Q;
+        if (threadIdx.x == 0) {
+            const uint32_t mb = (uint32_t)__cvta_generic_to_shared(sm + Dims<C>::SMEM_ELEMS);
+            constexpr uint32_t bytes_in = 8u * (Dims<C>::CTA - Dims<C>::CTA / Dims<C>::CLUSTER);
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes_in) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    u64 v[E];
+    {
+        const ST* p = src + layout_base(m.ld, tile, thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank));
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            if constexpr (VecAccess<C, 0, L>::value) {  // tile bit 0 is offset bit 0 in every layout
+                if ((j & 1) == 0) {
+                    const typename PairOf<ST>::type t = __ldcs(reinterpret_cast<const typename PairOf<ST>::type*>(p + m.ld.reg[j]));
+                    v[j] = (u64)(long long)t.x;
+                    v[j + 1] = (u64)(long long)t.y;
+                }
+            } else {
+                v[j] = (u64)(long long)__ldcs(p + m.ld.reg[j]);
+            }
+        }
+    }
+    if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    apply_stages<C, 0, L>(v);
+    run_rounds<C, L, 1>(v, sm, lane, warp, rank);
+    bool bad = false;
+    if constexpr (sizeof(DT) == 2) {  // the int32 stage after it cannot overflow (bw_fwht_i64_narrow)
+#pragma unroll
+        for (int j = 0; j < E; ++j) bad |= ((long long)v[j] > m.lim) | ((long long)v[j] < -m.lim);
+    }
+    DT* q = dst + layout_base(m.st, tile, thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank));
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        if constexpr (VecAccess<C, LAST, L>::value) {
+            if ((j & 1) == 0) {
+                typename PairOf<DT>::type t;
+                t.x = (DT)(long long)v[j];
+                t.y = (DT)(long long)v[j + 1];
+                st_pass(reinterpret_cast<typename PairOf<DT>::type*>(q + m.st.reg[j]), t);
+            }
+        } else {
+            st_pass(q + m.st.reg[j], (DT)(long long)v[j]);
+        }
+    }
+    if constexpr (sizeof(DT) == 2) {
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1u);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Small transforms (n <= 21): both passes of a two-pass plan in ONE
 // cooperative launch -- every CTA transforms its low-bits tile, the grid
 // synchronises (gpu-scope fences; each element was written by exactly one

@@ -214,6 +214,65 @@ def test_split_row_pass_extraction(monkeypatch):
     assert torch.equal(idx[:k][order], i2) and torch.equal(val[:k][order], v2)
 
 
+def narrow_run(x, plan=None, monkeypatch=None):
+    """bw_fwht_i64_narrow on a copy of x: (result, used_narrow)."""
+    t = dev(x)
+    n = int(t.numel()).bit_length() - 1
+    L = _lib.lib()
+    need = int(L.bw_narrow_scratch_bytes(n))
+    work = torch.empty(max(need, 16), dtype=torch.uint8, device="cuda")
+    used = ctypes.c_int(-1)
+    _lib.check(L.bw_fwht_i64_narrow(t.data_ptr(), n, work.data_ptr(), need, torch.cuda.current_stream().cuda_stream,
+                                    ctypes.byref(used), None))
+    return t.cpu().numpy(), used.value
+
+
+def test_narrow_intermediates_match_oracle(coracle, monkeypatch):
+    """int16 / int32 intermediates (k_pass_map, tile-major layouts): +-1 and
+    small-magnitude signals at every default 2- and 3-pass plan up to n=28
+    and on forced plans; wide inputs fall back to int64 -- all exact."""
+    for n in (16, 18, 20, 22, 23, 24, 25, 26, 27, 28):
+        has = _lib.lib().bw_narrow_npasses(n) > 0  # n = 25 plans a 4-CTA low pass: no narrow form
+        for x, expect in ((oracle_np.gen(1, 300 + n, [], 0, 1 << n), has),
+                          (np.random.default_rng(n).integers(-3, 4, 1 << n).astype(np.int64), has),
+                          (oracle_np.gen(2, 310 + n, [1 << 20], 0, 1 << n), 0)):
+            got, used = narrow_run(x)
+            assert used == expect, (n, used)
+            assert np.array_equal(got, c_fwht(coracle, x)), n
+    for plan in ("13,5,6", "13,2,9", "14,4,6", "13,10,1", "13,1,10", "14,10", "13,6,5", "13,3,8", "14,9,1"):
+        monkeypatch.setenv("BW_PLAN", plan)
+        n = sum(int(v) for v in plan.split(","))
+        x = oracle_np.gen(1, 77, [], 0, 1 << n)
+        got, used = narrow_run(x)
+        assert used == 1 and np.array_equal(got, c_fwht(coracle, x)), plan
+
+
+def test_narrow_int16_edge(coracle):
+    """The int16 check is exact: a low-pass output of +-32767 stays narrow,
+    +-32768 falls back (the signal untouched by the failed first pass)."""
+    n = 23  # plan 13 + 10: the low pass sums blocks of 2^13
+    for sign in (1, -1):
+        x = np.full(1 << n, sign, dtype=np.int64)
+        x[: 1 << 13] = 4 * sign
+        x[5] = 3 * sign  # block 0 sums to +-32767
+        got, used = narrow_run(x)
+        assert used == 1 and np.array_equal(got, c_fwht(coracle, x))
+        x[5] = 4 * sign  # +-32768
+        got, used = narrow_run(x)
+        assert used == 0 and np.array_equal(got, c_fwht(coracle, x))
+
+
+def test_fwht_array_narrow_option(coracle, monkeypatch):
+    from paper_1607_01039_b200 import core
+
+    x = oracle_np.gen(1, 5, [], 0, 1 << 24)
+    for narrow, env, expect in ((True, "0", True), (None, "1", True), (None, "0", False), (False, "1", False)):
+        monkeypatch.setenv("BW_NARROW", env)
+        t = dev(x)
+        bw.fwht_array(t, narrow=narrow)
+        assert core.last_narrow == expect and np.array_equal(t.cpu().numpy(), c_fwht(coracle, x))
+
+
 def test_involution_and_linearity():
     for n in (1, 5, 13, 14, 17, 23, 26):
         x = oracle_np.gen(2, 900 + n, [1000], 0, 1 << n)
