@@ -66,6 +66,8 @@ bool g_attr_done[kMaxDevices];
 int g_num_sms[kMaxDevices];
 // BW_TWO_PASS=0 disables the single-launch path for two-pass plans (A/B knob).
 const bool g_two_pass = !(getenv("BW_TWO_PASS") && getenv("BW_TWO_PASS")[0] == '0');
+// BW_NARROW_TPC=2|4: tiles per CTA of the narrow plan's single-CTA high passes (experiment knob).
+const int g_narrow_tpc = getenv("BW_NARROW_TPC") ? atoi(getenv("BW_NARROW_TPC")) : 1;
 // BW_SPLIT_PLANS=0 keeps the default planner to one-run high passes (A/B knob).
 const bool g_split_plans = !(getenv("BW_SPLIT_PLANS") && getenv("BW_SPLIT_PLANS")[0] == '0');
 // BW_HOST_PIPELINE=0 disables the copy/compute overlap of host-buffer transforms (A/B knob).
@@ -1122,20 +1124,39 @@ int launch_mapped(const Pass& p, int n, NarrowRole role, const void* src, void* 
                 if (smem > 48 * 1024) BW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                 return launch_cfg<C>(kern, grid, s, sp, dp, flag, m);
             };
+
             if constexpr (kLow) {
                 if (role != NARROW_FIRST) return fail(BW_BAD_ARGUMENTS, "a low pass is only the first narrow pass");
                 return go(bw::k_pass_map<C, L, long long, short>, reinterpret_cast<const long long*>(src),
                           reinterpret_cast<short*>(dst));
             } else {
+                // narrow sources on single-CTA tiles: TPC tiles per CTA (BW_NARROW_TPC, experiment knob)
+                auto go_tpc = [&](auto k1, auto k2, auto k4, const auto* sp, auto* dp) -> int {
+                    if constexpr (C::Q == 0) {
+                        if (g_narrow_tpc == 2) {
+                            if (smem > 48 * 1024) BW_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                            return launch_cfg<C>(k2, grid / 2, s, sp, dp, flag, m);
+                        }
+                        if (g_narrow_tpc == 4) {
+                            if (smem > 48 * 1024) BW_CUDA(cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                            return launch_cfg<C>(k4, grid / 4, s, sp, dp, flag, m);
+                        }
+                    }
+                    return go(k1, sp, dp);
+                };
+                constexpr int T2 = C::Q == 0 ? 2 : 1, T4 = C::Q == 0 ? 4 : 1;
                 if (role == NARROW_MID)
-                    return go(bw::k_pass_map<C, L, short, int>, reinterpret_cast<const short*>(src),
-                              reinterpret_cast<int*>(dst));
+                    return go_tpc(bw::k_pass_map<C, L, short, int>, bw::k_pass_map<C, L, short, int, T2>,
+                                  bw::k_pass_map<C, L, short, int, T4>, reinterpret_cast<const short*>(src),
+                                  reinterpret_cast<int*>(dst));
                 if (role == NARROW_LAST_FROM16)
-                    return go(bw::k_pass_map<C, L, short, long long>, reinterpret_cast<const short*>(src),
-                              reinterpret_cast<long long*>(dst));
+                    return go_tpc(bw::k_pass_map<C, L, short, long long>, bw::k_pass_map<C, L, short, long long, T2>,
+                                  bw::k_pass_map<C, L, short, long long, T4>, reinterpret_cast<const short*>(src),
+                                  reinterpret_cast<long long*>(dst));
                 if (role == NARROW_LAST_FROM32)
-                    return go(bw::k_pass_map<C, L, int, long long>, reinterpret_cast<const int*>(src),
-                              reinterpret_cast<long long*>(dst));
+                    return go_tpc(bw::k_pass_map<C, L, int, long long>, bw::k_pass_map<C, L, int, long long, T2>,
+                                  bw::k_pass_map<C, L, int, long long, T4>, reinterpret_cast<const int*>(src),
+                                  reinterpret_cast<long long*>(dst));
                 return fail(BW_BAD_ARGUMENTS, "a high pass is never the first narrow pass");
             }
         }

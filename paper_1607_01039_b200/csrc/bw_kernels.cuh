@@ -44,6 +44,33 @@ __device__ __forceinline__ T ld_pass(const T* p) {
         }
     } else return *p;
 }
+// Any 2- to 16-byte load with the passes' L2::256B fetch size (the mapped
+// passes' narrow and pair types).
+template <class T>
+__device__ __forceinline__ T ld_any(const T* p) {
+    T v;
+    if constexpr (sizeof(T) == 16) {
+        unsigned long long a, b;
+        asm volatile("ld.global.L2::256B.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+        memcpy(&v, &a, 8);
+        memcpy(reinterpret_cast<char*>(&v) + 8, &b, 8);
+    } else if constexpr (sizeof(T) == 8) {
+        unsigned long long a;
+        asm volatile("ld.global.L2::256B.u64 %0, [%1];" : "=l"(a) : "l"(p));
+        memcpy(&v, &a, 8);
+    } else if constexpr (sizeof(T) == 4) {
+        unsigned a;
+        asm volatile("ld.global.L2::256B.u32 %0, [%1];" : "=r"(a) : "l"(p));
+        memcpy(&v, &a, 4);
+    } else {
+        static_assert(sizeof(T) == 2, "2-16 byte loads");
+        unsigned short a;
+        asm volatile("ld.global.L2::256B.u16 %0, [%1];" : "=h"(a) : "l"(p));
+        memcpy(&v, &a, 2);
+    }
+    return v;
+}
+
 template <class T>
 __device__ __forceinline__ void st_pass(T* p, const T& v) {
     if constexpr (BW_ST_POLICY == 0) __stcs(p, v);
@@ -591,15 +618,19 @@ __device__ __forceinline__ unsigned long long layout_base(const LayoutTab& t, ui
     return off;
 }
 
-template <class C, int L, typename ST, typename DT>
+// TPC tiles per CTA (single-CTA configs): every tile's loads are issued
+// before the first tile is computed -- TPC times the bytes in flight, which
+// narrow sources need to keep the load phase as long as an int64 one.
+template <class C, int L, typename ST, typename DT, int TPC = 1>
 __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     k_pass_map(const ST* __restrict__ src, DT* __restrict__ dst, unsigned* flag, const __grid_constant__ MapArgs m) {
+    static_assert(TPC == 1 || C::Q == 0, "several tiles per CTA on single-CTA configs only");
     constexpr int E = Dims<C>::E, LAST = C::NR - 1;
     extern __shared__ u64 sm[];
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
     uint32_t rank = 0;
-    uint64_t tile = blockIdx.x;
+    uint64_t tile = (uint64_t)blockIdx.x * TPC;
     if constexpr (C::Q > 0) {
         rank = cluster_ctarank();
         tile = blockIdx.x >> C::Q;
@@ -612,42 +643,51 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
         }
         __syncthreads();
     }
-    u64 v[E];
-    {
-        const ST* p = src + layout_base(m.ld, tile, thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank));
+    const uint32_t tp0 = thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank);
+    ST raw[TPC][E];
+#pragma unroll
+    for (int u = 0; u < TPC; ++u) {
+        const ST* p = src + layout_base(m.ld, tile + u, tp0);
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             if constexpr (VecAccess<C, 0, L>::value) {  // tile bit 0 is offset bit 0 in every layout
                 if ((j & 1) == 0) {
-                    const typename PairOf<ST>::type t = __ldcs(reinterpret_cast<const typename PairOf<ST>::type*>(p + m.ld.reg[j]));
-                    v[j] = (u64)(long long)t.x;
-                    v[j + 1] = (u64)(long long)t.y;
+                    const typename PairOf<ST>::type t = ld_any(reinterpret_cast<const typename PairOf<ST>::type*>(p + m.ld.reg[j]));
+                    raw[u][j] = t.x;
+                    raw[u][j + 1] = t.y;
                 }
             } else {
-                v[j] = (u64)(long long)__ldcs(p + m.ld.reg[j]);
+                raw[u][j] = ld_any(p + m.ld.reg[j]);
             }
         }
     }
     if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-    apply_stages<C, 0, L>(v);
-    run_rounds<C, L, 1>(v, sm, lane, warp, rank);
     bool bad = false;
-    if constexpr (sizeof(DT) == 2) {  // the int32 stage after it cannot overflow (bw_fwht_i64_narrow)
 #pragma unroll
-        for (int j = 0; j < E; ++j) bad |= ((long long)v[j] > m.lim) | ((long long)v[j] < -m.lim);
-    }
-    DT* q = dst + layout_base(m.st, tile, thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank));
+    for (int u = 0; u < TPC; ++u) {
+        u64 v[E];
 #pragma unroll
-    for (int j = 0; j < E; ++j) {
-        if constexpr (VecAccess<C, LAST, L>::value) {
-            if ((j & 1) == 0) {
-                typename PairOf<DT>::type t;
-                t.x = (DT)(long long)v[j];
-                t.y = (DT)(long long)v[j + 1];
-                st_pass(reinterpret_cast<typename PairOf<DT>::type*>(q + m.st.reg[j]), t);
+        for (int j = 0; j < E; ++j) v[j] = (u64)(long long)raw[u][j];
+        if (u > 0) __syncthreads();  // the previous tile's last shared-memory reads
+        apply_stages<C, 0, L>(v);
+        run_rounds<C, L, 1>(v, sm, lane, warp, rank);
+        if constexpr (sizeof(DT) == 2) {  // the int32 stage after it cannot overflow (bw_fwht_i64_narrow)
+#pragma unroll
+            for (int j = 0; j < E; ++j) bad |= ((long long)v[j] > m.lim) | ((long long)v[j] < -m.lim);
+        }
+        DT* q = dst + layout_base(m.st, tile + u, thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank));
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            if constexpr (VecAccess<C, LAST, L>::value) {
+                if ((j & 1) == 0) {
+                    typename PairOf<DT>::type t;
+                    t.x = (DT)(long long)v[j];
+                    t.y = (DT)(long long)v[j + 1];
+                    st_pass(reinterpret_cast<typename PairOf<DT>::type*>(q + m.st.reg[j]), t);
+                }
+            } else {
+                st_pass(q + m.st.reg[j], (DT)(long long)v[j]);
             }
-        } else {
-            st_pass(q + m.st.reg[j], (DT)(long long)v[j]);
         }
     }
     if constexpr (sizeof(DT) == 2) {

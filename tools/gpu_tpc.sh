@@ -1,0 +1,9 @@
+#!/bin/bash
+# Narrow plan: tiles per CTA on the single-CTA last pass (n = 31, plan 13 + 10 + 8).
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+for v in "int64 1" "narrow 1" "narrow 2" "narrow 4"; do
+  set -- $v
+  BW_PLAN=13,10,8 BW_NARROW_TPC=$2 timeout 300 python bench.py --log2n 31 --steps 5 --warmup 3 --no-e2e --no-cpu --intermediates $1 > gpurun_out/tpc.log 2>&1
+  python -c "import json; d=json.loads([l for l in open('gpurun_out/tpc.log') if l.startswith('{')][0]); print('$1 tpc=$2', round(d['ms_per_step'],3), d['passes_ms'], d['passes_gbs'], d['config'].get('narrow_fallbacks'))" || tail -3 gpurun_out/tpc.log
+done
