@@ -339,3 +339,25 @@ def test_c_consumer_runs(tmp_path):
         r = subprocess.run([exe, n], capture_output=True, text=True, env=env, timeout=300)
         assert r.returncode == 0, r.stdout + r.stderr
         assert "c abi ok" in r.stdout
+
+
+def test_random_plans_check_and_emulate(coracle):
+    """Random legal plans (tests/plan_fuzz.py: every kernel shape, forced
+    cluster sizes, split-row passes in any position): the static checker
+    proves them at n <= 24 and the host emulator of the kernels' tables
+    matches the oracle at n <= 20."""
+    import random
+
+    from oracle import oracle_np
+    from plan_fuzz import random_plan
+
+    rng = random.Random(1607)
+    for i in range(60):
+        n = rng.randint(14, 24)
+        plan = random_plan(rng, n)
+        assert sharded.plan_check(n, plan) == n << (n - 1), plan
+        if n <= 20 and i % 3 == 0:
+            x = oracle_np.gen(2, 900 + i, [1 << 20], 0, 1 << n)
+            ref = x.copy()
+            coracle.oracle_fwht_i64(ref.ctypes.data, n)
+            assert np.array_equal(emulate(x, plan), ref), plan

@@ -707,3 +707,20 @@ def test_host_buffer_transform_overlapped_copies(coracle, n):
     b = pinned.numpy()
     assert bw.fwht_array(b) == n << (n - 1)
     assert np.array_equal(b, ref)
+
+
+def test_random_plans_on_device(coracle):
+    """Random legal plans (tests/plan_fuzz.py) executed on the B200: every
+    kernel shape, forced cluster sizes and split-row passes in any position,
+    byte-identical to the oracle."""
+    import random
+
+    from plan_fuzz import random_plan
+
+    rng = random.Random(34)
+    for n in (18, 21, 24, 26, 27):
+        x = oracle_np.gen(2, 40 + n, [1 << 20], 0, 1 << n)
+        ref = c_fwht(coracle, x)
+        for _ in range(10):
+            plan = random_plan(rng, n)
+            assert np.array_equal(planned(x, plan), ref), (n, plan)
