@@ -634,10 +634,10 @@ def run_e2e(a, x, spec, p, nl, rank, ws, peer):
     from paper_1607_01039_b200 import sharded, signals
 
     nbytes_local = 8 << nl
-    if ws == 1 and nbytes_local * 2 > host_ram_bytes() // 2:
-        return {"value": None, "unit": "points/s", "skipped": f"a pinned {nbytes_local >> 30} GiB host buffer "
-                "does not fit comfortably in host RAM"}
-    steps = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 5))
+    if ws == 1 and nbytes_local * 3 > host_ram_bytes() // 2:
+        return {"value": None, "unit": "points/s", "skipped": f"two pinned {nbytes_local >> 30} GiB host buffers "
+                "do not fit comfortably in host RAM"}
+    steps = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 8))
     host = torch.empty(1 << nl, dtype=torch.int64, pin_memory=True)
     signals.generate(spec, x, base=rank << nl)
     host.copy_(x)
@@ -646,16 +646,31 @@ def run_e2e(a, x, spec, p, nl, rank, ws, peer):
     extract = spec.threshold is not None and ws == 1
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    single = None
     if ws == 1 and not extract:
+        # Consecutive signals through fwht_arrays: two pinned host signals in
+        # turn, so one signal's H2D overlaps the previous one's D2H (PCIe full
+        # duplex).  Every step still copies its whole input in and its whole
+        # result out.
+        host2 = torch.empty(1 << nl, dtype=torch.int64, pin_memory=True)
+        host2.copy_(host)
+        h2np = host2.numpy()
         bw.fwht_array(hnp)  # warm-up (allocates the device staging buffer)
         torch.cuda.synchronize()
         e0.record(stream)
-        for _ in range(steps):
-            bw.fwht_array(hnp)
+        bw.fwht_array(hnp)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        single = {"ms_per_step": e0.elapsed_time(e1), "value": (2 ** nl) / (e0.elapsed_time(e1) / 1e3),
+                  "api": "paper_1607_01039_b200.fwht_array(one pinned numpy buffer)"}
+        bw.fwht_arrays([hnp, h2np])  # warm-up (the second device work buffer)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        bw.fwht_arrays([hnp if i % 2 == 0 else h2np for i in range(steps)])
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
-        api = "paper_1607_01039_b200.fwht_array(pinned numpy buffer)"
+        api = f"paper_1607_01039_b200.fwht_arrays({steps} consecutive pinned numpy signals)"
     elif extract:
         out = host.clone().pin_memory()
         torch.cuda.synchronize()
@@ -698,10 +713,13 @@ def run_e2e(a, x, spec, p, nl, rank, ws, peer):
     h2d_s, d2h_s = e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3
     value = steps * (2 ** (nl + p)) / (ms / 1e3)
     bound = (2 ** (nl + p)) / (h2d_s + d2h_s)
-    return {"value": value, "unit": "points/s", "h2d_bytes_per_step": nbytes,
+    out = {"value": value, "unit": "points/s", "h2d_bytes_per_step": nbytes,
             "d2h_bytes_per_step": nbytes, "steps": steps, "ms_per_step": ms / steps, "api": api,
             "pcie": {"h2d_gbs": nbytes_local / h2d_s / 1e9, "d2h_gbs": nbytes_local / d2h_s / 1e9,
                      "plain_copies_points_per_s": bound, "vs_plain_copies": value / bound}}
+    if single is not None:
+        out["single_signal"] = single
+    return out
 
 
 def main():

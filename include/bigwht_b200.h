@@ -213,6 +213,16 @@ int bw_fwht_host_i64(int64_t *host, int log2n, int64_t *work_dev,
                      int check_bound, void *stream, uint64_t *butterflies);
 
 /*
+ * A batch of host signals (fwht_array on each, core.py:97-117), bit-identical
+ * to bw_fwht_host_i64 per signal.  The signals alternate between two device
+ * buffers of 2^log2n int64 (work0 != work1 when count > 1), so signal
+ * i+1's host->device copy overlaps signal i's device->host copy: PCIe runs
+ * full duplex, which one signal alone cannot use.  Synchronous.
+ */
+int bw_fwht_host_batch_i64(int64_t *const *host, int count, int log2n, int64_t *work0,
+                           int64_t *work1, void *stream, uint64_t *butterflies);
+
+/*
  * Out-of-core transform of a HOST array larger than the device workspace --
  * the paper's blocked external algorithm (external.py:65-283, PAPER.md
  * Fig. 3) with host memory in the role of the disk and the GPU as the

@@ -17,6 +17,7 @@ from .core import (
     butterfly_count,
     check_magnitude_bound,
     fwht_array,
+    fwht_arrays,
     fwht_inplace,
     fwht_widen,
     inverse_wht_inplace,
@@ -44,6 +45,7 @@ __all__ = [
     "butterfly_count",
     "check_magnitude_bound",
     "fwht_array",
+    "fwht_arrays",
     "fwht_inplace",
     "fwht_widen",
     "inverse_wht_inplace",

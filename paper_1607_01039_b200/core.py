@@ -149,12 +149,12 @@ class _HostStage:
     _local = threading.local()
 
     @classmethod
-    def get(cls, n: int, dtype) -> torch.Tensor:
+    def get(cls, n: int, dtype, slot: int = 0) -> torch.Tensor:
         work = getattr(cls._local, "work", None)
         if work is None:
             work = cls._local.work = {}
         dev = torch.cuda.current_device()
-        key = (dev, dtype)
+        key = (dev, dtype) if slot == 0 else (dev, dtype, slot)
         w = work.get(key)
         if w is None or w.numel() < (1 << n):
             w = torch.empty(1 << n, dtype=dtype, device=f"cuda:{dev}")
@@ -274,6 +274,33 @@ def fwht_array(buf, narrow=None) -> int:
         else:
             _lib.check(L.bw_fwht_f64(buf.data_ptr(), n, _stream_handle(buf), ctypes.byref(bf)))
     return int(bf.value)
+
+
+def fwht_arrays(buffers) -> list[int]:
+    """fwht_array on each of several host int64 numpy buffers of the same
+    length 2**n (each in place; core.py:97-117 per buffer).  The device
+    alternates between two work buffers, so one buffer's host->device copy
+    overlaps the previous one's device->host copy (bw_fwht_host_batch_i64);
+    with pinned (page-locked) buffers PCIe then runs in both directions at
+    once.  Returns the butterfly counts."""
+    bufs = list(buffers)
+    if not bufs:
+        return []
+    for b in bufs:
+        if not isinstance(b, np.ndarray) or _dtype_kind(b) != "i64":
+            raise BadArguments("fwht_arrays takes int64 numpy buffers")
+        _check_contiguous(b)
+    n = _check_shape(bufs[0])
+    if any(b.shape != bufs[0].shape for b in bufs):
+        raise BadArguments("fwht_arrays needs buffers of one length")
+    _need_cuda()
+    w0 = _HostStage.get(n, torch.int64)
+    w1 = _HostStage.get(n, torch.int64, slot=1) if len(bufs) > 1 else w0
+    arr = (ctypes.c_void_p * len(bufs))(*[b.ctypes.data for b in bufs])
+    bf = ctypes.c_uint64(0)
+    _lib.check(_lib.lib().bw_fwht_host_batch_i64(arr, len(bufs), n, w0.data_ptr(), w1.data_ptr(),
+                                                 _stream_handle(w0), ctypes.byref(bf)))
+    return [int(bf.value)] * len(bufs)
 
 
 def fwht_widen(x) -> torch.Tensor:

@@ -1356,6 +1356,7 @@ namespace {
 // the caller's stream with events.  *done = false when the plan does not
 // have that shape (the caller then runs the plain sequence).
 cudaStream_t g_copy_stream[kMaxDevices];
+cudaStream_t g_d2h_stream[kMaxDevices];
 
 int host_pipelined(int64_t* host, int log2n, u64* d, int dev, cudaStream_t s, bool* done) {
     *done = false;
@@ -1456,6 +1457,69 @@ int bw_fwht_host_i64(int64_t* host, int log2n, int64_t* work_dev, int check_boun
     BW_CUDA(cudaStreamSynchronize(s));
     if (butterflies) *butterflies = butterfly_count(log2n);
     return BW_OK;
+}
+
+// A batch of host signals, each transformed like bw_fwht_host_i64: the
+// signals alternate between two device buffers, so signal i+1's H2D runs
+// while signal i's D2H runs (PCIe is full duplex; one signal alone cannot
+// overlap them, since no output is final before every input has arrived).
+// H2D, transforms and D2H run on three streams ordered by events.
+int bw_fwht_host_batch_i64(int64_t* const* host, int count, int log2n, int64_t* work0, int64_t* work1,
+                           void* stream, uint64_t* butterflies) {
+    if (!host || count < 0) return fail(BW_BAD_ARGUMENTS, "bad host signal list");
+    for (int i = 0; i < count; ++i)
+        if (!host[i]) return fail(BW_BAD_ARGUMENTS, "null host signal %d", i);
+    BW_TRY(check_signal(work0, log2n));
+    if (count > 1) BW_TRY(check_signal(work1, log2n));
+    if (butterflies) *butterflies = butterfly_count(log2n);
+    if (count == 0) return BW_OK;
+    if (count == 1) return bw_fwht_host_i64(host[0], log2n, work0, 0, stream, butterflies);
+    if (work0 == work1) return fail(BW_BAD_ARGUMENTS, "the two device buffers must differ");
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    cudaStream_t s = as_stream(stream);
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!g_copy_stream[dev]) BW_CUDA(cudaStreamCreateWithFlags(&g_copy_stream[dev], cudaStreamNonBlocking));
+        if (!g_d2h_stream[dev]) BW_CUDA(cudaStreamCreateWithFlags(&g_d2h_stream[dev], cudaStreamNonBlocking));
+    }
+    cudaStream_t up = g_copy_stream[dev], down = g_d2h_stream[dev];
+    const size_t bytes = (size_t)8 << log2n;
+    int64_t* work[2] = {work0, work1};
+    cudaEvent_t start, loaded[2], done[2], freed[2];
+    BW_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    for (int b = 0; b < 2; ++b) {
+        BW_CUDA(cudaEventCreateWithFlags(&loaded[b], cudaEventDisableTiming));
+        BW_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+        BW_CUDA(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
+    }
+    const int st = [&]() -> int {
+        BW_CUDA(cudaEventRecord(start, s));  // the copies follow earlier work on the caller's stream
+        BW_CUDA(cudaStreamWaitEvent(up, start, 0));
+        for (int i = 0; i < count; ++i) {
+            const int b = i & 1;
+            if (i >= 2) BW_CUDA(cudaStreamWaitEvent(up, freed[b], 0));  // signal i-2's D2H left this buffer
+            BW_CUDA(cudaMemcpyAsync(work[b], host[i], bytes, cudaMemcpyHostToDevice, up));
+            BW_CUDA(cudaEventRecord(loaded[b], up));
+            BW_CUDA(cudaStreamWaitEvent(s, loaded[b], 0));
+            BW_TRY(fwht_impl(work[b], log2n, nullptr, false, s));
+            BW_CUDA(cudaEventRecord(done[b], s));
+            BW_CUDA(cudaStreamWaitEvent(down, done[b], 0));
+            BW_CUDA(cudaMemcpyAsync(host[i], work[b], bytes, cudaMemcpyDeviceToHost, down));
+            BW_CUDA(cudaEventRecord(freed[b], down));
+        }
+        BW_CUDA(cudaStreamWaitEvent(s, freed[(count - 1) & 1], 0));
+        BW_CUDA(cudaStreamWaitEvent(s, freed[count & 1], 0));
+        return BW_OK;
+    }();
+    BW_CUDA(cudaStreamSynchronize(s));
+    cudaEventDestroy(start);
+    for (int b = 0; b < 2; ++b) {
+        cudaEventDestroy(loaded[b]);
+        cudaEventDestroy(done[b]);
+        cudaEventDestroy(freed[b]);
+    }
+    return st;
 }
 
 // ---- out-of-core transform of a host array (external.py:65-283) ----------

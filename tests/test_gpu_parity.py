@@ -709,6 +709,28 @@ def test_host_buffer_transform_overlapped_copies(coracle, n):
     assert np.array_equal(b, ref)
 
 
+@pytest.mark.parametrize("count", [1, 2, 3, 5])
+def test_host_batch_overlapped_signals(coracle, count):
+    """fwht_arrays: consecutive host signals through two device buffers
+    (H2D of one overlapping D2H of the previous), pinned and pageable, and a
+    signal list that reuses buffers (each use sees the previous result)."""
+    n = 22
+    xs = [oracle_np.gen(2, 700 + i, [1 << 20], 0, 1 << n) for i in range(count)]
+    refs = [c_fwht(coracle, x) for x in xs]
+    pageable = [x.copy() for x in xs]
+    assert bw.fwht_arrays(pageable) == [n << (n - 1)] * count
+    assert all(np.array_equal(a, r) for a, r in zip(pageable, refs))
+    pinned = [torch.from_numpy(x.copy()).pin_memory() for x in xs]
+    arrs = [t.numpy() for t in pinned]
+    bw.fwht_arrays(arrs)
+    assert all(np.array_equal(a, r) for a, r in zip(arrs, refs))
+    # two buffers in turn, as bench.py's e2e leg uses them: H H x = 2^n x
+    h = [torch.from_numpy(xs[0].copy()).pin_memory(), torch.from_numpy(xs[-1].copy()).pin_memory()]
+    hn = [t.numpy() for t in h]
+    bw.fwht_arrays([hn[i % 2] for i in range(4)])
+    assert np.array_equal(hn[0], xs[0] << n) and np.array_equal(hn[1], xs[-1] << n)
+
+
 def test_random_plans_on_device(coracle):
     """Random legal plans (tests/plan_fuzz.py) executed on the B200: every
     kernel shape, forced cluster sizes and split-row passes in any position,
