@@ -217,7 +217,8 @@ int bw_fwht_host_i64(int64_t *host, int log2n, int64_t *work_dev,
  * to bw_fwht_host_i64 per signal.  The signals alternate between two device
  * buffers of 2^log2n int64 (work0 != work1 when count > 1), so signal
  * i+1's host->device copy overlaps signal i's device->host copy: PCIe runs
- * full duplex, which one signal alone cannot use.  Synchronous.
+ * full duplex, which one signal alone cannot use.  A buffer listed twice in
+ * a row is processed in order.  Synchronous.
  */
 int bw_fwht_host_batch_i64(int64_t *const *host, int count, int log2n, int64_t *work0,
                            int64_t *work1, void *stream, uint64_t *butterflies);

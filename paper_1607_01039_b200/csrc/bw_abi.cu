@@ -1463,7 +1463,9 @@ int bw_fwht_host_i64(int64_t* host, int log2n, int64_t* work_dev, int check_boun
 // signals alternate between two device buffers, so signal i+1's H2D runs
 // while signal i's D2H runs (PCIe is full duplex; one signal alone cannot
 // overlap them, since no output is final before every input has arrived).
-// H2D, transforms and D2H run on three streams ordered by events.
+// H2D, transforms and D2H run on three streams ordered by events.  A host
+// buffer listed twice in a row is processed in order (its second H2D waits
+// for the first D2H), so the list behaves like fwht_array on each entry.
 int bw_fwht_host_batch_i64(int64_t* const* host, int count, int log2n, int64_t* work0, int64_t* work1,
                            void* stream, uint64_t* butterflies) {
     if (!host || count < 0) return fail(BW_BAD_ARGUMENTS, "bad host signal list");
@@ -1499,6 +1501,10 @@ int bw_fwht_host_batch_i64(int64_t* const* host, int count, int log2n, int64_t* 
         for (int i = 0; i < count; ++i) {
             const int b = i & 1;
             if (i >= 2) BW_CUDA(cudaStreamWaitEvent(up, freed[b], 0));  // signal i-2's D2H left this buffer
+            const char* hi = reinterpret_cast<const char*>(host[i]);
+            const char* hp = reinterpret_cast<const char*>(host[i - (i > 0)]);
+            if (i > 0 && hi < hp + bytes && hp < hi + bytes)  // the same host memory twice in a row: in order
+                BW_CUDA(cudaStreamWaitEvent(up, freed[b ^ 1], 0));
             BW_CUDA(cudaMemcpyAsync(work[b], host[i], bytes, cudaMemcpyHostToDevice, up));
             BW_CUDA(cudaEventRecord(loaded[b], up));
             BW_CUDA(cudaStreamWaitEvent(s, loaded[b], 0));

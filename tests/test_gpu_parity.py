@@ -729,6 +729,10 @@ def test_host_batch_overlapped_signals(coracle, count):
     hn = [t.numpy() for t in h]
     bw.fwht_arrays([hn[i % 2] for i in range(4)])
     assert np.array_equal(hn[0], xs[0] << n) and np.array_equal(hn[1], xs[-1] << n)
+    # the same buffer twice in a row runs in order: H H x = 2^n x
+    one = torch.from_numpy(xs[0].copy()).pin_memory().numpy()
+    bw.fwht_arrays([one, one])
+    assert np.array_equal(one, xs[0] << n)
 
 
 def test_random_plans_on_device(coracle):
