@@ -257,7 +257,9 @@ class CudaBackend:
                                                         _stream_handle(slots)))
 
     def sync(self, t: torch.Tensor) -> None:
-        torch.cuda.synchronize(t.device)
+        # the caller's stream only: copies of other signals on other streams
+        # (fwht_distributed_many) keep running across the barriers
+        torch.cuda.current_stream(t.device).synchronize()
 
 
 class _PeerMap:
@@ -329,7 +331,7 @@ def narrow_step(local: torch.Tensor, nw: NarrowWire, group, dist, p: int, device
     if device_barrier is not None:
         device_barrier()
     else:
-        torch.cuda.synchronize(local.device)
+        torch.cuda.current_stream(local.device).synchronize()
         dist.barrier(group)  # (ii) every slice exchanged before anyone widens
     mark(2)
     _widen(nw.packed, local)
@@ -369,7 +371,7 @@ def fwht_distributed(local: torch.Tensor, group=None, mode: str = "fused", backe
             nw = narrow_wire or NarrowWire(local, group, dist)
             done = narrow_step(local, nw, group, dist, p)
             if narrow_wire is None:  # barrier (ii) passed: no peer touches our packed shard any more
-                torch.cuda.synchronize(local.device)
+                torch.cuda.current_stream(local.device).synchronize()
                 nw.close()
             if done:
                 last_exchange = "narrow"
@@ -422,3 +424,58 @@ def fwht_distributed(local: torch.Tensor, group=None, mode: str = "fused", backe
         last_exchange = "a2a"
         return n << (n - 1)
     raise BadArguments(f"unknown mode {mode!r}")
+
+
+def fwht_distributed_many(hosts: list, group=None, mode: str = "fused", work=None, peer_maps=None,
+                          narrow_wires=None) -> int:
+    """fwht_distributed on a sequence of host shards (this rank's pinned
+    torch CPU tensors, one per signal; every rank calls it with the same
+    count): each is copied in, transformed across the group and copied back
+    in place.  The signals alternate between two device buffers, so one
+    signal's host->device copy overlaps the previous signal's device->host
+    copy (PCIe full duplex), as bw_fwht_host_batch_i64 does on one GPU.
+    work / peer_maps / narrow_wires: optional reusable per-buffer state (two
+    of each).  Returns n * 2**(n-1) per signal."""
+    import torch.distributed as dist
+
+    if not hosts:
+        return 0
+    m = hosts[0].numel()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    work = work or [torch.empty(m, dtype=torch.int64, device=dev) for _ in range(2)]
+    own_maps = peer_maps is None and mode in ("fused", "peer")
+    if own_maps:
+        peer_maps = [_PeerMap(w, group, dist) for w in work]
+    peer_maps = peer_maps or [None, None]
+    narrow_wires = narrow_wires or [None, None]
+    cur = torch.cuda.current_stream(dev)
+    up, down = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    loaded = [torch.cuda.Event() for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    freed = [torch.cuda.Event() for _ in range(2)]
+    up.wait_stream(cur)
+    bf = 0
+    for i, h in enumerate(hosts):
+        b = i & 1
+        with torch.cuda.stream(up):
+            if i >= 2:
+                up.wait_event(freed[b])  # signal i-2's copy-out left this buffer
+            if i > 0 and h.data_ptr() == hosts[i - 1].data_ptr():
+                up.wait_event(freed[b ^ 1])  # the same host shard twice in a row: in order
+            work[b].copy_(h, non_blocking=True)
+            loaded[b].record(up)
+        cur.wait_event(loaded[b])
+        bf = fwht_distributed(work[b], group=group, mode=mode, peer_map=peer_maps[b],
+                              narrow_wire=narrow_wires[b])
+        done[b].record(cur)
+        with torch.cuda.stream(down):
+            down.wait_event(done[b])
+            h.copy_(work[b], non_blocking=True)
+            freed[b].record(down)
+    cur.wait_stream(down)
+    cur.synchronize()
+    if own_maps:
+        dist.barrier(group)  # every rank's exchanges are done before the mappings close
+        for pm in peer_maps:
+            pm.close()
+    return bf

@@ -139,3 +139,46 @@ def test_narrow_wire_two_processes_one_gpu(tmp_path, coracle, kind, expect):
     coracle.oracle_fwht_i64(ref.ctypes.data, n)
     assert np.array_equal(got, ref)
     assert [open(tmp_path / f"mode{r}.txt").read() for r in range(world)] == [expect] * world
+
+
+def _many_worker(rank, world, port, n, out_dir, mode):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from oracle import oracle_np
+    from paper_1607_01039_b200 import sharded
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    p = world.bit_length() - 1
+    nl = n - p
+    hosts = [torch.from_numpy(oracle_np.gen(1 + s % 2, 11 + s, [1 << 20] if s % 2 else [], rank << nl, 1 << nl))
+             .pin_memory() for s in range(3)]
+    order = [hosts[0], hosts[1], hosts[2], hosts[2]]  # the last shard twice in a row: in order
+    bf = sharded.fwht_distributed_many(order, mode=mode)
+    assert bf == n << (n - 1)
+    for s, h in enumerate(hosts):
+        np.save(os.path.join(out_dir, f"sig{s}_shard{rank}.npy"), h.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["fused", "narrow", "peer"])
+def test_distributed_many_two_processes_one_gpu(tmp_path, coracle, mode):
+    """fwht_distributed_many: consecutive host shards through two device
+    buffers per rank (H2D of one overlapping D2H of the previous), every
+    exchange mode, a shard listed twice in a row (H H x = 2^n x)."""
+    from oracle import oracle_np
+
+    n, world = 20, 2
+    mp.spawn(_many_worker, args=(world, free_port(), n, str(tmp_path), mode), nprocs=world, join=True)
+    for s in range(3):
+        got = np.concatenate([np.load(tmp_path / f"sig{s}_shard{r}.npy") for r in range(world)])
+        x = oracle_np.gen(1 + s % 2, 11 + s, [1 << 20] if s % 2 else [], 0, 1 << n)
+        if s == 2:
+            ref = x << n
+        else:
+            ref = x.copy()
+            coracle.oracle_fwht_i64(ref.ctypes.data, n)
+        assert np.array_equal(got, ref), s
