@@ -66,8 +66,9 @@ bool g_attr_done[kMaxDevices];
 int g_num_sms[kMaxDevices];
 // BW_TWO_PASS=0 disables the single-launch path for two-pass plans (A/B knob).
 const bool g_two_pass = !(getenv("BW_TWO_PASS") && getenv("BW_TWO_PASS")[0] == '0');
-// BW_NARROW_TPC=2|4: tiles per CTA of the narrow plan's single-CTA high passes (experiment knob).
-const int g_narrow_tpc = getenv("BW_NARROW_TPC") ? atoi(getenv("BW_NARROW_TPC")) : 1;
+// BW_NARROW_TPC=1|2|4: tiles per CTA (or cluster) of the narrow plan's high passes (default 2,
+// measured best: n = 32 in 30.4 ms against 31.6 with one tile; four spill).
+const int g_narrow_tpc = getenv("BW_NARROW_TPC") ? atoi(getenv("BW_NARROW_TPC")) : 2;
 // BW_SPLIT_PLANS=0 keeps the default planner to one-run high passes (A/B knob).
 const bool g_split_plans = !(getenv("BW_SPLIT_PLANS") && getenv("BW_SPLIT_PLANS")[0] == '0');
 // BW_HOST_PIPELINE=0 disables the copy/compute overlap of host-buffer transforms (A/B knob).
@@ -1130,9 +1131,9 @@ int launch_mapped(const Pass& p, int n, NarrowRole role, const void* src, void* 
                 return go(bw::k_pass_map<C, L, long long, short>, reinterpret_cast<const long long*>(src),
                           reinterpret_cast<short*>(dst));
             } else {
-                // narrow sources on single-CTA tiles: TPC tiles per CTA (BW_NARROW_TPC, experiment knob)
+                // narrow sources: TPC tiles per CTA / cluster (BW_NARROW_TPC, experiment knob)
                 auto go_tpc = [&](auto k1, auto k2, auto k4, const auto* sp, auto* dp) -> int {
-                    if constexpr (C::Q == 0) {
+                    if constexpr (C::Q <= 1) {
                         if (g_narrow_tpc == 2) {
                             if (smem > 48 * 1024) BW_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                             return launch_cfg<C>(k2, grid / 2, s, sp, dp, flag, m);
@@ -1144,7 +1145,7 @@ int launch_mapped(const Pass& p, int n, NarrowRole role, const void* src, void* 
                     }
                     return go(k1, sp, dp);
                 };
-                constexpr int T2 = C::Q == 0 ? 2 : 1, T4 = C::Q == 0 ? 4 : 1;
+                constexpr int T2 = C::Q <= 1 ? 2 : 1, T4 = C::Q <= 1 ? 4 : 1;
                 if (role == NARROW_MID)
                     return go_tpc(bw::k_pass_map<C, L, short, int>, bw::k_pass_map<C, L, short, int, T2>,
                                   bw::k_pass_map<C, L, short, int, T4>, reinterpret_cast<const short*>(src),

@@ -386,7 +386,7 @@ __device__ __forceinline__ void exchange_write(const u64 (&v)[Dims<C>::E], u64* 
 
 template <class C, int L, int RD, bool FP = false>
 __device__ __forceinline__ void run_rounds(u64 (&v)[Dims<C>::E], u64* sm, uint32_t lane, uint32_t warp,
-                                           uint32_t rank) {
+                                           uint32_t rank, uint32_t parity = 0u) {
     if constexpr (RD < C::NR) {
         if constexpr (RD == C::XR) {
             static_assert((thread_part_bits<C, RD - 1>() & p_mask<C>()) == 0, "rank swap bits must be register bits");
@@ -396,7 +396,7 @@ __device__ __forceinline__ void run_rounds(u64 (&v)[Dims<C>::E], u64* sm, uint32
             asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
             exchange_write<C, RD - 1>(v, sm, thread_part<C, RD - 1>(lane, warp), rank);
             __syncthreads();  // this CTA's own stores
-            mbar_wait_parity((uint32_t)__cvta_generic_to_shared(sm + Dims<C>::SMEM_ELEMS), 0u);  // remote bytes
+            mbar_wait_parity((uint32_t)__cvta_generic_to_shared(sm + Dims<C>::SMEM_ELEMS), parity);  // remote bytes
         } else {
             if constexpr (RD > 1) __syncthreads();
             store_smem<C, RD - 1>(v, sm, thread_part<C, RD - 1>(lane, warp));
@@ -404,7 +404,7 @@ __device__ __forceinline__ void run_rounds(u64 (&v)[Dims<C>::E], u64* sm, uint32
         }
         load_smem<C, RD>(v, sm, thread_part<C, RD>(lane, warp));
         apply_stages<C, RD, L, FP>(v);
-        run_rounds<C, L, RD + 1, FP>(v, sm, lane, warp, rank);
+        run_rounds<C, L, RD + 1, FP>(v, sm, lane, warp, rank, parity);
     }
 }
 
@@ -618,13 +618,14 @@ __device__ __forceinline__ unsigned long long layout_base(const LayoutTab& t, ui
     return off;
 }
 
-// TPC tiles per CTA (single-CTA configs): every tile's loads are issued
-// before the first tile is computed -- TPC times the bytes in flight, which
-// narrow sources need to keep the load phase as long as an int64 one.
+// TPC tiles per CTA (per cluster): every tile's loads are issued before the
+// first tile is computed -- TPC times the bytes in flight, which narrow
+// sources need to keep the load phase as long as an int64 one.  On cluster
+// tiles each further tile re-arms the exchange mbarrier (phase u) and
+// passes one more cluster barrier (the partner's shared memory is free).
 template <class C, int L, typename ST, typename DT, int TPC = 1>
 __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     k_pass_map(const ST* __restrict__ src, DT* __restrict__ dst, unsigned* flag, const __grid_constant__ MapArgs m) {
-    static_assert(TPC == 1 || C::Q == 0, "several tiles per CTA on single-CTA configs only");
     constexpr int E = Dims<C>::E, LAST = C::NR - 1;
     extern __shared__ u64 sm[];
     const uint32_t lane = threadIdx.x & 31u;
@@ -633,7 +634,7 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     uint64_t tile = (uint64_t)blockIdx.x * TPC;
     if constexpr (C::Q > 0) {
         rank = cluster_ctarank();
-        tile = blockIdx.x >> C::Q;
+        tile = (uint64_t)(blockIdx.x >> C::Q) * TPC;
         if (threadIdx.x == 0) {
             const uint32_t mb = (uint32_t)__cvta_generic_to_shared(sm + Dims<C>::SMEM_ELEMS);
             constexpr uint32_t bytes_in = 8u * (Dims<C>::CTA - Dims<C>::CTA / Dims<C>::CLUSTER);
@@ -668,9 +669,22 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
         u64 v[E];
 #pragma unroll
         for (int j = 0; j < E; ++j) v[j] = (u64)(long long)raw[u][j];
-        if (u > 0) __syncthreads();  // the previous tile's last shared-memory reads
+        if (u > 0) {
+            if constexpr (C::Q > 0) {
+                if (threadIdx.x == 0) {  // phase u of the exchange mbarrier
+                    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(sm + Dims<C>::SMEM_ELEMS);
+                    constexpr uint32_t bytes_in = 8u * (Dims<C>::CTA - Dims<C>::CTA / Dims<C>::CLUSTER);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes_in) : "memory");
+                }
+                // this CTA's reads of tile u-1 are done (release); run_rounds waits
+                // for the partner's before writing into its shared memory
+                asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");
+            } else {
+                __syncthreads();  // the previous tile's last shared-memory reads
+            }
+        }
         apply_stages<C, 0, L>(v);
-        run_rounds<C, L, 1>(v, sm, lane, warp, rank);
+        run_rounds<C, L, 1>(v, sm, lane, warp, rank, (uint32_t)(u & 1));
         if constexpr (sizeof(DT) == 2) {  // the int32 stage after it cannot overflow (bw_fwht_i64_narrow)
 #pragma unroll
             for (int j = 0; j < E; ++j) bad |= ((long long)v[j] > m.lim) | ((long long)v[j] < -m.lim);
