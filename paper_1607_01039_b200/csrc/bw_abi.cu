@@ -69,6 +69,8 @@ const bool g_two_pass = !(getenv("BW_TWO_PASS") && getenv("BW_TWO_PASS")[0] == '
 // BW_NARROW_TPC=1|2|4: tiles per CTA (or cluster) of the narrow plan's high passes (default 2,
 // measured best: n = 32 in 30.4 ms against 31.6 with one tile; four spill).
 const int g_narrow_tpc = getenv("BW_NARROW_TPC") ? atoi(getenv("BW_NARROW_TPC")) : 2;
+// BW_FOLD_BLOCKS=0 keeps the L2-atomic fold for d_out > 14 (A/B knob).
+const bool g_fold_blocks = !(getenv("BW_FOLD_BLOCKS") && getenv("BW_FOLD_BLOCKS")[0] == '0');
 // BW_SPLIT_PLANS=0 keeps the default planner to one-run high passes (A/B knob).
 const bool g_split_plans = !(getenv("BW_SPLIT_PLANS") && getenv("BW_SPLIT_PLANS")[0] == '0');
 // BW_HOST_PIPELINE=0 disables the copy/compute overlap of host-buffer transforms (A/B knob).
@@ -1695,6 +1697,127 @@ int bw_sumsq_partials_i64(const int64_t* x, uint64_t count, uint64_t* partial_de
 }
 
 // fold (subspace.py:150-161) of a device signal, or of a generated one.
+// GF(2) helpers of the block fold (vectors as bit masks).
+namespace gf2 {
+// Insert v into a reduced basis (pivot = highest set bit); returns false if
+// v is dependent.  comb tracks which original vectors XOR to each basis vector.
+struct Basis {
+    std::vector<uint64_t> vec, comb;
+    bool insert(uint64_t v, uint64_t c, uint64_t* rest_comb = nullptr) {
+        for (size_t i = 0; i < vec.size(); ++i)
+            if ((v ^ vec[i]) < v) {  // vec[i]'s pivot bit is set in v
+                v ^= vec[i];
+                c ^= comb[i];
+            }
+        if (v == 0) {
+            if (rest_comb) *rest_comb = c;
+            return false;
+        }
+        // keep the basis sorted by decreasing pivot so one sweep reduces
+        size_t pos = 0;
+        while (pos < vec.size() && vec[pos] > v) ++pos;
+        vec.insert(vec.begin() + pos, v);
+        comb.insert(comb.begin() + pos, c);
+        return true;
+    }
+};
+// Inverse of the d x d matrix given by its columns (invertible).
+std::vector<uint64_t> inverse_cols(const std::vector<uint64_t>& col, int d) {
+    // rows of [M | I]
+    std::vector<uint64_t> row(d, 0), inv(d, 0);
+    for (int r = 0; r < d; ++r) {
+        for (int c = 0; c < d; ++c) row[r] |= ((col[c] >> r) & 1ull) << c;
+        inv[r] = 1ull << r;
+    }
+    for (int c = 0; c < d; ++c) {
+        int p = c;
+        while (p < d && !((row[p] >> c) & 1)) ++p;
+        std::swap(row[c], row[p]);
+        std::swap(inv[c], inv[p]);
+        for (int r = 0; r < d; ++r)
+            if (r != c && ((row[r] >> c) & 1)) {
+                row[r] ^= row[c];
+                inv[r] ^= inv[c];
+            }
+    }
+    std::vector<uint64_t> out(d, 0);  // columns of the inverse
+    for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) out[c] |= ((inv[r] >> c) & 1ull) << r;
+    return out;
+}
+uint64_t apply_cols(const std::vector<uint64_t>& col, uint64_t v) {
+    uint64_t o = 0;
+    for (size_t i = 0; i < col.size(); ++i)
+        if ((v >> i) & 1) o ^= col[i];
+    return o;
+}
+}  // namespace gf2
+
+// Plan of the block fold (k_fold_blocks) for d_out > 14; false when the low
+// 14 columns of L are dependent (then the L2-atomic fold runs).
+struct FoldBlockPlan {
+    std::vector<uint64_t> h0;
+    std::vector<unsigned> bval;
+    std::vector<unsigned long long> kap;
+    std::vector<unsigned> ftop, bmap;
+    uint64_t nchunk = 0;
+};
+
+static bool fold_block_plan(const uint64_t* cols, int d_in, int d_out, FoldBlockPlan* fp) {
+    constexpr int K = bw::kFoldBlockBits;
+    if (d_out <= K || d_in - K > 26 || d_out > 30) return false;
+    gf2::Basis low;
+    for (int i = 0; i < K; ++i)
+        if (!low.insert(cols[i], 0)) return false;
+    // B = [cols 0..13 | unit vectors completing a basis]; A = B^-1
+    std::vector<uint64_t> B(cols, cols + K);
+    for (int r = 0; r < d_out && (int)B.size() < d_out; ++r)
+        if (low.insert(1ull << r, 0)) B.push_back(1ull << r);
+    if ((int)B.size() != d_out) return false;
+    const std::vector<uint64_t> A = gf2::inverse_cols(B, d_out);
+    const int M = d_in - K;
+    std::vector<uint64_t> ftop(M), fbot(M);
+    for (int m = 0; m < M; ++m) {
+        const uint64_t f = gf2::apply_cols(A, cols[K + m]);
+        ftop[m] = f & ((1ull << K) - 1ull);
+        fbot[m] = f >> K;
+    }
+    gf2::Basis img;
+    std::vector<uint64_t> kern;
+    for (int m = 0; m < M; ++m) {
+        uint64_t kc = 0;
+        if (!img.insert(fbot[m], 1ull << m, &kc)) kern.push_back(kc);
+    }
+    const int r = (int)img.vec.size(), dk = (int)kern.size();
+    if (dk > 32) return false;
+    fp->h0.clear();
+    fp->bval.clear();
+    for (uint64_t sel = 0; sel < (1ull << r); ++sel) {  // every block of the image, with a chunk on it
+        uint64_t b = 0, h = 0;
+        for (int i = 0; i < r; ++i)
+            if ((sel >> i) & 1) {
+                b ^= img.vec[i];
+                h ^= img.comb[i];
+            }
+        fp->bval.push_back((unsigned)b);
+        fp->h0.push_back(h);
+    }
+    fp->kap.assign(1024, 0);
+    fp->ftop.assign(1024, 0);
+    fp->bmap.assign(1024, 0);
+    for (int g = 0; g < 4; ++g)
+        for (int v = 0; v < 256; ++v)
+            for (int i = 0; i < 8; ++i) {
+                if (!((v >> i) & 1)) continue;
+                const int bit = 8 * g + i;
+                if (bit < dk) fp->kap[256 * g + v] ^= kern[bit];
+                if (bit < M) fp->ftop[256 * g + v] ^= (unsigned)ftop[bit];
+                if (bit < d_out) fp->bmap[256 * g + v] ^= (unsigned)B[bit];
+            }
+    fp->nchunk = 1ull << dk;
+    return true;
+}
+
 static int fold_impl(const int64_t* x, int d_in, const uint64_t* col_masks, int d_out, int64_t* out_dev,
                      const bw::GenParams& g, cudaStream_t s) {
     if (!col_masks || !out_dev) return fail(BW_BAD_ARGUMENTS, "null pointer");
@@ -1720,6 +1843,44 @@ static int fold_impl(const int64_t* x, int d_in, const uint64_t* col_masks, int 
     const uint64_t count = 1ull << d_in;
     const int grid = grid_for(dev, count, 256, 8);
     unsigned long long* out = reinterpret_cast<unsigned long long*>(out_dev);
+    FoldBlockPlan fp;
+    if (d_out > 14 && g_fold_blocks && fold_block_plan(col_masks, d_in, d_out, &fp)) {
+        const int nb = (int)fp.bval.size();
+        int nsplit = (8 * g_num_sms[dev] + nb - 1) / nb;  // ~8 CTAs per SM over the run
+        if ((uint64_t)nsplit > fp.nchunk) nsplit = (int)fp.nchunk;
+        if (nsplit < 1) nsplit = 1;
+        const size_t tb = 8 * fp.h0.size() + 4 * fp.bval.size() + 8 * 1024 + 4 * 1024 * 2;
+        void* sc2 = nullptr;
+        BW_TRY(scratch(dev, 4096 + tab.size() * 4 + tb + 64, &sc2));
+        char* q = reinterpret_cast<char*>(sc2) + 4096 + ((tab.size() * 4 + 15) & ~size_t(15));
+        unsigned long long* dh0 = reinterpret_cast<unsigned long long*>(q);
+        unsigned long long* dkap = dh0 + fp.h0.size();
+        unsigned* dftop = reinterpret_cast<unsigned*>(dkap + 1024);
+        unsigned* dbmap = dftop + 1024;
+        unsigned* dbval = dbmap + 1024;
+        BW_CUDA(cudaMemcpyAsync(dh0, fp.h0.data(), 8 * fp.h0.size(), cudaMemcpyHostToDevice, s));
+        BW_CUDA(cudaMemcpyAsync(dkap, fp.kap.data(), 8 * 1024, cudaMemcpyHostToDevice, s));
+        BW_CUDA(cudaMemcpyAsync(dftop, fp.ftop.data(), 4 * 1024, cudaMemcpyHostToDevice, s));
+        BW_CUDA(cudaMemcpyAsync(dbmap, fp.bmap.data(), 4 * 1024, cudaMemcpyHostToDevice, s));
+        BW_CUDA(cudaMemcpyAsync(dbval, fp.bval.data(), 4 * fp.bval.size(), cudaMemcpyHostToDevice, s));
+        bw::FoldBlockArgs fa;
+        fa.x = reinterpret_cast<const long long*>(x);
+        fa.g = g;
+        fa.out = out;
+        fa.h0 = dh0;
+        fa.bval = dbval;
+        fa.kap = dkap;
+        fa.ftop = dftop;
+        fa.bmap = dbmap;
+        fa.nsplit = nsplit;
+        fa.nchunk = fp.nchunk;
+        constexpr size_t smem = (8 << bw::kFoldBlockBits) + 8 * 1024 + 4 * 1024 * 2;
+        BW_CUDA(cudaFuncSetAttribute(bw::k_fold_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        bw::k_fold_blocks<<<nb * nsplit, 1024, smem, s>>>(fa);
+        BW_LAUNCHED("k_fold_blocks launch");
+        BW_CUDA(cudaStreamSynchronize(s));  // the tables live in shared scratch
+        return BW_OK;
+    }
     if (d_out <= 14)  // up to 128 KB of shared bins: one 1024-thread CTA per SM (measured faster than 4 x 256)
         bw::k_fold<true, 1024><<<g_num_sms[dev], 1024, (size_t)8 << d_out, s>>>(
             reinterpret_cast<const long long*>(x), count, dtab, groups, d_out, out, g);

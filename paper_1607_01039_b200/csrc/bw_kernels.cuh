@@ -1388,6 +1388,97 @@ __global__ void __launch_bounds__(NT) k_fold(const long long* __restrict__ x, ui
 }
 
 // ---------------------------------------------------------------------------
+// fold with d_out > 14 through a change of output basis (bw_abi fold_blocks):
+// with the low 14 columns of L independent, an invertible A makes
+//   u = A L j = (e ^ c(h)) | blk(h) << 14,   j = h * 2^14 + e,
+// so every contiguous 2^14-point chunk h lands, permuted by XOR with c(h),
+// on ONE block of 2^14 bins.  A CTA owns one block in shared memory and
+// streams the chunks mapping to it (h = h0(b) ^ kernel combinations, each
+// chunk 128 KB contiguous): no atomics while accumulating, 8 B/point of
+// reads; the block is flushed to out[A^-1 u] at the end.
+// ---------------------------------------------------------------------------
+constexpr int kFoldBlockBits = 14;
+
+struct FoldBlockArgs {
+    const long long* x;  // nullptr: the seeded generator's signal
+    GenParams g;
+    unsigned long long* out;
+    const unsigned long long* h0;   // per image block: a chunk index mapping to it
+    const unsigned* bval;           // per image block: its u >> 14
+    const unsigned long long* kap;  // [4][256] XOR of kernel vectors by 8-bit groups of the chunk counter
+    const unsigned* ftop;           // [4][256] c(h) by 8-bit groups of h
+    const unsigned* bmap;           // [4][256] A^-1 u by 8-bit groups of u
+    int nsplit;                     // CTAs per block
+    uint64_t nchunk;                // chunks per block
+};
+
+__global__ void __launch_bounds__(1024, 1) k_fold_blocks(FoldBlockArgs a) {
+    extern __shared__ unsigned long long fsm[];
+    constexpr int B = 1 << kFoldBlockBits;
+    unsigned long long* acc = fsm;
+    unsigned long long* kap = fsm + B;
+    unsigned* ftop = reinterpret_cast<unsigned*>(kap + 1024);
+    unsigned* bmap = ftop + 1024;
+    const int bi = blockIdx.x / a.nsplit, sp = blockIdx.x % a.nsplit;
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+        kap[i] = a.kap[i];
+        ftop[i] = a.ftop[i];
+        bmap[i] = a.bmap[i];
+    }
+    for (int i = threadIdx.x; i < B; i += blockDim.x) acc[i] = 0ull;
+    __syncthreads();
+    const uint64_t q0 = a.nchunk * sp / a.nsplit, q1 = a.nchunk * (sp + 1) / a.nsplit;
+    const uint64_t h0 = a.h0[bi];
+    auto chunk_of = [&](uint64_t q) {
+        return h0 ^ kap[q & 255] ^ kap[256 + ((q >> 8) & 255)] ^ kap[512 + ((q >> 16) & 255)] ^
+               kap[768 + ((q >> 24) & 255)];
+    };
+    auto c_of = [&](uint64_t h) {
+        return ftop[h & 255] ^ ftop[256 + ((h >> 8) & 255)] ^ ftop[512 + ((h >> 16) & 255)] ^
+               ftop[768 + ((h >> 24) & 255)];
+    };
+    constexpr int PER = B / 1024 / 2;  // element pairs per thread per chunk
+    ulonglong2 cur[PER], nxt[PER];
+    auto load = [&](uint64_t h, ulonglong2 (&r)[PER]) {
+        const uint64_t base = h << kFoldBlockBits;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const uint64_t e = 2u * threadIdx.x + 2048u * i;
+            if (a.x) {
+                r[i] = __ldcs(reinterpret_cast<const ulonglong2*>(a.x + base + e));
+            } else {
+                r[i].x = (unsigned long long)gen_value(a.g, base + e);
+                r[i].y = (unsigned long long)gen_value(a.g, base + e + 1);
+            }
+        }
+    };
+    if (q0 < q1) load(chunk_of(q0), cur);
+    for (uint64_t q = q0; q < q1; ++q) {
+        const uint32_t c = c_of(chunk_of(q));
+        if (q + 1 < q1) load(chunk_of(q + 1), nxt);  // the next chunk's loads fly over this chunk's adds
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const uint32_t p = (2u * threadIdx.x + 2048u * i) ^ c;  // e ^ c; e + 1 lands on p ^ 1
+            acc[p] += cur[i].x;
+            acc[p ^ 1u] += cur[i].y;
+        }
+        __syncthreads();  // the next chunk's permutation differs: its bins may be another thread's
+#pragma unroll
+        for (int i = 0; i < PER; ++i) cur[i] = nxt[i];
+    }
+    const unsigned b = a.bval[bi];
+    for (int i = threadIdx.x; i < B; i += blockDim.x) {
+        const unsigned long long v = acc[i];
+        if (!v) continue;
+        const uint32_t u = (uint32_t)i | (b << kFoldBlockBits);
+        const uint32_t t = bmap[u & 255] ^ bmap[256 + ((u >> 8) & 255)] ^ bmap[512 + ((u >> 16) & 255)] ^
+                           bmap[768 + ((u >> 24) & 255)];
+        if (a.nsplit == 1) a.out[t] = v;
+        else atomicAdd(a.out + t, v);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Elementwise helpers for the inverse transform (core.py:147-173).
 // ---------------------------------------------------------------------------
 __global__ void k_check_divisible(const long long* __restrict__ data, uint64_t count, int n, int* flag) {

@@ -650,6 +650,32 @@ def test_fold_matches_reference(golden_npz, coracle):
         assert np.array_equal(subspace.fold(bw.Signal(t), rows).data.cpu().numpy(), want)
 
 
+def test_fold_blocks_large_outputs(coracle, monkeypatch):
+    """d_out > 14: the block fold (change of output basis, one 2^14-bin block
+    per CTA in shared memory, chunks streamed without atomics) equals the
+    oracle for resident and generated inputs; an L whose low 14 columns are
+    dependent takes the L2-atomic fold, and BW_FOLD_BLOCKS=0 forces it."""
+    from paper_1607_01039_b200 import subspace
+
+    cases = [(20, 15, 1), (22, 16, 2), (24, 20, 5), (23, 22, 1), (26, 18, 3)]
+    for n, d_out, idx in cases:
+        spec = signals.config(idx, n)
+        rows = subspace.random_full_rank(n, d_out, 100 + n)
+        if n == 26:  # dependent low columns: column 5 = column 3 ^ column 4 (still rank 18)
+            rows[:, 5] = rows[:, 3] ^ rows[:, 4]
+            assert subspace.gf2_rank(rows) == d_out
+        want = np.empty(1 << d_out, dtype=np.int64)
+        cols = oracle_np.column_masks(rows).astype(np.uint64)
+        arr = (ctypes.c_uint64 * len(spec.params))(*spec.params) if spec.params else None
+        assert coracle.oracle_fold_i64(None, n, cols.ctypes.data, d_out, spec.kind, spec.seed, arr,
+                                       len(spec.params), 4, want.ctypes.data) == 0
+        t = signals.make(spec)
+        for env in ("1", "0"):
+            monkeypatch.setenv("BW_FOLD_BLOCKS", env)
+            assert np.array_equal(subspace.fold_generated(spec, rows).cpu().numpy(), want), (n, d_out, env)
+            assert np.array_equal(subspace.fold(bw.Signal(t), rows).data.cpu().numpy(), want), (n, d_out, env)
+
+
 def test_int32_inputs_widened(coracle):
     """int32 inputs: the reference widened to int64 (overflow-free sums)."""
     rng = np.random.default_rng(32)

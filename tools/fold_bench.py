@@ -1,7 +1,8 @@
 """GPU fold timing (kernel k_fold, subspace.py:150-184): x'[L.j] += x[j] for a
 resident 2^n int64 signal (8 B/point read) and for the on-the-fly generated
-config input (no signal in memory), d_out = 12 (shared-memory bins) and 20
-(L2 atomics).  CUDA events, 5 reps after one warm-up."""
+config input (no signal in memory), d_out = 12 / 14 (shared-memory bins) and
+16 / 20 / 24 (the block fold; BW_FOLD_BLOCKS=0: L2 atomics).  CUDA events,
+5 reps after one warm-up."""
 import os
 import sys
 
@@ -29,7 +30,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 spec = signals.config(4, n)
 x = signals.make(spec)
 sig = Signal(x, Domain.TIME)
-for d_out in (12, 14, 20):
+for d_out in (12, 14, 16, 20, 24):
     rows = subspace.random_full_rank(n, d_out, 7)
     ms = timed(lambda: subspace.fold(sig, rows))
     print(f"fold resident n={n} -> d_out={d_out}: {ms:.3f} ms, {(1 << n) / (ms / 1e3):.3e} points/s, "
