@@ -1753,8 +1753,8 @@ uint64_t apply_cols(const std::vector<uint64_t>& col, uint64_t v) {
 }
 }  // namespace gf2
 
-// Plan of the block fold (k_fold_blocks) for d_out > 14; false when the low
-// 14 columns of L are dependent (then the L2-atomic fold runs).
+// Plan of the block fold (k_fold_blocks) for d_out > kFoldBlockBits; false when the low
+// kFoldBlockBits columns of L are dependent (then the L2-atomic fold runs).
 struct FoldBlockPlan {
     std::vector<uint64_t> h0;
     std::vector<unsigned> bval;
@@ -1765,11 +1765,11 @@ struct FoldBlockPlan {
 
 static bool fold_block_plan(const uint64_t* cols, int d_in, int d_out, FoldBlockPlan* fp) {
     constexpr int K = bw::kFoldBlockBits;
-    if (d_out <= K || d_in - K > 26 || d_out > 30) return false;
+    if (d_out <= K || d_in - K > 32 || d_out > 30) return false;
     gf2::Basis low;
     for (int i = 0; i < K; ++i)
         if (!low.insert(cols[i], 0)) return false;
-    // B = [cols 0..13 | unit vectors completing a basis]; A = B^-1
+    // B = [cols 0..K-1 | unit vectors completing a basis]; A = B^-1
     std::vector<uint64_t> B(cols, cols + K);
     for (int r = 0; r < d_out && (int)B.size() < d_out; ++r)
         if (low.insert(1ull << r, 0)) B.push_back(1ull << r);
@@ -1844,7 +1844,7 @@ static int fold_impl(const int64_t* x, int d_in, const uint64_t* col_masks, int 
     const int grid = grid_for(dev, count, 256, 8);
     unsigned long long* out = reinterpret_cast<unsigned long long*>(out_dev);
     FoldBlockPlan fp;
-    if (d_out > 14 && g_fold_blocks && fold_block_plan(col_masks, d_in, d_out, &fp)) {
+    if (d_out > bw::kFoldBlockBits && g_fold_blocks && fold_block_plan(col_masks, d_in, d_out, &fp)) {
         const int nb = (int)fp.bval.size();
         int nsplit = (8 * g_num_sms[dev] + nb - 1) / nb;  // ~8 CTAs per SM over the run
         if ((uint64_t)nsplit > fp.nchunk) nsplit = (int)fp.nchunk;
@@ -1876,7 +1876,7 @@ static int fold_impl(const int64_t* x, int d_in, const uint64_t* col_masks, int 
         fa.nchunk = fp.nchunk;
         constexpr size_t smem = (8 << bw::kFoldBlockBits) + 8 * 1024 + 4 * 1024 * 2;
         BW_CUDA(cudaFuncSetAttribute(bw::k_fold_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        bw::k_fold_blocks<<<nb * nsplit, 1024, smem, s>>>(fa);
+        bw::k_fold_blocks<<<nb * nsplit, bw::kFoldThreads, smem, s>>>(fa);
         BW_LAUNCHED("k_fold_blocks launch");
         BW_CUDA(cudaStreamSynchronize(s));  // the tables live in shared scratch
         return BW_OK;

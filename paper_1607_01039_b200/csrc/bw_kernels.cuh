@@ -1388,8 +1388,8 @@ __global__ void __launch_bounds__(NT) k_fold(const long long* __restrict__ x, ui
 }
 
 // ---------------------------------------------------------------------------
-// fold with d_out > 14 through a change of output basis (bw_abi fold_blocks):
-// with the low 14 columns of L independent, an invertible A makes
+// fold with d_out > 12 through a change of output basis (bw_abi fold_blocks):
+// with the low K columns of L independent, an invertible A makes
 //   u = A L j = (e ^ c(h)) | blk(h) << 14,   j = h * 2^14 + e,
 // so every contiguous 2^14-point chunk h lands, permuted by XOR with c(h),
 // on ONE block of 2^14 bins.  A CTA owns one block in shared memory and
@@ -1397,7 +1397,17 @@ __global__ void __launch_bounds__(NT) k_fold(const long long* __restrict__ x, ui
 // chunk 128 KB contiguous): no atomics while accumulating, 8 B/point of
 // reads; the block is flushed to out[A^-1 u] at the end.
 // ---------------------------------------------------------------------------
-constexpr int kFoldBlockBits = 14;
+// Bins per CTA 2^12 (32 KB) on 512 threads, several CTAs per SM: measured
+// best of 2^12..2^14 bins x 256..1024 threads (2^32 -> 2^20: 6.8 ms, against
+// 8.2 for 2^13 x 512 and 9.4 for 2^14 x 1024; profiles/r01_fold_ab*.log).
+#ifndef BW_FOLD_BITS
+#define BW_FOLD_BITS 12
+#endif
+#ifndef BW_FOLD_THREADS
+#define BW_FOLD_THREADS 512
+#endif
+constexpr int kFoldBlockBits = BW_FOLD_BITS;
+constexpr int kFoldThreads = BW_FOLD_THREADS;
 
 struct FoldBlockArgs {
     const long long* x;  // nullptr: the seeded generator's signal
@@ -1412,7 +1422,7 @@ struct FoldBlockArgs {
     uint64_t nchunk;                // chunks per block
 };
 
-__global__ void __launch_bounds__(1024, 1) k_fold_blocks(FoldBlockArgs a) {
+__global__ void __launch_bounds__(kFoldThreads, 1024 / kFoldThreads) k_fold_blocks(FoldBlockArgs a) {
     extern __shared__ unsigned long long fsm[];
     constexpr int B = 1 << kFoldBlockBits;
     unsigned long long* acc = fsm;
@@ -1437,13 +1447,13 @@ __global__ void __launch_bounds__(1024, 1) k_fold_blocks(FoldBlockArgs a) {
         return ftop[h & 255] ^ ftop[256 + ((h >> 8) & 255)] ^ ftop[512 + ((h >> 16) & 255)] ^
                ftop[768 + ((h >> 24) & 255)];
     };
-    constexpr int PER = B / 1024 / 2;  // element pairs per thread per chunk
+    constexpr int PER = B / kFoldThreads / 2;  // element pairs per thread per chunk
     ulonglong2 cur[PER], nxt[PER];
     auto load = [&](uint64_t h, ulonglong2 (&r)[PER]) {
         const uint64_t base = h << kFoldBlockBits;
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
-            const uint64_t e = 2u * threadIdx.x + 2048u * i;
+            const uint64_t e = 2u * threadIdx.x + 2u * kFoldThreads * i;
             if (a.x) {
                 r[i] = __ldcs(reinterpret_cast<const ulonglong2*>(a.x + base + e));
             } else {
@@ -1458,7 +1468,7 @@ __global__ void __launch_bounds__(1024, 1) k_fold_blocks(FoldBlockArgs a) {
         if (q + 1 < q1) load(chunk_of(q + 1), nxt);  // the next chunk's loads fly over this chunk's adds
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
-            const uint32_t p = (2u * threadIdx.x + 2048u * i) ^ c;  // e ^ c; e + 1 lands on p ^ 1
+            const uint32_t p = (2u * threadIdx.x + 2u * kFoldThreads * i) ^ c;  // e ^ c; e + 1 lands on p ^ 1
             acc[p] += cur[i].x;
             acc[p ^ 1u] += cur[i].y;
         }
