@@ -1936,22 +1936,26 @@ void fused_shape(int p, int r_last, int* q, int* L) {
 // local high pass of r_last + log2 P rows at k = n_local - r_last).
 int fused_plan(int nl, int p, std::vector<int>* local, int* r_last) {
     if (p < 1 || p > BW_MAX_LOG2P) return fail(BW_INVALID_WORKERS, "log2p = %d outside 1..%d", p, BW_MAX_LOG2P);
-    const int w0 = 13;
-    if (nl < w0 + 1) return fail(BW_BAD_ARGUMENTS, "fused cross-shard plan needs n_local >= %d", w0 + 1);
-    const int h = nl - w0;
+    if (nl < 14) return fail(BW_BAD_ARGUMENTS, "fused cross-shard plan needs n_local >= 14");
     long long best = -1;
     std::vector<int> hi;
-    for (int r = 1; r <= h && r + p <= bw::kMaxHighBits; ++r) {
-        int q = 0, L = 0;
-        fused_shape(p, r, &q, &L);
-        const int rows = r + p;
-        const int eff = rows <= bw::kRegOnlyMaxBits ? shape_eff(rows, 0, nl - r) : shape_eff(rows, q, nl - r);
-        const long long cost = best_high_split(w0, h - r, &hi) + 1000000 / eff;
-        if (best < 0 || cost < best) {
-            best = cost;
-            local->assign(1, w0);
-            local->insert(local->end(), hi.begin(), hi.end());
-            *r_last = r;
+    // low pass of 13, 14 or 15 bits (a 14-bit low pass saves a whole local
+    // pass when n_local + log2 P = 34: 14 + 10 + (7 + 3) instead of
+    // 13 + 7 + 5 + (6 + 3)), then the cheapest split, then the fused pass
+    for (int w0 = 13; w0 <= 15 && w0 < nl; ++w0) {
+        const int h = nl - w0;
+        for (int r = 1; r <= h && r + p <= bw::kMaxHighBits; ++r) {
+            int q = 0, L = 0;
+            fused_shape(p, r, &q, &L);
+            const int rows = r + p;
+            const int eff = rows <= bw::kRegOnlyMaxBits ? shape_eff(rows, 0, nl - r) : shape_eff(rows, q, nl - r);
+            const long long cost = 1000000 / kLowEff[w0 - 13] + best_high_split(w0, h - r, &hi) + 1000000 / eff;
+            if (best < 0 || cost < best) {
+                best = cost;
+                local->assign(1, w0);
+                local->insert(local->end(), hi.begin(), hi.end());
+                *r_last = r;
+            }
         }
     }
     if (best < 0) return fail(BW_BAD_ARGUMENTS, "no room for the fused pass");

@@ -48,7 +48,7 @@ def test_fused_plan_checker(p):
     the 2^(n_local+p) transform exactly once."""
     for nl in range(14, 31):
         widths, r = sharded.fused_plan(nl, p)
-        assert widths[0] == 13 and sum(w & 15 for w in widths) + r == nl and 1 <= r <= 10 - p
+        assert widths[0] in (13, 14, 15) and sum(w & 15 for w in widths) + r == nl and 1 <= r <= 10 - p
         if nl > 24:  # the checker's bitmap limit; the plans above repeat the n=24 shapes
             continue
         n = nl + p
