@@ -292,7 +292,11 @@ def run_ours(a):
     # Configs 3 and 5: the step is the transform with the |W| > tau test
     # fused into the last local pass, then the hits sorted by index.
     extract = spec.threshold is not None and p == 0
-    if extract:
+    # Configs 3/5 on N > 1 GPUs: every rank extracts |W| > tau from its own
+    # shard after the exchange (indices offset by the shard base, so the
+    # ranks' lists in rank order are the index-sorted result).
+    extract_dist = spec.threshold is not None and p > 0
+    if extract or extract_dist:
         cap = 4096
         hit_idx = torch.empty(cap, dtype=torch.int64, device="cuda")
         hit_val = torch.empty(cap, dtype=torch.int64, device="cuda")
@@ -397,6 +401,18 @@ def run_ours(a):
                 ev[npasses + 2].record(stream)
         ev[-1].record(stream)
 
+    if extract_dist:
+        x_step = step
+        dist_hits = {}
+
+        def step(ev):  # noqa: F811 -- the transform, then this rank's extraction, inside the step
+            x_step(ev)
+            cnt = ctypes.c_uint64(0)
+            _lib.check(L.bw_extract_ge_i64(ptr, nl, tau, rank << nl, hit_idx.data_ptr(), hit_val.data_ptr(), cap,
+                                           None, sh, ctypes.byref(cnt)))
+            dist_hits["k"] = int(cnt.value)
+            ev[-1].record(stream)
+
     def events():
         return [torch.cuda.Event(enable_timing=True) for _ in range(st["nev"])]
 
@@ -434,7 +450,7 @@ def run_ours(a):
     # Each transform changes the data; the fused extraction (configs 3/5) and
     # the narrow wire (int8 only while |x| <= 127 >> log2 P) need the config
     # input at every step, so it is regenerated between steps.
-    restore_each = extract or st["narrow"] or narrow_local
+    restore_each = extract or extract_dist or st["narrow"] or narrow_local
     hits_first = None
     for w in range(a.warmup):
         if restore_each:
@@ -443,6 +459,12 @@ def run_ours(a):
         if extract and w == 0:
             k = int(hit_cnt.item())
             hits_first = list(zip(hit_idx[:k].tolist(), hit_val[:k].tolist()))
+        if extract_dist and w == 0:  # gather the ranks' hit lists (reporting only, outside the timing)
+            k = min(dist_hits["k"], cap)
+            mine = list(zip(hit_idx[:k].tolist(), hit_val[:k].tolist()))
+            every = [None] * ws
+            dist.all_gather_object(every, mine)
+            hits_first = [h for part in every for h in part]
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
@@ -493,6 +515,8 @@ def run_ours(a):
     if narrow:  # pack, exchange, then the local plan with a widening first pass
         local_ms = sum(e[3].elapsed_time(e[4]) for e in evs) / len(evs)
         launches = a.steps * (2 + L.bw_plan_npasses(nl))
+    if extract_dist:  # k_extract_count / scan / write on every rank's shard
+        launches += a.steps * 3
     traffic = None  # dram read + write of the dominant pass, from the committed ncu capture
     try:
         tname = f"r01_traffic_n{nl}_narrow.json" if narrow_local else f"r01_traffic_n{nl}.json"
@@ -557,8 +581,10 @@ def run_ours(a):
         line["passes_ms"] = {"both_passes_one_launch": round(avg_pass[0], 4)}
         line["passes_gbs"] = {"both_passes_one_launch": round(bytes_per_pass / (avg_pass[0] / 1e3) / 1e9, 1)}
         line.pop("transform_gbs_per_pass_avg", None)
-    if extract:
-        line["extraction"] = {"tau": spec.threshold, "rule": "|W| > tau, sorted by index, fused into the last pass",
+    if extract or extract_dist:
+        rule = ("|W| > tau, sorted by index, fused into the last pass" if extract else
+                "|W| > tau, sorted by index: every rank extracts from its shard after the exchange (in the step)")
+        line["extraction"] = {"tau": spec.threshold, "rule": rule,
                               "hits": len(hits_first), "hit_indices": [h[0] for h in hits_first][:16],
                               "planted": sorted(spec.masks),
                               "recovered_planted": sorted(h[0] for h in hits_first) == sorted(spec.masks)}

@@ -69,3 +69,18 @@ def test_multirank_narrow_wire_two_processes_one_gpu():
     assert d["config"]["exchange"] == "narrow" and d["config"]["passes"]["fallbacks_to_int64"] == 0
     assert set(d["passes_ms"]) == {"pack_and_agree", "exchange", "local_transform"}
     assert d["nvlink"]["bytes_each_direction"] == (1 << 23) / 2
+
+
+@pytest.mark.gpu
+def test_multirank_extraction_config3_two_processes_one_gpu():
+    """Config 3 on 2 ranks: the transform, then every rank's extraction from
+    its shard inside the step; the gathered hits are the planted secret."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29519", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--config", "3", "--steps", "3", "--warmup", "3",
+           "--dist-backend", "gloo", "--no-cpu", "--no-e2e"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["extraction"]["recovered_planted"] is True, d["extraction"]
+    assert "every rank extracts" in d["extraction"]["rule"]
