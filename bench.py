@@ -368,7 +368,13 @@ def run_ours(a):
             ev[1].record(stream)
             device_barrier()  # every shard's local passes done
             ev[2].record(stream)
-            _lib.check(L.bw_fwht_xfused_pass_i64(ptrs, p, nl, st["f_r"], rank, sh))
+            if extract_dist:  # |W| > tau tested on the fused pass's final values
+                hit_cnt.zero_()
+                _lib.check(L.bw_fwht_xfused_pass_extract_i64(ptrs, p, nl, st["f_r"], rank, tau, 0, hit_idx.data_ptr(),
+                                                             hit_val.data_ptr(), cap, hit_cnt.data_ptr(), sh))
+                _lib.check(L.bw_sort_hits_i64(hit_idx.data_ptr(), hit_val.data_ptr(), hit_cnt.data_ptr(), sh))
+            else:
+                _lib.check(L.bw_fwht_xfused_pass_i64(ptrs, p, nl, st["f_r"], rank, sh))
             ev[3].record(stream)
             device_barrier()  # every fused pass done
             ev[-1].record(stream)
@@ -407,6 +413,9 @@ def run_ours(a):
 
         def step(ev):  # noqa: F811 -- the transform, then this rank's extraction, inside the step
             x_step(ev)
+            if st["fused"]:  # extracted inside the fused pass (this rank's tiles, every shard)
+                dist_hits["k"] = None
+                return
             cnt = ctypes.c_uint64(0)
             _lib.check(L.bw_extract_ge_i64(ptr, nl, tau, rank << nl, hit_idx.data_ptr(), hit_val.data_ptr(), cap,
                                            None, sh, ctypes.byref(cnt)))
@@ -460,11 +469,11 @@ def run_ours(a):
             k = int(hit_cnt.item())
             hits_first = list(zip(hit_idx[:k].tolist(), hit_val[:k].tolist()))
         if extract_dist and w == 0:  # gather the ranks' hit lists (reporting only, outside the timing)
-            k = min(dist_hits["k"], cap)
+            k = min(int(hit_cnt.item()) if dist_hits["k"] is None else dist_hits["k"], cap)
             mine = list(zip(hit_idx[:k].tolist(), hit_val[:k].tolist()))
             every = [None] * ws
             dist.all_gather_object(every, mine)
-            hits_first = [h for part in every for h in part]
+            hits_first = sorted(h for part in every for h in part)
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
@@ -515,8 +524,8 @@ def run_ours(a):
     if narrow:  # pack, exchange, then the local plan with a widening first pass
         local_ms = sum(e[3].elapsed_time(e[4]) for e in evs) / len(evs)
         launches = a.steps * (2 + L.bw_plan_npasses(nl))
-    if extract_dist:  # k_extract_count / scan / write on every rank's shard
-        launches += a.steps * 3
+    if extract_dist:  # fused: k_sort_hits; else k_extract_count / scan / write on every rank's shard
+        launches += a.steps * (1 if fused else 3)
     traffic = None  # dram read + write of the dominant pass, from the committed ncu capture
     try:
         tname = f"r01_traffic_n{nl}_narrow.json" if narrow_local else f"r01_traffic_n{nl}.json"
@@ -583,6 +592,7 @@ def run_ours(a):
         line.pop("transform_gbs_per_pass_avg", None)
     if extract or extract_dist:
         rule = ("|W| > tau, sorted by index, fused into the last pass" if extract else
+                "|W| > tau, sorted by index, fused into the cross-shard pass (K6') on every rank" if fused else
                 "|W| > tau, sorted by index: every rank extracts from its shard after the exchange (in the step)")
         line["extraction"] = {"tau": spec.threshold, "rule": rule,
                               "hits": len(hits_first), "hit_indices": [h[0] for h in hits_first][:16],

@@ -330,6 +330,17 @@ int bw_fwht_xfused_pass_i64(int64_t *const *shards, int log2p, int log2n_local, 
                             int rank, void *stream);
 
 /*
+ * The same fused pass with the threshold test of extract_above
+ * (noisy.py:185-222, |W| >= tau) on its final values: hits are appended
+ * unordered to out_idx / out_val (global indices base + shard * 2^n_local +
+ * offset, up to cap), their number accumulated in *count_dev; sort them with
+ * bw_sort_hits_i64 (<= 2048) or on the host.  Asynchronous.
+ */
+int bw_fwht_xfused_pass_extract_i64(int64_t *const *shards, int log2p, int log2n_local, int r_last,
+                                    int rank, uint64_t tau, uint64_t base, int64_t *out_idx,
+                                    int64_t *out_val, uint64_t cap, uint64_t *count_dev, void *stream);
+
+/*
  * Peer-memory plumbing for one process per GPU: export a device buffer as a
  * CUDA IPC handle (64 bytes) plus its offset inside the allocation, open a
  * peer's handle (NVLink peer access enabled lazily), close it again.

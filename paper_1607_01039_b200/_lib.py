@@ -77,6 +77,7 @@ _SIGNATURES = {
     "bw_fold_gen_i64": ([I32, I32, U64, PU64, I32, PU64, I32, P, P], I32),
     "bw_plan_fused": ([I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32)], I32),
     "bw_fwht_xfused_pass_i64": ([ctypes.POINTER(P), I32, I32, I32, I32, P], I32),
+    "bw_fwht_xfused_pass_extract_i64": ([ctypes.POINTER(P), I32, I32, I32, I32, U64, U64, P, P, U64, P, P], I32),
     "bw_xshard_i64": ([ctypes.POINTER(P), I32, U64, U64, P], I32),
     "bw_xshard_strided_i64": ([P, U64, I32, U64, U64, P], I32),
     "bw_ipc_get_handle": ([P, P, PU64], I32),

@@ -516,13 +516,20 @@ int for_all_f64_pass_kernels(F&& f) {
 
 template <int LOGP, int L>
 int set_fused_attr() {
-    if constexpr (L + LOGP <= 12)
+    if constexpr (L + LOGP <= 12) {
         BW_CUDA(cudaFuncSetAttribute(bw::k_pass_x<bw::CfgHigh13, L, LOGP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      bw::Dims<bw::CfgHigh13>::SMEM_BYTES));
-    if constexpr (L >= 4 && L <= 8 && L + LOGP <= 13)
+        BW_CUDA(cudaFuncSetAttribute(bw::k_pass_x<bw::CfgHigh13, L, LOGP, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, bw::Dims<bw::CfgHigh13>::SMEM_BYTES));
+    }
+    if constexpr (L >= 4 && L <= 8 && L + LOGP <= 13) {
         BW_CUDA(cudaFuncSetAttribute(bw::k_pass_x<bw::CfgHigh14c, L, LOGP>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      bw::Dims<bw::CfgHigh14c>::SMEM_BYTES));
+        BW_CUDA(cudaFuncSetAttribute(bw::k_pass_x<bw::CfgHigh14c, L, LOGP, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     bw::Dims<bw::CfgHigh14c>::SMEM_BYTES));
+    }
     return BW_OK;
 }
 template <int LOGP>
@@ -1994,7 +2001,10 @@ int bw_plan_fused(int log2n_local, int log2p, int* widths, int* nwidths, int* r_
 }
 
 // Device `rank`'s share of the fused last pass (K6') over the P shards.
-int bw_fwht_xfused_pass_i64(int64_t* const* shards, int log2p, int log2n_local, int r_last, int rank, void* stream) {
+}  // extern "C"
+namespace {
+int xfused_pass(int64_t* const* shards, int log2p, int log2n_local, int r_last, int rank, void* stream,
+                const bw::ExtractArgs* exp) {
     if (!shards || log2p < 1 || log2p > BW_MAX_LOG2P) return fail(BW_INVALID_WORKERS, "bad shard list");
     const int P = 1 << log2p;
     if (rank < 0 || rank >= P) return fail(BW_INVALID_WORKERS, "rank %d outside 0..%d", rank, P - 1);
@@ -2020,14 +2030,22 @@ int bw_fwht_xfused_pass_i64(int64_t* const* shards, int log2p, int log2n_local, 
         return with_fused_kernel<LOGP>(L, [&](auto l) -> int {
             constexpr int LL = decltype(l)::value;
             if (q == 1) {
-                if constexpr (LL >= 4 && LL <= 8 && LL + LOGP <= 13)
+                if constexpr (LL >= 4 && LL <= 8 && LL + LOGP <= 13) {
+                    if (exp)
+                        return launch_cfg<bw::CfgHigh14c>(bw::k_pass_x<bw::CfgHigh14c, LL, LOGP, true>,
+                                                          (unsigned)(per << 1), s, sp, k, (uint64_t)rank * per, *exp,
+                                                          log2n_local);
                     return launch_cfg<bw::CfgHigh14c>(bw::k_pass_x<bw::CfgHigh14c, LL, LOGP>, (unsigned)(per << 1), s,
-                                                      sp, k, (uint64_t)rank * per);
+                                                      sp, k, (uint64_t)rank * per, bw::ExtractArgs{}, log2n_local);
+                }
                 return fail(BW_BAD_ARGUMENTS, "no cluster fused kernel for L=%d p=%d", LL, LOGP);
             }
             if constexpr (LL + LOGP <= 12) {
+                if (exp)
+                    return launch_cfg<bw::CfgHigh13>(bw::k_pass_x<bw::CfgHigh13, LL, LOGP, true>, (unsigned)per, s, sp,
+                                                     k, (uint64_t)rank * per, *exp, log2n_local);
                 return launch_cfg<bw::CfgHigh13>(bw::k_pass_x<bw::CfgHigh13, LL, LOGP>, (unsigned)per, s, sp, k,
-                                                 (uint64_t)rank * per);
+                                                 (uint64_t)rank * per, bw::ExtractArgs{}, log2n_local);
             } else {
                 return fail(BW_BAD_ARGUMENTS, "no fused kernel for L=%d p=%d", LL, LOGP);
             }
@@ -2038,6 +2056,24 @@ int bw_fwht_xfused_pass_i64(int64_t* const* shards, int log2p, int log2n_local, 
         case 2: return go(ic<2>{});
         default: return go(ic<3>{});
     }
+}
+}  // namespace
+extern "C" {
+
+int bw_fwht_xfused_pass_i64(int64_t* const* shards, int log2p, int log2n_local, int r_last, int rank, void* stream) {
+    return xfused_pass(shards, log2p, log2n_local, r_last, rank, stream, nullptr);
+}
+
+// The fused pass with |W| >= tau tested on its final values (configs 3/5
+// over several GPUs; noisy.py:185-222): hits appended unordered with their
+// global indices (base + shard * 2^n_local + offset), *count_dev accumulated.
+int bw_fwht_xfused_pass_extract_i64(int64_t* const* shards, int log2p, int log2n_local, int r_last, int rank,
+                                    uint64_t tau, uint64_t base, int64_t* out_idx, int64_t* out_val, uint64_t cap,
+                                    uint64_t* count_dev, void* stream) {
+    if (!count_dev || (cap > 0 && (!out_idx || !out_val))) return fail(BW_BAD_ARGUMENTS, "null extraction output");
+    bw::ExtractArgs ex = {tau, base, reinterpret_cast<long long*>(out_idx), reinterpret_cast<long long*>(out_val),
+                          reinterpret_cast<unsigned long long*>(count_dev), cap};
+    return xfused_pass(shards, log2p, log2n_local, r_last, rank, stream, &ex);
 }
 
 // Cross-shard butterfly (parallel.py:103-110, all log2 P stage phases fused).

@@ -1036,8 +1036,9 @@ __global__ void __launch_bounds__(256) k_xshard_narrow(NarrowPtrs s, uint64_t be
 // bits are register, warp or cluster-rank bits, so every shard-pointer
 // lookup is warp-uniform.
 // ---------------------------------------------------------------------------
-template <class C, int L, int LOGP>
-__global__ void __launch_bounds__(Dims<C>::NT, C::MINB) k_pass_x(ShardPtrs s, int k, uint64_t tile0) {
+template <class C, int L, int LOGP, bool EX = false>
+__global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
+    k_pass_x(ShardPtrs s, int k, uint64_t tile0, ExtractArgs ex, int nl) {
     constexpr int T = C::T, E = Dims<C>::E, TL = T - LOGP, LAST = C::NR - 1;
     constexpr uint32_t lmask = (1u << TL) - 1u;
     extern __shared__ u64 sm[];
@@ -1075,6 +1076,31 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB) k_pass_x(ShardPtrs s, in
     for (int j = 0; j < E; ++j) {
         const uint32_t e = reg_part<C, LAST>(j);
         st_pass(s.p[(tp | e) >> TL] + t1 + global_off<TL, L>(e & lmask, k), v[j]);
+    }
+    // Fused extraction (configs 3/5 over several GPUs): |W| >= tau on the
+    // final values, global index = shard << nl + offset, warp-aggregated
+    // append (unordered; sorted afterwards).
+    if constexpr (EX) {
+        if (!__any_sync(0xffffffffu, any_hit<E>(v, ex.tau))) return;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            const bool h = hit_ge_u(v[j], ex.tau);
+            const unsigned b = __ballot_sync(0xffffffffu, h);
+            if (!b) continue;
+            const int leader = __ffs(b) - 1;
+            unsigned long long first = 0;
+            if ((int)lane == leader) first = atomicAdd(ex.count, (unsigned long long)__popc(b));
+            first = __shfl_sync(0xffffffffu, first, leader);
+            if (h) {
+                const unsigned long long pos = first + __popc(b & ((1u << lane) - 1u));
+                if (pos < ex.cap) {
+                    const uint32_t e = reg_part<C, LAST>(j);
+                    const uint64_t shard = (tp | e) >> TL;
+                    ex.idx[pos] = (long long)(ex.base + (shard << nl) + t1 + global_off<TL, L>(e & lmask, k));
+                    ex.val[pos] = (long long)v[j];
+                }
+            }
+        }
     }
 }
 

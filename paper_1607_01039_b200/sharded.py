@@ -148,6 +148,48 @@ def _fused_pass(ptrs: list[int], p: int, n_local: int, r: int, rank: int, dev: t
                                                       torch.cuda.current_stream(dev).cuda_stream))
 
 
+def _fused_pass_extract(ptrs: list[int], p: int, n_local: int, r: int, rank: int, dev: torch.device, tau: int,
+                        idx: torch.Tensor, val: torch.Tensor, count: torch.Tensor) -> None:
+    """K6' with |W| >= tau tested on its final values (hits appended with
+    global indices, unordered; count accumulated on the device)."""
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().bw_fwht_xfused_pass_extract_i64(
+            arr, p, n_local, r, rank, int(tau), 0, idx.data_ptr(), val.data_ptr(), idx.numel(), count.data_ptr(),
+            torch.cuda.current_stream(dev).cuda_stream))
+
+
+def fwht_shards_extract_ge(shards: list[torch.Tensor], tau: int, cap: int = 1 << 16):
+    """fwht_shards(fused=True) with the extraction (|W| >= tau, noisy.py:185-222)
+    fused into the cross-shard pass: returns (index, value) CUDA tensors of
+    the whole 2**n signal, sorted by index."""
+    p = log2_shards(len(shards))
+    local = shards[0].numel()
+    n_local = local.bit_length() - 1
+    if p == 0 or n_local < 14:
+        raise BadArguments("fused extraction needs P >= 2 shards of >= 2**14 points")
+    widths, r = fused_plan(n_local, p)
+    for s in shards:
+        _local_partial(s, n_local, widths)
+    devices = sorted({s.device.index for s in shards})
+    for d in devices:
+        torch.cuda.synchronize(d)
+    dev0 = shards[0].device
+    idx = torch.empty(cap, dtype=torch.int64, device=dev0)
+    val = torch.empty(cap, dtype=torch.int64, device=dev0)
+    count = torch.zeros(1, dtype=torch.int64, device=dev0)
+    ptrs = [s.data_ptr() for s in shards]
+    for g, s in enumerate(shards):
+        _fused_pass_extract(ptrs, p, n_local, r, g, s.device, tau, idx, val, count)
+    for d in devices:
+        torch.cuda.synchronize(d)
+    k = int(count.item())
+    if k > cap:
+        raise BadArguments(f"{k} hits exceed the capacity {cap}")
+    order = torch.argsort(idx[:k])
+    return idx[:k][order], val[:k][order]
+
+
 # ------------------------------------------------------- single process ---
 
 def xshard(shards: list[torch.Tensor], begin: int = 0, count: int | None = None) -> None:

@@ -72,15 +72,17 @@ def test_multirank_narrow_wire_two_processes_one_gpu():
 
 
 @pytest.mark.gpu
-def test_multirank_extraction_config3_two_processes_one_gpu():
-    """Config 3 on 2 ranks: the transform, then every rank's extraction from
-    its shard inside the step; the gathered hits are the planted secret."""
+@pytest.mark.parametrize("mode", ["fused", "narrow"])
+def test_multirank_extraction_config3_two_processes_one_gpu(mode):
+    """Config 3 on 2 ranks: the extraction fused into the cross-shard pass
+    (fused) or run on every rank's shard after the exchange (narrow), inside
+    the step; the gathered hits are the planted secret."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", "29519", os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--config", "3", "--steps", "3", "--warmup", "3",
-           "--dist-backend", "gloo", "--no-cpu", "--no-e2e"]
+           "--master-addr", "127.0.0.1", "--master-port", "29519" if mode == "fused" else "29520",
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "3", "--steps", "3", "--warmup", "3",
+           "--dist-backend", "gloo", "--no-cpu", "--no-e2e", "--mode", mode]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
     assert d["extraction"]["recovered_planted"] is True, d["extraction"]
-    assert "every rank extracts" in d["extraction"]["rule"]
+    assert ("cross-shard pass" if mode == "fused" else "after the exchange") in d["extraction"]["rule"]

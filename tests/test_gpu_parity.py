@@ -467,6 +467,24 @@ def test_sharded_fused_emulation(coracle, P):
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
+def test_sharded_fused_extraction_emulation(P):
+    """Extraction fused into the cross-shard pass (K6' + |W| >= tau) on P
+    buffers of one device equals a full transform + ordered extraction."""
+    p = P.bit_length() - 1
+    for nl in (14, 18, 21):
+        n = nl + p
+        tau = int(3.5 * 591 * 2 ** (n / 2))  # ~3.5 sigma of a transform of uniform +-1024: a few hits per 2^13
+        x = oracle_np.gen(2, 60 + n, [1 << 10], 0, 1 << n)
+        whole = dev(x)
+        bw.fwht_array(whole)
+        i2, v2 = bw.extract_ge(whole, tau, cap=1 << 18)
+        shards = [dev(c) for c in np.split(x, P)]
+        i1, v1 = sharded.fwht_shards_extract_ge(shards, tau, cap=1 << 18)
+        assert torch.equal(torch.cat(shards), whole), (P, nl)
+        assert i1.numel() > 0 and torch.equal(i1, i2) and torch.equal(v1, v2), (P, nl, i1.numel(), i2.numel())
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
 def test_sharded_narrow_emulation(coracle, P):
     """Narrow-wire exchange (int8 cross stages first, then widening local
     transforms) on P buffers of one device: +-1 signals, values at the wire
