@@ -361,3 +361,22 @@ def test_random_plans_check_and_emulate(coracle):
             ref = x.copy()
             coracle.oracle_fwht_i64(ref.ctypes.data, n)
             assert np.array_equal(emulate(x, plan), ref), plan
+
+
+def test_host_batch_validation_host_side():
+    import paper_1607_01039_b200 as bw
+
+    assert bw.fwht_arrays([]) == []
+    with pytest.raises(errors.BadArguments):
+        bw.fwht_arrays([np.zeros(8, dtype=np.float64)])
+    with pytest.raises(errors.BadArguments):
+        bw.fwht_arrays([np.zeros(8, dtype=np.int64), np.zeros(16, dtype=np.int64)])
+    with pytest.raises(errors.BadArguments):
+        bw.fwht_arrays([np.zeros(6, dtype=np.int64)])
+    with pytest.raises(errors.BadArguments):
+        bw.fwht_arrays([np.zeros((4, 4), dtype=np.int64)[:, 0]])  # not contiguous
+    L = _lib.lib()
+    with pytest.raises(errors.BadArguments):
+        _lib.check(L.bw_fwht_host_batch_i64(None, 2, 10, None, None, None, None))
+    with pytest.raises(errors.BadArguments):
+        _lib.check(L.bw_fwht_xfused_pass_extract_i64(None, 1, 20, 5, 0, 10, 0, None, None, 16, None, None))
