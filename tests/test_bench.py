@@ -86,3 +86,11 @@ def test_multirank_extraction_config3_two_processes_one_gpu(mode):
     d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
     assert d["extraction"]["recovered_planted"] is True, d["extraction"]
     assert ("cross-shard pass" if mode == "fused" else "after the exchange") in d["extraction"]["rule"]
+
+
+@pytest.mark.gpu
+def test_narrow_intermediates_bench_leg():
+    d = run_bench(["--steps", "3", "--warmup", "3", "--log2n", "26", "--no-cpu", "--no-e2e",
+                   "--intermediates", "narrow"])
+    assert d["config"]["narrow_fallbacks"] == 0 and d["config"]["algorithmic_bytes_per_point"] == [10, 6, 12]
+    assert d["roofline"]["kernel"].startswith("narrow pass") and "flag_readback_ms" in d
