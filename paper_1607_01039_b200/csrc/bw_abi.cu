@@ -662,13 +662,13 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractA
             if (ex.count) return launch_cfg<C>(bw::k_pass_split<C, L, true>, grid, s, d, p.karg(), ex, tab);
             return launch_cfg<C>(bw::k_pass_split<C, L, false>, grid, s, d, p.karg(), ex, tab);
         } else {
-        if constexpr (kLow) {
-            if (src && src_bytes == 4) return launch_cfg<C>(bw::k_pass<C, L, false, 4>, grid, s, d, p.k, ex, src);
-            if (src && src_bytes == 2) return launch_cfg<C>(bw::k_pass<C, L, false, 2>, grid, s, d, p.k, ex, src);
-            if (src) return launch_cfg<C>(bw::k_pass<C, L, false, 1>, grid, s, d, p.k, ex, src);
-        }
-        if (ex.count) return launch_cfg<C>(bw::k_pass<C, L, true>, grid, s, d, p.k, ex, none);
-        return launch_cfg<C>(bw::k_pass<C, L, false>, grid, s, d, p.k, ex, none);
+            if constexpr (kLow) {
+                if (src && src_bytes == 4) return launch_cfg<C>(bw::k_pass<C, L, false, 4>, grid, s, d, p.k, ex, src);
+                if (src && src_bytes == 2) return launch_cfg<C>(bw::k_pass<C, L, false, 2>, grid, s, d, p.k, ex, src);
+                if (src) return launch_cfg<C>(bw::k_pass<C, L, false, 1>, grid, s, d, p.k, ex, src);
+            }
+            if (ex.count) return launch_cfg<C>(bw::k_pass<C, L, true>, grid, s, d, p.k, ex, none);
+            return launch_cfg<C>(bw::k_pass<C, L, false>, grid, s, d, p.k, ex, none);
         }
     });
 }
