@@ -211,6 +211,7 @@ def run_ours(a):
     import torch.distributed as dist
 
     from paper_1607_01039_b200 import _lib, sharded, signals
+    from paper_1607_01039_b200.errors import BigWHTError
 
     ws, rank, local_rank = world()
     torch.cuda.set_device(local_rank % torch.cuda.device_count())
@@ -284,7 +285,14 @@ def run_ours(a):
     ptr = x.data_ptr()
     peer = None
     if p > 0:
-        peer = sharded._PeerMap(x, None, dist) if any(m in ("peer", "fused", "narrow") for m in candidates) else None
+        if any(m in ("peer", "fused", "narrow") for m in candidates):
+            try:
+                peer = sharded._PeerMap(x, None, dist)
+            except BigWHTError as e:  # no CUDA IPC between these ranks: the NCCL all-to-all exchange only
+                if a.dist_backend != "nccl":
+                    raise
+                print(f"rank {rank}: peer exchanges unavailable ({e}); using all-to-all", file=sys.stderr)
+                candidates = ["a2a"]
         ones = torch.ones(1, device="cuda")
         ptrs = (ctypes.c_void_p * ws)(*(peer.ptrs if peer else [ptr] * ws))
         b, c = sharded.slice_of(rank, ws, 1 << nl)

@@ -49,7 +49,7 @@ import torch
 
 from . import _lib
 from .core import _is_power_of_two, _stream_handle, fwht_array
-from .errors import BadArguments, InvalidWorkerCount
+from .errors import BadArguments, BigWHTError, DeviceError, InvalidWorkerCount
 
 
 def log2_shards(p_count: int) -> int:
@@ -305,27 +305,46 @@ class CudaBackend:
 
 
 class _PeerMap:
-    """CUDA IPC mapping of every rank's shard into this process."""
+    """CUDA IPC mapping of every rank's shard into this process.  Collective:
+    when any rank cannot export or map a shard (no IPC for the allocation, no
+    peer access), every rank raises DeviceError, so callers can fall back
+    together (bench.py drops to the NCCL all-to-all exchange)."""
 
     def __init__(self, local: torch.Tensor, group, dist):
         L = _lib.lib()
         handle = (ctypes.c_char * 64)()
         off = ctypes.c_uint64(0)
-        _lib.check(L.bw_ipc_get_handle(local.data_ptr(), handle, ctypes.byref(off)))
-        mine = (bytes(handle), int(off.value))
+        try:
+            _lib.check(L.bw_ipc_get_handle(local.data_ptr(), handle, ctypes.byref(off)))
+            mine = (bytes(handle), int(off.value))
+        except BigWHTError as e:
+            mine = ("error", str(e))
         world = dist.get_world_size(group)
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
+        bad = [r for r, h in enumerate(allh) if h[0] == "error"]
+        if bad:
+            raise DeviceError(f"CUDA IPC export failed on rank(s) {bad}: {allh[bad[0]][1]}")
         self.rank = dist.get_rank(group)
         self.ptrs, self.opened = [], []
+        err = None
         for r, (h, o) in enumerate(allh):
             if r == self.rank:
                 self.ptrs.append(local.data_ptr())
                 continue
             ptr = ctypes.c_void_p(0)
-            _lib.check(L.bw_ipc_open_handle(h, o, ctypes.byref(ptr)))
+            try:
+                _lib.check(L.bw_ipc_open_handle(h, o, ctypes.byref(ptr)))
+            except BigWHTError as e:
+                err = str(e)
+                break
             self.ptrs.append(ptr.value)
             self.opened.append((ptr.value, o))
+        errs = [None] * world
+        dist.all_gather_object(errs, err, group=group)
+        if any(e is not None for e in errs):
+            self.close()
+            raise DeviceError(f"CUDA IPC mapping failed: {next(e for e in errs if e is not None)}")
 
     def close(self):
         for ptr, o in self.opened:
