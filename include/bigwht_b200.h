@@ -214,14 +214,15 @@ int bw_fwht_host_i64(int64_t *host, int log2n, int64_t *work_dev,
 
 /*
  * A batch of host signals (fwht_array on each, core.py:97-117), bit-identical
- * to bw_fwht_host_i64 per signal.  The signals alternate between two device
- * buffers of 2^log2n int64 (work0 != work1 when count > 1), so signal
- * i+1's host->device copy overlaps signal i's device->host copy: PCIe runs
- * full duplex, which one signal alone cannot use.  A buffer listed twice in
- * a row is processed in order.  Synchronous.
+ * to bw_fwht_host_i64 per signal.  The signals rotate over nwork (1-4)
+ * distinct device buffers of 2^log2n int64, so signal i+1's host->device
+ * copy overlaps signal i's device->host copy: PCIe runs full duplex, which
+ * one signal alone cannot use.  With three buffers the next H2D never waits
+ * for a D2H.  A buffer listed twice in a row is processed in order.
+ * Synchronous.
  */
-int bw_fwht_host_batch_i64(int64_t *const *host, int count, int log2n, int64_t *work0,
-                           int64_t *work1, void *stream, uint64_t *butterflies);
+int bw_fwht_host_batch_i64(int64_t *const *host, int count, int log2n, int64_t *const *work,
+                           int nwork, void *stream, uint64_t *butterflies);
 
 /*
  * Out-of-core transform of a HOST array larger than the device workspace --

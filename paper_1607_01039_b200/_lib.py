@@ -67,7 +67,7 @@ _SIGNATURES = {
     "bw_check_bound_i64": ([P, I32, P, P, PU64], I32),
     "bw_fwht_inplace_i64": ([P, I32, P, P, PU64], I32),
     "bw_fwht_host_i64": ([P, I32, P, I32, P, PU64], I32),
-    "bw_fwht_host_batch_i64": ([ctypes.POINTER(P), I32, I32, P, P, P, PU64], I32),
+    "bw_fwht_host_batch_i64": ([ctypes.POINTER(P), I32, I32, ctypes.POINTER(P), I32, P, PU64], I32),
     "bw_fwht_host_ooc_i64": ([P, I32, P, I32, P, ctypes.POINTER(I32)], I32),
     "bw_inverse_i64": ([P, I32, P, P], I32),
     "bw_inverse_f64": ([P, I32, P], I32),

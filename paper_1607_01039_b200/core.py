@@ -294,12 +294,22 @@ def fwht_arrays(buffers) -> list[int]:
     if any(b.shape != bufs[0].shape for b in bufs):
         raise BadArguments("fwht_arrays needs buffers of one length")
     _need_cuda()
-    w0 = _HostStage.get(n, torch.int64)
-    w1 = _HostStage.get(n, torch.int64, slot=1) if len(bufs) > 1 else w0
+    # two device buffers: the steady state then runs at the PCIe duplex rate
+    # (~49 GB/s each way, tools/pcie_duplex.py); a third (BW_BATCH_BUFFERS=3)
+    # measured no faster (profiles/r01_e2e_buffers.log)
+    nwork = 1 if len(bufs) == 1 else 2
+    if len(bufs) > 2 and os.environ.get("BW_BATCH_BUFFERS", "2") == "3":
+        free, _ = torch.cuda.mem_get_info()
+        have = sum(w.numel() * 8 for k, w in getattr(_HostStage._local, "work", {}).items()
+                   if k[:2] == (torch.cuda.current_device(), torch.int64) and w.numel() >= (1 << n))
+        if (8 << n) * 3 - have + (2 << 30) <= free:
+            nwork = 3
+    works = [_HostStage.get(n, torch.int64, slot=b) for b in range(nwork)]
     arr = (ctypes.c_void_p * len(bufs))(*[b.ctypes.data for b in bufs])
+    warr = (ctypes.c_void_p * nwork)(*[w.data_ptr() for w in works])
     bf = ctypes.c_uint64(0)
-    _lib.check(_lib.lib().bw_fwht_host_batch_i64(arr, len(bufs), n, w0.data_ptr(), w1.data_ptr(),
-                                                 _stream_handle(w0), ctypes.byref(bf)))
+    _lib.check(_lib.lib().bw_fwht_host_batch_i64(arr, len(bufs), n, warr, nwork, _stream_handle(works[0]),
+                                                 ctypes.byref(bf)))
     return [int(bf.value)] * len(bufs)
 
 

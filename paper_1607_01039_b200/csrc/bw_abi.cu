@@ -1470,23 +1470,29 @@ int bw_fwht_host_i64(int64_t* host, int log2n, int64_t* work_dev, int check_boun
 }
 
 // A batch of host signals, each transformed like bw_fwht_host_i64: the
-// signals alternate between two device buffers, so signal i+1's H2D runs
+// signals rotate over nwork device buffers, so signal i+1's H2D runs
 // while signal i's D2H runs (PCIe is full duplex; one signal alone cannot
 // overlap them, since no output is final before every input has arrived).
 // H2D, transforms and D2H run on three streams ordered by events.  A host
 // buffer listed twice in a row is processed in order (its second H2D waits
 // for the first D2H), so the list behaves like fwht_array on each entry.
-int bw_fwht_host_batch_i64(int64_t* const* host, int count, int log2n, int64_t* work0, int64_t* work1,
+int bw_fwht_host_batch_i64(int64_t* const* host, int count, int log2n, int64_t* const* work, int nwork,
                            void* stream, uint64_t* butterflies) {
     if (!host || count < 0) return fail(BW_BAD_ARGUMENTS, "bad host signal list");
     for (int i = 0; i < count; ++i)
         if (!host[i]) return fail(BW_BAD_ARGUMENTS, "null host signal %d", i);
-    BW_TRY(check_signal(work0, log2n));
-    if (count > 1) BW_TRY(check_signal(work1, log2n));
+    if (!work || nwork < 1 || nwork > 4) return fail(BW_BAD_ARGUMENTS, "1 to 4 device work buffers");
+    for (int b = 0; b < nwork; ++b) {
+        BW_TRY(check_signal(work[b], log2n));
+        for (int c = 0; c < b; ++c)
+            if (work[c] == work[b]) return fail(BW_BAD_ARGUMENTS, "the device work buffers must differ");
+    }
     if (butterflies) *butterflies = butterfly_count(log2n);
     if (count == 0) return BW_OK;
-    if (count == 1) return bw_fwht_host_i64(host[0], log2n, work0, 0, stream, butterflies);
-    if (work0 == work1) return fail(BW_BAD_ARGUMENTS, "the two device buffers must differ");
+    if (count == 1 || nwork == 1) {
+        for (int i = 0; i < count; ++i) BW_TRY(bw_fwht_host_i64(host[i], log2n, work[0], 0, stream, nullptr));
+        return BW_OK;
+    }
     int dev = 0;
     BW_TRY(device_setup(&dev));
     cudaStream_t s = as_stream(stream);
@@ -1497,10 +1503,10 @@ int bw_fwht_host_batch_i64(int64_t* const* host, int count, int log2n, int64_t* 
     }
     cudaStream_t up = g_copy_stream[dev], down = g_d2h_stream[dev];
     const size_t bytes = (size_t)8 << log2n;
-    int64_t* work[2] = {work0, work1};
-    cudaEvent_t start, loaded[2], done[2], freed[2];
+    const int nb = nwork;
+    cudaEvent_t start, loaded[4], done[4], freed[4];
     BW_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < nb; ++b) {
         BW_CUDA(cudaEventCreateWithFlags(&loaded[b], cudaEventDisableTiming));
         BW_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
         BW_CUDA(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
@@ -1509,12 +1515,12 @@ int bw_fwht_host_batch_i64(int64_t* const* host, int count, int log2n, int64_t* 
         BW_CUDA(cudaEventRecord(start, s));  // the copies follow earlier work on the caller's stream
         BW_CUDA(cudaStreamWaitEvent(up, start, 0));
         for (int i = 0; i < count; ++i) {
-            const int b = i & 1;
-            if (i >= 2) BW_CUDA(cudaStreamWaitEvent(up, freed[b], 0));  // signal i-2's D2H left this buffer
+            const int b = i % nb;
+            if (i >= nb) BW_CUDA(cudaStreamWaitEvent(up, freed[b], 0));  // signal i-nb's D2H left this buffer
             const char* hi = reinterpret_cast<const char*>(host[i]);
             const char* hp = reinterpret_cast<const char*>(host[i - (i > 0)]);
             if (i > 0 && hi < hp + bytes && hp < hi + bytes)  // the same host memory twice in a row: in order
-                BW_CUDA(cudaStreamWaitEvent(up, freed[b ^ 1], 0));
+                BW_CUDA(cudaStreamWaitEvent(up, freed[(i - 1) % nb], 0));
             BW_CUDA(cudaMemcpyAsync(work[b], host[i], bytes, cudaMemcpyHostToDevice, up));
             BW_CUDA(cudaEventRecord(loaded[b], up));
             BW_CUDA(cudaStreamWaitEvent(s, loaded[b], 0));
@@ -1524,13 +1530,12 @@ int bw_fwht_host_batch_i64(int64_t* const* host, int count, int log2n, int64_t* 
             BW_CUDA(cudaMemcpyAsync(host[i], work[b], bytes, cudaMemcpyDeviceToHost, down));
             BW_CUDA(cudaEventRecord(freed[b], down));
         }
-        BW_CUDA(cudaStreamWaitEvent(s, freed[(count - 1) & 1], 0));
-        BW_CUDA(cudaStreamWaitEvent(s, freed[count & 1], 0));
+        for (int b = 0; b < nb && b < count; ++b) BW_CUDA(cudaStreamWaitEvent(s, freed[b], 0));
         return BW_OK;
     }();
     BW_CUDA(cudaStreamSynchronize(s));
     cudaEventDestroy(start);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < nb; ++b) {
         cudaEventDestroy(loaded[b]);
         cudaEventDestroy(done[b]);
         cudaEventDestroy(freed[b]);

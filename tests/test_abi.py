@@ -377,6 +377,6 @@ def test_host_batch_validation_host_side():
         bw.fwht_arrays([np.zeros((4, 4), dtype=np.int64)[:, 0]])  # not contiguous
     L = _lib.lib()
     with pytest.raises(errors.BadArguments):
-        _lib.check(L.bw_fwht_host_batch_i64(None, 2, 10, None, None, None, None))
+        _lib.check(L.bw_fwht_host_batch_i64(None, 2, 10, None, 2, None, None))
     with pytest.raises(errors.BadArguments):
         _lib.check(L.bw_fwht_xfused_pass_extract_i64(None, 1, 20, 5, 0, 10, 0, None, None, 16, None, None))
