@@ -69,8 +69,8 @@ const bool g_two_pass = !(getenv("BW_TWO_PASS") && getenv("BW_TWO_PASS")[0] == '
 // BW_NARROW_TPC=1|2|4: tiles per CTA (or cluster) of the narrow plan's high passes (default 2,
 // measured best: n = 32 in 30.4 ms against 31.6 with one tile; four spill).
 const int g_narrow_tpc = getenv("BW_NARROW_TPC") ? atoi(getenv("BW_NARROW_TPC")) : 2;
-// BW_FOLD_BLOCKS=0 keeps the L2-atomic fold for d_out > 14 (A/B knob).
-const bool g_fold_blocks = !(getenv("BW_FOLD_BLOCKS") && getenv("BW_FOLD_BLOCKS")[0] == '0');
+// BW_FOLD_BLOCKS=0 keeps the shared-bin / L2-atomic fold for d_out > 12 (A/B knob, read per call).
+bool fold_blocks_enabled() { return !(getenv("BW_FOLD_BLOCKS") && getenv("BW_FOLD_BLOCKS")[0] == '0'); }
 // BW_SPLIT_PLANS=0 keeps the default planner to one-run high passes (A/B knob).
 const bool g_split_plans = !(getenv("BW_SPLIT_PLANS") && getenv("BW_SPLIT_PLANS")[0] == '0');
 // BW_HOST_PIPELINE=0 disables the copy/compute overlap of host-buffer transforms (A/B knob).
@@ -1856,7 +1856,7 @@ static int fold_impl(const int64_t* x, int d_in, const uint64_t* col_masks, int 
     const int grid = grid_for(dev, count, 256, 8);
     unsigned long long* out = reinterpret_cast<unsigned long long*>(out_dev);
     FoldBlockPlan fp;
-    if (d_out > bw::kFoldBlockBits && g_fold_blocks && fold_block_plan(col_masks, d_in, d_out, &fp)) {
+    if (d_out > bw::kFoldBlockBits && fold_blocks_enabled() && fold_block_plan(col_masks, d_in, d_out, &fp)) {
         const int nb = (int)fp.bval.size();
         int nsplit = (8 * g_num_sms[dev] + nb - 1) / nb;  // ~8 CTAs per SM over the run
         if ((uint64_t)nsplit > fp.nchunk) nsplit = (int)fp.nchunk;
