@@ -1765,28 +1765,51 @@ uint64_t apply_cols(const std::vector<uint64_t>& col, uint64_t v) {
 }
 }  // namespace gf2
 
-// Plan of the block fold (k_fold_blocks) for d_out > kFoldBlockBits; false when the low
-// kFoldBlockBits columns of L are dependent (then the L2-atomic fold runs).
+// Plan of the block fold (k_fold_blocks) for d_out > kFoldBlockBits.  When
+// the low kFoldBlockBits columns of L are dependent, points of one chunk can
+// share a bin: the plan then carries the chunk's bin table (gtab) and the
+// kernel accumulates with shared-memory atomics (inj = false).
 struct FoldBlockPlan {
     std::vector<uint64_t> h0;
     std::vector<unsigned> bval;
     std::vector<unsigned long long> kap;
-    std::vector<unsigned> ftop, bmap;
+    std::vector<unsigned> ftop, bmap, gtab;  // gtab: in-block bin of chunk point e (dependent low columns)
     uint64_t nchunk = 0;
+    bool inj = true;  // the low K columns of L are independent
 };
 
 static bool fold_block_plan(const uint64_t* cols, int d_in, int d_out, FoldBlockPlan* fp) {
     constexpr int K = bw::kFoldBlockBits;
     if (d_out <= K || d_in - K > 32 || d_out > 30) return false;
+    // B = [the independent low columns (of 0..K-1) | unit vectors completing a
+    // basis]; A = B^-1 maps every low column into the first K coordinates
     gf2::Basis low;
+    std::vector<uint64_t> B;
     for (int i = 0; i < K; ++i)
-        if (!low.insert(cols[i], 0)) return false;
-    // B = [cols 0..K-1 | unit vectors completing a basis]; A = B^-1
-    std::vector<uint64_t> B(cols, cols + K);
+        if (low.insert(cols[i], 0)) B.push_back(cols[i]);
+    fp->inj = (int)B.size() == K;
     for (int r = 0; r < d_out && (int)B.size() < d_out; ++r)
         if (low.insert(1ull << r, 0)) B.push_back(1ull << r);
     if ((int)B.size() != d_out) return false;
     const std::vector<uint64_t> A = gf2::inverse_cols(B, d_out);
+    fp->gtab.clear();
+    // Shared-memory atomics (no barrier per chunk) measured faster than the
+    // race-free plain adds even when the chunk is injective: 2^32 -> 2^20 in
+    // 5.4 vs 6.8 ms (profiles/r01_fold_atomic_ab.log).  BW_FOLD_PLAIN=1 keeps
+    // the plain adds where they are race-free (A/B knob).
+    if (!(getenv("BW_FOLD_PLAIN") && getenv("BW_FOLD_PLAIN")[0] == '1')) fp->inj = false;
+    if (!fp->inj) {
+        std::vector<uint64_t> g(K);
+        for (int i = 0; i < K; ++i) {
+            g[i] = gf2::apply_cols(A, cols[i]);
+            if (g[i] >> K) return false;  // (cannot happen: spans of the independent low columns)
+        }
+        fp->gtab.assign((size_t)1 << K, 0u);
+        for (uint32_t e = 1; e < (1u << K); ++e) {
+            const int lowbit = __builtin_ctz(e);
+            fp->gtab[e] = fp->gtab[e & (e - 1)] ^ (unsigned)g[lowbit];
+        }
+    }
     const int M = d_in - K;
     std::vector<uint64_t> ftop(M), fbot(M);
     for (int m = 0; m < M; ++m) {
@@ -1861,7 +1884,7 @@ static int fold_impl(const int64_t* x, int d_in, const uint64_t* col_masks, int 
         int nsplit = (8 * g_num_sms[dev] + nb - 1) / nb;  // ~8 CTAs per SM over the run
         if ((uint64_t)nsplit > fp.nchunk) nsplit = (int)fp.nchunk;
         if (nsplit < 1) nsplit = 1;
-        const size_t tb = 8 * fp.h0.size() + 4 * fp.bval.size() + 8 * 1024 + 4 * 1024 * 2;
+        const size_t tb = 8 * fp.h0.size() + 4 * fp.bval.size() + 8 * 1024 + 4 * 1024 * 2 + 4 * fp.gtab.size();
         void* sc2 = nullptr;
         BW_TRY(scratch(dev, 4096 + tab.size() * 4 + tb + 64, &sc2));
         char* q = reinterpret_cast<char*>(sc2) + 4096 + ((tab.size() * 4 + 15) & ~size_t(15));
@@ -1875,6 +1898,8 @@ static int fold_impl(const int64_t* x, int d_in, const uint64_t* col_masks, int 
         BW_CUDA(cudaMemcpyAsync(dftop, fp.ftop.data(), 4 * 1024, cudaMemcpyHostToDevice, s));
         BW_CUDA(cudaMemcpyAsync(dbmap, fp.bmap.data(), 4 * 1024, cudaMemcpyHostToDevice, s));
         BW_CUDA(cudaMemcpyAsync(dbval, fp.bval.data(), 4 * fp.bval.size(), cudaMemcpyHostToDevice, s));
+        unsigned* dgtab = dbval + fp.bval.size();
+        if (!fp.inj) BW_CUDA(cudaMemcpyAsync(dgtab, fp.gtab.data(), 4 * fp.gtab.size(), cudaMemcpyHostToDevice, s));
         bw::FoldBlockArgs fa;
         fa.x = reinterpret_cast<const long long*>(x);
         fa.g = g;
@@ -1884,11 +1909,18 @@ static int fold_impl(const int64_t* x, int d_in, const uint64_t* col_masks, int 
         fa.kap = dkap;
         fa.ftop = dftop;
         fa.bmap = dbmap;
+        fa.gtab = dgtab;
         fa.nsplit = nsplit;
         fa.nchunk = fp.nchunk;
         constexpr size_t smem = (8 << bw::kFoldBlockBits) + 8 * 1024 + 4 * 1024 * 2;
-        BW_CUDA(cudaFuncSetAttribute(bw::k_fold_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        bw::k_fold_blocks<<<nb * nsplit, bw::kFoldThreads, smem, s>>>(fa);
+        if (fp.inj) {
+            BW_CUDA(cudaFuncSetAttribute(bw::k_fold_blocks<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            bw::k_fold_blocks<true><<<nb * nsplit, bw::kFoldThreads, smem, s>>>(fa);
+        } else {
+            constexpr size_t smem2 = smem + (4 << bw::kFoldBlockBits);
+            BW_CUDA(cudaFuncSetAttribute(bw::k_fold_blocks<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+            bw::k_fold_blocks<false><<<nb * nsplit, bw::kFoldThreads, smem2, s>>>(fa);
+        }
         BW_LAUNCHED("k_fold_blocks launch");
         BW_CUDA(cudaStreamSynchronize(s));  // the tables live in shared scratch
         return BW_OK;

@@ -1444,23 +1444,36 @@ struct FoldBlockArgs {
     const unsigned long long* kap;  // [4][256] XOR of kernel vectors by 8-bit groups of the chunk counter
     const unsigned* ftop;           // [4][256] c(h) by 8-bit groups of h
     const unsigned* bmap;           // [4][256] A^-1 u by 8-bit groups of u
+    const unsigned* gtab;           // !INJ: in-block bin of chunk point e (2^K entries)
     int nsplit;                     // CTAs per block
     uint64_t nchunk;                // chunks per block
 };
 
+// !INJ (the default): bin = gtab[e] ^ c, the bins are 32-bit low / high
+// words updated with native shared atomics and an exact carry, like
+// k_fold's shared bins -- correct for any L (also dependent low columns,
+// where points of one chunk share bins) and needs no barrier per chunk.
+// INJ (BW_FOLD_PLAIN=1, independent low columns): a chunk's points land on
+// distinct bins e ^ c, plain adds, one barrier per chunk (measured slower).
+template <bool INJ>
 __global__ void __launch_bounds__(kFoldThreads, 1024 / kFoldThreads) k_fold_blocks(FoldBlockArgs a) {
     extern __shared__ unsigned long long fsm[];
     constexpr int B = 1 << kFoldBlockBits;
     unsigned long long* acc = fsm;
+    unsigned* lo = reinterpret_cast<unsigned*>(fsm);
+    unsigned* hi = lo + B;
     unsigned long long* kap = fsm + B;
     unsigned* ftop = reinterpret_cast<unsigned*>(kap + 1024);
     unsigned* bmap = ftop + 1024;
+    unsigned* gtab = bmap + 1024;  // !INJ only
     const int bi = blockIdx.x / a.nsplit, sp = blockIdx.x % a.nsplit;
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
         kap[i] = a.kap[i];
         ftop[i] = a.ftop[i];
         bmap[i] = a.bmap[i];
     }
+    if constexpr (!INJ)
+        for (int i = threadIdx.x; i < B; i += blockDim.x) gtab[i] = a.gtab[i];
     for (int i = threadIdx.x; i < B; i += blockDim.x) acc[i] = 0ull;
     __syncthreads();
     const uint64_t q0 = a.nchunk * sp / a.nsplit, q1 = a.nchunk * (sp + 1) / a.nsplit;
@@ -1494,17 +1507,31 @@ __global__ void __launch_bounds__(kFoldThreads, 1024 / kFoldThreads) k_fold_bloc
         if (q + 1 < q1) load(chunk_of(q + 1), nxt);  // the next chunk's loads fly over this chunk's adds
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
-            const uint32_t p = (2u * threadIdx.x + 2u * kFoldThreads * i) ^ c;  // e ^ c; e + 1 lands on p ^ 1
-            acc[p] += cur[i].x;
-            acc[p ^ 1u] += cur[i].y;
+            const uint32_t e = 2u * threadIdx.x + 2u * kFoldThreads * i;
+            if constexpr (INJ) {
+                const uint32_t p = e ^ c;  // e + 1 lands on p ^ 1
+                acc[p] += cur[i].x;
+                acc[p ^ 1u] += cur[i].y;
+            } else {
+                const unsigned long long vv[2] = {cur[i].x, cur[i].y};
+#pragma unroll
+                for (int w = 0; w < 2; ++w) {
+                    const uint32_t t = gtab[e + w] ^ c;
+                    const unsigned vl = (unsigned)vv[w], vh = (unsigned)(vv[w] >> 32);
+                    const unsigned old = atomicAdd(&lo[t], vl);
+                    const unsigned carry = (old + vl) < old ? 1u : 0u;
+                    if (vh + carry) atomicAdd(&hi[t], vh + carry);
+                }
+            }
         }
-        __syncthreads();  // the next chunk's permutation differs: its bins may be another thread's
+        if constexpr (INJ) __syncthreads();  // the next chunk's permutation differs: its bins may be another thread's
 #pragma unroll
         for (int i = 0; i < PER; ++i) cur[i] = nxt[i];
     }
     const unsigned b = a.bval[bi];
+    if constexpr (!INJ) __syncthreads();
     for (int i = threadIdx.x; i < B; i += blockDim.x) {
-        const unsigned long long v = acc[i];
+        const unsigned long long v = INJ ? acc[i] : ((unsigned long long)hi[i] << 32) | lo[i];
         if (!v) continue;
         const uint32_t u = (uint32_t)i | (b << kFoldBlockBits);
         const uint32_t t = bmap[u & 255] ^ bmap[256 + ((u >> 8) & 255)] ^ bmap[512 + ((u >> 16) & 255)] ^

@@ -671,16 +671,21 @@ def test_fold_matches_reference(golden_npz, coracle):
 def test_fold_blocks_large_outputs(coracle, monkeypatch):
     """d_out > 14: the block fold (change of output basis, one 2^14-bin block
     per CTA in shared memory, chunks streamed without atomics) equals the
-    oracle for resident and generated inputs; an L whose low 14 columns are
-    dependent takes the L2-atomic fold, and BW_FOLD_BLOCKS=0 forces it."""
+    oracle for resident and generated inputs, also when L's low columns are
+    dependent (shared-memory atomics); BW_FOLD_BLOCKS=0 forces the shared-bin
+    / L2-atomic fold."""
     from paper_1607_01039_b200 import subspace
 
-    cases = [(20, 15, 1), (22, 16, 2), (24, 20, 5), (23, 22, 1), (26, 18, 3)]
+    cases = [(20, 15, 1), (22, 16, 2), (24, 20, 5), (23, 22, 1), (26, 18, 3), (25, 16, 2)]
     for n, d_out, idx in cases:
         spec = signals.config(idx, n)
         rows = subspace.random_full_rank(n, d_out, 100 + n)
         if n == 26:  # dependent low columns: column 5 = column 3 ^ column 4 (still rank 18)
             rows[:, 5] = rows[:, 3] ^ rows[:, 4]
+            assert subspace.gf2_rank(rows) == d_out
+        if n == 25:  # a zero low column and a repeated one: chunk points share bins
+            rows[:, 2] = 0
+            rows[:, 9] = rows[:, 0]
             assert subspace.gf2_rank(rows) == d_out
         want = np.empty(1 << d_out, dtype=np.int64)
         cols = oracle_np.column_masks(rows).astype(np.uint64)

@@ -37,6 +37,15 @@ for d_out in (12, 14, 16, 20, 24):
           f"{8 * (1 << n) / ms / 1e6:.1f} GB/s read", flush=True)
     msg = timed(lambda: subspace.fold_generated(spec, rows))
     print(f"fold generated n={n} -> d_out={d_out}: {msg:.3f} ms, {(1 << n) / (msg / 1e3):.3e} points/s", flush=True)
+rows = subspace.random_full_rank(n, 20, 7)
+x.copy_(signals.make(signals.config(2, n)))  # wide values: the shared atomics' high words work too
+ms = timed(lambda: subspace.fold(sig, rows))
+print(f"fold resident n={n} (config 2 values) -> d_out=20: {ms:.3f} ms, {(1 << n) / (ms / 1e3):.3e} points/s",
+      flush=True)
+rows[:, 3] = rows[:, 1] ^ rows[:, 2]  # dependent low columns: the block fold with shared atomics
+ms = timed(lambda: subspace.fold(sig, rows))
+print(f"fold resident n={n} -> d_out=20, dependent low columns: {ms:.3f} ms, {(1 << n) / (ms / 1e3):.3e} points/s",
+      flush=True)
 del x, sig
 torch.cuda.empty_cache()
 if n < 34:
