@@ -1780,7 +1780,7 @@ struct FoldBlockPlan {
 
 static bool fold_block_plan(const uint64_t* cols, int d_in, int d_out, FoldBlockPlan* fp) {
     constexpr int K = bw::kFoldBlockBits;
-    if (d_out <= K || d_in - K > 32 || d_out > 30) return false;
+    if (d_out < 8 || d_in <= K || d_in - K > 32 || d_out > 30) return false;
     // B = [the independent low columns (of 0..K-1) | unit vectors completing a
     // basis]; A = B^-1 maps every low column into the first K coordinates
     gf2::Basis low;
@@ -1879,9 +1879,10 @@ static int fold_impl(const int64_t* x, int d_in, const uint64_t* col_masks, int 
     const int grid = grid_for(dev, count, 256, 8);
     unsigned long long* out = reinterpret_cast<unsigned long long*>(out_dev);
     FoldBlockPlan fp;
-    if (d_out > bw::kFoldBlockBits && fold_blocks_enabled() && fold_block_plan(col_masks, d_in, d_out, &fp)) {
+    if (fold_blocks_enabled() && fold_block_plan(col_masks, d_in, d_out, &fp)) {
         const int nb = (int)fp.bval.size();
         int nsplit = (8 * g_num_sms[dev] + nb - 1) / nb;  // ~8 CTAs per SM over the run
+        if (nb == 1) nsplit = 4 * g_num_sms[dev];  // one block (d_out <= 12): one wave, fewer flush atomics
         if ((uint64_t)nsplit > fp.nchunk) nsplit = (int)fp.nchunk;
         if (nsplit < 1) nsplit = 1;
         const size_t tb = 8 * fp.h0.size() + 4 * fp.bval.size() + 8 * 1024 + 4 * 1024 * 2 + 4 * fp.gtab.size();

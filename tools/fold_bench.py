@@ -30,7 +30,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 spec = signals.config(4, n)
 x = signals.make(spec)
 sig = Signal(x, Domain.TIME)
-for d_out in (12, 14, 16, 20, 24):
+for d_out in (8, 10, 12, 14, 16, 20, 24):
     rows = subspace.random_full_rank(n, d_out, 7)
     ms = timed(lambda: subspace.fold(sig, rows))
     print(f"fold resident n={n} -> d_out={d_out}: {ms:.3f} ms, {(1 << n) / (ms / 1e3):.3e} points/s, "
