@@ -424,7 +424,7 @@ def parseval_energy(sig: Signal):
     x = _device_copy(sig.data)
     if not sig.is_exact:
         return float(torch.dot(x, x).item())
-    nblocks = 592
+    nblocks = max(1, min(4096, x.numel() >> 16))  # contiguous ranges of >= 2^16 points per CTA
     part = torch.empty(3 * nblocks, dtype=torch.int64, device=x.device)
     with torch.cuda.device(x.device):
         _lib.check(_lib.lib().bw_sumsq_partials_i64(x.data_ptr(), x.numel(), part.data_ptr(), nblocks,

@@ -793,9 +793,11 @@ int fwht_high_bits(u64* d, int n, int lo, cudaStream_t s) {
 int minmax_impl(const int64_t* data, uint64_t count, int64_t* out, int dev, cudaStream_t s) {
     bw::k_minmax_init<<<1, 1, 0, s>>>(reinterpret_cast<long long*>(out));
     BW_LAUNCHED("k_minmax_init launch");
-    const int grid = grid_for(dev, (count + 1) / 2, 512 * 4, 4);
-    bw::k_minmax<<<grid, 512, 0, s>>>(reinterpret_cast<const long long*>(data), count,
-                                     reinterpret_cast<long long*>(out));
+    (void)dev;
+    const uint64_t grid = (count + (1ull << bw::kMinmaxChunkBits) - 1) >> bw::kMinmaxChunkBits;
+    if (grid == 0) return BW_OK;
+    bw::k_minmax<<<(unsigned)grid, 512, 0, s>>>(reinterpret_cast<const long long*>(data), count,
+                                               reinterpret_cast<long long*>(out));
     BW_LAUNCHED("k_minmax launch");
     return BW_OK;
 }

@@ -837,33 +837,29 @@ __global__ void k_minmax_init(long long* out) {
     out[1] = (long long)0x7FFFFFFFFFFFFFFFull;  // running min starts at INT64_MAX
 }
 
+// One CTA per contiguous 2^16-point chunk (like k_extract_count): enough
+// CTAs for every SM to keep loads in flight to the end.  (A grid-stride loop
+// over one wave of CTAs read at 2.5 TB/s, tools/aux_bench.py.)
+constexpr int kMinmaxChunkBits = 16;
 __global__ void __launch_bounds__(512) k_minmax(const long long* __restrict__ data, uint64_t count,
                                                 long long* out) {
     long long mx = (long long)0x8000000000000000ull, mn = (long long)0x7FFFFFFFFFFFFFFFull;
-    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t start = (uint64_t)blockIdx.x << kMinmaxChunkBits;
+    const uint64_t end = min(count, start + (uint64_t)(1ull << kMinmaxChunkBits));
     const bool aligned = ((reinterpret_cast<uintptr_t>(data) & 15u) == 0);
-    uint64_t done = 0;
+    uint64_t done = start;
     if (aligned) {
-        const uint64_t pairs = count >> 1;
         const longlong2* p = reinterpret_cast<const longlong2*>(data);
-        uint64_t i = tid;
-        for (; i + 3 * nth < pairs; i += 4 * nth) {
-            longlong2 a = __ldcs(p + i), b = __ldcs(p + i + nth);
-            longlong2 c = __ldcs(p + i + 2 * nth), d = __ldcs(p + i + 3 * nth);
-            mx = max(mx, max(max(a.x, a.y), max(b.x, b.y)));
-            mx = max(mx, max(max(c.x, c.y), max(d.x, d.y)));
-            mn = min(mn, min(min(a.x, a.y), min(b.x, b.y)));
-            mn = min(mn, min(min(c.x, c.y), min(d.x, d.y)));
-        }
-        for (; i < pairs; i += nth) {
-            longlong2 a = __ldcs(p + i);
+        const uint64_t p0 = start >> 1, p1 = end >> 1;
+#pragma unroll 8
+        for (uint64_t i = p0 + threadIdx.x; i < p1; i += blockDim.x) {
+            const longlong2 a = __ldcs(p + i);
             mx = max(mx, max(a.x, a.y));
             mn = min(mn, min(a.x, a.y));
         }
-        done = pairs << 1;
+        done = p1 << 1;
     }
-    for (uint64_t i = done + tid; i < count; i += nth) {
+    for (uint64_t i = done + threadIdx.x; i < end; i += blockDim.x) {
         const long long a = data[i];
         mx = max(mx, a);
         mn = min(mn, a);
@@ -1300,18 +1296,33 @@ __global__ void __launch_bounds__(256) k_bruteforce(const long long* __restrict_
 
 // parseval_energy (core.py:176-185), exact for int64: every thread sums x^2
 // as a 192-bit integer (x^2 < 2^127), blocks write (lo, hi, top) partials.
+// CTA b sums the contiguous range [b * chunk, (b + 1) * chunk) with 16-byte
+// loads (contiguous ranges over many CTAs: every SM keeps loads in flight).
 __global__ void __launch_bounds__(256) k_sumsq(const long long* __restrict__ x, uint64_t count,
                                                unsigned long long* partial) {
     unsigned __int128 acc = 0;
     unsigned long long top = 0;
-    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += nth) {
-        const long long v = x[i];
+    const uint64_t chunk = ((count + gridDim.x - 1) / gridDim.x + 1) & ~1ull;  // even
+    const uint64_t start = min(count, (uint64_t)blockIdx.x * chunk), end = min(count, start + chunk);
+    auto add = [&](long long v) {
         const unsigned long long a = v < 0 ? 0ull - (unsigned long long)v : (unsigned long long)v;
         const unsigned __int128 sq = (unsigned __int128)a * a;
         acc += sq;
         top += acc < sq;
+    };
+    uint64_t done = start;
+    if ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
+        const longlong2* p = reinterpret_cast<const longlong2*>(x);
+#pragma unroll 4
+        for (uint64_t i = (start >> 1) + threadIdx.x; i < (end >> 1); i += blockDim.x) {
+            const longlong2 a = __ldcs(p + i);
+            add(a.x);
+            add(a.y);
+        }
+        done = (end >> 1) << 1;
+        if (done < start) done = start;
     }
+    for (uint64_t i = done + threadIdx.x; i < end; i += blockDim.x) add(x[i]);
     __shared__ unsigned long long s_lo[256], s_hi[256], s_top[256];
     s_lo[threadIdx.x] = (unsigned long long)acc;
     s_hi[threadIdx.x] = (unsigned long long)(acc >> 64);
