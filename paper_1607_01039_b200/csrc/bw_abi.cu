@@ -1665,8 +1665,8 @@ int bw_inverse_i64(int64_t* data, int log2n, int64_t* scratch_dev, void* stream)
     int* flag = reinterpret_cast<int*>(reinterpret_cast<char*>(p) + 32);
     BW_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
     const uint64_t count = 1ull << log2n;
-    const int grid = grid_for(dev, count, 256, 8);
-    bw::k_check_divisible<<<grid, 256, 0, s>>>(reinterpret_cast<const long long*>(data), count, log2n, flag);
+    const unsigned grid = (unsigned)((count + (1ull << bw::kMinmaxChunkBits) - 1) >> bw::kMinmaxChunkBits);
+    bw::k_check_divisible<<<grid, 512, 0, s>>>(reinterpret_cast<const long long*>(data), count, log2n, flag);
     BW_LAUNCHED("k_check_divisible launch");
     int h = 0;
     BW_CUDA(cudaMemcpyAsync(&h, flag, sizeof h, cudaMemcpyDeviceToHost, s));
@@ -1675,7 +1675,7 @@ int bw_inverse_i64(int64_t* data, int log2n, int64_t* scratch_dev, void* stream)
         // Undo (core.py:160-166): H(Hx) = 2^n x, and 2^n divides exactly.
         BW_TRY(fwht_impl(data, log2n, nullptr, false, s));
     }
-    bw::k_shift_right<<<grid, 256, 0, s>>>(reinterpret_cast<long long*>(data), count, log2n);
+    bw::k_shift_right<<<grid, 512, 0, s>>>(reinterpret_cast<long long*>(data), count, log2n);
     BW_LAUNCHED("k_shift_right launch");
     if (h) {
         BW_CUDA(cudaStreamSynchronize(s));

@@ -1555,17 +1555,42 @@ __global__ void __launch_bounds__(kFoldThreads, 1024 / kFoldThreads) k_fold_bloc
 // ---------------------------------------------------------------------------
 // Elementwise helpers for the inverse transform (core.py:147-173).
 // ---------------------------------------------------------------------------
-__global__ void k_check_divisible(const long long* __restrict__ data, uint64_t count, int n, int* flag) {
+// One CTA per contiguous 2^16-point chunk with 16-byte accesses (as k_minmax).
+__global__ void __launch_bounds__(512) k_check_divisible(const long long* __restrict__ data, uint64_t count, int n,
+                                                         int* flag) {
     const uint64_t m = (1ull << n) - 1ull;
-    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += nth)
-        if (((uint64_t)data[i]) & m) *flag = 1;  // Python % on ints: divisible iff low n bits are 0
+    const uint64_t start = (uint64_t)blockIdx.x << kMinmaxChunkBits;
+    const uint64_t end = min(count, start + (uint64_t)(1ull << kMinmaxChunkBits));
+    uint64_t bad = 0, done = start;
+    if ((reinterpret_cast<uintptr_t>(data) & 15u) == 0) {
+        const ulonglong2* p = reinterpret_cast<const ulonglong2*>(data);
+#pragma unroll 8
+        for (uint64_t i = (start >> 1) + threadIdx.x; i < (end >> 1); i += blockDim.x) {
+            const ulonglong2 a = __ldcs(p + i);
+            bad |= (a.x | a.y) & m;  // Python % on ints: divisible iff the low n bits are 0
+        }
+        done = (end >> 1) << 1;
+    }
+    for (uint64_t i = done + threadIdx.x; i < end; i += blockDim.x) bad |= ((uint64_t)data[i]) & m;
+    if (__any_sync(0xffffffffu, bad != 0) && (threadIdx.x & 31u) == 0) *flag = 1;
 }
 
-__global__ void k_shift_right(long long* __restrict__ data, uint64_t count, int n) {
-    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += nth)
-        data[i] = data[i] >> n;  // exact division (floor == exact when divisible)
+__global__ void __launch_bounds__(512) k_shift_right(long long* __restrict__ data, uint64_t count, int n) {
+    const uint64_t start = (uint64_t)blockIdx.x << kMinmaxChunkBits;
+    const uint64_t end = min(count, start + (uint64_t)(1ull << kMinmaxChunkBits));
+    uint64_t done = start;
+    if ((reinterpret_cast<uintptr_t>(data) & 15u) == 0) {
+        longlong2* p = reinterpret_cast<longlong2*>(data);
+#pragma unroll 8
+        for (uint64_t i = (start >> 1) + threadIdx.x; i < (end >> 1); i += blockDim.x) {
+            longlong2 a = p[i];
+            a.x >>= n;  // exact division (floor == exact when divisible)
+            a.y >>= n;
+            p[i] = a;
+        }
+        done = (end >> 1) << 1;
+    }
+    for (uint64_t i = done + threadIdx.x; i < end; i += blockDim.x) data[i] = data[i] >> n;
 }
 
 }  // namespace bw
