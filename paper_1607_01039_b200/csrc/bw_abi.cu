@@ -71,6 +71,8 @@ const bool g_two_pass = !(getenv("BW_TWO_PASS") && getenv("BW_TWO_PASS")[0] == '
 const int g_narrow_tpc = getenv("BW_NARROW_TPC") ? atoi(getenv("BW_NARROW_TPC")) : 2;
 // BW_FOLD_BLOCKS=0 keeps the shared-bin / L2-atomic fold for d_out > 12 (A/B knob, read per call).
 bool fold_blocks_enabled() { return !(getenv("BW_FOLD_BLOCKS") && getenv("BW_FOLD_BLOCKS")[0] == '0'); }
+// BW_F64_VEC_LOW=0 keeps the float64 low pass on 8-byte accesses (A/B knob).
+const bool g_f64_vec_low = !(getenv("BW_F64_VEC_LOW") && getenv("BW_F64_VEC_LOW")[0] == '0');
 // BW_SPLIT_PLANS=0 keeps the default planner to one-run high passes (A/B knob).
 const bool g_split_plans = !(getenv("BW_SPLIT_PLANS") && getenv("BW_SPLIT_PLANS")[0] == '0');
 // BW_HOST_PIPELINE=0 disables the copy/compute overlap of host-buffer transforms (A/B knob).
@@ -464,9 +466,10 @@ int for_all_pass_kernels(F&& f) {
 
 // ---- float64 passes (ascending stage order, CfgLow13F / CfgHigh13F / CfgReg)
 template <class F>
-int visit_pass_f64(const Pass& p, F&& f) {
+int visit_pass_f64(const Pass& p, F&& f, bool vec = true) {
     switch (p.kind) {
         case LOW:
+            if (vec && g_f64_vec_low) return f(tag<bw::CfgLow13FV>{}, ic<13>{});  // 16-byte aligned data
             return f(tag<bw::CfgLow13F>{}, ic<13>{});
         case HIGH:
             if (p.r == 8) return f(tag<bw::CfgHigh13F<5>>{}, ic<5>{});
@@ -508,7 +511,8 @@ int f64_passes(int n, std::vector<Pass>* passes) {
 
 template <class F>
 int for_all_f64_pass_kernels(F&& f) {
-    BW_TRY(visit_pass_f64(Pass{LOW, 0, 13, 0}, f));
+    BW_TRY(visit_pass_f64(Pass{LOW, 0, 13, 0}, f, true));
+    BW_TRY(visit_pass_f64(Pass{LOW, 0, 13, 0}, f, false));
     for (int r = 1; r <= kF64MaxHigh; ++r)
         BW_TRY(visit_pass_f64(Pass{r <= bw::kRegOnlyMaxBits ? REG : HIGH, 0, r, 0}, f));
     return BW_OK;
@@ -723,6 +727,7 @@ int launch_two_pass(const std::vector<Pass>& passes, u64* d, int n, int dev, cud
 // (FP) and int64 views that are 8- but not 16-byte aligned.
 template <bool FP>
 int run_scalar_plan(u64* d, int log2n, cudaStream_t s) {
+    const bool vec = !(reinterpret_cast<uintptr_t>(d) & 15u);  // the paired low pass needs 16-byte alignment
     std::vector<Pass> passes;
     BW_TRY(f64_passes(log2n, &passes));
     for (const Pass& p : passes) {
@@ -740,7 +745,7 @@ int run_scalar_plan(u64* d, int log2n, cudaStream_t s) {
             const unsigned grid = (unsigned)(1ull << (log2n - bw::kCtaBits));
             const void* none = nullptr;
             return launch_cfg<C>(bw::k_pass<C, L, false, false, FP>, grid, s, d, p.k, bw::ExtractArgs{}, none);
-        }));
+        }, vec));
     }
     return BW_OK;
 }
@@ -2817,8 +2822,18 @@ void stage_order(int k, std::vector<int>* out) {
 // Static checker of the float64 plan: the check_pass walk of every pass
 // (bijective loads/stores, every stage once) plus strictly ascending stage
 // order per element across the whole plan (bitwise numpy equality).
+namespace {
+int check_f64_plan(int log2n, bool vec, uint64_t* butterflies);
+}
+// Both low-pass layouts: the paired one (16-byte aligned data) and the
+// 8-byte one (float64 views and int64 views that are only 8-byte aligned).
 extern "C" int bw_plan_check_f64(int log2n, uint64_t* butterflies) {
     if (log2n < 0 || log2n > 24) return fail(BW_BAD_ARGUMENTS, "plan check supports 0 <= n <= 24");
+    BW_TRY(check_f64_plan(log2n, false, butterflies));
+    return check_f64_plan(log2n, true, butterflies);
+}
+namespace {
+int check_f64_plan(int log2n, bool vec, uint64_t* butterflies) {
     std::vector<Pass> passes;
     BW_TRY(f64_passes(log2n, &passes));
     uint64_t bfly = 0;
@@ -2837,7 +2852,7 @@ extern "C" int bw_plan_check_f64(int log2n, uint64_t* butterflies) {
                 constexpr int L = decltype(l)::value;
                 stage_order<C, L, 0>(p.k, &order);
                 return check_pass<C, L>(log2n, p.k, touched, &bits, &bfly);
-            }));
+            }, vec));
         }
         if (covered & bits) return fail(BW_BAD_ARGUMENTS, "stage applied twice");
         covered |= bits;
@@ -2849,6 +2864,7 @@ extern "C" int bw_plan_check_f64(int log2n, uint64_t* butterflies) {
     if (butterflies) *butterflies = bfly;
     return BW_OK;
 }
+}  // namespace
 
 // TEST HOOK ONLY: the float64 plan's exact tables executed on HOST memory
 // with IEEE double add/sub (n <= 24).

@@ -187,6 +187,30 @@ struct CfgLow13F {
     BW_HD static constexpr int P(int) { return 0; }
 };
 
+// The same four rounds with 16-byte global accesses: round 0 holds tile
+// bit 0 in a register (element pairs) and stages only it, the last round
+// holds it again for paired stores.
+//   round 0: reg {0,9,10,11,12}  lane {1,2,3,5,4}  warp {6,7,8}    stage 0
+//   round 1: reg {1..5}          lane {0,6,7,8,9}  warp {10,11,12} stages 1..5
+//   round 2: reg {6..10}         lane {0..4}       warp {5,11,12}  stages 6..10
+//   round 3: reg {0,11,12,6,7}   lane {1,2,3,5,4}  warp {8,9,10}   stages 11,12
+struct CfgLow13FV {
+    static constexpr int T = 13, Q = 0, R = 5, W = 3, NR = 4, XR = 4, MINB = BW_T13_MINB, PAD = 1;
+    BW_HD static constexpr int reg(int rd, int i) {
+        return nib(rd == 0 ? 0xCBA90ull : rd == 1 ? 0x54321ull : rd == 2 ? 0xA9876ull : 0x76CB0ull, i);
+    }
+    BW_HD static constexpr int lane(int rd, int i) {  // lanes {1,2,3,5,4}: conflict-free with the pad
+        return nib(rd == 1 ? 0x98760ull : rd == 2 ? 0x43210ull : 0x45321ull, i);
+    }
+    BW_HD static constexpr int warp(int rd, int i) {
+        return nib(rd == 0 ? 0x876ull : rd == 1 ? 0xCBAull : rd == 2 ? 0xCB5ull : 0xA98ull, i);
+    }
+    BW_HD static constexpr uint32_t stage(int rd) {
+        return rd == 0 ? 0x0001u : rd == 1 ? 0x003Eu : rd == 2 ? 0x07C0u : 0x1800u;
+    }
+    BW_HD static constexpr int P(int) { return 0; }
+};
+
 // Strided high-bits pass with LL column bits (r = 13 - LL = 6..8 rows,
 // tile bits LL..12), ascending: round 0 stages the five lowest rows, round 1
 // the rest; lanes stay on columns 0..4 (256-byte accesses).
