@@ -2,12 +2,21 @@
 
 import json
 import os
+import socket
 import subprocess
 import sys
 
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def free_port() -> str:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return str(port)
 
 
 def run_bench(args, env=None, timeout=600):
@@ -45,7 +54,7 @@ def test_multirank_path_two_processes_one_gpu():
     """The N > 1 bench path (CUDA-IPC peer exchange, max over ranks, rank-0
     JSON) with 2 ranks on one GPU; gloo carries the host-side collectives."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"),
+           "--master-addr", "127.0.0.1", "--master-port", free_port(), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "3", "--warmup", "3", "--log2n", "24", "--dist-backend", "gloo", "--no-cpu"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
@@ -60,7 +69,7 @@ def test_multirank_narrow_wire_two_processes_one_gpu():
     """bench --mode narrow: the int8 cross-first exchange, timed by phase,
     with no fallback on config 4's +-1 signal."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", "29518", os.path.join(ROOT, "bench.py"),
+           "--master-addr", "127.0.0.1", "--master-port", free_port(), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "3", "--warmup", "3", "--log2n", "24", "--dist-backend", "gloo", "--no-cpu",
            "--mode", "narrow"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
@@ -78,7 +87,7 @@ def test_multirank_extraction_config3_two_processes_one_gpu(mode):
     (fused) or run on every rank's shard after the exchange (narrow), inside
     the step; the gathered hits are the planted secret."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", "29519" if mode == "fused" else "29520",
+           "--master-addr", "127.0.0.1", "--master-port", free_port(),
            os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "3", "--steps", "3", "--warmup", "3",
            "--dist-backend", "gloo", "--no-cpu", "--no-e2e", "--mode", mode]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
