@@ -13,9 +13,15 @@ larger than the 126 MB L2, so no L2 flush is needed between steps.
 --config 1..5 selects the other BASELINE configs (3 and 5 add the fused
 |W| > tau extraction to every step; 1 and 2 flush L2 between steps).
 
---impl reference times the reference's own CPU algorithm (the oracle port of
-parallel.py run_parallel, numpy, all host cores) on a bounded sample of the
-same workload; rank 0 only.
+--impl reference times the reference's own CPU path -- the unmodified
+bigwht.parallel.run_parallel shipped in baseline/_ref by
+baseline/install_reference.sh (the numpy port oracle_np.run_parallel when it
+was not shipped), all power-of-two host threads -- on a bounded sample of the
+same workload; rank 0 only.  --cpu-full adds one run at the full size.
+
+On one GPU the line also carries "parity": the CPU sample against the GPU
+transform of the same input, and the measured step's full-size output at 2^20
+seeded indices against the CPU fold identity (both bit-exact).
 """
 
 from __future__ import annotations
@@ -50,6 +56,10 @@ def args_parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the in-run bit-exact checks against the CPU")
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="also time ONE reference run_parallel at the full config size (slow; written to "
+                         "profiles/r02_cpu_reference_full.json)")
     ap.add_argument("--intermediates", choices=["narrow", "int64"], default="int64",
                     help="narrow: the narrow-intermediate plan (int16/int32 between passes, checked, int64 "
                          "fallback; measured no faster, DESIGN.md section 5); int64: the plain int64 plan")
@@ -141,27 +151,76 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU legs ---
 
-def cpu_reference_sample(n_sample: int, reps: int, warm: int):
-    """The reference's CPU algorithm (numpy restatement of parallel.py
-    run_parallel) on a 2^n_sample sample, all power-of-two host threads.
-    Returns (list of seconds, threads)."""
+def reference_package():
+    """The UNMODIFIED reference package ``bigwht`` installed in baseline/_ref
+    (baseline/install_reference.sh), or None when it was not shipped."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "bigwht")):
+        return None
+    if ref not in sys.path:
+        sys.path.append(ref)
+    try:
+        import bigwht
+        import bigwht.core  # noqa: F401
+        import bigwht.parallel  # noqa: F401
+    except Exception as e:  # a broken install: fall back to the port, and say so
+        print(f"reference package in {ref} unusable ({e}); timing the oracle port", file=sys.stderr)
+        return None
+    return bigwht
+
+
+def config_input(spec, n_sample: int):
+    """The first 2^n_sample points of the config's input, generated on the
+    host by the CPU restatement of the generator (signals.py spec)."""
     import numpy as np
 
-    from oracle import load_c, oracle_np
+    from oracle import load_c
+
+    cores = len(os.sched_getaffinity(0))
+    x = np.empty(1 << n_sample, dtype=np.int64)
+    params = (ctypes.c_uint64 * max(1, len(spec.params)))(*[int(v) for v in spec.params])
+    load_c().oracle_gen_i64(x.ctypes.data, 0, x.size, spec.kind, spec.seed, params, len(spec.params), cores)
+    return x
+
+
+def cpu_reference_sample(spec, n_sample: int, reps: int, warm: int):
+    """The reference's CPU path on a 2^n_sample sample of the config input:
+    ``bigwht.parallel.run_parallel(Signal(x), plan_parallel(n, p))``
+    (parallel.py:162-198, including its bound check at :175) from the
+    shipped reference, with 2^p = the largest power of two <= the host cores
+    (run_parallel needs a power-of-two worker count, parallel.py:79-84);
+    the numpy port (oracle_np.run_parallel) when the reference was not
+    shipped.  Every run starts from the same input (copied back outside the
+    timing).  Returns a dict with the times, threads, kind, input and the
+    transformed sample."""
+    import numpy as np
 
     cores = len(os.sched_getaffinity(0))
     p = max(1, min(cores.bit_length() - 1, n_sample - 1))
-    x = np.empty(1 << n_sample, dtype=np.int64)
-    arr = (ctypes.c_uint64 * 1)(0)
-    load_c().oracle_gen_i64(x.ctypes.data, 0, x.size, 1, 32, arr, 0, cores)  # config-4 values, first chunk
+    x0 = config_input(spec, n_sample)
+    x = np.empty_like(x0)
+    ref = reference_package()
     times = []
     for i in range(warm + reps):
+        np.copyto(x, x0)
         t0 = time.perf_counter()
-        oracle_np.run_parallel(x, n_sample, p)
+        if ref is not None:
+            sig = ref.core.Signal(x, ref.core.Domain.TIME)
+            ref.parallel.run_parallel(sig, ref.parallel.plan_parallel(n_sample, p))
+        else:
+            from oracle import oracle_np
+
+            oracle_np.run_parallel(x, n_sample, p)
         dt = time.perf_counter() - t0
         if i >= warm:
             times.append(dt)
-    return times, 1 << p, cores
+    if ref is not None:
+        x = sig.data
+        what = f"bigwht.parallel.run_parallel (the unmodified reference from baseline/_ref, parallel.py:162-198) p={p}"
+    else:
+        what = f"oracle_np.run_parallel (numpy port of parallel.py:162-198; reference not shipped) p={p}"
+    return {"times": times, "threads": 1 << p, "cores": cores, "kind": "reference" if ref is not None else "port",
+            "what": what, "x0": x0, "y": x}
 
 
 def cpu_equivalent_rate(n_full: int, n_sample: int, seconds: float) -> float:
@@ -172,27 +231,52 @@ def cpu_equivalent_rate(n_full: int, n_sample: int, seconds: float) -> float:
     return 2 ** n_full / t_full
 
 
+FULL_CPU_RECORD = os.path.join(ROOT, "profiles", "r02_cpu_reference_full.json")
+
+
+def cpu_reference_full(spec, n: int):
+    """ONE run of the reference's run_parallel at the full config size n
+    (about 2.5x the array in host RAM), timed like the samples.  Slow: only
+    with --cpu-full.  The record is written to profiles/ for the default run
+    to cite."""
+    import numpy as np
+
+    need = (8 << n) * 3
+    if need > host_ram_bytes():
+        return {"skipped": f"needs ~{need >> 30} GiB host RAM, host has {host_ram_bytes() >> 30} GiB"}
+    r = cpu_reference_sample(spec, n, 1, 0)
+    rec = {"n": n, "seconds": r["times"][0], "points_per_s": (2 ** n) / r["times"][0], "threads": r["threads"],
+           "host_cores": r["cores"], "kind": r["kind"], "what": r["what"],
+           "output_sha256_16": __import__("hashlib").sha256(np.ascontiguousarray(r["y"]).tobytes()).hexdigest()[:16]}
+    return rec
+
+
 def run_reference(a):
     ws, rank, _ = world()
     if rank != 0:
         return
+    from paper_1607_01039_b200 import signals
+
+    spec = signals.config(a.config, a.n)
     n_s = min(CPU_SAMPLE_N, a.n)
-    times, threads, cores = cpu_reference_sample(n_s, max(1, a.steps), max(0, a.warmup))
+    r = cpu_reference_sample(spec, n_s, max(1, a.steps), max(0, a.warmup))
+    times = r["times"]
     mean = sum(times) / len(times)
     value = cpu_equivalent_rate(a.n, n_s, mean)
-    sample = (f"one 2^{n_s}-point run_parallel (numpy port of parallel.py:162-198, p={threads.bit_length() - 1}) "
-              f"per step on the config-{a.config} input; rate extrapolated to n={a.n} as "
-              f"2^n / (t * 2^(n-{n_s}) * n/{n_s})")
+    sample = (f"one 2^{n_s}-point {r['what']} per step on the first 2^{n_s} points of the config-{a.config} "
+              f"input; rate extrapolated to n={a.n} as 2^n / (t * 2^(n-{n_s}) * n/{n_s})")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": ws,
         "steps": len(times), "warmup": a.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": value / PUBLISHED_PTS, "dtype": "int64", "data": "synthetic",
         "config": {"workload": f"config{a.config}: n={a.n} int64 FWHT, {CONFIG_TEXT[a.config]}, natural order, "
                                "unnormalised", "n": a.n, "sample_n": n_s},
-        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "host_cores": cores,
-                         "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": r["threads"], "host_cores": r["cores"],
+                         "kind": r["kind"], "sample": sample},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if a.cpu_full:
+        line["cpu_baseline"]["full_size_measured"] = cpu_reference_full(spec, a.n)
     print(json.dumps(line), flush=True)
 
 
@@ -439,19 +523,36 @@ def run_ours(a):
     trial_ms = {}
     if len(candidates) > 1:  # two timed steps per candidate after one warm-up step, max over ranks
         for m in candidates:  # every step on the config input: the narrow wire depends on its magnitude
-            configure(m)
-            restore()
-            step(events())
-            tr = [events() for _ in range(2)]
-            for e in tr:
+            # A candidate that raises on any rank (an exchange this box cannot
+            # run) is dropped by every rank: the ranks agree through an
+            # all-reduce of their trial times (inf = failed) and share the error.
+            err = None
+            try:
+                configure(m)
                 restore()
-                step(e)
-            torch.cuda.synchronize()
-            t = torch.tensor([sum(e[0].elapsed_time(e[-1]) for e in tr) / len(tr)], dtype=torch.float64,
-                             device="cuda" if a.dist_backend == "nccl" else "cpu")
+                step(events())
+                tr = [events() for _ in range(2)]
+                for e in tr:
+                    restore()
+                    step(e)
+                torch.cuda.synchronize()
+                mine = sum(e[0].elapsed_time(e[-1]) for e in tr) / len(tr)
+            except Exception as e:  # noqa: BLE001 -- BigWHTError, NCCL / CUDA RuntimeError
+                err = f"rank {rank}: {type(e).__name__}: {e}"
+                mine = float("inf")
+            t = torch.tensor([mine], dtype=torch.float64, device="cuda" if a.dist_backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            trial_ms[m] = float(t.item())
-        configure(min(trial_ms, key=trial_ms.get))
+            if t.item() == float("inf"):
+                errs = [None] * ws
+                dist.all_gather_object(errs, err)
+                trial_ms[m] = "failed: " + "; ".join(e for e in errs if e)[:300]
+                print(f"exchange {m} dropped: {trial_ms[m]}", file=sys.stderr)
+            else:
+                trial_ms[m] = float(t.item())
+        ok = {m: v for m, v in trial_ms.items() if isinstance(v, float)}
+        if not ok:
+            raise SystemExit(f"every cross-GPU exchange failed: {trial_ms}")
+        configure(min(ok, key=ok.get))
         if st["mode"] != "a2a" and "recv" in st:
             del st["recv"]
             torch.cuda.empty_cache()
@@ -545,6 +646,17 @@ def run_ours(a):
             traffic = t_dom["dram_read_bytes"] + t_dom["dram_write_bytes"]
     except (OSError, KeyError, ValueError):
         traffic = None
+
+    # One more step of the same kind from the config input, then its output
+    # gathered at the row space of a seeded fold map: checked on the CPU
+    # below against WHT(fold(x, L)) (subspace.py:1-11), computed from the
+    # regenerated input -- the full-size output of the measured path itself.
+    spot = None
+    if rank == 0 and ws == 1 and not a.no_cpu and not a.no_parity:
+        restore()
+        step(events())
+        torch.cuda.synchronize()
+        spot = spot_check_gather(x, spec, n)
 
     e2e = None
     if not a.no_e2e:
@@ -643,13 +755,31 @@ def run_ours(a):
         line["e2e"] = e2e
     if rank == 0 and ws == 1 and not a.no_cpu:
         n_s = min(CPU_SAMPLE_N, n)
-        times, threads, cores = cpu_reference_sample(n_s, 4, 1)
-        mean = sum(times) / len(times)
+        r = cpu_reference_sample(spec, n_s, 4, 1)
+        mean = sum(r["times"]) / len(r["times"])
         line["cpu_baseline"] = {
-            "value": cpu_equivalent_rate(n, n_s, mean), "unit": "points/s", "cores": threads, "host_cores": cores,
-            "kind": "port",
-            "sample": f"2^{n_s}-point run_parallel (numpy port of parallel.py:162-198) x{len(times)}, "
-                      f"{mean:.3f} s each; extrapolated to n={n} by 2^(n-{n_s}) * n/{n_s}"}
+            "value": cpu_equivalent_rate(n, n_s, mean), "unit": "points/s", "cores": r["threads"],
+            "host_cores": r["cores"], "kind": r["kind"],
+            "sample": f"2^{n_s}-point {r['what']} on the first 2^{n_s} points of the config input "
+                      f"x{len(r['times'])}, {mean:.3f} s each; extrapolated to n={n} by 2^(n-{n_s}) * n/{n_s}"}
+        if a.cpu_full:
+            full = cpu_reference_full(spec, n)
+            full["config"] = a.config
+            if "seconds" in full:
+                with open(FULL_CPU_RECORD, "w") as f:
+                    json.dump(full, f, indent=1)
+            line["cpu_baseline"]["full_size_measured"] = full
+        else:
+            try:
+                with open(FULL_CPU_RECORD) as f:
+                    full = json.load(f)
+                if full.get("n") == n and full.get("config") == a.config:
+                    full["source"] = "profiles/r02_cpu_reference_full.json (an earlier bench.py --cpu-full run)"
+                    line["cpu_baseline"]["full_size_measured"] = full
+            except (OSError, ValueError):
+                pass
+        if not a.no_parity:
+            line["parity"] = parity_checks(r, spot, spec, n)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if peer is not None:
@@ -657,6 +787,72 @@ def run_ours(a):
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+SPOT_D_OUT = 20
+
+
+def spot_check_gather(x, spec, n):
+    """The 2^20 outputs WHT(x)[row_space(L)] of a seeded full-rank 20 x n map
+    L whose row space holds the planted masks, gathered from the device."""
+    import numpy as np
+    import torch
+
+    from oracle import oracle_np
+
+    d = min(SPOT_D_OUT, n)
+    rng = np.random.default_rng(spec.seed + 1000)
+    while True:
+        rows = rng.integers(0, 2, size=(d, n), dtype=np.uint8)
+        for i, m in enumerate(spec.masks[:d]):
+            rows[i] = [(m >> c) & 1 for c in range(n)]
+        if oracle_np.gf2_rank(rows) == d:
+            break
+    rs = torch.from_numpy(oracle_np.row_space(rows)).to(x.device)
+    return {"rows": rows, "got": x[rs].cpu().numpy()}
+
+
+def parity_checks(r, spot, spec, n):
+    """Bit-exact checks of this run's GPU results against the CPU:
+    (1) the CPU baseline's own sample (the reference's run_parallel output on
+    the first 2^s points of the config input) against the public GPU call
+    fwht_array on the same input; (2) the full-size output of the measured
+    step, at 2^20 seeded indices, against WHT(fold(x, L)) computed on the
+    host from the regenerated input (the C restatement of subspace.py's fold
+    + FWHT, oracle/bw_oracle.c)."""
+    import numpy as np
+    import torch
+
+    import paper_1607_01039_b200 as bw
+    from oracle import load_c, oracle_np
+
+    out = {}
+    t = torch.from_numpy(r["x0"]).cuda()
+    bw.fwht_array(t)
+    eq = bool(np.array_equal(t.cpu().numpy(), r["y"]))
+    del t
+    torch.cuda.empty_cache()
+    s = int(r["x0"].size).bit_length() - 1
+    out["sample"] = {"checked": f"all 2^{s} outputs of the CPU baseline's {r['kind']} run_parallel vs "
+                                "paper_1607_01039_b200.fwht_array on the same input", "points": 1 << s, "equal": eq}
+    if spot is not None:
+        t0 = time.perf_counter()
+        rows = spot["rows"]
+        d = rows.shape[0]
+        cols = oracle_np.column_masks(rows).astype(np.uint64)
+        want = np.empty(1 << d, dtype=np.int64)
+        params = (ctypes.c_uint64 * max(1, len(spec.params)))(*[int(v) for v in spec.params])
+        lib = load_c()
+        rc = lib.oracle_fold_i64(None, n, cols.ctypes.data, d, spec.kind, spec.seed, params, len(spec.params),
+                                 len(os.sched_getaffinity(0)), want.ctypes.data)
+        lib.oracle_fwht_i64(want.ctypes.data, d)
+        out["full_size_spot_check"] = {
+            "checked": f"2^{d} outputs of the measured n={n} step at row_space(L) (seeded full-rank {d} x {n} L "
+                       "holding the planted masks) vs WHT(fold(x, L)) from the regenerated input on the CPU",
+            "points": 1 << d, "equal": bool(rc == 0 and np.array_equal(spot["got"], want)),
+            "cpu_seconds": round(time.perf_counter() - t0, 2)}
+    out["equal"] = all(v["equal"] for v in out.values() if isinstance(v, dict))
+    return out
 
 
 def host_ram_bytes() -> int:
@@ -738,20 +934,30 @@ def run_e2e(a, x, spec, p, nl, rank, ws, peer):
         peer2 = sharded._PeerMap(x2, None, dist) if peer is not None else None
         maps = [peer, peer2] if peer is not None else None
         nws = [a.narrow_wire, a.narrow_wire] if a.narrow_wire is not None else None
+        orig = host.clone()
         sharded.fwht_distributed_many([host, host2], mode=a.exchange, work=[x, x2], peer_maps=maps,
                                       narrow_wires=nws)  # warm-up
+        if a.exchange == "narrow":
+            # the int8 wire needs the config input (|x| <= 127 >> log2 P): a
+            # transformed signal would fall back to the int64 fused pass, so
+            # two fresh signals, one per device buffer
+            steps = 2
+        host.copy_(orig)  # the config input again, outside the timing
+        host2.copy_(orig)
         torch.cuda.synchronize()
         dist.barrier()
         e0.record(stream)
         sharded.fwht_distributed_many([host if i % 2 == 0 else host2 for i in range(steps)], mode=a.exchange,
                                       work=[x, x2], peer_maps=maps, narrow_wires=nws)
+        ran = list(sharded.last_exchanges)
         e1.record(stream)
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64,
                          device="cuda" if a.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        api = f"sharded.fwht_distributed_many({steps} consecutive pinned host shards per rank)"
+        api = (f"sharded.fwht_distributed_many({steps} consecutive pinned host shards per rank; "
+               f"exchanges run: {', '.join(f'{k} x{ran.count(k)}' for k in dict.fromkeys(ran))})")
         dist.barrier()
         if peer2 is not None:
             peer2.close()

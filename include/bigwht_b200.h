@@ -203,6 +203,17 @@ int bw_fwht_inplace_i64(int64_t *data, int log2n, int64_t *scratch_dev,
                         void *stream, uint64_t *butterflies);
 
 /*
+ * fwht_inplace(sig) (core.py:120-125) when the caller knows a bound M >= max|x|
+ * (a generator, a previous check): M * 2^log2n < 2^63 is checked on the host
+ * (BW_OVERFLOW_BOUND before any launch, like core.py:122), then the
+ * transform -- no reduction pass, no synchronisation.  max_abs < 0: the
+ * device check of bw_fwht_inplace_i64.  A bound below the true max|x| is a
+ * caller error (the arithmetic still wraps mod 2^64 exactly like numpy).
+ */
+int bw_fwht_inplace_known_i64(int64_t *data, int log2n, int64_t max_abs,
+                              void *stream, uint64_t *butterflies);
+
+/*
  * End-to-end transform of a HOST buffer (pinned for full PCIe speed):
  * H2D into the caller's device workspace (2^log2n int64), fused bound
  * check + transform on the device, D2H of the result.  If check_bound and the

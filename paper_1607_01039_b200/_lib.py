@@ -66,6 +66,7 @@ _SIGNATURES = {
     "bw_minmax_i64": ([P, U64, P, P], I32),
     "bw_check_bound_i64": ([P, I32, P, P, PU64], I32),
     "bw_fwht_inplace_i64": ([P, I32, P, P, PU64], I32),
+    "bw_fwht_inplace_known_i64": ([P, I32, ctypes.c_int64, P, PU64], I32),
     "bw_fwht_host_i64": ([P, I32, P, I32, P, PU64], I32),
     "bw_fwht_host_batch_i64": ([ctypes.POINTER(P), I32, I32, ctypes.POINTER(P), I32, P, PU64], I32),
     "bw_fwht_host_ooc_i64": ([P, I32, P, I32, P, ctypes.POINTER(I32)], I32),

@@ -87,12 +87,37 @@ def cmd_transform_mem(args) -> None:
     _say(args, f"transformed {args.in_path} in GPU memory (threads={args.threads})")
 
 
+def _refuse_interrupted(path: str, meta: dict, resume: bool) -> None:
+    """A sidecar carrying the reference executor's pass-progress marker
+    belongs to an interrupted out-of-core run: its payload is partially
+    transformed although the domain still says time.  Refuse it with the
+    reference's messages (external.py:155-178) instead of transforming it
+    again; this engine cannot resume the reference's passes."""
+    marker = meta.get("pass_progress")
+    if marker is None:
+        return
+    if not resume:
+        raise BadArguments(
+            f"{path} has an interrupted transform "
+            f"({marker.get('passes_done')}/{marker.get('total_passes')} "
+            f"passes done); pass resume=True to continue")
+    if marker.get("writing"):
+        raise BadArguments(
+            f"{path}: pass {marker.get('passes_done')} was interrupted "
+            f"after its writes began, so the payload may be partially "
+            f"transformed; re-running it would corrupt the data. Rebuild "
+            f"the dataset from its source.")
+    raise BadArguments(f"{path} has an interrupted transform of the reference's disk executor; "
+                       "this engine keeps no pass-progress markers and cannot resume it")
+
+
 def cmd_transform_ext(args) -> None:
     """cli.py:175-219: out-of-core through a device workspace of 2**B
     elements, streaming the memory-mapped payload (no resume markers)."""
     from .outofcore import fwht_out_of_core
 
     _adopt_if_forced(args, args.in_path, "time")
+    _refuse_interrupted(args.in_path, dataset.read_meta(args.in_path), args.resume)
     if args.resume:
         raise BadArguments("--resume: this engine keeps no pass-progress markers (a run is one call)")
     if args.io_block_bytes is not None and (args.io_block_bytes < 8 or args.io_block_bytes % 8):

@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import BadArguments, DeviceError, OracleTooLarge, OverflowBoundError
+from .errors import BadArguments, DeviceError, NotPowerOfTwo, OracleTooLarge, OverflowBoundError
 
 # Brute force costs O(4**n); core.py:24-27 uses the same default limit.
 ORACLE_LIMIT_DEFAULT = 14
@@ -136,8 +136,9 @@ def _check_shape(buf) -> int:
         raise BadArguments("signal data must be one-dimensional")
     if not _is_power_of_two(_length(buf)):
         # The reference would raise numpy's ValueError after mutating part of
-        # the buffer; we refuse before any launch.
-        raise BadArguments(f"signal length {_length(buf)} is not a power of two")
+        # the buffer; we refuse before any launch, with
+        # an error that is both a BadArguments and a ValueError.
+        raise NotPowerOfTwo(f"signal length {_length(buf)} is not a power of two")
     return _log2(buf)
 
 
@@ -175,8 +176,12 @@ def check_magnitude_bound(data, log2_dim: int) -> None:
         return
     if isinstance(data, np.ndarray):
         _need_cuda()
-        work = _HostStage.get(_log2(data), torch.int64)
-        work.copy_(torch.from_numpy(np.ascontiguousarray(data)))
+        data = np.ascontiguousarray(data).reshape(-1)
+        if _is_power_of_two(_length(data)):
+            work = _HostStage.get(_log2(data), torch.int64)
+            work.copy_(torch.from_numpy(data))
+        else:
+            work = torch.from_numpy(data).cuda()
         data = work
     _require_cuda(data)
     with torch.cuda.device(data.device):
@@ -241,10 +246,14 @@ def fwht_array(buf, narrow=None) -> int:
     global last_narrow
     last_narrow = False
     _check_contiguous(buf)
+    if buf.ndim == 1 and _length(buf) == 0:
+        return 0  # core.py:106-107: n = -1, no stage runs
     n = _check_shape(buf)
     kind = _dtype_kind(buf)
+    if kind in ("int32", "torch.int32"):
+        return _fwht_int32(buf, n)
     if kind not in ("i64", "f64"):
-        raise BadArguments(f"unsupported dtype {kind}; use int64 or float64")
+        raise BadArguments(f"unsupported dtype {kind}; use int64 or float64 (or int32)")
     _need_cuda()
     bf = ctypes.c_uint64(0)
     L = _lib.lib()
@@ -273,6 +282,28 @@ def fwht_array(buf, narrow=None) -> int:
             _lib.check(L.bw_fwht_i64(buf.data_ptr(), n, _stream_handle(buf), ctypes.byref(bf)))
         else:
             _lib.check(L.bw_fwht_f64(buf.data_ptr(), n, _stream_handle(buf), ctypes.byref(bf)))
+    return int(bf.value)
+
+
+def _fwht_int32(buf, n: int) -> int:
+    """fwht_array on an int32 buffer: the reference transforms it in place
+    in wrapping int32 arithmetic (core.py:108-115 on an int32 array;
+    SURVEY.md 8b).  Reduction mod 2**32 commutes with every add/sub, so the
+    exact int64 transform (bw_fwht_widen_i32: the first pass reads the
+    int32 source) truncated to its low 32 bits is that result, bit for bit."""
+    _need_cuda()
+    src = torch.from_numpy(buf).cuda() if isinstance(buf, np.ndarray) else buf
+    _require_cuda(src)
+    bf = ctypes.c_uint64(0)
+    out = torch.empty(1 << n, dtype=torch.int64, device=src.device)
+    with torch.cuda.device(src.device):
+        _lib.check(_lib.lib().bw_fwht_widen_i32(src.data_ptr(), out.data_ptr(), n, _stream_handle(src),
+                                                ctypes.byref(bf)))
+        low = out.to(torch.int32)  # two's-complement truncation, mod 2**32
+        if isinstance(buf, np.ndarray):
+            buf[...] = low.cpu().numpy()
+        else:
+            buf.copy_(low)
     return int(bf.value)
 
 
@@ -337,25 +368,41 @@ def _flip(domain: Domain) -> Domain:
     return Domain.WALSH if domain == Domain.TIME else Domain.TIME
 
 
-def fwht_inplace(sig: Signal) -> Signal:
+def fwht_inplace(sig: Signal, max_abs: int | None = None) -> Signal:
     """Fast in-place WHT; flips the domain tag and returns its argument
     (core.py:120-125).  The magnitude bound is checked on the device before
-    any mutation (OverflowBoundError leaves the data untouched)."""
+    any mutation (OverflowBoundError leaves the data untouched).
+
+    ``max_abs``: a bound M >= max|x| the caller already knows (a generator's
+    range, an earlier check).  M * 2**n < 2**63 is then checked on the host
+    and the 8 B/point reduction pass is skipped (bw_fwht_inplace_known_i64),
+    so the call costs what fwht_array costs.  The caller vouches for M."""
     buf = sig.data
     n = sig.log2_dim
     _need_cuda()
     L = _lib.lib()
     bf = ctypes.c_uint64(0)
+    if max_abs is not None:
+        max_abs = int(max_abs)
+        if max_abs < 0:
+            raise BadArguments(f"max_abs must be >= 0, got {max_abs}")
+        if sig.is_exact and max_abs << n >= _INT64_LIMIT:
+            raise OverflowBoundError(
+                f"max |x| = {max_abs} with n = {n} can overflow int64; need |x| * 2**n < 2**63")
     if sig.is_exact:
         if isinstance(buf, np.ndarray):
             work = _HostStage.get(n, torch.int64)
-            _lib.check(L.bw_fwht_host_i64(buf.ctypes.data, n, work.data_ptr(), 1,
+            _lib.check(L.bw_fwht_host_i64(buf.ctypes.data, n, work.data_ptr(), 1 if max_abs is None else 0,
                                           _stream_handle(work), ctypes.byref(bf)))
         else:
             _require_cuda(buf)
             with torch.cuda.device(buf.device):
-                _lib.check(L.bw_fwht_inplace_i64(buf.data_ptr(), n, None, _stream_handle(buf),
-                                                 ctypes.byref(bf)))
+                if max_abs is not None:
+                    _lib.check(L.bw_fwht_inplace_known_i64(buf.data_ptr(), n, max_abs, _stream_handle(buf),
+                                                           ctypes.byref(bf)))
+                else:
+                    _lib.check(L.bw_fwht_inplace_i64(buf.data_ptr(), n, None, _stream_handle(buf),
+                                                     ctypes.byref(bf)))
     else:
         fwht_array(buf)
     sig.domain = _flip(sig.domain)

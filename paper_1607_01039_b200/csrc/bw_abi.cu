@@ -1040,6 +1040,20 @@ int bw_fwht_inplace_i64(int64_t* data, int log2n, int64_t* scratch_dev, void* st
     return bw_fwht_i64(data, log2n, stream, butterflies);
 }
 
+// fwht_inplace with the bound M supplied by the caller (SURVEY.md 8b
+// "max_abs_or_neg1"): M * 2^n < 2^63 is checked on the host, so no
+// reduction pass and no stream synchronisation; max_abs < 0 falls back to
+// the device check of bw_fwht_inplace_i64.
+int bw_fwht_inplace_known_i64(int64_t* data, int log2n, int64_t max_abs, void* stream, uint64_t* butterflies) {
+    if (max_abs < 0) return bw_fwht_inplace_i64(data, log2n, nullptr, stream, butterflies);
+    BW_TRY(check_signal(data, log2n));
+    if (!bound_ok(static_cast<uint64_t>(max_abs), log2n))
+        return fail(BW_OVERFLOW_BOUND,
+                    "max |x| = %llu with n = %d can overflow int64; need |x| * 2**n < 2**63",
+                    (unsigned long long)max_abs, log2n);
+    return bw_fwht_i64(data, log2n, stream, butterflies);
+}
+
 }  // extern "C"
 namespace {
 // ---- narrow intermediates (bw_fwht_i64_narrow) ----------------------------
@@ -1524,10 +1538,18 @@ int bw_fwht_host_batch_i64(int64_t* const* host, int count, int log2n, int64_t* 
         for (int i = 0; i < count; ++i) {
             const int b = i % nb;
             if (i >= nb) BW_CUDA(cudaStreamWaitEvent(up, freed[b], 0));  // signal i-nb's D2H left this buffer
+            // Host memory read here and written back by a signal whose D2H
+            // may still be in flight (i-nb+1 .. i-1; i-nb and earlier are
+            // ordered by freed[b] above, the D2H stream being in order):
+            // wait for the latest such D2H, which implies the earlier ones.
             const char* hi = reinterpret_cast<const char*>(host[i]);
-            const char* hp = reinterpret_cast<const char*>(host[i - (i > 0)]);
-            if (i > 0 && hi < hp + bytes && hp < hi + bytes)  // the same host memory twice in a row: in order
-                BW_CUDA(cudaStreamWaitEvent(up, freed[(i - 1) % nb], 0));
+            for (int j = i - 1; j > i - nb && j >= 0; --j) {
+                const char* hj = reinterpret_cast<const char*>(host[j]);
+                if (hi < hj + bytes && hj < hi + bytes) {
+                    BW_CUDA(cudaStreamWaitEvent(up, freed[j % nb], 0));
+                    break;
+                }
+            }
             BW_CUDA(cudaMemcpyAsync(work[b], host[i], bytes, cudaMemcpyHostToDevice, up));
             BW_CUDA(cudaEventRecord(loaded[b], up));
             BW_CUDA(cudaStreamWaitEvent(s, loaded[b], 0));

@@ -16,24 +16,12 @@ import os
 
 import numpy as np
 
-from .errors import BadArguments, BigWHTError, StorageError, ValidationError
+from .errors import BadArguments, BadMetadata, PathExists, SizeMismatch
 
 ELEMENT_BYTES = 8
 FORMAT_VERSION = 1
 _DTYPES = {"int64": np.dtype("<i8"), "float64": np.dtype("<f8")}
 _DOMAINS = ("time", "walsh")
-
-
-class BadMetadata(ValidationError):
-    """Sidecar missing, unparsable, or semantically invalid (errors.py:52)."""
-
-
-class SizeMismatch(ValidationError):
-    """Payload size disagrees with the sidecar (errors.py:48)."""
-
-
-class PathExists(StorageError):
-    """Refusing to overwrite an existing dataset (errors.py:76)."""
 
 
 def sidecar_path(path: str) -> str:
@@ -137,5 +125,5 @@ def read_signal(path: str) -> tuple[np.ndarray, str, str]:
     return arr, meta["element_kind"], meta["domain"]
 
 
-__all__ = ["BadMetadata", "SizeMismatch", "PathExists", "BigWHTError", "adopt", "open_memmap", "read_meta",
+__all__ = ["BadMetadata", "SizeMismatch", "PathExists", "adopt", "open_memmap", "read_meta",
            "read_signal", "set_domain", "sidecar_path", "write_signal"]

@@ -159,12 +159,33 @@ def _fused_pass_extract(ptrs: list[int], p: int, n_local: int, r: int, rank: int
             torch.cuda.current_stream(dev).cuda_stream))
 
 
+def _enable_peers(devices: list[int]) -> None:
+    """Peer access between every pair of the devices holding shards (no-op
+    for shards on one device): the K6 / K6' / narrow kernels on device d
+    load and store the other devices' shards, and the fused extraction
+    appends its hits into device 0's buffers."""
+    if len(devices) < 2:
+        return
+    for d in devices:
+        with torch.cuda.device(d):
+            for q in devices:
+                _lib.check(_lib.lib().bw_enable_peer_access(q))
+
+
+def _check_shards(shards: list[torch.Tensor]) -> int:
+    local = shards[0].numel()
+    for s in shards:
+        if s.numel() != local or s.dtype != torch.int64 or not s.is_cuda or not s.is_contiguous():
+            raise BadArguments("shards must be equal-length contiguous CUDA int64 tensors")
+    return local
+
+
 def fwht_shards_extract_ge(shards: list[torch.Tensor], tau: int, cap: int = 1 << 16):
     """fwht_shards(fused=True) with the extraction (|W| >= tau, noisy.py:185-222)
     fused into the cross-shard pass: returns (index, value) CUDA tensors of
     the whole 2**n signal, sorted by index."""
     p = log2_shards(len(shards))
-    local = shards[0].numel()
+    local = _check_shards(shards)
     n_local = local.bit_length() - 1
     if p == 0 or n_local < 14:
         raise BadArguments("fused extraction needs P >= 2 shards of >= 2**14 points")
@@ -174,6 +195,7 @@ def fwht_shards_extract_ge(shards: list[torch.Tensor], tau: int, cap: int = 1 <<
     devices = sorted({s.device.index for s in shards})
     for d in devices:
         torch.cuda.synchronize(d)
+    _enable_peers(devices)
     dev0 = shards[0].device
     idx = torch.empty(cap, dtype=torch.int64, device=dev0)
     val = torch.empty(cap, dtype=torch.int64, device=dev0)
@@ -212,10 +234,7 @@ def fwht_shards(shards: list[torch.Tensor], fused: bool = False, narrow: bool = 
     exchange first (falls back to fused when an input is too large).
     Returns n * 2**(n-1)."""
     p = log2_shards(len(shards))
-    local = shards[0].numel()
-    for s in shards:
-        if s.numel() != local or s.dtype != torch.int64 or not s.is_cuda or not s.is_contiguous():
-            raise BadArguments("shards must be equal-length contiguous CUDA int64 tensors")
+    local = _check_shards(shards)
     n_local = local.bit_length() - 1
     devices = sorted({s.device.index for s in shards})
     if narrow and narrow_ok(local, p):
@@ -225,11 +244,7 @@ def fwht_shards(shards: list[torch.Tensor], fused: bool = False, narrow: bool = 
             _pack(s, pk, f, p)
         if any(int(f.item()) for f in flags):  # (synchronises every device: barrier (i))
             return fwht_shards(shards, fused=True)
-        if len(devices) > 1:
-            for d in devices:
-                with torch.cuda.device(d):
-                    for q in devices:
-                        _lib.check(_lib.lib().bw_enable_peer_access(q))
+        _enable_peers(devices)
         ptrs = [pk.data_ptr() for pk in packed]
         m = local >> p
         for g, s in enumerate(shards):  # device g exchanges slice g of every packed shard
@@ -248,10 +263,7 @@ def fwht_shards(shards: list[torch.Tensor], fused: bool = False, narrow: bool = 
             _local_partial(s, n_local, widths)
         for d in devices:
             torch.cuda.synchronize(d)
-            if len(devices) > 1:
-                with torch.cuda.device(d):
-                    for q in devices:
-                        _lib.check(_lib.lib().bw_enable_peer_access(q))
+        _enable_peers(devices)
         ptrs = [s.data_ptr() for s in shards]
         for g, s in enumerate(shards):  # device g runs its share of K6'
             _fused_pass(ptrs, p, n_local, r, g, s.device)
@@ -267,10 +279,7 @@ def fwht_shards(shards: list[torch.Tensor], fused: bool = False, narrow: bool = 
     if len(devices) > 1:
         for d in devices:  # barrier (i): every local transform done
             torch.cuda.synchronize(d)
-        for d in devices:
-            with torch.cuda.device(d):
-                for q in devices:
-                    _lib.check(_lib.lib().bw_enable_peer_access(q))
+        _enable_peers(devices)
     # Slice g of the local range is exchanged by the device of shard g.
     for g, s in enumerate(shards):
         b, c = slice_of(g, len(shards), local)
@@ -401,6 +410,7 @@ def narrow_step(local: torch.Tensor, nw: NarrowWire, group, dist, p: int, device
 
 
 last_exchange = None  # the exchange the last fwht_distributed call actually ran (diagnostics)
+last_exchanges: list = []  # the exchange of every signal of the last fwht_distributed_many call
 
 
 def fwht_distributed(local: torch.Tensor, group=None, mode: str = "fused", backend=None,
@@ -499,6 +509,8 @@ def fwht_distributed_many(hosts: list, group=None, mode: str = "fused", work=Non
     of each).  Returns n * 2**(n-1) per signal."""
     import torch.distributed as dist
 
+    global last_exchanges
+    last_exchanges = []
     if not hosts:
         return 0
     m = hosts[0].numel()
@@ -528,6 +540,7 @@ def fwht_distributed_many(hosts: list, group=None, mode: str = "fused", work=Non
         cur.wait_event(loaded[b])
         bf = fwht_distributed(work[b], group=group, mode=mode, peer_map=peer_maps[b],
                               narrow_wire=narrow_wires[b])
+        last_exchanges.append(last_exchange)
         done[b].record(cur)
         with torch.cuda.stream(down):
             down.wait_event(done[b])

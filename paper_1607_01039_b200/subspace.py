@@ -19,15 +19,7 @@ import torch
 
 from . import _lib
 from .core import Domain, Signal, _need_cuda, _stream_handle
-from .errors import BadArguments, ValidationError
-
-
-class BadDims(ValidationError):
-    """Linear map dimensions are invalid (errors.py:60)."""
-
-
-class DimMismatch(ValidationError):
-    """Signal dimension does not match the linear map (errors.py:64)."""
+from .errors import BadArguments, BadDims, BadMetadata, DimMismatch
 
 
 def gf2_rank(matrix) -> int:
@@ -107,7 +99,6 @@ def save_map(rows, path: str) -> None:
 def load_map(path: str) -> np.ndarray:
     """subspace.py:296-310: the rows of a map file (BadMetadata on any
     malformed row)."""
-    from .dataset import BadMetadata
 
     try:
         with open(path, "r", encoding="utf-8") as f:

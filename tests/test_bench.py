@@ -34,8 +34,19 @@ def test_reference_arm_contract():
                 "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert key in d, key
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
-    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
+    shipped = os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "bigwht"))
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == ("reference" if shipped else "port")
     assert d["config"]["workload"].startswith("config4")
+    if shipped:
+        assert "bigwht.parallel.run_parallel" in d["cpu_baseline"]["sample"]
+
+
+def test_reference_arm_full_size_run():
+    """--cpu-full: one run of the reference at the full (here small) size,
+    reported beside the extrapolated sample rate."""
+    d = run_bench(["--impl", "reference", "--steps", "1", "--warmup", "0", "--log2n", "16", "--cpu-full"])
+    full = d["cpu_baseline"]["full_size_measured"]
+    assert full["n"] == 16 and full["seconds"] > 0 and full["points_per_s"] > 0
 
 
 @pytest.mark.gpu
@@ -47,6 +58,20 @@ def test_ours_contract_small():
     assert d["roofline"]["bound"] == "hbm" and d["roofline"]["peak"] > 0
     assert d["gpu_launches"] == 3 * len(d["config"]["passes"])
     assert d["e2e"]["h2d_bytes_per_step"] == 8 << 24
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config,n", [(4, 24), (3, 24), (2, 22)])
+def test_ours_parity_in_the_bench_line(config, n):
+    """The CPU baseline leg runs the reference (baseline/_ref when shipped)
+    on a sample; the same run checks it bit-exactly against the GPU, and
+    checks the measured step's own full-size output by the fold spot check."""
+    d = run_bench(["--config", str(config), "--steps", "3", "--warmup", "3", "--log2n", str(n), "--no-e2e"])
+    par = d["parity"]
+    assert par["equal"] is True, par
+    assert par["sample"]["equal"] and par["sample"]["points"] == 1 << n
+    assert par["full_size_spot_check"]["equal"] and par["full_size_spot_check"]["points"] == 1 << 20
+    assert d["cpu_baseline"]["value"] > 0
 
 
 @pytest.mark.gpu
@@ -78,6 +103,7 @@ def test_multirank_narrow_wire_two_processes_one_gpu():
     assert d["config"]["exchange"] == "narrow" and d["config"]["passes"]["fallbacks_to_int64"] == 0
     assert set(d["passes_ms"]) == {"pack_and_agree", "exchange", "local_transform"}
     assert d["nvlink"]["bytes_each_direction"] == (1 << 23) / 2
+    assert "narrow x2" in d["e2e"]["api"] and "fused" not in d["e2e"]["api"], d["e2e"]["api"]
 
 
 @pytest.mark.gpu

@@ -190,3 +190,27 @@ def test_cli_oracle_fold_threads_and_float_extract(tmp_path, coracle, golden_npz
     assert cli.run(["--json", "extract", "--in", wpath, "--threshold", "180.5"]) == 0
     doc = json.loads(capsys.readouterr().out)
     assert [(c["index"], c["coefficient"]) for c in doc["coefficients"]] == oracle_np.extract_above(w, 180.5)
+
+
+def test_cli_ext_refuses_interrupted_reference_run(tmp_path, capsys):
+    """A sidecar carrying the reference executor's pass-progress marker
+    (an interrupted `transform ext`, external.py:155-178) is refused with the
+    reference's messages, before any device work; the payload is untouched."""
+    path = copy_ref_dataset(tmp_path)
+    before = open(path, "rb").read()
+    meta = dataset.read_meta(path)
+    marker = {"mode": "blocked", "mem_log2": 6, "io_block_elems": 8, "passes_done": 1, "total_passes": 3,
+              "writing": False}
+    for writing, resume, needle in ((False, False, "has an interrupted transform (1/3 passes done)"),
+                                    (True, False, "has an interrupted transform (1/3 passes done)"),
+                                    (True, True, "was interrupted after its writes began"),
+                                    (False, True, "cannot resume")):
+        meta["pass_progress"] = dict(marker, writing=writing)
+        with open(path + ".meta.json", "w") as f:
+            json.dump(meta, f)
+        capsys.readouterr()
+        argv = ["transform", "ext", "--in", path, "-b", "6"] + (["--resume"] if resume else [])
+        assert cli.run(argv) == 3
+        assert needle in capsys.readouterr().err
+        assert open(path, "rb").read() == before
+        assert dataset.read_meta(path)["domain"] == "time"

@@ -784,6 +784,45 @@ def test_host_batch_overlapped_signals(coracle, count):
     assert np.array_equal(one, xs[0] << n)
 
 
+@pytest.mark.parametrize("nwork", [2, 3, 4])
+def test_host_batch_reused_buffers_any_work_count(nwork):
+    """bw_fwht_host_batch_i64 with 2-4 device buffers and host lists that
+    repeat a buffer 1..nwork-1 entries later ([h0, h1, h0, h1, ...],
+    [h0, h1, h2, h0, ...]): each use must read the previous use's result
+    (four uses: H^4 x = 2^(2n) x), also for partially overlapping views."""
+    import ctypes
+
+    from paper_1607_01039_b200 import _lib
+
+    n = 20
+    base = [oracle_np.gen(2, 900 + i, [1 << 10], 0, 1 << n) for i in range(3)]
+    works = [torch.empty(1 << n, dtype=torch.int64, device="cuda") for _ in range(nwork)]
+    warr = (ctypes.c_void_p * nwork)(*[w.data_ptr() for w in works])
+    for period in (2, 3):
+        hs = [torch.from_numpy(base[i].copy()).pin_memory() for i in range(period)]
+        seq = [hs[i % period] for i in range(4 * period)]  # every buffer used 4 times: H^4 x = 2^(2n) x
+        arr = (ctypes.c_void_p * len(seq))(*[t.data_ptr() for t in seq])
+        _lib.check(_lib.lib().bw_fwht_host_batch_i64(arr, len(seq), n, warr, nwork,
+                                                     torch.cuda.current_stream().cuda_stream, None))
+        torch.cuda.synchronize()
+        for i in range(period):
+            assert np.array_equal(hs[i].numpy(), base[i] << (2 * n)), (nwork, period, i)
+    # a partial overlap (a view starting inside another signal) also waits
+    big = torch.from_numpy(np.concatenate([base[0], base[1]])).pin_memory()
+    mid = big[(1 << n) // 2:(1 << n) // 2 + (1 << n)]
+    seq = [big[: 1 << n], mid]
+    arr = (ctypes.c_void_p * 2)(*[t.data_ptr() for t in seq])
+    _lib.check(_lib.lib().bw_fwht_host_batch_i64(arr, 2, n, warr, nwork, torch.cuda.current_stream().cuda_stream,
+                                                 None))
+    torch.cuda.synchronize()
+    first = base[0].copy()
+    oracle_np.fwht_array(first)
+    second = np.concatenate([first[(1 << n) // 2:], base[1][: (1 << n) // 2]])
+    oracle_np.fwht_array(second)
+    assert np.array_equal(big.numpy()[(1 << n) // 2:(1 << n) // 2 + (1 << n)], second)
+    assert np.array_equal(big.numpy()[: (1 << n) // 2], first[: (1 << n) // 2])
+
+
 def test_random_plans_on_device(coracle):
     """Random legal plans (tests/plan_fuzz.py) executed on the B200: every
     kernel shape, forced cluster sizes and split-row passes in any position,
