@@ -497,6 +497,71 @@ def fwht_distributed(local: torch.Tensor, group=None, mode: str = "fused", backe
     raise BadArguments(f"unknown mode {mode!r}")
 
 
+def fwht_distributed_extract_ge(local: torch.Tensor, tau: int, group=None, mode: str = "fused",
+                                cap: int = 1 << 16, peer_map: _PeerMap | None = None):
+    """fwht_distributed, then every coefficient of the WHOLE 2**n signal with
+    |W| >= tau (noisy.py:185-222), as (index, value) CUDA tensors sorted by
+    index, on every rank (configs 3/5 over P GPUs).  Must be called by every
+    rank of ``group``.
+
+    mode="fused": the threshold test runs on the fused cross-shard pass's
+    final values (kernel K6' with the extraction epilogue): each rank's tiles
+    span every shard, so its hits carry global indices and are unordered.
+    Other modes: the exchange, then the ordered extraction of this rank's own
+    shard (indices offset by the shard base).  Either way the ranks' lists
+    are gathered (all_gather_object: a few thousand pairs at most) and
+    merged by index."""
+    import torch.distributed as dist
+
+    global last_exchange
+    if tau < 0:
+        raise BadArguments(f"tau must be >= 0, got {tau}")
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    p = log2_shards(world)
+    if not (local.is_cuda and local.dtype == torch.int64 and local.is_contiguous()):
+        raise BadArguments("fwht_distributed_extract needs a contiguous CUDA int64 shard")
+    n_local = local.numel().bit_length() - 1
+    idx = torch.empty(cap, dtype=torch.int64, device=local.device)
+    val = torch.empty(cap, dtype=torch.int64, device=local.device)
+    if mode == "fused" and p > 0 and n_local >= 14:
+        widths, r = fused_plan(n_local, p)
+        _local_partial(local, n_local, widths)
+        pm = peer_map or _PeerMap(local, group, dist)
+        torch.cuda.current_stream(local.device).synchronize()
+        dist.barrier(group)  # (i) every shard's local passes are done
+        count = torch.zeros(1, dtype=torch.int64, device=local.device)
+        _fused_pass_extract(pm.ptrs, p, n_local, r, rank, local.device, int(tau), idx, val, count)
+        torch.cuda.current_stream(local.device).synchronize()
+        dist.barrier(group)  # (ii) every fused pass is done
+        if peer_map is None:
+            pm.close()
+        k = int(count.item())
+        last_exchange = "fused"
+    else:
+        from .extract import extract_ge
+
+        fwht_distributed(local, group=group, mode=mode, peer_map=peer_map)
+        i2, v2 = extract_ge(local, int(tau), base=rank << n_local, cap=cap)
+        k = int(i2.numel())
+        idx[:k] = i2
+        val[:k] = v2
+    if k > cap:
+        raise BadArguments(f"{k} hits on rank {rank} exceed the capacity {cap}")
+    mine = list(zip(idx[:k].tolist(), val[:k].tolist()))
+    every = [None] * world
+    dist.all_gather_object(every, mine, group=group)
+    hits = sorted(h for part in every for h in part)
+    out_i = torch.tensor([h[0] for h in hits], dtype=torch.int64, device=local.device)
+    out_v = torch.tensor([h[1] for h in hits], dtype=torch.int64, device=local.device)
+    return out_i, out_v
+
+
+def fwht_distributed_extract_gt(local: torch.Tensor, tau: int, group=None, mode: str = "fused", **kw):
+    """Config semantics (BASELINE configs 3/5): |W| > tau, sorted by index."""
+    return fwht_distributed_extract_ge(local, int(tau) + 1, group=group, mode=mode, **kw)
+
+
 def fwht_distributed_many(hosts: list, group=None, mode: str = "fused", work=None, peer_maps=None,
                           narrow_wires=None) -> int:
     """fwht_distributed on a sequence of host shards (this rank's pinned

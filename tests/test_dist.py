@@ -182,3 +182,124 @@ def test_distributed_many_two_processes_one_gpu(tmp_path, coracle, mode):
             ref = x.copy()
             coracle.oracle_fwht_i64(ref.ctypes.data, n)
         assert np.array_equal(got, ref), s
+
+
+# ---------------------------------------------- world 4 / 8 on one GPU ---
+#
+# The N > 1 path at the world sizes of an 8 x B200 box, with every rank on
+# the one GPU this build has (gloo for the host barriers, CUDA IPC for the
+# peer pointers).  No kernel waits on another kernel (the barriers are host
+# side), so co-resident ranks are safe.  Configs 4 (n = 24, +-1) and 5
+# (n = 26, 8 planted masks, threshold scaled to 2^29 >> (34 - n)), each
+# exchange mode, with the distributed extraction for config 5.
+
+def _cfg_worker(rank, world, port, cfg, n, out_dir, mode):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from paper_1607_01039_b200 import sharded, signals
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    p = world.bit_length() - 1
+    nl = n - p
+    spec = signals.config(cfg, n)
+    t = torch.empty(1 << nl, dtype=torch.int64, device="cuda")
+    signals.generate(spec, t, base=rank << nl)
+    if spec.threshold is not None:
+        tau = spec.threshold >> (34 - n)
+        i, v = sharded.fwht_distributed_extract_gt(t, tau, mode=mode)
+        np.save(os.path.join(out_dir, f"hits{rank}.npy"), np.stack([i.cpu().numpy(), v.cpu().numpy()]))
+    else:
+        assert sharded.fwht_distributed(t, mode=mode) == n << (n - 1)
+    with open(os.path.join(out_dir, f"mode{rank}.txt"), "w") as f:
+        f.write(str(sharded.last_exchange))
+    np.save(os.path.join(out_dir, f"shard{rank}.npy"), t.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [4, 8])
+@pytest.mark.parametrize("cfg,n", [(4, 24), (5, 26)])
+@pytest.mark.parametrize("mode", ["fused", "peer", "narrow"])
+def test_world_4_8_one_gpu_configs(tmp_path, coracle, world, cfg, n, mode):
+    from oracle import oracle_np
+    from paper_1607_01039_b200 import signals
+
+    mp.spawn(_cfg_worker, args=(world, free_port(), cfg, n, str(tmp_path), mode), nprocs=world, join=True)
+    spec = signals.config(cfg, n)
+    ref = oracle_np.gen(spec.kind, spec.seed, list(spec.params), 0, 1 << n)
+    coracle.oracle_fwht_i64(ref.ctypes.data, n)
+    got = np.concatenate([np.load(tmp_path / f"shard{r}.npy") for r in range(world)])
+    assert np.array_equal(got, ref)
+    ran = {open(tmp_path / f"mode{r}.txt").read() for r in range(world)}
+    assert ran == {mode}, ran  # +-1 and 8-mask inputs both fit the int8 wire at P <= 8
+    if spec.threshold is not None:
+        tau = spec.threshold >> (34 - n)
+        want = oracle_np.extract_gt_by_index(ref, tau)
+        for r in range(world):  # every rank holds the whole merged list
+            h = np.load(tmp_path / f"hits{r}.npy")
+            assert [tuple(map(int, c)) for c in h.T] == [tuple(map(int, w)) for w in zip(*want)]
+        assert sorted(int(i) for i in np.load(tmp_path / "hits0.npy")[0]) == sorted(spec.masks)
+
+
+# ------------------------------------------------ NCCL on the GPU box ---
+
+def _nccl_worker(rank, world, port, out_dir):
+    import ctypes as C
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from oracle import oracle_np
+    from paper_1607_01039_b200 import _lib, sharded
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    # every NCCL call the bench's N > 1 path makes, in a world-size-1 group
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    ones = torch.ones(1, device="cuda")
+    dist.all_reduce(ones)  # the device-side barrier of the timed loop
+    torch.cuda.synchronize()
+    assert ones.item() == world
+    every = [None] * world
+    dist.all_gather_object(every, [(rank, 1)])  # the hit gather of configs 3/5
+    assert every == [[(0, 1)]]
+    t = torch.tensor([1.5], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)  # the max-over-ranks timing
+    results = {}
+    for p in (1, 2, 3):  # the a2a exchange: all_to_all_single, K6 on the [P, m] receive rows, back
+        P, m = 1 << p, 1 << 12
+        x = torch.from_numpy(oracle_np.gen(2, 40 + p, [1 << 20], 0, P * m)).cuda()
+        recv = torch.empty_like(x)
+        dist.all_to_all_single(recv, x)
+        _lib.check(_lib.lib().bw_xshard_strided_i64(recv.data_ptr(), m, p, 0, m,
+                                                    torch.cuda.current_stream().cuda_stream))
+        dist.all_to_all_single(x, recv)
+        rows = oracle_np.gen(2, 40 + p, [1 << 20], 0, P * m).reshape(P, m)
+        for b in range(p):  # P-point WHT across the rows (parallel.py:103-110)
+            for r in range(P):
+                if not (r >> b) & 1:
+                    a, c = rows[r].copy(), rows[r + (1 << b)].copy()
+                    rows[r], rows[r + (1 << b)] = a + c, a - c
+        results[p] = bool(np.array_equal(x.cpu().numpy().reshape(P, m), rows))
+    # the public multi-GPU entry points over an NCCL group (P = 1: local transform only)
+    y = torch.from_numpy(oracle_np.gen(2, 5, [1 << 20], 0, 1 << 16)).cuda()
+    for mode in ("fused", "peer", "a2a", "narrow"):
+        z = y.clone()
+        sharded.fwht_distributed(z, mode=mode)
+        ref = y.cpu().numpy().copy()
+        oracle_np.fwht_array(ref)
+        results[mode] = bool(np.array_equal(z.cpu().numpy(), ref))
+    with open(os.path.join(out_dir, "nccl.txt"), "w") as f:
+        f.write(repr(results))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_calls_world_size_one(tmp_path):
+    mp.spawn(_nccl_worker, args=(1, free_port(), str(tmp_path)), nprocs=1, join=True)
+    res = eval(open(tmp_path / "nccl.txt").read())
+    assert res == {1: True, 2: True, 3: True, "fused": True, "peer": True, "a2a": True, "narrow": True}, res

@@ -47,6 +47,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) k_walk(u64* 
     for (int j = 0; j < 32; ++j) g[c_joff[j]] = v[j] + 1;
 }
 
+// Fill with high-entropy 64-bit values (SplitMix64 of the index): the
+// config-5 passes see such data, the zero-filled walk does not.
+__global__ void k_fill_rand(u64* d, u64 count) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x) {
+        u64 z = i * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        d[i] = z ^ (z >> 31);
+    }
+}
+
 // rows: the 14 - L global row bits, in tile-bit order (the last one is the
 // cluster rank).
 static void run(u64* d, int n, int L, std::vector<int> rows, const char* name) {
@@ -102,12 +113,15 @@ static std::vector<int> cat(std::vector<int> a, std::vector<int> b) {
     return a;
 }
 
-int main() {
+int main(int argc, char** argv) {
+    // argv[1] == "rand": high-entropy data (else zeros, incremented by each walk)
+    const bool rnd = argc > 1 && argv[1][0] == 'r';
     for (int n : {32, 34}) {
         u64* d = nullptr;
         if (cudaMalloc(&d, 8ull << n) != cudaSuccess) return 1;
         cudaMemset(d, 0, 8ull << n);
-        printf("n=%d\n", n);
+        if (rnd) k_fill_rand<<<148 * 8, 512>>>(d, 1ull << n);
+        printf("n=%d data=%s\n", n, rnd ? "random 64-bit" : "zeros");
         if (n == 32) {
             run(d, n, 4, range(13, 23), "contig r10 k13 (current pass 2)");
             run(d, n, 4, range(14, 24), "contig r10 k14");
