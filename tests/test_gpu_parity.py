@@ -324,7 +324,7 @@ def test_argument_errors_before_launch():
     with pytest.raises(errors.BadArguments):
         bw.fwht_array(t.view(4, 4))
     with pytest.raises(errors.BadArguments):
-        bw.fwht_array(t.to(torch.int32))
+        bw.fwht_array(t.to(torch.float32))  # int32 wraps like the reference; other dtypes are refused
     with pytest.raises(errors.BadArguments):
         bw.fwht_array(torch.arange(16, dtype=torch.int64))  # CPU tensor: no CPU path
     assert t.cpu().tolist() == list(range(16))
