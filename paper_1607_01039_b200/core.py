@@ -212,7 +212,8 @@ NARROW_MIN_N = 22  # below this the transform is launch-bound and the flag readb
 def _narrow_wanted(n: int, narrow) -> int:
     """Work-buffer bytes of the narrow-intermediate plan if it should be
     tried for this call, else 0.  narrow=None follows BW_NARROW=1 (off by
-    default: measured no faster than the int64 plan),
+    default: 5% faster at n = 32 on +-1 signals, but it needs a work buffer of
+    3/4 of the signal (24 GiB at n = 32)),
     for n >= NARROW_MIN_N and when the work buffer fits in free device
     memory with 2 GiB left."""
     if narrow is False:
@@ -240,8 +241,9 @@ def fwht_array(buf, narrow=None) -> int:
     (bw_fwht_i64_narrow: int16 / int32 intermediates for signals whose
     values stay within +-32767 after the low pass, e.g. +-1 Boolean
     signals; otherwise the int64 plan runs, results identical either way).
-    It measured no faster than the int64 plan, so the default (None) uses
-    it only when BW_NARROW=1.
+    It measured 5% faster at n = 32 (30.4 vs 32.1 ms, two tiles per CTA) but
+    needs a work buffer of 3/4 of the signal, so the default (None) uses it
+    only when BW_NARROW=1.
     """
     global last_narrow
     last_narrow = False

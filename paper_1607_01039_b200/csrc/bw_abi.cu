@@ -141,8 +141,8 @@ int grid_for(int dev, uint64_t work_items, int threads, int per_sm) {
 // contiguous tiles; w0 = 13, 14 or 15 uses a cluster of 1, 2 or 4 CTAs, and
 // w0 = n <= 12 the single-CTA small kernel) followed by high-bits passes in
 // ascending bit order.  A high width r picks its kernel: r <= 5 the
-// register-only pass, r = 6..8 a single-CTA tile, r = 9 a cluster of 2 and
-// r = 10 a cluster of 4 (so every row segment stays >= 256 B).  Tests may
+// register-only pass, r = 6..8 a single-CTA tile, r = 9 and 10 a cluster of 2
+// (high_default_q; the measured planner below may pick other sizes).  Tests may
 // force the cluster size of a high pass with the entry r | (q + 1) << 4.
 //
 // A high entry r | (q + 1) << 4 | a << 8 | k2 << 12 with a > 0 is a SPLIT
