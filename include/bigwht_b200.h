@@ -165,6 +165,37 @@ int bw_fwht_i64_narrow_pass(int64_t *data, int log2n, void *work, uint64_t work_
 int bw_plan_check_narrow(int log2n);
 
 /*
+ * fwht_array with COMPACT IN-PLACE INTERMEDIATES: for |x| <= lim(n)
+ * (bw_compact_limit; 8191 at n = 32, 2047 at n = 34 -- the +-1 Boolean
+ * signals of the paper and any small-integer signal) the high-bit stages
+ * run first with the signal stored as int32 inside its own buffer, and the
+ * low-bit pass widens back to natural int64: 12 + 8 (m - 1) + 12 bytes per
+ * point for m high passes instead of 16 per pass, and NO work buffer.  Exact:
+ * no int32 intermediate can wrap below the limit, and int64 stages commute
+ * (core.py:84-86), so the result is bit-identical to fwht_array.
+ * max_abs >= 0: the caller's bound on |x| (fwht_inplace computes it first,
+ * core.py:122): <= lim runs the plan asynchronously, above it the int64
+ * plan.  max_abs < 0 (unknown, the fwht_array case): the first pass tests
+ * every input; if any exceeds lim, no tile that saw it wrote anything, the
+ * tiles that did are restored exactly and the int64 plan runs (synchronises
+ * the stream once).  *used_compact: which plan ran.
+ * Reference: fwht_array (core.py:97-117).
+ */
+int bw_fwht_i64_compact(int64_t *data, int log2n, long long max_abs, void *stream, int *used_compact,
+                        uint64_t *butterflies);
+/* lim(n) of the compact plan (-1: none for this n), its pass count (0: none). */
+long long bw_compact_limit(int log2n);
+int bw_compact_npasses(int log2n);
+/* One compact pass, asynchronous (instrumentation); checked = 1 only for pass 0:
+ * tileflag_dev (2^(n-13) words, zeroed) and *abort_dev (zeroed) record the outcome. */
+int bw_fwht_i64_compact_pass(int64_t *data, int log2n, int pass_index, int checked, uint32_t *tileflag_dev,
+                             uint32_t *abort_dev, void *stream);
+/* Test hook: the exact restore of the tiles a checked pass 0 wrote. */
+int bw_fwht_i64_compact_restore(int64_t *data, int log2n, uint32_t *tileflag_dev, void *stream);
+/* Test hook: static check of the compact plan (in place, layouts, coverage), 16 <= n <= 24. */
+int bw_plan_check_compact(int log2n);
+
+/*
  * float64 fwht_array (core.py:97-117 on a float64 Signal, core.py:56-59):
  * stages applied strictly in ascending order with the same IEEE a+b / a-b
  * as numpy, so results are bitwise identical to the reference (the order

@@ -230,7 +230,24 @@ def _narrow_wanted(n: int, narrow) -> int:
     return need
 
 
-def fwht_array(buf, narrow=None) -> int:
+last_compact = False  # whether the last fwht_array call ran the compact in-place plan (diagnostics)
+COMPACT_MIN_N = 22  # below this the checked plan's one stream synchronisation outweighs the bytes it saves
+
+
+def _compact_wanted(n: int, compact) -> bool:
+    """Whether fwht_array tries the compact in-place plan (int32
+    intermediates inside the signal's own buffer, bw_fwht_i64_compact).
+    compact=None follows BW_COMPACT (off unless "1": the plan moves a third
+    fewer bytes but measured no faster) for
+    n >= COMPACT_MIN_N."""
+    if compact is False or _lib.lib().bw_compact_npasses(n) == 0:
+        return False
+    if compact is None:
+        return os.environ.get("BW_COMPACT", "0") == "1" and n >= COMPACT_MIN_N
+    return True
+
+
+def fwht_array(buf, narrow=None, compact=None) -> int:
     """Transform ``buf`` (length 2**n, contiguous) in place (core.py:97-117).
 
     Stage k pairs elements at stride 2**k and replaces (a, b) with
@@ -244,9 +261,19 @@ def fwht_array(buf, narrow=None) -> int:
     It measured 5% faster at n = 32 (30.4 vs 32.1 ms, two tiles per CTA) but
     needs a work buffer of 3/4 of the signal, so the default (None) uses it
     only when BW_NARROW=1.
+
+    compact (CUDA int64 tensors): the compact in-place plan
+    (bw_fwht_i64_compact) -- the high-bit stages first with the signal kept
+    as int32 inside its own buffer, then the low pass widening back to int64.
+    Its first pass tests every input against lim(n) (8191 at n = 32); if one
+    is larger, the tiles already written are restored exactly and the int64
+    plan runs.  Results are identical either way.  None: only with
+    BW_COMPACT=1 (n >= 22); True: the checked plan; an int: a bound on |x|
+    the caller guarantees (no test, no synchronisation).
     """
-    global last_narrow
+    global last_narrow, last_compact
     last_narrow = False
+    last_compact = False
     _check_contiguous(buf)
     if buf.ndim == 1 and _length(buf) == 0:
         return 0  # core.py:106-107: n = -1, no stage runs
@@ -274,7 +301,15 @@ def fwht_array(buf, narrow=None) -> int:
     _require_cuda(buf)
     with torch.cuda.device(buf.device):
         need = _narrow_wanted(n, narrow) if kind == "i64" else 0
-        if need:
+        if kind == "i64" and not need and _compact_wanted(n, compact):
+            used = ctypes.c_int(0)
+            bound = -1 if compact is None or compact is True else int(compact)
+            if bound < -1:
+                raise BadArguments(f"compact bound must be >= 0, got {bound}")
+            _lib.check(L.bw_fwht_i64_compact(buf.data_ptr(), n, bound, _stream_handle(buf), ctypes.byref(used),
+                                             ctypes.byref(bf)))
+            last_compact = bool(used.value)
+        elif need:
             work = torch.empty(need, dtype=torch.uint8, device=buf.device)
             used = ctypes.c_int(0)
             _lib.check(L.bw_fwht_i64_narrow(buf.data_ptr(), n, work.data_ptr(), need, _stream_handle(buf),

@@ -69,6 +69,11 @@ const bool g_two_pass = !(getenv("BW_TWO_PASS") && getenv("BW_TWO_PASS")[0] == '
 // BW_NARROW_TPC=1|2|4: tiles per CTA (or cluster) of the narrow plan's high passes (default 2,
 // measured best: n = 32 in 30.4 ms against 31.6 with one tile; four spill).
 const int g_narrow_tpc = getenv("BW_NARROW_TPC") ? atoi(getenv("BW_NARROW_TPC")) : 2;
+// BW_SPLIT_CT=0: split-row passes read their offsets from the table (A/B knob).
+const bool g_split_ct = !(getenv("BW_SPLIT_CT") && getenv("BW_SPLIT_CT")[0] == '0');
+// BW_COMPACT=1: fwht_inplace picks the compact in-place plan when its bound
+// allows (opt-in: measured no faster than the int64 plan).
+const bool g_compact = getenv("BW_COMPACT") && getenv("BW_COMPACT")[0] == '1';
 // BW_FOLD_BLOCKS=0 keeps the shared-bin / L2-atomic fold for d_out > 12 (A/B knob, read per call).
 bool fold_blocks_enabled() { return !(getenv("BW_FOLD_BLOCKS") && getenv("BW_FOLD_BLOCKS")[0] == '0'); }
 // BW_F64_VEC_LOW=0 keeps the float64 low pass on 8-byte accesses (A/B knob).
@@ -312,11 +317,15 @@ bool env_plan(int n, std::vector<int>* widths) {
 }
 
 // Split-row passes on a cluster of 2 (9 or 10 rows: a low rows right above
-// the low pass plus the top rows of the signal), TB/s x 100 by a = 1..9.
-// Measured by tools/sweep_split.py at n = 32, 33, 34 (profiles/
-// r01_split_n*.json): the rate depends on a (how many rows share a DRAM
-// page neighbourhood), not on n or on where the top run starts.
-constexpr int kSplitEff[10] = {0, 552, 566, 572, 580, 583, 583, 583, 583, 583};
+// the low pass plus the top rows of the signal), TB/s x 100 by rows (9, 10)
+// and a = 1..9.  Measured by tools/sweep_split.py at n = 32, 33, 34 with the
+// compile-time-offset kernel (k_pass_split<..., A>; profiles/r02_split_n*.json,
+// median over n and the low-pass width): the rate depends on a (how many rows
+// share a DRAM page neighbourhood), not on n or on where the top run starts.
+// (The offset-table kernel measured 5.52-5.83 for every a, r01_split_n*.json.)
+constexpr int kSplitEff[2][10] = {
+    {0, 648, 645, 615, 651, 640, 635, 645, 649, 0},     // 9 rows
+    {0, 571, 602, 609, 619, 628, 630, 628, 624, 615}};  // 10 rows
 
 // Three-pass plans with a split pass: low w0, the split pass (rows
 // [w0, w0+a) u [n-(rs-a), n)), and one contiguous pass over the bits in
@@ -339,7 +348,8 @@ long long best_split_plan(int n, int w0, std::vector<int>* out) {
                     entry = rm | (1 << 4);
                 }
             }
-            const long long cost = 1000000 / kSplitEff[a] + 1000000 / em;
+            if (!kSplitEff[rs - 9][a]) continue;
+            const long long cost = 1000000 / kSplitEff[rs - 9][a] + 1000000 / em;
             if (best < 0 || cost < best) {
                 best = cost;
                 out->assign({rs | (2 << 4) | (a << 8) | (k2 << 12), entry});
@@ -376,7 +386,7 @@ int default_plan(int n, std::vector<int>* widths) {
             widths->assign(1, w0);
             widths->insert(widths->end(), hi.begin(), hi.end());
         }
-        if (g_split_plans) {
+        if (g_split_plans && n >= 32) {  // measured at n = 32..34 (profiles/r02_split_n*.json)
             const long long sc = best_split_plan(n, w0, &hi);
             if (sc >= 0 && 1000000 / kLowEff[w0 - 13] + sc < best_cost) {
                 best_cost = 1000000 / kLowEff[w0 - 13] + sc;
@@ -559,6 +569,18 @@ int set_two_pass_attr() {
     return BW_OK;
 }
 
+// k_pass_split with a compile-time low-run length A: dynamic shared memory
+// attributes for every A (1 <= A < rows).
+template <class C, int L, int A>
+int split_ct_attributes(int smem) {
+    if constexpr (A < C::T - L) {
+        BW_CUDA(cudaFuncSetAttribute(bw::k_pass_split<C, L, false, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        BW_CUDA(cudaFuncSetAttribute(bw::k_pass_split<C, L, true, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        return split_ct_attributes<C, L, A + 1>(smem);
+    }
+    return BW_OK;
+}
+
 int set_all_pass_attributes() {
     for (int r = 1; r <= 8; ++r) {
         const Pass p{r <= bw::kRegOnlyMaxBits ? REG : HIGH, 13, r, 0};
@@ -591,6 +613,10 @@ int set_all_pass_attributes() {
         if constexpr (bw::SplitOf<C>::value) {
             BW_CUDA(cudaFuncSetAttribute(bw::k_pass_split<C, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             BW_CUDA(cudaFuncSetAttribute(bw::k_pass_split<C, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            if constexpr (C::Q == 1) {
+                const int rc_ = split_ct_attributes<C, L, 1>(smem);
+                if (rc_ != BW_OK) return rc_;
+            }
         } else if (smem > 48 * 1024) {
             BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             BW_CUDA(cudaFuncSetAttribute(bw::k_pass<C, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -625,6 +651,20 @@ int launch_cfg(void (*kern)(KArgs...), unsigned grid, cudaStream_t s, Args... ar
     cfg.numAttrs = C::Q > 0 ? 1 : 0;
     BW_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
     return BW_OK;
+}
+
+// k_pass_split with the low-run length a as a compile-time A (1 <= A <
+// rows), by recursion over A.
+template <class C, int L, int A>
+int launch_split_ct(int a, bool extract, unsigned grid, cudaStream_t s, u64* d, int karg, bw::ExtractArgs ex,
+                    const bw::SplitTab& tab) {
+    if constexpr (A < C::T - L) {
+        if (a == A)
+            return launch_cfg<C>(extract ? bw::k_pass_split<C, L, true, A> : bw::k_pass_split<C, L, false, A>, grid, s,
+                                 d, karg, ex, tab);
+        return launch_split_ct<C, L, A + 1>(a, extract, grid, s, d, karg, ex, tab);
+    }
+    return fail(BW_BAD_ARGUMENTS, "split pass with a = %d low rows", a);
 }
 
 // Element offsets of every register index in the load and the store round
@@ -663,6 +703,10 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractA
         const void* none = nullptr;
         if constexpr (bw::SplitOf<C>::value) {
             const bw::SplitTab tab = split_table<C, L>(p.karg());
+            if constexpr (C::Q == 1) {  // compile-time low-run length (no offset table)
+                if (g_split_ct && p.a >= 1 && p.a < C::T - L)
+                    return launch_split_ct<C, L, 1>(p.a, ex.count != nullptr, grid, s, d, p.karg(), ex, tab);
+            }
             if (ex.count) return launch_cfg<C>(bw::k_pass_split<C, L, true>, grid, s, d, p.karg(), ex, tab);
             return launch_cfg<C>(bw::k_pass_split<C, L, false>, grid, s, d, p.karg(), ex, tab);
         } else {
@@ -1035,8 +1079,13 @@ int bw_check_bound_i64(const int64_t* data, int log2n, int64_t* scratch_dev, voi
 }
 
 // fwht_inplace (core.py:120-125): bound first (raise before mutation), then transform.
+// The bound M it computes also picks the plan: M <= lim(n) runs the compact
+// in-place plan (int32 intermediates, bw_fwht_i64_compact), else int64.
 int bw_fwht_inplace_i64(int64_t* data, int log2n, int64_t* scratch_dev, void* stream, uint64_t* butterflies) {
-    BW_TRY(bw_check_bound_i64(data, log2n, scratch_dev, stream, nullptr));
+    uint64_t m = 0;
+    BW_TRY(bw_check_bound_i64(data, log2n, scratch_dev, stream, &m));
+    if (g_compact && m <= (uint64_t)0x7fffffff)
+        return bw_fwht_i64_compact(data, log2n, (long long)m, stream, nullptr, butterflies);
     return bw_fwht_i64(data, log2n, stream, butterflies);
 }
 
@@ -1051,6 +1100,7 @@ int bw_fwht_inplace_known_i64(int64_t* data, int log2n, int64_t max_abs, void* s
         return fail(BW_OVERFLOW_BOUND,
                     "max |x| = %llu with n = %d can overflow int64; need |x| * 2**n < 2**63",
                     (unsigned long long)max_abs, log2n);
+    if (g_compact && max_abs <= 0x7fffffff) return bw_fwht_i64_compact(data, log2n, max_abs, stream, nullptr, butterflies);
     return bw_fwht_i64(data, log2n, stream, butterflies);
 }
 
@@ -1374,6 +1424,415 @@ int bw_fwht_i64_narrow(int64_t* data, int log2n, void* work, uint64_t work_bytes
     if (bad) return fwht_impl(data, log2n, nullptr, false, s);  // data untouched: the int64 plan
     for (size_t i = 1; i < passes.size(); ++i) BW_TRY(narrow_pass(data, log2n, work, passes, (int)i, flag, s));
     if (used_narrow) *used_narrow = 1;
+    return BW_OK;
+}
+
+}  // extern "C"
+namespace {
+// ---- compact in-place intermediates (bw_fwht_i64_compact) -----------------
+//
+// For signals with small values (the +-1 Boolean signals of the paper, any
+// |x| <= lim(n)) every pass but the last can keep the signal as int32, and
+// the signal's own buffer holds the int32 copy: no work buffer.  Stages
+// commute (Z/2^64), so the plan runs its HIGH passes first, in int32, and the
+// low pass last, which widens to int64 and writes the natural order:
+//   P1: natural int64 -> int32,  P2..Pm: int32 -> int32,  C: int32 -> int64
+// = 12 + 8*(m-1) + 12 bytes per point instead of 16 * (m+1).
+//
+// Layouts.  w = the low pass's width (13 or 14 bits), c = w - 1.  A "block"
+// is the 2^w contiguous int64 slots of one low-pass tile = 2^(w+1) int32
+// slots; its half h holds the int32 copy of the block's 2^w elements:
+//   int32 slot = block << (w+1) | h << w | perm(i mod 2^w),
+//   perm: i0..i3 -> slot bits 0..3, i_c -> bit 4, i4..i_(c-1) -> bits 5..c.
+// Every high pass's tile contains the bits {0,1,2,3,c} (plus low bits 4, 5,
+// .. when it has fewer than 9 stage rows) as its non-stage "columns", so a
+// 128-byte int32 segment is 32 elements of ONE tile for every pass.
+// In-place safety (bw_plan_check_compact proves it on the exact tables):
+//   P1 reads every int64 slot; tile t's outputs land in its own rows with
+//     i_c = h (it contains bit c), i.e. inside what t itself read.
+//   P_j (j >= 2) reads half h_(j-1) and writes the other half, which no tile
+//     reads in that pass.
+//   C reads the half of its own block and writes the whole block.
+// lim(n) = (2^31 - 1) >> (n - w): no int32 value of the high passes wraps.
+// Unknown magnitudes: P1 tests every input; a tile with |x| > lim (or one
+// that starts after another failed) writes nothing and every CTA of its
+// cluster agrees; written tiles are marked.  After a failure the marked
+// tiles are restored exactly -- P1's stages again on their int32 copy, then
+// >> r1 (H H = 2^r1 I) -- and the int64 plan runs.
+struct CompactPlan {
+    int n = 0, w = 0, c = 0, m = 0;  // m high passes, then the low pass
+    std::vector<Pass> pass;           // shapes for the kernel visitor
+    std::vector<PassGeom> geom;
+    std::vector<int> half;            // half written by high pass j
+    long long lim = 0;
+};
+
+// BW_COMPACT_ROWS="r1,r2,..": stage rows of the high passes (experiments;
+// default: balanced, at most 9).  BW_COMPACT_W=13|14: the low pass width.
+bool compact_plan(int n, CompactPlan* cp) {
+    if (n < 16 || n > 36) return false;
+    int w = n <= 31 ? 13 : 14;
+    if (const char* e = getenv("BW_COMPACT_W")) w = atoi(e) == 14 ? 14 : 13;
+    const int H = n - w;
+    std::vector<int> rows;
+    if (const char* e = getenv("BW_COMPACT_ROWS")) {
+        int sum = 0;
+        for (const char* q = e; *q;) {
+            const int r = atoi(q);
+            rows.push_back(r);
+            sum += r;
+            while (*q && *q != ',') ++q;
+            if (*q == ',') ++q;
+        }
+        if (sum != H) return false;
+    } else {
+        const int m = (H + 8) / 9;
+        for (int j = 0; j < m; ++j) rows.push_back(H / m + (j < H % m ? 1 : 0));
+    }
+    if (rows.empty() || rows.size() > 4) return false;
+    cp->n = n;
+    cp->w = w;
+    cp->c = w - 1;
+    cp->m = (int)rows.size();
+    cp->lim = 0x7fffffffll >> H;
+    cp->pass.clear();
+    cp->geom.clear();
+    cp->half.clear();
+    int k = w;
+    for (int j = 0; j < cp->m; ++j) {
+        const int r = rows[j];
+        if (r < 1 || r > 9) return false;
+        Pass p;
+        p.kind = r <= 5 ? REG : HIGH;
+        p.q = r <= 5 ? 0 : 1;
+        p.k = k;
+        p.r = r;
+        const int T = r <= 5 ? bw::CfgReg::T : bw::CfgHigh14c::T;
+        PassGeom g;
+        g.T = T;
+        g.L = T - r;
+        int vb = 0;
+        for (int b = 0; b < 4; ++b) g.gb[vb++] = b;
+        g.gb[vb++] = cp->c;
+        for (int b = 4; vb < g.L; ++b) g.gb[vb++] = b;  // extra columns: low bits 4, 5, .. (all < c)
+        for (int i = 0; i < r; ++i) g.gb[vb++] = k + i;
+        g.tile_mask = 0;
+        for (int i = 0; i < T; ++i) g.tile_mask |= 1ull << g.gb[i];
+        cp->pass.push_back(p);
+        cp->geom.push_back(g);
+        cp->half.push_back((cp->m - 1 - j) & 1);  // the last high pass writes half 0
+        k += r;
+    }
+    Pass low;
+    low.kind = LOW;
+    low.q = w == 14 ? 1 : 0;
+    low.k = 0;
+    low.r = w;
+    PassGeom g;
+    g.T = w;
+    g.L = w;
+    for (int b = 0; b < w; ++b) g.gb[b] = b;
+    g.tile_mask = (1ull << w) - 1ull;
+    cp->pass.push_back(low);
+    cp->geom.push_back(g);
+    return true;
+}
+
+// int32 layout of the half-block copies (offset bit of every index bit; the
+// half h is the pointer offset h << w).
+Layout compact_layout(const CompactPlan& cp) {
+    Layout o;
+    for (int b = 0; b < 64; ++b) o.pos[b] = -1;
+    for (int b = 0; b < 4; ++b) o.pos[b] = b;
+    o.pos[cp.c] = 4;
+    for (int b = 4; b < cp.c; ++b) o.pos[b] = b + 1;
+    for (int b = cp.w; b < cp.n; ++b) o.pos[b] = b + 1;
+    if (getenv("BW_COMPACT_BREAK")) {  // test hook: NOT in place (bit c trades places with the top bit)
+        const int t = o.pos[cp.c];
+        o.pos[cp.c] = o.pos[cp.n - 1];
+        o.pos[cp.n - 1] = t;
+    }
+    return o;
+}
+
+template <class F>
+int visit_compact(const Pass& p, F&& f) {
+    if (p.kind == LOW) {
+        if (p.q == 0) return f(tag<bw::CfgLow13>{}, ic<13>{});
+        return f(tag<bw::CfgLow14c>{}, ic<14>{});
+    }
+    if (p.kind == REG) return with_L<bw::CfgReg, 8, 12>(bw::CfgReg::T - p.r, f);
+    if (p.kind == HIGH && p.q == 1) return with_L<bw::CfgHigh14c, 5, 8>(bw::CfgHigh14c::T - p.r, f);
+    return fail(BW_BAD_ARGUMENTS, "no compact form of this pass shape");
+}
+
+enum CompactMode { COMPACT_PLAIN, COMPACT_CHECK, COMPACT_RESTORE };
+
+// Pass i of the compact plan (i < m: high pass i; i == m: the low pass).
+// mode CHECK / RESTORE apply to pass 0 only.
+int launch_compact(const CompactPlan& cp, int i, int64_t* data, CompactMode mode, unsigned* tileflag,
+                   unsigned* abort, cudaStream_t s) {
+    const Layout nat = natural_layout(cp.n), lam = compact_layout(cp);
+    int* d32 = reinterpret_cast<int*>(data);
+    long long* d64 = reinterpret_cast<long long*>(data);
+    const Pass& p = cp.pass[i];
+    const PassGeom& g = cp.geom[i];
+    const int tpc = getenv("BW_COMPACT_TPC") ? atoi(getenv("BW_COMPACT_TPC")) : 1;
+    return visit_compact(p, [&](auto t, auto l) -> int {
+        using C = typename decltype(t)::type;
+        constexpr int L = decltype(l)::value;
+        constexpr bool kLow = L >= C::T;
+        bw::MapArgs m;
+        memset(&m, 0, sizeof m);
+        m.tileflag = tileflag;
+        m.abort = abort;
+        m.lim = cp.lim;
+        const unsigned grid = (unsigned)(1ull << (cp.n - bw::kCtaBits));
+        constexpr int smem = bw::Dims<C>::SMEM_BYTES;
+        auto go = [&](auto kern, unsigned gr, int sm_bytes, const auto* sp, auto* dp) -> int {
+            if (sm_bytes > 48 * 1024)
+                BW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_bytes));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(gr);
+            cfg.blockDim = dim3(bw::Dims<C>::NT);
+            cfg.dynamicSmemBytes = sm_bytes;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = bw::Dims<C>::CLUSTER;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = C::Q > 0 ? 1 : 0;
+            BW_CUDA(cudaLaunchKernelEx(&cfg, kern, sp, dp, (unsigned*)nullptr, m));
+            return BW_OK;
+        };
+        if constexpr (kLow) {
+            if (i != cp.m) return fail(BW_BAD_ARGUMENTS, "the low pass is the compact plan's last");
+            fill_layout_tab<C, 0>(g, cp.n, lam, &m.ld);
+            fill_layout_tab<C, C::NR - 1>(g, cp.n, nat, &m.st);
+            if (m.ld.nruns > 6 || m.st.nruns > 6) return fail(BW_BAD_ARGUMENTS, "layout needs too many runs");
+            return go(bw::k_pass_map<C, L, int, long long>, grid, smem, d32 + ((size_t)cp.half[cp.m - 1] << cp.w), d64);
+        } else {
+            if (i >= cp.m) return fail(BW_BAD_ARGUMENTS, "bad compact pass %d", i);
+            int* dst32 = d32 + ((size_t)cp.half[i] << cp.w);
+            if (i == 0) {
+                if (mode == COMPACT_RESTORE) {  // the int32 copy -> P1's stages again -> >> r -> natural int64
+                    fill_layout_tab<C, 0>(g, cp.n, lam, &m.ld);
+                    fill_layout_tab<C, C::NR - 1>(g, cp.n, nat, &m.st);
+                    m.shift = p.r;
+                    return go(bw::k_pass_map<C, L, int, long long, 1, bw::MAP_RESTORE>, grid, smem, dst32, d64);
+                }
+                fill_layout_tab<C, 0>(g, cp.n, nat, &m.ld);
+                fill_layout_tab<C, C::NR - 1>(g, cp.n, lam, &m.st);
+                if (mode == COMPACT_CHECK)
+                    return go(bw::k_pass_map<C, L, long long, int, 1, bw::MAP_CHECK>, grid,
+                              smem + (C::Q > 0 ? 8 * bw::Dims<C>::CLUSTER : 0), d64, dst32);
+                return go(bw::k_pass_map<C, L, long long, int>, grid, smem, d64, dst32);
+            }
+            fill_layout_tab<C, 0>(g, cp.n, lam, &m.ld);
+            fill_layout_tab<C, C::NR - 1>(g, cp.n, lam, &m.st);
+            const int* src32 = d32 + ((size_t)cp.half[i - 1] << cp.w);
+            if constexpr (C::Q <= 1) {
+                if (tpc == 2) return go(bw::k_pass_map<C, L, int, int, 2>, grid / 2, smem, src32, dst32);
+            }
+            return go(bw::k_pass_map<C, L, int, int>, grid, smem, src32, dst32);
+        }
+    });
+}
+
+int compact_scratch(int dev, const CompactPlan& cp, unsigned** tileflag, unsigned** abort, cudaStream_t s) {
+    const size_t tiles = 1ull << (cp.n - cp.geom[0].T);
+    void* sc = nullptr;
+    BW_TRY(scratch(dev, 64 + 4 * tiles, &sc));
+    *abort = reinterpret_cast<unsigned*>(sc);
+    *tileflag = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(sc) + 64);
+    BW_CUDA(cudaMemsetAsync(sc, 0, 64 + 4 * tiles, s));
+    return BW_OK;
+}
+}  // namespace
+extern "C" {
+
+long long bw_compact_limit(int log2n) {
+    CompactPlan cp;
+    if (log2n < 0 || log2n > BW_MAX_LOG2N || !compact_plan(log2n, &cp)) return -1;
+    return cp.lim;
+}
+
+int bw_compact_npasses(int log2n) {
+    CompactPlan cp;
+    if (log2n < 0 || log2n > BW_MAX_LOG2N || !compact_plan(log2n, &cp)) return 0;
+    return cp.m + 1;
+}
+
+// One pass of the compact plan, asynchronous (benchmark instrumentation):
+// checked = 1 runs pass 0 with the input test (then *abort_dev says whether
+// it wrote nothing-or-everything; tileflag_dev holds 2^(n-13) words).
+int bw_fwht_i64_compact_pass(int64_t* data, int log2n, int pass_index, int checked, uint32_t* tileflag_dev,
+                             uint32_t* abort_dev, void* stream) {
+    BW_TRY(check_signal(data, log2n));
+    CompactPlan cp;
+    if ((reinterpret_cast<uintptr_t>(data) & 15u) || !compact_plan(log2n, &cp))
+        return fail(BW_BAD_ARGUMENTS, "no compact plan for this signal (n = %d)", log2n);
+    if (pass_index < 0 || pass_index > cp.m) return fail(BW_BAD_ARGUMENTS, "bad compact pass %d", pass_index);
+    if (checked && (pass_index != 0 || !tileflag_dev || !abort_dev))
+        return fail(BW_BAD_ARGUMENTS, "only pass 0 is checked, with tile flags and an abort word");
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    return launch_compact(cp, pass_index, data, checked ? COMPACT_CHECK : COMPACT_PLAIN,
+                          reinterpret_cast<unsigned*>(tileflag_dev), reinterpret_cast<unsigned*>(abort_dev),
+                          as_stream(stream));
+}
+
+// fwht_array with compact in-place intermediates.  max_abs >= 0: the
+// caller's bound on |x| (fwht_inplace has just computed it); <= lim(n) runs
+// the compact plan unchecked and asynchronously, above it the int64 plan.
+// max_abs < 0: unknown -- pass 0 tests every input (synchronises the stream
+// once); on a failure the written tiles are restored and the int64 plan runs.
+// *used_compact says which plan produced the result (bit-identical anyway).
+int bw_fwht_i64_compact(int64_t* data, int log2n, long long max_abs, void* stream, int* used_compact,
+                        uint64_t* butterflies) {
+    BW_TRY(check_signal(data, log2n));
+    if (used_compact) *used_compact = 0;
+    if (butterflies) *butterflies = butterfly_count(log2n);
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    cudaStream_t s = as_stream(stream);
+    CompactPlan cp;
+    if ((reinterpret_cast<uintptr_t>(data) & 15u) || !compact_plan(log2n, &cp) || max_abs > cp.lim)
+        return fwht_impl(data, log2n, nullptr, false, s);
+    if (max_abs >= 0) {
+        for (int i = 0; i <= cp.m; ++i) BW_TRY(launch_compact(cp, i, data, COMPACT_PLAIN, nullptr, nullptr, s));
+        if (used_compact) *used_compact = 1;
+        return BW_OK;
+    }
+    unsigned *tileflag = nullptr, *abort = nullptr;
+    BW_TRY(compact_scratch(dev, cp, &tileflag, &abort, s));
+    BW_TRY(launch_compact(cp, 0, data, COMPACT_CHECK, tileflag, abort, s));
+    unsigned bad = 0;
+    BW_CUDA(cudaMemcpyAsync(&bad, abort, sizeof bad, cudaMemcpyDeviceToHost, s));
+    BW_CUDA(cudaStreamSynchronize(s));
+    if (bad) {
+        BW_TRY(launch_compact(cp, 0, data, COMPACT_RESTORE, tileflag, abort, s));
+        return fwht_impl(data, log2n, nullptr, false, s);
+    }
+    for (int i = 1; i <= cp.m; ++i) BW_TRY(launch_compact(cp, i, data, COMPACT_PLAIN, nullptr, nullptr, s));
+    if (used_compact) *used_compact = 1;
+    return BW_OK;
+}
+
+// Test hook: restore after a checked pass 0 (the fallback's first step),
+// asynchronous.  tileflag_dev / abort_dev as bw_fwht_i64_compact_pass left them.
+int bw_fwht_i64_compact_restore(int64_t* data, int log2n, uint32_t* tileflag_dev, void* stream) {
+    BW_TRY(check_signal(data, log2n));
+    CompactPlan cp;
+    if ((reinterpret_cast<uintptr_t>(data) & 15u) || !compact_plan(log2n, &cp) || !tileflag_dev)
+        return fail(BW_BAD_ARGUMENTS, "no compact plan for this signal (n = %d) or no tile flags", log2n);
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    return launch_compact(cp, 0, data, COMPACT_RESTORE, reinterpret_cast<unsigned*>(tileflag_dev), nullptr,
+                          as_stream(stream));
+}
+
+// Static checker of the compact plan (TEST HOOK, 16 <= n <= 24): runs the
+// kernels' exact address tables for every element of every pass and checks
+//   - pass 0 loads natural int64, the last pass stores natural int64;
+//   - pass i+1 loads every element at the bytes (and width) pass i stored it;
+//   - no two stores of a pass overlap, every access stays in the buffer;
+//   - IN PLACE: no tile stores into bytes another tile of the same pass
+//     loads (4-byte granules; cluster tiles count as one tile);
+//   - every index bit is staged by exactly one pass.
+int bw_plan_check_compact(int log2n) {
+    if (log2n < 16 || log2n > 24) return fail(BW_BAD_ARGUMENTS, "compact plan check supports 16 <= n <= 24");
+    CompactPlan cp;
+    if (!compact_plan(log2n, &cp)) return fail(BW_BAD_ARGUMENTS, "no compact plan for n = %d", log2n);
+    const uint64_t N = 1ull << log2n, G = 2 * N;  // 4-byte granules of the buffer
+    const Layout nat = natural_layout(log2n), lam = compact_layout(cp);
+    std::vector<uint64_t> ld(N), st(N), prev(N);
+    std::vector<uint8_t> ldw(N), stw(N), prevw(N);
+    std::vector<int32_t> reader(G), writer(G);
+    uint64_t staged = 0;
+    auto base_of = [](const bw::LayoutTab& t, uint64_t tile, uint32_t vt) {
+        unsigned long long off = 0;
+        for (int r = 0; r < t.nruns; ++r) off += ((tile >> t.rsrc[r]) & ((1ull << t.rlen[r]) - 1ull)) << t.rdst[r];
+        for (int b = 0; b < 16; ++b)
+            if ((vt >> b) & 1u) off += t.bit[b];
+        return off;
+    };
+    for (int q = 0; q <= cp.m; ++q) {
+        const int ok = visit_compact(cp.pass[q], [&](auto t, auto l) -> int {
+            using C = typename decltype(t)::type;
+            constexpr int L = decltype(l)::value;
+            constexpr int NQ = 1 << C::Q, LAST = C::NR - 1;
+            const PassGeom& g = cp.geom[q];
+            const bool low = q == cp.m;
+            // source / destination: layout, element bytes, element offset of the pointer
+            const Layout& sl = q == 0 ? nat : lam;
+            const Layout& dl = low ? nat : lam;
+            const int sb = q == 0 ? 8 : 4, db = low ? 8 : 4;
+            const uint64_t so = q == 0 ? 0 : (uint64_t)cp.half[q - 1] << cp.w;
+            const uint64_t dof = low ? 0 : (uint64_t)cp.half[q] << cp.w;
+            bw::LayoutTab tl, ts, tgi, tgo;
+            fill_layout_tab<C, 0>(g, log2n, sl, &tl);
+            fill_layout_tab<C, LAST>(g, log2n, dl, &ts);
+            fill_layout_tab<C, 0>(g, log2n, nat, &tgi);  // global index of the loaded element
+            fill_layout_tab<C, LAST>(g, log2n, nat, &tgo);
+            for (int vb = L >= C::T ? 0 : L; vb < C::T; ++vb) {  // a low pass stages its whole tile
+                if ((staged >> g.gb[vb]) & 1) return fail(BW_BAD_ARGUMENTS, "bit %d staged twice", g.gb[vb]);
+                staged |= 1ull << g.gb[vb];
+            }
+            std::fill(reader.begin(), reader.end(), -1);
+            std::fill(writer.begin(), writer.end(), -1);
+            const uint64_t ctas = 1ull << (log2n - bw::kCtaBits);
+            for (int phase = 0; phase < 2; ++phase) {  // loads first (owners), then stores
+                for (uint64_t cta = 0; cta < ctas; ++cta) {
+                    const uint32_t rank = (uint32_t)(cta & (NQ - 1));
+                    const int32_t tile = (int32_t)(cta >> C::Q);
+                    for (uint32_t th = 0; th < (uint32_t)bw::Dims<C>::NT; ++th) {
+                        const uint32_t lane = th & 31u, warp = th >> 5;
+                        const uint32_t v0 = bw::thread_part<C, 0>(lane, warp) | bw::rank_bits<C, 0>(rank);
+                        const uint32_t v1 = bw::thread_part<C, LAST>(lane, warp) | bw::rank_bits<C, LAST>(rank);
+                        for (int j = 0; j < bw::Dims<C>::E; ++j) {
+                            if (phase == 0) {
+                                const uint64_t gi = base_of(tgi, tile, v0) + tgi.reg[j];
+                                const uint64_t a = (so + base_of(tl, tile, v0) + tl.reg[j]) * sb;
+                                if (gi >= N || a + sb > 8 * N) return fail(BW_BAD_ARGUMENTS, "pass %d loads outside", q);
+                                ld[gi] = a;
+                                ldw[gi] = (uint8_t)sb;
+                                for (uint64_t gr = a / 4; gr < (a + sb) / 4; ++gr) reader[gr] = tile;
+                            } else {
+                                const uint64_t go = base_of(tgo, tile, v1) + tgo.reg[j];
+                                const uint64_t a = (dof + base_of(ts, tile, v1) + ts.reg[j]) * db;
+                                if (go >= N || a + db > 8 * N) return fail(BW_BAD_ARGUMENTS, "pass %d stores outside", q);
+                                st[go] = a;
+                                stw[go] = (uint8_t)db;
+                                for (uint64_t gr = a / 4; gr < (a + db) / 4; ++gr) {
+                                    if (writer[gr] != -1) return fail(BW_BAD_ARGUMENTS, "pass %d stores twice", q);
+                                    writer[gr] = tile;
+                                    if (reader[gr] != -1 && reader[gr] != tile)
+                                        return fail(BW_BAD_ARGUMENTS,
+                                                    "pass %d: tile %lld stores over bytes tile %lld loads (not in place)",
+                                                    q, (long long)tile, (long long)reader[gr]);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            return BW_OK;
+        });
+        if (ok != BW_OK) return ok;
+        for (uint64_t i = 0; i < N; ++i) {
+            if (q == 0 && (ld[i] != 8 * i || ldw[i] != 8)) return fail(BW_BAD_ARGUMENTS, "pass 0 does not load natural int64");
+            if (q > 0 && (ld[i] != prev[i] || ldw[i] != prevw[i]))
+                return fail(BW_BAD_ARGUMENTS, "pass %d loads index %llu elsewhere", q, (unsigned long long)i);
+            if (q == cp.m && (st[i] != 8 * i || stw[i] != 8))
+                return fail(BW_BAD_ARGUMENTS, "last pass does not store natural int64");
+        }
+        prev.swap(st);
+        prevw.swap(stw);
+    }
+    if (staged != N - 1) return fail(BW_BAD_ARGUMENTS, "stages cover 0x%llx, not every bit", (unsigned long long)staged);
     return BW_OK;
 }
 

@@ -531,7 +531,20 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
 // parameter space.  (A separate body, not a flag on k_pass: routing k_pass
 // through a shared device function perturbed its register allocation and
 // cost the 9-stage pass 1%, tools/gpu_ab.sh.)
-template <class C, int L, bool EX = false>
+//
+// A > 0: the low run's length is the compile-time A, and every offset is
+// computed like k_pass's (col + low rows << k + high rows << k2, the row
+// parts compile-time per register) instead of read from the table: the
+// table version keeps all 32 64-bit addresses live before the first load
+// (128 registers) and ran 8-9% under its access-pattern walk at n = 34.
+template <int T, int L, int A>
+__device__ __forceinline__ uint64_t split_off_ct(uint32_t e, int k1, int k2) {
+    const uint64_t col = e & ((1u << L) - 1u);
+    const uint32_t row = e >> L;
+    return col + ((uint64_t)(row & ((1u << A) - 1u)) << k1) + ((uint64_t)(row >> A) << k2);
+}
+
+template <class C, int L, bool EX = false, int A = 0>
 __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     k_pass_split(u64* __restrict__ data, int k, ExtractArgs ex, const __grid_constant__ SplitTab tab) {
     static_assert(SplitOf<C>::value && L < C::T, "k_pass_split takes split-row high-pass configs");
@@ -561,13 +574,27 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
         __syncthreads();
     }
     u64 v[E];
-    load_global_tab<C, T, L>(v, g, thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k, tab);
+    const uint32_t tp0 = thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank);
+    [[maybe_unused]] const int k1 = split_k(k), k2 = split_k2(k);
+    if constexpr (A > 0) {
+        const u64* p = g + split_off_ct<T, L, A>(tp0, k1, k2);
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = ld_pass(p + split_off_ct<T, L, A>(reg_part<C, 0>(j), k1, k2));
+    } else {
+        load_global_tab<C, T, L>(v, g, tp0, k, tab);
+    }
     if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     apply_stages<C, 0, L>(v);
     run_rounds<C, L, 1>(v, sm, lane, warp, rank);
     constexpr int LAST = C::NR - 1;
     const uint32_t tp_last = thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank);
-    store_global_tab<C, T, L>(v, g, tp_last, k, tab);
+    if constexpr (A > 0) {
+        u64* p = g + split_off_ct<T, L, A>(tp_last, k1, k2);
+#pragma unroll
+        for (int j = 0; j < E; ++j) st_pass(p + split_off_ct<T, L, A>(reg_part<C, LAST>(j), k1, k2), v[j]);
+    } else {
+        store_global_tab<C, T, L>(v, g, tp_last, k, tab);
+    }
     if constexpr (EX) extract_hits<C, LAST, T, L>(v, g, tile_base<T, L, true>(tile, k), tp_last, k, ex);
 }
 
@@ -591,7 +618,16 @@ struct LayoutTab {
 struct MapArgs {
     LayoutTab ld, st;
     long long lim;  // stores narrower than 8 bytes: every |v| <= lim, else *flag |= 1
+    // compact in-place plan (bw_fwht_i64_compact): MAP_CHECK passes test
+    // every INPUT against lim, a tile writes only if its whole tile passed
+    // and no tile has aborted (then tileflag[tile] = 1); MAP_RESTORE passes
+    // run only on tiles with tileflag set and shift the result right.
+    unsigned* tileflag;
+    unsigned* abort;
+    int shift;
 };
+
+enum { MAP_PLAIN = 0, MAP_CHECK = 1, MAP_RESTORE = 2 };
 
 template <typename T>
 struct PairOf;
@@ -623,18 +659,32 @@ __device__ __forceinline__ unsigned long long layout_base(const LayoutTab& t, ui
 // sources need to keep the load phase as long as an int64 one.  On cluster
 // tiles each further tile re-arms the exchange mbarrier (phase u) and
 // passes one more cluster barrier (the partner's shared memory is free).
-template <class C, int L, typename ST, typename DT, int TPC = 1>
+//
+// MODE (the compact in-place plan, bw_fwht_i64_compact; TPC = 1):
+//   MAP_CHECK: a CTA that finds *abort set skips its loads; every input is
+//     tested against |x| <= lim; the CTAs of a cluster agree through DSMEM
+//     flags and one more cluster barrier; a tile stores (and sets
+//     tileflag[tile]) only if no CTA of it is bad, else it stores nothing and
+//     sets *abort.  So every tile either wrote its narrow output or left its
+//     int64 input untouched.  Dynamic shared memory: + 8 B per cluster CTA.
+//   MAP_RESTORE: tiles whose tileflag is 0 exit at once (uniformly per
+//     cluster); the others shift their final values right by m.shift.
+template <class C, int L, typename ST, typename DT, int TPC = 1, int MODE = MAP_PLAIN>
 __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     k_pass_map(const ST* __restrict__ src, DT* __restrict__ dst, unsigned* flag, const __grid_constant__ MapArgs m) {
+    static_assert(MODE == MAP_PLAIN || TPC == 1, "check / restore passes hold one tile per CTA");
     constexpr int E = Dims<C>::E, LAST = C::NR - 1;
     extern __shared__ u64 sm[];
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
     uint32_t rank = 0;
     uint64_t tile = (uint64_t)blockIdx.x * TPC;
+    if constexpr (C::Q > 0) tile = (uint64_t)(blockIdx.x >> C::Q) * TPC;
+    if constexpr (MODE == MAP_RESTORE) {
+        if (*reinterpret_cast<volatile unsigned*>(m.tileflag + tile) == 0u) return;  // the same for every CTA of the tile
+    }
     if constexpr (C::Q > 0) {
         rank = cluster_ctarank();
-        tile = (uint64_t)(blockIdx.x >> C::Q) * TPC;
         if (threadIdx.x == 0) {
             const uint32_t mb = (uint32_t)__cvta_generic_to_shared(sm + Dims<C>::SMEM_ELEMS);
             constexpr uint32_t bytes_in = 8u * (Dims<C>::CTA - Dims<C>::CTA / Dims<C>::CLUSTER);
@@ -645,9 +695,19 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
         __syncthreads();
     }
     const uint32_t tp0 = thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank);
+    bool skip = false;  // MAP_CHECK: another tile already failed, this one only keeps the cluster in step
+    if constexpr (MODE == MAP_CHECK)
+        skip = __syncthreads_or(threadIdx.x == 0 && *reinterpret_cast<volatile unsigned*>(m.abort) != 0u);
     ST raw[TPC][E];
 #pragma unroll
     for (int u = 0; u < TPC; ++u) {
+        if constexpr (MODE == MAP_CHECK) {
+            if (skip) {
+#pragma unroll
+                for (int j = 0; j < E; ++j) raw[u][j] = 0;
+                continue;
+            }
+        }
         const ST* p = src + layout_base(m.ld, tile + u, tp0);
 #pragma unroll
         for (int j = 0; j < E; ++j) {
@@ -664,6 +724,11 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     }
     if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     bool bad = false;
+    if constexpr (MODE == MAP_CHECK) {
+        bad = skip;
+#pragma unroll
+        for (int j = 0; j < E; ++j) bad |= ((long long)raw[0][j] > m.lim) | ((long long)raw[0][j] < -m.lim);
+    }
 #pragma unroll
     for (int u = 0; u < TPC; ++u) {
         u64 v[E];
@@ -685,9 +750,36 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
         }
         apply_stages<C, 0, L>(v);
         run_rounds<C, L, 1>(v, sm, lane, warp, rank, (uint32_t)(u & 1));
-        if constexpr (sizeof(DT) == 2) {  // the int32 stage after it cannot overflow (bw_fwht_i64_narrow)
+        if constexpr (MODE == MAP_PLAIN && sizeof(DT) == 2) {  // the int32 stage after it cannot overflow (bw_fwht_i64_narrow)
 #pragma unroll
             for (int j = 0; j < E; ++j) bad |= ((long long)v[j] > m.lim) | ((long long)v[j] < -m.lim);
+        }
+        if constexpr (MODE == MAP_RESTORE) {
+#pragma unroll
+            for (int j = 0; j < E; ++j) v[j] = (u64)((long long)v[j] >> m.shift);
+        }
+        if constexpr (MODE == MAP_CHECK) {
+            // Tile-wide agreement: every CTA of the cluster stores, or none.
+            bool tile_bad = __syncthreads_or(bad);
+            if constexpr (C::Q > 0) {
+                const uint32_t fl = (uint32_t)__cvta_generic_to_shared(sm + Dims<C>::SMEM_ELEMS + 1);
+                if (threadIdx.x == 0) {
+#pragma unroll
+                    for (uint32_t d = 0; d < (uint32_t)Dims<C>::CLUSTER; ++d)
+                        if (d != rank) asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(map_to_rank(fl + 8u * rank, d)),
+                                                    "l"((u64)tile_bad)
+                                                    : "memory");
+                }
+                cluster_sync_all();
+#pragma unroll
+                for (uint32_t d = 0; d < (uint32_t)Dims<C>::CLUSTER; ++d)
+                    if (d != rank) tile_bad |= reinterpret_cast<volatile u64*>(sm + Dims<C>::SMEM_ELEMS + 1)[d] != 0ull;
+            }
+            if (tile_bad) {
+                if (threadIdx.x == 0 && !skip) atomicExch(m.abort, 1u);
+                return;
+            }
+            if (threadIdx.x == 0 && rank == 0) m.tileflag[tile] = 1u;
         }
         DT* q = dst + layout_base(m.st, tile + u, thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank));
 #pragma unroll
@@ -704,7 +796,7 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
             }
         }
     }
-    if constexpr (sizeof(DT) == 2) {
+    if constexpr (MODE == MAP_PLAIN && sizeof(DT) == 2) {
         if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1u);
     }
 }

@@ -380,3 +380,29 @@ def test_host_batch_validation_host_side():
         _lib.check(L.bw_fwht_host_batch_i64(None, 2, 10, None, 2, None, None))
     with pytest.raises(errors.BadArguments):
         _lib.check(L.bw_fwht_xfused_pass_extract_i64(None, 1, 20, 5, 0, 10, 0, None, None, 16, None, None))
+
+
+@pytest.mark.parametrize("n", [16, 19, 22])
+def test_compact_plan_checks(n):
+    """The compact in-place plan's exact address tables (bw_plan_check_compact):
+    natural int64 in and out, every pass loads where the previous one
+    stored, no tile stores over bytes another tile of the same pass loads,
+    every bit staged once."""
+    L = _lib.lib()
+    assert L.bw_plan_check_compact(n) == 0, _lib.last_error()
+    assert L.bw_compact_npasses(n) >= 2
+    assert L.bw_compact_limit(n) == (2**31 - 1) >> (n - 13)
+
+
+@pytest.mark.parametrize("rows,w", [("4,4,3", 13), ("5,5", 14), ("9,1", 14), ("3,3,2,2", 14)])
+def test_compact_plan_shapes_check(monkeypatch, rows, w):
+    monkeypatch.setenv("BW_COMPACT_ROWS", rows)
+    monkeypatch.setenv("BW_COMPACT_W", str(w))
+    n = w + sum(int(r) for r in rows.split(","))
+    assert _lib.lib().bw_plan_check_compact(n) == 0, _lib.last_error()
+
+
+def test_compact_checker_catches_a_layout_that_is_not_in_place(monkeypatch):
+    monkeypatch.setenv("BW_COMPACT_BREAK", "1")  # bit c trades places with the top bit
+    assert _lib.lib().bw_plan_check_compact(20) != 0
+    assert "not in place" in _lib.last_error()

@@ -1,0 +1,175 @@
+"""The compact in-place plan (bw_fwht_i64_compact: high-bit stages first on
+int32 copies kept inside the signal's own buffer, then the low pass widening
+back to int64) against the C oracle of fwht_array (core.py:97-117): bit-exact
+for every plan shape, for inputs at the limit, and through the fallback
+(inputs over the limit: the tiles already written are restored exactly and
+the int64 plan runs)."""
+
+import ctypes
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1607_01039_b200 as bw
+from paper_1607_01039_b200 import _lib
+from oracle import oracle_np
+
+pytestmark = pytest.mark.gpu
+
+
+def c_fwht(coracle, x):
+    y = np.ascontiguousarray(x, dtype=np.int64).copy()
+    coracle.oracle_fwht_i64(y.ctypes.data, int(y.size).bit_length() - 1)
+    return y
+
+
+def compact(x, max_abs=-1):
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    n = int(t.numel()).bit_length() - 1
+    used = ctypes.c_int(0)
+    bf = ctypes.c_uint64(0)
+    _lib.check(_lib.lib().bw_fwht_i64_compact(t.data_ptr(), n, max_abs, torch.cuda.current_stream().cuda_stream,
+                                              ctypes.byref(used), ctypes.byref(bf)))
+    assert bf.value == n << (n - 1)
+    return t.cpu().numpy(), used.value
+
+
+@pytest.mark.parametrize("n", [16, 18, 20, 21, 22, 23, 24, 25, 26])
+def test_compact_pm1_every_n(coracle, n):
+    x = oracle_np.gen(1, 100 + n, [], 0, 1 << n)
+    for bound in (-1, 1):
+        y, used = compact(x, bound)
+        assert used == 1
+        assert np.array_equal(y, c_fwht(coracle, x)), f"n={n} bound={bound}"
+
+
+@pytest.mark.parametrize("rows,w", [("9,9", 14), ("9,9", 13), ("6,5", 13), ("5,5,3", 13), ("4,4,3,2", 14),
+                                    ("9,1", 14), ("4,3,3", 13), ("3,2", 14)])
+def test_compact_plan_shapes(coracle, monkeypatch, rows, w):
+    """Every high-pass shape the plan can take (2-CTA tiles with 6..9 rows,
+    register-only tiles with <= 5 rows, 1..4 high passes, low pass 13 / 14),
+    checked statically and on the device at the limit value."""
+    monkeypatch.setenv("BW_COMPACT_ROWS", rows)
+    monkeypatch.setenv("BW_COMPACT_W", str(w))
+    n = w + sum(int(r) for r in rows.split(","))
+    if n <= 24:
+        assert _lib.lib().bw_plan_check_compact(n) == 0, _lib.last_error()
+    lim = _lib.lib().bw_compact_limit(n)
+    rng = np.random.default_rng(n * 7 + w)
+    x = rng.integers(-lim, lim + 1, size=1 << n, dtype=np.int64)
+    x[rng.integers(0, 1 << n, size=64)] = lim
+    x[rng.integers(0, 1 << n, size=64)] = -lim
+    y, used = compact(x)
+    assert used == 1
+    assert np.array_equal(y, c_fwht(coracle, x))
+
+
+@pytest.mark.parametrize("where", ["first", "last", "middle", "everywhere"])
+def test_compact_fallback_restores_exactly(coracle, where):
+    """One input over lim(n): the checked first pass leaves that tile (and
+    every tile after the abort) untouched, the written tiles are restored by
+    their own stages + an exact shift, and the int64 plan gives the
+    reference's result."""
+    n = 24
+    lim = _lib.lib().bw_compact_limit(n)
+    rng = np.random.default_rng(5)
+    x = rng.integers(-lim, lim + 1, size=1 << n, dtype=np.int64)
+    if where == "first":
+        x[3] = lim + 1
+    elif where == "last":
+        x[-1] = -(lim + 1)
+    elif where == "middle":
+        x[(1 << n) // 2 + 12345] = 1 << 40
+    else:
+        x = rng.integers(-(1 << 30), 1 << 30, size=1 << n, dtype=np.int64)
+    y, used = compact(x)
+    assert used == 0
+    assert np.array_equal(y, c_fwht(coracle, x))
+
+
+def test_compact_restore_is_identity():
+    """The restore step alone: a checked pass 0 that wrote every tile, then
+    the restore, gives the input back bit for bit."""
+    n = 22
+    x = oracle_np.gen(2, 8, [1000], 0, 1 << n)
+    t = torch.from_numpy(x.copy()).cuda()
+    tiles = 1 << (n - 13)
+    flags = torch.zeros(tiles, dtype=torch.int32, device="cuda")
+    abort = torch.zeros(1, dtype=torch.int32, device="cuda")
+    sh = torch.cuda.current_stream().cuda_stream
+    L = _lib.lib()
+    _lib.check(L.bw_fwht_i64_compact_pass(t.data_ptr(), n, 0, 1, flags.data_ptr(), abort.data_ptr(), sh))
+    assert abort.item() == 0 and int(flags.sum().item()) == 1 << (n - 14)
+    assert not np.array_equal(t.cpu().numpy(), x)
+    _lib.check(L.bw_fwht_i64_compact_restore(t.data_ptr(), n, flags.data_ptr(), sh))
+    assert np.array_equal(t.cpu().numpy(), x)
+
+
+def test_fwht_array_and_inplace_pick_compact(coracle):
+    n = 23
+    x = oracle_np.gen(1, 23, [], 0, 1 << n)
+    t = torch.from_numpy(x.copy()).cuda()
+    bw.fwht_array(t, compact=True)
+    assert bw.core.last_compact
+    assert np.array_equal(t.cpu().numpy(), c_fwht(coracle, x))
+    t = torch.from_numpy(x.copy()).cuda()
+    bw.fwht_array(t, compact=1)  # a bound the caller guarantees
+    assert bw.core.last_compact
+    assert np.array_equal(t.cpu().numpy(), c_fwht(coracle, x))
+    sig = bw.fwht_inplace(bw.Signal(torch.from_numpy(x.copy()).cuda()))
+    assert np.array_equal(sig.data.cpu().numpy(), c_fwht(coracle, x))
+    big = oracle_np.gen(2, 4, [1 << 30], 0, 1 << n)
+    t = torch.from_numpy(big.copy()).cuda()
+    bw.fwht_array(t, compact=True)
+    assert not bw.core.last_compact
+    assert np.array_equal(t.cpu().numpy(), c_fwht(coracle, big))
+    t = torch.from_numpy(x.copy()).cuda()
+    bw.fwht_array(t, compact=False)
+    assert not bw.core.last_compact
+    assert np.array_equal(t.cpu().numpy(), c_fwht(coracle, x))
+
+
+def test_compact_unaligned_view_runs_int64_plan(coracle):
+    n = 22
+    x = oracle_np.gen(1, 9, [], 0, (1 << n) + 1)
+    t = torch.from_numpy(x.copy()).cuda()
+    v = t[1:]  # 8- but not 16-byte aligned
+    bw.fwht_array(v, compact=True)
+    assert not bw.core.last_compact
+    assert np.array_equal(v.cpu().numpy(), c_fwht(coracle, x[1:]))
+
+
+@pytest.mark.skipif(torch.cuda.is_available() and torch.cuda.get_device_properties(0).total_memory < (100 << 30),
+                    reason="needs a B200")
+def test_compact_full_size_n32_spot_check():
+    """n = 32 (config 4) through the compact plan: the fold spot check of
+    2^20 outputs (subspace.py:1-11) against the CPU."""
+    from paper_1607_01039_b200 import signals
+
+    n = 32
+    spec = signals.config(4, n)
+    t = torch.empty(1 << n, dtype=torch.int64, device="cuda")
+    signals.generate(spec, t)
+    bw.fwht_array(t, compact=True)
+    assert bw.core.last_compact
+    d = 20
+    rng = np.random.default_rng(77)
+    while True:
+        rows = rng.integers(0, 2, size=(d, n), dtype=np.uint8)
+        if oracle_np.gf2_rank(rows) == d:
+            break
+    got = t[torch.from_numpy(oracle_np.row_space(rows)).cuda()].cpu().numpy()
+    del t
+    from oracle import load_c
+
+    lib = load_c()
+    cols = oracle_np.column_masks(rows).astype(np.uint64)
+    want = np.empty(1 << d, dtype=np.int64)
+    params = (ctypes.c_uint64 * max(1, len(spec.params)))(*[int(v) for v in spec.params])
+    rc = lib.oracle_fold_i64(None, n, cols.ctypes.data, d, spec.kind, spec.seed, params, len(spec.params),
+                             len(os.sched_getaffinity(0)), want.ctypes.data)
+    assert rc == 0
+    lib.oracle_fwht_i64(want.ctypes.data, d)
+    assert np.array_equal(got, want)
