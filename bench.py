@@ -636,16 +636,19 @@ def run_ours(a):
     if extract_dist:  # fused: k_sort_hits; else k_extract_count / scan / write on every rank's shard
         launches += a.steps * (1 if fused else 3)
     traffic = None  # dram read + write of the dominant pass, from the committed ncu capture
-    try:
-        tname = f"r01_traffic_n{nl}_narrow.json" if narrow_local else f"r01_traffic_n{nl}.json"
-        with open(os.path.join(ROOT, "profiles", tname)) as f:
-            tr = json.load(f)
-        plan_kinds = [q["kind"] for q in plan["passes"]]
-        if len(tr["passes"]) == npasses and plan_kinds[0] == "low":
-            t_dom = tr["passes"][dom]
-            traffic = t_dom["dram_read_bytes"] + t_dom["dram_write_bytes"]
-    except (OSError, KeyError, ValueError):
-        traffic = None
+    # the round-2 capture records its plan and counts only when it is this
+    # run's plan; round 1's (one-run plans, no plan recorded) only for the
+    # narrow plan it was taken on
+    cur_plan = [[q["kind"], q["k"], q["r"], q.get("split_a", 0), q.get("k2", 0)] for q in plan["passes"]]
+    for tname in ([f"r01_traffic_n{nl}_narrow.json"] if narrow_local else [f"r02_traffic_n{nl}.json"]):
+        try:
+            with open(os.path.join(ROOT, "profiles", tname)) as f:
+                tr = json.load(f)
+            if len(tr["passes"]) == npasses and (narrow_local or tr.get("plan") == cur_plan):
+                t_dom = tr["passes"][dom]
+                traffic = t_dom["dram_read_bytes"] + t_dom["dram_write_bytes"]
+        except (OSError, KeyError, ValueError, IndexError):
+            traffic = None
 
     # One more step of the same kind from the config input, then its output
     # gathered at the row space of a seeded fold map: checked on the CPU

@@ -58,5 +58,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+STRESS_OUT = os.path.join(HERE, "lib", "libbigwht_b200_stress.so")
+
+
+def build_stress(force: bool = False) -> str:
+    """The race-stress build (-DBW_RACE_STRESS: random warp sleeps at every
+    synchronisation point of the pass kernels; tools/race_stress.sh and
+    tests/test_gpu_race_stress.py load it through BW_LIB_PATH).  Test
+    infrastructure: the product path never loads it."""
+    if not force and os.path.exists(STRESS_OUT) and all(
+            os.path.getmtime(d) <= os.path.getmtime(STRESS_OUT) for d in DEPS if os.path.exists(d)):
+        return STRESS_OUT
+    os.makedirs(os.path.dirname(STRESS_OUT), exist_ok=True)
+    cmd = [nvcc(), *NVCC_FLAGS, "-DBW_RACE_STRESS=1", "-o", STRESS_OUT + ".tmp", SRC]
+    subprocess.run(cmd, check=True)
+    os.replace(STRESS_OUT + ".tmp", STRESS_OUT)
+    return STRESS_OUT
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--stress" in sys.argv:
+        print(build_stress(force="--force" in sys.argv))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

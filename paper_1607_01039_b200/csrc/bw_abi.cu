@@ -362,7 +362,9 @@ long long best_split_plan(int n, int w0, std::vector<int>* out) {
 // Default plan: the cheapest plan under the measured cost model (low pass
 // of 13, 14 or 15 bits, then the best split of the rest into one-run high
 // passes, or a split-row pass plus one contiguous pass).  Cached per n.
-int default_plan(int n, std::vector<int>* widths) {
+// one_run = true: only one-run high passes (the narrow plan's layouts have
+// no split form).
+int default_plan(int n, std::vector<int>* widths, bool one_run = false) {
     widths->clear();
     if (env_plan(n, widths)) return BW_OK;
     if (n == 0) return BW_OK;
@@ -371,10 +373,10 @@ int default_plan(int n, std::vector<int>* widths) {
         return BW_OK;
     }
     static std::mutex mu;
-    static std::vector<int> cache[BW_MAX_LOG2N + 1];
+    static std::vector<int> cache[2][BW_MAX_LOG2N + 1];
     std::lock_guard<std::mutex> lock(mu);
-    if (n <= BW_MAX_LOG2N && !cache[n].empty()) {
-        *widths = cache[n];
+    if (n <= BW_MAX_LOG2N && !cache[one_run][n].empty()) {
+        *widths = cache[one_run][n];
         return BW_OK;
     }
     long long best_cost = -1;
@@ -386,7 +388,7 @@ int default_plan(int n, std::vector<int>* widths) {
             widths->assign(1, w0);
             widths->insert(widths->end(), hi.begin(), hi.end());
         }
-        if (g_split_plans && n >= 32) {  // measured at n = 32..34 (profiles/r02_split_n*.json)
+        if (g_split_plans && !one_run && n >= 32) {  // measured at n = 32..34 (profiles/r02_split_n*.json)
             const long long sc = best_split_plan(n, w0, &hi);
             if (sc >= 0 && 1000000 / kLowEff[w0 - 13] + sc < best_cost) {
                 best_cost = 1000000 / kLowEff[w0 - 13] + sc;
@@ -395,7 +397,7 @@ int default_plan(int n, std::vector<int>* widths) {
             }
         }
     }
-    if (n <= BW_MAX_LOG2N) cache[n] = *widths;
+    if (n <= BW_MAX_LOG2N) cache[one_run][n] = *widths;
     return BW_OK;
 }
 
@@ -1248,7 +1250,7 @@ int launch_mapped(const Pass& p, int n, NarrowRole role, const void* src, void* 
 // one-run high passes on tiles of one or two CTAs.
 bool narrow_plan(int n, std::vector<Pass>* passes) {
     std::vector<int> w;
-    if (default_plan(n, &w) != BW_OK) return false;
+    if (default_plan(n, &w, true) != BW_OK) return false;
     if (build_passes(n, w, passes) != BW_OK) return false;
     if (passes->size() < 2 || passes->size() > 3 || (*passes)[0].kind != LOW || (*passes)[0].q > 1) return false;
     for (size_t i = 1; i < passes->size(); ++i)
@@ -1852,7 +1854,10 @@ int host_pipelined(int64_t* host, int log2n, u64* d, int dev, cudaStream_t s, bo
     *done = false;
     if (log2n < 24) return BW_OK;
     std::vector<int> w;
-    BW_TRY(default_plan(log2n, &w));
+    // one-run passes: every pass but the last stays inside a chunk (a split
+    // pass would reach the top bits; the overlap saves far more, ~65 ms at
+    // n = 32, than the split plan's 0.8 ms)
+    BW_TRY(default_plan(log2n, &w, true));
     std::vector<Pass> passes;
     BW_TRY(build_passes(log2n, w, &passes));
     if (passes.size() < 2) return BW_OK;

@@ -14,6 +14,27 @@ namespace bw {
 
 typedef unsigned long long u64;
 
+// Race stress (a build with -DBW_RACE_STRESS, tools/race_stress.sh): at every
+// synchronisation point of the pass kernels, about one warp in four sleeps a
+// pseudo-random 0..~2 us, so the orders in which CTAs and warps reach the
+// cluster barriers, the DSMEM exchange, the mbarrier waits and the shared-
+// memory transposes vary from run to run.  A missing or misplaced barrier
+// then shows up as a result that differs from the oracle.  (The pool has
+// compute-sanitizer closed; this is the dynamic check that replaces it.)
+#ifdef BW_RACE_STRESS
+__device__ __forceinline__ void race_stress(uint32_t id) {
+    uint32_t h = blockIdx.x * 0x9E3779B1u ^ (threadIdx.x >> 5) * 0x85EBCA6Bu ^ id * 0xC2B2AE35u;
+    h ^= (uint32_t)clock64() & 0xffu;
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    if ((h & 3u) == 0u) __nanosleep((h >> 16) & 2047u);
+}
+#define BW_STRESS(id) ::bw::race_stress(id)
+#else
+#define BW_STRESS(id) ((void)0)
+#endif
+
 // Cache policy of the pass kernels' global accesses (A/B knob: 0 = .cs
 // streaming, 1 = .cg, 2 = default, 3 = default + L2::256B fetch size).
 // Measured on B200 (profiles/r01_*): default loads lift the vectorised low
@@ -298,6 +319,7 @@ __device__ __forceinline__ void st_async_v2(uint32_t addr, u64 a, u64 b, uint32_
                  : "memory");
 }
 __device__ __forceinline__ void mbar_wait_parity(uint32_t mbar, uint32_t parity) {
+    BW_STRESS(40);
     uint32_t done = 0;
     while (!done) {
         asm volatile(
@@ -393,15 +415,20 @@ __device__ __forceinline__ void run_rounds(u64 (&v)[Dims<C>::E], u64* sm, uint32
             static_assert(RD == 1, "the DSMEM exchange is the first transpose (smem still unused)");
             // Partners have started (the arrive was issued right after the
             // loads); no smem has been read yet, so no WAR hazard exists.
+            BW_STRESS(41);
             asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
             exchange_write<C, RD - 1>(v, sm, thread_part<C, RD - 1>(lane, warp), rank);
+            BW_STRESS(42);
             __syncthreads();  // this CTA's own stores
             mbar_wait_parity((uint32_t)__cvta_generic_to_shared(sm + Dims<C>::SMEM_ELEMS), parity);  // remote bytes
         } else {
+            BW_STRESS(43);
             if constexpr (RD > 1) __syncthreads();
             store_smem<C, RD - 1>(v, sm, thread_part<C, RD - 1>(lane, warp));
+            BW_STRESS(44);
             __syncthreads();
         }
+        BW_STRESS(45);
         load_smem<C, RD>(v, sm, thread_part<C, RD>(lane, warp));
         apply_stages<C, RD, L, FP>(v);
         run_rounds<C, L, RD + 1, FP>(v, sm, lane, warp, rank, parity);
@@ -517,11 +544,13 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
                                            thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
     else
         load_global<C, 0, T, L>(v, g, thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
+    BW_STRESS(46);
     if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     apply_stages<C, 0, L, FP>(v);
     run_rounds<C, L, 1, FP>(v, sm, lane, warp, rank);
     constexpr int LAST = C::NR - 1;
     const uint32_t tp_last = thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank);
+    BW_STRESS(47);
     store_global<C, LAST, T, L>(v, g, tp_last, k);
     if constexpr (EX) extract_hits<C, LAST, T, L>(v, g, tile_base<T, L>(tile, k), tp_last, k, ex);
 }
@@ -583,11 +612,13 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     } else {
         load_global_tab<C, T, L>(v, g, tp0, k, tab);
     }
+    BW_STRESS(48);
     if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     apply_stages<C, 0, L>(v);
     run_rounds<C, L, 1>(v, sm, lane, warp, rank);
     constexpr int LAST = C::NR - 1;
     const uint32_t tp_last = thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank);
+    BW_STRESS(49);
     if constexpr (A > 0) {
         u64* p = g + split_off_ct<T, L, A>(tp_last, k1, k2);
 #pragma unroll
@@ -722,6 +753,7 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
             }
         }
     }
+    BW_STRESS(50);
     if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     bool bad = false;
     if constexpr (MODE == MAP_CHECK) {
@@ -743,6 +775,7 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
                 }
                 // this CTA's reads of tile u-1 are done (release); run_rounds waits
                 // for the partner's before writing into its shared memory
+                BW_STRESS(51);
                 asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");
             } else {
                 __syncthreads();  // the previous tile's last shared-memory reads
@@ -770,6 +803,7 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
                                                     "l"((u64)tile_bad)
                                                     : "memory");
                 }
+                BW_STRESS(52);
                 cluster_sync_all();
 #pragma unroll
                 for (uint32_t d = 0; d < (uint32_t)Dims<C>::CLUSTER; ++d)
@@ -826,6 +860,7 @@ template <class C1, int L1, class C2, int L2, bool FP = false>
 __global__ void __launch_bounds__(256, 1) k_two_pass(u64* __restrict__ data, int k2) {
     extern __shared__ u64 sm[];
     single_tile<C1, L1, FP>(data, 0, blockIdx.x, sm);
+    BW_STRESS(53);
     __syncthreads();  // shared memory is reused by the second tile
     cooperative_groups::this_grid().sync();
     single_tile<C2, L2, FP>(data, k2, blockIdx.x, sm);
@@ -1155,11 +1190,13 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
             v[j] = ld_pass(s.p[(tp | e) >> TL] + t0 + global_off<TL, L>(e & lmask, k));
         }
     }
+    BW_STRESS(54);
     if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     apply_stages<C, 0, L>(v);
     run_rounds<C, L, 1>(v, sm, lane, warp, rank);
     const uint32_t tp = thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank);
     const uint64_t t1 = base + global_off<TL, L>(tp & lmask, k);
+    BW_STRESS(55);
 #pragma unroll
     for (int j = 0; j < E; ++j) {
         const uint32_t e = reg_part<C, LAST>(j);

@@ -101,3 +101,32 @@ def test_involution_n30():
     bw.fwht_array(t)
     x.mul_(1 << 30)
     assert torch.equal(t, x)
+
+
+def test_config4_n32_full_output_equals_the_reference_run():
+    """Full-size parity with the reference itself: the sha256 of all 2^32
+    outputs of the GPU transform of config 4 equals the digest of the
+    UNMODIFIED reference's run_parallel (parallel.py:162-198) on the same
+    input, recorded by `bench.py --cpu-full` on a GPU box's host
+    (profiles/r02_cpu_reference_full.json; 44 s on 16 cores)."""
+    import hashlib
+    import json
+
+    rec_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                            "r02_cpu_reference_full.json")
+    with open(rec_path) as f:
+        rec = json.load(f)
+    assert rec["n"] == 32 and rec["config"] == 4 and rec["kind"] == "reference"
+    spec = signals.config(4, 32)
+    free, _ = torch.cuda.mem_get_info()
+    if free < (8 << spec.n) + (2 << 30):
+        pytest.skip("needs 34 GiB of free device memory")
+    t = signals.make(spec)
+    bw.fwht_array(t)
+    h = hashlib.sha256()
+    chunk = 1 << 27  # 1 GiB of int64
+    host = torch.empty(chunk, dtype=torch.int64, pin_memory=True)
+    for off in range(0, t.numel(), chunk):
+        host.copy_(t[off:off + chunk])
+        h.update(host.numpy().data)
+    assert h.hexdigest()[:16] == rec["output_sha256_16"]

@@ -1,8 +1,11 @@
-"""Summarise an ncu --set full report into profiles/: one row per kernel of
-the headline metrics, the full details page, and the per-pass DRAM traffic
-JSON that bench.py reports as roofline.traffic.
+"""Summarise an ncu --set full report: one row per kernel of the headline
+metrics, the full details page, the source-level stall page of the first
+kernel, and the per-pass DRAM traffic JSON that bench.py reports as
+roofline.traffic (with the plan it was captured on; bench.py uses it only
+when the plan matches).
 
-    python tools/ncu_summary.py gpurun_out/prof_n32_final.ncu-rep r01_final_n32 [n]
+    python tools/ncu_summary.py gpurun_out/prof_n32.ncu-rep gpurun_out/r02_n32 32
+      -> gpurun_out/r02_n32_summary.csv, _details.csv, _source.csv, _traffic.json
 """
 import csv
 import io
@@ -10,7 +13,7 @@ import json
 import subprocess
 import sys
 
-rep, tag = sys.argv[1], sys.argv[2]
+rep, prefix = sys.argv[1], sys.argv[2]
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 32
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
@@ -22,15 +25,19 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "lts__t_sector_hit_rate.pct", "dram__cycles_active.avg.pct_of_peak_sustained_elapsed"]
 idx = {h: i for i, h in enumerate(head)}
 cols = [w for w in want if w in idx]
-with open(f"profiles/{tag}_summary.csv", "w", newline="") as f:
+with open(f"{prefix}_summary.csv", "w", newline="") as f:
     w = csv.writer(f)
     w.writerow(["Kernel Name"] + cols)
     w.writerow([""] + [units[idx[c]] for c in cols])
     for r in data:
         w.writerow([r[idx["Kernel Name"]]] + [r[idx[c]] for c in cols])
 det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True, check=True).stdout
-with open(f"profiles/{tag}_details.csv", "w") as f:
+with open(f"{prefix}_details.csv", "w") as f:
     f.write(det)
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
+                     text=True).stdout
+with open(f"{prefix}_source.csv", "w") as f:
+    f.write(src)
 
 
 def to_bytes(v, unit):
@@ -46,8 +53,17 @@ for i, r in enumerate(data):
                        units[idx["gpu__time_duration.sum"]], 1),
                    "dram_read_bytes": to_bytes(r[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_read.sum"]]),
                    "dram_write_bytes": to_bytes(r[idx["dram__bytes_write.sum"]], units[idx["dram__bytes_write.sum"]])})
-with open(f"profiles/r01_traffic_n{n}.json", "w") as f:
-    json.dump({"source": f"ncu --set full --clock-control none, tools/gpu_prof_final.sh ({rep})", "n": n,
+plan = None
+try:
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_1607_01039_b200 import sharded
+
+    plan = [[q["kind"], q["k"], q["r"], q.get("split_a", 0), q.get("k2", 0)] for q in sharded.plan(n, 0)["passes"]]
+except Exception as e:  # noqa: BLE001 -- the summary is still useful without the plan
+    print("plan unavailable:", e)
+with open(f"{prefix}_traffic.json", "w") as f:
+    json.dump({"source": f"ncu --set full --clock-control none ({rep})", "n": n, "plan": plan,
                "algorithmic_bytes_per_pass": 16 * 2 ** n, "passes": passes}, f, indent=1)
 for p in passes:
     print(p)

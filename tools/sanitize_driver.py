@@ -8,6 +8,8 @@ Families (the kernel templates of csrc/bw_kernels.cuh they launch):
   cluster   k_pass<CfgLow14c> + k_pass<CfgHigh14c> (2-CTA DSMEM st.async / mbarrier),
             k_pass<CfgLow15c> + k_pass<CfgHigh15c> (4-CTA)
   split     k_pass_split<CfgHigh13S / CfgHigh14cS>
+  split_ct  k_pass_split<CfgHigh14cS, L, EX, A> (compile-time low run, the n = 32..34 plans)
+  compact   k_pass_map<..., MAP_CHECK / MAP_RESTORE> + the compact plan's passes
   two_pass  k_two_pass (cooperative grid sync)
   map       k_pass_map<..., TPC=2> (narrow intermediates: per-tile mbarrier phase re-arm on clusters)
   xfused    k_pass_x (fused cross-shard pass, P = 2 / 4 shards on one device) + extraction epilogue
@@ -81,6 +83,36 @@ def fam_split():
     ref = ref_fwht(x)
     check("split r=9 on 2 CTAs", np.array_equal(planned(x, [13, split(9, 1, 4, 19), 2]), ref))
     check("split r=6 on 1 CTA", np.array_equal(planned(x, [13, split(6, 0, 3, 21), 5]), ref))
+
+
+def fam_split_ct():
+    """k_pass_split with a compile-time low run (A = 1..9 on 10 rows, 1..8 on 9)."""
+    n = 26
+    x = oracle_np.gen(2, 12, [1 << 20], 0, 1 << n)
+    ref = ref_fwht(x)
+    for a in (1, 4, 5, 9):
+        check(f"split r=10 a={a} (compile-time offsets)",
+              np.array_equal(planned(x, [13, split(10, 1, a, 26 - (10 - a)), 3]), ref))
+    check("split r=9 a=4", np.array_equal(planned(x, [13, split(9, 1, 4, 21), 4]), ref))
+
+
+def fam_compact():
+    """The compact in-place plan: checked first pass (cluster agreement through
+    DSMEM flags), the exact restore after an abort, unchecked passes."""
+    n = 24
+    lim = int(_lib.lib().bw_compact_limit(n))
+    x = oracle_np.gen(2, 13, [lim], 0, 1 << n)
+    for bound in (-1, lim):
+        t = torch.from_numpy(x.copy()).cuda()
+        bw.fwht_array(t, compact=True if bound < 0 else bound)
+        check(f"compact plan (bound {bound}) used={bw.core.last_compact}",
+              bw.core.last_compact and np.array_equal(t.cpu().numpy(), ref_fwht(x)))
+    y = x.copy()
+    y[(1 << n) - 5] = lim + 1  # the last tiles abort: most tiles are written, then restored
+    t = torch.from_numpy(y.copy()).cuda()
+    bw.fwht_array(t, compact=True)
+    check("compact fallback (restore + int64 plan)",
+          not bw.core.last_compact and np.array_equal(t.cpu().numpy(), ref_fwht(y)))
 
 
 def fam_two_pass():
