@@ -71,6 +71,15 @@ const bool g_two_pass = !(getenv("BW_TWO_PASS") && getenv("BW_TWO_PASS")[0] == '
 const int g_narrow_tpc = getenv("BW_NARROW_TPC") ? atoi(getenv("BW_NARROW_TPC")) : 2;
 // BW_SPLIT_CT=0: split-row passes read their offsets from the table (A/B knob).
 const bool g_split_ct = !(getenv("BW_SPLIT_CT") && getenv("BW_SPLIT_CT")[0] == '0');
+// BW_LOW_PREFETCH=<tiles>[,<tiles for clusters>]: the low passes bulk-prefetch into L2 the tile
+// that many launches ahead (A/B knob; read per call).
+int low_prefetch_tiles(int q) {
+    const char* e = getenv("BW_LOW_PREFETCH");
+    if (!e || !*e) return 0;
+    const int a = atoi(e);
+    const char* c = strchr(e, ',');
+    return (q > 0 && c) ? atoi(c + 1) : a;
+}
 // BW_COMPACT=1: fwht_inplace picks the compact in-place plan when its bound
 // allows (opt-in: measured no faster than the int64 plan).
 const bool g_compact = getenv("BW_COMPACT") && getenv("BW_COMPACT")[0] == '1';
@@ -717,8 +726,10 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractA
                 if (src && src_bytes == 2) return launch_cfg<C>(bw::k_pass<C, L, false, 2>, grid, s, d, p.k, ex, src);
                 if (src) return launch_cfg<C>(bw::k_pass<C, L, false, 1>, grid, s, d, p.k, ex, src);
             }
-            if (ex.count) return launch_cfg<C>(bw::k_pass<C, L, true>, grid, s, d, p.k, ex, none);
-            return launch_cfg<C>(bw::k_pass<C, L, false>, grid, s, d, p.k, ex, none);
+            // low passes: k carries the L2 prefetch distance (BW_LOW_PREFETCH, tiles)
+            const int karg = kLow ? low_prefetch_tiles(C::Q) : p.k;
+            if (ex.count) return launch_cfg<C>(bw::k_pass<C, L, true>, grid, s, d, karg, ex, none);
+            return launch_cfg<C>(bw::k_pass<C, L, false>, grid, s, d, karg, ex, none);
         }
     });
 }

@@ -506,7 +506,7 @@ __device__ __forceinline__ void extract_hits(const u64 (&v)[Dims<C>::E], const u
 
 // One pass over every tile: load (round 0 layout) -> stages -> [transpose ->
 // stages]* -> store (last round layout).  k = first global stage bit of the
-// rows (ignored for L == T).  Cluster configs (Q > 0) put 2^Q CTAs on one
+// rows; for a low pass (L == T) the L2 prefetch distance in tiles (0: none).  Cluster configs (Q > 0) put 2^Q CTAs on one
 // tile; grid = 2^(n-13) CTAs for every config.  SB > 0: the loads read a
 // narrow SB-byte source `src` (widening first pass), the stores go to data.
 template <class C, int L, bool EX = false, int SB = 0, bool FP = false>
@@ -544,6 +544,18 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
                                            thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
     else
         load_global<C, 0, T, L>(v, g, thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
+    if constexpr (L >= T && SB == 0) {
+        // Low pass: k is an L2 prefetch distance in tiles (0 = none).  One
+        // bulk prefetch of this CTA's 64 KB of the tile k launches ahead, so
+        // that tile's loads find their lines in L2.
+        if (k > 0 && threadIdx.x == 0) {
+            const uint64_t pt = tile + (uint64_t)k;
+            if (pt < (uint64_t)(gridDim.x >> C::Q)) {
+                const u64* pp = data + (pt << T) + ((uint64_t)rank << kCtaBits);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pp), "r"(8u << kCtaBits) : "memory");
+            }
+        }
+    }
     BW_STRESS(46);
     if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     apply_stages<C, 0, L, FP>(v);
