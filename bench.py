@@ -57,6 +57,8 @@ def args_parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the in-run bit-exact checks against the CPU")
+    ap.add_argument("--no-entry-points", action="store_true",
+                    help="skip timing fwht_inplace (device and known bound) beside fwht_array")
     ap.add_argument("--cpu-full", action="store_true",
                     help="also time ONE reference run_parallel at the full config size (slow; written to "
                          "profiles/r02_cpu_reference_full.json)")
@@ -650,6 +652,35 @@ def run_ours(a):
         except (OSError, KeyError, ValueError, IndexError):
             traffic = None
 
+    # The reference's other entry point, fwht_inplace (core.py:120-125: bound
+    # check before mutation, then the transform), beside fwht_array on the
+    # same input: with the bound computed on the device (8 B/point reduction)
+    # and with the bound the generator guarantees (max_abs, no reduction).
+    # Device-timed, input regenerated outside the events, one GPU only.
+    entry_points = None
+    if rank == 0 and ws == 1 and p == 0 and spec.threshold is None and not a.no_entry_points:
+        import paper_1607_01039_b200 as bw
+
+        calls = {"fwht_array": lambda: bw.fwht_array(x),
+                 "fwht_inplace": lambda: bw.fwht_inplace(bw.Signal(x)),
+                 "fwht_inplace_known_bound": lambda: bw.fwht_inplace(bw.Signal(x), max_abs=spec.max_abs)}
+        entry_points = {}
+        for name, fn in calls.items():
+            ts = []
+            for _ in range(4):
+                restore()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            entry_points[name + "_ms"] = round(sum(ts[1:]) / len(ts[1:]), 3)  # the first call warms up
+        entry_points["known_bound_vs_fwht_array"] = round(
+            entry_points["fwht_inplace_known_bound_ms"] / entry_points["fwht_array_ms"], 4)
+        entry_points["max_abs"] = spec.max_abs
+
     # One more step of the same kind from the config input, then its output
     # gathered at the row space of a seeded fold map: checked on the CPU
     # below against WHT(fold(x, L)) (subspace.py:1-11), computed from the
@@ -697,6 +728,8 @@ def run_ours(a):
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if entry_points:
+        line["entry_points"] = entry_points
     if narrow_local:
         line["config"]["intermediates"] = ("int16 after the low pass (checked, int64 plan on overflow), "
                                            + ("int32 after the middle pass, " if npasses == 3 else "")
@@ -880,7 +913,9 @@ def run_e2e(a, x, spec, p, nl, rank, ws, peer):
     if ws == 1 and nbytes_local * 3 > host_ram_bytes() // 2:
         return {"value": None, "unit": "points/s", "skipped": f"two pinned {nbytes_local >> 30} GiB host buffers "
                 "do not fit comfortably in host RAM"}
-    steps = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 8))
+    # the same K consecutive signals as the device-timed leg: the first H2D and
+    # the last D2H cannot overlap anything, so fewer signals weigh them more
+    steps = a.e2e_steps if a.e2e_steps is not None else max(1, a.steps)
     host = torch.empty(1 << nl, dtype=torch.int64, pin_memory=True)
     signals.generate(spec, x, base=rank << nl)
     host.copy_(x)

@@ -497,10 +497,30 @@ __device__ __noinline__ void extract_slow(const u64* g, uint64_t gbase, uint32_t
     }
 }
 
+// Cheap prefilter: OR over the registers of (x ^ sign(x)) (= |x| for x >= 0,
+// |x| - 1 below), 3 instructions per value against any_hit's 5.  If that OR
+// is below 2^p with 2^p <= tau - 1, every |x| <= 2^p <= tau - 1: no hit.
+template <int E>
+__device__ __forceinline__ bool maybe_hit(const u64 (&v)[E], unsigned long long tau) {
+    if (tau < 2) return true;  // tau 0 / 1: (almost) everything hits, test exactly
+    uint32_t ahi = 0, alo = 0;
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        const uint32_t hi = (uint32_t)(v[j] >> 32), lo = (uint32_t)v[j];
+        const uint32_t sg = (uint32_t)((int32_t)hi >> 31);
+        ahi |= hi ^ sg;
+        alo |= lo ^ sg;
+    }
+    const u64 acc = ((u64)ahi << 32) | alo;
+    const int p = 63 - __clzll((long long)(tau - 1));  // 2^p <= tau - 1
+    return (acc >> p) != 0;
+}
+
 template <class C, int RD, int T, int L>
 __device__ __forceinline__ void extract_hits(const u64 (&v)[Dims<C>::E], const u64* g, uint64_t gbase, uint32_t tp,
                                              int k, const ExtractArgs& ex) {
-    if (!__any_sync(0xffffffffu, any_hit<Dims<C>::E>(v, ex.tau))) return;  // the common case: no hit in this warp
+    if (!__any_sync(0xffffffffu, maybe_hit<Dims<C>::E>(v, ex.tau))) return;  // the common case: no value near tau
+    if (!__any_sync(0xffffffffu, any_hit<Dims<C>::E>(v, ex.tau))) return;    // exact: no hit in this warp
     extract_slow<C, RD, T, L>(g, gbase, tp, k, ex);
 }
 
@@ -1218,6 +1238,7 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     // final values, global index = shard << nl + offset, warp-aggregated
     // append (unordered; sorted afterwards).
     if constexpr (EX) {
+        if (!__any_sync(0xffffffffu, maybe_hit<E>(v, ex.tau))) return;
         if (!__any_sync(0xffffffffu, any_hit<E>(v, ex.tau))) return;
 #pragma unroll
         for (int j = 0; j < E; ++j) {

@@ -58,6 +58,8 @@ def test_ours_contract_small():
     assert d["roofline"]["bound"] == "hbm" and d["roofline"]["peak"] > 0
     assert d["gpu_launches"] == 3 * len(d["config"]["passes"])
     assert d["e2e"]["h2d_bytes_per_step"] == 8 << 24
+    ep = d["entry_points"]  # fwht_inplace beside fwht_array (core.py:120-125)
+    assert ep["max_abs"] == 1 and ep["fwht_inplace_ms"] > 0 and ep["fwht_inplace_known_bound_ms"] > 0
 
 
 @pytest.mark.gpu

@@ -10,3 +10,5 @@ for d in 0 37 74 148 296 592 0; do
     BW_LOW_PREFETCH=$d timeout 300 python tools/pass_data_study.py --n $n --reps 2 --kinds zeros,pm1 2>&1 | grep -v "^{" >> $O/ab.log
   done
 done
+timeout 900 python -m pytest -q -m gpu tests -k "extract or xfused or fused or config3 or config5" > $O/pytest_extract.log 2>&1; echo "rc=$?" >> $O/pytest_extract.log
+timeout 900 python bench.py --config 5 --steps 5 --warmup 3 --no-e2e --no-cpu > $O/bench_c5.log 2>&1; echo "rc=$?" >> $O/bench_c5.log

@@ -9,6 +9,7 @@
 //   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/bin/mb_split tools/mb_split.cu
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
 #include <vector>
 #include <cuda_runtime.h>
 
@@ -115,7 +116,25 @@ static std::vector<int> cat(std::vector<int> a, std::vector<int> b) {
 
 int main(int argc, char** argv) {
     // argv[1] == "rand": high-entropy data (else zeros, incremented by each walk)
-    const bool rnd = argc > 1 && argv[1][0] == 'r';
+    const bool rnd = argc > 1 && argv[1][0] == 'r' && argv[1][1] != '1';
+    if (argc > 1 && !strcmp(argv[1], "r11")) {
+        // 11-row passes on a 2^14 tile (3 column bits, 64-byte segments): would
+        // let n = 34 run 13 + 11 + 10 instead of 14 + 10 + 10.
+        const int n = 34;
+        u64* d = nullptr;
+        if (cudaMalloc(&d, 8ull << n) != cudaSuccess) return 1;
+        cudaMemset(d, 0, 8ull << n);
+        printf("n=%d data=zeros, 11-row walks\n", n);
+        run(d, n, 3, range(13, 24), "contig r11 k13");
+        run(d, n, 3, cat(range(13, 18), range(28, 34)), "split r11 {13..17}+{28..33}");
+        run(d, n, 3, cat(range(13, 19), range(29, 34)), "split r11 {13..18}+{29..33}");
+        run(d, n, 3, cat(range(13, 20), range(30, 34)), "split r11 {13..19}+{30..33}");
+        run(d, n, 3, cat(range(13, 21), range(31, 34)), "split r11 {13..20}+{31..33}");
+        run(d, n, 4, range(19, 29), "contig r10 k19");
+        run(d, n, 4, cat(range(14, 18), range(28, 34)), "split r10 {14..17}+{28..33} (current)");
+        cudaFree(d);
+        return 0;
+    }
     for (int n : {32, 34}) {
         u64* d = nullptr;
         if (cudaMalloc(&d, 8ull << n) != cudaSuccess) return 1;

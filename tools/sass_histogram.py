@@ -22,9 +22,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KERNELS = [
     ("k_pass<CfgLow13, 13> (n = 32 pass 1, low 13 bits)", r"k_passINS_8CfgLow13ELi13ELb0ELi0ELb0E"),
     ("k_pass<CfgLow14c, 14> (n = 34 pass 1, low 14 bits, 2-CTA)", r"k_passINS_9CfgLow14cELi14ELb0ELi0ELb0E"),
-    ("k_pass<CfgHigh14c, 4> (n = 32 pass 2, r = 10, 2-CTA)", r"k_passINS_10CfgHigh14cELi4ELb0ELi0ELb0E"),
+    ("k_pass_split<CfgHigh14cS, 4, A = 5> (n = 32/33 pass 2: split r = 10, 2-CTA)",
+     r"k_pass_splitINS_11CfgHigh14cSELi4ELb0ELi5E"),
+    ("k_pass_split<CfgHigh14cS, 4, A = 4> (n = 34 pass 2: split r = 10, 2-CTA)",
+     r"k_pass_splitINS_11CfgHigh14cSELi4ELb0ELi4E"),
+    ("k_pass_split<CfgHigh14cS, 4> offset table (round 1's split kernel, fallback)",
+     r"k_pass_splitINS_11CfgHigh14cSELi4ELb0ELi0E"),
     ("k_pass<CfgHigh14c, 5> (n = 32 pass 3, r = 9, 2-CTA)", r"k_passINS_10CfgHigh14cELi5ELb0ELi0ELb0E"),
-    ("k_pass_split<CfgHigh14cS, 4> (n = 33/34 split pass, r = 10, 2-CTA)", r"k_pass_splitINS_11CfgHigh14cSELi4ELb0E"),
+    ("k_pass<CfgHigh14c, 4> (n = 33/34 pass 3, r = 10, 2-CTA)", r"k_passINS_10CfgHigh14cELi4ELb0ELi0ELb0E"),
 ]
 
 GROUPS = [
@@ -68,12 +73,14 @@ def main():
     lines = ["# SASS instruction histogram of the default-plan pass kernels (sm_100a)", "",
              f"`cuobjdump -sass {os.path.relpath(a.lib, ROOT)}` (tools/sass_histogram.py). Static counts per "
              "kernel body (fully unrolled: one tile per CTA).", ""]
-    hdr = "| kernel | total | " + " | ".join(g for g, _ in GROUPS) + " | widest LDG / STG |"
-    lines += [hdr, "|" + "---|" * (len(GROUPS) + 3)]
+    hdr = "| kernel | registers | total | " + " | ".join(g for g, _ in GROUPS) + " | widest LDG / STG |"
+    lines += [hdr, "|" + "---|" * (len(GROUPS) + 4)]
+    res = subprocess.run(["cuobjdump", "-res-usage", a.lib], capture_output=True, text=True).stdout
+    regs = dict(re.findall(r"Function (\S+):\s+REG:(\d+)", res))
     for title, pat in KERNELS:
         name = next((f for f in funcs if re.search(pat, f)), None)
         if name is None:
-            lines.append(f"| {title} | (not found) |" + " |" * (len(GROUPS) + 1))
+            lines.append(f"| {title} | (not found) |" + " |" * (len(GROUPS) + 2))
             continue
         ops = funcs[name]
         cnt = collections.Counter()
@@ -83,7 +90,7 @@ def main():
                     cnt[g] += 1
         ldg = sorted({op for op in ops if op.startswith("LDG")})
         stg = sorted({op for op in ops if op.startswith("STG")})
-        lines.append(f"| {title} | {len(ops)} | " + " | ".join(str(cnt[g]) for g, _ in GROUPS)
+        lines.append(f"| {title} | {regs.get(name, '?')} | {len(ops)} | " + " | ".join(str(cnt[g]) for g, _ in GROUPS)
                      + f" | {', '.join(ldg)} / {', '.join(stg)} |")
     lines += ["", "Reading: every tile element is loaded and stored once (32 LDG.E.64 or 16 LDG.E.128 per "
               "thread); the 2-CTA kernels move half the tile through DSMEM with STAS and wait on one "
