@@ -665,9 +665,9 @@ def run_ours(a):
                  "fwht_inplace": lambda: bw.fwht_inplace(bw.Signal(x)),
                  "fwht_inplace_known_bound": lambda: bw.fwht_inplace(bw.Signal(x), max_abs=spec.max_abs)}
         entry_points = {}
-        for name, fn in calls.items():
-            ts = []
-            for _ in range(4):
+        ts = {name: [] for name in calls}
+        for rep in range(7):  # round robin, so drifting clocks or power weigh on every entry point alike
+            for name, fn in calls.items():
                 restore()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 torch.cuda.synchronize()
@@ -675,8 +675,10 @@ def run_ours(a):
                 fn()
                 e1.record(stream)
                 torch.cuda.synchronize()
-                ts.append(e0.elapsed_time(e1))
-            entry_points[name + "_ms"] = round(sum(ts[1:]) / len(ts[1:]), 3)  # the first call warms up
+                if rep:  # the first round warms up
+                    ts[name].append(e0.elapsed_time(e1))
+        for name, v in ts.items():
+            entry_points[name + "_ms"] = round(statistics.median(v), 3)
         entry_points["known_bound_vs_fwht_array"] = round(
             entry_points["fwht_inplace_known_bound_ms"] / entry_points["fwht_array_ms"], 4)
         entry_points["max_abs"] = spec.max_abs

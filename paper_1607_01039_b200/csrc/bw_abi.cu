@@ -80,6 +80,8 @@ int low_prefetch_tiles(int q) {
     const char* c = strchr(e, ',');
     return (q > 0 && c) ? atoi(c + 1) : a;
 }
+// BW_FUSED_BOUND=0: fwht_inplace runs the separate bound reduction first (A/B knob).
+const bool g_fused_bound = !(getenv("BW_FUSED_BOUND") && getenv("BW_FUSED_BOUND")[0] == '0');
 // BW_COMPACT=1: fwht_inplace picks the compact in-place plan when its bound
 // allows (opt-in: measured no faster than the int64 plan).
 const bool g_compact = getenv("BW_COMPACT") && getenv("BW_COMPACT")[0] == '1';
@@ -1091,10 +1093,106 @@ int bw_check_bound_i64(const int64_t* data, int log2n, int64_t* scratch_dev, voi
     return bound_impl(data, log2n, scratch_dev, dev, as_stream(stream), max_abs);
 }
 
+}  // extern "C"
+namespace {
+// fwht_inplace with the magnitude bound fused into the low pass (n >= 22,
+// 16-byte aligned, a 13- or 14-bit first pass): the pass tests every input
+// against |x| <= 2^(63-n) - 1 (core.py:80-94 element-wise) and a tile with a
+// bad input writes nothing; after the pass one word says whether any tile
+// failed.  Then either the other passes run (no separate 8 B/point reduction
+// pass), or the tiles that did write are restored exactly -- the same stages
+// again, >> w (H H = 2^w I; no wrap below the bound) -- and the call fails
+// like core.py:122, before any visible mutation.  *handled = false: shape
+// not covered, the caller checks the bound first.
+int fused_bound_inplace(int64_t* data, int log2n, cudaStream_t s, bool* handled) {
+    *handled = false;
+    if (!g_fused_bound || log2n < 22 || log2n > 62 || (reinterpret_cast<uintptr_t>(data) & 15u)) return BW_OK;
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    std::vector<int> w;
+    BW_TRY(default_plan(log2n, &w));
+    std::vector<Pass> passes;
+    BW_TRY(build_passes(log2n, w, &passes));
+    if (passes.size() < 2 || passes[0].kind != LOW || passes[0].q > 1) return BW_OK;
+    const Pass& p0 = passes[0];
+    const size_t tiles = 1ull << (log2n - p0.r);
+    void* sc = nullptr;
+    BW_TRY(scratch(dev, 64 + 4 * tiles, &sc));
+    unsigned long long* abort = reinterpret_cast<unsigned long long*>(sc);
+    unsigned* flags = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(sc) + 64);
+    BW_CUDA(cudaMemsetAsync(sc, 0, 64 + 4 * tiles, s));
+    u64* d = reinterpret_cast<u64*>(data);
+    auto low = [&](int mode, unsigned long long arg) -> int {
+        return visit_pass(p0, [&](auto t, auto l) -> int {
+            using C = typename decltype(t)::type;
+            constexpr int L = decltype(l)::value;
+            if constexpr (L >= C::T && C::Q <= 1) {
+                bw::ExtractArgs ex = {};
+                ex.tau = arg;
+                ex.count = abort;
+                ex.idx = reinterpret_cast<long long*>(flags);
+                const unsigned grid = (unsigned)(1ull << (log2n - bw::kCtaBits));
+                const void* none = nullptr;
+                int zero = 0;
+                if (mode == bw::MAP_CHECK) {
+                    auto kern = bw::k_pass<C, L, false, 0, false, bw::MAP_CHECK>;
+                    const int smem = bw::Dims<C>::SMEM_BYTES + (C::Q > 0 ? 8 * bw::Dims<C>::CLUSTER : 0);
+                    BW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                    cudaLaunchConfig_t cfg = {};
+                    cfg.gridDim = dim3(grid);
+                    cfg.blockDim = dim3(bw::Dims<C>::NT);
+                    cfg.dynamicSmemBytes = smem;
+                    cfg.stream = s;
+                    cudaLaunchAttribute attr[1];
+                    attr[0].id = cudaLaunchAttributeClusterDimension;
+                    attr[0].val.clusterDim.x = bw::Dims<C>::CLUSTER;
+                    attr[0].val.clusterDim.y = 1;
+                    attr[0].val.clusterDim.z = 1;
+                    cfg.attrs = attr;
+                    cfg.numAttrs = C::Q > 0 ? 1 : 0;
+                    BW_CUDA(cudaLaunchKernelEx(&cfg, kern, d, zero, ex, none));
+                    return BW_OK;
+                }
+                auto kern = bw::k_pass<C, L, false, 0, false, bw::MAP_RESTORE>;
+                BW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::Dims<C>::SMEM_BYTES));
+                return launch_cfg<C>(kern, grid, s, d, zero, ex, none);
+            } else {
+                return fail(BW_BAD_ARGUMENTS, "no checked form of this low pass");
+            }
+        });
+    };
+    const unsigned long long lim = (1ull << (63 - log2n)) - 1ull;
+    BW_TRY(low(bw::MAP_CHECK, lim));
+    unsigned long long bad = 0;
+    BW_CUDA(cudaMemcpyAsync(&bad, abort, sizeof bad, cudaMemcpyDeviceToHost, s));
+    BW_CUDA(cudaStreamSynchronize(s));
+    *handled = true;
+    if (bad) {
+        BW_TRY(low(bw::MAP_RESTORE, (unsigned long long)p0.r));
+        BW_TRY(bound_impl(data, log2n, nullptr, dev, s, nullptr));  // the reference's error, with M
+        return fail(BW_CUDA_ERROR, "fused bound check failed but the reduction found the bound satisfied");
+    }
+    for (size_t i = 1; i < passes.size(); ++i) BW_TRY(launch_pass(passes[i], d, log2n, s));
+    return BW_OK;
+}
+}  // namespace
+extern "C" {
+
 // fwht_inplace (core.py:120-125): bound first (raise before mutation), then transform.
-// The bound M it computes also picks the plan: M <= lim(n) runs the compact
-// in-place plan (int32 intermediates, bw_fwht_i64_compact), else int64.
+// Large signals check the bound inside the low pass (fused_bound_inplace);
+// the others run the reduction first.  With BW_COMPACT=1 the bound M also
+// picks the compact in-place plan when M <= lim(n).
 int bw_fwht_inplace_i64(int64_t* data, int log2n, int64_t* scratch_dev, void* stream, uint64_t* butterflies) {
+    BW_TRY(check_signal(data, log2n));
+    if (!g_compact) {
+        bool handled = false;
+        const int rc = fused_bound_inplace(data, log2n, as_stream(stream), &handled);
+        if (handled) {
+            if (rc == BW_OK && butterflies) *butterflies = butterfly_count(log2n);
+            return rc;
+        }
+        if (rc != BW_OK) return rc;
+    }
     uint64_t m = 0;
     BW_TRY(bw_check_bound_i64(data, log2n, scratch_dev, stream, &m));
     if (g_compact && m <= (uint64_t)0x7fffffff)

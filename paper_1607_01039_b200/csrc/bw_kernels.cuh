@@ -435,6 +435,10 @@ __device__ __forceinline__ void run_rounds(u64 (&v)[Dims<C>::E], u64* sm, uint32
     }
 }
 
+// Modes of the checked / restoring passes (k_pass's fused bound check,
+// k_pass_map's compact plan).
+enum { MAP_PLAIN = 0, MAP_CHECK = 1, MAP_RESTORE = 2 };
+
 // Threshold extraction fused into the last pass (noisy.py:185-222 with
 // |x| >= tau): the final register values are tested before the store and
 // hits are appended (warp-aggregated) to an unordered list; bw_abi sorts
@@ -529,10 +533,22 @@ __device__ __forceinline__ void extract_hits(const u64 (&v)[Dims<C>::E], const u
 // rows; for a low pass (L == T) the L2 prefetch distance in tiles (0: none).  Cluster configs (Q > 0) put 2^Q CTAs on one
 // tile; grid = 2^(n-13) CTAs for every config.  SB > 0: the loads read a
 // narrow SB-byte source `src` (widening first pass), the stores go to data.
-template <class C, int L, bool EX = false, int SB = 0, bool FP = false>
+//
+// MODE (the low pass of fwht_inplace with the magnitude bound fused in,
+// bw_fwht_inplace_i64; int64, no extraction, no narrow source):
+//   MAP_CHECK: ex.tau = lim, ex.count = the abort word, ex.idx = the tile
+//     flags.  A CTA that finds the abort word set skips its loads; every
+//     input is tested against |x| <= lim (= 2^(63-n) - 1, core.py:80-94);
+//     the CTAs of a cluster agree (DSMEM flags + one more cluster barrier);
+//     a tile stores and sets its flag only if none of it is bad, else it
+//     stores nothing and sets the abort word.
+//   MAP_RESTORE: tiles without a flag exit; the others apply the same stages
+//     again and shift right by ex.tau (H H = 2^w I): the input comes back.
+template <class C, int L, bool EX = false, int SB = 0, bool FP = false, int MODE = MAP_PLAIN>
 __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     k_pass(u64* __restrict__ data, int k, ExtractArgs ex, const void* __restrict__ src) {
     static_assert(!SplitOf<C>::value, "split-row configs launch k_pass_split");
+    static_assert(MODE == MAP_PLAIN || (L >= C::T && !EX && SB == 0 && !FP), "checked / restore: int64 low passes");
     constexpr int T = C::T;
     constexpr int E = Dims<C>::E;
     extern __shared__ u64 sm[];
@@ -540,10 +556,11 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     const uint32_t warp = threadIdx.x >> 5;
     uint32_t rank = 0;
     uint64_t tile = blockIdx.x;
-    if constexpr (C::Q > 0) {
-        rank = cluster_ctarank();
-        tile = blockIdx.x >> C::Q;
+    if constexpr (C::Q > 0) tile = blockIdx.x >> C::Q;
+    if constexpr (MODE == MAP_RESTORE) {
+        if (*reinterpret_cast<volatile unsigned*>(reinterpret_cast<unsigned*>(ex.idx) + tile) == 0u) return;
     }
+    if constexpr (C::Q > 0) rank = cluster_ctarank();
     u64* g = data + tile_base<T, L>(tile, k);
 
     if constexpr (C::Q > 0) {
@@ -559,7 +576,17 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
         __syncthreads();
     }
     u64 v[E];
-    if constexpr (SB > 0)
+    [[maybe_unused]] bool skip = false, bad = false;
+    if constexpr (MODE == MAP_CHECK) {
+        skip = __syncthreads_or(threadIdx.x == 0 && *reinterpret_cast<volatile unsigned long long*>(ex.count) != 0ull);
+        if (skip) {
+#pragma unroll
+            for (int j = 0; j < E; ++j) v[j] = 0;
+        }
+    }
+    if (MODE == MAP_CHECK && skip) {
+        // another tile failed the bound: keep the cluster in step, touch nothing
+    } else if constexpr (SB > 0)
         load_global_narrow<C, 0, T, L, SB>(v, reinterpret_cast<const typename NarrowType<SB>::one*>(src) + tile_base<T, L>(tile, k),
                                            thread_part<C, 0>(lane, warp) | rank_bits<C, 0>(rank), k);
     else
@@ -578,10 +605,45 @@ __global__ void __launch_bounds__(Dims<C>::NT, C::MINB)
     }
     BW_STRESS(46);
     if constexpr (C::Q > 0) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    if constexpr (MODE == MAP_CHECK) {
+        // |x| <= lim  <=>  x + lim in [0, 2 lim] (mod 2^64)
+        const u64 lim = ex.tau, span = 2 * ex.tau;
+        bad = skip;
+#pragma unroll
+        for (int j = 0; j < E; ++j) bad |= (v[j] + lim) > span;
+    }
     apply_stages<C, 0, L, FP>(v);
     run_rounds<C, L, 1, FP>(v, sm, lane, warp, rank);
     constexpr int LAST = C::NR - 1;
     const uint32_t tp_last = thread_part<C, LAST>(lane, warp) | rank_bits<C, LAST>(rank);
+    if constexpr (MODE == MAP_RESTORE) {
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = (u64)((long long)v[j] >> (int)ex.tau);
+    }
+    if constexpr (MODE == MAP_CHECK) {
+        bool tile_bad = __syncthreads_or(bad);
+        if constexpr (C::Q > 0) {
+            const uint32_t fl = (uint32_t)__cvta_generic_to_shared(sm + Dims<C>::SMEM_ELEMS + 1);
+            if (threadIdx.x == 0) {
+#pragma unroll
+                for (uint32_t d = 0; d < (uint32_t)Dims<C>::CLUSTER; ++d)
+                    if (d != rank)
+                        asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(map_to_rank(fl + 8u * rank, d)),
+                                     "l"((u64)tile_bad)
+                                     : "memory");
+            }
+            BW_STRESS(56);
+            cluster_sync_all();
+#pragma unroll
+            for (uint32_t d = 0; d < (uint32_t)Dims<C>::CLUSTER; ++d)
+                if (d != rank) tile_bad |= reinterpret_cast<volatile u64*>(sm + Dims<C>::SMEM_ELEMS + 1)[d] != 0ull;
+        }
+        if (tile_bad) {
+            if (threadIdx.x == 0 && !skip) atomicExch(ex.count, 1ull);
+            return;
+        }
+        if (threadIdx.x == 0 && rank == 0) reinterpret_cast<unsigned*>(ex.idx)[tile] = 1u;
+    }
     BW_STRESS(47);
     store_global<C, LAST, T, L>(v, g, tp_last, k);
     if constexpr (EX) extract_hits<C, LAST, T, L>(v, g, tile_base<T, L>(tile, k), tp_last, k, ex);
@@ -690,7 +752,6 @@ struct MapArgs {
     int shift;
 };
 
-enum { MAP_PLAIN = 0, MAP_CHECK = 1, MAP_RESTORE = 2 };
 
 template <typename T>
 struct PairOf;

@@ -10,6 +10,7 @@ Families (the kernel templates of csrc/bw_kernels.cuh they launch):
   split     k_pass_split<CfgHigh13S / CfgHigh14cS>
   split_ct  k_pass_split<CfgHigh14cS, L, EX, A> (compile-time low run, the n = 32..34 plans)
   compact   k_pass_map<..., MAP_CHECK / MAP_RESTORE> + the compact plan's passes
+  bound     k_pass<low, MAP_CHECK / MAP_RESTORE> (fwht_inplace's fused bound check)
   two_pass  k_two_pass (cooperative grid sync)
   map       k_pass_map<..., TPC=2> (narrow intermediates: per-tile mbarrier phase re-arm on clusters)
   xfused    k_pass_x (fused cross-shard pass, P = 2 / 4 shards on one device) + extraction epilogue
@@ -113,6 +114,25 @@ def fam_compact():
     bw.fwht_array(t, compact=True)
     check("compact fallback (restore + int64 plan)",
           not bw.core.last_compact and np.array_equal(t.cpu().numpy(), ref_fwht(y)))
+
+
+def fam_bound():
+    """fwht_inplace's low pass with the bound fused in (k_pass<..., MAP_CHECK>
+    and the MAP_RESTORE pass after a violation), 1- and 2-CTA low passes."""
+    for n in (22, 24):
+        edge = (1 << (63 - n)) - 1
+        x = oracle_np.gen(2, 14 + n, [1 << 20], 0, 1 << n)
+        s = bw.fwht_inplace(bw.Signal(torch.from_numpy(x.copy()).cuda()))
+        check(f"fused bound n={n}", np.array_equal(s.data.cpu().numpy(), ref_fwht(x)))
+        y = x.copy()
+        y[(1 << n) - 9] = edge + 1
+        t = torch.from_numpy(y.copy()).cuda()
+        try:
+            bw.fwht_inplace(bw.Signal(t))
+            ok = False
+        except bw.errors.OverflowBoundError:
+            ok = np.array_equal(t.cpu().numpy(), y)
+        check(f"fused bound violation restored n={n}", ok)
 
 
 def fam_two_pass():
