@@ -1959,16 +1959,26 @@ namespace {
 cudaStream_t g_copy_stream[kMaxDevices];
 cudaStream_t g_d2h_stream[kMaxDevices];
 
-int host_pipelined(int64_t* host, int log2n, u64* d, int dev, cudaStream_t s, bool* done) {
-    *done = false;
+// Geometry of a copy-overlapped host transform: one-run passes, the H2D in
+// <= 128 chunks of 2^cb points each followed by the passes that stay inside
+// a chunk (every pass but the last), the last pass in 16 column slices of
+// 2^wb columns, each sliced out with a 2-D D2H.  ok = false: no such shape.
+struct HostPipe {
+    bool ok = false;
+    std::vector<Pass> passes;
+    int B = 0, cb = 0, wb = 0, nchunks = 0, nslices = 0;
+};
+
+int host_pipe_plan(int log2n, HostPipe* hp) {
+    hp->ok = false;
     if (log2n < 24) return BW_OK;
     std::vector<int> w;
     // one-run passes: every pass but the last stays inside a chunk (a split
     // pass would reach the top bits; the overlap saves far more, ~65 ms at
     // n = 32, than the split plan's 0.8 ms)
     BW_TRY(default_plan(log2n, &w, true));
-    std::vector<Pass> passes;
-    BW_TRY(build_passes(log2n, w, &passes));
+    BW_TRY(build_passes(log2n, w, &hp->passes));
+    const std::vector<Pass>& passes = hp->passes;
     if (passes.size() < 2) return BW_OK;
     const Pass last = passes.back();
     if ((last.kind != HIGH && last.kind != REG) || last.a || last.k + last.r != log2n) return BW_OK;
@@ -1983,12 +1993,28 @@ int host_pipelined(int64_t* host, int log2n, u64* d, int dev, cudaStream_t s, bo
         return BW_OK;
     }));
     if (wb < colbits || wb + last.r < bw::kCtaBits + last.q) return BW_OK;
+    hp->B = B;
+    hp->cb = cb;
+    hp->wb = wb;
+    hp->nchunks = 1 << (log2n - cb);
+    hp->nslices = 1 << (B - wb);
+    hp->ok = true;
+    return BW_OK;
+}
+
+int host_pipelined(int64_t* host, int log2n, u64* d, int dev, cudaStream_t s, bool* done) {
+    *done = false;
+    HostPipe hp;
+    BW_TRY(host_pipe_plan(log2n, &hp));
+    if (!hp.ok) return BW_OK;
+    const std::vector<Pass>& passes = hp.passes;
+    const Pass last = passes.back();
+    const int B = hp.B, cb = hp.cb, wb = hp.wb, nchunks = hp.nchunks, nslices = hp.nslices;
     {
         std::lock_guard<std::mutex> lk(g_mu);
         if (!g_copy_stream[dev]) BW_CUDA(cudaStreamCreateWithFlags(&g_copy_stream[dev], cudaStreamNonBlocking));
     }
     cudaStream_t cs = g_copy_stream[dev];
-    const int nchunks = 1 << (log2n - cb), nslices = 1 << (B - wb);
     std::vector<cudaEvent_t> ev(nchunks + nslices + 2);
     for (auto& e : ev) BW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     const int st = [&]() -> int {
@@ -2099,6 +2125,14 @@ int bw_fwht_host_batch_i64(int64_t* const* host, int count, int log2n, int64_t* 
     const size_t bytes = (size_t)8 << log2n;
     const int nb = nwork;
     cudaEvent_t start, loaded[4], done[4], freed[4];
+    // BW_BATCH_PIPELINE=0: whole-signal copies around each transform (A/B knob)
+    HostPipe hp;
+    BW_TRY(host_pipe_plan(log2n, &hp));
+    const bool pipe = hp.ok && g_host_pipeline && !(getenv("BW_BATCH_PIPELINE") && getenv("BW_BATCH_PIPELINE")[0] == '0') &&
+                      !(reinterpret_cast<uintptr_t>(work[0]) & 15u) && !(reinterpret_cast<uintptr_t>(work[nwork - 1]) & 15u);
+    std::vector<cudaEvent_t> chunk_ev(pipe ? hp.nchunks : 0), slice_ev(pipe ? hp.nslices : 0);
+    for (auto& e : chunk_ev) BW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : slice_ev) BW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     BW_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
     for (int b = 0; b < nb; ++b) {
         BW_CUDA(cudaEventCreateWithFlags(&loaded[b], cudaEventDisableTiming));
@@ -2123,6 +2157,30 @@ int bw_fwht_host_batch_i64(int64_t* const* host, int count, int log2n, int64_t* 
                     break;
                 }
             }
+            if (pipe) {
+                // chunked H2D, each chunk's inner passes as soon as it lands;
+                // the last pass in column slices, each slice's D2H right after
+                // it: the transform hides under the copies of its neighbours
+                u64* d = reinterpret_cast<u64*>(work[b]);
+                for (int c = 0; c < hp.nchunks; ++c) {
+                    const size_t off = (size_t)c << hp.cb;
+                    BW_CUDA(cudaMemcpyAsync(d + off, host[i] + off, (size_t)8 << hp.cb, cudaMemcpyHostToDevice, up));
+                    BW_CUDA(cudaEventRecord(chunk_ev[c], up));
+                    BW_CUDA(cudaStreamWaitEvent(s, chunk_ev[c], 0));
+                    for (size_t q = 0; q + 1 < hp.passes.size(); ++q) BW_TRY(launch_pass(hp.passes[q], d + off, hp.cb, s));
+                }
+                const Pass& last = hp.passes.back();
+                for (int j = 0; j < hp.nslices; ++j) {
+                    const size_t off = (size_t)j << hp.wb;
+                    BW_TRY(launch_pass(last, d + off, hp.wb + last.r, s));
+                    BW_CUDA(cudaEventRecord(slice_ev[j], s));
+                    BW_CUDA(cudaStreamWaitEvent(down, slice_ev[j], 0));
+                    BW_CUDA(cudaMemcpy2DAsync(host[i] + off, (size_t)8 << hp.B, d + off, (size_t)8 << hp.B,
+                                              (size_t)8 << hp.wb, (size_t)1 << last.r, cudaMemcpyDeviceToHost, down));
+                }
+                BW_CUDA(cudaEventRecord(freed[b], down));
+                continue;
+            }
             BW_CUDA(cudaMemcpyAsync(work[b], host[i], bytes, cudaMemcpyHostToDevice, up));
             BW_CUDA(cudaEventRecord(loaded[b], up));
             BW_CUDA(cudaStreamWaitEvent(s, loaded[b], 0));
@@ -2142,6 +2200,8 @@ int bw_fwht_host_batch_i64(int64_t* const* host, int count, int log2n, int64_t* 
         cudaEventDestroy(done[b]);
         cudaEventDestroy(freed[b]);
     }
+    for (auto& e : chunk_ev) cudaEventDestroy(e);
+    for (auto& e : slice_ev) cudaEventDestroy(e);
     return st;
 }
 

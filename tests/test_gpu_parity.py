@@ -758,12 +758,13 @@ def test_host_buffer_transform_overlapped_copies(coracle, n):
     assert np.array_equal(b, ref)
 
 
-@pytest.mark.parametrize("count", [1, 2, 3, 5])
-def test_host_batch_overlapped_signals(coracle, count):
+@pytest.mark.parametrize("count,n", [(1, 22), (2, 22), (3, 22), (5, 22), (3, 24), (5, 25)])
+def test_host_batch_overlapped_signals(coracle, count, n):
     """fwht_arrays: consecutive host signals through two device buffers
     (H2D of one overlapping D2H of the previous), pinned and pageable, and a
-    signal list that reuses buffers (each use sees the previous result)."""
-    n = 22
+    signal list that reuses buffers (each use sees the previous result).
+    n >= 24: each signal's H2D in chunks with the inner passes as chunks
+    land, its last pass in column slices with a 2-D D2H each."""
     xs = [oracle_np.gen(2, 700 + i, [1 << 20], 0, 1 << n) for i in range(count)]
     refs = [c_fwht(coracle, x) for x in xs]
     pageable = [x.copy() for x in xs]
@@ -784,8 +785,8 @@ def test_host_batch_overlapped_signals(coracle, count):
     assert np.array_equal(one, xs[0] << n)
 
 
-@pytest.mark.parametrize("nwork", [2, 3, 4])
-def test_host_batch_reused_buffers_any_work_count(nwork):
+@pytest.mark.parametrize("nwork,n", [(2, 20), (3, 20), (4, 20), (2, 24), (3, 24)])
+def test_host_batch_reused_buffers_any_work_count(nwork, n):
     """bw_fwht_host_batch_i64 with 2-4 device buffers and host lists that
     repeat a buffer 1..nwork-1 entries later ([h0, h1, h0, h1, ...],
     [h0, h1, h2, h0, ...]): each use must read the previous use's result
@@ -794,7 +795,6 @@ def test_host_batch_reused_buffers_any_work_count(nwork):
 
     from paper_1607_01039_b200 import _lib
 
-    n = 20
     base = [oracle_np.gen(2, 900 + i, [1 << 10], 0, 1 << n) for i in range(3)]
     works = [torch.empty(1 << n, dtype=torch.int64, device="cuda") for _ in range(nwork)]
     warr = (ctypes.c_void_p * nwork)(*[w.data_ptr() for w in works])
