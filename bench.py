@@ -573,7 +573,7 @@ def run_ours(a):
     # 3/5) and the narrow wire (int8 only while |x| <= 127 >> log2 P) need the
     # config input anyway.  So every step starts from the config input,
     # regenerated between steps outside the step's events.
-    restore_each = True
+    restore_each = os.environ.get("BW_BENCH_RESTORE", "1") != "0"  # 0: back-to-back steps (A/B only)
     hits_first = None
     for w in range(a.warmup):
         if restore_each:
