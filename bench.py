@@ -608,6 +608,22 @@ def run_ours(a):
     if ws > 1:
         dist.barrier()
     clk = clocks.stop()
+    # The same K steps back to back on the resident buffer, no regeneration
+    # (reported beside the headline, not as it: after four transforms a +-1
+    # signal is 0 mod 2^64, and the kernels run slightly faster on zeros).
+    b2b = None
+    if restore_each and ws == 1 and p == 0 and not (extract or extract_dist):
+        torch.cuda.synchronize()
+        restore()
+        bev = [events() for _ in range(a.steps)]
+        torch.cuda.synchronize()
+        for e in bev:
+            step(e)
+        torch.cuda.synchronize()
+        b2b = {"ms_per_step": round(bev[0][0].elapsed_time(bev[-1][-1]) / a.steps, 4),
+               "note": "the same K steps back to back on the resident buffer without regenerating the input "
+                       "(most steps then transform zeros); the headline regenerates the input before every step"}
+        restore()
     step_ms = [e[0].elapsed_time(e[-1]) for e in evs]
     per_step = flush or restore_each  # something untimed runs between steps
     total_ms = sum(step_ms) if per_step else evs[0][0].elapsed_time(evs[-1][-1])
@@ -735,6 +751,8 @@ def run_ours(a):
     }
     if entry_points:
         line["entry_points"] = entry_points
+    if b2b:
+        line["back_to_back"] = b2b
     if narrow_local:
         line["config"]["intermediates"] = ("int16 after the low pass (checked, int64 plan on overflow), "
                                            + ("int32 after the middle pass, " if npasses == 3 else "")
