@@ -730,6 +730,15 @@ int launch_pass(const Pass& p, u64* d, int n, cudaStream_t s, const bw::ExtractA
             }
             // low passes: k carries the L2 prefetch distance (BW_LOW_PREFETCH, tiles)
             const int karg = kLow ? low_prefetch_tiles(C::Q) : p.k;
+            if constexpr (std::is_same_v<C, bw::CfgLow14c>) {
+                static const bool minb3 = getenv("BW_LOW14_MINB3") && getenv("BW_LOW14_MINB3")[0] == '1';
+                if (minb3 && !ex.count) {
+                    auto kern = bw::k_pass<bw::CfgLow14c3, 14, false>;
+                    BW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 bw::Dims<bw::CfgLow14c3>::SMEM_BYTES));
+                    return launch_cfg<bw::CfgLow14c3>(kern, grid, s, d, karg, ex, none);
+                }
+            }
             if (ex.count) return launch_cfg<C>(bw::k_pass<C, L, true>, grid, s, d, karg, ex, none);
             return launch_cfg<C>(bw::k_pass<C, L, false>, grid, s, d, karg, ex, none);
         }

@@ -87,6 +87,13 @@ struct CfgLow14c {
     BW_HD static constexpr int P(int) { return 12; }
 };
 
+// The same layout budgeted for three CTAs per SM (register cap 80; the
+// BW_LOW14_MINB3=1 experiment of the n = 34 low pass: 57.4 ms = 4.79 TB/s
+// against 46.4 ms with two, profiles/r02_evidence/low14_minb3_negative.log).
+struct CfgLow14c3 : CfgLow14c {
+    static constexpr int MINB = 3;
+};
+
 // Low-bits pass over stages 0..14: cluster of 4; the rank bits (13, 14)
 // swap with tile bits 11, 12 in the first (DSMEM) transpose.
 //   round 0: reg {8..12}              lane {0,1,2,3,4}  warp {5,6,7}
