@@ -192,8 +192,13 @@ int bw_fwht_i64_compact_pass(int64_t *data, int log2n, int pass_index, int check
                              uint32_t *abort_dev, void *stream);
 /* Test hook: the exact restore of the tiles a checked pass 0 wrote. */
 int bw_fwht_i64_compact_restore(int64_t *data, int log2n, uint32_t *tileflag_dev, void *stream);
-/* Test hook: static check of the compact plan (in place, layouts, coverage), 16 <= n <= 24. */
+/* Test hook: static check of the compact plan (in place, layouts, coverage;
+ * for the int32-engine passes also every round's bank conflicts), 16 <= n <= 24. */
 int bw_plan_check_compact(int log2n);
+/* Test hook: host emulation of the compact plan whose passes after the first
+ * run on the int32 engine (n <= 32 plans), from the kernels' own tables;
+ * 16 <= n <= 24, in place on host memory. */
+int bw_debug_emulate_compact(int64_t *host, int log2n);
 
 /*
  * float64 fwht_array (core.py:97-117 on a float64 Signal, core.py:56-59):

@@ -62,6 +62,7 @@ _SIGNATURES = {
     "bw_fwht_i64_compact_pass": ([P, I32, I32, I32, P, P, P], I32),
     "bw_fwht_i64_compact_restore": ([P, I32, P, P], I32),
     "bw_plan_check_compact": ([I32], I32),
+    "bw_debug_emulate_compact": ([P, I32], I32),
     "bw_pack_narrow_i64": ([P, U64, I32, I32, P, P, P], I32),
     "bw_xshard_narrow": ([ctypes.POINTER(P), I32, I32, U64, U64, P], I32),
     "bw_extract_ge_f64": ([P, I32, ctypes.c_double, ctypes.c_uint64, P, P, ctypes.c_uint64, P, P, PU64], I32),

@@ -17,7 +17,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc", "bw_abi.cu")
 OUT = os.path.join(HERE, "lib", "libbigwht_b200.so")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("bw_abi.cu", "bw_kernels.cuh", "bw_layouts.h")] + [
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("bw_abi.cu", "bw_kernels.cuh", "bw_kernels32.cuh", "bw_layouts.h")] + [
     os.path.join(HERE, "..", "include", "bigwht_b200.h")
 ]
 

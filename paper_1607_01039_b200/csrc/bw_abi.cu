@@ -17,6 +17,7 @@
 
 #include "../../include/bigwht_b200.h"
 #include "bw_kernels.cuh"
+#include "bw_kernels32.cuh"
 #include "bw_layouts.h"
 
 using bw::u64;
@@ -604,6 +605,10 @@ int set_all_pass_attributes() {
             return BW_OK;
         }));
     }
+    // the int32 engine of the compact plan (64 KiB of shared memory, 2 CTAs/SM)
+    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_high<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
+    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_high<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
+    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_low, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
     BW_TRY(set_fused_attrs<1>());
     BW_TRY(set_fused_attrs<2>());
     BW_TRY(set_fused_attrs<3>());
@@ -1581,6 +1586,7 @@ namespace {
 // >> r1 (H H = 2^r1 I) -- and the int64 plan runs.
 struct CompactPlan {
     int n = 0, w = 0, c = 0, m = 0;  // m high passes, then the low pass
+    bool v2 = false;                  // passes after the first on the int32 engine (bw_kernels32.cuh)
     std::vector<Pass> pass;           // shapes for the kernel visitor
     std::vector<PassGeom> geom;
     std::vector<int> half;            // half written by high pass j
@@ -1589,22 +1595,45 @@ struct CompactPlan {
 
 // BW_COMPACT_ROWS="r1,r2,..": stage rows of the high passes (experiments;
 // default: balanced, at most 9).  BW_COMPACT_W=13|14: the low pass width.
+//
+// v2 (n <= 32, the default; BW_COMPACT_V2=0 selects v1): the passes after
+// the first run on the int32 engine -- k32_high (8 or 9 rows, 2^14 int32 per
+// CTA) and the 14-bit low pass k32_low, whose last four stages (bits 10..13)
+// run in int64 registers.  So v2 admits |x| <= (2^31 - 1) >> (n - 4): every
+// stage but the last four keeps |value| <= 2^31 - 1.  Rows: one high pass
+// for H <= 9, else H - r2 then r2 = 9 (BW_COMPACT_R2=8: 8).
+bool compact_v2_enabled() { return !(getenv("BW_COMPACT_V2") && getenv("BW_COMPACT_V2")[0] == '0'); }
+
 bool compact_plan(int n, CompactPlan* cp) {
     if (n < 16 || n > 36) return false;
+    std::vector<int> rows;
+    int sum = 0;
+    const char* rows_env = getenv("BW_COMPACT_ROWS");
+    for (const char* q = rows_env; q && *q;) {
+        const int r = atoi(q);
+        rows.push_back(r);
+        sum += r;
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+    }
+    // v2 unless disabled, n > 32, a low-pass width is forced, or forced rows
+    // do not fit the int32 engine (one high pass, or a second of 8 / 9 rows)
+    bool v2 = compact_v2_enabled() && n <= 32 && !getenv("BW_COMPACT_W");
+    if (v2 && rows_env)
+        v2 = sum == n - 14 && (rows.size() == 1 || (rows.size() == 2 && (rows[1] == 8 || rows[1] == 9)));
     int w = n <= 31 ? 13 : 14;
     if (const char* e = getenv("BW_COMPACT_W")) w = atoi(e) == 14 ? 14 : 13;
+    if (v2) w = 14;
     const int H = n - w;
-    std::vector<int> rows;
-    if (const char* e = getenv("BW_COMPACT_ROWS")) {
-        int sum = 0;
-        for (const char* q = e; *q;) {
-            const int r = atoi(q);
-            rows.push_back(r);
-            sum += r;
-            while (*q && *q != ',') ++q;
-            if (*q == ',') ++q;
-        }
+    if (rows_env) {
         if (sum != H) return false;
+    } else if (v2) {
+        const int r2 = getenv("BW_COMPACT_R2") && atoi(getenv("BW_COMPACT_R2")) == 8 ? 8 : 9;
+        if (H <= 9) rows.push_back(H);
+        else if (H - r2 >= 1 && H - r2 <= 9) {
+            rows.push_back(H - r2);
+            rows.push_back(r2);
+        } else return false;
     } else {
         const int m = (H + 8) / 9;
         for (int j = 0; j < m; ++j) rows.push_back(H / m + (j < H % m ? 1 : 0));
@@ -1614,7 +1643,8 @@ bool compact_plan(int n, CompactPlan* cp) {
     cp->w = w;
     cp->c = w - 1;
     cp->m = (int)rows.size();
-    cp->lim = 0x7fffffffll >> H;
+    cp->v2 = v2;
+    cp->lim = 0x7fffffffll >> (v2 ? n - 4 : H);
     cp->pass.clear();
     cp->geom.clear();
     cp->half.clear();
@@ -1698,6 +1728,24 @@ int launch_compact(const CompactPlan& cp, int i, int64_t* data, CompactMode mode
     const Pass& p = cp.pass[i];
     const PassGeom& g = cp.geom[i];
     const int tpc = getenv("BW_COMPACT_TPC") ? atoi(getenv("BW_COMPACT_TPC")) : 1;
+    if (cp.v2 && i > 0) {  // the int32 engine: 2^14 elements per CTA, no cluster
+        const unsigned grid = (unsigned)(1ull << (cp.n - bw::w32::kBits));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(bw::w32::kNT);
+        cfg.dynamicSmemBytes = bw::w32::kSmemBytes;
+        cfg.stream = s;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(d32 + ((size_t)cp.half[i - 1] << cp.w));
+        if (i == cp.m) {
+            BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_low, src, reinterpret_cast<unsigned long long*>(data)));
+            return BW_OK;
+        }
+        uint32_t* dst = reinterpret_cast<uint32_t*>(d32 + ((size_t)cp.half[i] << cp.w));
+        if (p.r == 9) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_high<5>, src, dst, p.k));
+        else if (p.r == 8) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_high<6>, src, dst, p.k));
+        else return fail(BW_BAD_ARGUMENTS, "no int32-engine pass of %d rows", p.r);
+        return BW_OK;
+    }
     return visit_compact(p, [&](auto t, auto l) -> int {
         using C = typename decltype(t)::type;
         constexpr int L = decltype(l)::value;
@@ -1854,6 +1902,279 @@ int bw_fwht_i64_compact_restore(int64_t* data, int log2n, uint32_t* tileflag_dev
                           as_stream(stream));
 }
 
+}  // extern "C"
+namespace {
+// ---- the int32 engine (bw_kernels32.cuh): static checks and host emulation
+// of its exact tables (TEST HOOKS) -----------------------------------------
+
+// Every round covers the 14 tile bits once (the low pass's sub-rounds: 13
+// plus the sub-round bit), stages only register bits, keeps vector accesses
+// aligned, and every 4/8/16-byte shared-memory access phase (32 / 16 / 8
+// lanes) touches distinct banks.
+template <class C, int RD>
+bool w32_round_ok(std::string* why) {
+    constexpr int NREG = C::nreg(RD);
+    uint32_t seen = 0, regs = 0;
+    auto add = [&](int b) {
+        if (b < 0 || b >= bw::w32::kBits || ((seen >> b) & 1u)) return false;
+        seen |= 1u << b;
+        return true;
+    };
+    for (int i = 0; i < NREG; ++i) {
+        if (!add(C::reg(RD, i))) { *why = "register bits overlap"; return false; }
+        regs |= 1u << C::reg(RD, i);
+    }
+    for (int i = 0; i < 5; ++i) if (!add(C::lane(RD, i))) { *why = "lane bits overlap"; return false; }
+    for (int i = 0; i < 3; ++i) if (!add(C::warp(RD, i))) { *why = "warp bits overlap"; return false; }
+    uint32_t sub = 0;
+    if constexpr (NREG == 5) {
+        sub = 1u << C::SUB;
+        if (!add(C::SUB)) { *why = "sub-round bit overlaps"; return false; }
+    }
+    if (seen != (1u << bw::w32::kBits) - 1u) { *why = "round does not cover the tile"; return false; }
+    if (C::stage(RD) & ~regs) { *why = "a staged bit is not a register bit"; return false; }
+    constexpr int V = bw::w32::vec<C, RD>();
+    constexpr int phase = V == 4 ? 8 : V == 2 ? 16 : 32;
+    for (uint32_t s = 0; s < (sub ? 2u : 1u); ++s)
+        for (uint32_t warp = 0; warp < 8; ++warp)
+            for (int j = 0; j < (1 << NREG); j += V)
+                for (uint32_t g0 = 0; g0 < 32; g0 += phase) {
+                    uint32_t used = 0;
+                    for (uint32_t l = g0; l < g0 + phase; ++l) {
+                        const uint32_t e = bw::w32::thread_part<C, RD>(l, warp) | bw::w32::reg_part<C, RD>(j) |
+                                           (s ? sub : 0u);
+                        const uint32_t slot = C::slot(e);
+                        if (slot % V) { *why = "misaligned vector access"; return false; }
+                        for (int q = 1; q < V; ++q)
+                            if (C::slot(e | bw::w32::reg_part<C, RD>(q)) != slot + q) {
+                                *why = "vector elements not consecutive";
+                                return false;
+                            }
+                        for (int q = 0; q < V; ++q) {
+                            const uint32_t bank = (slot + q) & 31u;
+                            if ((used >> bank) & 1u) { *why = "shared-memory bank conflict"; return false; }
+                            used |= 1u << bank;
+                        }
+                    }
+                }
+    return true;
+}
+
+template <class C, int RD = 0>
+bool w32_rounds_ok(std::string* why) {
+    if constexpr (RD < C::NR) {
+        if (!w32_round_ok<C, RD>(why)) return false;
+        return w32_rounds_ok<C, RD + 1>(why);
+    }
+    return true;
+}
+
+// Index of a compact int32 slot (without the half bit).
+uint64_t compact_index_of(const Layout& lam, int n, uint64_t slot) {
+    uint64_t i = 0;
+    for (int b = 0; b < n; ++b)
+        if ((slot >> lam.pos[b]) & 1u) i |= 1ull << b;
+    return i;
+}
+
+// Calls f(phase, tile, e, addr_bytes, width, index) for every element access
+// of int32-engine pass q (phase 0: loads in round 0, phase 1: stores in the
+// last round) with the kernel's exact address functions.
+template <class F>
+int w32_visit_pass(const CompactPlan& cp, int q, F&& f) {
+    namespace w = bw::w32;
+    const Layout lam = compact_layout(cp);
+    const int n = cp.n;
+    const uint64_t tiles = 1ull << (n - w::kBits);
+    const uint64_t so = (uint64_t)cp.half[q - 1] << cp.w;
+    std::string why;
+    if (q == cp.m) {
+        using C = w::CfgLowW;
+        if (!w32_rounds_ok<C>(&why)) return fail(BW_BAD_ARGUMENTS, "int32 low pass layout: %s", why.c_str());
+        for (uint64_t b = 0; b < tiles; ++b)
+            for (uint32_t th = 0; th < (uint32_t)w::kNT; ++th) {
+                const uint32_t lane = th & 31u, warp = th >> 5;
+                for (int j = 0; j < w::kE; ++j) {
+                    const uint32_t e = w::thread_part<C, 0>(lane, warp) | w::reg_part<C, 0>(j);
+                    const uint64_t slot = (b << (w::kBits + 1)) + C::src_off(e);
+                    f(0, b, e, (so + slot) * 4, 4, compact_index_of(lam, n, slot));
+                }
+                for (uint32_t s = 0; s < 2; ++s)
+                    for (int j = 0; j < 32; ++j) {
+                        const uint32_t e = w::thread_part<C, 2>(lane, warp) | (s << C::SUB) | w::reg_part<C, 2>(j);
+                        const uint64_t gi = (b << w::kBits) + e;
+                        f(1, b, e, gi * 8, 8, gi);
+                    }
+            }
+        return BW_OK;
+    }
+    const Pass& p = cp.pass[q];
+    const uint64_t dof = (uint64_t)cp.half[q] << cp.w;
+    auto run = [&](auto cfg, auto lc) -> int {
+        using C = typename decltype(cfg)::type;
+        constexpr int L = decltype(lc)::value;
+        if (!w32_rounds_ok<C>(&why)) return fail(BW_BAD_ARGUMENTS, "int32 high pass layout: %s", why.c_str());
+        const int kk = p.k + 1;
+        for (uint64_t t = 0; t < tiles; ++t) {
+            const uint64_t base = w::high_tile_base<L>(t, kk);
+            for (uint32_t th = 0; th < (uint32_t)w::kNT; ++th) {
+                const uint32_t lane = th & 31u, warp = th >> 5;
+                for (int j = 0; j < w::kE; ++j) {
+                    const uint32_t ei = w::thread_part<C, 0>(lane, warp) | w::reg_part<C, 0>(j);
+                    const uint64_t si = base + w::high_off<L>(ei, kk);
+                    f(0, t, ei, (so + si) * 4, 4, compact_index_of(lam, n, si));
+                    const uint32_t eo = w::thread_part<C, 1>(lane, warp) | w::reg_part<C, 1>(j);
+                    const uint64_t sd = base + w::high_off<L>(eo, kk);
+                    f(1, t, eo, (dof + sd) * 4, 4, compact_index_of(lam, n, sd));
+                }
+            }
+        }
+        return BW_OK;
+    };
+    if (p.r == 9) return run(tag<w::CfgHighW<5>>{}, ic<5>{});
+    if (p.r == 8) return run(tag<w::CfgHighW<6>>{}, ic<6>{});
+    return fail(BW_BAD_ARGUMENTS, "no int32-engine pass of %d rows", p.r);
+}
+
+// Host emulation of the compact plan with its int32-engine passes (TEST
+// HOOK): pass 0 by its definition (its rows' stages, then the int32 store
+// into the compact layout), every later pass thread by thread with the
+// kernels' own tables, rounds, swizzled shared-memory slots and int32 /
+// int64 arithmetic.
+int w32_emulate(int64_t* host, const CompactPlan& cp) {
+    namespace w = bw::w32;
+    const int n = cp.n;
+    const uint64_t N = 1ull << n;
+    const Layout lam = compact_layout(cp);
+    std::vector<uint32_t> buf(2 * N);
+    memcpy(buf.data(), host, 8 * N);
+    {  // pass 0: rows [w, w + r) staged on the int64 values, stored as int32
+        std::vector<u64> x(N);
+        memcpy(x.data(), host, 8 * N);
+        const Pass& p = cp.pass[0];
+        for (int k = p.k; k < p.k + p.r; ++k)
+            for (uint64_t i = 0; i < N; ++i)
+                if (!((i >> k) & 1)) {
+                    const u64 a = x[i], b = x[i | (1ull << k)];
+                    x[i] = a + b;
+                    x[i | (1ull << k)] = a - b;
+                }
+        const uint64_t dof = (uint64_t)cp.half[0] << cp.w;
+        for (uint64_t i = 0; i < N; ++i) {
+            uint64_t slot = 0;
+            for (int b = 0; b < n; ++b)
+                if ((i >> b) & 1) slot |= 1ull << lam.pos[b];
+            buf[dof + slot] = (uint32_t)x[i];
+        }
+    }
+    std::vector<uint32_t> v((size_t)w::kNT * w::kE), sm(1u << w::kBits);
+    auto stages32 = [&](auto cfg, auto rdc) {
+        using C = typename decltype(cfg)::type;
+        constexpr int RD = decltype(rdc)::value;
+        for (uint32_t th = 0; th < (uint32_t)w::kNT; ++th)
+            for (int i = 0; i < C::nreg(RD); ++i)
+                if ((C::stage(RD) >> C::reg(RD, i)) & 1u)
+                    for (int j = 0; j < w::kE; ++j)
+                        if (!((j >> i) & 1)) {
+                            uint32_t& a = v[th * w::kE + j];
+                            uint32_t& b = v[th * w::kE + (j | (1 << i))];
+                            const uint32_t x = a, y = b;
+                            a = x + y;
+                            b = x - y;
+                        }
+    };
+    auto to_smem = [&](auto cfg, auto rdc) {
+        using C = typename decltype(cfg)::type;
+        constexpr int RD = decltype(rdc)::value;
+        for (uint32_t th = 0; th < (uint32_t)w::kNT; ++th)
+            for (int j = 0; j < w::kE; ++j)
+                sm[C::slot(w::thread_part<C, RD>(th & 31u, th >> 5) | w::reg_part<C, RD>(j))] = v[th * w::kE + j];
+    };
+    auto from_smem = [&](auto cfg, auto rdc) {
+        using C = typename decltype(cfg)::type;
+        constexpr int RD = decltype(rdc)::value;
+        for (uint32_t th = 0; th < (uint32_t)w::kNT; ++th)
+            for (int j = 0; j < w::kE; ++j)
+                v[th * w::kE + j] = sm[C::slot(w::thread_part<C, RD>(th & 31u, th >> 5) | w::reg_part<C, RD>(j))];
+    };
+    const uint64_t tiles = 1ull << (n - w::kBits);
+    for (int q = 1; q <= cp.m; ++q) {
+        const uint64_t so = (uint64_t)cp.half[q - 1] << cp.w;
+        if (q == cp.m) {
+            using C = w::CfgLowW;
+            for (uint64_t b = 0; b < tiles; ++b) {
+                for (uint32_t th = 0; th < (uint32_t)w::kNT; ++th)
+                    for (int j = 0; j < w::kE; ++j)
+                        v[th * w::kE + j] = buf[so + (b << (w::kBits + 1)) +
+                                                C::src_off(w::thread_part<C, 0>(th & 31u, th >> 5) | w::reg_part<C, 0>(j))];
+                stages32(tag<C>{}, ic<0>{});
+                to_smem(tag<C>{}, ic<0>{});
+                from_smem(tag<C>{}, ic<1>{});
+                stages32(tag<C>{}, ic<1>{});
+                to_smem(tag<C>{}, ic<1>{});
+                for (uint32_t th = 0; th < (uint32_t)w::kNT; ++th)
+                    for (uint32_t s = 0; s < 2; ++s) {
+                        const uint32_t tp = w::thread_part<C, 2>(th & 31u, th >> 5) | (s << C::SUB);
+                        u64 x[32];
+                        for (int j = 0; j < 32; ++j) x[j] = (u64)(int64_t)(int32_t)sm[C::slot(tp | w::reg_part<C, 2>(j))];
+                        for (int i = 0; i < 5; ++i)
+                            if ((C::stage(2) >> C::reg(2, i)) & 1u)
+                                for (int j = 0; j < 32; ++j)
+                                    if (!((j >> i) & 1)) {
+                                        const u64 a = x[j], c = x[j | (1 << i)];
+                                        x[j] = a + c;
+                                        x[j | (1 << i)] = a - c;
+                                    }
+                        for (int j = 0; j < 32; ++j) {
+                            const uint64_t gi = (b << w::kBits) + (tp | w::reg_part<C, 2>(j));
+                            buf[2 * gi] = (uint32_t)x[j];
+                            buf[2 * gi + 1] = (uint32_t)(x[j] >> 32);
+                        }
+                    }
+            }
+            continue;
+        }
+        const Pass& p = cp.pass[q];
+        const uint64_t dof = (uint64_t)cp.half[q] << cp.w;
+        auto run = [&](auto cfg, auto lc) {
+            using C = typename decltype(cfg)::type;
+            constexpr int L = decltype(lc)::value;
+            const int kk = p.k + 1;
+            for (uint64_t t = 0; t < tiles; ++t) {
+                const uint64_t base = w::high_tile_base<L>(t, kk);
+                for (uint32_t th = 0; th < (uint32_t)w::kNT; ++th)
+                    for (int j = 0; j < w::kE; ++j)
+                        v[th * w::kE + j] =
+                            buf[so + base + w::high_off<L>(w::thread_part<C, 0>(th & 31u, th >> 5) | w::reg_part<C, 0>(j), kk)];
+                stages32(tag<C>{}, ic<0>{});
+                to_smem(tag<C>{}, ic<0>{});
+                from_smem(tag<C>{}, ic<1>{});
+                stages32(tag<C>{}, ic<1>{});
+                for (uint32_t th = 0; th < (uint32_t)w::kNT; ++th)
+                    for (int j = 0; j < w::kE; ++j)
+                        buf[dof + base + w::high_off<L>(w::thread_part<C, 1>(th & 31u, th >> 5) | w::reg_part<C, 1>(j), kk)] =
+                            v[th * w::kE + j];
+            }
+        };
+        if (p.r == 9) run(tag<w::CfgHighW<5>>{}, ic<5>{});
+        else if (p.r == 8) run(tag<w::CfgHighW<6>>{}, ic<6>{});
+        else return fail(BW_BAD_ARGUMENTS, "no int32-engine pass of %d rows", p.r);
+    }
+    memcpy(host, buf.data(), 8 * N);
+    return BW_OK;
+}
+}  // namespace
+extern "C" {
+
+// TEST HOOK ONLY: host emulation of the compact plan (v2: its int32-engine
+// passes run thread by thread from the kernels' tables), 16 <= n <= 24.
+int bw_debug_emulate_compact(int64_t* host, int log2n) {
+    if (!host || log2n < 16 || log2n > 24) return fail(BW_BAD_ARGUMENTS, "compact emulation supports 16 <= n <= 24");
+    CompactPlan cp;
+    if (!compact_plan(log2n, &cp) || !cp.v2) return fail(BW_BAD_ARGUMENTS, "no int32-engine compact plan for n = %d", log2n);
+    return w32_emulate(host, cp);
+}
+
 // Static checker of the compact plan (TEST HOOK, 16 <= n <= 24): runs the
 // kernels' exact address tables for every element of every pass and checks
 //   - pass 0 loads natural int64, the last pass stores natural int64;
@@ -1880,7 +2201,38 @@ int bw_plan_check_compact(int log2n) {
         return off;
     };
     for (int q = 0; q <= cp.m; ++q) {
-        const int ok = visit_compact(cp.pass[q], [&](auto t, auto l) -> int {
+        int ok;
+        if (cp.v2 && q > 0) {  // the int32 engine's exact address functions
+            std::fill(reader.begin(), reader.end(), -1);
+            std::fill(writer.begin(), writer.end(), -1);
+            const Pass& p = cp.pass[q];
+            const uint64_t bits = q == cp.m ? (1ull << cp.w) - 1ull : ((1ull << p.r) - 1ull) << p.k;
+            if (staged & bits) return fail(BW_BAD_ARGUMENTS, "pass %d stages a bit twice", q);
+            staged |= bits;
+            const char* err = nullptr;
+            ok = w32_visit_pass(cp, q, [&](int phase, uint64_t tile, uint32_t, uint64_t a, int width, uint64_t gi) {
+                if (gi >= N || a + width > 8 * N) { err = "an access leaves the buffer"; return; }
+                if (phase == 0) {
+                    ld[gi] = a;
+                    ldw[gi] = (uint8_t)width;
+                    for (uint64_t gr = a / 4; gr < (a + width) / 4; ++gr) reader[gr] = (int32_t)tile;
+                } else {
+                    st[gi] = a;
+                    stw[gi] = (uint8_t)width;
+                }
+            });
+            if (ok == BW_OK) {  // stores checked after every load of the pass is known
+                ok = w32_visit_pass(cp, q, [&](int phase, uint64_t tile, uint32_t, uint64_t a, int width, uint64_t) {
+                    if (phase != 1) return;
+                    for (uint64_t gr = a / 4; gr < (a + width) / 4; ++gr) {
+                        if (writer[gr] != -1) { err = "two stores to one granule"; return; }
+                        writer[gr] = (int32_t)tile;
+                        if (reader[gr] != -1 && reader[gr] != (int32_t)tile) { err = "a tile stores over bytes another tile loads (not in place)"; return; }
+                    }
+                });
+            }
+            if (ok == BW_OK && err) return fail(BW_BAD_ARGUMENTS, "pass %d: %s", q, err);
+        } else ok = visit_compact(cp.pass[q], [&](auto t, auto l) -> int {
             using C = typename decltype(t)::type;
             constexpr int L = decltype(l)::value;
             constexpr int NQ = 1 << C::Q, LAST = C::NR - 1;

@@ -1,0 +1,349 @@
+// bw_kernels32.cuh -- the int32 register engine of the compact plan.
+//
+// The compact in-place plan (bw_abi.cu, bw_fwht_i64_compact) keeps the
+// signal as int32 inside its own buffer between the first high pass and the
+// low pass.  The int64 engine (bw_kernels.cuh) holds 2^13 elements per CTA,
+// so on int32 data it moves half the bytes per tile, and a pass's time is
+// set by its load latency and per-tile machinery, not by its bytes
+// (DESIGN.md section 5).  This engine holds 2^14 int32 per CTA (256 threads
+// x 64 registers, 64 KiB of shared memory, two CTAs per SM): the same bytes
+// in flight per tile as the int64 engine, so an int32 pass should take the
+// time of its bytes.
+//
+//   k32_high<C, L>: int32 -> int32 high pass, r = 14 - L stage rows of the
+//     compact layout (2^L contiguous int32 columns, rows at slot stride
+//     2^(k+1)); one CTA per tile, two rounds joined by one shared-memory
+//     transpose.
+//   k32_low<C>: int32 -> int64 low pass (stages 0..13 of every 2^14 block),
+//     reading the block's int32 half and writing the natural int64 block.
+//     Rounds 0 and 1 stage 10 bits in int32; round 2 runs as two sub-rounds
+//     of 2^13 elements (32 per thread) that widen to int64 and stage the
+//     last 4 bits (10..13) in int64 registers, then store 16-byte pairs.
+//
+// Exactness: the plan admits only |x| <= (2^31 - 1) >> (n - 4) (bw_abi.cu
+// compact_plan), so every int32 intermediate -- all stages but the last
+// four -- is the exact value and the wrapping uint32 add/sub below equals it.
+//
+// Layout tables use the nibble packing of bw_layouts.h: round RD assigns
+// every virtual tile bit (0..13) to a register bit (6, or 5 in the low
+// pass's sub-rounds), a lane bit (5) or a warp bit (3); butterflies run on
+// register bits.  Shared-memory slots are a linear XOR swizzle of the tile
+// index, chosen so that every 4/8/16-byte access phase of every round is
+// conflict-free (bw_plan_check_w32 verifies it; tools/design32.py searched it).
+#pragma once
+#include <stdint.h>
+
+#include "bw_kernels.cuh"
+#include "bw_layouts.h"
+
+namespace bw {
+namespace w32 {
+
+typedef uint32_t u32;
+constexpr int kBits = 14;  // elements per CTA tile
+constexpr int kNT = 256;   // threads per CTA
+constexpr int kE = 64;     // int32 registers per thread
+constexpr int kSmemBytes = 4 << kBits;
+
+// Low pass over stages 0..13, int32 compact source -> int64 natural.
+// Virtual bit b = index bit i_b of the block.
+//   round 0: reg {0,1,6,7,8,9}    lane {2,3,13,4,5}  warp {10,11,12}  stages 0,1,6..9   (16-byte loads)
+//   round 1: reg {0,1,2,3,4,5}    lane {6..10}       warp {11,12,13}  stages 2..5
+//   round 2: reg {0,10,11,12,13}  lane {1..5}        warp {6,7,8}     stages 10..13 in int64,
+//            sub-round bit 9 (two halves of 32 values per thread), 16-byte int64 stores
+// Source slot of the compact layout (bw_abi.cu compact_layout, w = 14):
+// i0..i3 -> 0..3, i13 -> 4, i4..i12 -> 5..13.
+struct CfgLowW {
+    static constexpr int NR = 3;
+    static constexpr int SUB = 9;
+    BW_HD static constexpr int nreg(int rd) { return rd == 2 ? 5 : 6; }
+    BW_HD static constexpr int reg(int rd, int i) {
+        return nib(rd == 0 ? 0x987610ull : rd == 1 ? 0x543210ull : 0xDCBA0ull, i);
+    }
+    BW_HD static constexpr int lane(int rd, int i) {
+        return nib(rd == 0 ? 0x54D32ull : rd == 1 ? 0xA9876ull : 0x54321ull, i);
+    }
+    BW_HD static constexpr int warp(int rd, int i) { return nib(rd == 0 ? 0xCBAull : rd == 1 ? 0xDCBull : 0x876ull, i); }
+    BW_HD static constexpr uint32_t stage(int rd) { return rd == 0 ? 0x3C3u : rd == 1 ? 0x3Cu : 0x3C00u; }
+    // slot bits 2, 3, 4 ^= e6, e7, e8 ^ e13
+    BW_HD static constexpr uint32_t slot(uint32_t e) { return e ^ ((e >> 4) & 0x1Cu) ^ ((e >> 9) & 0x10u); }
+    BW_HD static constexpr uint32_t src_off(uint32_t e) {
+        return (e & 0xFu) | (((e >> 13) & 1u) << 4) | (((e >> 4) & 0x1FFu) << 5);
+    }
+};
+
+// High pass, r = 14 - L rows: virtual bits 0..L-1 are the columns (slot bits
+// 0..L-1 of the compact layout), L..13 the rows.
+//   L = 5 (9 rows): round 0 reg {0,5..9}   lane {1,2,3,4,10} warp {11,12,13} stages 5..9  (8-byte loads)
+//                   round 1 reg {0,1,10..13} lane {2..6}      warp {7,8,9}    stages 10..13 (16-byte stores)
+//   L = 6 (8 rows): round 0 reg {0,6..10}  lane {1..5}       warp {11,12,13} stages 6..10
+//                   round 1 reg {0,1,11,12,13,6} lane {2,3,4,5,7} warp {8,9,10} stages 11..13
+template <int L>
+struct CfgHighW {
+    static_assert(L == 5 || L == 6, "int32 high passes of 8 or 9 rows");
+    static constexpr int NR = 2;
+    BW_HD static constexpr int nreg(int) { return 6; }
+    BW_HD static constexpr int reg(int rd, int i) {
+        return nib(L == 5 ? (rd == 0 ? 0x987650ull : 0xDCBA10ull) : (rd == 0 ? 0xA98760ull : 0x6DCB10ull), i);
+    }
+    BW_HD static constexpr int lane(int rd, int i) {
+        return nib(L == 5 ? (rd == 0 ? 0xA4321ull : 0x65432ull) : (rd == 0 ? 0x54321ull : 0x75432ull), i);
+    }
+    BW_HD static constexpr int warp(int rd, int i) {
+        return nib(L == 5 ? (rd == 0 ? 0xDCBull : 0x987ull) : (rd == 0 ? 0xDCBull : 0xA98ull), i);
+    }
+    BW_HD static constexpr uint32_t stage(int rd) {
+        return L == 5 ? (rd == 0 ? 0x3E0u : 0x3C00u) : (rd == 0 ? 0x7C0u : 0x3800u);
+    }
+    BW_HD static constexpr uint32_t slot(uint32_t e) { return e; }
+};
+
+// Tile index bits of register index j in round RD.
+template <class C, int RD>
+BW_HD constexpr uint32_t reg_part(int j) {
+    uint32_t e = 0;
+    for (int i = 0; i < C::nreg(RD); ++i)
+        if ((j >> i) & 1) e |= 1u << C::reg(RD, i);
+    return e;
+}
+
+template <class C, int RD>
+BW_HD inline uint32_t thread_part(uint32_t lane, uint32_t warp) {
+    uint32_t e = 0;
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+    for (int i = 0; i < 5; ++i) e |= ((lane >> i) & 1u) << C::lane(RD, i);
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+    for (int i = 0; i < 3; ++i) e |= ((warp >> i) & 1u) << C::warp(RD, i);
+    return e;
+}
+
+// Elements per shared-memory / global access of round RD: registers 0 and 1
+// on tile bits 0 and 1 give 4 consecutive int32, register 0 on bit 0 a pair.
+template <class C, int RD>
+BW_HD constexpr int vec() {
+    return C::reg(RD, 0) != 0 ? 1 : (C::nreg(RD) > 1 && C::reg(RD, 1) == 1) ? 4 : 2;
+}
+
+// Element offset of tile index e in a high pass's tile (kk = k + 1: the
+// compact layout moves index bits >= 14 up by one slot bit).
+template <int L>
+BW_HD inline uint64_t high_off(uint32_t e, int kk) {
+    return (uint64_t)(e & ((1u << L) - 1u)) + ((uint64_t)(e >> L) << kk);
+}
+
+// Slot of element 0 of tile t: the free slot bits [L, 14), [15, kk),
+// [kk + 14 - L, ...) take the tile id's bits in ascending order, so
+// neighbouring CTAs run neighbouring column groups.
+template <int L>
+BW_HD inline uint64_t high_tile_base(uint64_t t, int kk) {
+    constexpr int m1 = kBits - L;
+    const int m2 = kk - (kBits + 1);
+    const uint64_t lo = t & ((1ull << m1) - 1ull);
+    const uint64_t mid = (t >> m1) & ((1ull << m2) - 1ull);
+    const uint64_t hi = t >> (m1 + m2);
+    return (lo << L) | (mid << (kBits + 1)) | (hi << (kk + kBits - L));
+}
+
+#if defined(__CUDACC__)
+template <class C, int RD>
+__device__ __forceinline__ void stages32(u32 (&v)[kE]) {
+#pragma unroll
+    for (int i = 0; i < C::nreg(RD); ++i) {
+        if ((C::stage(RD) >> C::reg(RD, i)) & 1u) {
+#pragma unroll
+            for (int j = 0; j < kE; ++j) {
+                if (!((j >> i) & 1)) {
+                    const u32 a = v[j], b = v[j | (1 << i)];
+                    v[j] = a + b;
+                    v[j | (1 << i)] = a - b;
+                }
+            }
+        }
+    }
+}
+
+template <class C, int RD>
+__device__ __forceinline__ void smem_store32(const u32 (&v)[kE], u32* sm, uint32_t tp) {
+    constexpr int V = vec<C, RD>();
+    const uint32_t st = C::slot(tp);
+#pragma unroll
+    for (int j = 0; j < kE; j += V) {
+        u32* p = sm + (st ^ C::slot(reg_part<C, RD>(j)));
+        if constexpr (V == 4) *reinterpret_cast<uint4*>(p) = make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        else if constexpr (V == 2) *reinterpret_cast<uint2*>(p) = make_uint2(v[j], v[j + 1]);
+        else *p = v[j];
+    }
+}
+
+template <class C, int RD>
+__device__ __forceinline__ void smem_load32(u32 (&v)[kE], const u32* sm, uint32_t tp) {
+    constexpr int V = vec<C, RD>();
+    const uint32_t st = C::slot(tp);
+#pragma unroll
+    for (int j = 0; j < kE; j += V) {
+        const u32* p = sm + (st ^ C::slot(reg_part<C, RD>(j)));
+        if constexpr (V == 4) {
+            const uint4 t = *reinterpret_cast<const uint4*>(p);
+            v[j] = t.x;
+            v[j + 1] = t.y;
+            v[j + 2] = t.z;
+            v[j + 3] = t.w;
+        } else if constexpr (V == 2) {
+            const uint2 t = *reinterpret_cast<const uint2*>(p);
+            v[j] = t.x;
+            v[j + 1] = t.y;
+        } else {
+            v[j] = *p;
+        }
+    }
+}
+
+__device__ __forceinline__ uint4 ld4(const u32* p) {
+    uint4 t;
+    asm volatile("ld.global.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w)
+                 : "l"(p));
+    return t;
+}
+__device__ __forceinline__ uint2 ld2(const u32* p) {
+    uint2 t;
+    asm volatile("ld.global.L2::256B.v2.u32 {%0, %1}, [%2];" : "=r"(t.x), "=r"(t.y) : "l"(p));
+    return t;
+}
+__device__ __forceinline__ u32 ld1(const u32* p) {
+    u32 t;
+    asm volatile("ld.global.L2::256B.u32 %0, [%1];" : "=r"(t) : "l"(p));
+    return t;
+}
+
+// int32 -> int32 high pass over rows [k, k + 14 - L) of the compact layout.
+// src / dst: the int32 view of the signal, offset by the read / write half.
+template <int L>
+__global__ void __launch_bounds__(kNT, 2) k32_high(const u32* __restrict__ src, u32* __restrict__ dst, int k) {
+    using C = CfgHighW<L>;
+    extern __shared__ __align__(16) u32 sm32[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const int kk = k + 1;
+    const uint64_t base = high_tile_base<L>(blockIdx.x, kk);
+    u32 v[kE];
+    {
+        const uint32_t tp = thread_part<C, 0>(lane, warp);
+        const u32* p = src + base + high_off<L>(tp, kk);
+        constexpr int V = vec<C, 0>();
+#pragma unroll
+        for (int j = 0; j < kE; j += V) {
+            const u32* q = p + high_off<L>(reg_part<C, 0>(j), kk);
+            if constexpr (V == 4) {
+                const uint4 t = ld4(q);
+                v[j] = t.x;
+                v[j + 1] = t.y;
+                v[j + 2] = t.z;
+                v[j + 3] = t.w;
+            } else if constexpr (V == 2) {
+                const uint2 t = ld2(q);
+                v[j] = t.x;
+                v[j + 1] = t.y;
+            } else {
+                v[j] = ld1(q);
+            }
+        }
+    }
+    stages32<C, 0>(v);
+    BW_STRESS(60);
+    smem_store32<C, 0>(v, sm32, thread_part<C, 0>(lane, warp));
+    BW_STRESS(61);
+    __syncthreads();
+    const uint32_t tp = thread_part<C, 1>(lane, warp);
+    smem_load32<C, 1>(v, sm32, tp);
+    stages32<C, 1>(v);
+    u32* p = dst + base + high_off<L>(tp, kk);
+    constexpr int V = vec<C, 1>();
+#pragma unroll
+    for (int j = 0; j < kE; j += V) {
+        u32* q = p + high_off<L>(reg_part<C, 1>(j), kk);
+        if constexpr (V == 4) *reinterpret_cast<uint4*>(q) = make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        else if constexpr (V == 2) *reinterpret_cast<uint2*>(q) = make_uint2(v[j], v[j + 1]);
+        else *q = v[j];
+    }
+}
+
+// int32 -> int64 low pass over stages 0..13 of every block.  src: the int32
+// view offset by the read half (block b's copy at src + (b << 15)); dst: the
+// int64 signal (block b at dst + (b << 14)).
+__global__ void __launch_bounds__(kNT, 2) k32_low(const u32* __restrict__ src, unsigned long long* __restrict__ dst) {
+    using C = CfgLowW;
+    extern __shared__ __align__(16) u32 sm32[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t b = blockIdx.x;
+    u32 v[kE];
+    {
+        const uint32_t tp = thread_part<C, 0>(lane, warp);
+        const u32* p = src + (b << (kBits + 1)) + C::src_off(tp);
+        static_assert(vec<C, 0>() == 4, "16-byte loads");
+#pragma unroll
+        for (int j = 0; j < kE; j += 4) {
+            const uint4 t = ld4(p + C::src_off(reg_part<C, 0>(j)));
+            v[j] = t.x;
+            v[j + 1] = t.y;
+            v[j + 2] = t.z;
+            v[j + 3] = t.w;
+        }
+    }
+    stages32<C, 0>(v);
+    BW_STRESS(62);
+    smem_store32<C, 0>(v, sm32, thread_part<C, 0>(lane, warp));
+    BW_STRESS(63);
+    __syncthreads();
+    const uint32_t tp1 = thread_part<C, 1>(lane, warp);
+    smem_load32<C, 1>(v, sm32, tp1);
+    stages32<C, 1>(v);
+    BW_STRESS(64);
+    __syncthreads();  // every round-1 read is done before the slots are rewritten
+    smem_store32<C, 1>(v, sm32, tp1);
+    BW_STRESS(65);
+    __syncthreads();
+    unsigned long long* o = dst + (b << kBits);
+    static_assert(vec<C, 2>() == 2, "int32 pairs from shared memory, int64 pairs to global");
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const uint32_t tp = thread_part<C, 2>(lane, warp) | ((uint32_t)s << C::SUB);
+        const uint32_t st = C::slot(tp);
+        unsigned long long w[32];
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+            const uint2 t = *reinterpret_cast<const uint2*>(sm32 + (st ^ C::slot(reg_part<C, 2>(j))));
+            w[j] = (unsigned long long)(long long)(int)t.x;
+            w[j + 1] = (unsigned long long)(long long)(int)t.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            if ((C::stage(2) >> C::reg(2, i)) & 1u) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (!((j >> i) & 1)) {
+                        const unsigned long long a = w[j], c = w[j | (1 << i)];
+                        w[j] = a + c;
+                        w[j | (1 << i)] = a - c;
+                    }
+                }
+            }
+        }
+        BW_STRESS(66);
+        unsigned long long* p = o + tp;
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+            ulonglong2 t;
+            t.x = w[j];
+            t.y = w[j + 1];
+            st_pass(reinterpret_cast<ulonglong2*>(p + reg_part<C, 2>(j)), t);
+        }
+    }
+}
+#endif  // __CUDACC__
+
+}  // namespace w32
+}  // namespace bw

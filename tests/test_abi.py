@@ -382,16 +382,42 @@ def test_host_batch_validation_host_side():
         _lib.check(L.bw_fwht_xfused_pass_extract_i64(None, 1, 20, 5, 0, 10, 0, None, None, 16, None, None))
 
 
-@pytest.mark.parametrize("n", [16, 19, 22])
-def test_compact_plan_checks(n):
+@pytest.mark.parametrize("v2", ["0", "1"])
+@pytest.mark.parametrize("n", [16, 19, 22, 24])
+def test_compact_plan_checks(monkeypatch, n, v2):
     """The compact in-place plan's exact address tables (bw_plan_check_compact):
     natural int64 in and out, every pass loads where the previous one
     stored, no tile stores over bytes another tile of the same pass loads,
-    every bit staged once."""
+    every bit staged once; for the int32-engine passes (v2) also every
+    round's coverage, vector alignment and shared-memory bank conflicts."""
+    monkeypatch.setenv("BW_COMPACT_V2", v2)
     L = _lib.lib()
     assert L.bw_plan_check_compact(n) == 0, _lib.last_error()
     assert L.bw_compact_npasses(n) >= 2
-    assert L.bw_compact_limit(n) == (2**31 - 1) >> (n - 13)
+    # v1: no int32 value of the high passes wraps (H = n - 13 high stages);
+    # v2: every stage but the last four (int64) stays in int32
+    assert L.bw_compact_limit(n) == (2**31 - 1) >> (n - 4 if v2 == "1" else n - 13)
+
+
+@pytest.mark.parametrize("n,r2", [(16, "9"), (20, "9"), (24, "9"), (24, "8")])
+def test_compact_v2_host_emulation_matches_oracle(monkeypatch, coracle, n, r2):
+    """The int32-engine passes' exact tables (rounds, swizzled shared-memory
+    slots, int32 / int64 arithmetic) run on the host (bw_debug_emulate_compact)
+    on inputs at +-lim(n): bit-identical to the C oracle of fwht_array."""
+    monkeypatch.setenv("BW_COMPACT_R2", r2)
+    L = _lib.lib()
+    lim = L.bw_compact_limit(n)
+    rng = np.random.default_rng(n)
+    x = rng.integers(-lim, lim + 1, size=1 << n, dtype=np.int64)
+    x[rng.integers(0, 1 << n, size=256)] = lim
+    x[rng.integers(0, 1 << n, size=256)] = -lim
+    if n == 16:
+        x[:] = lim  # the extreme: index 0 reaches lim * 2^(n-4) = 2^31 - 1 - ... before the int64 stages
+    ref = x.copy()
+    coracle.oracle_fwht_i64(ref.ctypes.data, n)
+    y = x.copy()
+    assert L.bw_debug_emulate_compact(y.ctypes.data, n) == 0, _lib.last_error()
+    assert np.array_equal(y, ref)
 
 
 @pytest.mark.parametrize("rows,w", [("4,4,3", 13), ("5,5", 14), ("9,1", 14), ("3,3,2,2", 14)])
@@ -404,5 +430,10 @@ def test_compact_plan_shapes_check(monkeypatch, rows, w):
 
 def test_compact_checker_catches_a_layout_that_is_not_in_place(monkeypatch):
     monkeypatch.setenv("BW_COMPACT_BREAK", "1")  # bit c trades places with the top bit
+    monkeypatch.setenv("BW_COMPACT_V2", "0")
     assert _lib.lib().bw_plan_check_compact(20) != 0
     assert "not in place" in _lib.last_error()
+    # v2: the int32-engine low pass reads its fixed layout, which the broken
+    # first pass no longer writes
+    monkeypatch.setenv("BW_COMPACT_V2", "1")
+    assert _lib.lib().bw_plan_check_compact(20) != 0

@@ -66,6 +66,54 @@ def test_compact_plan_shapes(coracle, monkeypatch, rows, w):
     assert np.array_equal(y, c_fwht(coracle, x))
 
 
+@pytest.mark.parametrize("n,r2", [(16, "9"), (22, "9"), (23, "9"), (24, "9"), (24, "8"), (25, "9"), (26, "9"),
+                                  (27, "8"), (28, "9"), (29, "9"), (30, "9"), (30, "8")])
+def test_compact_v2_limit_values(coracle, monkeypatch, n, r2):
+    """The int32-engine plan (k32_high with 9 / 8 rows, k32_low with its last
+    four stages in int64) on inputs at +-lim(n) = (2^31 - 1) >> (n - 4),
+    with every first-pass shape (1..9 rows) over n = 24..30."""
+    monkeypatch.setenv("BW_COMPACT_R2", r2)
+    L = _lib.lib()
+    lim = L.bw_compact_limit(n)
+    assert lim == (2**31 - 1) >> (n - 4)
+    rng = np.random.default_rng(n * 3 + int(r2))
+    x = rng.integers(-lim, lim + 1, size=1 << n, dtype=np.int64)
+    x[rng.integers(0, 1 << n, size=4096)] = lim
+    x[rng.integers(0, 1 << n, size=4096)] = -lim
+    y, used = compact(x)
+    assert used == 1
+    assert np.array_equal(y, c_fwht(coracle, x))
+    y, used = compact(x, lim)  # known bound: unchecked, asynchronous
+    assert used == 1
+    assert np.array_equal(y, c_fwht(coracle, x))
+
+
+@pytest.mark.parametrize("n", [16, 24])
+def test_compact_v2_extreme_constant_signal(coracle, n):
+    """x = lim everywhere: index 0 carries lim * 2^(n-4) <= 2^31 - 1 into the
+    int64 stages -- the largest value the int32 engine ever holds."""
+    lim = _lib.lib().bw_compact_limit(n)
+    for v in (lim, -lim):
+        x = np.full(1 << n, v, dtype=np.int64)
+        y, used = compact(x)
+        assert used == 1
+        want = np.zeros(1 << n, dtype=np.int64)
+        want[0] = v << n
+        assert np.array_equal(y, want)
+
+
+def test_compact_v1_still_selectable(coracle, monkeypatch):
+    """BW_COMPACT_V2=0: the round-2 plan (int64-engine passes on int32 data)."""
+    monkeypatch.setenv("BW_COMPACT_V2", "0")
+    n = 24
+    lim = _lib.lib().bw_compact_limit(n)
+    assert lim == (2**31 - 1) >> (n - 13)
+    x = np.random.default_rng(3).integers(-lim, lim + 1, size=1 << n, dtype=np.int64)
+    y, used = compact(x)
+    assert used == 1
+    assert np.array_equal(y, c_fwht(coracle, x))
+
+
 @pytest.mark.parametrize("where", ["first", "last", "middle", "everywhere"])
 def test_compact_fallback_restores_exactly(coracle, where):
     """One input over lim(n): the checked first pass leaves that tile (and
