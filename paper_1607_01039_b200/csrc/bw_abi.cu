@@ -1996,8 +1996,9 @@ int w32_visit_pass(const CompactPlan& cp, int q, F&& f) {
                 const uint32_t lane = th & 31u, warp = th >> 5;
                 for (int j = 0; j < w::kE; ++j) {
                     const uint32_t e = w::thread_part<C, 0>(lane, warp) | w::reg_part<C, 0>(j);
+                    // the kernel treats tile element e as index (b << 14) + e
                     const uint64_t slot = (b << (w::kBits + 1)) + C::src_off(e);
-                    f(0, b, e, (so + slot) * 4, 4, compact_index_of(lam, n, slot));
+                    f(0, b, e, (so + slot) * 4, 4, (b << w::kBits) + e);
                 }
                 for (uint32_t s = 0; s < 2; ++s)
                     for (int j = 0; j < 32; ++j) {
@@ -2015,6 +2016,9 @@ int w32_visit_pass(const CompactPlan& cp, int q, F&& f) {
         constexpr int L = decltype(lc)::value;
         if (!w32_rounds_ok<C>(&why)) return fail(BW_BAD_ARGUMENTS, "int32 high pass layout: %s", why.c_str());
         const int kk = p.k + 1;
+        for (int i = 0; i < p.r; ++i)  // tile row i is index bit k + i (the stage the kernel applies)
+            if (compact_index_of(lam, n, w::high_off<L>(1u << (L + i), kk)) != 1ull << (p.k + i))
+                return fail(BW_BAD_ARGUMENTS, "int32 high pass row %d is not index bit %d", i, p.k + i);
         for (uint64_t t = 0; t < tiles; ++t) {
             const uint64_t base = w::high_tile_base<L>(t, kk);
             for (uint32_t th = 0; th < (uint32_t)w::kNT; ++th) {
