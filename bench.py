@@ -62,9 +62,12 @@ def args_parse():
     ap.add_argument("--cpu-full", action="store_true",
                     help="also time ONE reference run_parallel at the full config size (slow; written to "
                          "profiles/r02_cpu_reference_full.json)")
-    ap.add_argument("--intermediates", choices=["narrow", "int64"], default="int64",
-                    help="narrow: the narrow-intermediate plan (int16/int32 between passes, checked, int64 "
-                         "fallback; 5%% faster at n = 32 with a 24 GiB work buffer, DESIGN.md section 5); int64: the plain int64 plan")
+    ap.add_argument("--intermediates", choices=["auto", "compact", "narrow", "int64"], default="auto",
+                    help="auto: what fwht_array runs by default -- the compact in-place plan (int32 intermediates "
+                         "inside the signal's own buffer, first pass checked, int64 plan on larger values) where "
+                         "the library picks it (n = 30..32, one GPU, no fused extraction), else the int64 plan; "
+                         "compact: the compact plan wherever one exists; narrow: the narrow-intermediate plan "
+                         "(needs a 24 GiB work buffer at n = 32, DESIGN.md section 5); int64: the plain int64 plan")
     ap.add_argument("--mode", choices=["auto", "fused", "peer", "a2a", "narrow"], default="auto",
                     help="cross-GPU exchange (N > 1); auto times fused and a2a (peer with gloo) on two "
                          "steps each and keeps the faster")
@@ -336,6 +339,24 @@ def run_ours(a):
         nflag = torch.zeros(1, dtype=torch.int32, device="cuda")
         npasses = nn
         n_fallback = 0
+    # Compact in-place intermediates (one GPU, no fused extraction): what
+    # bw_fwht_i64 / fwht_array run by default at these sizes, pass by pass --
+    # the checked first pass (natural int64 -> int32 inside the buffer), the
+    # verdict readback, the int32 -> int32 pass(es), the widening low pass.
+    ncp = L.bw_compact_npasses(nl) if (p == 0 and spec.threshold is None and not whole) else 0
+    compact_local = (not narrow_local and ncp > 0 and
+                     (a.intermediates == "compact" or (a.intermediates == "auto" and L.bw_compact_auto(nl) == 1)))
+    n_fallback = 0
+    if compact_local:
+        cflags = torch.zeros(1 << max(nl - 13, 0), dtype=torch.int32, device="cuda")
+        cabort = torch.zeros(1, dtype=torch.int32, device="cuda")
+        npasses = nn = ncp
+        cinfo = []
+        for i in range(ncp):
+            k_, r_, e_, b_ = (ctypes.c_int(0) for _ in range(4))
+            _lib.check(L.bw_compact_pass_info(nl, i, ctypes.byref(k_), ctypes.byref(r_), ctypes.byref(e_),
+                                              ctypes.byref(b_)))
+            cinfo.append({"k": k_.value, "r": r_.value, "engine": e_.value, "bytes_per_point": b_.value})
     # Cross-GPU exchange candidates (N > 1): the fused pass over peer
     # pointers (K6'), the separate peer exchange (K6), or NCCL all-to-all +
     # K6 on the receive rows.  "auto" times the first two that apply.
@@ -364,7 +385,7 @@ def run_ours(a):
             st["f_arr"] = (ctypes.c_int * len(st["f_widths"]))(*st["f_widths"])
         if mode == "a2a" and "recv" not in st:
             st["recv"] = torch.empty_like(x)
-        st["nev"] = 2 if whole else 2 * nn + 1 if narrow_local else st["npasses"] + 4
+        st["nev"] = 2 if whole else 2 * nn + 1 if (narrow_local or compact_local) else st["npasses"] + 4
 
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
@@ -411,10 +432,10 @@ def run_ours(a):
             dist.barrier()
 
     def step(ev):
+        nonlocal n_fallback
         npasses = st["npasses"]
         if narrow_local:
             # ev[2i] .. ev[2i+1]: narrow pass i; ev[1] .. ev[2]: the flag readback
-            nonlocal n_fallback
             ev[0].record(stream)
             nflag.zero_()
             _lib.check(L.bw_fwht_i64_narrow_pass(ptr, nl, nwork.data_ptr(), nneed, 0, nflag.data_ptr(), sh))
@@ -423,12 +444,36 @@ def run_ours(a):
             ev[2].record(stream)
             if bad:  # a value over int16 after the low pass: the int64 plan (the signal is untouched)
                 n_fallback += 1
-                _lib.check(L.bw_fwht_i64(ptr, nl, sh, None))
+                _lib.check(L.bw_fwht_i64_int64plan(ptr, nl, sh, None))
                 for i in range(3, 2 * nn + 1):
                     ev[i].record(stream)
                 return
             for i in range(1, nn):
                 _lib.check(L.bw_fwht_i64_narrow_pass(ptr, nl, nwork.data_ptr(), nneed, i, nflag.data_ptr(), sh))
+                ev[2 * i + 1].record(stream)
+                if i + 1 < nn:
+                    ev[2 * i + 2].record(stream)
+            ev[-1].record(stream)
+            return
+        if compact_local:
+            # ev[2i] .. ev[2i+1]: compact pass i; ev[1] .. ev[2]: the verdict readback (one stream
+            # synchronisation, as inside bw_fwht_i64); the flag words are cleared inside the step
+            ev[0].record(stream)
+            cflags.zero_()
+            cabort.zero_()
+            _lib.check(L.bw_fwht_i64_compact_pass(ptr, nl, 0, 1, cflags.data_ptr(), cabort.data_ptr(), sh))
+            ev[1].record(stream)
+            bad = int(cabort.item())
+            ev[2].record(stream)
+            if bad:  # a value over lim(n): the written tiles restored, then the int64 plan
+                n_fallback += 1
+                _lib.check(L.bw_fwht_i64_compact_restore(ptr, nl, cflags.data_ptr(), sh))
+                _lib.check(L.bw_fwht_i64_int64plan(ptr, nl, sh, None))
+                for i in range(3, 2 * nn + 1):
+                    ev[i].record(stream)
+                return
+            for i in range(1, nn):
+                _lib.check(L.bw_fwht_i64_compact_pass(ptr, nl, i, 0, None, None, sh))
                 ev[2 * i + 1].record(stream)
                 if i + 1 < nn:
                     ev[2 * i + 2].record(stream)
@@ -620,7 +665,9 @@ def run_ours(a):
     # (reported beside the headline, not as it: after four transforms a +-1
     # signal is 0 mod 2^64, and the kernels run slightly faster on zeros).
     b2b = None
-    if restore_each and ws == 1 and p == 0 and not (extract or extract_dist):
+    # (not for the compact / narrow plans: a second transform of the output exceeds their limits and would
+    # run -- and count -- the int64 fallback)
+    if restore_each and ws == 1 and p == 0 and not (extract or extract_dist) and not (compact_local or narrow_local):
         torch.cuda.synchronize()
         restore()
         bev = [events() for _ in range(a.steps)]
@@ -635,7 +682,7 @@ def run_ours(a):
     step_ms = [e[0].elapsed_time(e[-1]) for e in evs]
     per_step = flush or restore_each  # something untimed runs between steps
     total_ms = sum(step_ms) if per_step else evs[0][0].elapsed_time(evs[-1][-1])
-    if narrow_local:  # pass i runs between ev[2i] and ev[2i+1]; ev[1] .. ev[2] is the flag readback
+    if narrow_local or compact_local:  # pass i runs between ev[2i] and ev[2i+1]; ev[1] .. ev[2] is the flag readback
         pass_ms = [[e[0 if i == 0 else 2 * i].elapsed_time(e[1 if i == 0 else 2 * i + 1]) for e in evs]
                    for i in range(npasses)]
     else:
@@ -651,7 +698,8 @@ def run_ours(a):
     peak, peak_src = hbm_peak()
     bytes_per_pass = 16 * (2 ** nl) * (2 if whole else 1)
     # algorithmic bytes per point of each pass (read + write)
-    bpp = ([10, 6, 12] if npasses == 3 else [10, 10]) if narrow_local else [bytes_per_pass // (2 ** nl)] * npasses
+    bpp = (([10, 6, 12] if npasses == 3 else [10, 10]) if narrow_local else
+           [c["bytes_per_point"] for c in cinfo] if compact_local else [bytes_per_pass // (2 ** nl)] * npasses)
     dom = max(range(npasses), key=lambda i: avg_pass[i])
     achieved = bpp[dom] * (2 ** nl) / (avg_pass[dom] / 1e3) / 1e9
     launches = a.steps * (npasses + (1 if extract else 0) + (1 if p > 0 else 0))  # whole: 1 launch per step
@@ -669,7 +717,10 @@ def run_ours(a):
     # run's plan; round 1's (one-run plans, no plan recorded) only for the
     # narrow plan it was taken on
     cur_plan = [[q["kind"], q["k"], q["r"], q.get("split_a", 0), q.get("k2", 0)] for q in plan["passes"]]
-    for tname in ([f"r01_traffic_n{nl}_narrow.json"] if narrow_local else [f"r02_traffic_n{nl}.json"]):
+    if compact_local:
+        cur_plan = [["compact", c["k"], c["r"], c["engine"]] for c in cinfo]
+    for tname in ([f"r01_traffic_n{nl}_narrow.json"] if narrow_local else
+                  [f"r02_traffic_n{nl}_compact.json"] if compact_local else [f"r02_traffic_n{nl}.json"]):
         try:
             with open(os.path.join(ROOT, "profiles", tname)) as f:
                 tr = json.load(f)
@@ -689,6 +740,7 @@ def run_ours(a):
         import paper_1607_01039_b200 as bw
 
         calls = {"fwht_array": lambda: bw.fwht_array(x),
+                 "fwht_array_int64_plan": lambda: bw.fwht_array(x, compact=False),
                  "fwht_inplace": lambda: bw.fwht_inplace(bw.Signal(x)),
                  "fwht_inplace_known_bound": lambda: bw.fwht_inplace(bw.Signal(x), max_abs=spec.max_abs)}
         entry_points = {}
@@ -709,6 +761,7 @@ def run_ours(a):
         entry_points["known_bound_vs_fwht_array"] = round(
             entry_points["fwht_inplace_known_bound_ms"] / entry_points["fwht_array_ms"], 4)
         entry_points["max_abs"] = spec.max_abs
+        entry_points["fwht_array_ran_compact_plan"] = bool(L.bw_compact_auto(nl)) and spec.max_abs <= L.bw_compact_limit(nl)
 
     # One more step of the same kind from the config input, then its output
     # gathered at the row space of a seeded fold map: checked on the CPU
@@ -769,6 +822,22 @@ def run_ours(a):
         line["config"]["algorithmic_bytes_per_point"] = bpp
         line["roofline"]["kernel"] = (f"narrow pass {dom} (k_pass_map, "
                                       f"{['int64->int16', 'int16->int32', 'int32->int64'][dom] if npasses == 3 else ['int64->int16', 'int16->int64'][dom]})")
+        line["flag_readback_ms"] = round(sum(e[1].elapsed_time(e[2]) for e in evs) / len(evs), 4)
+    elif compact_local:
+        names = ["k32_first (natural int64 -> int32 in place, every input tested)" if cinfo[0]["engine"] == 32
+                 else "k_pass_map (int64 -> int32, every input tested)"]
+        names += ["k32_high (int32 -> int32)" if c["engine"] == 32 else "k_pass_map (int32 -> int32)" for c in cinfo[1:-1]]
+        names += ["k32_low (int32 -> natural int64, last four stages in int64)" if cinfo[-1]["engine"] == 32
+                  else "k_pass_map (int32 -> int64)"]
+        line["config"]["intermediates"] = ("compact in place: int32 copies inside the signal's own buffer between "
+                                           "the passes, high stages first, first pass checked (|x| <= "
+                                           f"{L.bw_compact_limit(nl)}), int64 plan after an exact restore otherwise; "
+                                           "the library's default at this size")
+        line["config"]["passes"] = [{"kernel": nm, "stages": f"{c['k']}..{c['k'] + c['r'] - 1}",
+                                     "bytes_per_point": c["bytes_per_point"]} for nm, c in zip(names, cinfo)]
+        line["config"]["compact_fallbacks"] = n_fallback
+        line["config"]["algorithmic_bytes_per_point"] = bpp
+        line["roofline"]["kernel"] = f"compact pass {dom}: {names[dom]}, stages {line['config']['passes'][dom]['stages']}"
         line["flag_readback_ms"] = round(sum(e[1].elapsed_time(e[2]) for e in evs) / len(evs), 4)
     else:
         line["config"]["intermediates"] = "int64"

@@ -69,7 +69,10 @@ int bw_device_cc(int device);
  * In-place FWHT of data[0 .. 2^log2n).  Replaces `fwht_array(buf) -> int`
  * (/root/reference/pkg/src/bigwht/core.py:97-117): no magnitude check (the
  * reference has none either), returns the butterfly count n*2^(n-1)
- * (core.py:117) in *butterflies (may be NULL).  Asynchronous.
+ * (core.py:117) in *butterflies (may be NULL).  Asynchronous, except for
+ * the sizes bw_compact_auto() names (n = 30..32 by default), where the
+ * compact plan is tried first and the call waits once for its first pass's
+ * verdict (below: bw_fwht_i64_compact; bw_fwht_i64_int64plan never does).
  * Pass plan: one fused low-bits pass over stages 0..12/13/14 followed by
  * strided high-bits passes of <= 10 stages each, chosen by the measured
  * cost model, i.e. the blocked decomposition of
@@ -166,8 +169,9 @@ int bw_plan_check_narrow(int log2n);
 
 /*
  * fwht_array with COMPACT IN-PLACE INTERMEDIATES: for |x| <= lim(n)
- * (bw_compact_limit; 8191 at n = 32, 2047 at n = 34 -- the +-1 Boolean
- * signals of the paper and any small-integer signal) the high-bit stages
+ * (bw_compact_limit; 7 at n = 32 and 31 at n = 30 with the int32 engine,
+ * 2047 at n = 34 with the int64 engine's passes -- the +-1 Boolean signals
+ * of the paper and any small-integer signal) the high-bit stages
  * run first with the signal stored as int32 inside its own buffer, and the
  * low-bit pass widens back to natural int64: 12 + 8 (m - 1) + 12 bytes per
  * point for m high passes instead of 16 per pass, and NO work buffer.  Exact:
@@ -183,9 +187,27 @@ int bw_plan_check_narrow(int log2n);
  */
 int bw_fwht_i64_compact(int64_t *data, int log2n, long long max_abs, void *stream, int *used_compact,
                         uint64_t *butterflies);
+/*
+ * Whether bw_fwht_i64 / bw_fwht_inplace_i64 / bw_fwht_inplace_known_i64 try
+ * the compact plan by themselves on a 16-byte aligned signal of 2^log2n
+ * points: by default (BW_COMPACT unset or "auto") for the sizes whose every
+ * pass runs on the int32 engine and measured faster (n = 30..32: 21.5 vs
+ * 31.4 ms at n = 32); BW_COMPACT=1: wherever a compact plan exists (n >= 22);
+ * BW_COMPACT=0: never.  fwht_array then synchronises the stream once (the
+ * first pass's verdict) and is otherwise unchanged: same result bit for bit,
+ * the int64 plan for signals with larger values.
+ */
+int bw_compact_auto(int log2n);
+/* fwht_array (core.py:97-117) on the int64 plan whatever the data: asynchronous,
+ * never the compact plan (the A/B partner and fallback of bw_fwht_i64). */
+int bw_fwht_i64_int64plan(int64_t *data, int log2n, void *stream, uint64_t *butterflies);
 /* lim(n) of the compact plan (-1: none for this n), its pass count (0: none). */
 long long bw_compact_limit(int log2n);
 int bw_compact_npasses(int log2n);
+/* Pass i of the compact plan (instrumentation): first stage bit, stage count, the
+ * engine (32: the int32 register engine, 64: the int64 engine's mapped passes)
+ * and algorithmic bytes per point (12 / 8 / 12); any pointer may be NULL. */
+int bw_compact_pass_info(int log2n, int pass_index, int *k, int *r, int *engine, int *bytes_per_point);
 /* One compact pass, asynchronous (instrumentation); checked = 1 only for pass 0:
  * tileflag_dev (2^(n-13) words, zeroed) and *abort_dev (zeroed) record the outcome. */
 int bw_fwht_i64_compact_pass(int64_t *data, int log2n, int pass_index, int checked, uint32_t *tileflag_dev,

@@ -57,6 +57,9 @@ _SIGNATURES = {
     "bw_fwht_i64_narrow_pass": ([P, I32, P, U64, I32, P, P], I32),
     "bw_plan_check_narrow": ([I32], I32),
     "bw_fwht_i64_compact": ([P, I32, ctypes.c_longlong, P, ctypes.POINTER(I32), PU64], I32),
+    "bw_compact_auto": ([I32], I32),
+    "bw_fwht_i64_int64plan": ([P, I32, P, PU64], I32),
+    "bw_compact_pass_info": ([I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32)], I32),
     "bw_compact_limit": ([I32], ctypes.c_longlong),
     "bw_compact_npasses": ([I32], I32),
     "bw_fwht_i64_compact_pass": ([P, I32, I32, I32, P, P, P], I32),

@@ -231,19 +231,18 @@ def _narrow_wanted(n: int, narrow) -> int:
 
 
 last_compact = False  # whether the last fwht_array call ran the compact in-place plan (diagnostics)
-COMPACT_MIN_N = 22  # below this the checked plan's one stream synchronisation outweighs the bytes it saves
 
 
 def _compact_wanted(n: int, compact) -> bool:
     """Whether fwht_array tries the compact in-place plan (int32
     intermediates inside the signal's own buffer, bw_fwht_i64_compact).
-    compact=None follows BW_COMPACT (off unless "1": the plan moves a third
-    fewer bytes but measured no faster) for
-    n >= COMPACT_MIN_N."""
+    compact=None follows the library's default (bw_compact_auto: n = 30..32,
+    where every pass runs on the int32 engine and the plan measured a third
+    faster; BW_COMPACT=1 / 0 widens it to n >= 22 / turns it off)."""
     if compact is False or _lib.lib().bw_compact_npasses(n) == 0:
         return False
     if compact is None:
-        return os.environ.get("BW_COMPACT", "0") == "1" and n >= COMPACT_MIN_N
+        return bool(_lib.lib().bw_compact_auto(n))
     return True
 
 
@@ -265,11 +264,13 @@ def fwht_array(buf, narrow=None, compact=None) -> int:
     compact (CUDA int64 tensors): the compact in-place plan
     (bw_fwht_i64_compact) -- the high-bit stages first with the signal kept
     as int32 inside its own buffer, then the low pass widening back to int64.
-    Its first pass tests every input against lim(n) (8191 at n = 32); if one
-    is larger, the tiles already written are restored exactly and the int64
-    plan runs.  Results are identical either way.  None: only with
-    BW_COMPACT=1 (n >= 22); True: the checked plan; an int: a bound on |x|
-    the caller guarantees (no test, no synchronisation).
+    Its first pass tests every input against lim(n) (7 at n = 32, 31 at
+    n = 30); if one is larger, the tiles already written are restored exactly
+    and the int64 plan runs.  Results are identical either way.  None: the
+    library's default (tried at n = 30..32, where it measured a third faster:
+    21.5 vs 31.4 ms at n = 32; BW_COMPACT=1 / 0: n >= 22 / never); True: the
+    checked plan; False: the int64 plan; an int: a bound on |x| the caller
+    guarantees (no test, no synchronisation).
     """
     global last_narrow, last_compact
     last_narrow = False
@@ -315,8 +316,8 @@ def fwht_array(buf, narrow=None, compact=None) -> int:
             _lib.check(L.bw_fwht_i64_narrow(buf.data_ptr(), n, work.data_ptr(), need, _stream_handle(buf),
                                             ctypes.byref(used), ctypes.byref(bf)))
             last_narrow = bool(used.value)
-        elif kind == "i64":
-            _lib.check(L.bw_fwht_i64(buf.data_ptr(), n, _stream_handle(buf), ctypes.byref(bf)))
+        elif kind == "i64":  # (the compact default was decided above: bw_fwht_i64 would ask again)
+            _lib.check(L.bw_fwht_i64_int64plan(buf.data_ptr(), n, _stream_handle(buf), ctypes.byref(bf)))
         else:
             _lib.check(L.bw_fwht_f64(buf.data_ptr(), n, _stream_handle(buf), ctypes.byref(bf)))
     return int(bf.value)

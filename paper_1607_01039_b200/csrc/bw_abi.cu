@@ -83,9 +83,17 @@ int low_prefetch_tiles(int q) {
 }
 // BW_FUSED_BOUND=0: fwht_inplace runs the separate bound reduction first (A/B knob).
 const bool g_fused_bound = !(getenv("BW_FUSED_BOUND") && getenv("BW_FUSED_BOUND")[0] == '0');
-// BW_COMPACT=1: fwht_inplace picks the compact in-place plan when its bound
-// allows (opt-in: measured no faster than the int64 plan).
-const bool g_compact = getenv("BW_COMPACT") && getenv("BW_COMPACT")[0] == '1';
+// BW_COMPACT (read per call): unset / "auto" -- fwht_array and fwht_inplace
+// try the compact in-place plan where it measured faster than the int64 plan
+// (compact_default below: every pass on the int32 engine, n = 30..32); "1" --
+// wherever a compact plan exists (n >= 22); "0" -- never.
+int compact_mode() {
+    const char* e = getenv("BW_COMPACT");
+    if (!e || !*e || e[0] == 'a') return -1;
+    return e[0] == '1' ? 1 : 0;
+}
+bool compact_default(int log2n, const void* data);                       // after compact_plan
+int compact_try(int64_t* data, int log2n, cudaStream_t s, int* used);  // after launch_compact
 // BW_FOLD_BLOCKS=0 keeps the shared-bin / L2-atomic fold for d_out > 12 (A/B knob, read per call).
 bool fold_blocks_enabled() { return !(getenv("BW_FOLD_BLOCKS") && getenv("BW_FOLD_BLOCKS")[0] == '0'); }
 // BW_F64_VEC_LOW=0 keeps the float64 low pass on 8-byte accesses (A/B knob).
@@ -609,6 +617,12 @@ int set_all_pass_attributes() {
     BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_high<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
     BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_high<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
     BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_low, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
+    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_first<5, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
+    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_first<5, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
+    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_first<6, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
+    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_first<6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
+    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_restore<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
+    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_restore<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
     BW_TRY(set_fused_attrs<1>());
     BW_TRY(set_fused_attrs<2>());
     BW_TRY(set_fused_attrs<3>());
@@ -935,6 +949,17 @@ int bw_device_cc(int device) {
 
 // fwht_array (core.py:97-117)
 int bw_fwht_i64(int64_t* data, int log2n, void* stream, uint64_t* butterflies) {
+    BW_TRY(check_signal(data, log2n));
+    // signals the compact plan is faster on try it first: its first pass tests
+    // every input and the int64 plan takes over (after an exact restore) when
+    // a value is too large for int32 intermediates; bit-identical either way
+    if (compact_default(log2n, data)) return bw_fwht_i64_compact(data, log2n, -1, stream, nullptr, butterflies);
+    return bw_fwht_i64_int64plan(data, log2n, stream, butterflies);
+}
+
+// fwht_array on the int64 plan, whatever the data (asynchronous; the A/B
+// partner of the default above and its fallback).
+int bw_fwht_i64_int64plan(int64_t* data, int log2n, void* stream, uint64_t* butterflies) {
     BW_TRY(fwht_impl(data, log2n, nullptr, false, as_stream(stream)));
     if (butterflies) *butterflies = butterfly_count(log2n);
     return BW_OK;
@@ -1198,6 +1223,19 @@ extern "C" {
 // picks the compact in-place plan when M <= lim(n).
 int bw_fwht_inplace_i64(int64_t* data, int log2n, int64_t* scratch_dev, void* stream, uint64_t* butterflies) {
     BW_TRY(check_signal(data, log2n));
+    const bool auto_compact = compact_mode() < 0 && compact_default(log2n, data);
+    if (auto_compact) {
+        // the compact plan's input test (|x| <= lim(n) < 2^(63-n)) is stricter
+        // than the overflow bound: a signal that passes it is transformed at
+        // once; otherwise the buffer is as it was and the bound is checked below
+        int used = 0;
+        BW_TRY(compact_try(data, log2n, as_stream(stream), &used));
+        if (used) {
+            if (butterflies) *butterflies = butterfly_count(log2n);
+            return BW_OK;
+        }
+    }
+    const bool g_compact = compact_mode() == 1;
     if (!g_compact) {
         bool handled = false;
         const int rc = fused_bound_inplace(data, log2n, as_stream(stream), &handled);
@@ -1211,7 +1249,7 @@ int bw_fwht_inplace_i64(int64_t* data, int log2n, int64_t* scratch_dev, void* st
     BW_TRY(bw_check_bound_i64(data, log2n, scratch_dev, stream, &m));
     if (g_compact && m <= (uint64_t)0x7fffffff)
         return bw_fwht_i64_compact(data, log2n, (long long)m, stream, nullptr, butterflies);
-    return bw_fwht_i64(data, log2n, stream, butterflies);
+    return bw_fwht_i64_int64plan(data, log2n, stream, butterflies);
 }
 
 // fwht_inplace with the bound M supplied by the caller (SURVEY.md 8b
@@ -1225,8 +1263,9 @@ int bw_fwht_inplace_known_i64(int64_t* data, int log2n, int64_t max_abs, void* s
         return fail(BW_OVERFLOW_BOUND,
                     "max |x| = %llu with n = %d can overflow int64; need |x| * 2**n < 2**63",
                     (unsigned long long)max_abs, log2n);
-    if (g_compact && max_abs <= 0x7fffffff) return bw_fwht_i64_compact(data, log2n, max_abs, stream, nullptr, butterflies);
-    return bw_fwht_i64(data, log2n, stream, butterflies);
+    if ((compact_mode() == 1 || compact_default(log2n, data)) && max_abs <= 0x7fffffff)
+        return bw_fwht_i64_compact(data, log2n, max_abs, stream, nullptr, butterflies);  // int64 plan above lim(n)
+    return bw_fwht_i64_int64plan(data, log2n, stream, butterflies);
 }
 
 }  // extern "C"
@@ -1587,6 +1626,7 @@ namespace {
 struct CompactPlan {
     int n = 0, w = 0, c = 0, m = 0;  // m high passes, then the low pass
     bool v2 = false;                  // passes after the first on the int32 engine (bw_kernels32.cuh)
+    bool first32 = false;             // v2 and the first pass on it too (8 or 9 rows)
     std::vector<Pass> pass;           // shapes for the kernel visitor
     std::vector<PassGeom> geom;
     std::vector<int> half;            // half written by high pass j
@@ -1601,8 +1641,13 @@ struct CompactPlan {
 // CTA) and the 14-bit low pass k32_low, whose last four stages (bits 10..13)
 // run in int64 registers.  So v2 admits |x| <= (2^31 - 1) >> (n - 4): every
 // stage but the last four keeps |value| <= 2^31 - 1.  Rows: one high pass
-// for H <= 9, else H - r2 then r2 = 9 (BW_COMPACT_R2=8: 8).
+// for H <= 9, else H - r2 then r2 = 8 (256-byte row segments), 9 at H = 18
+// (BW_COMPACT_R2=8|9 forces it).  A FIRST pass of 8 or 9 rows also runs on
+// the int32 engine (k32_first: natural int64 -> int32, the input test of the
+// unknown-bound case inside it; BW_COMPACT_FIRST=0: the int64 engine's
+// k_pass_map as before).
 bool compact_v2_enabled() { return !(getenv("BW_COMPACT_V2") && getenv("BW_COMPACT_V2")[0] == '0'); }
+bool compact_first32_enabled() { return !(getenv("BW_COMPACT_FIRST") && getenv("BW_COMPACT_FIRST")[0] == '0'); }
 
 bool compact_plan(int n, CompactPlan* cp) {
     if (n < 16 || n > 36) return false;
@@ -1628,7 +1673,8 @@ bool compact_plan(int n, CompactPlan* cp) {
     if (rows_env) {
         if (sum != H) return false;
     } else if (v2) {
-        const int r2 = getenv("BW_COMPACT_R2") && atoi(getenv("BW_COMPACT_R2")) == 8 ? 8 : 9;
+        int r2 = H - 8 <= 9 ? 8 : 9;
+        if (const char* e = getenv("BW_COMPACT_R2")) r2 = atoi(e) == 8 ? 8 : 9;
         if (H <= 9) rows.push_back(H);
         else if (H - r2 >= 1 && H - r2 <= 9) {
             rows.push_back(H - r2);
@@ -1644,6 +1690,7 @@ bool compact_plan(int n, CompactPlan* cp) {
     cp->c = w - 1;
     cp->m = (int)rows.size();
     cp->v2 = v2;
+    cp->first32 = v2 && compact_first32_enabled() && (rows[0] == 8 || rows[0] == 9);
     cp->lim = 0x7fffffffll >> (v2 ? n - 4 : H);
     cp->pass.clear();
     cp->geom.clear();
@@ -1728,13 +1775,32 @@ int launch_compact(const CompactPlan& cp, int i, int64_t* data, CompactMode mode
     const Pass& p = cp.pass[i];
     const PassGeom& g = cp.geom[i];
     const int tpc = getenv("BW_COMPACT_TPC") ? atoi(getenv("BW_COMPACT_TPC")) : 1;
-    if (cp.v2 && i > 0) {  // the int32 engine: 2^14 elements per CTA, no cluster
+    if (cp.v2 && (i > 0 || cp.first32)) {  // the int32 engine: 2^14 elements per CTA, no cluster
         const unsigned grid = (unsigned)(1ull << (cp.n - bw::w32::kBits));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(bw::w32::kNT);
         cfg.dynamicSmemBytes = bw::w32::kSmemBytes;
         cfg.stream = s;
+        if (i == 0) {  // natural int64 -> int32 (plain / input test), or the restore of the tiles it wrote
+            namespace w = bw::w32;
+            const unsigned long long* s64 = reinterpret_cast<const unsigned long long*>(data);
+            unsigned long long* d64u = reinterpret_cast<unsigned long long*>(data);
+            uint32_t* h32 = reinterpret_cast<uint32_t*>(d32 + ((size_t)cp.half[0] << cp.w));
+            const uint32_t lim = (uint32_t)cp.lim;
+            if (mode != COMPACT_PLAIN && !tileflag) return fail(BW_BAD_ARGUMENTS, "checked / restore passes need tile flags");
+            if (mode == COMPACT_CHECK && !abort) return fail(BW_BAD_ARGUMENTS, "a checked pass needs the abort word");
+            if (p.r == 9) {
+                if (mode == COMPACT_RESTORE) BW_CUDA(cudaLaunchKernelEx(&cfg, w::k32_restore<5>, (const uint32_t*)h32, d64u, p.k, (const unsigned*)tileflag));
+                else if (mode == COMPACT_CHECK) BW_CUDA(cudaLaunchKernelEx(&cfg, w::k32_first<5, w::FIRST_CHECK>, s64, h32, p.k, lim, tileflag, abort));
+                else BW_CUDA(cudaLaunchKernelEx(&cfg, w::k32_first<5, w::FIRST_PLAIN>, s64, h32, p.k, lim, (unsigned*)nullptr, (unsigned*)nullptr));
+            } else {
+                if (mode == COMPACT_RESTORE) BW_CUDA(cudaLaunchKernelEx(&cfg, w::k32_restore<6>, (const uint32_t*)h32, d64u, p.k, (const unsigned*)tileflag));
+                else if (mode == COMPACT_CHECK) BW_CUDA(cudaLaunchKernelEx(&cfg, w::k32_first<6, w::FIRST_CHECK>, s64, h32, p.k, lim, tileflag, abort));
+                else BW_CUDA(cudaLaunchKernelEx(&cfg, w::k32_first<6, w::FIRST_PLAIN>, s64, h32, p.k, lim, (unsigned*)nullptr, (unsigned*)nullptr));
+            }
+            return BW_OK;
+        }
         const uint32_t* src = reinterpret_cast<const uint32_t*>(d32 + ((size_t)cp.half[i - 1] << cp.w));
         if (i == cp.m) {
             BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_low, src, reinterpret_cast<unsigned long long*>(data)));
@@ -1818,8 +1884,47 @@ int compact_scratch(int dev, const CompactPlan& cp, unsigned** tileflag, unsigne
     BW_CUDA(cudaMemsetAsync(sc, 0, 64 + 4 * tiles, s));
     return BW_OK;
 }
+
+// The compact plan on a signal of unknown magnitude: the first pass tests
+// every input (one stream synchronisation to read the verdict).  *used = 1:
+// the transform is done (asynchronously).  *used = 0: an input was too large
+// (or there is no plan): the buffer holds the caller's input again.
+int compact_try(int64_t* data, int log2n, cudaStream_t s, int* used) {
+    *used = 0;
+    CompactPlan cp;
+    if ((reinterpret_cast<uintptr_t>(data) & 15u) || !compact_plan(log2n, &cp)) return BW_OK;
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    unsigned *tileflag = nullptr, *abort = nullptr;
+    BW_TRY(compact_scratch(dev, cp, &tileflag, &abort, s));
+    BW_TRY(launch_compact(cp, 0, data, COMPACT_CHECK, tileflag, abort, s));
+    unsigned bad = 0;
+    BW_CUDA(cudaMemcpyAsync(&bad, abort, sizeof bad, cudaMemcpyDeviceToHost, s));
+    BW_CUDA(cudaStreamSynchronize(s));
+    if (bad) return launch_compact(cp, 0, data, COMPACT_RESTORE, tileflag, abort, s);
+    for (int i = 1; i <= cp.m; ++i) BW_TRY(launch_compact(cp, i, data, COMPACT_PLAIN, nullptr, nullptr, s));
+    *used = 1;
+    return BW_OK;
+}
+
+// Whether fwht_array / fwht_inplace try the compact plan on this signal
+// without being asked (BW_COMPACT, see compact_mode): in auto mode only the
+// sizes whose every pass runs on the int32 engine, where the plan measured
+// 21.5 vs 31.4 ms (n = 32), 10.5 vs 15.6 (n = 31), 5.2 vs 7.8 (n = 30).
+constexpr int kCompactAutoMin = 30;
+bool compact_default(int log2n, const void* data) {
+    const int mode = compact_mode();
+    if (mode == 0 || (reinterpret_cast<uintptr_t>(data) & 15u)) return false;
+    CompactPlan cp;
+    if (log2n < 22 || !compact_plan(log2n, &cp)) return false;
+    return mode == 1 || (cp.v2 && cp.first32 && log2n >= kCompactAutoMin);
+}
 }  // namespace
 extern "C" {
+
+// Whether bw_fwht_i64 / bw_fwht_inplace_i64 try the compact plan on a
+// 16-byte aligned signal of this size (BW_COMPACT and the measured range).
+int bw_compact_auto(int log2n) { return log2n >= 0 && log2n <= BW_MAX_LOG2N && compact_default(log2n, nullptr) ? 1 : 0; }
 
 long long bw_compact_limit(int log2n) {
     CompactPlan cp;
@@ -1831,6 +1936,24 @@ int bw_compact_npasses(int log2n) {
     CompactPlan cp;
     if (log2n < 0 || log2n > BW_MAX_LOG2N || !compact_plan(log2n, &cp)) return 0;
     return cp.m + 1;
+}
+
+// Description of the compact plan's pass i (instrumentation): *k, *r = its
+// first stage bit and stage count (the low pass last: k = 0, r = w);
+// *engine = 32 when the pass runs on the int32 engine (bw_kernels32.cuh), 64
+// on the int64 engine's mapped passes; *bytes_per_point = its algorithmic
+// bytes (read + write).
+int bw_compact_pass_info(int log2n, int pass_index, int* k, int* r, int* engine, int* bytes_per_point) {
+    CompactPlan cp;
+    if (log2n < 0 || log2n > BW_MAX_LOG2N || !compact_plan(log2n, &cp))
+        return fail(BW_BAD_ARGUMENTS, "no compact plan for n = %d", log2n);
+    if (pass_index < 0 || pass_index > cp.m) return fail(BW_BAD_ARGUMENTS, "bad compact pass %d", pass_index);
+    const Pass& p = cp.pass[pass_index];
+    if (k) *k = p.k;
+    if (r) *r = p.r;
+    if (engine) *engine = cp.v2 && (pass_index > 0 || cp.first32) ? 32 : 64;
+    if (bytes_per_point) *bytes_per_point = (pass_index == 0 || pass_index == cp.m) ? 12 : 8;
+    return BW_OK;
 }
 
 // One pass of the compact plan, asynchronous (benchmark instrumentation):
@@ -1874,19 +1997,10 @@ int bw_fwht_i64_compact(int64_t* data, int log2n, long long max_abs, void* strea
         if (used_compact) *used_compact = 1;
         return BW_OK;
     }
-    unsigned *tileflag = nullptr, *abort = nullptr;
-    BW_TRY(compact_scratch(dev, cp, &tileflag, &abort, s));
-    BW_TRY(launch_compact(cp, 0, data, COMPACT_CHECK, tileflag, abort, s));
-    unsigned bad = 0;
-    BW_CUDA(cudaMemcpyAsync(&bad, abort, sizeof bad, cudaMemcpyDeviceToHost, s));
-    BW_CUDA(cudaStreamSynchronize(s));
-    if (bad) {
-        BW_TRY(launch_compact(cp, 0, data, COMPACT_RESTORE, tileflag, abort, s));
-        return fwht_impl(data, log2n, nullptr, false, s);
-    }
-    for (int i = 1; i <= cp.m; ++i) BW_TRY(launch_compact(cp, i, data, COMPACT_PLAIN, nullptr, nullptr, s));
-    if (used_compact) *used_compact = 1;
-    return BW_OK;
+    int used = 0;
+    BW_TRY(compact_try(data, log2n, s, &used));
+    if (used_compact) *used_compact = used;
+    return used ? BW_OK : fwht_impl(data, log2n, nullptr, false, s);
 }
 
 // Test hook: restore after a checked pass 0 (the fallback's first step),
@@ -1986,7 +2100,7 @@ int w32_visit_pass(const CompactPlan& cp, int q, F&& f) {
     const Layout lam = compact_layout(cp);
     const int n = cp.n;
     const uint64_t tiles = 1ull << (n - w::kBits);
-    const uint64_t so = (uint64_t)cp.half[q - 1] << cp.w;
+    const uint64_t so = q > 0 ? (uint64_t)cp.half[q - 1] << cp.w : 0;
     std::string why;
     if (q == cp.m) {
         using C = w::CfgLowW;
@@ -2026,7 +2140,12 @@ int w32_visit_pass(const CompactPlan& cp, int q, F&& f) {
                 for (int j = 0; j < w::kE; ++j) {
                     const uint32_t ei = w::thread_part<C, 0>(lane, warp) | w::reg_part<C, 0>(j);
                     const uint64_t si = base + w::high_off<L>(ei, kk);
-                    f(0, t, ei, (so + si) * 4, 4, compact_index_of(lam, n, si));
+                    if (q == 0) {  // k32_first: the natural int64 element (k32_restore stores the same addresses)
+                        const uint64_t gi = w::first_base(base) + w::first_off<L>(ei, p.k);
+                        if (gi != compact_index_of(lam, n, si)) return fail(BW_BAD_ARGUMENTS, "first pass: natural / compact tile maps differ");
+                        f(0, t, ei, gi * 8, 8, gi);
+                    } else
+                        f(0, t, ei, (so + si) * 4, 4, compact_index_of(lam, n, si));
                     const uint32_t eo = w::thread_part<C, 1>(lane, warp) | w::reg_part<C, 1>(j);
                     const uint64_t sd = base + w::high_off<L>(eo, kk);
                     f(1, t, eo, (dof + sd) * 4, 4, compact_index_of(lam, n, sd));
@@ -2052,7 +2171,7 @@ int w32_emulate(int64_t* host, const CompactPlan& cp) {
     const Layout lam = compact_layout(cp);
     std::vector<uint32_t> buf(2 * N);
     memcpy(buf.data(), host, 8 * N);
-    {  // pass 0: rows [w, w + r) staged on the int64 values, stored as int32
+    if (!cp.first32) {  // pass 0: rows [w, w + r) staged on the int64 values, stored as int32
         std::vector<u64> x(N);
         memcpy(x.data(), host, 8 * N);
         const Pass& p = cp.pass[0];
@@ -2102,8 +2221,8 @@ int w32_emulate(int64_t* host, const CompactPlan& cp) {
                 v[th * w::kE + j] = sm[C::slot(w::thread_part<C, RD>(th & 31u, th >> 5) | w::reg_part<C, RD>(j))];
     };
     const uint64_t tiles = 1ull << (n - w::kBits);
-    for (int q = 1; q <= cp.m; ++q) {
-        const uint64_t so = (uint64_t)cp.half[q - 1] << cp.w;
+    for (int q = cp.first32 ? 0 : 1; q <= cp.m; ++q) {
+        const uint64_t so = q > 0 ? (uint64_t)cp.half[q - 1] << cp.w : 0;
         if (q == cp.m) {
             using C = w::CfgLowW;
             for (uint64_t b = 0; b < tiles; ++b) {
@@ -2147,9 +2266,12 @@ int w32_emulate(int64_t* host, const CompactPlan& cp) {
             for (uint64_t t = 0; t < tiles; ++t) {
                 const uint64_t base = w::high_tile_base<L>(t, kk);
                 for (uint32_t th = 0; th < (uint32_t)w::kNT; ++th)
-                    for (int j = 0; j < w::kE; ++j)
-                        v[th * w::kE + j] =
-                            buf[so + base + w::high_off<L>(w::thread_part<C, 0>(th & 31u, th >> 5) | w::reg_part<C, 0>(j), kk)];
+                    for (int j = 0; j < w::kE; ++j) {
+                        const uint32_t e = w::thread_part<C, 0>(th & 31u, th >> 5) | w::reg_part<C, 0>(j);
+                        // k32_first keeps the low word of the natural int64 element (little endian)
+                        v[th * w::kE + j] = q == 0 ? buf[2 * (w::first_base(base) + w::first_off<L>(e, p.k))]
+                                                   : buf[so + base + w::high_off<L>(e, kk)];
+                    }
                 stages32(tag<C>{}, ic<0>{});
                 to_smem(tag<C>{}, ic<0>{});
                 from_smem(tag<C>{}, ic<1>{});
@@ -2206,7 +2328,7 @@ int bw_plan_check_compact(int log2n) {
     };
     for (int q = 0; q <= cp.m; ++q) {
         int ok;
-        if (cp.v2 && q > 0) {  // the int32 engine's exact address functions
+        if (cp.v2 && (q > 0 || cp.first32)) {  // the int32 engine's exact address functions
             std::fill(reader.begin(), reader.end(), -1);
             std::fill(writer.begin(), writer.end(), -1);
             const Pass& p = cp.pass[q];

@@ -220,6 +220,44 @@ __device__ __forceinline__ u32 ld1(const u32* p) {
     return t;
 }
 
+// rounds 0 and 1 of a high pass on registers v (loaded in round 0's layout),
+// ending with the int32 stores into the compact layout
+// CHECK (k32_first's input test): the barrier between the rounds also
+// carries the tile's verdict -- no global store precedes it -- so a tile with
+// a bad input, or one that saw the abort word, stops there having written
+// nothing; the others flag themselves and store.
+template <int L, bool CHECK = false>
+__device__ __forceinline__ void high_rounds_store(u32 (&v)[kE], u32* sm32, u32* dst, uint64_t base, int kk, uint32_t lane,
+                                                  uint32_t warp, bool bad = false, unsigned* tileflag = nullptr,
+                                                  unsigned* abort = nullptr) {
+    using C = CfgHighW<L>;
+    stages32<C, 0>(v);
+    BW_STRESS(60);
+    smem_store32<C, 0>(v, sm32, thread_part<C, 0>(lane, warp));
+    BW_STRESS(61);
+    if constexpr (CHECK) {
+        if (__syncthreads_or(bad)) {
+            if (threadIdx.x == 0) atomicExch(abort, 1u);
+            return;
+        }
+        if (threadIdx.x == 0) tileflag[blockIdx.x] = 1u;
+    } else {
+        __syncthreads();
+    }
+    const uint32_t tp = thread_part<C, 1>(lane, warp);
+    smem_load32<C, 1>(v, sm32, tp);
+    stages32<C, 1>(v);
+    u32* p = dst + base + high_off<L>(tp, kk);
+    constexpr int V = vec<C, 1>();
+#pragma unroll
+    for (int j = 0; j < kE; j += V) {
+        u32* q = p + high_off<L>(reg_part<C, 1>(j), kk);
+        if constexpr (V == 4) *reinterpret_cast<uint4*>(q) = make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        else if constexpr (V == 2) *reinterpret_cast<uint2*>(q) = make_uint2(v[j], v[j + 1]);
+        else *q = v[j];
+    }
+}
+
 // int32 -> int32 high pass over rows [k, k + 14 - L) of the compact layout.
 // src / dst: the int32 view of the signal, offset by the read / write half.
 template <int L>
@@ -252,25 +290,122 @@ __global__ void __launch_bounds__(kNT, 2) k32_high(const u32* __restrict__ src, 
             }
         }
     }
+    high_rounds_store<L>(v, sm32, dst, base, kk, lane, warp);
+}
+
+// ---------------------------------------------------------------------------
+// The plan's FIRST pass on this engine: natural int64 -> int32 compact, the
+// same tile, rounds and stores as k32_high<L> (k = 14: rows 14 .. 14 + r).
+// The tile's columns are index bits {0,1,2,3,13} (L = 6: and 4), so every
+// int32 slot it writes lies inside the int64 bytes it read itself (in place;
+// bw_plan_check_compact runs these exact address functions).
+//
+// Loads: 16-byte int64 pairs, narrowed as they arrive, in four groups of 16
+// values so that at most half of the 128 registers hold raw int64 data.
+// FIRST_CHECK: every input is tested against |x| <= lim (the high word is the
+// sign extension of the low word, and |low| <= lim).  A tile that finds the
+// abort word set, or a bad input, stores nothing (the verdict rides on the
+// barrier between the two rounds); else it sets tileflag[tile] and stores.
+// So after the pass every tile either holds its int32 output or its
+// untouched int64 input, and the flags say which (k32_restore).
+// ---------------------------------------------------------------------------
+enum { FIRST_PLAIN = 0, FIRST_CHECK = 1 };
+
+// natural int64 offset of tile index e (rows at index bits k ..)
+template <int L>
+BW_HD inline uint64_t first_off(uint32_t e, int k) {
+    return (uint64_t)(e & 15u) | ((uint64_t)((e >> 4) & 1u) << 13) |
+           ((uint64_t)((e >> 5) & ((1u << (L - 5)) - 1u)) << 4) | ((uint64_t)(e >> L) << k);
+}
+// natural index of a tile's element 0 from its compact slot base: slot bits
+// 5..13 are index bits 4..12, slot bits >= 15 index bits >= 14
+BW_HD inline uint64_t first_base(uint64_t slot_base) {
+    return (((slot_base >> 5) & 0x1FFull) << 4) | ((slot_base >> 15) << 14);
+}
+
+__device__ __forceinline__ ulonglong2 ld2x64(const unsigned long long* p) {
+    ulonglong2 t;
+    asm volatile("ld.global.L2::256B.v2.u64 {%0, %1}, [%2];" : "=l"(t.x), "=l"(t.y) : "l"(p));
+    return t;
+}
+
+template <int L, int MODE>
+__global__ void __launch_bounds__(kNT, 2)
+    k32_first(const unsigned long long* __restrict__ src, u32* __restrict__ dst, int k, u32 lim, unsigned* tileflag,
+              unsigned* abort) {
+    using C = CfgHighW<L>;
+    static_assert(vec<C, 0>() == 2, "int64 pairs in round 0");
+    extern __shared__ __align__(16) u32 sm32[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const int kk = k + 1;
+    const uint64_t base = high_tile_base<L>(blockIdx.x, kk);
+    u32 v[kE];
+    u32 acc_hi = 0, acc_lo = 0;
+    if constexpr (MODE == FIRST_CHECK)  // another tile failed: this one stores nothing either (in flight with the loads)
+        acc_hi = *reinterpret_cast<volatile unsigned*>(abort);
+    {
+        const unsigned long long* p = src + first_base(base) + first_off<L>(thread_part<C, 0>(lane, warp), k);
+#pragma unroll
+        for (int g = 0; g < kE; g += 16) {
+            ulonglong2 t[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) t[q] = ld2x64(p + first_off<L>(reg_part<C, 0>(g + 2 * q), k));
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                v[g + 2 * q] = (u32)t[q].x;
+                v[g + 2 * q + 1] = (u32)t[q].y;
+                if constexpr (MODE == FIRST_CHECK) {
+                    const int a = (int)(u32)t[q].x, b = (int)(u32)t[q].y;
+                    acc_hi |= ((u32)(t[q].x >> 32) ^ (u32)(a >> 31)) | ((u32)(t[q].y >> 32) ^ (u32)(b >> 31));
+                    acc_lo |= (u32)__builtin_abs(a) | (u32)__builtin_abs(b);  // abs(INT_MIN) = 2^31 as unsigned: rejected
+                }
+            }
+        }
+    }
+    BW_STRESS(67);
+    high_rounds_store<L, MODE == FIRST_CHECK>(v, sm32, dst, base, kk, lane, warp, acc_hi != 0u || acc_lo > lim, tileflag,
+                                              abort);
+}
+
+// Undo k32_first on the tiles it wrote (tileflag set): the int32 copy, the
+// same r stages again (H H = 2^r I), >> r, stored as natural int64 over the
+// bytes the tile read in the first place.
+template <int L>
+__global__ void __launch_bounds__(kNT, 2)
+    k32_restore(const u32* __restrict__ src, unsigned long long* __restrict__ dst, int k, const unsigned* tileflag) {
+    using C = CfgHighW<L>;
+    static_assert(vec<C, 0>() == 2 && vec<C, 1>() == 4, "int32 pairs in, int64 pairs out");
+    extern __shared__ __align__(16) u32 sm32[];
+    if (*reinterpret_cast<const volatile unsigned*>(tileflag + blockIdx.x) == 0u) return;  // uniform per CTA
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const int kk = k + 1;
+    const uint64_t base = high_tile_base<L>(blockIdx.x, kk);
+    u32 v[kE];
+    {
+        const u32* p = src + base + high_off<L>(thread_part<C, 0>(lane, warp), kk);
+#pragma unroll
+        for (int j = 0; j < kE; j += 2) {
+            const uint2 t = ld2(p + high_off<L>(reg_part<C, 0>(j), kk));
+            v[j] = t.x;
+            v[j + 1] = t.y;
+        }
+    }
     stages32<C, 0>(v);
-    BW_STRESS(60);
     smem_store32<C, 0>(v, sm32, thread_part<C, 0>(lane, warp));
-    BW_STRESS(61);
-    __syncthreads();
+    __syncthreads();  // every load of the tile precedes every store over it
     const uint32_t tp = thread_part<C, 1>(lane, warp);
     smem_load32<C, 1>(v, sm32, tp);
     stages32<C, 1>(v);
-    u32* p = dst + base + high_off<L>(tp, kk);
-    constexpr int V = vec<C, 1>();
+    constexpr int r = kBits - L;
+    unsigned long long* p = dst + first_base(base) + first_off<L>(tp, k);
 #pragma unroll
-    for (int j = 0; j < kE; j += V) {
-        u32* q = p + high_off<L>(reg_part<C, 1>(j), kk);
-        if constexpr (V == 4) *reinterpret_cast<uint4*>(q) = make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        else if constexpr (V == 2) *reinterpret_cast<uint2*>(q) = make_uint2(v[j], v[j + 1]);
-        else *q = v[j];
+    for (int j = 0; j < kE; j += 2) {
+        ulonglong2 t;
+        t.x = (unsigned long long)(long long)((int)v[j] >> r);
+        t.y = (unsigned long long)(long long)((int)v[j + 1] >> r);
+        *reinterpret_cast<ulonglong2*>(p + first_off<L>(reg_part<C, 1>(j), k)) = t;
     }
 }
-
 // int32 -> int64 low pass over stages 0..13 of every block.  src: the int32
 // view offset by the read half (block b's copy at src + (b << 15)); dst: the
 // int64 signal (block b at dst + (b << 14)).

@@ -382,14 +382,19 @@ def test_host_batch_validation_host_side():
         _lib.check(L.bw_fwht_xfused_pass_extract_i64(None, 1, 20, 5, 0, 10, 0, None, None, 16, None, None))
 
 
-@pytest.mark.parametrize("v2", ["0", "1"])
-@pytest.mark.parametrize("n", [16, 19, 22, 24])
+@pytest.mark.parametrize("v2", ["0", "1", "first0"])
+@pytest.mark.parametrize("n", [16, 19, 22, 23, 24])
 def test_compact_plan_checks(monkeypatch, n, v2):
     """The compact in-place plan's exact address tables (bw_plan_check_compact):
     natural int64 in and out, every pass loads where the previous one
     stored, no tile stores over bytes another tile of the same pass loads,
     every bit staged once; for the int32-engine passes (v2) also every
-    round's coverage, vector alignment and shared-memory bank conflicts."""
+    round's coverage, vector alignment and shared-memory bank conflicts.
+    n = 22 / 23: the first pass (8 / 9 rows) is the int32 engine's k32_first
+    ("first0": BW_COMPACT_FIRST=0 keeps it on the int64 engine)."""
+    if v2 == "first0":
+        monkeypatch.setenv("BW_COMPACT_FIRST", "0")
+        v2 = "1"
     monkeypatch.setenv("BW_COMPACT_V2", v2)
     L = _lib.lib()
     assert L.bw_plan_check_compact(n) == 0, _lib.last_error()
@@ -399,7 +404,7 @@ def test_compact_plan_checks(monkeypatch, n, v2):
     assert L.bw_compact_limit(n) == (2**31 - 1) >> (n - 4 if v2 == "1" else n - 13)
 
 
-@pytest.mark.parametrize("n,r2", [(16, "9"), (20, "9"), (24, "9"), (24, "8")])
+@pytest.mark.parametrize("n,r2", [(16, "9"), (20, "9"), (22, "9"), (23, "9"), (24, "9"), (24, "8")])
 def test_compact_v2_host_emulation_matches_oracle(monkeypatch, coracle, n, r2):
     """The int32-engine passes' exact tables (rounds, swizzled shared-memory
     slots, int32 / int64 arithmetic) run on the host (bw_debug_emulate_compact)

@@ -131,3 +131,32 @@ def test_narrow_intermediates_bench_leg():
                    "--intermediates", "narrow"])
     assert d["config"]["narrow_fallbacks"] == 0 and d["config"]["algorithmic_bytes_per_point"] == [10, 6, 12]
     assert d["roofline"]["kernel"].startswith("narrow pass") and "flag_readback_ms" in d
+
+
+@pytest.mark.gpu
+def test_compact_intermediates_bench_leg():
+    """--intermediates compact at a small size: the first pass checked inside
+    the step, no fallback on the +-1 config input, 12 / 8 / 12 bytes per point,
+    and the in-run parity of the measured step."""
+    d = run_bench(["--steps", "3", "--warmup", "3", "--log2n", "24", "--no-e2e", "--intermediates", "compact"])
+    assert d["config"]["compact_fallbacks"] == 0 and d["config"]["algorithmic_bytes_per_point"] == [12, 8, 12]
+    assert d["roofline"]["kernel"].startswith("compact pass") and "flag_readback_ms" in d
+    assert d["gpu_launches"] == 3 * 3
+    assert d["parity"]["equal"] is True
+
+
+@pytest.mark.gpu
+def test_default_bench_runs_the_compact_plan_where_the_library_does():
+    """n = 30: the library's default (bw_compact_auto) is the compact plan on
+    the int32 engine, so the default bench line measures it; config 2's
+    wide inputs at the same size run the int64 plan after the restore."""
+    d = run_bench(["--steps", "3", "--warmup", "3", "--log2n", "30", "--no-e2e", "--no-cpu"])
+    assert d["config"]["compact_fallbacks"] == 0
+    assert [q["bytes_per_point"] for q in d["config"]["passes"]] == [12, 8, 12]
+    assert all(q["kernel"].startswith("k32_") for q in d["config"]["passes"])
+    ep = d["entry_points"]
+    assert ep["fwht_array_ran_compact_plan"] is True
+    assert ep["fwht_array_ms"] < ep["fwht_array_int64_plan_ms"]
+    d = run_bench(["--config", "2", "--steps", "3", "--warmup", "3", "--log2n", "30", "--no-e2e", "--no-cpu",
+                   "--no-entry-points"])
+    assert d["config"]["compact_fallbacks"] == 6

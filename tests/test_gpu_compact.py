@@ -114,13 +114,14 @@ def test_compact_v1_still_selectable(coracle, monkeypatch):
     assert np.array_equal(y, c_fwht(coracle, x))
 
 
+@pytest.mark.parametrize("n", [22, 23, 24])
 @pytest.mark.parametrize("where", ["first", "last", "middle", "everywhere"])
-def test_compact_fallback_restores_exactly(coracle, where):
+def test_compact_fallback_restores_exactly(coracle, where, n):
     """One input over lim(n): the checked first pass leaves that tile (and
     every tile after the abort) untouched, the written tiles are restored by
     their own stages + an exact shift, and the int64 plan gives the
-    reference's result."""
-    n = 24
+    reference's result.  n = 22 / 23: the first pass on the int32 engine
+    (k32_first<6> / <5> and k32_restore); n = 24: the int64 engine's."""
     lim = _lib.lib().bw_compact_limit(n)
     rng = np.random.default_rng(5)
     x = rng.integers(-lim, lim + 1, size=1 << n, dtype=np.int64)
@@ -135,6 +136,58 @@ def test_compact_fallback_restores_exactly(coracle, where):
     y, used = compact(x)
     assert used == 0
     assert np.array_equal(y, c_fwht(coracle, x))
+
+
+@pytest.mark.parametrize("n", [22, 23])
+@pytest.mark.parametrize("bad", [2**31, -(2**31), 2**32, 2**32 + 1, -(2**32), -(2**32) + 1, 2**62, -(2**63), "lim+1", "-lim-1"])
+def test_compact_first_pass_input_test_edges(coracle, n, bad):
+    """k32_first's input test keeps the low word and must refuse every value
+    whose high word is not its sign extension, and |low| > lim -- values
+    whose low word alone looks small included."""
+    lim = _lib.lib().bw_compact_limit(n)
+    if bad == "lim+1":
+        bad = lim + 1
+    elif bad == "-lim-1":
+        bad = -lim - 1
+    x = oracle_np.gen(1, 40 + n, [], 0, 1 << n)
+    x[(1 << n) - 77] = bad
+    y, used = compact(x)
+    assert used == 0
+    assert np.array_equal(y, c_fwht(coracle, x))
+
+
+@pytest.mark.parametrize("n", [22, 23])
+def test_compact_first_pass_flags_say_which_tiles_were_written(n):
+    """A violation in the LAST tile: the checked first pass aborts there; every
+    tile is either written and flagged or untouched, and the restore gives the
+    input back bit for bit."""
+    L = _lib.lib()
+    lim = L.bw_compact_limit(n)
+    x = oracle_np.gen(1, 60 + n, [], 0, 1 << n)
+    x[-1] = lim + 1
+    t = torch.from_numpy(x.copy()).cuda()
+    flags = torch.zeros(1 << (n - 13), dtype=torch.int32, device="cuda")
+    abort = torch.zeros(1, dtype=torch.int32, device="cuda")
+    sh = torch.cuda.current_stream().cuda_stream
+    _lib.check(L.bw_fwht_i64_compact_pass(t.data_ptr(), n, 0, 1, flags.data_ptr(), abort.data_ptr(), sh))
+    assert abort.item() == 1
+    assert 0 <= int(flags.sum().item()) < 1 << (n - 14)
+    _lib.check(L.bw_fwht_i64_compact_restore(t.data_ptr(), n, flags.data_ptr(), sh))
+    assert np.array_equal(t.cpu().numpy(), x)
+
+
+def test_compact_first_pass_engines_agree(coracle, monkeypatch):
+    """BW_COMPACT_FIRST=0 runs the first pass on the int64 engine
+    (k_pass_map) as before: same result."""
+    n = 23
+    x = oracle_np.gen(1, 5, [], 0, 1 << n)
+    want = c_fwht(coracle, x)
+    for first in ("1", "0"):
+        monkeypatch.setenv("BW_COMPACT_FIRST", first)
+        for bound in (-1, 1):
+            y, used = compact(x, bound)
+            assert used == 1
+            assert np.array_equal(y, want)
 
 
 def test_compact_restore_is_identity():
