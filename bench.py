@@ -343,7 +343,9 @@ def run_ours(a):
     # bw_fwht_i64 / fwht_array run by default at these sizes, pass by pass --
     # the checked first pass (natural int64 -> int32 inside the buffer), the
     # verdict readback, the int32 -> int32 pass(es), the widening low pass.
-    ncp = L.bw_compact_npasses(nl) if (p == 0 and spec.threshold is None and not whole) else 0
+    ncp = L.bw_compact_npasses(nl) if (p == 0 and not whole) else 0
+    if spec.threshold is not None and not L.bw_compact_auto(nl):  # the fused extraction needs the int32 engine's low pass
+        ncp = 0
     compact_local = (not narrow_local and ncp > 0 and
                      (a.intermediates == "compact" or (a.intermediates == "auto" and L.bw_compact_auto(nl) == 1)))
     n_fallback = 0
@@ -461,6 +463,8 @@ def run_ours(a):
             ev[0].record(stream)
             cflags.zero_()
             cabort.zero_()
+            if extract:
+                hit_cnt.zero_()
             _lib.check(L.bw_fwht_i64_compact_pass(ptr, nl, 0, 1, cflags.data_ptr(), cabort.data_ptr(), sh))
             ev[1].record(stream)
             bad = int(cabort.item())
@@ -468,12 +472,25 @@ def run_ours(a):
             if bad:  # a value over lim(n): the written tiles restored, then the int64 plan
                 n_fallback += 1
                 _lib.check(L.bw_fwht_i64_compact_restore(ptr, nl, cflags.data_ptr(), sh))
-                _lib.check(L.bw_fwht_i64_int64plan(ptr, nl, sh, None))
+                if extract:
+                    n64 = L.bw_plan_npasses(nl)
+                    for i in range(n64 - 1):
+                        _lib.check(L.bw_fwht_i64_pass(ptr, nl, i, sh))
+                    _lib.check(L.bw_fwht_i64_pass_extract(ptr, nl, n64 - 1, tau, 0, hit_idx.data_ptr(),
+                                                          hit_val.data_ptr(), cap, hit_cnt.data_ptr(), sh))
+                    _lib.check(L.bw_sort_hits_i64(hit_idx.data_ptr(), hit_val.data_ptr(), hit_cnt.data_ptr(), sh))
+                else:
+                    _lib.check(L.bw_fwht_i64_int64plan(ptr, nl, sh, None))
                 for i in range(3, 2 * nn + 1):
                     ev[i].record(stream)
                 return
             for i in range(1, nn):
-                _lib.check(L.bw_fwht_i64_compact_pass(ptr, nl, i, 0, None, None, sh))
+                if extract and i == nn - 1:  # |W| > tau tested on the low pass's final values, then the hits sorted
+                    _lib.check(L.bw_fwht_i64_compact_pass_extract(ptr, nl, tau, 0, hit_idx.data_ptr(), hit_val.data_ptr(),
+                                                                  cap, hit_cnt.data_ptr(), sh))
+                    _lib.check(L.bw_sort_hits_i64(hit_idx.data_ptr(), hit_val.data_ptr(), hit_cnt.data_ptr(), sh))
+                else:
+                    _lib.check(L.bw_fwht_i64_compact_pass(ptr, nl, i, 0, None, None, sh))
                 ev[2 * i + 1].record(stream)
                 if i + 1 < nn:
                     ev[2 * i + 2].record(stream)
@@ -827,7 +844,8 @@ def run_ours(a):
         names = ["k32_first (natural int64 -> int32 in place, every input tested)" if cinfo[0]["engine"] == 32
                  else "k_pass_map (int64 -> int32, every input tested)"]
         names += ["k32_high (int32 -> int32)" if c["engine"] == 32 else "k_pass_map (int32 -> int32)" for c in cinfo[1:-1]]
-        names += ["k32_low (int32 -> natural int64, last four stages in int64)" if cinfo[-1]["engine"] == 32
+        names += [("k32_low (int32 -> natural int64, last four stages in int64"
+                   + (", |W| > tau fused in)" if extract else ")")) if cinfo[-1]["engine"] == 32
                   else "k_pass_map (int32 -> int64)"]
         line["config"]["intermediates"] = ("compact in place: int32 copies inside the signal's own buffer between "
                                            "the passes, high stages first, first pass checked (|x| <= "

@@ -212,6 +212,12 @@ int bw_compact_pass_info(int log2n, int pass_index, int *k, int *r, int *engine,
  * tileflag_dev (2^(n-13) words, zeroed) and *abort_dev (zeroed) record the outcome. */
 int bw_fwht_i64_compact_pass(int64_t *data, int log2n, int pass_index, int checked, uint32_t *tileflag_dev,
                              uint32_t *abort_dev, void *stream);
+/* The compact plan's last pass (the widening low pass) with the threshold extraction of
+ * extract_above (noisy.py:185-222, |W| >= tau) fused in, as bw_fwht_i64_pass_extract does for
+ * the int64 plan; asynchronous; int32-engine plans only (n <= 32).  bw_fwht_extract_i64 runs
+ * this by itself on signals the compact plan admits. */
+int bw_fwht_i64_compact_pass_extract(int64_t *data, int log2n, uint64_t tau, uint64_t base, int64_t *out_idx,
+                                     int64_t *out_val, uint64_t cap, uint64_t *count_dev, void *stream);
 /* Test hook: the exact restore of the tiles a checked pass 0 wrote. */
 int bw_fwht_i64_compact_restore(int64_t *data, int log2n, uint32_t *tileflag_dev, void *stream);
 /* Test hook: static check of the compact plan (in place, layouts, coverage;

@@ -60,6 +60,7 @@ _SIGNATURES = {
     "bw_compact_auto": ([I32], I32),
     "bw_fwht_i64_int64plan": ([P, I32, P, PU64], I32),
     "bw_compact_pass_info": ([I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32)], I32),
+    "bw_fwht_i64_compact_pass_extract": ([P, I32, U64, U64, P, P, U64, P, P], I32),
     "bw_compact_limit": ([I32], ctypes.c_longlong),
     "bw_compact_npasses": ([I32], I32),
     "bw_fwht_i64_compact_pass": ([P, I32, I32, I32, P, P, P], I32),

@@ -93,7 +93,8 @@ int compact_mode() {
     return e[0] == '1' ? 1 : 0;
 }
 bool compact_default(int log2n, const void* data);                       // after compact_plan
-int compact_try(int64_t* data, int log2n, cudaStream_t s, int* used);  // after launch_compact
+int compact_try(int64_t* data, int log2n, cudaStream_t s, int* used,
+                const bw::ExtractArgs* ex = nullptr);  // after launch_compact
 // BW_FOLD_BLOCKS=0 keeps the shared-bin / L2-atomic fold for d_out > 12 (A/B knob, read per call).
 bool fold_blocks_enabled() { return !(getenv("BW_FOLD_BLOCKS") && getenv("BW_FOLD_BLOCKS")[0] == '0'); }
 // BW_F64_VEC_LOW=0 keeps the float64 low pass on 8-byte accesses (A/B knob).
@@ -616,7 +617,8 @@ int set_all_pass_attributes() {
     // the int32 engine of the compact plan (64 KiB of shared memory, 2 CTAs/SM)
     BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_high<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
     BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_high<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
-    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_low, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
+    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_low<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
+    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_low<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
     BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_first<5, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
     BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_first<5, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
     BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_first<6, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
@@ -1767,8 +1769,9 @@ enum CompactMode { COMPACT_PLAIN, COMPACT_CHECK, COMPACT_RESTORE };
 
 // Pass i of the compact plan (i < m: high pass i; i == m: the low pass).
 // mode CHECK / RESTORE apply to pass 0 only.
+// ex (the low pass on the int32 engine only): the fused threshold extraction.
 int launch_compact(const CompactPlan& cp, int i, int64_t* data, CompactMode mode, unsigned* tileflag,
-                   unsigned* abort, cudaStream_t s) {
+                   unsigned* abort, cudaStream_t s, const bw::ExtractArgs* ex = nullptr) {
     const Layout nat = natural_layout(cp.n), lam = compact_layout(cp);
     int* d32 = reinterpret_cast<int*>(data);
     long long* d64 = reinterpret_cast<long long*>(data);
@@ -1803,15 +1806,19 @@ int launch_compact(const CompactPlan& cp, int i, int64_t* data, CompactMode mode
         }
         const uint32_t* src = reinterpret_cast<const uint32_t*>(d32 + ((size_t)cp.half[i - 1] << cp.w));
         if (i == cp.m) {
-            BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_low, src, reinterpret_cast<unsigned long long*>(data)));
+            unsigned long long* d64u = reinterpret_cast<unsigned long long*>(data);
+            if (ex) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_low<true>, src, d64u, *ex));
+            else BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_low<false>, src, d64u, bw::ExtractArgs{}));
             return BW_OK;
         }
+        if (ex) return fail(BW_BAD_ARGUMENTS, "only the compact plan's low pass carries the extraction");
         uint32_t* dst = reinterpret_cast<uint32_t*>(d32 + ((size_t)cp.half[i] << cp.w));
         if (p.r == 9) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_high<5>, src, dst, p.k));
         else if (p.r == 8) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_high<6>, src, dst, p.k));
         else return fail(BW_BAD_ARGUMENTS, "no int32-engine pass of %d rows", p.r);
         return BW_OK;
     }
+    if (ex) return fail(BW_BAD_ARGUMENTS, "the fused extraction needs the int32 engine's low pass");
     return visit_compact(p, [&](auto t, auto l) -> int {
         using C = typename decltype(t)::type;
         constexpr int L = decltype(l)::value;
@@ -1889,10 +1896,11 @@ int compact_scratch(int dev, const CompactPlan& cp, unsigned** tileflag, unsigne
 // every input (one stream synchronisation to read the verdict).  *used = 1:
 // the transform is done (asynchronously).  *used = 0: an input was too large
 // (or there is no plan): the buffer holds the caller's input again.
-int compact_try(int64_t* data, int log2n, cudaStream_t s, int* used) {
+// ex: the threshold extraction fused into the low pass (v2 plans only).
+int compact_try(int64_t* data, int log2n, cudaStream_t s, int* used, const bw::ExtractArgs* ex) {
     *used = 0;
     CompactPlan cp;
-    if ((reinterpret_cast<uintptr_t>(data) & 15u) || !compact_plan(log2n, &cp)) return BW_OK;
+    if ((reinterpret_cast<uintptr_t>(data) & 15u) || !compact_plan(log2n, &cp) || (ex && !cp.v2)) return BW_OK;
     int dev = 0;
     BW_TRY(device_setup(&dev));
     unsigned *tileflag = nullptr, *abort = nullptr;
@@ -1902,22 +1910,27 @@ int compact_try(int64_t* data, int log2n, cudaStream_t s, int* used) {
     BW_CUDA(cudaMemcpyAsync(&bad, abort, sizeof bad, cudaMemcpyDeviceToHost, s));
     BW_CUDA(cudaStreamSynchronize(s));
     if (bad) return launch_compact(cp, 0, data, COMPACT_RESTORE, tileflag, abort, s);
-    for (int i = 1; i <= cp.m; ++i) BW_TRY(launch_compact(cp, i, data, COMPACT_PLAIN, nullptr, nullptr, s));
+    for (int i = 1; i <= cp.m; ++i)
+        BW_TRY(launch_compact(cp, i, data, COMPACT_PLAIN, nullptr, nullptr, s, i == cp.m ? ex : nullptr));
     *used = 1;
     return BW_OK;
 }
 
 // Whether fwht_array / fwht_inplace try the compact plan on this signal
-// without being asked (BW_COMPACT, see compact_mode): in auto mode only the
-// sizes whose every pass runs on the int32 engine, where the plan measured
-// 21.5 vs 31.4 ms (n = 32), 10.5 vs 15.6 (n = 31), 5.2 vs 7.8 (n = 30).
-constexpr int kCompactAutoMin = 30;
+// without being asked (BW_COMPACT, see compact_mode): in auto mode the sizes
+// where the checked plan, its verdict readback included, measured faster
+// than the int64 plan on +-1 signals (profiles/r02_compact/passes.log):
+// n = 32: 23.7 vs 31.4 ms, 31: 11.3 vs 15.5, 30: 5.57 vs 7.72, 29: 3.22 vs
+// 3.88, 28: 1.63 vs 1.93, 27: 0.69 vs 0.97, 26: 0.36 vs 0.49 (n = 25: 0.197
+// vs 0.224, n = 24: 0.115 vs 0.107 -- left to the int64 plan, which stays
+// asynchronous).  Above n = 32 there is no int32-engine plan.
+constexpr int kCompactAutoMin = 26;
 bool compact_default(int log2n, const void* data) {
     const int mode = compact_mode();
     if (mode == 0 || (reinterpret_cast<uintptr_t>(data) & 15u)) return false;
     CompactPlan cp;
     if (log2n < 22 || !compact_plan(log2n, &cp)) return false;
-    return mode == 1 || (cp.v2 && cp.first32 && log2n >= kCompactAutoMin);
+    return mode == 1 || (cp.v2 && log2n >= kCompactAutoMin);
 }
 }  // namespace
 extern "C" {
@@ -1973,6 +1986,23 @@ int bw_fwht_i64_compact_pass(int64_t* data, int log2n, int pass_index, int check
     return launch_compact(cp, pass_index, data, checked ? COMPACT_CHECK : COMPACT_PLAIN,
                           reinterpret_cast<unsigned*>(tileflag_dev), reinterpret_cast<unsigned*>(abort_dev),
                           as_stream(stream));
+}
+
+// The compact plan's LAST pass (the widening low pass) with the threshold
+// extraction fused in, asynchronous (instrumentation; the pass-level form of
+// bw_fwht_extract_i64 on small-valued signals).  Needs an int32-engine plan.
+int bw_fwht_i64_compact_pass_extract(int64_t* data, int log2n, uint64_t tau, uint64_t base, int64_t* out_idx,
+                                     int64_t* out_val, uint64_t cap, uint64_t* count_dev, void* stream) {
+    BW_TRY(check_signal(data, log2n));
+    if (!count_dev || (cap > 0 && (!out_idx || !out_val))) return fail(BW_BAD_ARGUMENTS, "null extraction output");
+    CompactPlan cp;
+    if ((reinterpret_cast<uintptr_t>(data) & 15u) || !compact_plan(log2n, &cp) || !cp.v2)
+        return fail(BW_BAD_ARGUMENTS, "no int32-engine compact plan for this signal (n = %d)", log2n);
+    int dev = 0;
+    BW_TRY(device_setup(&dev));
+    bw::ExtractArgs ex = {tau, base, reinterpret_cast<long long*>(out_idx), reinterpret_cast<long long*>(out_val),
+                          reinterpret_cast<unsigned long long*>(count_dev), cap};
+    return launch_compact(cp, cp.m, data, COMPACT_PLAIN, nullptr, nullptr, as_stream(stream), &ex);
 }
 
 // fwht_array with compact in-place intermediates.  max_abs >= 0: the
@@ -3493,15 +3523,22 @@ int bw_fwht_extract_i64(int64_t* data, int log2n, uint64_t tau, uint64_t base, i
         BW_TRY(fwht_impl(data, log2n, nullptr, false, s));
         return bw_extract_ge_i64(data, log2n, tau, base, out_idx, out_val, cap, nullptr, stream, count);
     }
-    void* sc = nullptr;
-    BW_TRY(scratch(dev, 64, &sc));
-    unsigned long long* dcount = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(sc) + 48);
+    // the hit counter lives apart from the compact plan's flag words (scratch() hands out one buffer per device)
+    static thread_local unsigned long long* dcounts[64] = {};
+    if (dev < 0 || dev >= 64) return fail(BW_BAD_ARGUMENTS, "device %d out of range", dev);
+    if (!dcounts[dev]) BW_CUDA(cudaMalloc(&dcounts[dev], 64));
+    unsigned long long* dcount = dcounts[dev];
     BW_CUDA(cudaMemsetAsync(dcount, 0, sizeof(unsigned long long), s));
     bw::ExtractArgs ex = {tau, base, reinterpret_cast<long long*>(out_idx), reinterpret_cast<long long*>(out_val),
                           dcount, cap};
     u64* d = reinterpret_cast<u64*>(data);
-    for (size_t i = 0; i < passes.size(); ++i)
-        BW_TRY(launch_pass(passes[i], d, log2n, s, i + 1 == passes.size() ? &ex : nullptr));
+    // small-valued signals (the noisy +-1 sums of configs 3 / 5 at n <= 32): the compact plan with the
+    // extraction in its low pass; larger values leave the buffer as it was for the int64 plan below
+    int used = 0;
+    if (compact_mode() != 0 && compact_default(log2n, data)) BW_TRY(compact_try(data, log2n, s, &used, &ex));
+    if (!used)
+        for (size_t i = 0; i < passes.size(); ++i)
+            BW_TRY(launch_pass(passes[i], d, log2n, s, i + 1 == passes.size() ? &ex : nullptr));
     unsigned long long total = 0;
     BW_CUDA(cudaMemcpyAsync(&total, dcount, sizeof total, cudaMemcpyDeviceToHost, s));
     BW_CUDA(cudaStreamSynchronize(s));

@@ -226,12 +226,19 @@ __device__ __forceinline__ u32 ld1(const u32* p) {
 // carries the tile's verdict -- no global store precedes it -- so a tile with
 // a bad input, or one that saw the abort word, stops there having written
 // nothing; the others flag themselves and store.
-template <int L, bool CHECK = false>
+// PRE_SYNC (k32_first with half its loads landing in shared memory): one
+// more barrier after round 0's stages, before the transpose overwrites the
+// landing slots other threads may still be reading.
+template <int L, bool CHECK = false, bool PRE_SYNC = false>
 __device__ __forceinline__ void high_rounds_store(u32 (&v)[kE], u32* sm32, u32* dst, uint64_t base, int kk, uint32_t lane,
                                                   uint32_t warp, bool bad = false, unsigned* tileflag = nullptr,
                                                   unsigned* abort = nullptr) {
     using C = CfgHighW<L>;
     stages32<C, 0>(v);
+    if constexpr (PRE_SYNC) {
+        BW_STRESS(68);
+        __syncthreads();
+    }
     BW_STRESS(60);
     smem_store32<C, 0>(v, sm32, thread_part<C, 0>(lane, warp));
     BW_STRESS(61);
@@ -260,8 +267,8 @@ __device__ __forceinline__ void high_rounds_store(u32 (&v)[kE], u32* sm32, u32* 
 
 // int32 -> int32 high pass over rows [k, k + 14 - L) of the compact layout.
 // src / dst: the int32 view of the signal, offset by the read / write half.
-template <int L>
-__global__ void __launch_bounds__(kNT, 2) k32_high(const u32* __restrict__ src, u32* __restrict__ dst, int k) {
+template <int L, int MINB = 2>
+__global__ void __launch_bounds__(kNT, MINB) k32_high(const u32* __restrict__ src, u32* __restrict__ dst, int k) {
     using C = CfgHighW<L>;
     extern __shared__ __align__(16) u32 sm32[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -329,22 +336,96 @@ __device__ __forceinline__ ulonglong2 ld2x64(const unsigned long long* p) {
     return t;
 }
 
-template <int L, int MODE>
+// FIRST_CHECK's evidence against a pair of inputs.  CHK 0: per value, the
+// high word against the low word's sign extension and |low| (4 operations
+// per value on two serial chains).  CHK 1: y = x + lim in 64 bits; |x| <= lim
+// iff y <= 2 lim, i.e. high(y) == 0 and low(y) <= 2 lim (lim < 2^31): OR of
+// the high words, max of the low words, on four independent accumulators.
+struct FirstAcc {
+    u32 hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+};
+template <int MODE, int CHK>
+__device__ __forceinline__ void first_test(const ulonglong2& t, int q, u32 lim, FirstAcc& acc) {
+    if constexpr (MODE == FIRST_CHECK) {
+        if constexpr (CHK == 0) {
+            const int a = (int)(u32)t.x, b = (int)(u32)t.y;
+            acc.hi[0] |= ((u32)(t.x >> 32) ^ (u32)(a >> 31)) | ((u32)(t.y >> 32) ^ (u32)(b >> 31));
+            acc.lo[0] |= (u32)__builtin_abs(a) | (u32)__builtin_abs(b);  // abs(INT_MIN) = 2^31 as unsigned: rejected
+        } else {
+            const unsigned long long y0 = t.x + lim, y1 = t.y + lim;
+            acc.hi[q & 3] |= (u32)(y0 >> 32) | (u32)(y1 >> 32);
+            acc.lo[q & 3] = max(acc.lo[q & 3], max((u32)y0, (u32)y1));
+        }
+    }
+}
+template <int CHK>
+__device__ __forceinline__ bool first_bad(const FirstAcc& acc, u32 lim) {
+    const u32 hi = acc.hi[0] | acc.hi[1] | acc.hi[2] | acc.hi[3];
+    const u32 lo = max(max(acc.lo[0], acc.lo[1]), max(acc.lo[2], acc.lo[3]));
+    return hi != 0u || lo > (CHK == 0 ? lim : 2u * lim);
+}
+
+// VAR (measured variants of the load phase, tools/mb_first32.cu):
+//   0: all 32 pair loads into registers, narrowed in four groups;
+//   1: as 0 with the abort word read before them;
+//   2: registers 32..63 land in the CTA's (still unused) shared memory through
+//      cp.async, registers 0..31 through plain loads: the whole tile is in
+//      flight at once with 64 instead of 128 registers of raw data, so the
+//      checked pass (which needs the high words) no longer splits its loads;
+//   3: as 2 with the biased-add test (CHK 1).
+// n = 32, 12 B/point: plain 8.02 ms in every variant; checked 9.72 (0, 1),
+// 8.71 (2) -- profiles/r02_compact/mb_first32.log.
+constexpr int kFirstVar = 3;
+
+template <int L, int MODE, int VAR = kFirstVar>
 __global__ void __launch_bounds__(kNT, 2)
     k32_first(const unsigned long long* __restrict__ src, u32* __restrict__ dst, int k, u32 lim, unsigned* tileflag,
               unsigned* abort) {
     using C = CfgHighW<L>;
     static_assert(vec<C, 0>() == 2, "int64 pairs in round 0");
+    constexpr int CHK = VAR == 3 ? 1 : 0;
+    constexpr bool LAND = VAR >= 2;
     extern __shared__ __align__(16) u32 sm32[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const int kk = k + 1;
     const uint64_t base = high_tile_base<L>(blockIdx.x, kk);
     u32 v[kE];
-    u32 acc_hi = 0, acc_lo = 0;
-    if constexpr (MODE == FIRST_CHECK)  // another tile failed: this one stores nothing either (in flight with the loads)
-        acc_hi = *reinterpret_cast<volatile unsigned*>(abort);
-    {
-        const unsigned long long* p = src + first_base(base) + first_off<L>(thread_part<C, 0>(lane, warp), k);
+    FirstAcc acc;
+    if constexpr (MODE == FIRST_CHECK) {  // another tile failed: this one stores nothing either (in flight with the loads)
+        if constexpr (VAR == 0) acc.hi[0] = *reinterpret_cast<volatile unsigned*>(abort);
+        else asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(acc.hi[0]) : "l"(abort));
+    }
+    const unsigned long long* p = src + first_base(base) + first_off<L>(thread_part<C, 0>(lane, warp), k);
+    if constexpr (LAND) {
+        const uint32_t land = (uint32_t)__cvta_generic_to_shared(sm32) + threadIdx.x * 16u;
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(land + q * (kNT * 16u)),
+                         "l"(p + first_off<L>(reg_part<C, 0>(32 + 2 * q), k))
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        ulonglong2 t[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) t[q] = ld2x64(p + first_off<L>(reg_part<C, 0>(2 * q), k));
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            v[2 * q] = (u32)t[q].x;
+            v[2 * q + 1] = (u32)t[q].y;
+            first_test<MODE, CHK>(t[q], q, lim, acc);
+        }
+        // this thread's own copies: no CTA barrier needed to read them.  The warp barrier keeps ptxas from
+        // hoisting the wait above the plain loads (which would then start a second round trip)
+        __syncwarp();
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            ulonglong2 u;
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(u.x), "=l"(u.y) : "r"(land + q * (kNT * 16u)));
+            v[32 + 2 * q] = (u32)u.x;
+            v[32 + 2 * q + 1] = (u32)u.y;
+            first_test<MODE, CHK>(u, q, lim, acc);
+        }
+    } else {
 #pragma unroll
         for (int g = 0; g < kE; g += 16) {
             ulonglong2 t[8];
@@ -354,17 +435,13 @@ __global__ void __launch_bounds__(kNT, 2)
             for (int q = 0; q < 8; ++q) {
                 v[g + 2 * q] = (u32)t[q].x;
                 v[g + 2 * q + 1] = (u32)t[q].y;
-                if constexpr (MODE == FIRST_CHECK) {
-                    const int a = (int)(u32)t[q].x, b = (int)(u32)t[q].y;
-                    acc_hi |= ((u32)(t[q].x >> 32) ^ (u32)(a >> 31)) | ((u32)(t[q].y >> 32) ^ (u32)(b >> 31));
-                    acc_lo |= (u32)__builtin_abs(a) | (u32)__builtin_abs(b);  // abs(INT_MIN) = 2^31 as unsigned: rejected
-                }
+                first_test<MODE, CHK>(t[q], q, lim, acc);
             }
         }
     }
     BW_STRESS(67);
-    high_rounds_store<L, MODE == FIRST_CHECK>(v, sm32, dst, base, kk, lane, warp, acc_hi != 0u || acc_lo > lim, tileflag,
-                                              abort);
+    high_rounds_store<L, MODE == FIRST_CHECK, LAND>(v, sm32, dst, base, kk, lane, warp,
+                                                     MODE == FIRST_CHECK && first_bad<CHK>(acc, lim), tileflag, abort);
 }
 
 // Undo k32_first on the tiles it wrote (tileflag set): the int32 copy, the
@@ -409,7 +486,38 @@ __global__ void __launch_bounds__(kNT, 2)
 // int32 -> int64 low pass over stages 0..13 of every block.  src: the int32
 // view offset by the read half (block b's copy at src + (b << 15)); dst: the
 // int64 signal (block b at dst + (b << 14)).
-__global__ void __launch_bounds__(kNT, 2) k32_low(const u32* __restrict__ src, unsigned long long* __restrict__ dst) {
+// EX: the threshold extraction of the last pass (noisy.py:185-222 with
+// |W| >= tau, as k_pass's): each sub-round's final values are tested in
+// registers after their store; a warp holding a hit re-reads its stored
+// values and appends (index, value) to the unordered hit list.
+__device__ __noinline__ void low_extract_slow(const unsigned long long* o, uint64_t gbase, uint32_t tp, ExtractArgs ex) {
+    using C = CfgLowW;
+    const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll 1
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t off = tp | reg_part<C, 2>(j);
+        const u64 x = o[off];
+        const bool h = hit_ge_u(x, ex.tau);
+        const unsigned b = __ballot_sync(0xffffffffu, h);
+        if (b) {
+            const int leader = __ffs(b) - 1;
+            unsigned long long first = 0;
+            if ((int)lane == leader) first = atomicAdd(ex.count, (unsigned long long)__popc(b));
+            first = __shfl_sync(0xffffffffu, first, leader);
+            if (h) {
+                const unsigned long long pos = first + __popc(b & ((1u << lane) - 1u));
+                if (pos < ex.cap) {
+                    ex.idx[pos] = (long long)(ex.base + gbase + off);
+                    ex.val[pos] = (long long)x;
+                }
+            }
+        }
+    }
+}
+
+template <bool EX = false>
+__global__ void __launch_bounds__(kNT, 2)
+    k32_low(const u32* __restrict__ src, unsigned long long* __restrict__ dst, ExtractArgs ex) {
     using C = CfgLowW;
     extern __shared__ __align__(16) u32 sm32[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -475,6 +583,10 @@ __global__ void __launch_bounds__(kNT, 2) k32_low(const u32* __restrict__ src, u
             t.x = w[j];
             t.y = w[j + 1];
             st_pass(reinterpret_cast<ulonglong2*>(p + reg_part<C, 2>(j)), t);
+        }
+        if constexpr (EX) {
+            if (__any_sync(0xffffffffu, maybe_hit<32>(w, ex.tau)) && __any_sync(0xffffffffu, any_hit<32>(w, ex.tau)))
+                low_extract_slow(o, b << kBits, tp, ex);
         }
     }
 }

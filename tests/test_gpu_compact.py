@@ -274,3 +274,86 @@ def test_compact_full_size_n32_spot_check():
     assert rc == 0
     lib.oracle_fwht_i64(want.ctypes.data, d)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("n,cfg", [(26, 3), (27, 3), (26, 5), (28, 3)])
+def test_compact_fused_extraction_matches_two_step(coracle, monkeypatch, n, cfg):
+    """bw_fwht_extract_i64 on the noisy +-1 sums of configs 3 / 5: by default
+    (n >= 26) the compact plan with |W| >= tau tested in k32_low's final
+    registers; the same hits, in the same order, as the int64 plan
+    (BW_COMPACT=0) and as transform-then-extract, and the planted masks."""
+    from paper_1607_01039_b200 import signals
+
+    spec = signals.config(cfg, n=n)
+    assert spec.max_abs <= _lib.lib().bw_compact_limit(n)
+    tau = 1 << 20  # between the noise floor (~2^(n/2) * 5 * sqrt(K)) and the planted bias (0.1 / 0.04 * 2^n)
+    a = signals.make(spec)
+    x = a.cpu().numpy().copy()
+    i1, v1 = bw.fwht_extract_ge(a, tau)
+    monkeypatch.setenv("BW_COMPACT", "0")
+    b = torch.from_numpy(x.copy()).cuda()
+    i2, v2 = bw.fwht_extract_ge(b, tau)
+    monkeypatch.delenv("BW_COMPACT")
+    want = c_fwht(coracle, x)
+    assert np.array_equal(a.cpu().numpy(), want) and torch.equal(a, b)
+    assert torch.equal(i1, i2) and torch.equal(v1, v2)
+    hits = np.nonzero(np.abs(want) >= tau)[0]
+    assert i1.tolist() == hits.tolist() and v1.tolist() == want[hits].tolist()
+    assert sorted(spec.masks) == hits.tolist()
+
+
+def test_compact_fused_extraction_many_hits_and_wide_values(coracle):
+    """tau = 0 (every point hits: the ordered two-phase extraction takes
+    over) and a wide-valued signal (the checked pass refuses it: int64 plan
+    with its own fused extraction), both at a size the default tries the
+    compact plan on."""
+    n = 26
+    x = oracle_np.gen(1, 5, [], 0, 1 << n)
+    a = torch.from_numpy(x.copy()).cuda()
+    i1, v1 = bw.fwht_extract_ge(a, 0, cap=16)
+    want = c_fwht(coracle, x)
+    assert np.array_equal(a.cpu().numpy(), want)
+    assert torch.equal(i1, torch.arange(1 << n, device="cuda")) and np.array_equal(v1.cpu().numpy(), want)
+    x = oracle_np.gen(2, 6, [1 << 20], 0, 1 << n)
+    a = torch.from_numpy(x.copy()).cuda()
+    want = c_fwht(coracle, x)
+    tau = int(np.sort(np.abs(want))[-50])
+    i1, v1 = bw.fwht_extract_ge(a, tau)
+    hits = np.nonzero(np.abs(want) >= tau)[0]
+    assert np.array_equal(a.cpu().numpy(), want)
+    assert i1.tolist() == hits.tolist() and v1.tolist() == want[hits].tolist()
+
+
+def test_default_picks_compact_from_n26(coracle):
+    """bw_fwht_i64 / fwht_array / fwht_inplace with no arguments: the compact
+    plan from n = 26 up (bw_compact_auto), the int64 plan below and for wide
+    values; identical results."""
+    L = _lib.lib()
+    assert [L.bw_compact_auto(n) for n in (24, 25, 26, 30, 32, 33, 34)] == [0, 0, 1, 1, 1, 0, 0]
+    for n in (25, 26):
+        x = oracle_np.gen(1, n, [], 0, 1 << n)
+        want = c_fwht(coracle, x)
+        t = torch.from_numpy(x.copy()).cuda()
+        bw.fwht_array(t)
+        assert bw.core.last_compact == (n >= 26)
+        assert np.array_equal(t.cpu().numpy(), want)
+        t = torch.from_numpy(x.copy()).cuda()
+        _lib.check(L.bw_fwht_i64(t.data_ptr(), n, torch.cuda.current_stream().cuda_stream, None))
+        assert np.array_equal(t.cpu().numpy(), want)
+        sig = bw.fwht_inplace(bw.Signal(torch.from_numpy(x.copy()).cuda()))
+        assert np.array_equal(sig.data.cpu().numpy(), want)
+        sig = bw.fwht_inplace(bw.Signal(torch.from_numpy(x.copy()).cuda()), max_abs=1)
+        assert np.array_equal(sig.data.cpu().numpy(), want)
+    n = 26
+    x = oracle_np.gen(2, 9, [1 << 20], 0, 1 << n)  # wide values: the int64 plan after the exact restore
+    want = c_fwht(coracle, x)
+    t = torch.from_numpy(x.copy()).cuda()
+    bw.fwht_array(t)
+    assert not bw.core.last_compact and np.array_equal(t.cpu().numpy(), want)
+    sig = bw.fwht_inplace(bw.Signal(torch.from_numpy(x.copy()).cuda()))
+    assert np.array_equal(sig.data.cpu().numpy(), want)
+    x[12345] = 1 << 40  # over the overflow bound: raised before mutation, as ever (core.py:122)
+    t = torch.from_numpy(x.copy()).cuda()
+    with pytest.raises(bw.errors.OverflowBoundError):
+        bw.fwht_inplace(bw.Signal(t))
+    assert np.array_equal(t.cpu().numpy(), x)

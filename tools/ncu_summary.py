@@ -54,16 +54,28 @@ for i, r in enumerate(data):
                    "dram_read_bytes": to_bytes(r[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_read.sum"]]),
                    "dram_write_bytes": to_bytes(r[idx["dram__bytes_write.sum"]], units[idx["dram__bytes_write.sum"]])})
 plan = None
+alg = 16 * 2 ** n
+compact = any("k32_" in p["kernel"] for p in passes)  # the compact plan's int32-engine kernels
 try:
+    import ctypes
     import os
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    from paper_1607_01039_b200 import sharded
+    from paper_1607_01039_b200 import _lib, sharded
 
-    plan = [[q["kind"], q["k"], q["r"], q.get("split_a", 0), q.get("k2", 0)] for q in sharded.plan(n, 0)["passes"]]
+    if compact:  # the plan key bench.py compares with: [["compact", k, r, engine], ...]
+        L = _lib.lib()
+        plan, alg = [], []
+        for i in range(L.bw_compact_npasses(n)):
+            k_, r_, e_, b_ = (ctypes.c_int(0) for _ in range(4))
+            _lib.check(L.bw_compact_pass_info(n, i, ctypes.byref(k_), ctypes.byref(r_), ctypes.byref(e_), ctypes.byref(b_)))
+            plan.append(["compact", k_.value, r_.value, e_.value])
+            alg.append(b_.value * 2 ** n)
+    else:
+        plan = [[q["kind"], q["k"], q["r"], q.get("split_a", 0), q.get("k2", 0)] for q in sharded.plan(n, 0)["passes"]]
 except Exception as e:  # noqa: BLE001 -- the summary is still useful without the plan
     print("plan unavailable:", e)
 with open(f"{prefix}_traffic.json", "w") as f:
     json.dump({"source": f"ncu --set full --clock-control none ({rep})", "n": n, "plan": plan,
-               "algorithmic_bytes_per_pass": 16 * 2 ** n, "passes": passes}, f, indent=1)
+               "algorithmic_bytes_per_pass": alg, "passes": passes}, f, indent=1)
 for p in passes:
     print(p)

@@ -1,4 +1,6 @@
-"""Run the default FWHT pass plan a few times (profiling driver for ncu)."""
+"""Run the default FWHT pass plan a few times (profiling driver for ncu);
+the config input is regenerated before every transform, so each one runs the
+plan fwht_array picks for that input (the compact plan at n = 26..32)."""
 import argparse
 import os
 import sys
@@ -14,8 +16,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=28)
 ap.add_argument("--reps", type=int, default=2)
 a = ap.parse_args()
-t = signals.make(signals.config(4, a.n))
-for _ in range(a.reps):
+spec = signals.config(4, a.n)
+t = signals.make(spec)
+for rep in range(a.reps):
+    if rep:
+        signals.generate(spec, t)
     bw.fwht_array(t)
 torch.cuda.synchronize()
 print("ok", a.n)
