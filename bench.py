@@ -829,6 +829,12 @@ def run_ours(a):
     }
     if entry_points:
         line["entry_points"] = entry_points
+        if compact_local:  # the same call on the plan that takes any data, for comparison with `value`
+            t64 = entry_points["fwht_array_int64_plan_ms"]
+            line["int64_plan"] = {"ms_per_call": t64, "value": (2 ** n) / (t64 / 1e3), "unit": "points/s",
+                                  "note": "fwht_array(compact=False): the int64 plan (48 B/point at n = 32), which "
+                                          "signals with |x| above the compact limit run after the checked first pass "
+                                          "refuses them; same result bit for bit"}
     if b2b:
         line["back_to_back"] = b2b
     if narrow_local:

@@ -1901,6 +1901,12 @@ int compact_try(int64_t* data, int log2n, cudaStream_t s, int* used, const bw::E
     *used = 0;
     CompactPlan cp;
     if ((reinterpret_cast<uintptr_t>(data) & 15u) || !compact_plan(log2n, &cp) || (ex && !cp.v2)) return BW_OK;
+    // the verdict readback synchronises the stream, which a capturing stream cannot do: the int64 plan then
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return BW_OK;
+    }
     int dev = 0;
     BW_TRY(device_setup(&dev));
     unsigned *tileflag = nullptr, *abort = nullptr;

@@ -357,3 +357,28 @@ def test_default_picks_compact_from_n26(coracle):
     with pytest.raises(bw.errors.OverflowBoundError):
         bw.fwht_inplace(bw.Signal(t))
     assert np.array_equal(t.cpu().numpy(), x)
+
+
+def test_default_under_stream_capture_runs_the_int64_plan(coracle):
+    """The compact plan reads its first pass's verdict on the host, which a
+    capturing stream cannot do: bw_fwht_i64 then launches the (asynchronous)
+    int64 plan, so the call stays capturable; the replayed graph gives the
+    reference's result."""
+    n = 26
+    x = oracle_np.gen(1, 77, [], 0, 1 << n)
+    want = c_fwht(coracle, x)
+    t = torch.from_numpy(x.copy()).cuda()
+    L = _lib.lib()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        _lib.check(L.bw_fwht_i64_int64plan(t.data_ptr(), n, side.cuda_stream, None))  # warm-up: attributes, scratch
+    side.synchronize()
+    t.copy_(torch.from_numpy(x))
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        _lib.check(L.bw_fwht_i64(t.data_ptr(), n, torch.cuda.current_stream().cuda_stream, None))
+    assert np.array_equal(t.cpu().numpy(), x)  # captured, not run
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(t.cpu().numpy(), want)

@@ -114,6 +114,33 @@ def fam_compact():
     bw.fwht_array(t, compact=True)
     check("compact fallback (restore + int64 plan)",
           not bw.core.last_compact and np.array_equal(t.cpu().numpy(), ref_fwht(y)))
+    # the int32 engine's first pass (k32_first<6> / <5>: half of the tile landing in shared memory
+    # through cp.async, the verdict on the inter-round barrier), k32_restore, k32_high, k32_low
+    for n in (22, 23, 26):
+        lim = int(_lib.lib().bw_compact_limit(n))
+        x = oracle_np.gen(2, 17 + n, [min(lim, 1 << 20)], 0, 1 << n)
+        ref = ref_fwht(x)
+        for bound in (-1, lim):
+            t = torch.from_numpy(x.copy()).cuda()
+            bw.fwht_array(t, compact=True if bound < 0 else bound)
+            check(f"int32-engine compact plan n={n} (bound {bound})",
+                  bw.core.last_compact and np.array_equal(t.cpu().numpy(), ref))
+        y = x.copy()
+        y[(1 << n) - 5] = lim + 1
+        t = torch.from_numpy(y.copy()).cuda()
+        bw.fwht_array(t, compact=True)
+        check(f"int32-engine compact fallback n={n} (k32_restore + int64 plan)",
+              not bw.core.last_compact and np.array_equal(t.cpu().numpy(), ref_fwht(y)))
+    n = 26  # the threshold extraction in k32_low's final registers (the default at this size)
+    x = oracle_np.gen(1, 3, [], 0, 1 << n)
+    x[::4099] = 1
+    ref = ref_fwht(x)
+    tau = int(np.sort(np.abs(ref))[-40])
+    t = torch.from_numpy(x.copy()).cuda()
+    i, v = bw.fwht_extract_ge(t, tau)
+    hits = np.nonzero(np.abs(ref) >= tau)[0]
+    check("fused extraction in k32_low", np.array_equal(t.cpu().numpy(), ref) and i.cpu().tolist() == hits.tolist()
+          and v.cpu().tolist() == ref[hits].tolist())
 
 
 def fam_bound():
