@@ -617,6 +617,8 @@ int set_all_pass_attributes() {
     // the int32 engine of the compact plan (64 KiB of shared memory, 2 CTAs/SM)
     BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_high<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
     BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_high<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
+    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_high<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
+    BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_high<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
     BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_low<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
     BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_low<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
     BW_CUDA(cudaFuncSetAttribute(bw::w32::k32_first<5, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::w32::kSmemBytes));
@@ -1643,8 +1645,9 @@ struct CompactPlan {
 // CTA) and the 14-bit low pass k32_low, whose last four stages (bits 10..13)
 // run in int64 registers.  So v2 admits |x| <= (2^31 - 1) >> (n - 4): every
 // stage but the last four keeps |value| <= 2^31 - 1.  Rows: one high pass
-// for H <= 9, else H - r2 then r2 = 8 (256-byte row segments), 9 at H = 18
-// (BW_COMPACT_R2=8|9 forces it).  A FIRST pass of 8 or 9 rows also runs on
+// for H <= 9; H = 10..13: H - 8 then 8; H = 14..16: 8 then H - 8 (k32_high of
+// 6, 7 or 8 rows); H = 17, 18: 9 then 8 / 9 (BW_COMPACT_R2=6..9 forces the
+// second pass's rows).  A FIRST pass of 8 or 9 rows also runs on
 // the int32 engine (k32_first: natural int64 -> int32, the input test of the
 // unknown-bound case inside it; BW_COMPACT_FIRST=0: the int64 engine's
 // k_pass_map as before).
@@ -1667,7 +1670,7 @@ bool compact_plan(int n, CompactPlan* cp) {
     // do not fit the int32 engine (one high pass, or a second of 8 / 9 rows)
     bool v2 = compact_v2_enabled() && n <= 32 && !getenv("BW_COMPACT_W");
     if (v2 && rows_env)
-        v2 = sum == n - 14 && (rows.size() == 1 || (rows.size() == 2 && (rows[1] == 8 || rows[1] == 9)));
+        v2 = sum == n - 14 && (rows.size() == 1 || (rows.size() == 2 && rows[1] >= 6 && rows[1] <= 9));
     int w = n <= 31 ? 13 : 14;
     if (const char* e = getenv("BW_COMPACT_W")) w = atoi(e) == 14 ? 14 : 13;
     if (v2) w = 14;
@@ -1675,8 +1678,10 @@ bool compact_plan(int n, CompactPlan* cp) {
     if (rows_env) {
         if (sum != H) return false;
     } else if (v2) {
-        int r2 = H - 8 <= 9 ? 8 : 9;
-        if (const char* e = getenv("BW_COMPACT_R2")) r2 = atoi(e) == 8 ? 8 : 9;
+        // H < 14: a short first pass (registers only on the int64 engine, fast) then 8 rows; H = 14..16: 8 rows
+        // on the int32 engine first (256-byte segments), then H - 8 = 6..8; H = 17, 18: 9 then 8 / 9
+        int r2 = H < 14 ? 8 : H <= 16 ? H - 8 : H - 9;
+        if (const char* e = getenv("BW_COMPACT_R2")) r2 = atoi(e) >= 6 && atoi(e) <= 9 ? atoi(e) : 9;
         if (H <= 9) rows.push_back(H);
         else if (H - r2 >= 1 && H - r2 <= 9) {
             rows.push_back(H - r2);
@@ -1815,6 +1820,8 @@ int launch_compact(const CompactPlan& cp, int i, int64_t* data, CompactMode mode
         uint32_t* dst = reinterpret_cast<uint32_t*>(d32 + ((size_t)cp.half[i] << cp.w));
         if (p.r == 9) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_high<5>, src, dst, p.k));
         else if (p.r == 8) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_high<6>, src, dst, p.k));
+        else if (p.r == 7) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_high<7>, src, dst, p.k));
+        else if (p.r == 6) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_high<8>, src, dst, p.k));
         else return fail(BW_BAD_ARGUMENTS, "no int32-engine pass of %d rows", p.r);
         return BW_OK;
     }
@@ -2192,6 +2199,8 @@ int w32_visit_pass(const CompactPlan& cp, int q, F&& f) {
     };
     if (p.r == 9) return run(tag<w::CfgHighW<5>>{}, ic<5>{});
     if (p.r == 8) return run(tag<w::CfgHighW<6>>{}, ic<6>{});
+    if (p.r == 7 && q > 0) return run(tag<w::CfgHighW<7>>{}, ic<7>{});
+    if (p.r == 6 && q > 0) return run(tag<w::CfgHighW<8>>{}, ic<8>{});
     return fail(BW_BAD_ARGUMENTS, "no int32-engine pass of %d rows", p.r);
 }
 
@@ -2320,6 +2329,8 @@ int w32_emulate(int64_t* host, const CompactPlan& cp) {
         };
         if (p.r == 9) run(tag<w::CfgHighW<5>>{}, ic<5>{});
         else if (p.r == 8) run(tag<w::CfgHighW<6>>{}, ic<6>{});
+        else if (p.r == 7 && q > 0) run(tag<w::CfgHighW<7>>{}, ic<7>{});
+        else if (p.r == 6 && q > 0) run(tag<w::CfgHighW<8>>{}, ic<8>{});
         else return fail(BW_BAD_ARGUMENTS, "no int32-engine pass of %d rows", p.r);
     }
     memcpy(host, buf.data(), 8 * N);

@@ -74,26 +74,45 @@ struct CfgLowW {
 
 // High pass, r = 14 - L rows: virtual bits 0..L-1 are the columns (slot bits
 // 0..L-1 of the compact layout), L..13 the rows.
-//   L = 5 (9 rows): round 0 reg {0,5..9}   lane {1,2,3,4,10} warp {11,12,13} stages 5..9  (8-byte loads)
-//                   round 1 reg {0,1,10..13} lane {2..6}      warp {7,8,9}    stages 10..13 (16-byte stores)
-//   L = 6 (8 rows): round 0 reg {0,6..10}  lane {1..5}       warp {11,12,13} stages 6..10
+//   L = 5 (9 rows): round 0 reg {0,5..9}     lane {1,2,3,4,10} warp {11,12,13} stages 5..9  (8-byte loads)
+//                   round 1 reg {0,1,10..13} lane {2..6}       warp {7,8,9}    stages 10..13 (16-byte stores)
+//   L = 6 (8 rows): round 0 reg {0,6..10}    lane {1..5}       warp {11,12,13} stages 6..10
 //                   round 1 reg {0,1,11,12,13,6} lane {2,3,4,5,7} warp {8,9,10} stages 11..13
+//   L = 7 (7 rows): round 0 reg {0,7..11}    lane {1..5}       warp {6,12,13}  stages 7..11
+//                   round 1 reg {0,1,12,13,7,8} lane {2..6}    warp {9,10,11}  stages 12, 13
+//   L = 8 (6 rows): round 0 reg {0,8..12}    lane {1..5}       warp {6,7,13}   stages 8..12
+//                   round 1 reg {0,1,13,8,9,10} lane {2..6}    warp {7,11,12}  stage 13
+// (L = 7, 8: second passes only, as 8 rows then 7 / 6 at n = 29 / 28.)
 template <int L>
 struct CfgHighW {
-    static_assert(L == 5 || L == 6, "int32 high passes of 8 or 9 rows");
+    static_assert(L >= 5 && L <= 8, "int32 high passes of 6 to 9 rows");
     static constexpr int NR = 2;
     BW_HD static constexpr int nreg(int) { return 6; }
     BW_HD static constexpr int reg(int rd, int i) {
-        return nib(L == 5 ? (rd == 0 ? 0x987650ull : 0xDCBA10ull) : (rd == 0 ? 0xA98760ull : 0x6DCB10ull), i);
+        return nib(L == 5   ? (rd == 0 ? 0x987650ull : 0xDCBA10ull)
+                   : L == 6 ? (rd == 0 ? 0xA98760ull : 0x6DCB10ull)
+                   : L == 7 ? (rd == 0 ? 0xBA9870ull : 0x87DC10ull)
+                            : (rd == 0 ? 0xCBA980ull : 0xA98D10ull),
+                   i);
     }
     BW_HD static constexpr int lane(int rd, int i) {
-        return nib(L == 5 ? (rd == 0 ? 0xA4321ull : 0x65432ull) : (rd == 0 ? 0x54321ull : 0x75432ull), i);
+        return nib(L == 5   ? (rd == 0 ? 0xA4321ull : 0x65432ull)
+                   : L == 6 ? (rd == 0 ? 0x54321ull : 0x75432ull)
+                            : (rd == 0 ? 0x54321ull : 0x65432ull),
+                   i);
     }
     BW_HD static constexpr int warp(int rd, int i) {
-        return nib(L == 5 ? (rd == 0 ? 0xDCBull : 0x987ull) : (rd == 0 ? 0xDCBull : 0xA98ull), i);
+        return nib(L == 5   ? (rd == 0 ? 0xDCBull : 0x987ull)
+                   : L == 6 ? (rd == 0 ? 0xDCBull : 0xA98ull)
+                   : L == 7 ? (rd == 0 ? 0xDC6ull : 0xBA9ull)
+                            : (rd == 0 ? 0xD76ull : 0xCB7ull),
+                   i);
     }
     BW_HD static constexpr uint32_t stage(int rd) {
-        return L == 5 ? (rd == 0 ? 0x3E0u : 0x3C00u) : (rd == 0 ? 0x7C0u : 0x3800u);
+        return L == 5   ? (rd == 0 ? 0x3E0u : 0x3C00u)
+               : L == 6 ? (rd == 0 ? 0x7C0u : 0x3800u)
+               : L == 7 ? (rd == 0 ? 0xF80u : 0x3000u)
+                        : (rd == 0 ? 0x1F00u : 0x2000u);
     }
     BW_HD static constexpr uint32_t slot(uint32_t e) { return e; }
 };

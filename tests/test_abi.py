@@ -404,7 +404,7 @@ def test_compact_plan_checks(monkeypatch, n, v2):
     assert L.bw_compact_limit(n) == (2**31 - 1) >> (n - 4 if v2 == "1" else n - 13)
 
 
-@pytest.mark.parametrize("n,r2", [(16, "9"), (20, "9"), (22, "9"), (23, "9"), (24, "9"), (24, "8")])
+@pytest.mark.parametrize("n,r2", [(16, "9"), (20, "9"), (22, "9"), (23, "9"), (24, "9"), (24, "8"), (24, "7"), (24, "6")])
 def test_compact_v2_host_emulation_matches_oracle(monkeypatch, coracle, n, r2):
     """The int32-engine passes' exact tables (rounds, swizzled shared-memory
     slots, int32 / int64 arithmetic) run on the host (bw_debug_emulate_compact)
@@ -442,3 +442,17 @@ def test_compact_checker_catches_a_layout_that_is_not_in_place(monkeypatch):
     # first pass no longer writes
     monkeypatch.setenv("BW_COMPACT_V2", "1")
     assert _lib.lib().bw_plan_check_compact(20) != 0
+
+
+@pytest.mark.parametrize("r2", ["6", "7", "8", "9"])
+def test_compact_plan_checks_every_second_pass_shape(monkeypatch, r2):
+    """k32_high with 6, 7, 8 and 9 rows as the second high pass (n = 24: 10 - r2
+    rows first): the static checker on the kernels' exact address functions
+    (coverage, bank conflicts, in place, every bit staged once)."""
+    monkeypatch.setenv("BW_COMPACT_R2", r2)
+    L = _lib.lib()
+    assert L.bw_plan_check_compact(24) == 0, _lib.last_error()
+    assert L.bw_compact_npasses(24) == 3
+    k, r = ctypes.c_int(0), ctypes.c_int(0)
+    assert L.bw_compact_pass_info(24, 1, ctypes.byref(k), ctypes.byref(r), None, None) == 0
+    assert r.value == int(r2) and k.value == 14 + 10 - int(r2)

@@ -67,7 +67,7 @@ def test_compact_plan_shapes(coracle, monkeypatch, rows, w):
 
 
 @pytest.mark.parametrize("n,r2", [(16, "9"), (22, "9"), (23, "9"), (24, "9"), (24, "8"), (25, "9"), (26, "9"),
-                                  (27, "8"), (28, "9"), (29, "9"), (30, "9"), (30, "8")])
+                                  (27, "8"), (28, "9"), (28, "6"), (29, "9"), (29, "7"), (29, "8"), (30, "9"), (30, "8")])
 def test_compact_v2_limit_values(coracle, monkeypatch, n, r2):
     """The int32-engine plan (k32_high with 9 / 8 rows, k32_low with its last
     four stages in int64) on inputs at +-lim(n) = (2^31 - 1) >> (n - 4),
