@@ -248,11 +248,10 @@ __device__ __forceinline__ u32 ld1(const u32* p) {
 // PRE_SYNC (k32_first with half its loads landing in shared memory): one
 // more barrier after round 0's stages, before the transpose overwrites the
 // landing slots other threads may still be reading.
-template <int L, bool CHECK = false, bool PRE_SYNC = false>
+template <int L, bool CHECK = false, bool PRE_SYNC = false, class C = CfgHighW<L>>
 __device__ __forceinline__ void high_rounds_store(u32 (&v)[kE], u32* sm32, u32* dst, uint64_t base, int kk, uint32_t lane,
                                                   uint32_t warp, bool bad = false, unsigned* tileflag = nullptr,
                                                   unsigned* abort = nullptr) {
-    using C = CfgHighW<L>;
     stages32<C, 0>(v);
     if constexpr (PRE_SYNC) {
         BW_STRESS(68);
@@ -286,9 +285,8 @@ __device__ __forceinline__ void high_rounds_store(u32 (&v)[kE], u32* sm32, u32* 
 
 // int32 -> int32 high pass over rows [k, k + 14 - L) of the compact layout.
 // src / dst: the int32 view of the signal, offset by the read / write half.
-template <int L, int MINB = 2>
+template <int L, int MINB = 2, class C = CfgHighW<L>>
 __global__ void __launch_bounds__(kNT, MINB) k32_high(const u32* __restrict__ src, u32* __restrict__ dst, int k) {
-    using C = CfgHighW<L>;
     extern __shared__ __align__(16) u32 sm32[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const int kk = k + 1;
@@ -316,7 +314,7 @@ __global__ void __launch_bounds__(kNT, MINB) k32_high(const u32* __restrict__ sr
             }
         }
     }
-    high_rounds_store<L>(v, sm32, dst, base, kk, lane, warp);
+    high_rounds_store<L, false, false, C>(v, sm32, dst, base, kk, lane, warp);
 }
 
 // ---------------------------------------------------------------------------

@@ -22,9 +22,22 @@ __global__ void k_fill32(int* x, uint64_t n) {
     }
 }
 
-template <int L, int MINB>
-static void run(int* x, int n, int k, int reps) {
-    auto kern = k32_high<L, MINB>;
+// 9 rows with 16-byte loads and 8-byte stores (the mirror image of CfgHighW<5>):
+//   round 0 reg {0,1,5,6,7,8} lane {2,3,4,9,10} warp {11,12,13} stages 5..8
+//   round 1 reg {0,9..13}     lane {1..5}       warp {6,7,8}    stages 9..13
+struct CfgHighW5B {
+    static constexpr int NR = 2;
+    BW_HD static constexpr int nreg(int) { return 6; }
+    BW_HD static constexpr int reg(int rd, int i) { return bw::nib(rd == 0 ? 0x876510ull : 0xDCBA90ull, i); }
+    BW_HD static constexpr int lane(int rd, int i) { return bw::nib(rd == 0 ? 0xA9432ull : 0x54321ull, i); }
+    BW_HD static constexpr int warp(int rd, int i) { return bw::nib(rd == 0 ? 0xDCBull : 0x876ull, i); }
+    BW_HD static constexpr uint32_t stage(int rd) { return rd == 0 ? 0x1E0u : 0x3E00u; }
+    BW_HD static constexpr uint32_t slot(uint32_t e) { return e; }
+};
+
+template <int L, int MINB, class C = CfgHighW<L>>
+static void run(int* x, int n, int k, int reps, const char* what = "") {
+    auto kern = k32_high<L, MINB, C>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kNT, kSmemBytes);
@@ -43,8 +56,8 @@ static void run(int* x, int n, int k, int reps) {
         cudaEventElapsedTime(&ms, e0, e1);
         if (r) total += ms;
     }
-    printf("k32_high<L=%d> %d CTAs/SM asked, %d resident: n=%d stages %d..%d: %.3f ms, %.2f TB/s of 8 B/point  %s\n", L, MINB,
-           occ, n, k, k + 13 - L, total / reps, 8.0 * (double)(1ull << n) / (total / reps / 1e3) / 1e12,
+    printf("k32_high<L=%d>%s %d CTAs/SM asked, %d resident: n=%d stages %d..%d: %.3f ms, %.2f TB/s of 8 B/point  %s\n", L,
+           what, MINB, occ, n, k, k + 13 - L, total / reps, 8.0 * (double)(1ull << n) / (total / reps / 1e3) / 1e12,
            cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -53,6 +66,7 @@ int main(int argc, char** argv) {
     int* x = nullptr;
     if (cudaMalloc(&x, 8ull << 32) != cudaSuccess) return 1;
     run<5, 2>(x, 32, 23, reps);
+    run<5, 2, CfgHighW5B>(x, 32, 23, reps, " (16-byte loads, 8-byte stores)");
     run<5, 3>(x, 32, 23, reps);
     run<6, 2>(x, 31, 23, reps);
     run<6, 3>(x, 31, 23, reps);
