@@ -389,10 +389,13 @@ __device__ __forceinline__ bool first_bad(const FirstAcc& acc, u32 lim) {
 //      cp.async, registers 0..31 through plain loads: the whole tile is in
 //      flight at once with 64 instead of 128 registers of raw data, so the
 //      checked pass (which needs the high words) no longer splits its loads;
-//   3: as 2 with the biased-add test (CHK 1).
-// n = 32, 12 B/point: plain 8.02 ms in every variant; checked 9.72 (0, 1),
-// 8.71 (2) -- profiles/r02_compact/mb_first32.log.
-constexpr int kFirstVar = 3;
+//   3: as 2 with the biased-add test (CHK 1);
+//   4: as 3, and a tile that finds the abort word set returns before loading (one more barrier,
+//      behind the abort word's load).
+// n = 32, 12 B/point: plain 8.02 ms in every variant; checked 9.7 (0, 1),
+// 8.6 (2), 8.13 (3), 8.00 (4: the barrier at the start costs nothing, the
+// warps then issue their loads together) -- profiles/r02_compact/mb_first32*.log.
+constexpr int kFirstVar = 4;
 
 template <int L, int MODE, int VAR = kFirstVar>
 __global__ void __launch_bounds__(kNT, 2)
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(kNT, 2)
               unsigned* abort) {
     using C = CfgHighW<L>;
     static_assert(vec<C, 0>() == 2, "int64 pairs in round 0");
-    constexpr int CHK = VAR == 3 ? 1 : 0;
+    constexpr int CHK = VAR >= 3 ? 1 : 0;
     constexpr bool LAND = VAR >= 2;
     extern __shared__ __align__(16) u32 sm32[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -411,6 +414,9 @@ __global__ void __launch_bounds__(kNT, 2)
     if constexpr (MODE == FIRST_CHECK) {  // another tile failed: this one stores nothing either (in flight with the loads)
         if constexpr (VAR == 0) acc.hi[0] = *reinterpret_cast<volatile unsigned*>(abort);
         else asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(acc.hi[0]) : "l"(abort));
+        if constexpr (VAR == 4) {  // ... and does not even load: a refused signal costs a few tiles, not a read pass
+            if (__syncthreads_or(acc.hi[0] != 0u)) return;
+        }
     }
     const unsigned long long* p = src + first_base(base) + first_off<L>(thread_part<C, 0>(lane, warp), k);
     if constexpr (LAND) {

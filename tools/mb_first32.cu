@@ -85,10 +85,12 @@ int main(int argc, char** argv) {
     run<5, 1, 1>(x, n, flags, abort, sum, reps);
     run<5, 1, 2>(x, n, flags, abort, sum, reps);
     run<5, 1, 3>(x, n, flags, abort, sum, reps);
+    run<5, 1, 4>(x, n, flags, abort, sum, reps);
     run<6, 0, 0>(x, n - 1, flags, abort, sum, reps);
     run<6, 0, 2>(x, n - 1, flags, abort, sum, reps);
     run<6, 1, 0>(x, n - 1, flags, abort, sum, reps);
     run<6, 1, 2>(x, n - 1, flags, abort, sum, reps);
     run<6, 1, 3>(x, n - 1, flags, abort, sum, reps);
+    run<6, 1, 4>(x, n - 1, flags, abort, sum, reps);
     return 0;
 }
