@@ -10,15 +10,19 @@
 // in flight per tile as the int64 engine, so an int32 pass should take the
 // time of its bytes.
 //
-//   k32_high<C, L>: int32 -> int32 high pass, r = 14 - L stage rows of the
+//   k32_first<L, MODE>: the plan's first pass, natural int64 -> int32 in
+//     place (8 or 9 rows), with the input test of the unknown-bound case
+//     (MODE = FIRST_CHECK); k32_restore<L> undoes it on the tiles it wrote.
+//   k32_high<L>: int32 -> int32 high pass, r = 14 - L = 6..9 stage rows of the
 //     compact layout (2^L contiguous int32 columns, rows at slot stride
 //     2^(k+1)); one CTA per tile, two rounds joined by one shared-memory
 //     transpose.
-//   k32_low<C>: int32 -> int64 low pass (stages 0..13 of every 2^14 block),
+//   k32_low<EX>: int32 -> int64 low pass (stages 0..13 of every 2^14 block),
 //     reading the block's int32 half and writing the natural int64 block.
 //     Rounds 0 and 1 stage 10 bits in int32; round 2 runs as two sub-rounds
 //     of 2^13 elements (32 per thread) that widen to int64 and stage the
 //     last 4 bits (10..13) in int64 registers, then store 16-byte pairs.
+//     EX: the threshold extraction (|W| >= tau) on the final registers.
 //
 // Exactness: the plan admits only |x| <= (2^31 - 1) >> (n - 4) (bw_abi.cu
 // compact_plan), so every int32 intermediate -- all stages but the last
@@ -29,7 +33,7 @@
 // pass's sub-rounds), a lane bit (5) or a warp bit (3); butterflies run on
 // register bits.  Shared-memory slots are a linear XOR swizzle of the tile
 // index, chosen so that every 4/8/16-byte access phase of every round is
-// conflict-free (bw_plan_check_w32 verifies it; tools/design32.py searched it).
+// conflict-free (bw_plan_check_compact verifies every round of every config).
 #pragma once
 #include <stdint.h>
 
