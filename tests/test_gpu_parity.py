@@ -2,6 +2,7 @@
 golden outputs and the CPU oracle.  int64 results must be bit-exact."""
 
 import ctypes
+import os
 import hashlib
 
 import numpy as np
@@ -30,8 +31,18 @@ def gpu_fwht(x):
 
 
 def c_fwht(coracle, x):
+    """The C oracle's transform of x: oracle_fwht_i64 (core.py:97-117) below
+    n = 24; from there its restatement of the reference's run_parallel
+    decomposition (parallel.py:162-198, one thread per worker) -- the same
+    butterflies, so the same bits (tests/test_oracle.py pins both to the
+    reference's digests), in a fraction of the single-threaded time."""
     y = np.ascontiguousarray(x, dtype=np.int64).copy()
-    coracle.oracle_fwht_i64(y.ctypes.data, int(y.size).bit_length() - 1)
+    n = int(y.size).bit_length() - 1
+    if n >= 24:
+        p = max(1, min(4, (len(os.sched_getaffinity(0)) or 1).bit_length() - 1))
+        assert coracle.oracle_run_parallel_i64(y.ctypes.data, n, p) == 0
+    else:
+        coracle.oracle_fwht_i64(y.ctypes.data, n)
     return y
 
 
