@@ -66,6 +66,8 @@ int main(int argc, char** argv) {
     int* x = nullptr;
     if (cudaMalloc(&x, 8ull << 32) != cudaSuccess) return 1;
     run<5, 2>(x, 32, 23, reps);
+    run<5, 2>(x, 32, 18, reps);
+    run<5, 2>(x, 32, 14, reps);
     run<5, 2, CfgHighW5B>(x, 32, 23, reps, " (16-byte loads, 8-byte stores)");
     run<5, 3>(x, 32, 23, reps);
     run<6, 2>(x, 31, 23, reps);
