@@ -254,12 +254,13 @@ def test_compact_unaligned_view_runs_int64_plan(coracle):
 
 @pytest.mark.skipif(torch.cuda.is_available() and torch.cuda.get_device_properties(0).total_memory < (100 << 30),
                     reason="needs a B200")
-def test_compact_full_size_n32_spot_check():
-    """n = 32 (config 4) through the compact plan: the fold spot check of
-    2^20 outputs (subspace.py:1-11) against the CPU."""
+@pytest.mark.parametrize("n", [31, 32])
+def test_compact_full_size_n32_spot_check(n):
+    """n = 32 (config 4: 9 + 9 rows) and n = 31 (9 + 8 rows) through the
+    compact plan: the fold spot check of 2^20 outputs (subspace.py:1-11)
+    against the CPU."""
     from paper_1607_01039_b200 import signals
 
-    n = 32
     spec = signals.config(4, n)
     t = torch.empty(1 << n, dtype=torch.int64, device="cuda")
     signals.generate(spec, t)
