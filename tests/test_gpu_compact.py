@@ -254,11 +254,11 @@ def test_compact_unaligned_view_runs_int64_plan(coracle):
 
 @pytest.mark.skipif(torch.cuda.is_available() and torch.cuda.get_device_properties(0).total_memory < (100 << 30),
                     reason="needs a B200")
-@pytest.mark.parametrize("n", [31, 32])
-def test_compact_full_size_n32_spot_check(n):
-    """n = 32 (config 4: 9 + 9 rows) and n = 31 (9 + 8 rows) through the
-    compact plan: the fold spot check of 2^20 outputs (subspace.py:1-11)
-    against the CPU."""
+@pytest.mark.parametrize("n", [28, 29, 30, 31, 32])
+def test_compact_full_size_spot_check(n):
+    """n = 32 (config 4: 9 + 9 rows), 31 (9 + 8), 30 (8 + 8), 29 (8 + 7) and
+    28 (8 + 6) through the compact plan: the fold spot check of 2^20 outputs
+    (subspace.py:1-11) against the CPU."""
     from paper_1607_01039_b200 import signals
 
     spec = signals.config(4, n)
