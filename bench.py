@@ -65,7 +65,7 @@ def args_parse():
     ap.add_argument("--intermediates", choices=["auto", "compact", "narrow", "int64"], default="auto",
                     help="auto: what fwht_array runs by default -- the compact in-place plan (int32 intermediates "
                          "inside the signal's own buffer, first pass checked, int64 plan on larger values) where "
-                         "the library picks it (n = 30..32, one GPU, no fused extraction), else the int64 plan; "
+                         "the library picks it (n = 26..34, one GPU), else the int64 plan; "
                          "compact: the compact plan wherever one exists; narrow: the narrow-intermediate plan "
                          "(needs a 24 GiB work buffer at n = 32, DESIGN.md section 5); int64: the plain int64 plan")
     ap.add_argument("--mode", choices=["auto", "fused", "peer", "a2a", "narrow"], default="auto",
@@ -348,6 +348,10 @@ def run_ours(a):
         ncp = 0
     compact_local = (not narrow_local and ncp > 0 and
                      (a.intermediates == "compact" or (a.intermediates == "auto" and L.bw_compact_auto(nl) == 1)))
+    # n >= 33: the library tests a sample of the first inputs before the attempt and goes straight to the
+    # int64 plan when it fails (config 5's sums of 8 exceed lim(34) = 1); the pass-level step does the same
+    if compact_local and a.intermediates == "auto" and nl >= 33 and spec.max_abs > L.bw_compact_limit(nl):
+        compact_local = False
     n_fallback = 0
     if compact_local:
         cflags = torch.zeros(1 << max(nl - 13, 0), dtype=torch.int32, device="cuda")
@@ -849,7 +853,8 @@ def run_ours(a):
     elif compact_local:
         names = ["k32_first (natural int64 -> int32 in place, every input tested)" if cinfo[0]["engine"] == 32
                  else "k_pass_map (int64 -> int32, every input tested)"]
-        names += ["k32_high (int32 -> int32)" if c["engine"] == 32 else "k_pass_map (int32 -> int32)" for c in cinfo[1:-1]]
+        names += [("k32_reg (int32 -> int32, registers only)" if c["r"] <= 4 else "k32_high (int32 -> int32)")
+                  if c["engine"] == 32 else "k_pass_map (int32 -> int32)" for c in cinfo[1:-1]]
         names += [("k32_low (int32 -> natural int64, last four stages in int64"
                    + (", |W| > tau fused in)" if extract else ")")) if cinfo[-1]["engine"] == 32
                   else "k_pass_map (int32 -> int64)"]

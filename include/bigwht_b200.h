@@ -70,7 +70,7 @@ int bw_device_cc(int device);
  * (/root/reference/pkg/src/bigwht/core.py:97-117): no magnitude check (the
  * reference has none either), returns the butterfly count n*2^(n-1)
  * (core.py:117) in *butterflies (may be NULL).  Asynchronous, except for
- * the sizes bw_compact_auto() names (n = 30..32 by default), where the
+ * the sizes bw_compact_auto() names (n = 26..34 by default), where the
  * compact plan is tried first and the call waits once for its first pass's
  * verdict (below: bw_fwht_i64_compact; bw_fwht_i64_int64plan never does).
  * Pass plan: one fused low-bits pass over stages 0..12/13/14 followed by
@@ -169,8 +169,7 @@ int bw_plan_check_narrow(int log2n);
 
 /*
  * fwht_array with COMPACT IN-PLACE INTERMEDIATES: for |x| <= lim(n)
- * (bw_compact_limit; 7 at n = 32 and 31 at n = 30 with the int32 engine,
- * 2047 at n = 34 with the int64 engine's passes -- the +-1 Boolean signals
+ * (bw_compact_limit; 7 at n = 32, 31 at n = 30, 1 at n = 34 -- the +-1 Boolean signals
  * of the paper and any small-integer signal) the high-bit stages
  * run first with the signal stored as int32 inside its own buffer, and the
  * low-bit pass widens back to natural int64: 12 + 8 (m - 1) + 12 bytes per
@@ -190,9 +189,9 @@ int bw_fwht_i64_compact(int64_t *data, int log2n, long long max_abs, void *strea
 /*
  * Whether bw_fwht_i64 / bw_fwht_inplace_i64 / bw_fwht_inplace_known_i64 try
  * the compact plan by themselves on a 16-byte aligned signal of 2^log2n
- * points: by default (BW_COMPACT unset or "auto") for the sizes whose every
- * pass runs on the int32 engine and measured faster (n = 30..32: 21.5 vs
- * 31.4 ms at n = 32); BW_COMPACT=1: wherever a compact plan exists (n >= 22);
+ * points: by default (BW_COMPACT unset or "auto") for the sizes where it
+ * measured faster (n = 26..34: 21.7 vs 31.4 ms at n = 32, 103.8 vs 140.1 ms
+ * at n = 34); BW_COMPACT=1: wherever a compact plan exists (n >= 22);
  * BW_COMPACT=0: never.  fwht_array then synchronises the stream once (the
  * first pass's verdict) and is otherwise unchanged: same result bit for bit,
  * the int64 plan for signals with larger values.

@@ -236,9 +236,9 @@ last_compact = False  # whether the last fwht_array call ran the compact in-plac
 def _compact_wanted(n: int, compact) -> bool:
     """Whether fwht_array tries the compact in-place plan (int32
     intermediates inside the signal's own buffer, bw_fwht_i64_compact).
-    compact=None follows the library's default (bw_compact_auto: n = 30..32,
-    where every pass runs on the int32 engine and the plan measured a third
-    faster; BW_COMPACT=1 / 0 widens it to n >= 22 / turns it off)."""
+    compact=None follows the library's default (bw_compact_auto: n = 26..34,
+    where the plan measured a fifth to a third faster; BW_COMPACT=1 / 0 widens
+    it to n >= 22 / turns it off)."""
     if compact is False or _lib.lib().bw_compact_npasses(n) == 0:
         return False
     if compact is None:
@@ -267,8 +267,9 @@ def fwht_array(buf, narrow=None, compact=None) -> int:
     Its first pass tests every input against lim(n) (7 at n = 32, 31 at
     n = 30); if one is larger, the tiles already written are restored exactly
     and the int64 plan runs.  Results are identical either way.  None: the
-    library's default (tried at n = 30..32, where it measured a third faster:
-    21.5 vs 31.4 ms at n = 32; BW_COMPACT=1 / 0: n >= 22 / never); True: the
+    library's default (tried at n = 26..34, where it measured faster: 21.7 vs
+    31.4 ms at n = 32, 103.8 vs 140.1 at n = 34; BW_COMPACT=1 / 0: n >= 22 /
+    never); True: the
     checked plan; False: the int64 plan; an int: a bound on |x| the caller
     guarantees (no test, no synchronisation).
     """

@@ -1668,9 +1668,13 @@ bool compact_plan(int n, CompactPlan* cp) {
     }
     // v2 unless disabled, n > 32, a low-pass width is forced, or forced rows
     // do not fit the int32 engine (one high pass, or a second of 8 / 9 rows)
-    bool v2 = compact_v2_enabled() && n <= 32 && !getenv("BW_COMPACT_W");
+    bool v2 = compact_v2_enabled() && n <= 35 && !getenv("BW_COMPACT_W");
     if (v2 && rows_env)
-        v2 = sum == n - 14 && (rows.size() == 1 || (rows.size() == 2 && rows[1] >= 6 && rows[1] <= 9));
+    {   // ... a first pass of any shape, later ones of 6..9 (k32_high) or 1..4 rows (k32_reg)
+        bool ok = sum == n - 14 && !rows.empty() && rows.size() <= 3;
+        for (size_t j = 1; ok && j < rows.size(); ++j) ok = rows[j] >= 1 && rows[j] <= 9 && rows[j] != 5;
+        v2 = ok;
+    }
     int w = n <= 31 ? 13 : 14;
     if (const char* e = getenv("BW_COMPACT_W")) w = atoi(e) == 14 ? 14 : 13;
     if (v2) w = 14;
@@ -1683,7 +1687,11 @@ bool compact_plan(int n, CompactPlan* cp) {
         int r2 = H < 14 ? 8 : H <= 16 ? H - 8 : H - 9;
         if (const char* e = getenv("BW_COMPACT_R2")) r2 = atoi(e) >= 6 && atoi(e) <= 9 ? atoi(e) : 9;
         if (H <= 9) rows.push_back(H);
-        else if (H - r2 >= 1 && H - r2 <= 9) {
+        else if (H >= 19 && H <= 21 && !getenv("BW_COMPACT_R2")) {  // n = 33..35: 9 rows, 8 rows, then 2..4 in registers
+            rows.push_back(9);
+            rows.push_back(8);
+            rows.push_back(H - 17);
+        } else if (H - r2 >= 1 && H - r2 <= 9) {
             rows.push_back(H - r2);
             rows.push_back(r2);
         } else return false;
@@ -1822,6 +1830,14 @@ int launch_compact(const CompactPlan& cp, int i, int64_t* data, CompactMode mode
         else if (p.r == 8) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_high<6>, src, dst, p.k));
         else if (p.r == 7) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_high<7>, src, dst, p.k));
         else if (p.r == 6) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_high<8>, src, dst, p.k));
+        else if (p.r >= 1 && p.r <= 4) {  // registers only: 4 slots of every row per thread
+            cfg.gridDim = dim3((unsigned)(1ull << (cp.n - p.r - 10)));
+            cfg.dynamicSmemBytes = 0;
+            if (p.r == 1) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_reg<1>, src, dst, p.k));
+            else if (p.r == 2) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_reg<2>, src, dst, p.k));
+            else if (p.r == 3) BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_reg<3>, src, dst, p.k));
+            else BW_CUDA(cudaLaunchKernelEx(&cfg, bw::w32::k32_reg<4>, src, dst, p.k));
+        }
         else return fail(BW_BAD_ARGUMENTS, "no int32-engine pass of %d rows", p.r);
         return BW_OK;
     }
@@ -1918,8 +1934,16 @@ int compact_try(int64_t* data, int log2n, cudaStream_t s, int* used, const bw::E
     BW_TRY(device_setup(&dev));
     unsigned *tileflag = nullptr, *abort = nullptr;
     BW_TRY(compact_scratch(dev, cp, &tileflag, &abort, s));
-    BW_TRY(launch_compact(cp, 0, data, COMPACT_CHECK, tileflag, abort, s));
     unsigned bad = 0;
+    if (cp.v2 && log2n >= 33) {  // a sample first: a refused full attempt would cost ~2.5 ms at n = 34
+        bw::w32::k32_sample<<<1, bw::w32::kNT, 0, s>>>(reinterpret_cast<const unsigned long long*>(data), (uint32_t)cp.lim,
+                                                        abort);
+        BW_LAUNCHED("k32_sample launch");
+        BW_CUDA(cudaMemcpyAsync(&bad, abort, sizeof bad, cudaMemcpyDeviceToHost, s));
+        BW_CUDA(cudaStreamSynchronize(s));
+        if (bad) return BW_OK;  // nothing was written
+    }
+    BW_TRY(launch_compact(cp, 0, data, COMPACT_CHECK, tileflag, abort, s));
     BW_CUDA(cudaMemcpyAsync(&bad, abort, sizeof bad, cudaMemcpyDeviceToHost, s));
     BW_CUDA(cudaStreamSynchronize(s));
     if (bad) return launch_compact(cp, 0, data, COMPACT_RESTORE, tileflag, abort, s);
@@ -1936,14 +1960,16 @@ int compact_try(int64_t* data, int log2n, cudaStream_t s, int* used, const bw::E
 // n = 32: 23.7 vs 31.4 ms, 31: 11.3 vs 15.5, 30: 5.57 vs 7.72, 29: 3.22 vs
 // 3.88, 28: 1.63 vs 1.93, 27: 0.69 vs 0.97, 26: 0.36 vs 0.49 (n = 25: 0.197
 // vs 0.224, n = 24: 0.115 vs 0.107 -- left to the int64 plan, which stays
-// asynchronous).  Above n = 32 there is no int32-engine plan.
+// asynchronous).  n = 33 / 34 (lim = 3 / 1: +-1 signals): 52.0 vs 66.2 and
+// 103.7 vs 141.3 ms (profiles/r02_compact/passes_n33_n34.log).
 constexpr int kCompactAutoMin = 26;
+constexpr int kCompactAutoMax = 34;  // n = 33, 34: three high passes (the third in registers); lim(n) = 3, 1
 bool compact_default(int log2n, const void* data) {
     const int mode = compact_mode();
     if (mode == 0 || (reinterpret_cast<uintptr_t>(data) & 15u)) return false;
     CompactPlan cp;
     if (log2n < 22 || !compact_plan(log2n, &cp)) return false;
-    return mode == 1 || (cp.v2 && log2n >= kCompactAutoMin);
+    return mode == 1 || (cp.v2 && log2n >= kCompactAutoMin && log2n <= kCompactAutoMax);
 }
 }  // namespace
 extern "C" {
@@ -2168,6 +2194,24 @@ int w32_visit_pass(const CompactPlan& cp, int q, F&& f) {
     }
     const Pass& p = cp.pass[q];
     const uint64_t dof = (uint64_t)cp.half[q] << cp.w;
+    if (q > 0 && p.r >= 1 && p.r <= 4) {  // k32_reg: every thread's 4 slots of every row, read half -> write half
+        const int kk = p.k + 1, R = p.r;
+        const uint64_t threads = 1ull << (n - R - 2);
+        for (uint64_t th = 0; th < threads; ++th) {
+            const uint64_t base = R == 1 ? w::reg_slot_base<1>(th * 4, kk) : R == 2 ? w::reg_slot_base<2>(th * 4, kk)
+                                  : R == 3 ? w::reg_slot_base<3>(th * 4, kk) : w::reg_slot_base<4>(th * 4, kk);
+            for (uint64_t r = 0; r < (1ull << R); ++r)
+                for (uint64_t c = 0; c < 4; ++c) {
+                    const uint64_t sl = base + (r << kk) + c;
+                    const uint64_t gi = compact_index_of(lam, n, sl);
+                    if (c == 0 && (compact_index_of(lam, n, base + (r << kk)) ^ compact_index_of(lam, n, base)) != (r << p.k))
+                        return fail(BW_BAD_ARGUMENTS, "int32 register pass: row %llu is not at index bit %d", (unsigned long long)r, p.k);
+                    f(0, th / w::kNT, (uint32_t)(r * 4 + c), (so + sl) * 4, 4, gi);
+                    f(1, th / w::kNT, (uint32_t)(r * 4 + c), (dof + sl) * 4, 4, gi);
+                }
+        }
+        return BW_OK;
+    }
     auto run = [&](auto cfg, auto lc) -> int {
         using C = typename decltype(cfg)::type;
         constexpr int L = decltype(lc)::value;
@@ -2304,6 +2348,26 @@ int w32_emulate(int64_t* host, const CompactPlan& cp) {
         }
         const Pass& p = cp.pass[q];
         const uint64_t dof = (uint64_t)cp.half[q] << cp.w;
+        if (q > 0 && p.r >= 1 && p.r <= 4) {  // k32_reg, thread by thread
+            const int kk = p.k + 1, R = p.r;
+            for (uint64_t th = 0; th < (1ull << (n - R - 2)); ++th) {
+                const uint64_t base = R == 1 ? w::reg_slot_base<1>(th * 4, kk) : R == 2 ? w::reg_slot_base<2>(th * 4, kk)
+                                      : R == 3 ? w::reg_slot_base<3>(th * 4, kk) : w::reg_slot_base<4>(th * 4, kk);
+                for (uint64_t c = 0; c < 4; ++c) {
+                    uint32_t x[16];
+                    for (uint64_t r = 0; r < (1ull << R); ++r) x[r] = buf[so + base + (r << kk) + c];
+                    for (int i = 0; i < R; ++i)
+                        for (uint64_t r = 0; r < (1ull << R); ++r)
+                            if (!((r >> i) & 1)) {
+                                const uint32_t a = x[r], b = x[r | (1ull << i)];
+                                x[r] = a + b;
+                                x[r | (1ull << i)] = a - b;
+                            }
+                    for (uint64_t r = 0; r < (1ull << R); ++r) buf[dof + base + (r << kk) + c] = x[r];
+                }
+            }
+            continue;
+        }
         auto run = [&](auto cfg, auto lc) {
             using C = typename decltype(cfg)::type;
             constexpr int L = decltype(lc)::value;

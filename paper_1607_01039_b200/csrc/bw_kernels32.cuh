@@ -321,6 +321,44 @@ __global__ void __launch_bounds__(kNT, MINB) k32_high(const u32* __restrict__ sr
     high_rounds_store<L, false, false, C>(v, sm32, dst, base, kk, lane, warp);
 }
 
+// int32 -> int32 pass of R = 1..4 stage rows in registers only (no shared
+// memory, no barrier): the third high pass of the n = 33 / 34 plans.  Every
+// thread holds 4 consecutive slots (16-byte accesses) of 2^R rows; a warp
+// covers 512 contiguous bytes of each row.  u = the thread's linear index
+// over the half's slots without the row bits; src / dst: the read / write
+// half (never in place).
+template <int R>
+BW_HD inline uint64_t reg_slot_base(uint64_t u, int kk) {
+    const uint64_t lo = u & ((1ull << kBits) - 1ull);                      // slot bits 0..13
+    const uint64_t mid = (u >> kBits) & ((1ull << (kk - (kBits + 1))) - 1ull);  // slot bits 15..kk-1
+    const uint64_t hi = u >> (kk - 1);                                      // above the rows
+    return lo | (mid << (kBits + 1)) | (hi << (kk + R));
+}
+
+template <int R>
+__global__ void __launch_bounds__(kNT) k32_reg(const u32* __restrict__ src, u32* __restrict__ dst, int k) {
+    static_assert(R >= 1 && R <= 4, "1 to 4 rows in registers");
+    constexpr int NR = 1 << R;
+    const int kk = k + 1;
+    const uint64_t base = reg_slot_base<R>(((uint64_t)blockIdx.x * kNT + threadIdx.x) * 4u, kk);
+    uint4 v[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) v[r] = ld4(src + base + ((uint64_t)r << kk));
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            if (!((r >> i) & 1)) {
+                const uint4 a = v[r], b = v[r | (1 << i)];
+                v[r] = make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+                v[r | (1 << i)] = make_uint4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) *reinterpret_cast<uint4*>(dst + base + ((uint64_t)r << kk)) = v[r];
+}
+
 // ---------------------------------------------------------------------------
 // The plan's FIRST pass on this engine: natural int64 -> int32 compact, the
 // same tile, rounds and stores as k32_high<L> (k = 14: rows 14 .. 14 + r).
@@ -469,6 +507,20 @@ __global__ void __launch_bounds__(kNT, 2)
     BW_STRESS(67);
     high_rounds_store<L, MODE == FIRST_CHECK, LAND>(v, sm32, dst, base, kk, lane, warp,
                                                      MODE == FIRST_CHECK && first_bad<CHK>(acc, lim), tileflag, abort);
+}
+
+// The input test on the first 2^14 inputs only (one CTA): at n >= 33 a refused
+// attempt costs two sweeps of 2^(n-14) returning CTAs, so signals whose first
+// values already exceed lim (wide-valued data, config 5's sums) are turned
+// away by this sample instead.
+__global__ void __launch_bounds__(kNT) k32_sample(const unsigned long long* __restrict__ x, u32 lim, unsigned* abort) {
+    u32 hi = 0, lo = 0;
+    for (uint32_t j = threadIdx.x; j < (1u << kBits); j += kNT) {
+        const unsigned long long y = x[j] + lim;
+        hi |= (u32)(y >> 32);
+        lo = max(lo, (u32)y);
+    }
+    if (hi != 0u || lo > 2u * lim) atomicExch(abort, 1u);
 }
 
 // Undo k32_first on the tiles it wrote (tileflag set): the int32 copy, the

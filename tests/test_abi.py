@@ -456,3 +456,44 @@ def test_compact_plan_checks_every_second_pass_shape(monkeypatch, r2):
     k, r = ctypes.c_int(0), ctypes.c_int(0)
     assert L.bw_compact_pass_info(24, 1, ctypes.byref(k), ctypes.byref(r), None, None) == 0
     assert r.value == int(r2) and k.value == 14 + 10 - int(r2)
+
+
+@pytest.mark.parametrize("rows", ["1,6,3", "2,7,1", "1,7,2", "2,6,2", "6,4", "7,3", "8,2", "9,1"])
+def test_compact_plan_with_register_passes(monkeypatch, coracle, rows):
+    """k32_reg (1..4 rows in registers, the third high pass of the n = 33 / 34
+    plans) after k32_high or directly after the first pass, at n = 24: the
+    static checker on the exact address functions and the host emulation
+    against the oracle at +-lim."""
+    monkeypatch.setenv("BW_COMPACT_ROWS", rows)
+    n = 14 + sum(int(r) for r in rows.split(","))
+    L = _lib.lib()
+    assert L.bw_plan_check_compact(n) == 0, _lib.last_error()
+    assert L.bw_compact_npasses(n) == len(rows.split(",")) + 1
+    eng = ctypes.c_int(0)
+    assert L.bw_compact_pass_info(n, 1, None, None, ctypes.byref(eng), None) == 0 and eng.value == 32
+    lim = L.bw_compact_limit(n)
+    assert lim == (2**31 - 1) >> (n - 4)
+    rng = np.random.default_rng(n + len(rows))
+    x = rng.integers(-lim, lim + 1, size=1 << n, dtype=np.int64)
+    ref = x.copy()
+    coracle.oracle_fwht_i64(ref.ctypes.data, n)
+    y = x.copy()
+    assert L.bw_debug_emulate_compact(y.ctypes.data, n) == 0, _lib.last_error()
+    assert np.array_equal(y, ref)
+
+
+def test_compact_plans_of_n33_n34():
+    """n = 33 / 34: 9 rows (k32_first), 8 rows (k32_high), then 2 / 3 rows in
+    registers (k32_reg), the 14-bit low pass; lim = 3 / 1; tried by default
+    (bw_compact_auto) behind a sample of the first inputs."""
+    L = _lib.lib()
+    for n, third in ((33, 2), (34, 3)):
+        assert L.bw_compact_npasses(n) == 4
+        want = [(14, 9), (23, 8), (31, third), (0, 14)]
+        for i, (k0, r0) in enumerate(want):
+            k, r, e, b = (ctypes.c_int(0) for _ in range(4))
+            assert L.bw_compact_pass_info(n, i, ctypes.byref(k), ctypes.byref(r), ctypes.byref(e), ctypes.byref(b)) == 0
+            assert (k.value, r.value, e.value) == (k0, r0, 32)
+            assert b.value == (12 if i in (0, 3) else 8)
+        assert L.bw_compact_limit(n) == (2**31 - 1) >> (n - 4)
+        assert L.bw_compact_auto(n) == 1

@@ -254,10 +254,11 @@ def test_compact_unaligned_view_runs_int64_plan(coracle):
 
 @pytest.mark.skipif(torch.cuda.is_available() and torch.cuda.get_device_properties(0).total_memory < (100 << 30),
                     reason="needs a B200")
-@pytest.mark.parametrize("n", [28, 29, 30, 31, 32])
+@pytest.mark.parametrize("n", [28, 29, 30, 31, 32, 33, 34])
 def test_compact_full_size_spot_check(n):
-    """n = 32 (config 4: 9 + 9 rows), 31 (9 + 8), 30 (8 + 8), 29 (8 + 7) and
-    28 (8 + 6) through the compact plan: the fold spot check of 2^20 outputs
+    """n = 32 (config 4: 9 + 9 rows), 31 (9 + 8), 30 (8 + 8), 29 (8 + 7), 28
+    (8 + 6) and n = 33 / 34 (9 + 8 rows, then 2 / 3 in registers: 64 / 128 GiB
+    in place) through the compact plan: the fold spot check of 2^20 outputs
     (subspace.py:1-11) against the CPU."""
     from paper_1607_01039_b200 import signals
 
@@ -340,7 +341,7 @@ def test_default_picks_compact_from_n26(coracle):
     plan from n = 26 up (bw_compact_auto), the int64 plan below and for wide
     values; identical results."""
     L = _lib.lib()
-    assert [L.bw_compact_auto(n) for n in (24, 25, 26, 30, 32, 33, 34)] == [0, 0, 1, 1, 1, 0, 0]
+    assert [L.bw_compact_auto(n) for n in (24, 25, 26, 30, 32, 33, 34)] == [0, 0, 1, 1, 1, 1, 1]
     for n in (25, 26):
         x = oracle_np.gen(1, n, [], 0, 1 << n)
         want = c_fwht(coracle, x)
@@ -393,3 +394,24 @@ def test_default_under_stream_capture_runs_the_int64_plan(coracle):
     g.replay()
     torch.cuda.synchronize()
     assert np.array_equal(t.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("rows", ["8,6,1", "8,6,2", "9,6,1", "8,4", "9,3"])
+def test_compact_plans_with_register_passes(coracle, monkeypatch, rows):
+    """k32_reg (1..4 rows, registers only) as the second or third high pass
+    behind k32_first / k32_high -- the shapes of the n = 33 / 34 plans at sizes
+    the oracle reaches -- on inputs at +-lim, unknown and known bound."""
+    monkeypatch.setenv("BW_COMPACT_ROWS", rows)
+    n = 14 + sum(int(r) for r in rows.split(","))
+    L = _lib.lib()
+    lim = L.bw_compact_limit(n)
+    assert lim == (2**31 - 1) >> (n - 4) and L.bw_compact_npasses(n) == len(rows.split(",")) + 1
+    rng = np.random.default_rng(n)
+    x = rng.integers(-lim, lim + 1, size=1 << n, dtype=np.int64)
+    x[rng.integers(0, 1 << n, size=4096)] = lim
+    x[rng.integers(0, 1 << n, size=4096)] = -lim
+    want = c_fwht(coracle, x)
+    for bound in (-1, lim):
+        y, used = compact(x, bound)
+        assert used == 1
+        assert np.array_equal(y, want)
