@@ -263,6 +263,9 @@ def test_compact_full_size_spot_check(n):
     from paper_1607_01039_b200 import signals
 
     spec = signals.config(4, n)
+    torch.cuda.empty_cache()
+    if torch.cuda.mem_get_info()[0] < (8 << n) + (1 << 30):
+        pytest.skip(f"needs {(8 << n) >> 30} GiB of free device memory")
     t = torch.empty(1 << n, dtype=torch.int64, device="cuda")
     signals.generate(spec, t)
     bw.fwht_array(t, compact=True)
@@ -275,6 +278,7 @@ def test_compact_full_size_spot_check(n):
             break
     got = t[torch.from_numpy(oracle_np.row_space(rows)).cuda()].cpu().numpy()
     del t
+    torch.cuda.empty_cache()  # up to 128 GiB: give it back before the next test asks for free memory
     from oracle import load_c
 
     lib = load_c()

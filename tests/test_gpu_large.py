@@ -53,6 +53,7 @@ def cpu_spot_check(coracle, spec, rows):
 
 def run_config(coracle, idx, n=None):
     spec = signals.config(idx, n)
+    torch.cuda.empty_cache()  # blocks cached from earlier tests of the same process count as free
     free, _ = torch.cuda.mem_get_info()
     if free < (8 << spec.n) + (1 << 30):
         pytest.skip(f"needs {(8 << spec.n) >> 30} GiB of free device memory")
@@ -118,6 +119,7 @@ def test_config4_n32_full_output_equals_the_reference_run():
         rec = json.load(f)
     assert rec["n"] == 32 and rec["config"] == 4 and rec["kind"] == "reference"
     spec = signals.config(4, 32)
+    torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
     if free < (8 << spec.n) + (2 << 30):
         pytest.skip("needs 34 GiB of free device memory")
