@@ -30,18 +30,29 @@ KERNELS = [
      r"k_pass_splitINS_11CfgHigh14cSELi4ELb0ELi0E"),
     ("k_pass<CfgHigh14c, 5> (n = 32 pass 3, r = 9, 2-CTA)", r"k_passINS_10CfgHigh14cELi5ELb0ELi0ELb0E"),
     ("k_pass<CfgHigh14c, 4> (n = 33/34 pass 3, r = 10, 2-CTA)", r"k_passINS_10CfgHigh14cELi4ELb0ELi0ELb0E"),
+    # the compact plan's int32 engine (bw_kernels32.cuh; the default at n = 26..34 on small-valued signals)
+    ("k32_first<5, CHECK> (compact pass 1 at n = 31..34: int64 -> int32, 9 rows, input test)", r"k32_firstILi5ELi1ELi4E"),
+    ("k32_first<5, PLAIN> (the same, known bound)", r"k32_firstILi5ELi0ELi4E"),
+    ("k32_first<6, CHECK> (compact pass 1 at n = 28..30: 8 rows)", r"k32_firstILi6ELi1ELi4E"),
+    ("k32_high<5> (compact pass 2 at n = 32: int32 -> int32, 9 rows)", r"k32_highILi5ELi2E"),
+    ("k32_high<6> (compact pass 2 at n = 30, 31, 33, 34: 8 rows)", r"k32_highILi6ELi2E"),
+    ("k32_reg<3> (compact pass 3 at n = 34: 3 rows in registers)", r"k32_regILi3E"),
+    ("k32_low (compact last pass: int32 -> int64, low 14 bits)", r"k32_lowILb0E"),
+    ("k32_low<EX> (the same with the fused threshold extraction)", r"k32_lowILb1E"),
 ]
 
 GROUPS = [
-    ("LDG (global load)", r"^LDG"),
+    ("LDG (global load)", r"^LDG\."),
     ("STG (global store)", r"^STG"),
     ("LDS (shared load)", r"^LDS"),
     ("STS (shared store)", r"^STS"),
+    ("LDGSTS (cp.async global -> shared)", r"^LDGSTS"),
     ("STAS (st.async to a cluster partner)", r"^STAS"),
     ("SYNCS (mbarrier)", r"^SYNCS"),
     ("UCGABAR (cluster barrier)", r"^UCGABAR"),
     ("BAR (CTA barrier)", r"^BAR"),
-    ("IADD3 / IADD (butterfly add/sub)", r"^IADD"),
+    ("IADD3 / IADD / IMAD.IADD (butterfly add/sub)", r"^(IADD|IMAD\.IADD)"),
+    ("VIMNMX3 (3-input max: the input test)", r"^VIMNMX3"),
     ("UTMALDG / UTMASTG / UBLKCP (TMA)", r"^(UTMA|UBLKCP)"),
     ("UTC* (tcgen05)", r"^UTC"),
 ]
@@ -88,7 +99,7 @@ def main():
             for g, rx in GROUPS:
                 if re.match(rx, op):
                     cnt[g] += 1
-        ldg = sorted({op for op in ops if op.startswith("LDG")})
+        ldg = sorted({op for op in ops if op.startswith("LDG.")})
         stg = sorted({op for op in ops if op.startswith("STG")})
         lines.append(f"| {title} | {regs.get(name, '?')} | {len(ops)} | " + " | ".join(str(cnt[g]) for g, _ in GROUPS)
                      + f" | {', '.join(ldg)} / {', '.join(stg)} |")
@@ -97,7 +108,12 @@ def main():
               "mbarrier (SYNCS) after a split cluster barrier (UCGABAR arrive / wait). No TMA or tcgen05 "
               "instruction appears: `tools/mb_tma.cu` / `mb_bulk.cu` measured TMA tiles and bulk copies "
               "below plain LDG/STG for these row shapes (profiles/r01_mb_tma.log, r01_mb_bulk.log), and "
-              "the transform has nothing to multiply."]
+              "the transform has nothing to multiply.", "",
+              "The int32 engine's kernels (k32_*, one CTA per 2^14-element tile, no cluster): k32_first stages "
+              "half of its int64 tile through shared memory with 16 LDGSTS (cp.async, 16 bytes each) next to 16 "
+              "LDG.128, so the checked pass keeps the whole tile in flight; its input test is a 64-bit add plus "
+              "LOP3 / VIMNMX3 per pair of values; the int32 butterflies are IADD3 / IMAD.IADD on 32-bit "
+              "registers; k32_reg has no shared-memory instruction at all."]
     with open(a.out, "w") as f:
         f.write("\n".join(lines) + "\n")
     print("\n".join(lines))
