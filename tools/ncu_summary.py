@@ -46,6 +46,7 @@ def to_bytes(v, unit):
 
 
 passes = []
+data = [r for r in data if "k32_sample" not in r[idx["Kernel Name"]]]  # the one-CTA sample test is not a pass
 for i, r in enumerate(data):
     passes.append({"pass": i, "kernel": r[idx["Kernel Name"]].split("(")[0].replace("void ", ""),
                    "duration_ms": float(r[idx["gpu__time_duration.sum"]].replace(",", "")) *
